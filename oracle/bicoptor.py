@@ -1,0 +1,338 @@
+"""UBL Bicoptor 2.0 DReLU (Alg 7) and ReLU (Alg 8) -- oracle; test infrastructure only.
+
+Follows Alg 7 and Alg 8 step by step, per party,
+vectorised over the element batch with numpy (elements are independent,
+P:996).  Every random value is drawn from the pre-shared seeds with
+the ChaCha keystream of ``oracle.chacha``; the byte layout of those draws is
+the spec's own -- the paper fixes none, so the exact
+share values are "parity unpinned" beyond the RFC 8439 vector, while every
+reconstructed output is pinned against plaintext sign / ReLU by the tests.
+
+Notation: ell ring bits; lx key-bit width (ell_x); f window
+offset of the key bits (sec. 6.1, reading C5); w = lx+1 ("guard", default,
+reading C6) or lx ("literal", the paper's Z_{2^lx}); p = smallest prime
+> 2^w (reading C7); S = lx+1 ladder slots.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import ring
+from .chacha import chacha_blocks, element_u32, element_u64, label_u64
+
+# Stream labels (domain separation of the seeds' keystreams).
+L_TAPE = label_u64(b"bc2.tape")    # seed01: 32 B/element (compact tape)
+L_TAPEW = label_u64(b"bc2.tapw")   # seed01: 64 B/element (wide tape)
+L_FALLBACK = label_u64(b"bc2.fb01")  # seed01: rejection fallback, counter j*256+k
+L_RESP = label_u64(b"bc2.resp")    # seed02: [DReLU']_0, 8 B/element
+L_TRIP02 = label_u64(b"bc2.tr02")  # seed02: [a]_0,[b]_0,[c]_0, 24 B/element
+L_TRIP12 = label_u64(b"bc2.tr12")  # seed12: [a]_1,[b]_1, 16 B/element
+
+PERM_LIMIT_COMPACT = 53261 * 40320  # largest multiple of 8! below 2^31
+
+
+@dataclass(frozen=True)
+class Params:
+    ell: int = 64
+    lx: int = 7
+    f: int = 24
+    mode: str = "guard"   # "guard": w = lx+1 (default); "literal": w = lx
+    rounds: int = 20
+
+    def __post_init__(self):
+        if not (2 <= self.ell <= 64):
+            raise ValueError("ell must be in [2, 64]")
+        if not (2 <= self.lx <= 7):
+            raise ValueError("lx must be in [2, 7] (at most 8 ladder slots)")
+        if self.mode not in ("guard", "literal"):
+            raise ValueError("mode must be 'guard' or 'literal'")
+        if self.f < 0 or self.f + self.lx + self.w > self.ell:
+            raise ValueError("window does not fit: need f + lx + w <= ell")
+        if self.rounds not in (8, 12, 20):
+            raise ValueError("rounds must be 8, 12 or 20")
+
+    @property
+    def w(self) -> int:
+        return self.lx + 1 if self.mode == "guard" else self.lx
+
+    @property
+    def p(self) -> int:
+        return ring.prime_above(self.w)
+
+    @property
+    def slots(self) -> int:
+        return self.lx + 1
+
+    @property
+    def compact(self) -> bool:
+        """Compact 32-B tape iff p = 257 and 8 slots (masks are exact bytes)."""
+        return self.p == 257 and self.slots == 8
+
+
+# --- PRG tape: t, Pi, r_m, rho_m for one element (Alg 7 steps 1, 6, 7, 8) -------------
+
+def _fallback_words(seed01: bytes, j: int, rounds: int):
+    """Sequential u32 words of ChaCha(seed01, L_FALLBACK, counter = j*256 + k)."""
+    k = 0
+    while True:
+        blk = chacha_blocks(seed01, L_FALLBACK, [j * 256 + k], rounds)[0]
+        for wd in blk:
+            yield int(wd)
+        k += 1
+
+
+def _perm_swaps(idx, S: int):
+    """Mixed-radix digits of idx in [0, S!): k_m = idx mod (m+1), idx //= (m+1),
+    for m = S-1 .. 1.  Column m of the result is the Fisher-Yates swap partner
+    of slot m (column 0 unused)."""
+    idx = np.asarray(idx, dtype=np.uint64) % np.uint64(math.factorial(S))
+    k = np.zeros(idx.shape + (S,), dtype=np.int64)
+    for m in range(S - 1, 0, -1):
+        k[..., m] = (idx % np.uint64(m + 1)).astype(np.int64)
+        idx = idx // np.uint64(m + 1)
+    return k
+
+
+def tape(prm: Params, seed01: bytes, j) -> dict:
+    """Decode the seed01 randomness of elements j.
+
+    Alg 7 step 1: random bit t.  Step 6: permutation Pi as
+    Fisher-Yates swaps (reading C9).  Step 7: masks r_m in Z_p^*.
+    Step 8: reshare values rho_m in Z_p (reading C11).  Exact
+    rejection sampling with a deterministic fallback stream (reading C10).
+    Parity unpinned beyond the ChaCha vector (the layout is the spec's).
+    """
+    j = np.atleast_1d(np.asarray(j, dtype=np.uint64))
+    n, S, p = j.size, prm.slots, prm.p
+    if prm.compact:
+        T = element_u32(seed01, L_TAPE, prm.rounds, j, 8)
+        t = (T[:, 0] >> np.uint32(31)).astype(np.uint64)
+        idx = (T[:, 0] & np.uint32(0x7FFFFFFF)).astype(np.uint64)
+        idx_ok = idx < np.uint64(PERM_LIMIT_COMPACT)
+        rbytes = np.ascontiguousarray(T[:, 1:3]).view(np.uint8).reshape(n, 8).astype(np.uint64)
+        r = rbytes + np.uint64(1)
+        r_ok = np.ones((n, S), dtype=bool)
+        u = np.ascontiguousarray(T[:, 3:7]).view("<u2").reshape(n, 8).astype(np.uint64)
+        perm_lim = PERM_LIMIT_COMPACT
+        mask_lim = None
+    else:
+        T = element_u32(seed01, L_TAPEW, prm.rounds, j, 16)
+        t = (T[:, 0] >> np.uint32(31)).astype(np.uint64)
+        idx = (T[:, 0] & np.uint32(0x7FFFFFFF)).astype(np.uint64)
+        perm_lim = ((1 << 31) // math.factorial(S)) * math.factorial(S)
+        idx_ok = idx < np.uint64(perm_lim)
+        um = np.ascontiguousarray(T[:, 1:5]).view("<u2").reshape(n, 8)[:, :S].astype(np.uint64)
+        mask_lim = (65536 // (p - 1)) * (p - 1)
+        r_ok = um < np.uint64(mask_lim)
+        r = np.uint64(1) + um % np.uint64(p - 1)
+        u = np.ascontiguousarray(T[:, 5:9]).view("<u2").reshape(n, 8).astype(np.uint64)
+    u = u[:, :S]
+    rho_lim = (65536 // p) * p
+    rho_ok = u < np.uint64(rho_lim)
+    rho = u % np.uint64(p)
+    r = r[:, :S].copy()
+
+    bad = np.nonzero(~idx_ok | ~r_ok.all(axis=1) | ~rho_ok.all(axis=1))[0]
+    for row in bad:  # rare: resample rejected draws from the fallback stream, in order
+        fb = _fallback_words(seed01, int(j[row]), prm.rounds)
+        if not idx_ok[row]:
+            v = next(fb) & 0x7FFFFFFF
+            while v >= perm_lim:
+                v = next(fb) & 0x7FFFFFFF
+            idx[row] = v
+        if mask_lim is not None:
+            for m in range(S):
+                if not r_ok[row, m]:
+                    v = next(fb) & 0xFFFF
+                    while v >= mask_lim:
+                        v = next(fb) & 0xFFFF
+                    r[row, m] = 1 + v % (p - 1)
+        for m in range(S):
+            if not rho_ok[row, m]:
+                v = next(fb) & 0xFFFF
+                while v >= rho_lim:
+                    v = next(fb) & 0xFFFF
+                rho[row, m] = v % p
+    return {"t": t, "k": _perm_swaps(idx, S), "r": r, "rho": rho}
+
+
+# --- Alg 7 steps 3-5: ladder, pairwise sums, modulo switch --------------------------
+
+def ladder(prm: Params, party: int, s) -> np.ndarray:
+    """Alg 7 step 3 with the key-bit offset f (reading C5):
+    u_i := trc(s, f+i, ell-w-f-i) mod 2^w for i in [0, lx]  (Alg 5).  (n, S)."""
+    s = np.atleast_1d(np.asarray(s, dtype=np.uint64))
+    cols = [ring.trc_det_mid(party, s, prm.f + i, prm.ell - prm.w - prm.f - i, prm.ell)
+            for i in range(prm.lx + 1)]
+    return np.stack(cols, axis=1).astype(np.uint64)
+
+
+def pairwise(prm: Params, party: int, u) -> np.ndarray:
+    """Alg 7 step 4: v_i := u_i + u_{i+1} - 1 (i < lx), v_lx := u_lx - 1,
+    all mod 2^w.  The public constant -1 is added by P0 only (reading C8)."""
+    one = np.uint64(1 if party == 0 else 0)
+    wm = np.uint64(ring.mask(prm.w))
+    v = np.empty_like(u)
+    with np.errstate(over="ignore"):
+        v[:, :-1] = (u[:, :-1] + u[:, 1:] - one) & wm
+        v[:, -1] = (u[:, -1] - one) & wm
+    return v
+
+
+def ladder_modswitch(prm: Params, party: int, s) -> np.ndarray:
+    """Alg 7 steps 3-5 on a share as given (no blinding): v'_i in Z_p^*, (n, S)."""
+    v = pairwise(prm, party, ladder(prm, party, s))
+    return ring.modswitch(party, v, prm.w, prm.p)
+
+
+def ladder_modswitch_bytes(prm: Params, party: int, s) -> np.ndarray:
+    """Output format of bc_ladder_modswitch: byte m = v'_m - 1 (v' is never 0,
+    see Alg 6), bytes S..7 zero.  (n, 8) uint8."""
+    vp = ladder_modswitch(prm, party, s)
+    out = np.zeros((vp.shape[0], 8), dtype=np.uint8)
+    out[:, : prm.slots] = (vp - np.uint64(1)).astype(np.uint8)
+    return out
+
+
+# --- Alg 7 per party ---------------------------------------------------------------
+
+def shuffle(k: np.ndarray, v: np.ndarray) -> np.ndarray:
+    """Alg 7 step 6: Fisher-Yates, for m = S-1 .. 1 swap(v[m], v[k_m])
+    (reading C9; both parties use the same seed01-derived k)."""
+    v = v.copy()
+    rows = np.arange(v.shape[0])
+    for m in range(v.shape[1] - 1, 0, -1):
+        km = k[:, m]
+        a = v[rows, m].copy()
+        v[rows, m] = v[rows, km]
+        v[rows, km] = a
+    return v
+
+
+def drelu_send(prm: Params, party: int, xb, j, seed01: bytes) -> dict:
+    """Alg 7 steps 1-8 for party P0 (party=0) or P1 (party=1).
+
+    1  t from seed01;                      2  s := (-1)^t [x]_b mod 2^ell
+    3  ladder u_i (Alg 5);                 4  pairwise v_i
+    5  modulo switch (Alg 6);              6  shuffle with Pi
+    7  w_m := v_m * r_m mod p;             8  reshare: P0 sends w + rho, P1 sends w - rho
+    Returns {"t", "W"} with W the (n, S) message to P2 in Z_p.
+    """
+    xb = np.atleast_1d(np.asarray(xb, dtype=np.uint64))
+    tp = tape(prm, seed01, j)
+    t = tp["t"]
+    s = np.where(t == 1, ring.neg(xb, prm.ell), xb).astype(np.uint64)       # steps 1-2
+    vp = ladder_modswitch(prm, party, s)                                      # steps 3-5
+    vp = shuffle(tp["k"], vp)                                                 # step 6
+    P = np.uint64(prm.p)
+    wv = (vp * tp["r"]) % P                                                   # step 7
+    if party == 0:                                                            # step 8
+        W = (wv + tp["rho"]) % P
+    else:
+        W = (wv + P - tp["rho"]) % P
+    return {"t": t, "W": W}
+
+
+def zero_test(prm: Params, W0, W1) -> np.ndarray:
+    """Alg 7 step 9: P2 reconstructs w_m = W0_m + W1_m mod p and
+    sets DReLU' := 1 iff some w_m = 0."""
+    wsum = (np.asarray(W0, dtype=np.uint64) + np.asarray(W1, dtype=np.uint64)) % np.uint64(prm.p)
+    return (wsum == 0).any(axis=1).astype(np.uint64)
+
+
+def drelu_helper(prm: Params, W0, W1, j, seed02: bytes) -> dict:
+    """Alg 7 steps 9-10: zero test, then reshare DReLU' in Z_{2^ell}:
+    [D']_0 := seed02 stream value q, [D']_1 := DReLU' - q (reading C12)."""
+    z = zero_test(prm, W0, W1)
+    q = element_u64(seed02, L_RESP, prm.rounds, j, 1)[:, 0] & np.uint64(ring.mask(prm.ell))
+    return {"z": z, "D0": q, "D1": ring.sub(z, q, prm.ell)}
+
+
+def drelu_finish(prm: Params, party: int, t, Db) -> np.ndarray:
+    """Alg 7 step 11: [DReLU] = t + (1-2t)[DReLU'] mod 2^ell; the
+    public t is added by P0 only (reading C8)."""
+    t = np.asarray(t, dtype=np.uint64)
+    Db = np.asarray(Db, dtype=np.uint64)
+    signed = np.where(t == 1, ring.neg(Db, prm.ell), Db).astype(np.uint64)
+    if party == 0:
+        return ring.add(signed, t, prm.ell)
+    return signed
+
+
+def drelu(prm: Params, x0, x1, j, seeds) -> dict:
+    """Alg 7 end to end with all three parties (two rounds)."""
+    m0 = drelu_send(prm, 0, x0, j, seeds.s01)
+    m1 = drelu_send(prm, 1, x1, j, seeds.s01)
+    h = drelu_helper(prm, m0["W"], m1["W"], j, seeds.s02)
+    y0 = drelu_finish(prm, 0, m0["t"], h["D0"])
+    y1 = drelu_finish(prm, 1, m1["t"], h["D1"])
+    return {"y0": y0, "y1": y1, "t": m0["t"], "W0": m0["W"], "W1": m1["W"], **h}
+
+
+# --- Alg 8: ReLU -------------------------------------------------------------------
+
+def triple(prm: Params, j, seed02: bytes, seed12: bytes) -> dict:
+    """Alg 8 preprocessing: P0,P2 draw [a]_0,[b]_0,[c]_0 from seed02;
+    P1,P2 draw [a]_1,[b]_1 from seed12; P2 sets [c]_1 := (a0+a1)(b0+b1) - c0."""
+    L = prm.ell
+    m = np.uint64(ring.mask(L))
+    t02 = element_u64(seed02, L_TRIP02, prm.rounds, j, 3) & m
+    t12 = element_u64(seed12, L_TRIP12, prm.rounds, j, 2) & m
+    a0, b0, c0 = t02[:, 0], t02[:, 1], t02[:, 2]
+    a1, b1 = t12[:, 0], t12[:, 1]
+    c1 = ring.sub(ring.mul(ring.add(a0, a1, L), ring.add(b0, b1, L), L), c0, L)
+    return {"a0": a0, "b0": b0, "c0": c0, "a1": a1, "b1": b1, "c1": c1}
+
+
+def relu(prm: Params, x0, x1, j, seeds) -> dict:
+    """Alg 8, all three parties.
+
+    1  P0, P1 run Alg 7 steps 1-8 and send [w] to P2
+    2  P2 reconstructs w, DReLU' := 1 iff some w_m = 0
+    3  P2 sends e := DReLU' - b (b = b0 + b1) to P0 and P1, and [c]_1 to P1
+    4  P0, P1 open d := x - a
+    5  [ReLU] = t[x] + (1-2t)(de + d[b] + e[a] + [c]) mod 2^ell;
+       the public de is added by P0 only (reading C8).
+    """
+    L = prm.ell
+    x0 = np.atleast_1d(np.asarray(x0, dtype=np.uint64))
+    x1 = np.atleast_1d(np.asarray(x1, dtype=np.uint64))
+    m0 = drelu_send(prm, 0, x0, j, seeds.s01)
+    m1 = drelu_send(prm, 1, x1, j, seeds.s01)
+    z = zero_test(prm, m0["W"], m1["W"])
+    tr = triple(prm, j, seeds.s02, seeds.s12)
+    e = ring.sub(z, ring.add(tr["b0"], tr["b1"], L), L)                          # step 3
+    d0 = ring.sub(x0, tr["a0"], L)                                               # step 4
+    d1 = ring.sub(x1, tr["a1"], L)
+    d = ring.add(d0, d1, L)
+    t = m0["t"]
+    inner0 = ring.add(ring.add(ring.mul(d, e, L), ring.mul(d, tr["b0"], L), L),
+                      ring.add(ring.mul(e, tr["a0"], L), tr["c0"], L), L)
+    inner1 = ring.add(ring.add(ring.mul(d, tr["b1"], L), ring.mul(e, tr["a1"], L), L), tr["c1"], L)
+    y0 = ring.add(ring.mul(t, x0, L), np.where(t == 1, ring.neg(inner0, L), inner0).astype(np.uint64), L)
+    y1 = ring.add(ring.mul(t, x1, L), np.where(t == 1, ring.neg(inner1, L), inner1).astype(np.uint64), L)
+    return {"y0": y0, "y1": y1, "t": t, "W0": m0["W"], "W1": m1["W"], "z": z,
+            "e": e, "d0": d0, "d1": d1, **tr}
+
+
+# --- wire format of the P0/P1 -> P2 message (Alg 7 step 8) ---------------------------
+
+def encode_msg(W: np.ndarray):
+    """Slot m of W (values < p <= 257) -> low byte plane (n, 8) and a high-bit
+    plane (n,) with bit m = bit 8 of W_m.  (ell_x+1) * ceil(log2 p) bits per
+    element on the wire: 72 (guard, p=257) / 64 (literal, p=131)."""
+    W = np.asarray(W, dtype=np.uint64)
+    n, S = W.shape
+    lo = np.zeros((n, 8), dtype=np.uint8)
+    lo[:, :S] = (W & np.uint64(0xFF)).astype(np.uint8)
+    hi = np.zeros(n, dtype=np.uint8)
+    for m in range(S):
+        hi |= ((W[:, m] >> np.uint64(8)) & np.uint64(1)).astype(np.uint8) << np.uint8(m)
+    return lo, hi
+
+
+def reconstruct(y0, y1, ell: int):
+    return ring.add(np.asarray(y0, dtype=np.uint64), np.asarray(y1, dtype=np.uint64), ell)
