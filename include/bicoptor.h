@@ -1,0 +1,189 @@
+/*
+ * bicoptor.h -- C ABI of libbicoptor: the B200 (sm_100a) hot path of the
+ * Bicoptor 2.0 UBL DReLU / ReLU protocol (arXiv 2309.04909).
+ *
+ * Citations: "P:n" = line n of the paper's LaTeX source, with the
+ * algorithm / section it falls in; readings Cn are listed in DESIGN.md.
+ *
+ * Conventions (every entry point)
+ *   - Returns BC_OK (0) or a negative BC_E* code; bc_strerror() maps it to text.
+ *   - All array arguments are DEVICE pointers owned by the caller.  The library
+ *     never allocates, frees or synchronises; every call is asynchronous on
+ *     `stream` (a cudaStream_t passed as void*, NULL = legacy default stream).
+ *     Asynchronous CUDA faults surface at the caller's next synchronisation.
+ *   - Share vectors are uint64_t[n]: element i holds a value of Z_{2^ell} in
+ *     its low ell bits (high bits of inputs are ignored, high bits of outputs
+ *     are zero).  Arrays of uint64_t must be 16-byte aligned (BC_EALIGN).
+ *   - n = 0 is a no-op that still validates the parameters.
+ *   - Inputs and outputs must not overlap (BC_EALIAS), except where stated.
+ *   - elem_base is the global index of element 0 of this call; every PRG draw
+ *     is addressed by global index j = elem_base + i, so a batch split into
+ *     shards (or chunks) gives bit-identical results to one call.  It must be
+ *     a multiple of 8 (BC_EALIGN).
+ *   - Seeds are 32-byte keys passed by value; a party-phase call takes only the
+ *     seeds that party holds: P0 {seed01, seed02}, P1 {seed01, seed12},
+ *     P2 {seed02, seed12}.
+ *   - Stateless and thread-safe.
+ */
+#ifndef BICOPTOR_H
+#define BICOPTOR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BC_OK 0
+#define BC_EINVAL (-1)   /* bad parameter (party id, ell, lx, mode, rounds, NULL) */
+#define BC_ERANGE (-2)   /* key-bit window does not fit: need f + lx + w <= ell  */
+#define BC_EALIGN (-3)   /* pointer not 16-B aligned, or elem_base % 8 != 0      */
+#define BC_ECUDA  (-4)   /* CUDA launch error (bc_last_cuda_error() has the code) */
+#define BC_EALIAS (-5)   /* an output overlaps an input                          */
+
+#define BC_MODE_GUARD   0 /* w = lx + 1, p = 257 at lx = 7 (default; reading C6) */
+#define BC_MODE_LITERAL 1 /* w = lx, the paper's Z_{2^lx} (64-bit wire)  */
+
+/* Protocol parameters (Alg 7 "Setting"; key bits, sec. 6.1).
+ *   ell    ring bits, 2..64
+ *   lx     key-bit width ell_x, 2..7 (lx + 1 <= 8 ladder slots)
+ *   f      key-bit window offset: the ladder reads bits [f, f+lx+w) (reading C5;
+ *          f = 24 keeps 5+2 of the paper's 5+26 fixed point)
+ *   mode   BC_MODE_GUARD / BC_MODE_LITERAL
+ *   rounds ChaCha rounds 8, 12 or 20 (reading C19)
+ * Derived by bc_params_init: w (window width), p (smallest prime > 2^w,
+ * reading C7), slots = lx + 1, compact = (p == 257 && slots == 8): the 32-B
+ * per-element PRG tape, else the 64-B tape. */
+typedef struct bc_params {
+  int32_t ell, lx, f, mode, rounds;
+  uint32_t w, p, slots;
+  int32_t compact;
+} bc_params;
+
+/* Pre-shared seeds seed01, seed02, seed12. */
+typedef struct bc_seeds {
+  uint8_t s01[32];
+  uint8_t s02[32];
+  uint8_t s12[32];
+} bc_seeds;
+
+/* Optional transcript of the simulated three-party run (bc_drelu / bc_relu):
+ * the messages P0 and P1 send to P2 (Alg 7 step 8), in the wire format
+ * of bc_drelu_send.  Any pointer may be NULL (that plane is not written). */
+typedef struct bc_transcript {
+  uint8_t *w0_lo, *w0_hi, *w1_lo, *w1_hi;
+} bc_transcript;
+
+/* Validate and derive parameters.  BC_EINVAL / BC_ERANGE on bad input. */
+int bc_params_init(bc_params *out, int ell, int lx, int f, int mode, int rounds);
+
+/* Alg 4 / Alg 5 deterministic truncation for one party:
+ *   P0: out = cut(in, k1, k2) mod 2^(ell-k1-k2)
+ *   P1: out = 2^ell - cut(2^ell - in, k1, k2) mod 2^(ell-k1-k2)  (readings C2-C4)
+ * k2 = 0 is Alg 4.  Requires k1 + k2 < ell.  in, out: uint64_t[n]. */
+int bc_trc(int party, const uint64_t *in, uint64_t *out, size_t n, int ell, int k1, int k2,
+           void *stream);
+
+/* Alg 1 SecureML probabilistic truncation for one party, the
+ * prior-work baseline whose e1 error the paper analyses:
+ *   P0: cut(in, k) mod 2^ell;  P1: 2^ell - cut(2^ell - in, k) mod 2^ell (C3). */
+int bc_trc_prob(int party, const uint64_t *in, uint64_t *out, size_t n, int ell, int k,
+                void *stream);
+
+/* Alg 6 modulo switch for one party: shares of x in Z_{2^lp} ->
+ * shares in Z_p.  P0: in == 0 ? 2^lp mod p : in mod p;  P1: (p + in - 2^lp) mod p.
+ * Requires 1 <= lp <= 31 and 2^lp < p < 2^32 (p need not be checked prime).
+ * in: uint64_t[n] (low lp bits used), out: uint32_t[n] (4-B aligned). */
+int bc_modswitch(int party, const uint64_t *in, uint32_t *out, size_t n, int lp, uint32_t p,
+                 void *stream);
+
+/* Alg 7 steps 3-5 for one party on its share as given (no blinding bit, no
+ * shuffle): ladder u_i = Alg 5 with k1 = f+i, k2 = ell-w-f-i,
+ * pairwise v_i (P0 carries the -1, reading C8), modulo switch
+ * (Alg 6).  Output v: uint8_t[n][8], byte m of row i = v'_m - 1 (v' lies in
+ * Z_p^* so this is lossless for p <= 257), bytes m >= slots are 0.  v must be
+ * 16-B aligned. */
+int bc_ladder_modswitch(int party, const uint64_t *x, uint8_t *v, size_t n,
+                        const bc_params *prm, void *stream);
+
+/* Alg 7, all three parties simulated on one GPU in one fused
+ * kernel: y0 + y1 = DReLU(x0 + x1) mod 2^ell (1 for positive, 0 for negative
+ * in-band x; x = 0 gives the random bit t, reading C13).  tr may be NULL. */
+int bc_drelu(const uint64_t *x0, const uint64_t *x1, uint64_t *y0, uint64_t *y1, size_t n,
+             uint64_t elem_base, const bc_params *prm, const bc_seeds *seeds,
+             const bc_transcript *tr, void *stream);
+
+/* Alg 8, all three parties on one GPU in one fused kernel:
+ * y0 + y1 = x * DReLU(x) mod 2^ell (x = x0 + x1). */
+int bc_relu(const uint64_t *x0, const uint64_t *x1, uint64_t *y0, uint64_t *y1, size_t n,
+            uint64_t elem_base, const bc_params *prm, const bc_seeds *seeds,
+            const bc_transcript *tr, void *stream);
+
+/* ---- party-separated phases (each party on its own device; the caller moves
+ * the message buffers, e.g. with NCCL send/recv) --------------------------- */
+
+/* Alg 7 steps 1-8 for P0 (party 0) or P1 (party 1): the message to P2 in the
+ * wire format lo: uint8_t[n][8] (low 8 bits of W_m, 16-B aligned), hi:
+ * uint8_t[n] (bit m = bit 8 of W_m; may be NULL when p <= 256), plus the
+ * party's blinding bits tbits: uint8_t[(n+7)/8] (bit i%8 of byte i/8 = t_i),
+ * kept locally for the finish phase.  (lx+1)*ceil(log2 p) bits per element:
+ * 72 in guard mode, 64 literal (Table 1). */
+int bc_drelu_send(int party, const uint64_t *x, uint8_t *lo, uint8_t *hi, uint8_t *tbits,
+                  size_t n, uint64_t elem_base, const bc_params *prm, const uint8_t seed01[32],
+                  void *stream);
+
+/* Alg 7 steps 9-10 for P2: zero test of w = W0 + W1 mod p, then
+ * reshare DReLU' in Z_{2^ell}: [D']_0 = seed02 stream value (P0 can derive
+ * it; written to resp0 only if resp0 != NULL, the paper-literal transport,
+ * reading C12), resp1 = DReLU' - [D']_0.  resp0/resp1: uint64_t[n]. */
+int bc_drelu_helper(const uint8_t *lo0, const uint8_t *hi0, const uint8_t *lo1,
+                    const uint8_t *hi1, uint64_t *resp0, uint64_t *resp1, size_t n,
+                    uint64_t elem_base, const bc_params *prm, const uint8_t seed02[32],
+                    void *stream);
+
+/* Alg 7 step 11: y = t + (1-2t)[D']_b (P0 adds t, reading C8).
+ * P0 with resp == NULL derives [D']_0 from seed02 itself (pass seed02; P1
+ * passes NULL). */
+int bc_drelu_finish(int party, const uint8_t *tbits, const uint64_t *resp, uint64_t *y,
+                    size_t n, uint64_t elem_base, const bc_params *prm,
+                    const uint8_t seed02[32], void *stream);
+
+/* Alg 8 step 1 and the first half of step 4 for P0 / P1: the Alg 7 message
+ * (as bc_drelu_send) and the party's share of d = x - a: dshare = x_b - [a]_b,
+ * sent to the other computing party.  seed_tr = seed02 for P0, seed12 for P1
+ * (Alg 8 preprocessing). */
+int bc_relu_send(int party, const uint64_t *x, uint8_t *lo, uint8_t *hi, uint8_t *tbits,
+                 uint64_t *dshare, size_t n, uint64_t elem_base, const bc_params *prm,
+                 const uint8_t seed01[32], const uint8_t seed_tr[32], void *stream);
+
+/* Alg 8 steps 2-3 for P2: DReLU' by the zero test, e = DReLU' -
+ * ([b]_0 + [b]_1) sent to both, and [c]_1 = ([a]_0+[a]_1)([b]_0+[b]_1) - [c]_0
+ * sent to P1 (c1 may be NULL if it was delivered in preprocessing, C20). */
+int bc_relu_helper(const uint8_t *lo0, const uint8_t *hi0, const uint8_t *lo1,
+                   const uint8_t *hi1, uint64_t *e, uint64_t *c1, size_t n, uint64_t elem_base,
+                   const bc_params *prm, const uint8_t seed02[32], const uint8_t seed12[32],
+                   void *stream);
+
+/* Alg 8 steps 4-5 for P0 / P1: d = d_own + d_peer, then
+ * y_b = t x_b + (1-2t)(de + d[b]_b + e[a]_b + [c]_b), P0 adding de (C8).
+ * c1 is P1's [c]_1 (NULL for P0).  seed_tr as in bc_relu_send. */
+int bc_relu_finish(int party, const uint64_t *x, const uint8_t *tbits, const uint64_t *d_own,
+                   const uint64_t *d_peer, const uint64_t *e, const uint64_t *c1, uint64_t *y,
+                   size_t n, uint64_t elem_base, const bc_params *prm,
+                   const uint8_t seed_tr[32], void *stream);
+
+/* Human-readable text for a BC_* code (static storage). */
+const char *bc_strerror(int code);
+
+/* cudaError_t of the most recent BC_ECUDA on this thread (0 if none). */
+int bc_last_cuda_error(void);
+
+/* Library ABI version (major * 100 + minor). */
+int bc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BICOPTOR_H */

@@ -28,8 +28,11 @@ L_TAPE = label_u64(b"bc2.tape")    # seed01: 32 B/element (compact tape)
 L_TAPEW = label_u64(b"bc2.tapw")   # seed01: 64 B/element (wide tape)
 L_FALLBACK = label_u64(b"bc2.fb01")  # seed01: rejection fallback, counter j*256+k
 L_RESP = label_u64(b"bc2.resp")    # seed02: [DReLU']_0, 8 B/element
-L_TRIP02 = label_u64(b"bc2.tr02")  # seed02: [a]_0,[b]_0,[c]_0, 24 B/element
-L_TRIP12 = label_u64(b"bc2.tr12")  # seed12: [a]_1,[b]_1, 16 B/element
+L_A02 = label_u64(b"bc2.ta02")     # seed02: [a]_0, 8 B/element
+L_B02 = label_u64(b"bc2.tb02")     # seed02: [b]_0, 8 B/element
+L_C02 = label_u64(b"bc2.tc02")     # seed02: [c]_0, 8 B/element
+L_A12 = label_u64(b"bc2.ta12")     # seed12: [a]_1, 8 B/element
+L_B12 = label_u64(b"bc2.tb12")     # seed12: [b]_1, 8 B/element
 
 PERM_LIMIT_COMPACT = 53261 * 40320  # largest multiple of 8! below 2^31
 
@@ -279,12 +282,50 @@ def triple(prm: Params, j, seed02: bytes, seed12: bytes) -> dict:
     P1,P2 draw [a]_1,[b]_1 from seed12; P2 sets [c]_1 := (a0+a1)(b0+b1) - c0."""
     L = prm.ell
     m = np.uint64(ring.mask(L))
-    t02 = element_u64(seed02, L_TRIP02, prm.rounds, j, 3) & m
-    t12 = element_u64(seed12, L_TRIP12, prm.rounds, j, 2) & m
-    a0, b0, c0 = t02[:, 0], t02[:, 1], t02[:, 2]
-    a1, b1 = t12[:, 0], t12[:, 1]
+    a0, b0, c0 = (element_u64(seed02, lab, prm.rounds, j, 1)[:, 0] & m for lab in (L_A02, L_B02, L_C02))
+    a1, b1 = (element_u64(seed12, lab, prm.rounds, j, 1)[:, 0] & m for lab in (L_A12, L_B12))
     c1 = ring.sub(ring.mul(ring.add(a0, a1, L), ring.add(b0, b1, L), L), c0, L)
     return {"a0": a0, "b0": b0, "c0": c0, "a1": a1, "b1": b1, "c1": c1}
+
+
+def relu_send(prm: Params, party: int, xb, j, seed01: bytes, seed_tr: bytes) -> dict:
+    """Alg 8 steps 1 and 4 for P0 / P1: the Alg 7 message to P2
+    and the party's share of d = x - a, [d]_b = [x]_b - [a]_b, sent to the other
+    computing party.  seed_tr is seed02 (P0, [a]_0) or seed12 (P1, [a]_1)."""
+    m = drelu_send(prm, party, xb, j, seed01)
+    lab = L_A02 if party == 0 else L_A12
+    a = element_u64(seed_tr, lab, prm.rounds, j, 1)[:, 0] & np.uint64(ring.mask(prm.ell))
+    return {"t": m["t"], "W": m["W"], "d": ring.sub(np.asarray(xb, dtype=np.uint64), a, prm.ell)}
+
+
+def relu_helper(prm: Params, W0, W1, j, seed02: bytes, seed12: bytes) -> dict:
+    """Alg 8 steps 2-3 for P2: DReLU' by the zero test, then
+    e := DReLU' - b (b = [b]_0 + [b]_1) to P0 and P1, and [c]_1 to P1."""
+    z = zero_test(prm, W0, W1)
+    tr = triple(prm, j, seed02, seed12)
+    e = ring.sub(z, ring.add(tr["b0"], tr["b1"], prm.ell), prm.ell)
+    return {"z": z, "e": e, "c1": tr["c1"]}
+
+
+def relu_finish(prm: Params, party: int, xb, t, d_own, d_peer, e, c1, j, seed_tr: bytes) -> np.ndarray:
+    """Alg 8 steps 4-5 for P0 / P1:
+    d := [d]_0 + [d]_1 (opened);
+    [ReLU]_b = t [x]_b + (1-2t)(de + d[b]_b + e[a]_b + [c]_b), de added by P0 only
+    (reading C8).  P0 regenerates [a]_0,[b]_0,[c]_0 from seed02, P1 regenerates
+    [a]_1,[b]_1 from seed12 and uses the received [c]_1."""
+    L = prm.ell
+    m = np.uint64(ring.mask(L))
+    xb = np.asarray(xb, dtype=np.uint64)
+    t = np.asarray(t, dtype=np.uint64)
+    d = ring.add(d_own, d_peer, L)
+    if party == 0:
+        a, b, c = (element_u64(seed_tr, lab, prm.rounds, j, 1)[:, 0] & m for lab in (L_A02, L_B02, L_C02))
+        inner = ring.add(ring.add(ring.mul(d, e, L), ring.mul(d, b, L), L), ring.add(ring.mul(e, a, L), c, L), L)
+    else:
+        a, b = (element_u64(seed_tr, lab, prm.rounds, j, 1)[:, 0] & m for lab in (L_A12, L_B12))
+        inner = ring.add(ring.add(ring.mul(d, b, L), ring.mul(e, a, L), L), np.asarray(c1, dtype=np.uint64), L)
+    signed = np.where(t == 1, ring.neg(inner, L), inner).astype(np.uint64)
+    return ring.add(ring.mul(t, xb, L), signed, L)
 
 
 def relu(prm: Params, x0, x1, j, seeds) -> dict:
@@ -292,30 +333,19 @@ def relu(prm: Params, x0, x1, j, seeds) -> dict:
 
     1  P0, P1 run Alg 7 steps 1-8 and send [w] to P2
     2  P2 reconstructs w, DReLU' := 1 iff some w_m = 0
-    3  P2 sends e := DReLU' - b (b = b0 + b1) to P0 and P1, and [c]_1 to P1
+    3  P2 sends e := DReLU' - b to P0 and P1, and [c]_1 to P1
     4  P0, P1 open d := x - a
-    5  [ReLU] = t[x] + (1-2t)(de + d[b] + e[a] + [c]) mod 2^ell;
-       the public de is added by P0 only (reading C8).
+    5  [ReLU] = t[x] + (1-2t)(de + d[b] + e[a] + [c]) mod 2^ell
     """
-    L = prm.ell
     x0 = np.atleast_1d(np.asarray(x0, dtype=np.uint64))
     x1 = np.atleast_1d(np.asarray(x1, dtype=np.uint64))
-    m0 = drelu_send(prm, 0, x0, j, seeds.s01)
-    m1 = drelu_send(prm, 1, x1, j, seeds.s01)
-    z = zero_test(prm, m0["W"], m1["W"])
-    tr = triple(prm, j, seeds.s02, seeds.s12)
-    e = ring.sub(z, ring.add(tr["b0"], tr["b1"], L), L)                          # step 3
-    d0 = ring.sub(x0, tr["a0"], L)                                               # step 4
-    d1 = ring.sub(x1, tr["a1"], L)
-    d = ring.add(d0, d1, L)
-    t = m0["t"]
-    inner0 = ring.add(ring.add(ring.mul(d, e, L), ring.mul(d, tr["b0"], L), L),
-                      ring.add(ring.mul(e, tr["a0"], L), tr["c0"], L), L)
-    inner1 = ring.add(ring.add(ring.mul(d, tr["b1"], L), ring.mul(e, tr["a1"], L), L), tr["c1"], L)
-    y0 = ring.add(ring.mul(t, x0, L), np.where(t == 1, ring.neg(inner0, L), inner0).astype(np.uint64), L)
-    y1 = ring.add(ring.mul(t, x1, L), np.where(t == 1, ring.neg(inner1, L), inner1).astype(np.uint64), L)
-    return {"y0": y0, "y1": y1, "t": t, "W0": m0["W"], "W1": m1["W"], "z": z,
-            "e": e, "d0": d0, "d1": d1, **tr}
+    m0 = relu_send(prm, 0, x0, j, seeds.s01, seeds.s02)
+    m1 = relu_send(prm, 1, x1, j, seeds.s01, seeds.s12)
+    h = relu_helper(prm, m0["W"], m1["W"], j, seeds.s02, seeds.s12)
+    y0 = relu_finish(prm, 0, x0, m0["t"], m0["d"], m1["d"], h["e"], None, j, seeds.s02)
+    y1 = relu_finish(prm, 1, x1, m1["t"], m1["d"], m0["d"], h["e"], h["c1"], j, seeds.s12)
+    return {"y0": y0, "y1": y1, "t": m0["t"], "W0": m0["W"], "W1": m1["W"], "z": h["z"],
+            "e": h["e"], "c1": h["c1"], "d0": m0["d"], "d1": m1["d"]}
 
 
 # --- wire format of the P0/P1 -> P2 message (Alg 7 step 8) ---------------------------

@@ -1,0 +1,298 @@
+"""Thin Python binding of libbicoptor (include/bicoptor.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA
+kernels behind the C ABI.  PyTorch provides device memory and streams.
+There is no CPU fallback: if the shared library is missing or a tensor is not
+on a CUDA device, the call raises.
+
+Share vectors are 1-D CUDA tensors of 8-byte elements (torch.int64 or
+torch.uint64) holding Z_{2^ell} values bit for bit.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbicoptor.so")
+
+MODE = {"guard": 0, "literal": 1}
+
+c_u64p = ctypes.c_void_p
+
+
+class BicoptorError(RuntimeError):
+    pass
+
+
+class bc_params(ctypes.Structure):
+    _fields_ = [("ell", ctypes.c_int32), ("lx", ctypes.c_int32), ("f", ctypes.c_int32),
+                ("mode", ctypes.c_int32), ("rounds", ctypes.c_int32), ("w", ctypes.c_uint32),
+                ("p", ctypes.c_uint32), ("slots", ctypes.c_uint32), ("compact", ctypes.c_int32)]
+
+
+class bc_seeds(ctypes.Structure):
+    _fields_ = [("s01", ctypes.c_uint8 * 32), ("s02", ctypes.c_uint8 * 32), ("s12", ctypes.c_uint8 * 32)]
+
+
+class bc_transcript(ctypes.Structure):
+    _fields_ = [("w0_lo", ctypes.c_void_p), ("w0_hi", ctypes.c_void_p),
+                ("w1_lo", ctypes.c_void_p), ("w1_hi", ctypes.c_void_p)]
+
+
+# name -> (restype, argtypes); mirrors include/bicoptor.h
+_P = ctypes.c_void_p
+_SIG = {
+    "bc_version": (ctypes.c_int, []),
+    "bc_last_cuda_error": (ctypes.c_int, []),
+    "bc_strerror": (ctypes.c_char_p, [ctypes.c_int]),
+    "bc_params_init": (ctypes.c_int, [ctypes.POINTER(bc_params), ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_int, ctypes.c_int]),
+    "bc_trc": (ctypes.c_int, [ctypes.c_int, _P, _P, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]),
+    "bc_trc_prob": (ctypes.c_int, [ctypes.c_int, _P, _P, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, _P]),
+    "bc_modswitch": (ctypes.c_int, [ctypes.c_int, _P, _P, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint32, _P]),
+    "bc_ladder_modswitch": (ctypes.c_int, [ctypes.c_int, _P, _P, ctypes.c_size_t, ctypes.POINTER(bc_params), _P]),
+    "bc_drelu": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64, ctypes.POINTER(bc_params),
+                                ctypes.POINTER(bc_seeds), ctypes.POINTER(bc_transcript), _P]),
+    "bc_relu": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64, ctypes.POINTER(bc_params),
+                               ctypes.POINTER(bc_seeds), ctypes.POINTER(bc_transcript), _P]),
+    "bc_drelu_send": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64,
+                                     ctypes.POINTER(bc_params), ctypes.c_char_p, _P]),
+    "bc_drelu_helper": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64,
+                                       ctypes.POINTER(bc_params), ctypes.c_char_p, _P]),
+    "bc_drelu_finish": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64,
+                                       ctypes.POINTER(bc_params), ctypes.c_char_p, _P]),
+    "bc_relu_send": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64,
+                                    ctypes.POINTER(bc_params), ctypes.c_char_p, ctypes.c_char_p, _P]),
+    "bc_relu_helper": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64,
+                                      ctypes.POINTER(bc_params), ctypes.c_char_p, ctypes.c_char_p, _P]),
+    "bc_relu_finish": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64,
+                                      ctypes.POINTER(bc_params), ctypes.c_char_p, _P]),
+}
+EXPORTS = tuple(_SIG)
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libbicoptor.so (built in-tree by __graft_entry__.build())."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise BicoptorError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIG.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = lib().bc_strerror(rc).decode()
+        if rc == -4:
+            msg += f" (cudaError {lib().bc_last_cuda_error()})"
+        raise BicoptorError(f"{what}: {msg} [{rc}]")
+
+
+@dataclass(frozen=True)
+class Params:
+    """Protocol parameters (see bc_params in include/bicoptor.h)."""
+    ell: int = 64
+    lx: int = 7
+    f: int = 24
+    mode: str = "guard"
+    rounds: int = 20
+
+    def c(self) -> bc_params:
+        p = bc_params()
+        _check(lib().bc_params_init(ctypes.byref(p), self.ell, self.lx, self.f, MODE[self.mode], self.rounds),
+               "bc_params_init")
+        return p
+
+
+def seeds_struct(seeds) -> bc_seeds:
+    s = bc_seeds()
+    for name in ("s01", "s02", "s12"):
+        v = getattr(seeds, name)
+        assert len(v) == 32
+        ctypes.memmove(getattr(s, name), v, 32)
+    return s
+
+
+def _dev(t: torch.Tensor, name: str, itemsize: int | None = 8) -> int:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise BicoptorError(f"{name} must be a CUDA tensor (no CPU path exists)")
+    if not t.is_contiguous():
+        raise BicoptorError(f"{name} must be contiguous")
+    if itemsize is not None and t.element_size() != itemsize:
+        raise BicoptorError(f"{name} must have {itemsize}-byte elements")
+    return t.data_ptr()
+
+
+def _opt(t, name, itemsize=8):
+    return None if t is None else _dev(t, name, itemsize)
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def empty_u64(n: int, device) -> torch.Tensor:
+    return torch.empty(n, dtype=torch.int64, device=device)
+
+
+# ---- elementwise primitives --------------------------------------------------------
+
+def trc(party: int, x: torch.Tensor, ell: int, k1: int, k2: int = 0, out=None, stream=None) -> torch.Tensor:
+    """Alg 4 / Alg 5 deterministic truncation of one party's share."""
+    out = torch.empty_like(x) if out is None else out
+    _check(lib().bc_trc(party, _dev(x, "x"), _dev(out, "out"), x.numel(), ell, k1, k2, _stream(stream)), "bc_trc")
+    return out
+
+
+def trc_prob(party: int, x: torch.Tensor, ell: int, k: int, out=None, stream=None) -> torch.Tensor:
+    """Alg 1 SecureML probabilistic truncation of one party's share."""
+    out = torch.empty_like(x) if out is None else out
+    _check(lib().bc_trc_prob(party, _dev(x, "x"), _dev(out, "out"), x.numel(), ell, k, _stream(stream)), "bc_trc_prob")
+    return out
+
+
+def modswitch(party: int, x: torch.Tensor, lp: int, p: int, out=None, stream=None) -> torch.Tensor:
+    """Alg 6 modulo switch Z_{2^lp} -> Z_p of one party's share (uint32 out, in int32 storage)."""
+    out = torch.empty(x.numel(), dtype=torch.int32, device=x.device) if out is None else out
+    _check(lib().bc_modswitch(party, _dev(x, "x"), _dev(out, "out", 4), x.numel(), lp, p, _stream(stream)),
+           "bc_modswitch")
+    return out
+
+
+def ladder_modswitch(party: int, x: torch.Tensor, prm: Params, out=None, stream=None) -> torch.Tensor:
+    """Alg 7 steps 3-5 on one party's share: (n, 8) uint8, byte m = v'_m - 1."""
+    out = torch.empty((x.numel(), 8), dtype=torch.uint8, device=x.device) if out is None else out
+    _check(lib().bc_ladder_modswitch(party, _dev(x, "x"), _dev(out, "out", 1), x.numel(), ctypes.byref(prm.c()),
+                                     _stream(stream)), "bc_ladder_modswitch")
+    return out
+
+
+# ---- fused three-party (simulated on one GPU) ----------------------------------------
+
+def _fused(fn, what, x0, x1, prm, seeds, elem_base, y0, y1, transcript, stream):
+    n = x0.numel()
+    if x1.numel() != n:
+        raise BicoptorError("x0 and x1 differ in length")
+    y0 = torch.empty_like(x0) if y0 is None else y0
+    y1 = torch.empty_like(x1) if y1 is None else y1
+    tr = None
+    if transcript is not None:
+        tr = bc_transcript(*(_opt(transcript.get(k), k, 1) for k in ("w0_lo", "w0_hi", "w1_lo", "w1_hi")))
+    cp, cs = prm.c(), seeds_struct(seeds)
+    _check(fn(_dev(x0, "x0"), _dev(x1, "x1"), _dev(y0, "y0"), _dev(y1, "y1"), n, elem_base, ctypes.byref(cp),
+              ctypes.byref(cs), ctypes.byref(tr) if tr is not None else None, _stream(stream)), what)
+    return y0, y1
+
+
+def transcript_buffers(n: int, device) -> dict:
+    """Caller-owned buffers for the P0/P1 -> P2 message transcript."""
+    return {"w0_lo": torch.empty((n, 8), dtype=torch.uint8, device=device),
+            "w0_hi": torch.empty(n, dtype=torch.uint8, device=device),
+            "w1_lo": torch.empty((n, 8), dtype=torch.uint8, device=device),
+            "w1_hi": torch.empty(n, dtype=torch.uint8, device=device)}
+
+
+def drelu(x0, x1, prm: Params, seeds, elem_base: int = 0, y0=None, y1=None, transcript=None, stream=None):
+    """Alg 7 with all three parties in one fused kernel: returns (y0, y1), y0 + y1 = DReLU(x)."""
+    return _fused(lib().bc_drelu, "bc_drelu", x0, x1, prm, seeds, elem_base, y0, y1, transcript, stream)
+
+
+def relu(x0, x1, prm: Params, seeds, elem_base: int = 0, y0=None, y1=None, transcript=None, stream=None):
+    """Alg 8 with all three parties in one fused kernel: returns (y0, y1), y0 + y1 = ReLU(x)."""
+    return _fused(lib().bc_relu, "bc_relu", x0, x1, prm, seeds, elem_base, y0, y1, transcript, stream)
+
+
+# ---- party-separated phases ---------------------------------------------------------
+
+def msg_buffers(n: int, device):
+    lo = torch.empty((n, 8), dtype=torch.uint8, device=device)
+    hi = torch.empty(n, dtype=torch.uint8, device=device)
+    tb = torch.empty((n + 7) // 8, dtype=torch.uint8, device=device)
+    return lo, hi, tb
+
+
+def drelu_send(party, x, prm: Params, seed01: bytes, elem_base=0, out=None, stream=None):
+    """Alg 7 steps 1-8 for P0/P1: returns (lo, hi, tbits)."""
+    n = x.numel()
+    lo, hi, tb = msg_buffers(n, x.device) if out is None else out
+    _check(lib().bc_drelu_send(party, _dev(x, "x"), _dev(lo, "lo", 1), _dev(hi, "hi", 1), _dev(tb, "tbits", 1), n,
+                               elem_base, ctypes.byref(prm.c()), seed01, _stream(stream)), "bc_drelu_send")
+    return lo, hi, tb
+
+
+def drelu_helper(lo0, hi0, lo1, hi1, prm: Params, seed02: bytes, elem_base=0, paper_literal=False, out=None,
+                 stream=None):
+    """Alg 7 steps 9-10 for P2: returns (resp0 or None, resp1)."""
+    n = lo0.shape[0]
+    if out is None:
+        r0 = torch.empty(n, dtype=torch.int64, device=lo0.device) if paper_literal else None
+        r1 = torch.empty(n, dtype=torch.int64, device=lo0.device)
+    else:
+        r0, r1 = out
+    _check(lib().bc_drelu_helper(_dev(lo0, "lo0", 1), _opt(hi0, "hi0", 1), _dev(lo1, "lo1", 1), _opt(hi1, "hi1", 1),
+                                 _opt(r0, "resp0"), _dev(r1, "resp1"), n, elem_base, ctypes.byref(prm.c()), seed02,
+                                 _stream(stream)), "bc_drelu_helper")
+    return r0, r1
+
+
+def drelu_finish(party, tbits, resp, prm: Params, n: int, seed02: bytes | None = None, elem_base=0, out=None,
+                 stream=None):
+    """Alg 7 step 11 for P0/P1 (P0 may pass resp=None and seed02)."""
+    y = torch.empty(n, dtype=torch.int64, device=tbits.device) if out is None else out
+    _check(lib().bc_drelu_finish(party, _dev(tbits, "tbits", 1), _opt(resp, "resp"), _dev(y, "y"), n, elem_base,
+                                 ctypes.byref(prm.c()), seed02, _stream(stream)), "bc_drelu_finish")
+    return y
+
+
+def relu_send(party, x, prm: Params, seed01: bytes, seed_tr: bytes, elem_base=0, out=None, stream=None):
+    """Alg 8 steps 1, 4 for P0/P1: returns (lo, hi, tbits, dshare)."""
+    n = x.numel()
+    if out is None:
+        lo, hi, tb = msg_buffers(n, x.device)
+        d = torch.empty_like(x)
+    else:
+        lo, hi, tb, d = out
+    _check(lib().bc_relu_send(party, _dev(x, "x"), _dev(lo, "lo", 1), _dev(hi, "hi", 1), _dev(tb, "tbits", 1),
+                              _dev(d, "dshare"), n, elem_base, ctypes.byref(prm.c()), seed01, seed_tr,
+                              _stream(stream)), "bc_relu_send")
+    return lo, hi, tb, d
+
+
+def relu_helper(lo0, hi0, lo1, hi1, prm: Params, seed02: bytes, seed12: bytes, elem_base=0, with_c1=True, out=None,
+                stream=None):
+    """Alg 8 steps 2-3 for P2: returns (e, c1 or None)."""
+    n = lo0.shape[0]
+    if out is None:
+        e = torch.empty(n, dtype=torch.int64, device=lo0.device)
+        c1 = torch.empty(n, dtype=torch.int64, device=lo0.device) if with_c1 else None
+    else:
+        e, c1 = out
+    _check(lib().bc_relu_helper(_dev(lo0, "lo0", 1), _opt(hi0, "hi0", 1), _dev(lo1, "lo1", 1), _opt(hi1, "hi1", 1),
+                                _dev(e, "e"), _opt(c1, "c1"), n, elem_base, ctypes.byref(prm.c()), seed02, seed12,
+                                _stream(stream)), "bc_relu_helper")
+    return e, c1
+
+
+def relu_finish(party, x, tbits, d_own, d_peer, e, c1, prm: Params, seed_tr: bytes, elem_base=0, out=None,
+                stream=None):
+    """Alg 8 steps 4-5 for P0/P1."""
+    n = x.numel()
+    y = torch.empty_like(x) if out is None else out
+    _check(lib().bc_relu_finish(party, _dev(x, "x"), _dev(tbits, "tbits", 1), _dev(d_own, "d_own"),
+                                _dev(d_peer, "d_peer"), _dev(e, "e"), _opt(c1, "c1"), _dev(y, "y"), n, elem_base,
+                                ctypes.byref(prm.c()), seed_tr, _stream(stream)), "bc_relu_finish")
+    return y

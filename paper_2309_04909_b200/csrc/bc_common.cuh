@@ -1,0 +1,77 @@
+// bc_common.cuh -- shared device templates and host utilities of libbicoptor.
+//
+// Thread <-> data mapping: one thread owns a group of 8
+// consecutive elements.  That is the natural unit of the PRG: the compact
+// seed01 tape is 32 B per element (4 ChaCha blocks per group) and every 8-B
+// per-element stream of seed02 / seed12 is exactly one block per group, so no
+// keystream byte is generated twice and no keystream is exchanged between
+// threads.  Share vectors move as 4 x 16-B vector accesses per party per group.
+// Grids are persistent: (#SM x resident blocks) CTAs in a grid-stride loop.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <type_traits>
+
+#include "bc_device.cuh"
+#include "bicoptor.h"
+
+namespace bc {
+
+constexpr int TPB = 256;
+
+__device__ __forceinline__ uint64_t u64_of(const uint32_t (&B)[16], int e) {
+  return (uint64_t)B[2 * e] | ((uint64_t)B[2 * e + 1] << 32);
+}
+
+// seed01 tape block h of the group starting at global index j0 (j0 % 8 == 0).
+template <int R, bool COMPACT>
+__device__ __forceinline__ void tape_block(const Key& k01, uint64_t j0, int h, uint32_t (&B)[16]) {
+  if (COMPACT) chacha<R>(k01, (j0 >> 1) + (uint64_t)h, L_TAPE, B);
+  else chacha<R>(k01, j0 + (uint64_t)h, L_TAPEW, B);
+}
+
+template <int R, bool COMPACT>
+__device__ __forceinline__ void decode(const uint32_t (&B)[16], int s, uint64_t j, const Key& k01, const KP& kp,
+                                       Tape& tp) {
+  if (COMPACT) decode_compact<R>(&B[8 * s], j, k01, tp);
+  else decode_wide<R>(B, j, k01, kp, tp);
+}
+
+template <bool COMPACT, int PARTY>
+__device__ __forceinline__ void party_W(uint64_t x, const KP& kp, const Tape& tp, uint32_t (&W)[8]) {
+  if (COMPACT) party_W_compact<PARTY>(x, kp.f, tp, W);
+  else party_W_wide<PARTY>(x, kp, tp, W);
+}
+
+__device__ __forceinline__ uint64_t load_hi8(const uint8_t* hi, uint64_t i0, uint32_t cnt) {
+  if (!hi) return 0;
+  if (cnt == 8) return __ldg(reinterpret_cast<const unsigned long long*>(hi + i0));
+  uint64_t v = 0;
+  for (uint32_t e = 0; e < cnt; ++e) v |= (uint64_t)hi[i0 + e] << (8 * e);
+  return v;
+}
+
+// ---- host utilities (bc_host.cu) ------------------------------------------
+namespace host {
+int check_launch();                                  // cudaGetLastError -> BC_OK / BC_ECUDA
+int grid_for(const void* fn, uint64_t nthreads_work);  // persistent grid size
+bool aligned16(const void* p);
+bool aligned8(const void* p);
+bool overlap(const void* a, size_t na, const void* b, size_t nb);
+int check_params(const bc_params* prm);              // re-derives and compares
+KP make_kp(const bc_params* prm);
+Key make_key(const uint8_t* s);
+
+template <typename F>
+int dispatch_rounds(int rounds, F&& f) {
+  switch (rounds) {
+    case 8: return f(std::integral_constant<int, 8>{});
+    case 12: return f(std::integral_constant<int, 12>{});
+    case 20: return f(std::integral_constant<int, 20>{});
+    default: return BC_EINVAL;
+  }
+}
+}  // namespace host
+}  // namespace bc

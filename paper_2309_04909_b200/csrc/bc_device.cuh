@@ -1,0 +1,383 @@
+// bc_device.cuh -- device-side building blocks of the Bicoptor 2.0 hot path
+// (sm_100a).  Integer-only: no tensor cores, nothing here is a contraction.
+//
+// Per element j (global index) the computing parties run Alg 7 steps 1-8
+// (P:875-888), P2 runs steps 9-10 and P0/P1 step 11;
+// ReLU (Alg 8) adds the Beaver combine.  The randomness is a
+// ChaCha keystream per (seed, label), addressed by global element index
+// (DESIGN.md "PRG tape"), generated in registers and never stored.
+#pragma once
+#include <cstdint>
+
+namespace bc {
+
+// ---------------------------------------------------------------------------
+// Stream labels: 8 ASCII bytes read little-endian (ChaCha state words 14-15).
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr uint64_t lbl(const char (&s)[9]) {
+  uint64_t v = 0;
+  for (int i = 7; i >= 0; --i) v = (v << 8) | (uint64_t)(uint8_t)s[i];
+  return v;
+}
+constexpr uint64_t L_TAPE = lbl("bc2.tape");   // seed01, 32 B / element (compact)
+constexpr uint64_t L_TAPEW = lbl("bc2.tapw");  // seed01, 64 B / element (wide)
+constexpr uint64_t L_FB = lbl("bc2.fb01");     // seed01, fallback, counter j*256+k
+constexpr uint64_t L_RESP = lbl("bc2.resp");   // seed02, [DReLU']_0
+constexpr uint64_t L_A02 = lbl("bc2.ta02");    // seed02, [a]_0
+constexpr uint64_t L_B02 = lbl("bc2.tb02");    // seed02, [b]_0
+constexpr uint64_t L_C02 = lbl("bc2.tc02");    // seed02, [c]_0
+constexpr uint64_t L_A12 = lbl("bc2.ta12");    // seed12, [a]_1
+constexpr uint64_t L_B12 = lbl("bc2.tb12");    // seed12, [b]_1
+
+constexpr uint32_t PERM_LIMIT_8 = 53261u * 40320u;  // largest multiple of 8! below 2^31
+
+struct Key {
+  uint32_t k[8];
+};
+
+// Kernel-side protocol constants (derived on the host from bc_params).
+struct KP {
+  uint64_t ymask;      // 2^ell - 1
+  uint32_t f, w, p, S, lx;
+  uint32_t wmask;      // 2^w - 1
+  uint32_t perm_lim;   // floor(2^31 / S!) * S!
+  uint32_t fact;       // S!
+  uint32_t mask_lim;   // floor(65536 / (p-1)) * (p-1)
+  uint32_t rho_lim;    // floor(65536 / p) * p
+};
+
+// ---------------------------------------------------------------------------
+// ChaCha_R block (RFC 8439 sec. 2.3), words 12-13 = 64-bit counter, 14-15 =
+// 64-bit label.  Fully unrolled; the key lives in the constant bank.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t rotl(uint32_t v, int n) { return __funnelshift_l(v, v, n); }
+
+#define BC_QR(a, b, c, d)          \
+  a += b; d ^= a; d = rotl(d, 16); \
+  c += d; b ^= c; b = rotl(b, 12); \
+  a += b; d ^= a; d = rotl(d, 8);  \
+  c += d; b ^= c; b = rotl(b, 7);
+
+template <int R>
+__device__ __forceinline__ void chacha(const Key& key, uint64_t ctr, uint64_t label, uint32_t (&o)[16]) {
+  uint32_t x0 = 0x61707865u, x1 = 0x3320646eu, x2 = 0x79622d32u, x3 = 0x6b206574u;
+  uint32_t x4 = key.k[0], x5 = key.k[1], x6 = key.k[2], x7 = key.k[3];
+  uint32_t x8 = key.k[4], x9 = key.k[5], x10 = key.k[6], x11 = key.k[7];
+  const uint32_t c0 = (uint32_t)ctr, c1 = (uint32_t)(ctr >> 32);
+  const uint32_t l0 = (uint32_t)label, l1 = (uint32_t)(label >> 32);
+  uint32_t x12 = c0, x13 = c1, x14 = l0, x15 = l1;
+#pragma unroll
+  for (int r = 0; r < R; r += 2) {
+    BC_QR(x0, x4, x8, x12) BC_QR(x1, x5, x9, x13) BC_QR(x2, x6, x10, x14) BC_QR(x3, x7, x11, x15)
+    BC_QR(x0, x5, x10, x15) BC_QR(x1, x6, x11, x12) BC_QR(x2, x7, x8, x13) BC_QR(x3, x4, x9, x14)
+  }
+  o[0] = x0 + 0x61707865u; o[1] = x1 + 0x3320646eu; o[2] = x2 + 0x79622d32u; o[3] = x3 + 0x6b206574u;
+  o[4] = x4 + key.k[0]; o[5] = x5 + key.k[1]; o[6] = x6 + key.k[2]; o[7] = x7 + key.k[3];
+  o[8] = x8 + key.k[4]; o[9] = x9 + key.k[5]; o[10] = x10 + key.k[6]; o[11] = x11 + key.k[7];
+  o[12] = x12 + c0; o[13] = x13 + c1; o[14] = x14 + l0; o[15] = x15 + l1;
+}
+
+// ---------------------------------------------------------------------------
+// Small helpers
+// ---------------------------------------------------------------------------
+// x mod 257 for any 32-bit x: floor(x/257) = floor(x * (2^40+1)/257 / 2^40).
+__device__ __forceinline__ uint32_t mod257(uint32_t x) {
+  const uint32_t q = __umulhi(x, 0xFF00FF01u) >> 8;
+  return x - q * 257u;
+}
+// Zero-extended byte m (0..3) of v.
+__device__ __forceinline__ uint32_t byte_of(uint32_t v, int m) { return __byte_perm(v, 0u, 0x4440u | (uint32_t)m); }
+
+// Fisher-Yates over S slots on a nibble array (reading C9): for m = S-1..1,
+// k_m = q mod (m+1), q /= (m+1), swap nibbles m and k_m.  Nibble m of the
+// result is the pre-shuffle slot that lands in slot m (a PRMT selector).
+template <int S>
+__device__ __forceinline__ uint32_t perm_sel(uint32_t q) {
+  uint32_t sel = 0x76543210u;
+#pragma unroll
+  for (int m = S - 1; m >= 1; --m) {
+    const uint32_t k = q % (uint32_t)(m + 1);
+    q /= (uint32_t)(m + 1);
+    const uint32_t a = (sel >> (4 * m)) & 15u, b = (sel >> (4 * k)) & 15u, d = a ^ b;
+    sel ^= (d << (4 * m)) | (d << (4 * k));
+  }
+  return sel;
+}
+
+__device__ __forceinline__ uint32_t perm_sel_rt(uint32_t q, uint32_t S) {
+  uint32_t sel = 0x76543210u;
+#pragma unroll
+  for (int m = 7; m >= 1; --m) {
+    if ((uint32_t)m < S) {
+      const uint32_t k = q % (uint32_t)(m + 1);
+      q /= (uint32_t)(m + 1);
+      const uint32_t a = (sel >> (4 * m)) & 15u, b = (sel >> (4 * k)) & 15u, d = a ^ b;
+      sel ^= (d << (4 * m)) | (d << (4 * k));
+    }
+  }
+  return sel;
+}
+
+// Pack bytes a_i = (v >> i) & 255, i = 0..7, into two words (little endian).
+__device__ __forceinline__ void window_bytes(uint32_t v, uint32_t& lo, uint32_t& hi) {
+  lo = (v & 0xFFu) | ((v << 7) & 0xFF00u) | ((v << 14) & 0xFF0000u) | ((v << 21) & 0xFF000000u);
+  hi = ((v >> 4) & 0xFFu) | ((v << 3) & 0xFF00u) | ((v << 10) & 0xFF0000u) | ((v << 17) & 0xFF000000u);
+}
+
+// ---------------------------------------------------------------------------
+// Rejection fallback (reading C10): sequential u32 words of
+// ChaCha(seed01, L_FB, counter j*256 + k).  Rare (~1e-4 per element); kept
+// out of line so the fast path carries no extra block.
+// ---------------------------------------------------------------------------
+template <int R>
+struct FbStream {
+  Key key;
+  uint64_t j;
+  uint32_t blk[16];
+  uint32_t pos, kc;
+  __device__ uint32_t next() {
+    if (pos == 16) {
+      chacha<R>(key, j * 256u + kc, L_FB, blk);
+      ++kc;
+      pos = 0;
+    }
+    return blk[pos++];
+  }
+};
+
+struct Draws {  // raw draws of one element: perm index, 8 mask u16, 8 reshare u16
+  uint32_t idx;
+  uint32_t um[8];
+  uint32_t ur[8];
+};
+
+template <int R>
+__device__ __noinline__ void fallback(Draws& d, uint64_t j, Key key, uint32_t S, uint32_t perm_lim,
+                                      uint32_t mask_lim /*0: masks never rejected*/, uint32_t rho_lim) {
+  FbStream<R> fb;
+  fb.key = key; fb.j = j; fb.pos = 16; fb.kc = 0;
+  if (d.idx >= perm_lim) {
+    uint32_t v = fb.next() & 0x7FFFFFFFu;
+    while (v >= perm_lim) v = fb.next() & 0x7FFFFFFFu;
+    d.idx = v;
+  }
+  if (mask_lim) {
+    for (uint32_t m = 0; m < S; ++m)
+      if (d.um[m] >= mask_lim) {
+        uint32_t v = fb.next() & 0xFFFFu;
+        while (v >= mask_lim) v = fb.next() & 0xFFFFu;
+        d.um[m] = v;
+      }
+  }
+  for (uint32_t m = 0; m < S; ++m)
+    if (d.ur[m] >= rho_lim) {
+      uint32_t v = fb.next() & 0xFFFFu;
+      while (v >= rho_lim) v = fb.next() & 0xFFFFu;
+      d.ur[m] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Decoded seed01 randomness of one element (Alg 7 steps 1, 6, 7, 8).
+// ---------------------------------------------------------------------------
+struct Tape {
+  uint32_t t;        // blinding bit (step 1)
+  uint32_t sel;      // permutation as a PRMT nibble selector (step 6)
+  uint32_t rm1[2];   // compact: bytes r_m - 1 (step 7)
+  uint32_t r[8];     // wide: r_m in Z_p^*
+  uint32_t rho[8];   // reshare rho_m in Z_p (step 8)
+};
+
+// Compact tape: 8 words T[0..7] = keystream bytes [32 j, 32 j + 32).
+//   T0: bit 31 = t, bits 0..30 = permutation index (reject >= 53261 * 8!)
+//   T1, T2: bytes m = r_m - 1 (exactly uniform on Z_257^*)
+//   T3..T6: u16 m = reshare draw (reject 65535), rho_m = u mod 257
+template <int R>
+__device__ __forceinline__ void decode_compact(const uint32_t* T, uint64_t j, const Key& k01, Tape& tp) {
+  const uint32_t T0 = T[0];
+  tp.t = T0 >> 31;
+  uint32_t idx = T0 & 0x7FFFFFFFu;
+  uint32_t w3 = T[3], w4 = T[4], w5 = T[5], w6 = T[6];
+  // any u16 == 0xFFFF  <=>  some halfword of ~w is zero
+  const uint32_t n3 = ~w3, n4 = ~w4, n5 = ~w5, n6 = ~w6;
+  const bool bad_rho = ((n3 & 0xFFFFu) == 0) | ((n3 >> 16) == 0) | ((n4 & 0xFFFFu) == 0) | ((n4 >> 16) == 0) |
+                       ((n5 & 0xFFFFu) == 0) | ((n5 >> 16) == 0) | ((n6 & 0xFFFFu) == 0) | ((n6 >> 16) == 0);
+  if (__builtin_expect(bad_rho | (idx >= PERM_LIMIT_8), 0)) {
+    Draws d;
+    d.idx = idx;
+    d.ur[0] = w3 & 0xFFFFu; d.ur[1] = w3 >> 16; d.ur[2] = w4 & 0xFFFFu; d.ur[3] = w4 >> 16;
+    d.ur[4] = w5 & 0xFFFFu; d.ur[5] = w5 >> 16; d.ur[6] = w6 & 0xFFFFu; d.ur[7] = w6 >> 16;
+    fallback<R>(d, j, k01, 8, PERM_LIMIT_8, 0, 65535u);
+    idx = d.idx;
+    w3 = d.ur[0] | (d.ur[1] << 16); w4 = d.ur[2] | (d.ur[3] << 16);
+    w5 = d.ur[4] | (d.ur[5] << 16); w6 = d.ur[6] | (d.ur[7] << 16);
+  }
+  tp.rm1[0] = T[1];
+  tp.rm1[1] = T[2];
+  tp.rho[0] = mod257(w3 & 0xFFFFu); tp.rho[1] = mod257(w3 >> 16);
+  tp.rho[2] = mod257(w4 & 0xFFFFu); tp.rho[3] = mod257(w4 >> 16);
+  tp.rho[4] = mod257(w5 & 0xFFFFu); tp.rho[5] = mod257(w5 >> 16);
+  tp.rho[6] = mod257(w6 & 0xFFFFu); tp.rho[7] = mod257(w6 >> 16);
+  tp.sel = perm_sel<8>(idx % 40320u);
+}
+
+// Wide tape: 16 words T[0..15] = keystream bytes [64 j, 64 j + 64).
+//   T0: t | perm index (reject >= floor(2^31/S!) S!)
+//   T1..T4: u16 m = mask draw, r_m = 1 + u mod (p-1) (reject >= floor(65536/(p-1))(p-1))
+//   T5..T8: u16 m = reshare draw, rho_m = u mod p (reject >= floor(65536/p) p)
+template <int R>
+__device__ __forceinline__ void decode_wide(const uint32_t* T, uint64_t j, const Key& k01, const KP& kp, Tape& tp) {
+  Draws d;
+  tp.t = T[0] >> 31;
+  d.idx = T[0] & 0x7FFFFFFFu;
+  bool bad = d.idx >= kp.perm_lim;
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    d.um[m] = (T[1 + m / 2] >> (16 * (m & 1))) & 0xFFFFu;
+    d.ur[m] = (T[5 + m / 2] >> (16 * (m & 1))) & 0xFFFFu;
+    if ((uint32_t)m < kp.S) bad |= (d.um[m] >= kp.mask_lim) | (d.ur[m] >= kp.rho_lim);
+  }
+  if (__builtin_expect(bad, 0)) fallback<R>(d, j, k01, kp.S, kp.perm_lim, kp.mask_lim, kp.rho_lim);
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    tp.r[m] = 1u + d.um[m] % (kp.p - 1u);
+    tp.rho[m] = d.ur[m] % kp.p;
+  }
+  tp.sel = perm_sel_rt(d.idx % kp.fact, kp.S);
+}
+
+// ---------------------------------------------------------------------------
+// Alg 7 steps 1-8 for one party: W_m, the message to P2 (values in Z_p).
+//   1-2 s = (-1)^t x;  P1 works on n = -s (Alg 5, reading C3)
+//   3   u_i = window [f+i, f+i+w) (Alg 5, k1 = f+i, k2 = ell-w-f-i)
+//   4   v_i = u_i + u_{i+1} - 1 (P0 carries the -1), v_lx = u_lx - 1
+//   5   modulo switch (Alg 6) -> encoded as bytes v'-1
+//   6   shuffle: PRMT with the permutation selector
+//   7-8 W_m = v'_m r_m + rho_m (P0) / v'_m r_m - rho_m (P1)  mod p
+// ---------------------------------------------------------------------------
+template <int PARTY>
+__device__ __forceinline__ void party_W_compact(uint64_t x, uint32_t f, const Tape& tp, uint32_t (&W)[8]) {
+  const uint64_t nx = 0ull - x;
+  // P0: s0 = t ? -x : x.   P1: n1 = -s1 = t ? x : -x.
+  const uint64_t v = (PARTY == 0) ? (tp.t ? nx : x) : (tp.t ? x : nx);
+  const uint32_t win = (uint32_t)(v >> f);
+  uint32_t A_lo, A_hi;
+  window_bytes(win, A_lo, A_hi);                         // u_i (P0) or -u_i (P1), w = 8
+  const uint32_t N_lo = __byte_perm(A_lo, A_hi, 0x4321u); // u_{i+1}, u_8 := 0
+  const uint32_t N_hi = A_hi >> 8;
+  uint32_t C_lo, C_hi;
+  if (PARTY == 0) {  // v'-1 = (u_i + u_{i+1} - 1 == 0 ? 256 : ...) - 1 = u_i + u_{i+1} - 2 mod 256
+    C_lo = __vsub4(__vadd4(A_lo, N_lo), 0x02020202u);
+    C_hi = __vsub4(__vadd4(A_hi, N_hi), 0x02020202u);
+  } else {           // v' - 1 = (257 + v - 256) mod 257 - 1 = v = -(B_i + B_{i+1}) mod 256
+    C_lo = __vneg4(__vadd4(A_lo, N_lo));
+    C_hi = __vneg4(__vadd4(A_hi, N_hi));
+  }
+  const uint32_t P_lo = __byte_perm(C_lo, C_hi, tp.sel & 0xFFFFu);
+  const uint32_t P_hi = __byte_perm(C_lo, C_hi, tp.sel >> 16);
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const uint32_t c = byte_of(m < 4 ? P_lo : P_hi, m & 3);
+    const uint32_t r = byte_of(tp.rm1[m >> 2], m & 3) + 1u;
+    const uint32_t add = (PARTY == 0) ? r + tp.rho[m] : r + 257u - tp.rho[m];
+    W[m] = mod257(c * r + add);                          // ((c+1) r +- rho) mod 257
+  }
+}
+
+template <int PARTY>
+__device__ __forceinline__ void party_W_wide(uint64_t x, const KP& kp, const Tape& tp, uint32_t (&W)[8]) {
+  const uint64_t nx = 0ull - x;
+  const uint64_t v = (PARTY == 0) ? (tp.t ? nx : x) : (tp.t ? x : nx);
+  const uint32_t win = (uint32_t)(v >> kp.f);
+  uint32_t u[9];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t a = (win >> i) & kp.wmask;
+    u[i] = (PARTY == 0) ? a : ((0u - a) & kp.wmask);  // P1: -cut(-s) mod 2^w
+  }
+  u[8] = 0;
+  uint32_t bytes_lo = 0, bytes_hi = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    uint32_t e = 0;
+    if ((uint32_t)i <= kp.lx) {
+      const uint32_t nxt = ((uint32_t)i < kp.lx) ? u[i + 1] : 0u;
+      uint32_t vi = (u[i] + nxt - (PARTY == 0 ? 1u : 0u)) & kp.wmask;  // step 4
+      uint32_t vp;                                                      // step 5 (Alg 6)
+      if (PARTY == 0) vp = (vi == 0) ? ((1u << kp.w) % kp.p) : vi % kp.p;
+      else vp = (kp.p + vi - (1u << kp.w)) % kp.p;
+      e = vp - 1u;
+    }
+    if (i < 4) bytes_lo |= e << (8 * i); else bytes_hi |= e << (8 * (i - 4));
+  }
+  const uint32_t P_lo = __byte_perm(bytes_lo, bytes_hi, tp.sel & 0xFFFFu);
+  const uint32_t P_hi = __byte_perm(bytes_lo, bytes_hi, tp.sel >> 16);
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const uint32_t c = byte_of(m < 4 ? P_lo : P_hi, m & 3) + 1u;
+    const uint32_t rr = (PARTY == 0) ? tp.rho[m] : (kp.p - tp.rho[m]);
+    W[m] = ((uint32_t)m < kp.S) ? (c * tp.r[m] + rr) % kp.p : 0u;
+  }
+}
+
+// P2's zero test (Alg 7 step 9): 1 iff some (W0_m + W1_m) mod p == 0.
+__device__ __forceinline__ uint32_t zero_test(const uint32_t (&W0)[8], const uint32_t (&W1)[8], uint32_t p, uint32_t S) {
+  uint32_t z = 0;
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const uint32_t s = W0[m] + W1[m];
+    z |= ((uint32_t)m < S) & ((s == 0) | (s == p));
+  }
+  return z;
+}
+
+// Wire format: low bytes as one u64, high bits (bit 8 of W_m) as one byte.
+__device__ __forceinline__ uint64_t pack_lo(const uint32_t (&W)[8]) {
+  // [W0.b0, W1.b0, W0.b1, W1.b1] then merge the low halves: 3 PRMT per word
+  const uint32_t lo = __byte_perm(__byte_perm(W[0], W[1], 0x5140u), __byte_perm(W[2], W[3], 0x5140u), 0x5410u);
+  const uint32_t hi = __byte_perm(__byte_perm(W[4], W[5], 0x5140u), __byte_perm(W[6], W[7], 0x5140u), 0x5410u);
+  return (uint64_t)lo | ((uint64_t)hi << 32);
+}
+__device__ __forceinline__ uint32_t pack_hi(const uint32_t (&W)[8]) {
+  uint32_t h = 0;
+#pragma unroll
+  for (int m = 0; m < 8; ++m) h |= ((W[m] >> 8) & 1u) << m;
+  return h;
+}
+__device__ __forceinline__ void unpack_W(uint64_t lo, uint32_t hi, uint32_t (&W)[8]) {
+#pragma unroll
+  for (int m = 0; m < 8; ++m) W[m] = (uint32_t)((lo >> (8 * m)) & 0xFFu) | (((hi >> m) & 1u) << 8);
+}
+
+// ---------------------------------------------------------------------------
+// Vector loads / stores of 8 consecutive u64 (one group).  The caller
+// guarantees 16-B alignment of the array base; full groups are 64-B aligned
+// relative to it.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void load8(const uint64_t* __restrict__ p, uint64_t (&v)[8], uint32_t cnt) {
+  if (cnt >= 8) {
+    const ulonglong2* q = reinterpret_cast<const ulonglong2*>(p);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const ulonglong2 t = __ldg(q + i);
+      v[2 * i] = t.x;
+      v[2 * i + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = ((uint32_t)i < cnt) ? __ldg(p + i) : 0ull;
+  }
+}
+__device__ __forceinline__ void store8(uint64_t* __restrict__ p, const uint64_t (&v)[8], uint32_t cnt) {
+  if (cnt >= 8) {
+    ulonglong2* q = reinterpret_cast<ulonglong2*>(p);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) q[i] = make_ulonglong2(v[2 * i], v[2 * i + 1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if ((uint32_t)i < cnt) p[i] = v[i];
+  }
+}
+
+}  // namespace bc

@@ -1,0 +1,223 @@
+// bc_elem.cu -- elementwise primitives, HBM-bound: Alg 4/5 deterministic
+// truncation, Alg 1 SecureML truncation, Alg 6 modulo switch and Alg 7 steps
+// 3-5 (ladder + pairwise + modulo switch).  Two elements per thread per
+// iteration: one 16-B load and one 16-B (or 8-B) store, fully coalesced.
+#include "bc_common.cuh"
+
+using namespace bc;
+using namespace bc::host;
+
+namespace {
+
+struct EwArgs {
+  const uint64_t* in;
+  void* out;
+  uint64_t n;
+  uint64_t ymask;   // output modulus mask
+  uint64_t inmask;  // 2^ell - 1
+  uint32_t k1;
+  uint32_t lp, p;
+  int party;
+};
+
+__device__ __forceinline__ void load_pair(const uint64_t* __restrict__ in, uint64_t i, uint64_t n, uint64_t (&v)[2]) {
+  if (2 * i + 1 < n) {
+    const ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(in) + i);
+    v[0] = t.x;
+    v[1] = t.y;
+  } else {
+    v[0] = __ldg(in + 2 * i);
+    v[1] = 0;
+  }
+}
+
+__device__ __forceinline__ void store_pair(uint64_t* __restrict__ out, uint64_t i, uint64_t n, const uint64_t (&v)[2]) {
+  if (2 * i + 1 < n) reinterpret_cast<ulonglong2*>(out)[i] = make_ulonglong2(v[0], v[1]);
+  else out[2 * i] = v[0];
+}
+
+// Alg 5 (k2 = 0: Alg 4): P0 cut(x, k1, k2); P1 -cut(-x, k1, k2), mod 2^(ell-k1-k2).
+__global__ void __launch_bounds__(TPB) k_trc(EwArgs a) {
+  const uint64_t npairs = (a.n + 1) >> 1;
+  for (uint64_t i = (uint64_t)blockIdx.x * TPB + threadIdx.x; i < npairs; i += (uint64_t)gridDim.x * TPB) {
+    uint64_t v[2];
+    load_pair(a.in, i, a.n, v);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const uint64_t x = a.party == 0 ? v[k] : (0ull - v[k]) & a.inmask;
+      const uint64_t c = (x >> a.k1) & a.ymask;
+      v[k] = a.party == 0 ? c : (0ull - c) & a.ymask;
+    }
+    store_pair(static_cast<uint64_t*>(a.out), i, a.n, v);
+  }
+}
+
+// Alg 1: P0 cut(x, k) mod 2^ell; P1 2^ell - cut(2^ell - x, k) mod 2^ell (reading C3).
+__global__ void __launch_bounds__(TPB) k_trc_prob(EwArgs a) {
+  const uint64_t npairs = (a.n + 1) >> 1;
+  for (uint64_t i = (uint64_t)blockIdx.x * TPB + threadIdx.x; i < npairs; i += (uint64_t)gridDim.x * TPB) {
+    uint64_t v[2];
+    load_pair(a.in, i, a.n, v);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const uint64_t x = v[k] & a.inmask;
+      v[k] = a.party == 0 ? (x >> a.k1) : (0ull - (((0ull - x) & a.inmask) >> a.k1)) & a.inmask;
+    }
+    store_pair(static_cast<uint64_t*>(a.out), i, a.n, v);
+  }
+}
+
+// Alg 6.
+__global__ void __launch_bounds__(TPB) k_modswitch(EwArgs a) {
+  const uint64_t npairs = (a.n + 1) >> 1;
+  const uint64_t lmask = (1ull << a.lp) - 1ull;
+  const uint64_t two_lp = 1ull << a.lp;
+  uint32_t* out = static_cast<uint32_t*>(a.out);
+  const bool vec = (reinterpret_cast<uintptr_t>(out) & 7) == 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * TPB + threadIdx.x; i < npairs; i += (uint64_t)gridDim.x * TPB) {
+    uint64_t v[2];
+    load_pair(a.in, i, a.n, v);
+    uint32_t o[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const uint64_t x = v[k] & lmask;
+      if (a.party == 0) o[k] = (uint32_t)(x == 0 ? two_lp % a.p : x % a.p);
+      else o[k] = (uint32_t)(((uint64_t)a.p + x - two_lp) % a.p);
+    }
+    if (2 * i + 1 < a.n && vec) {
+      reinterpret_cast<uint2*>(out)[i] = make_uint2(o[0], o[1]);
+    } else {
+      out[2 * i] = o[0];
+      if (2 * i + 1 < a.n) out[2 * i + 1] = o[1];
+    }
+  }
+}
+
+// Alg 7 steps 3-5 on the share as given: bytes v'_m - 1 (slot m -> byte m).
+template <int PARTY>
+__device__ __forceinline__ uint64_t ladder_bytes(uint64_t x, const KP& kp, bool compact) {
+  const uint64_t v = PARTY == 0 ? x : 0ull - x;  // P1 works on -[x]_1 (Alg 5, reading C3)
+  const uint32_t win = (uint32_t)(v >> kp.f);
+  if (compact) {  // w = 8, p = 257: SWAR over the 8 windows
+    uint32_t A_lo, A_hi;
+    window_bytes(win, A_lo, A_hi);
+    const uint32_t N_lo = __byte_perm(A_lo, A_hi, 0x4321u), N_hi = A_hi >> 8;
+    uint32_t C_lo, C_hi;
+    if (PARTY == 0) {
+      C_lo = __vsub4(__vadd4(A_lo, N_lo), 0x02020202u);
+      C_hi = __vsub4(__vadd4(A_hi, N_hi), 0x02020202u);
+    } else {
+      C_lo = __vneg4(__vadd4(A_lo, N_lo));
+      C_hi = __vneg4(__vadd4(A_hi, N_hi));
+    }
+    return (uint64_t)C_lo | ((uint64_t)C_hi << 32);
+  }
+  uint32_t u[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t b = (win >> i) & kp.wmask;
+    u[i] = PARTY == 0 ? b : ((0u - b) & kp.wmask);
+  }
+  uint64_t out = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if ((uint32_t)i <= kp.lx) {
+      const uint32_t nxt = ((uint32_t)i < kp.lx) ? u[i + 1] : 0u;
+      const uint32_t vi = (u[i] + nxt - (PARTY == 0 ? 1u : 0u)) & kp.wmask;
+      uint32_t vp;
+      if (PARTY == 0) vp = (vi == 0) ? ((1u << kp.w) % kp.p) : vi % kp.p;
+      else vp = (kp.p + vi - (1u << kp.w)) % kp.p;
+      out |= (uint64_t)(vp - 1u) << (8 * i);
+    }
+  }
+  return out;
+}
+
+template <int PARTY>
+__global__ void __launch_bounds__(TPB) k_ladder(const uint64_t* __restrict__ x, uint64_t* __restrict__ v, uint64_t n,
+                                                KP kp, int compact) {
+  const uint64_t npairs = (n + 1) >> 1;
+  for (uint64_t i = (uint64_t)blockIdx.x * TPB + threadIdx.x; i < npairs; i += (uint64_t)gridDim.x * TPB) {
+    uint64_t t[2];
+    load_pair(x, i, n, t);
+    t[0] = ladder_bytes<PARTY>(t[0], kp, compact);
+    t[1] = ladder_bytes<PARTY>(t[1], kp, compact);
+    store_pair(v, i, n, t);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int bc_trc(int party, const uint64_t* in, uint64_t* out, size_t n, int ell, int k1, int k2, void* stream) {
+  if ((party != 0 && party != 1) || !in || !out || ell < 2 || ell > 64 || k1 < 0 || k2 < 0 || k1 + k2 >= ell)
+    return BC_EINVAL;
+  if (!aligned16(in) || !aligned16(out)) return BC_EALIGN;
+  if (overlap(in, n * 8, out, n * 8)) return BC_EALIAS;
+  if (n == 0) return BC_OK;
+  const int lp = ell - k1 - k2;
+  EwArgs a{};
+  a.in = in;
+  a.out = out;
+  a.n = n;
+  a.party = party;
+  a.k1 = (uint32_t)k1;
+  a.ymask = lp == 64 ? ~0ull : ((1ull << lp) - 1ull);
+  a.inmask = ell == 64 ? ~0ull : ((1ull << ell) - 1ull);
+  k_trc<<<grid_for((const void*)k_trc, (n + 1) / 2), TPB, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  return check_launch();
+}
+
+int bc_trc_prob(int party, const uint64_t* in, uint64_t* out, size_t n, int ell, int k, void* stream) {
+  if ((party != 0 && party != 1) || !in || !out || ell < 2 || ell > 64 || k < 0 || k >= ell) return BC_EINVAL;
+  if (!aligned16(in) || !aligned16(out)) return BC_EALIGN;
+  if (overlap(in, n * 8, out, n * 8)) return BC_EALIAS;
+  if (n == 0) return BC_OK;
+  EwArgs a{};
+  a.in = in;
+  a.out = out;
+  a.n = n;
+  a.party = party;
+  a.k1 = (uint32_t)k;
+  a.inmask = ell == 64 ? ~0ull : ((1ull << ell) - 1ull);
+  k_trc_prob<<<grid_for((const void*)k_trc_prob, (n + 1) / 2), TPB, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  return check_launch();
+}
+
+int bc_modswitch(int party, const uint64_t* in, uint32_t* out, size_t n, int lp, uint32_t p, void* stream) {
+  if ((party != 0 && party != 1) || !in || !out || lp < 1 || lp > 31 || (uint64_t)p <= (1ull << lp))
+    return BC_EINVAL;
+  if (!aligned16(in) || (reinterpret_cast<uintptr_t>(out) & 3)) return BC_EALIGN;
+  if (overlap(in, n * 8, out, n * 4)) return BC_EALIAS;
+  if (n == 0) return BC_OK;
+  EwArgs a{};
+  a.in = in;
+  a.out = out;
+  a.n = n;
+  a.party = party;
+  a.lp = (uint32_t)lp;
+  a.p = p;
+  k_modswitch<<<grid_for((const void*)k_modswitch, (n + 1) / 2), TPB, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  return check_launch();
+}
+
+int bc_ladder_modswitch(int party, const uint64_t* x, uint8_t* v, size_t n, const bc_params* prm, void* stream) {
+  const int rc = check_params(prm);
+  if (rc) return rc;
+  if ((party != 0 && party != 1) || !x || !v) return BC_EINVAL;
+  if (!aligned16(x) || !aligned16(v)) return BC_EALIGN;
+  if (overlap(x, n * 8, v, n * 8)) return BC_EALIAS;
+  if (n == 0) return BC_OK;
+  const KP kp = make_kp(prm);
+  const int compact = prm->compact;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint64_t* vo = reinterpret_cast<uint64_t*>(v);
+  if (party == 0)
+    k_ladder<0><<<grid_for((const void*)k_ladder<0>, (n + 1) / 2), TPB, 0, st>>>(x, vo, n, kp, compact);
+  else
+    k_ladder<1><<<grid_for((const void*)k_ladder<1>, (n + 1) / 2), TPB, 0, st>>>(x, vo, n, kp, compact);
+  return check_launch();
+}
+
+}  // extern "C"

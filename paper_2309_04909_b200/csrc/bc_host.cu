@@ -1,0 +1,152 @@
+// bc_host.cu -- host-side utilities and the parameter / error entry points of the C ABI.
+#include <cstring>
+#include <mutex>
+
+#include "bc_common.cuh"
+
+namespace {
+thread_local int g_last_cuda = 0;
+
+bool is_prime(uint32_t v) {
+  if (v < 2) return false;
+  for (uint32_t d = 2; (uint64_t)d * d <= v; ++d)
+    if (v % d == 0) return false;
+  return true;
+}
+
+uint32_t factorial(uint32_t s) {
+  uint32_t f = 1;
+  for (uint32_t i = 2; i <= s; ++i) f *= i;
+  return f;
+}
+}  // namespace
+
+namespace bc {
+namespace host {
+
+int check_launch() {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_last_cuda = (int)e;
+    return BC_ECUDA;
+  }
+  return BC_OK;
+}
+
+// Persistent grid: min(#work blocks, #SM x resident blocks per SM), cached per (kernel, device).
+int grid_for(const void* fn, uint64_t nthreads_work) {
+  struct Entry {
+    const void* fn;
+    int dev;
+    int cap;
+  };
+  static std::mutex mu;
+  static Entry cache[512];
+  static int ncache = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int cap = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (int i = 0; i < ncache; ++i)
+      if (cache[i].fn == fn && cache[i].dev == dev) {
+        cap = cache[i].cap;
+        break;
+      }
+    if (!cap) {
+      int sms = 0, occ = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, TPB, 0);
+      cap = std::max(1, sms) * std::max(1, occ);
+      if (ncache < 512) cache[ncache++] = Entry{fn, dev, cap};
+    }
+  }
+  const uint64_t want = (nthreads_work + TPB - 1) / TPB;
+  return (int)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)cap));
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+bool aligned8(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7u) == 0; }
+
+bool overlap(const void* a, size_t na, const void* b, size_t nb) {
+  if (!a || !b || !na || !nb) return false;
+  const uintptr_t x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+  return x < y + nb && y < x + na;
+}
+
+int check_params(const bc_params* prm) {
+  if (!prm) return BC_EINVAL;
+  bc_params ref;
+  const int rc = bc_params_init(&ref, prm->ell, prm->lx, prm->f, prm->mode, prm->rounds);
+  if (rc) return rc;
+  if (ref.w != prm->w || ref.p != prm->p || ref.slots != prm->slots || ref.compact != prm->compact) return BC_EINVAL;
+  return BC_OK;
+}
+
+KP make_kp(const bc_params* prm) {
+  KP kp;
+  kp.ymask = prm->ell == 64 ? ~0ull : ((1ull << prm->ell) - 1ull);
+  kp.f = (uint32_t)prm->f;
+  kp.w = prm->w;
+  kp.p = prm->p;
+  kp.S = prm->slots;
+  kp.lx = (uint32_t)prm->lx;
+  kp.wmask = (1u << prm->w) - 1u;
+  kp.fact = factorial(prm->slots);
+  kp.perm_lim = (uint32_t)((0x80000000ull / kp.fact) * kp.fact);
+  kp.mask_lim = (65536u / (prm->p - 1u)) * (prm->p - 1u);
+  kp.rho_lim = (65536u / prm->p) * prm->p;
+  return kp;
+}
+
+Key make_key(const uint8_t* s) {
+  Key k;
+  std::memcpy(k.k, s, 32);  // little-endian host: words are the LE u32 of the seed
+  return k;
+}
+
+}  // namespace host
+}  // namespace bc
+
+extern "C" {
+
+int bc_version(void) { return 100; }
+
+int bc_last_cuda_error(void) { return g_last_cuda; }
+
+const char* bc_strerror(int code) {
+  switch (code) {
+    case BC_OK: return "ok";
+    case BC_EINVAL: return "invalid parameter";
+    case BC_ERANGE: return "key-bit window does not fit: need f + lx + w <= ell";
+    case BC_EALIGN: return "pointer misaligned (16 B for u64 arrays) or elem_base not a multiple of 8";
+    case BC_ECUDA: return "CUDA launch error (see bc_last_cuda_error)";
+    case BC_EALIAS: return "output overlaps an input";
+    default: return "unknown error";
+  }
+}
+
+int bc_params_init(bc_params* out, int ell, int lx, int f, int mode, int rounds) {
+  if (!out) return BC_EINVAL;
+  if (ell < 2 || ell > 64 || lx < 2 || lx > 7 || f < 0 || (mode != BC_MODE_GUARD && mode != BC_MODE_LITERAL) ||
+      (rounds != 8 && rounds != 12 && rounds != 20))
+    return BC_EINVAL;
+  const uint32_t w = (uint32_t)(mode == BC_MODE_GUARD ? lx + 1 : lx);
+  if ((uint64_t)f + (uint64_t)lx + w > (uint64_t)ell) return BC_ERANGE;
+  uint32_t p = (1u << w) + 1u;  // smallest prime > 2^w (reading C7)
+  while (!is_prime(p)) ++p;
+  bc_params r;
+  r.ell = ell;
+  r.lx = lx;
+  r.f = f;
+  r.mode = mode;
+  r.rounds = rounds;
+  r.w = w;
+  r.p = p;
+  r.slots = (uint32_t)lx + 1u;
+  r.compact = (p == 257u && r.slots == 8u) ? 1 : 0;
+  *out = r;
+  return BC_OK;
+}
+
+}  // extern "C"

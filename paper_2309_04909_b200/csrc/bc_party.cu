@@ -1,0 +1,340 @@
+// bc_party.cu -- party-separated phases of Alg 7 / Alg 8: send (P0, P1),
+// helper (P2), finish (P0, P1).  Each party runs its phase on its own device;
+// the caller moves the message buffers (NCCL send/recv over NVLink).
+#include "bc_common.cuh"
+
+using namespace bc;
+using namespace bc::host;
+
+namespace {
+
+struct SendArgs {
+  const uint64_t* x;
+  uint8_t* lo;
+  uint8_t* hi;
+  uint8_t* tbits;
+  uint64_t* dshare;
+  uint64_t n, base;
+};
+
+// Alg 7 steps 1-8 (and Alg 8's [d]_b) for one computing party.
+template <int R, bool COMPACT, int PARTY, bool RELU>
+__global__ void __launch_bounds__(TPB, 2) k_send(SendArgs a, KP kp, Key k01, Key ktr) {
+  const uint64_t ngroups = (a.n + 7) >> 3;
+  for (uint64_t g = (uint64_t)blockIdx.x * TPB + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB) {
+    const uint64_t i0 = g << 3;
+    const uint64_t j0 = a.base + i0;
+    const uint32_t cnt = (uint32_t)min((uint64_t)8, a.n - i0);
+    uint64_t x[8], lo[8];
+    load8(a.x + i0, x, cnt);
+    uint32_t tb = 0;
+    uint64_t hi = 0;
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      uint32_t B[16];
+      if (COMPACT) tape_block<R, true>(k01, j0, h, B);
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int e = 2 * h + s;
+        if (!COMPACT) tape_block<R, false>(k01, j0, e, B);
+        Tape tp;
+        decode<R, COMPACT>(B, COMPACT ? s : 0, j0 + e, k01, kp, tp);
+        uint32_t W[8];
+        party_W<COMPACT, PARTY>(x[e], kp, tp, W);
+        lo[e] = pack_lo(W);
+        hi |= (uint64_t)pack_hi(W) << (8 * e);
+        tb |= tp.t << e;
+      }
+    }
+    store8(reinterpret_cast<uint64_t*>(a.lo) + i0, lo, cnt);
+    if (a.hi) {
+      if (cnt == 8) *reinterpret_cast<uint64_t*>(a.hi + i0) = hi;
+      else
+        for (uint32_t e = 0; e < cnt; ++e) a.hi[i0 + e] = (uint8_t)(hi >> (8 * e));
+    }
+    a.tbits[g] = (uint8_t)(tb & ((1u << cnt) - 1u));
+    if (RELU) {  // Alg 8 step 4: [d]_b = [x]_b - [a]_b
+      uint32_t Ak[16];
+      chacha<R>(ktr, j0 >> 3, PARTY == 0 ? L_A02 : L_A12, Ak);
+      uint64_t d[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) d[e] = (x[e] - u64_of(Ak, e)) & kp.ymask;
+      store8(a.dshare + i0, d, cnt);
+    }
+  }
+}
+
+struct HelperArgs {
+  const uint8_t *lo0, *hi0, *lo1, *hi1;
+  uint64_t* out0;  // DReLU: resp0 (nullable)   ReLU: e
+  uint64_t* out1;  // DReLU: resp1              ReLU: c1 (nullable)
+  uint64_t n, base;
+};
+
+// P2: Alg 7 steps 9-10, or Alg 8 steps 2-3 with the triple's [c]_1.
+template <int R, bool RELU>
+__global__ void __launch_bounds__(TPB, 2) k_helper(HelperArgs a, KP kp, Key k02, Key k12) {
+  const uint64_t ngroups = (a.n + 7) >> 3;
+  for (uint64_t g = (uint64_t)blockIdx.x * TPB + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB) {
+    const uint64_t i0 = g << 3;
+    const uint64_t j0 = a.base + i0;
+    const uint32_t cnt = (uint32_t)min((uint64_t)8, a.n - i0);
+    uint64_t l0[8], l1[8];
+    load8(reinterpret_cast<const uint64_t*>(a.lo0) + i0, l0, cnt);
+    load8(reinterpret_cast<const uint64_t*>(a.lo1) + i0, l1, cnt);
+    const uint64_t h0 = load_hi8(a.hi0, i0, cnt), h1 = load_hi8(a.hi1, i0, cnt);
+    uint32_t zbits = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {  // step 9: reconstruct w_m, look for a zero
+      uint32_t W0[8], W1[8];
+      unpack_W(l0[e], (uint32_t)(h0 >> (8 * e)) & 0xFFu, W0);
+      unpack_W(l1[e], (uint32_t)(h1 >> (8 * e)) & 0xFFu, W1);
+      zbits |= zero_test(W0, W1, kp.p, kp.S) << e;
+    }
+    uint64_t o0[8], o1[8];
+    if (!RELU) {  // step 10: [D']_0 from seed02, [D']_1 = D' - [D']_0
+      uint32_t Q[16];
+      chacha<R>(k02, j0 >> 3, L_RESP, Q);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint64_t q = u64_of(Q, e) & kp.ymask;
+        o0[e] = q;
+        o1[e] = (((zbits >> e) & 1u) - q) & kp.ymask;
+      }
+    } else {
+      uint32_t Bk0[16], Bk1[16];
+      chacha<R>(k02, j0 >> 3, L_B02, Bk0);
+      chacha<R>(k12, j0 >> 3, L_B12, Bk1);
+      uint64_t bsum[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        bsum[e] = u64_of(Bk0, e) + u64_of(Bk1, e);
+        o0[e] = (((zbits >> e) & 1u) - bsum[e]) & kp.ymask;  // e = DReLU' - b
+      }
+      if (a.out1) {  // [c]_1 = ([a]_0 + [a]_1)([b]_0 + [b]_1) - [c]_0
+        uint32_t Ak0[16], Ak1[16];
+        chacha<R>(k02, j0 >> 3, L_A02, Ak0);
+        chacha<R>(k12, j0 >> 3, L_A12, Ak1);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o1[e] = (u64_of(Ak0, e) + u64_of(Ak1, e)) * bsum[e];
+        uint32_t Ck[16];
+        chacha<R>(k02, j0 >> 3, L_C02, Ck);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o1[e] = (o1[e] - u64_of(Ck, e)) & kp.ymask;
+      }
+    }
+    if (a.out0) store8(a.out0 + i0, o0, cnt);
+    if (a.out1) store8(a.out1 + i0, o1, cnt);
+  }
+}
+
+struct FinishArgs {
+  const uint64_t* x;
+  const uint8_t* tbits;
+  const uint64_t* resp;  // DReLU: [D']_b (nullable for P0)    ReLU: e
+  const uint64_t* d_own;
+  const uint64_t* d_peer;
+  const uint64_t* c1;
+  uint64_t* y;
+  uint64_t n, base;
+};
+
+template <int R, int PARTY, bool RELU>
+__global__ void __launch_bounds__(TPB, 2) k_finish(FinishArgs a, KP kp, Key ks) {
+  const uint64_t ngroups = (a.n + 7) >> 3;
+  for (uint64_t g = (uint64_t)blockIdx.x * TPB + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB) {
+    const uint64_t i0 = g << 3;
+    const uint64_t j0 = a.base + i0;
+    const uint32_t cnt = (uint32_t)min((uint64_t)8, a.n - i0);
+    const uint32_t tb = a.tbits[g];
+    uint64_t y[8];
+    if (!RELU) {  // Alg 7 step 11
+      uint64_t D[8];
+      if (a.resp) {
+        load8(a.resp + i0, D, cnt);
+      } else {  // P0 derives [D']_0 from seed02 (reading C12)
+        uint32_t Q[16];
+        chacha<R>(ks, j0 >> 3, L_RESP, Q);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) D[e] = u64_of(Q, e);
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint64_t t = (tb >> e) & 1u, d = D[e] & kp.ymask;
+        y[e] = PARTY == 0 ? (t ? (1ull - d) & kp.ymask : d) : (t ? (0ull - d) & kp.ymask : d);
+      }
+    } else {  // Alg 8 steps 4-5
+      uint64_t x[8], ev[8], acc[8];
+      load8(a.x + i0, x, cnt);
+      load8(a.resp + i0, ev, cnt);
+      {
+        uint64_t dp[8];
+        load8(a.d_own + i0, acc, cnt);
+        load8(a.d_peer + i0, dp, cnt);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += dp[e];  // d = [d]_0 + [d]_1 (opened)
+      }
+      uint32_t Ak[16], Bk[16];
+      chacha<R>(ks, j0 >> 3, PARTY == 0 ? L_A02 : L_A12, Ak);
+      chacha<R>(ks, j0 >> 3, PARTY == 0 ? L_B02 : L_B12, Bk);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint64_t d = acc[e];
+        acc[e] = d * u64_of(Bk, e) + ev[e] * u64_of(Ak, e) + (PARTY == 0 ? d * ev[e] : 0ull);
+      }
+      if (PARTY == 0) {
+        uint32_t Ck[16];
+        chacha<R>(ks, j0 >> 3, L_C02, Ck);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += u64_of(Ck, e);
+      } else {
+        uint64_t c1[8];
+        load8(a.c1 + i0, c1, cnt);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += c1[e];
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint64_t t = (tb >> e) & 1u;
+        y[e] = ((t ? x[e] : 0ull) + (t ? 0ull - acc[e] : acc[e])) & kp.ymask;
+      }
+    }
+    store8(a.y + i0, y, cnt);
+  }
+}
+
+template <bool RELU>
+int send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits, uint64_t* dshare, size_t n,
+         uint64_t base, const bc_params* prm, const uint8_t* s01, const uint8_t* str, void* stream) {
+  const int rc = check_params(prm);
+  if (rc) return rc;
+  if ((party != 0 && party != 1) || !x || !lo || !tbits || !s01 || (RELU && (!dshare || !str))) return BC_EINVAL;
+  if (!hi && prm->p > 256) return BC_EINVAL;
+  if (!aligned16(x) || !aligned16(lo) || (hi && !aligned8(hi)) || (RELU && !aligned16(dshare)) || (base & 7))
+    return BC_EALIGN;
+  const size_t nb = n * 8;
+  if (overlap(lo, nb, x, nb) || overlap(hi, n, x, nb) || overlap(tbits, (n + 7) / 8, x, nb) ||
+      (RELU && overlap(dshare, nb, x, nb)))
+    return BC_EALIAS;
+  if (n == 0) return BC_OK;
+  SendArgs a{x, lo, hi, tbits, dshare, (uint64_t)n, base};
+  const KP kp = make_kp(prm);
+  const Key k01 = make_key(s01);
+  const Key ktr = RELU ? make_key(str) : Key{};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t ngroups = (n + 7) / 8;
+  return dispatch_rounds(prm->rounds, [&](auto Rc) {
+    constexpr int R = decltype(Rc)::value;
+    auto go = [&](auto fn) { fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k01, ktr); };
+    if (prm->compact) {
+      if (party == 0) go(k_send<R, true, 0, RELU>);
+      else go(k_send<R, true, 1, RELU>);
+    } else {
+      if (party == 0) go(k_send<R, false, 0, RELU>);
+      else go(k_send<R, false, 1, RELU>);
+    }
+    return check_launch();
+  });
+}
+
+template <bool RELU>
+int helper(const uint8_t* lo0, const uint8_t* hi0, const uint8_t* lo1, const uint8_t* hi1, uint64_t* out0,
+           uint64_t* out1, size_t n, uint64_t base, const bc_params* prm, const uint8_t* s02, const uint8_t* s12,
+           void* stream) {
+  const int rc = check_params(prm);
+  if (rc) return rc;
+  if (!lo0 || !lo1 || !s02 || (RELU && (!s12 || !out0)) || (!RELU && !out1)) return BC_EINVAL;
+  if (prm->p > 256 && (!hi0 || !hi1)) return BC_EINVAL;
+  if (!aligned16(lo0) || !aligned16(lo1) || (hi0 && !aligned8(hi0)) || (hi1 && !aligned8(hi1)) ||
+      (out0 && !aligned16(out0)) || (out1 && !aligned16(out1)) || (base & 7))
+    return BC_EALIGN;
+  const size_t nb = n * 8;
+  if (overlap(out0, nb, lo0, nb) || overlap(out0, nb, lo1, nb) || overlap(out1, nb, lo0, nb) ||
+      overlap(out1, nb, lo1, nb) || overlap(out0, nb, out1, nb) || overlap(out0, nb, hi0, n) ||
+      overlap(out0, nb, hi1, n) || overlap(out1, nb, hi0, n) || overlap(out1, nb, hi1, n))
+    return BC_EALIAS;
+  if (n == 0) return BC_OK;
+  HelperArgs a{lo0, hi0, lo1, hi1, out0, out1, (uint64_t)n, base};
+  const KP kp = make_kp(prm);
+  const Key k02 = make_key(s02);
+  const Key k12 = RELU ? make_key(s12) : Key{};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t ngroups = (n + 7) / 8;
+  return dispatch_rounds(prm->rounds, [&](auto Rc) {
+    constexpr int R = decltype(Rc)::value;
+    auto fn = k_helper<R, RELU>;
+    fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k02, k12);
+    return check_launch();
+  });
+}
+
+template <bool RELU>
+int finish(int party, const uint64_t* x, const uint8_t* tbits, const uint64_t* resp, const uint64_t* d_own,
+           const uint64_t* d_peer, const uint64_t* c1, uint64_t* y, size_t n, uint64_t base, const bc_params* prm,
+           const uint8_t* seed, void* stream) {
+  const int rc = check_params(prm);
+  if (rc) return rc;
+  if ((party != 0 && party != 1) || !tbits || !y) return BC_EINVAL;
+  if (!RELU && !resp && (party != 0 || !seed)) return BC_EINVAL;
+  if (RELU && (!x || !resp || !d_own || !d_peer || !seed || (party == 1 && !c1))) return BC_EINVAL;
+  if (!aligned16(y) || (resp && !aligned16(resp)) || (x && !aligned16(x)) || (d_own && !aligned16(d_own)) ||
+      (d_peer && !aligned16(d_peer)) || (c1 && !aligned16(c1)) || (base & 7))
+    return BC_EALIGN;
+  const size_t nb = n * 8;
+  if (overlap(y, nb, resp, nb) || overlap(y, nb, x, nb) || overlap(y, nb, d_own, nb) || overlap(y, nb, d_peer, nb) ||
+      overlap(y, nb, c1, nb) || overlap(y, nb, tbits, (n + 7) / 8))
+    return BC_EALIAS;
+  if (n == 0) return BC_OK;
+  FinishArgs a{x, tbits, resp, d_own, d_peer, party == 1 ? c1 : nullptr, y, (uint64_t)n, base};
+  const KP kp = make_kp(prm);
+  const Key ks = seed ? make_key(seed) : Key{};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t ngroups = (n + 7) / 8;
+  return dispatch_rounds(prm->rounds, [&](auto Rc) {
+    constexpr int R = decltype(Rc)::value;
+    auto go = [&](auto fn) { fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, ks); };
+    if (party == 0) go(k_finish<R, 0, RELU>);
+    else go(k_finish<R, 1, RELU>);
+    return check_launch();
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+int bc_drelu_send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits, size_t n,
+                  uint64_t elem_base, const bc_params* prm, const uint8_t seed01[32], void* stream) {
+  return send<false>(party, x, lo, hi, tbits, nullptr, n, elem_base, prm, seed01, nullptr, stream);
+}
+
+int bc_drelu_helper(const uint8_t* lo0, const uint8_t* hi0, const uint8_t* lo1, const uint8_t* hi1, uint64_t* resp0,
+                    uint64_t* resp1, size_t n, uint64_t elem_base, const bc_params* prm, const uint8_t seed02[32],
+                    void* stream) {
+  return helper<false>(lo0, hi0, lo1, hi1, resp0, resp1, n, elem_base, prm, seed02, nullptr, stream);
+}
+
+int bc_drelu_finish(int party, const uint8_t* tbits, const uint64_t* resp, uint64_t* y, size_t n, uint64_t elem_base,
+                    const bc_params* prm, const uint8_t seed02[32], void* stream) {
+  return finish<false>(party, nullptr, tbits, resp, nullptr, nullptr, nullptr, y, n, elem_base, prm, seed02, stream);
+}
+
+int bc_relu_send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits, uint64_t* dshare, size_t n,
+                 uint64_t elem_base, const bc_params* prm, const uint8_t seed01[32], const uint8_t seed_tr[32],
+                 void* stream) {
+  return send<true>(party, x, lo, hi, tbits, dshare, n, elem_base, prm, seed01, seed_tr, stream);
+}
+
+int bc_relu_helper(const uint8_t* lo0, const uint8_t* hi0, const uint8_t* lo1, const uint8_t* hi1, uint64_t* e,
+                   uint64_t* c1, size_t n, uint64_t elem_base, const bc_params* prm, const uint8_t seed02[32],
+                   const uint8_t seed12[32], void* stream) {
+  return helper<true>(lo0, hi0, lo1, hi1, e, c1, n, elem_base, prm, seed02, seed12, stream);
+}
+
+int bc_relu_finish(int party, const uint64_t* x, const uint8_t* tbits, const uint64_t* d_own, const uint64_t* d_peer,
+                   const uint64_t* e, const uint64_t* c1, uint64_t* y, size_t n, uint64_t elem_base,
+                   const bc_params* prm, const uint8_t seed_tr[32], void* stream) {
+  return finish<true>(party, x, tbits, e, d_own, d_peer, c1, y, n, elem_base, prm, seed_tr, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,286 @@
+"""GPU parity: the CUDA path through the C ABI against the oracle, element by
+element, bit-exact (all integer share arithmetic)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import synth  # noqa: E402
+from oracle import bicoptor as B  # noqa: E402
+from oracle import ring  # noqa: E402
+from plain import band_sign, relu_plain  # noqa: E402
+
+SEEDS = synth.seeds(0)
+
+
+@pytest.fixture(scope="module")
+def api():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2309_04909_b200 import api as a
+    a.lib()
+    return a
+
+
+DEV = "cuda:0"
+
+
+def dev(a: np.ndarray):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).to(DEV)
+
+
+def host(t) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint64)
+
+
+def both(prm_kw):
+    return B.Params(**prm_kw), prm_kw
+
+
+PARAMS = [
+    dict(ell=64, lx=7, f=24, mode="guard", rounds=20),    # the paper's 5+2 key bits of 5+26
+    dict(ell=64, lx=7, f=26, mode="guard", rounds=12),    # 7+0 key bits
+    dict(ell=64, lx=7, f=24, mode="guard", rounds=8),
+    dict(ell=16, lx=7, f=0, mode="guard", rounds=20),     # config 1
+    dict(ell=16, lx=7, f=0, mode="literal", rounds=20),   # paper-literal Z_{2^7}, p = 131 (wide tape)
+    dict(ell=32, lx=5, f=3, mode="guard", rounds=20),     # p = 67, 6 slots (wide tape)
+    dict(ell=12, lx=3, f=1, mode="literal", rounds=8),    # p = 11, 4 slots
+]
+SIZES = [1, 7, 8, 9, 1000, 4099]
+
+
+def _ids(p):
+    return f"l{p['ell']}x{p['lx']}f{p['f']}{p['mode'][0]}R{p['rounds']}"
+
+
+# ---- elementwise primitives --------------------------------------------------------
+
+@pytest.mark.parametrize("ell,k1,k2", [(64, 24, 0), (64, 24, 32), (64, 0, 63), (16, 4, 1), (8, 4, 1), (33, 7, 9)])
+def test_trc_parity(api, ell, k1, k2):
+    rng = np.random.default_rng(ell * 100 + k1)
+    x = rng.integers(0, 2**63, size=4099, dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, 4099, dtype=np.uint64)
+    x &= np.uint64(ring.mask(ell))
+    for party in (0, 1):
+        got = host(api.trc(party, dev(x), ell, k1, k2))
+        assert np.array_equal(got, ring.trc_det_mid(party, x, k1, k2, ell))
+
+
+@pytest.mark.parametrize("ell,k", [(64, 24), (8, 4), (32, 31), (64, 0)])
+def test_trc_prob_parity(api, ell, k):
+    rng = np.random.default_rng(k)
+    x = rng.integers(0, 2**64 - 1, size=3001, dtype=np.uint64, endpoint=True) & np.uint64(ring.mask(ell))
+    x[:5] = 0
+    for party in (0, 1):
+        assert np.array_equal(host(api.trc_prob(party, dev(x), ell, k)), ring.trc_secureml(party, x, k, ell))
+
+
+@pytest.mark.parametrize("lp", [1, 7, 8, 16, 31])
+def test_modswitch_parity(api, lp):
+    p = ring.prime_above(lp)
+    rng = np.random.default_rng(lp)
+    x = rng.integers(0, 1 << lp, size=2049, dtype=np.uint64)
+    x[:3] = 0
+    for party in (0, 1):
+        got = api.modswitch(party, dev(x), lp, p).cpu().numpy().view(np.uint32).astype(np.uint64)
+        assert np.array_equal(got, ring.modswitch(party, x, lp, p))
+
+
+@pytest.mark.parametrize("kw", PARAMS, ids=_ids)
+def test_ladder_modswitch_parity(api, kw):
+    oprm = B.Params(**kw)
+    x, x0, x1 = synth.shares(4099, kw["ell"], kw["lx"], kw["f"], "D1")
+    for party, xs in ((0, x0), (1, x1)):
+        got = api.ladder_modswitch(party, dev(xs), api.Params(**kw)).cpu().numpy()
+        assert np.array_equal(got, B.ladder_modswitch_bytes(oprm, party, xs))
+
+
+# ---- fused three-party DReLU / ReLU ------------------------------------------------
+
+@pytest.mark.parametrize("kw", PARAMS, ids=_ids)
+@pytest.mark.parametrize("fn", ["drelu", "relu"])
+def test_fused_parity_with_transcript(api, kw, fn):
+    oprm = B.Params(**kw)
+    prm = api.Params(**kw)
+    for n in SIZES:
+        for base in (0, 8, 1 << 40):
+            x, x0, x1 = synth.shares(n, kw["ell"], kw["lx"], kw["f"], "D1", run=n)
+            j = np.arange(n, dtype=np.uint64) + np.uint64(base)
+            ref = getattr(B, fn)(oprm, x0, x1, j, SEEDS)
+            tr = api.transcript_buffers(n, DEV)
+            y0, y1 = getattr(api, fn)(dev(x0), dev(x1), prm, SEEDS, elem_base=base, transcript=tr)
+            assert np.array_equal(host(y0), ref["y0"]), (n, base)
+            assert np.array_equal(host(y1), ref["y1"]), (n, base)
+            lo0, hi0 = B.encode_msg(ref["W0"])
+            lo1, hi1 = B.encode_msg(ref["W1"])
+            assert np.array_equal(tr["w0_lo"].cpu().numpy(), lo0) and np.array_equal(tr["w0_hi"].cpu().numpy(), hi0)
+            assert np.array_equal(tr["w1_lo"].cpu().numpy(), lo1) and np.array_equal(tr["w1_hi"].cpu().numpy(), hi1)
+
+
+def test_fused_rejection_fallback(api):
+    """Elements whose compact tape rejects (u16 reshare 65535 or perm index
+    >= 53261*8!) take the fallback stream; they must match the oracle too."""
+    from oracle.chacha import element_u32
+    kw = PARAMS[0]
+    oprm = B.Params(**kw)
+    jj = np.arange(400000, dtype=np.uint64)
+    T = element_u32(SEEDS.s01, B.L_TAPE, oprm.rounds, jj, 8)
+    u = np.ascontiguousarray(T[:, 3:7]).view("<u2").reshape(-1, 8)
+    rej = np.nonzero((u == 65535).any(axis=1) | ((T[:, 0] & 0x7FFFFFFF) >= B.PERM_LIMIT_COMPACT))[0]
+    assert len(rej) >= 10
+    for r in rej[:10]:
+        base = int(r) - int(r) % 8
+        x, x0, x1 = synth.shares(64, 64, 7, 24, "D2", run=int(r))
+        j = np.arange(64, dtype=np.uint64) + np.uint64(base)
+        for fn in ("drelu", "relu"):
+            ref = getattr(B, fn)(oprm, x0, x1, j, SEEDS)
+            y0, y1 = getattr(api, fn)(dev(x0), dev(x1), api.Params(**kw), SEEDS, elem_base=base)
+            assert np.array_equal(host(y0), ref["y0"]) and np.array_equal(host(y1), ref["y1"])
+
+
+def test_sharding_is_bit_identical(api):
+    """elem_base addresses every PRG draw by global index: four shards equal one call."""
+    kw = PARAMS[0]
+    n = 40000
+    x, x0, x1 = synth.shares(n, 64, 7, 24, "D2")
+    prm = api.Params(**kw)
+    for fn in (api.drelu, api.relu):
+        y0, y1 = fn(dev(x0), dev(x1), prm, SEEDS)
+        cuts = [0, 8, 16000, 30000, n]
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            s0, s1 = fn(dev(x0[a:b]), dev(x1[a:b]), prm, SEEDS, elem_base=a)
+            assert torch.equal(s0, y0[a:b]) and torch.equal(s1, y1[a:b])
+
+
+def test_config1_exhaustive_ell16(api):
+    """Config 1: DReLU at ell=16, all key bits (lx=7, f=0), every x in Z_{2^16}
+    once (masks from the synthetic generator): bit-exact against the oracle for
+    all 65536 inputs; reconstructed sign exact on the band."""
+    kw = dict(ell=16, lx=7, f=0, mode="guard", rounds=20)
+    oprm = B.Params(**kw)
+    x = np.arange(1 << 16, dtype=np.uint64)
+    x0, x1 = synth.share(x, 16)
+    j = np.arange(x.size, dtype=np.uint64)
+    ref = B.drelu(oprm, x0, x1, j, SEEDS)
+    y0, y1 = api.drelu(dev(x0), dev(x1), api.Params(**kw), SEEDS)
+    assert np.array_equal(host(y0), ref["y0"]) and np.array_equal(host(y1), ref["y1"])
+    y = (host(y0) + host(y1)) & np.uint64(0xFFFF)
+    s, valid = band_sign(x, 16, 7, 0)
+    assert valid.sum() == 254 and np.array_equal(y[valid], s[valid])
+
+
+def test_config1_all_masks_sign(api):
+    """Config 1, exhaustive over masks: the 254 in-band nonzero x times all 2^16
+    masks R (16.6M instances) on the GPU; every reconstruction equals the
+    plaintext sign (guard mode), ReLU equals max(x,0); oracle parity on a sample."""
+    kw = dict(ell=16, lx=7, f=0, mode="guard", rounds=20)
+    xi = np.arange(1, 128, dtype=np.uint64)
+    xs = np.concatenate([xi, (np.uint64(1 << 16) - xi)])
+    R = np.arange(1 << 16, dtype=np.uint64)
+    x = np.repeat(xs, R.size)
+    Rr = np.tile(R, xs.size)
+    x0 = (x + Rr) & np.uint64(0xFFFF)
+    x1 = (np.uint64(1 << 16) - Rr) & np.uint64(0xFFFF)
+    prm = api.Params(**kw)
+    t0, t1 = dev(x0), dev(x1)
+    y0, y1 = api.drelu(t0, t1, prm, SEEDS)
+    y = host(y0 + y1) & np.uint64(0xFFFF)
+    s, valid = band_sign(x, 16, 7, 0)
+    assert valid.all() and np.array_equal(y, s)
+    r0, r1 = api.relu(t0, t1, prm, SEEDS)
+    assert np.array_equal(host(r0 + r1) & np.uint64(0xFFFF), relu_plain(x, 16, 7, 0))
+    idx = np.sort(np.random.default_rng(3).choice(x.size, 4096, replace=False)).astype(np.uint64)
+    ref = B.drelu(B.Params(**kw), x0[idx], x1[idx], idx, SEEDS)
+    assert np.array_equal(host(y0)[idx], ref["y0"]) and np.array_equal(host(y1)[idx], ref["y1"])
+
+
+@pytest.mark.parametrize("fn", ["drelu", "relu"])
+def test_config3_full_size_sampled(api, fn):
+    """Config 3 (2^24 elements, ell=64, 5+2 key bits) in the launch the bench
+    times: oracle parity on a seeded 2^14-element sample; reconstructed
+    sign / ReLU on every element whose sign the key bits determine."""
+    n = 1 << 24
+    kw = PARAMS[0]
+    x, x0, x1 = synth.shares(n, 64, 7, 24, "D2")
+    y0, y1 = getattr(api, fn)(dev(x0), dev(x1), api.Params(**kw), SEEDS)
+    g0, g1 = host(y0), host(y1)
+    idx = np.sort(np.random.default_rng(11).choice(n, 1 << 14, replace=False)).astype(np.uint64)
+    ref = getattr(B, fn)(B.Params(**kw), x0[idx], x1[idx], idx, SEEDS)
+    assert np.array_equal(g0[idx], ref["y0"]) and np.array_equal(g1[idx], ref["y1"])
+    with np.errstate(over="ignore"):
+        y = g0 + g1
+    s, valid = band_sign(x, 64, 7, 24)
+    if fn == "drelu":
+        assert np.array_equal(y[valid], s[valid])
+    else:
+        assert np.array_equal(y[valid], relu_plain(x, 64, 7, 24)[valid])
+
+
+def test_config2_ladder_full_size_sampled(api):
+    """Config 2 (trc + modswitch alone, ell=64, 2^28 elements): sampled parity."""
+    n = 1 << 28
+    kw = PARAMS[0]
+    rng = np.random.default_rng(5)
+    x = rng.integers(0, 2**64 - 1, size=n, dtype=np.uint64, endpoint=True)
+    t = dev(x)
+    del x
+    idx = np.sort(rng.choice(n, 1 << 14, replace=False))
+    xs = t[torch.from_numpy(idx).to(DEV)].cpu().numpy().view(np.uint64)
+    for party in (0, 1):
+        out = api.ladder_modswitch(party, t, api.Params(**kw))
+        got = out[torch.from_numpy(idx).to(DEV)].cpu().numpy()
+        assert np.array_equal(got, B.ladder_modswitch_bytes(B.Params(**kw), party, xs))
+        del out
+
+
+# ---- party-separated phases on one device ------------------------------------------
+
+@pytest.mark.parametrize("kw", [PARAMS[0], PARAMS[4], PARAMS[5]], ids=_ids)
+def test_party_phases_match_oracle_and_fused(api, kw):
+    oprm, prm = B.Params(**kw), api.Params(**kw)
+    n, base = 4099, 1 << 20
+    x, x0, x1 = synth.shares(n, kw["ell"], kw["lx"], kw["f"], "D1")
+    j = np.arange(n, dtype=np.uint64) + np.uint64(base)
+    t0, t1 = dev(x0), dev(x1)
+    # DReLU
+    lo0, hi0, tb0 = api.drelu_send(0, t0, prm, SEEDS.s01, base)
+    lo1, hi1, tb1 = api.drelu_send(1, t1, prm, SEEDS.s01, base)
+    m0 = B.drelu_send(oprm, 0, x0, j, SEEDS.s01)
+    el0, eh0 = B.encode_msg(m0["W"])
+    assert np.array_equal(lo0.cpu().numpy(), el0) and np.array_equal(hi0.cpu().numpy(), eh0)
+    r0, r1 = api.drelu_helper(lo0, hi0, lo1, hi1, prm, SEEDS.s02, base, paper_literal=True)
+    ya = api.drelu_finish(0, tb0, None, prm, n, SEEDS.s02, base)
+    yb = api.drelu_finish(0, tb0, r0, prm, n, None, base)
+    y1 = api.drelu_finish(1, tb1, r1, prm, n, None, base)
+    f0, f1 = api.drelu(t0, t1, prm, SEEDS, elem_base=base)
+    assert torch.equal(ya, f0) and torch.equal(yb, f0) and torch.equal(y1, f1)
+    # ReLU
+    L0, H0, T0, d0 = api.relu_send(0, t0, prm, SEEDS.s01, SEEDS.s02, base)
+    L1, H1, T1, d1 = api.relu_send(1, t1, prm, SEEDS.s01, SEEDS.s12, base)
+    e, c1 = api.relu_helper(L0, H0, L1, H1, prm, SEEDS.s02, SEEDS.s12, base)
+    ref = B.relu(oprm, x0, x1, j, SEEDS)
+    assert np.array_equal(host(d0), ref["d0"]) and np.array_equal(host(e), ref["e"]) and np.array_equal(host(c1), ref["c1"])
+    z0 = api.relu_finish(0, t0, T0, d0, d1, e, None, prm, SEEDS.s02, base)
+    z1 = api.relu_finish(1, t1, T1, d1, d0, e, c1, prm, SEEDS.s12, base)
+    g0, g1 = api.relu(t0, t1, prm, SEEDS, elem_base=base)
+    assert torch.equal(z0, g0) and torch.equal(z1, g1)
+    assert np.array_equal(host(z0), ref["y0"]) and np.array_equal(host(z1), ref["y1"])
+
+
+# ---- boundary errors ---------------------------------------------------------------
+
+def test_abi_errors(api):
+    prm = api.Params()
+    x = torch.zeros(33, dtype=torch.int64, device=DEV)
+    with pytest.raises(api.BicoptorError, match="aligned|multiple"):
+        api.drelu(x[1:17], x[1:17].clone(), prm, SEEDS)          # misaligned x0
+    with pytest.raises(api.BicoptorError, match="multiple"):
+        api.drelu(x[:16], x[16:32], prm, SEEDS, elem_base=3)     # elem_base % 8
+    with pytest.raises(api.BicoptorError, match="overlaps"):
+        api.drelu(x[:16], x[16:32], prm, SEEDS, y0=x[:16])      # aliasing
+    with pytest.raises(api.BicoptorError, match="window"):
+        api.Params(ell=16, lx=7, f=2).c()                        # f + lx + w > ell
+    with pytest.raises(api.BicoptorError, match="CUDA tensor"):
+        api.drelu(torch.zeros(8, dtype=torch.int64), torch.zeros(8, dtype=torch.int64), prm, SEEDS)
+    y0, y1 = api.drelu(x[:0], x[16:16], prm, SEEDS)                # n = 0 is a no-op
+    assert y0.numel() == 0
