@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""Benchmark of the Bicoptor 2.0 DReLU / ReLU hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl cuda|reference]
+    torchrun --nproc-per-node N ... bench.py --gpus N ...     (N > 1)
+
+Workload (BASELINE.json config 3): DReLU, ell = 64, the paper's key-bit window
+(lx = 7, f = 24: 5+2 of the 5+26 fixed point), guard mode, ChaCha20
+PRG, 2^24 elements per GPU, D2 activation-like inputs.  A step is one fused
+three-party pass (Alg 7: both computing parties, the helper's zero test and
+reshare, the unblinding) over the batch, inputs resident in HBM.  The same
+run times ReLU (Alg 8) on the same batch and the trc+modswitch primitive of
+config 2 (HBM roofline check); they are reported as sub-objects.
+
+Multi-GPU: elements are independent.  Each rank owns 2^24 elements
+at global offset rank * 2^24 (weak scaling); every PRG draw is addressed by
+global index, so there is no data-path collective.  Time = max over ranks of
+the CUDA-event time between two barriers.
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+N_PER_GPU = 1 << 24
+ELL, LX, F, MODE, ROUNDS = 64, 7, 24, "guard", 20
+METRIC = "DReLU & ReLU elements/s at ell=64 on 1/2/4/8 B200; % of HBM roofline"
+CHACHA_OPS_PER_BLOCK = {20: 976, 12: 592, 8: 400}   # R*4*12 word ops + 16 feed-forward adds
+BLOCKS_PER_ELEM = {"drelu": 0.625, "relu": 1.125}
+BYTES_PER_ELEM = {"drelu": 32, "relu": 32, "ladder": 16}  # algorithmic HBM bytes per element
+SM_COUNT_B200 = 148
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--n", type=int, default=N_PER_GPU)
+    ap.add_argument("--rounds", type=int, default=ROUNDS)
+    ap.add_argument("--no-extras", action="store_true", help="skip ReLU / ladder / variants / e2e / cpu legs")
+    ap.add_argument("--only", choices=["drelu", "relu", "ladder"], help="profiling aid: launch one op steps+warmup times, print nothing")
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d.get("hbm_gbs", 6650.0), "sm_max_mhz": d.get("sm_max_mhz", 1965.0), "src": "measured"}
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "src": "fallback"}
+
+
+def load_traffic():
+    """Per-launch DRAM bytes from the committed ncu --set full capture (or None)."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return {}
+    return {}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle leg (cpu_baseline / --impl reference): the oracle as it stands,
+# on a bounded sample, in a process pool over the host cores.
+# ---------------------------------------------------------------------------
+def _oracle_chunk(args):
+    """One worker: generate its slice of the workload, then time only the oracle call."""
+    lo, hi, fn, rounds = args
+    import synth
+    from oracle import bicoptor as B
+    prm = B.Params(ell=ELL, lx=LX, f=F, mode=MODE, rounds=rounds)
+    x = synth.plaintext(hi, ELL, LX, F, "D2")
+    x0, x1 = synth.share(x, ELL)
+    j = np.arange(lo, hi, dtype=np.uint64)
+    t0 = time.perf_counter()
+    getattr(B, fn)(prm, x0[lo:hi], x1[lo:hi], j, synth.seeds(0))
+    return hi - lo, time.perf_counter() - t0
+
+
+def oracle_rate(fn: str, rounds: int, budget_s: float = 12.0):
+    """Elements/s of the numpy oracle on the host cores for the bench workload:
+    one process per core, each timing the oracle on its own slice; rate = all
+    elements / slowest worker."""
+    import concurrent.futures as cf
+    cores = min(os.cpu_count() or 1, 16)
+    cnt, dt = _oracle_chunk((0, 4096, fn, rounds))   # calibrate on one core
+    per = max(4096, int(cnt / dt * budget_s))
+    per = 1 << int(math.log2(per))
+    tasks = [(k * per, (k + 1) * per, fn, rounds) for k in range(cores)]
+    with cf.ProcessPoolExecutor(max_workers=cores) as ex:
+        res = list(ex.map(_oracle_chunk, tasks))
+    done = sum(r[0] for r in res)
+    dt = max(r[1] for r in res)
+    return done / dt, cores, (f"{cores} processes x 2^{int(math.log2(per))} elements of the bench workload "
+                              f"({fn}, D2), oracle.bicoptor.{fn} (numpy)")
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    times = []
+    rate = None
+    for s in range(a.warmup + a.steps):
+        t0 = time.perf_counter()
+        rate, cores, sample = oracle_rate("drelu", a.rounds, budget_s=4.0 if s >= a.warmup else 1.0)
+        if s >= a.warmup:
+            times.append(time.perf_counter() - t0)
+    value = rate
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": workload_config(a),
+        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def workload_config(a):
+    return {"workload": f"config3: DReLU ell={ELL} lx={LX} f={F} {MODE} ChaCha{a.rounds}, 2^{int(math.log2(a.n))} elements/GPU, D2",
+            "n_per_gpu": a.n, "ell": ELL, "lx": LX, "f": F, "mode": MODE, "rounds": a.rounds, "dist": "D2",
+            "parallelism": f"element-sharded x{a.gpus} (3 parties simulated per GPU)",
+            "l2": "no flush: inputs+outputs = 32 B/elem = 512 MiB per GPU > 126 MB L2"}
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+class Clocks:
+    """nvidia-smi sampler; only samples stamped inside [mark_start, mark_end] count."""
+    Q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.t0 = self.t1 = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.1)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        import datetime
+        rows, all_rows = [], []
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                row = (ts, float(parts[1]), float(parts[2]), parts[3:7])
+            except ValueError:
+                continue
+            all_rows.append(row)
+            if self.t0 is not None and self.t0 <= ts <= (self.t1 or ts):
+                rows.append(row)
+        if not rows:
+            rows = all_rows[-3:]  # region shorter than the sampling period: nearest samples
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k, v in enumerate(r[3]) if v.lower().startswith("active")})
+        return {"sm_mhz": float(np.median([r[1] for r in rows])), "sm_max_mhz": max(r[2] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# CUDA leg
+# ---------------------------------------------------------------------------
+def run_cuda(a):
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2309_04909_b200 import api
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    api.lib()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    n = a.n
+    base = rank * n
+    seeds = synth.seeds(0)
+    prm = api.Params(ell=ELL, lx=LX, f=F, mode=MODE, rounds=a.rounds)
+    x = synth.plaintext(n, ELL, LX, F, "D2", run=rank)
+    x0h, x1h = synth.share(x, ELL, run=rank)
+    x0 = torch.from_numpy(x0h.view(np.int64)).to(dev)
+    x1 = torch.from_numpy(x1h.view(np.int64)).to(dev)
+    y0 = torch.empty_like(x0)
+    y1 = torch.empty_like(x1)
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(fn, steps, warmup, launches_per_step=1, clocks=None):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize(dev)
+        barrier()
+        torch.cuda.synchronize(dev)
+        if clocks:
+            clocks.start()
+            for _ in range(warmup):  # keep the GPU busy while the sampler comes up
+                fn()
+            time.sleep(0.2)
+            torch.cuda.synchronize(dev)
+            clocks.mark_start()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        ev[0].record(stream)
+        for s in range(steps):
+            fn()
+            ev[s + 1].record(stream)
+        torch.cuda.synchronize(dev)
+        if clocks:
+            clocks.mark_end()
+        barrier()
+        torch.cuda.synchronize(dev)
+        ck = clocks.stop() if clocks else None
+        per = [ev[s].elapsed_time(ev[s + 1]) for s in range(steps)]
+        total_ms = ev[0].elapsed_time(ev[steps])
+        return max_over_ranks(total_ms), per, ck
+
+    if a.only:  # profiling aid (ncu): just the launches, no timing output
+        v_lad = torch.empty((n, 8), dtype=torch.uint8, device=dev)
+        op = {"drelu": lambda: api.drelu(x0, x1, prm, seeds, base, y0, y1, stream=stream),
+              "relu": lambda: api.relu(x0, x1, prm, seeds, base, y0, y1, stream=stream),
+              "ladder": lambda: api.ladder_modswitch(0, x0, prm, out=v_lad, stream=stream)}[a.only]
+        for _ in range(a.warmup + a.steps):
+            op()
+        torch.cuda.synchronize(dev)
+        return
+
+    # ---- headline: fused DReLU ------------------------------------------------
+    ck = Clocks(local)
+    t_ms, per, clocks = timed(lambda: api.drelu(x0, x1, prm, seeds, base, y0, y1, stream=stream),
+                              a.steps, max(a.warmup, 3), clocks=ck)
+    ms = t_ms / a.steps
+    value = world * n / (ms * 1e-3)
+    peaks = load_peaks()
+    traffic = load_traffic()
+    clk_mhz = peaks["sm_max_mhz"]
+    alu_peak = SM_COUNT_B200 * 4 * 32 * clk_mhz * 1e6 / 1e12  # Tops/s: 1 warp-instr/clk/SMSP
+
+    def roofline(kind, elems_per_s, launch_ms):
+        bytes_ = BYTES_PER_ELEM[kind]
+        hbm_gbs = elems_per_s * bytes_ / 1e9 / max(world, 1)
+        out = {"hbm": {"achieved": hbm_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                       "frac": hbm_gbs / peaks["hbm_gbs"], "bytes_per_elem": bytes_}}
+        if kind in BLOCKS_PER_ELEM:
+            ops = BLOCKS_PER_ELEM[kind] * CHACHA_OPS_PER_BLOCK[a.rounds]
+            ach = elems_per_s / max(world, 1) * ops / 1e12
+            out.update({"bound": "alu", "achieved": ach, "peak": alu_peak, "unit": "Tops/s", "frac": ach / alu_peak,
+                        "ops_per_elem": ops, "peak_note": f"148 SM x 4 SMSP x 32 lanes x 1 instr/clk x {clk_mhz:.0f} MHz ({peaks['src']} sm_max)"})
+        else:
+            out.update({"bound": "hbm", "achieved": hbm_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                        "frac": hbm_gbs / peaks["hbm_gbs"]})
+        tr = traffic.get(kind)
+        out["traffic"] = tr
+        out["launch_ms"] = launch_ms
+        return out
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world, "steps": a.steps,
+        "warmup": max(a.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded; shares of D2 activations)",
+        "config": workload_config(a),
+        "roofline": roofline("drelu", value, ms),
+        "gpu_launches": a.steps,
+        "clocks": clocks,
+    }
+
+    if not a.no_extras:
+        # ---- ReLU (Alg 8) on the same batch ------------------------------------
+        t_ms_r, _, _ = timed(lambda: api.relu(x0, x1, prm, seeds, base, y0, y1, stream=stream),
+                             max(a.steps // 2, 5), 3)
+        ms_r = t_ms_r / max(a.steps // 2, 5)
+        v_r = world * n / (ms_r * 1e-3)
+        line["relu"] = {"value": v_r, "unit": "elements/s", "ms_per_step": ms_r, "roofline": roofline("relu", v_r, ms_r)}
+        # ---- ChaCha round-count variants of DReLU --------------------------------
+        var = {}
+        for R in (12, 8):
+            if R == a.rounds:
+                continue
+            pr = api.Params(ell=ELL, lx=LX, f=F, mode=MODE, rounds=R)
+            tv, _, _ = timed(lambda: api.drelu(x0, x1, pr, seeds, base, y0, y1, stream=stream), 50, 3)
+            tr_, _, _ = timed(lambda: api.relu(x0, x1, pr, seeds, base, y0, y1, stream=stream), 50, 3)
+            var[f"chacha{R}"] = {"drelu": world * n / (tv / 50 * 1e-3), "relu": world * n / (tr_ / 50 * 1e-3)}
+        line["variants"] = var
+        # ---- config 2: ladder + modswitch (Alg 7 steps 3-5), HBM-bound ---------
+        v_lad = torch.empty((n, 8), dtype=torch.uint8, device=dev)
+        tl, _, _ = timed(lambda: api.ladder_modswitch(0, x0, prm, out=v_lad, stream=stream), 100, 5)
+        ms_l = tl / 100
+        v_l = world * n / (ms_l * 1e-3)
+        line["trc_modswitch"] = {"value": v_l, "unit": "elements/s", "ms_per_step": ms_l,
+                                 "roofline": roofline("ladder", v_l, ms_l),
+                                 "note": "one party, 8 B in + 8 B out per element (config 2 primitive)"}
+        del v_lad
+        # ---- e2e through the public API with pinned HOST buffers ----------------
+        line["e2e"] = e2e(api, prm, seeds, x0h, x1h, base, dev, world, max_over_ranks, barrier, a)
+    if rank == 0 and not a.no_extras:
+        rate, cores, sample = oracle_rate("drelu", a.rounds)
+        line["cpu_baseline"] = {"value": rate, "unit": "elements/s", "cores": cores, "kind": "oracle", "sample": sample}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e(api, prm, seeds, x0h, x1h, base, dev, world, max_over_ranks, barrier, a):
+    """Same metric through api.drelu_host: pinned host shares in, pinned host
+    shares out, H2D / kernel / D2H pipelined in chunks inside the timed region."""
+    import torch
+    from paper_2309_04909_b200 import host as H
+    n = x0h.size
+    hx0 = torch.from_numpy(x0h.view(np.int64)).pin_memory()
+    hx1 = torch.from_numpy(x1h.view(np.int64)).pin_memory()
+    hy0 = torch.empty(n, dtype=torch.int64).pin_memory()
+    hy1 = torch.empty(n, dtype=torch.int64).pin_memory()
+    ex = H.HostPipeline(n, dev, chunks=8)
+    steps = max(5, a.steps // 20)
+    for _ in range(2):
+        ex.drelu(hx0, hx1, hy0, hy1, prm, seeds, base)
+    torch.cuda.synchronize(dev)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        ex.drelu(hx0, hx1, hy0, hy1, prm, seeds, base)
+    torch.cuda.synchronize(dev)
+    dt = max_over_ranks(time.perf_counter() - t0)
+    return {"value": world * n * steps / dt, "unit": "elements/s", "h2d_bytes_per_step": 16 * n,
+            "d2h_bytes_per_step": 16 * n, "chunks": 8,
+            "note": "api host pipeline: pinned x0,x1 -> HBM -> fused DReLU -> pinned y0,y1, wall clock, max over ranks"}
+
+
+if __name__ == "__main__":
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_cuda(args)

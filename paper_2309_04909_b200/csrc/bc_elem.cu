@@ -151,11 +151,12 @@ __global__ void __launch_bounds__(TPB) k_ladder(const uint64_t* __restrict__ x, 
 extern "C" {
 
 int bc_trc(int party, const uint64_t* in, uint64_t* out, size_t n, int ell, int k1, int k2, void* stream) {
-  if ((party != 0 && party != 1) || !in || !out || ell < 2 || ell > 64 || k1 < 0 || k2 < 0 || k1 + k2 >= ell)
+  if ((party != 0 && party != 1) || ell < 2 || ell > 64 || k1 < 0 || k2 < 0 || k1 + k2 >= ell)
     return BC_EINVAL;
+  if (n == 0) return BC_OK;  // no-op after parameter validation
+  if (!in || !out) return BC_EINVAL;
   if (!aligned16(in) || !aligned16(out)) return BC_EALIGN;
   if (overlap(in, n * 8, out, n * 8)) return BC_EALIAS;
-  if (n == 0) return BC_OK;
   const int lp = ell - k1 - k2;
   EwArgs a{};
   a.in = in;
@@ -170,10 +171,11 @@ int bc_trc(int party, const uint64_t* in, uint64_t* out, size_t n, int ell, int 
 }
 
 int bc_trc_prob(int party, const uint64_t* in, uint64_t* out, size_t n, int ell, int k, void* stream) {
-  if ((party != 0 && party != 1) || !in || !out || ell < 2 || ell > 64 || k < 0 || k >= ell) return BC_EINVAL;
+  if ((party != 0 && party != 1) || ell < 2 || ell > 64 || k < 0 || k >= ell) return BC_EINVAL;
+  if (n == 0) return BC_OK;  // no-op after parameter validation
+  if (!in || !out) return BC_EINVAL;
   if (!aligned16(in) || !aligned16(out)) return BC_EALIGN;
   if (overlap(in, n * 8, out, n * 8)) return BC_EALIAS;
-  if (n == 0) return BC_OK;
   EwArgs a{};
   a.in = in;
   a.out = out;
@@ -186,11 +188,12 @@ int bc_trc_prob(int party, const uint64_t* in, uint64_t* out, size_t n, int ell,
 }
 
 int bc_modswitch(int party, const uint64_t* in, uint32_t* out, size_t n, int lp, uint32_t p, void* stream) {
-  if ((party != 0 && party != 1) || !in || !out || lp < 1 || lp > 31 || (uint64_t)p <= (1ull << lp))
+  if ((party != 0 && party != 1) || lp < 1 || lp > 31 || (uint64_t)p <= (1ull << lp))
     return BC_EINVAL;
+  if (n == 0) return BC_OK;  // no-op after parameter validation
+  if (!in || !out) return BC_EINVAL;
   if (!aligned16(in) || (reinterpret_cast<uintptr_t>(out) & 3)) return BC_EALIGN;
   if (overlap(in, n * 8, out, n * 4)) return BC_EALIAS;
-  if (n == 0) return BC_OK;
   EwArgs a{};
   a.in = in;
   a.out = out;
@@ -205,10 +208,10 @@ int bc_modswitch(int party, const uint64_t* in, uint32_t* out, size_t n, int lp,
 int bc_ladder_modswitch(int party, const uint64_t* x, uint8_t* v, size_t n, const bc_params* prm, void* stream) {
   const int rc = check_params(prm);
   if (rc) return rc;
-  if ((party != 0 && party != 1) || !x || !v) return BC_EINVAL;
+  if (n == 0) return BC_OK;  // no-op after parameter validation
+  if (party != 0 && party != 1) return BC_EINVAL;
   if (!aligned16(x) || !aligned16(v)) return BC_EALIGN;
   if (overlap(x, n * 8, v, n * 8)) return BC_EALIAS;
-  if (n == 0) return BC_OK;
   const KP kp = make_kp(prm);
   const int compact = prm->compact;
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -146,6 +146,7 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
           const bc_params* prm, const bc_seeds* seeds, const bc_transcript* tr, void* stream) {
   const int rc = check_params(prm);
   if (rc) return rc;
+  if (n == 0) return BC_OK;  // no-op after parameter validation
   if (!x0 || !x1 || !y0 || !y1 || !seeds) return BC_EINVAL;
   if (!aligned16(x0) || !aligned16(x1) || !aligned16(y0) || !aligned16(y1) || (base & 7)) return BC_EALIGN;
   const size_t nb = n * 8;
@@ -161,7 +162,6 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
     a.w1lo = tr->w1_lo;
     a.w1hi = tr->w1_hi;
   }
-  if (n == 0) return BC_OK;
   const KP kp = make_kp(prm);
   const Key k01 = make_key(seeds->s01), k02 = make_key(seeds->s02), k12 = make_key(seeds->s12);
   cudaStream_t st = static_cast<cudaStream_t>(stream);

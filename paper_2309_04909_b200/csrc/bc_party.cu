@@ -208,6 +208,7 @@ int send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits,
          uint64_t base, const bc_params* prm, const uint8_t* s01, const uint8_t* str, void* stream) {
   const int rc = check_params(prm);
   if (rc) return rc;
+  if (n == 0) return BC_OK;  // no-op after parameter validation
   if ((party != 0 && party != 1) || !x || !lo || !tbits || !s01 || (RELU && (!dshare || !str))) return BC_EINVAL;
   if (!hi && prm->p > 256) return BC_EINVAL;
   if (!aligned16(x) || !aligned16(lo) || (hi && !aligned8(hi)) || (RELU && !aligned16(dshare)) || (base & 7))
@@ -216,7 +217,6 @@ int send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits,
   if (overlap(lo, nb, x, nb) || overlap(hi, n, x, nb) || overlap(tbits, (n + 7) / 8, x, nb) ||
       (RELU && overlap(dshare, nb, x, nb)))
     return BC_EALIAS;
-  if (n == 0) return BC_OK;
   SendArgs a{x, lo, hi, tbits, dshare, (uint64_t)n, base};
   const KP kp = make_kp(prm);
   const Key k01 = make_key(s01);
@@ -243,6 +243,7 @@ int helper(const uint8_t* lo0, const uint8_t* hi0, const uint8_t* lo1, const uin
            void* stream) {
   const int rc = check_params(prm);
   if (rc) return rc;
+  if (n == 0) return BC_OK;  // no-op after parameter validation
   if (!lo0 || !lo1 || !s02 || (RELU && (!s12 || !out0)) || (!RELU && !out1)) return BC_EINVAL;
   if (prm->p > 256 && (!hi0 || !hi1)) return BC_EINVAL;
   if (!aligned16(lo0) || !aligned16(lo1) || (hi0 && !aligned8(hi0)) || (hi1 && !aligned8(hi1)) ||
@@ -253,7 +254,6 @@ int helper(const uint8_t* lo0, const uint8_t* hi0, const uint8_t* lo1, const uin
       overlap(out1, nb, lo1, nb) || overlap(out0, nb, out1, nb) || overlap(out0, nb, hi0, n) ||
       overlap(out0, nb, hi1, n) || overlap(out1, nb, hi0, n) || overlap(out1, nb, hi1, n))
     return BC_EALIAS;
-  if (n == 0) return BC_OK;
   HelperArgs a{lo0, hi0, lo1, hi1, out0, out1, (uint64_t)n, base};
   const KP kp = make_kp(prm);
   const Key k02 = make_key(s02);
@@ -274,6 +274,7 @@ int finish(int party, const uint64_t* x, const uint8_t* tbits, const uint64_t* r
            const uint8_t* seed, void* stream) {
   const int rc = check_params(prm);
   if (rc) return rc;
+  if (n == 0) return BC_OK;  // no-op after parameter validation
   if ((party != 0 && party != 1) || !tbits || !y) return BC_EINVAL;
   if (!RELU && !resp && (party != 0 || !seed)) return BC_EINVAL;
   if (RELU && (!x || !resp || !d_own || !d_peer || !seed || (party == 1 && !c1))) return BC_EINVAL;
@@ -284,7 +285,6 @@ int finish(int party, const uint64_t* x, const uint8_t* tbits, const uint64_t* r
   if (overlap(y, nb, resp, nb) || overlap(y, nb, x, nb) || overlap(y, nb, d_own, nb) || overlap(y, nb, d_peer, nb) ||
       overlap(y, nb, c1, nb) || overlap(y, nb, tbits, (n + 7) / 8))
     return BC_EALIAS;
-  if (n == 0) return BC_OK;
   FinishArgs a{x, tbits, resp, d_own, d_peer, party == 1 ? c1 : nullptr, y, (uint64_t)n, base};
   const KP kp = make_kp(prm);
   const Key ks = seed ? make_key(seed) : Key{};
