@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <type_traits>
 
+#include "bc_compact.cuh"
 #include "bc_device.cuh"
 #include "bicoptor.h"
 
@@ -25,24 +26,10 @@ __device__ __forceinline__ uint64_t u64_of(const uint32_t (&B)[16], int e) {
   return (uint64_t)B[2 * e] | ((uint64_t)B[2 * e + 1] << 32);
 }
 
-// seed01 tape block h of the group starting at global index j0 (j0 % 8 == 0).
-template <int R, bool COMPACT>
-__device__ __forceinline__ void tape_block(const Key& k01, uint64_t j0, int h, uint32_t (&B)[16]) {
-  if (COMPACT) chacha<R>(k01, (j0 >> 1) + (uint64_t)h, L_TAPE, B);
-  else chacha<R>(k01, j0 + (uint64_t)h, L_TAPEW, B);
-}
-
-template <int R, bool COMPACT>
-__device__ __forceinline__ void decode(const uint32_t (&B)[16], int s, uint64_t j, const Key& k01, const KP& kp,
-                                       Tape& tp) {
-  if (COMPACT) decode_compact<R>(&B[8 * s], j, k01, tp);
-  else decode_wide<R>(B, j, k01, kp, tp);
-}
-
-template <bool COMPACT, int PARTY>
-__device__ __forceinline__ void party_W(uint64_t x, const KP& kp, const Tape& tp, uint32_t (&W)[8]) {
-  if (COMPACT) party_W_compact<PARTY>(x, kp.f, tp, W);
-  else party_W_wide<PARTY>(x, kp, tp, W);
+// Two consecutive elements (one 16-B vector per party); zero past n.
+__device__ __forceinline__ ulonglong2 load2(const uint64_t* __restrict__ p, uint64_t i, uint64_t n) {
+  if (i + 1 < n) return __ldg(reinterpret_cast<const ulonglong2*>(p + i));
+  return make_ulonglong2(i < n ? __ldg(p + i) : 0ull, 0ull);
 }
 
 __device__ __forceinline__ uint64_t load_hi8(const uint8_t* hi, uint64_t i0, uint32_t cnt) {

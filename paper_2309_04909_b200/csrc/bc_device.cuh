@@ -39,6 +39,7 @@ struct Key {
 struct KP {
   uint64_t ymask;      // 2^ell - 1
   uint32_t f, w, p, S, lx;
+  uint32_t fsh, fhi;   // f & 31, f >= 32 (window extraction)
   uint32_t wmask;      // 2^w - 1
   uint32_t perm_lim;   // floor(2^31 / S!) * S!
   uint32_t fact;       // S!
@@ -48,7 +49,7 @@ struct KP {
 
 // ---------------------------------------------------------------------------
 // ChaCha_R block (RFC 8439 sec. 2.3), words 12-13 = 64-bit counter, 14-15 =
-// 64-bit label.  Fully unrolled; the key lives in the constant bank.
+// 64-bit label.  The key lives in the constant bank.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t rotl(uint32_t v, int n) { return __funnelshift_l(v, v, n); }
 
@@ -58,6 +59,14 @@ __device__ __forceinline__ uint32_t rotl(uint32_t v, int n) { return __funnelshi
   a += b; d ^= a; d = rotl(d, 8);  \
   c += d; b ^= c; b = rotl(b, 7);
 
+// Double rounds are kept rolled by default: a full R = 20 unroll is ~1000
+// instructions per call site and the fused kernel's call sites then overflow
+// the instruction cache (ncu: "no_instruction" was the top stall).
+#ifndef BC_CHACHA_UNROLL
+#define BC_CHACHA_UNROLL 1
+#endif
+constexpr int kChachaUnroll = BC_CHACHA_UNROLL;
+
 template <int R>
 __device__ __forceinline__ void chacha(const Key& key, uint64_t ctr, uint64_t label, uint32_t (&o)[16]) {
   uint32_t x0 = 0x61707865u, x1 = 0x3320646eu, x2 = 0x79622d32u, x3 = 0x6b206574u;
@@ -66,7 +75,7 @@ __device__ __forceinline__ void chacha(const Key& key, uint64_t ctr, uint64_t la
   const uint32_t c0 = (uint32_t)ctr, c1 = (uint32_t)(ctr >> 32);
   const uint32_t l0 = (uint32_t)label, l1 = (uint32_t)(label >> 32);
   uint32_t x12 = c0, x13 = c1, x14 = l0, x15 = l1;
-#pragma unroll
+#pragma unroll kChachaUnroll
   for (int r = 0; r < R; r += 2) {
     BC_QR(x0, x4, x8, x12) BC_QR(x1, x5, x9, x13) BC_QR(x2, x6, x10, x14) BC_QR(x3, x7, x11, x15)
     BC_QR(x0, x5, x10, x15) BC_QR(x1, x6, x11, x12) BC_QR(x2, x7, x8, x13) BC_QR(x3, x4, x9, x14)
@@ -116,12 +125,6 @@ __device__ __forceinline__ uint32_t perm_sel_rt(uint32_t q, uint32_t S) {
     }
   }
   return sel;
-}
-
-// Pack bytes a_i = (v >> i) & 255, i = 0..7, into two words (little endian).
-__device__ __forceinline__ void window_bytes(uint32_t v, uint32_t& lo, uint32_t& hi) {
-  lo = (v & 0xFFu) | ((v << 7) & 0xFF00u) | ((v << 14) & 0xFF0000u) | ((v << 21) & 0xFF000000u);
-  hi = ((v >> 4) & 0xFFu) | ((v << 3) & 0xFF00u) | ((v << 10) & 0xFF0000u) | ((v << 17) & 0xFF000000u);
 }
 
 // ---------------------------------------------------------------------------
@@ -180,46 +183,13 @@ __device__ __noinline__ void fallback(Draws& d, uint64_t j, Key key, uint32_t S,
 // ---------------------------------------------------------------------------
 // Decoded seed01 randomness of one element (Alg 7 steps 1, 6, 7, 8).
 // ---------------------------------------------------------------------------
+// Wide-tape (generic p, slots) randomness of one element.
 struct Tape {
   uint32_t t;        // blinding bit (step 1)
   uint32_t sel;      // permutation as a PRMT nibble selector (step 6)
-  uint32_t rm1[2];   // compact: bytes r_m - 1 (step 7)
-  uint32_t r[8];     // wide: r_m in Z_p^*
+  uint32_t r[8];     // r_m in Z_p^* (step 7)
   uint32_t rho[8];   // reshare rho_m in Z_p (step 8)
 };
-
-// Compact tape: 8 words T[0..7] = keystream bytes [32 j, 32 j + 32).
-//   T0: bit 31 = t, bits 0..30 = permutation index (reject >= 53261 * 8!)
-//   T1, T2: bytes m = r_m - 1 (exactly uniform on Z_257^*)
-//   T3..T6: u16 m = reshare draw (reject 65535), rho_m = u mod 257
-template <int R>
-__device__ __forceinline__ void decode_compact(const uint32_t* T, uint64_t j, const Key& k01, Tape& tp) {
-  const uint32_t T0 = T[0];
-  tp.t = T0 >> 31;
-  uint32_t idx = T0 & 0x7FFFFFFFu;
-  uint32_t w3 = T[3], w4 = T[4], w5 = T[5], w6 = T[6];
-  // any u16 == 0xFFFF  <=>  some halfword of ~w is zero
-  const uint32_t n3 = ~w3, n4 = ~w4, n5 = ~w5, n6 = ~w6;
-  const bool bad_rho = ((n3 & 0xFFFFu) == 0) | ((n3 >> 16) == 0) | ((n4 & 0xFFFFu) == 0) | ((n4 >> 16) == 0) |
-                       ((n5 & 0xFFFFu) == 0) | ((n5 >> 16) == 0) | ((n6 & 0xFFFFu) == 0) | ((n6 >> 16) == 0);
-  if (__builtin_expect(bad_rho | (idx >= PERM_LIMIT_8), 0)) {
-    Draws d;
-    d.idx = idx;
-    d.ur[0] = w3 & 0xFFFFu; d.ur[1] = w3 >> 16; d.ur[2] = w4 & 0xFFFFu; d.ur[3] = w4 >> 16;
-    d.ur[4] = w5 & 0xFFFFu; d.ur[5] = w5 >> 16; d.ur[6] = w6 & 0xFFFFu; d.ur[7] = w6 >> 16;
-    fallback<R>(d, j, k01, 8, PERM_LIMIT_8, 0, 65535u);
-    idx = d.idx;
-    w3 = d.ur[0] | (d.ur[1] << 16); w4 = d.ur[2] | (d.ur[3] << 16);
-    w5 = d.ur[4] | (d.ur[5] << 16); w6 = d.ur[6] | (d.ur[7] << 16);
-  }
-  tp.rm1[0] = T[1];
-  tp.rm1[1] = T[2];
-  tp.rho[0] = mod257(w3 & 0xFFFFu); tp.rho[1] = mod257(w3 >> 16);
-  tp.rho[2] = mod257(w4 & 0xFFFFu); tp.rho[3] = mod257(w4 >> 16);
-  tp.rho[4] = mod257(w5 & 0xFFFFu); tp.rho[5] = mod257(w5 >> 16);
-  tp.rho[6] = mod257(w6 & 0xFFFFu); tp.rho[7] = mod257(w6 >> 16);
-  tp.sel = perm_sel<8>(idx % 40320u);
-}
 
 // Wide tape: 16 words T[0..15] = keystream bytes [64 j, 64 j + 64).
 //   T0: t | perm index (reject >= floor(2^31/S!) S!)
@@ -255,35 +225,6 @@ __device__ __forceinline__ void decode_wide(const uint32_t* T, uint64_t j, const
 //   6   shuffle: PRMT with the permutation selector
 //   7-8 W_m = v'_m r_m + rho_m (P0) / v'_m r_m - rho_m (P1)  mod p
 // ---------------------------------------------------------------------------
-template <int PARTY>
-__device__ __forceinline__ void party_W_compact(uint64_t x, uint32_t f, const Tape& tp, uint32_t (&W)[8]) {
-  const uint64_t nx = 0ull - x;
-  // P0: s0 = t ? -x : x.   P1: n1 = -s1 = t ? x : -x.
-  const uint64_t v = (PARTY == 0) ? (tp.t ? nx : x) : (tp.t ? x : nx);
-  const uint32_t win = (uint32_t)(v >> f);
-  uint32_t A_lo, A_hi;
-  window_bytes(win, A_lo, A_hi);                         // u_i (P0) or -u_i (P1), w = 8
-  const uint32_t N_lo = __byte_perm(A_lo, A_hi, 0x4321u); // u_{i+1}, u_8 := 0
-  const uint32_t N_hi = A_hi >> 8;
-  uint32_t C_lo, C_hi;
-  if (PARTY == 0) {  // v'-1 = (u_i + u_{i+1} - 1 == 0 ? 256 : ...) - 1 = u_i + u_{i+1} - 2 mod 256
-    C_lo = __vsub4(__vadd4(A_lo, N_lo), 0x02020202u);
-    C_hi = __vsub4(__vadd4(A_hi, N_hi), 0x02020202u);
-  } else {           // v' - 1 = (257 + v - 256) mod 257 - 1 = v = -(B_i + B_{i+1}) mod 256
-    C_lo = __vneg4(__vadd4(A_lo, N_lo));
-    C_hi = __vneg4(__vadd4(A_hi, N_hi));
-  }
-  const uint32_t P_lo = __byte_perm(C_lo, C_hi, tp.sel & 0xFFFFu);
-  const uint32_t P_hi = __byte_perm(C_lo, C_hi, tp.sel >> 16);
-#pragma unroll
-  for (int m = 0; m < 8; ++m) {
-    const uint32_t c = byte_of(m < 4 ? P_lo : P_hi, m & 3);
-    const uint32_t r = byte_of(tp.rm1[m >> 2], m & 3) + 1u;
-    const uint32_t add = (PARTY == 0) ? r + tp.rho[m] : r + 257u - tp.rho[m];
-    W[m] = mod257(c * r + add);                          // ((c+1) r +- rho) mod 257
-  }
-}
-
 template <int PARTY>
 __device__ __forceinline__ void party_W_wide(uint64_t x, const KP& kp, const Tape& tp, uint32_t (&W)[8]) {
   const uint64_t nx = 0ull - x;

@@ -96,21 +96,11 @@ __global__ void __launch_bounds__(TPB) k_modswitch(EwArgs a) {
 // Alg 7 steps 3-5 on the share as given: bytes v'_m - 1 (slot m -> byte m).
 template <int PARTY>
 __device__ __forceinline__ uint64_t ladder_bytes(uint64_t x, const KP& kp, bool compact) {
-  const uint64_t v = PARTY == 0 ? x : 0ull - x;  // P1 works on -[x]_1 (Alg 5, reading C3)
-  const uint32_t win = (uint32_t)(v >> kp.f);
-  if (compact) {  // w = 8, p = 257: SWAR over the 8 windows
-    uint32_t A_lo, A_hi;
-    window_bytes(win, A_lo, A_hi);
-    const uint32_t N_lo = __byte_perm(A_lo, A_hi, 0x4321u), N_hi = A_hi >> 8;
-    uint32_t C_lo, C_hi;
-    if (PARTY == 0) {
-      C_lo = __vsub4(__vadd4(A_lo, N_lo), 0x02020202u);
-      C_hi = __vsub4(__vadd4(A_hi, N_hi), 0x02020202u);
-    } else {
-      C_lo = __vneg4(__vadd4(A_lo, N_lo));
-      C_hi = __vneg4(__vadd4(A_hi, N_hi));
-    }
-    return (uint64_t)C_lo | ((uint64_t)C_hi << 32);
+  const uint32_t win = window_of<PARTY>(x, 0u, kp.fsh, kp.fhi != 0);  // P1 works on -[x]_1 (reading C3)
+  if (compact) {  // w = 8, p = 257: all 8 windows at once (SWAR)
+    uint32_t lo, hi;
+    ladder_swar<PARTY>(win, lo, hi);
+    return (uint64_t)lo | ((uint64_t)hi << 32);
   }
   uint32_t u[8];
 #pragma unroll

@@ -20,124 +20,156 @@ struct FusedArgs {
   uint8_t *w0lo, *w0hi, *w1lo, *w1hi;
 };
 
-// Two consecutive elements (one 16-B vector per party).
-__device__ __forceinline__ ulonglong2 load2(const uint64_t* __restrict__ p, uint64_t i, uint64_t n) {
-  if (i + 1 < n) return __ldg(reinterpret_cast<const ulonglong2*>(p + i));
-  return make_ulonglong2(i < n ? __ldg(p + i) : 0ull, 0ull);
+// ---- shared finish: Alg 7 steps 10-11, or Alg 8 (triple, e, d, Beaver combine) ----
+template <int R, bool RELU>
+__device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, const Key& k02, const Key& k12,
+                                             uint64_t i0, uint64_t j0, uint32_t cnt, uint32_t zbits,
+                                             uint32_t tbits) {
+  uint64_t y0[8], y1[8];
+  if (!RELU) {
+    // Alg 7 step 10: P2 reshares DReLU' ([D']_0 from seed02); step 11: P0/P1 unblind.
+    uint32_t Q[16];
+    chacha<R>(k02, j0 >> 3, L_RESP, Q);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint64_t z = (zbits >> e) & 1u, t = (tbits >> e) & 1u;
+      const uint64_t q = u64_of(Q, e) & kp.ymask;  // [D']_0
+      const uint64_t d1 = (z - q) & kp.ymask;      // [D']_1 = D' - [D']_0
+      y0[e] = t ? ((1ull - q) & kp.ymask) : q;     // t + (1-2t)[D']_0
+      y1[e] = t ? ((0ull - d1) & kp.ymask) : d1;   // (1-2t)[D']_1
+    }
+  } else {
+    // Alg 8: triple from seed02 / seed12, e from P2, d opened by P0/P1, combine.
+    uint64_t b0[8], b1[8], ev[8];
+    {
+      uint32_t Bk[16];
+      chacha<R>(k02, j0 >> 3, L_B02, Bk);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) b0[e] = u64_of(Bk, e);
+      chacha<R>(k12, j0 >> 3, L_B12, Bk);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        b1[e] = u64_of(Bk, e);
+        ev[e] = ((zbits >> e) & 1u) - b0[e] - b1[e];  // P2: e = DReLU' - ([b]_0 + [b]_1)
+      }
+    }
+    {
+      uint32_t Ak0[16], Ak1[16];
+      chacha<R>(k02, j0 >> 3, L_A02, Ak0);
+      chacha<R>(k12, j0 >> 3, L_A12, Ak1);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const ulonglong2 v0 = load2(a.x0, i0 + 2 * h, a.n), v1 = load2(a.x1, i0 + 2 * h, a.n);
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const int e = 2 * h + s;
+          const uint64_t a0 = u64_of(Ak0, e), a1 = u64_of(Ak1, e);
+          const uint64_t d = ((s ? v0.y : v0.x) - a0) + ((s ? v1.y : v1.x) - a1);  // opened d = x - a
+          y0[e] = d * ev[e] + d * b0[e] + ev[e] * a0;                          // P0: de + d[b]_0 + e[a]_0
+          y1[e] = d * b1[e] + ev[e] * a1 + (a0 + a1) * (b0[e] + b1[e]);        // P1: d[b]_1 + e[a]_1 + ab
+        }
+      }
+    }
+    {
+      uint32_t Ck[16];
+      chacha<R>(k02, j0 >> 3, L_C02, Ck);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const ulonglong2 v0 = load2(a.x0, i0 + 2 * h, a.n), v1 = load2(a.x1, i0 + 2 * h, a.n);
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const int e = 2 * h + s;
+          const uint64_t c0v = u64_of(Ck, e);
+          const uint64_t t = (tbits >> e) & 1u;
+          const uint64_t in0 = y0[e] + c0v;  // ... + [c]_0
+          const uint64_t in1 = y1[e] - c0v;  // [c]_1 = ab - [c]_0 (P2)
+          const uint64_t x0v = s ? v0.y : v0.x, x1v = s ? v1.y : v1.x;
+          y0[e] = ((t ? x0v : 0ull) + (t ? 0ull - in0 : in0)) & kp.ymask;  // t[x] + (1-2t)(...)
+          y1[e] = ((t ? x1v : 0ull) + (t ? 0ull - in1 : in1)) & kp.ymask;
+        }
+      }
+    }
+  }
+  store8(a.y0 + i0, y0, cnt);
+  store8(a.y1 + i0, y1, cnt);
 }
 
-template <int R, bool COMPACT, bool RELU>
-__global__ void __launch_bounds__(TPB, 2) k_fused(FusedArgs a, KP kp, Key k01, Key k02, Key k12) {
+// Compact tape (p = 257, 8 slots): 4 seed01 blocks per 8-element group, one
+// block per element pair; the pair loop is kept rolled (instruction cache).
+template <int R, bool RELU>
+__global__ void __launch_bounds__(TPB, 2) k_fused_c(FusedArgs a, KP kp, Key k01, Key k02, Key k12) {
+  __shared__ uint32_t sA[PERM_A], sB[PERM_B];
+  build_perm_tables(sA, sB);
+  __syncthreads();
+  const bool fhi = kp.fhi != 0;
   const uint64_t ngroups = (a.n + 7) >> 3;
   for (uint64_t g = (uint64_t)blockIdx.x * TPB + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB) {
     const uint64_t i0 = g << 3;
     const uint64_t j0 = a.base + i0;
     const uint32_t cnt = (uint32_t)min((uint64_t)8, a.n - i0);
-
-    // ---- Alg 7 steps 1-9: P0 and P1 local phase, P2 zero test --------------
-    // Shares are streamed two elements at a time; the next pair's loads are
-    // issued before the current pair's ChaCha block so their latency hides.
     uint32_t zbits = 0, tbits = 0;
-    ulonglong2 c0 = load2(a.x0, i0, a.n), c1 = load2(a.x1, i0, a.n);
-#pragma unroll
+#pragma unroll 1
     for (int h = 0; h < 4; ++h) {
-      ulonglong2 n0 = c0, n1 = c1;
-      if (h < 3) {
-        n0 = load2(a.x0, i0 + 2 * h + 2, a.n);
-        n1 = load2(a.x1, i0 + 2 * h + 2, a.n);
-      }
-      uint32_t B[16];  // compact: one block serves the pair; wide: one block per element
-      if (COMPACT) tape_block<R, true>(k01, j0, h, B);
+      const ulonglong2 v0 = load2(a.x0, i0 + 2 * h, a.n), v1 = load2(a.x1, i0 + 2 * h, a.n);
+      uint32_t B[16];
+      chacha<R>(k01, (j0 >> 1) + (uint64_t)h, L_TAPE, B);
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         const int e = 2 * h + s;
-        if (!COMPACT) tape_block<R, false>(k01, j0, e, B);
-        Tape tp;
-        decode<R, COMPACT>(B, COMPACT ? s : 0, j0 + e, k01, kp, tp);
-        uint32_t W0[8], W1[8];
-        const uint64_t xa = s ? c0.y : c0.x, xb = s ? c1.y : c1.x;
-        party_W<COMPACT, 0>(xa, kp, tp, W0);
-        party_W<COMPACT, 1>(xb, kp, tp, W1);
-        zbits |= zero_test(W0, W1, kp.p, kp.S) << e;
+        const uint32_t* T = &B[8 * s];
+        TapeC tp;
+        decode_c<R>(T[0], T[1], T[2], T[3], T[4], T[5], T[6], j0 + (uint64_t)e, k01, sA, sB, tp);
+        const uint64_t xa = s ? v0.y : v0.x, xb = s ? v1.y : v1.x;
+        uint32_t W0[8], W1[8], z;
+        if (a.w0lo != nullptr) {  // transcript of the P0/P1 -> P2 messages (uniform branch)
+          z = elem_both<true>(xa, xb, tp, kp.fsh, fhi, W0, W1);
+          if ((uint32_t)e < cnt) {
+            reinterpret_cast<uint64_t*>(a.w0lo)[i0 + e] = pack_lo(W0);
+            reinterpret_cast<uint64_t*>(a.w1lo)[i0 + e] = pack_lo(W1);
+            a.w0hi[i0 + e] = (uint8_t)pack_hi(W0);
+            a.w1hi[i0 + e] = (uint8_t)pack_hi(W1);
+          }
+        } else {
+          z = elem_both<false>(xa, xb, tp, kp.fsh, fhi, W0, W1);
+        }
+        zbits |= z << e;
         tbits |= tp.t << e;
-        if (a.w0lo != nullptr && (uint32_t)e < cnt) {  // optional transcript of the messages to P2
-          reinterpret_cast<uint64_t*>(a.w0lo)[i0 + e] = pack_lo(W0);
-          reinterpret_cast<uint64_t*>(a.w1lo)[i0 + e] = pack_lo(W1);
-          a.w0hi[i0 + e] = (uint8_t)pack_hi(W0);
-          a.w1hi[i0 + e] = (uint8_t)pack_hi(W1);
-        }
       }
-      c0 = n0;
-      c1 = n1;
     }
+    finish_group<R, RELU>(a, kp, k02, k12, i0, j0, cnt, zbits, tbits);
+  }
+}
 
-    uint64_t y0[8], y1[8];
-    if (!RELU) {
-      // ---- Alg 7 step 10: P2 reshares DReLU'; step 11: P0/P1 unblind -------
-      uint32_t Q[16];
-      chacha<R>(k02, j0 >> 3, L_RESP, Q);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const uint64_t z = (zbits >> e) & 1u, t = (tbits >> e) & 1u;
-        const uint64_t q = u64_of(Q, e) & kp.ymask;  // [D']_0 from seed02
-        const uint64_t d1 = (z - q) & kp.ymask;      // [D']_1 = D' - [D']_0
-        y0[e] = t ? ((1ull - q) & kp.ymask) : q;     // t + (1-2t)[D']_0
-        y1[e] = t ? ((0ull - d1) & kp.ymask) : d1;   // (1-2t)[D']_1
-      }
-    } else {
-      // ---- Alg 8: triple from seeds, e from P2, d opened, Beaver combine ---
-      uint64_t b0[8], b1[8], ev[8];
-      {
-        uint32_t Bk[16];
-        chacha<R>(k02, j0 >> 3, L_B02, Bk);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) b0[e] = u64_of(Bk, e);
-        chacha<R>(k12, j0 >> 3, L_B12, Bk);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          b1[e] = u64_of(Bk, e);
-          ev[e] = ((zbits >> e) & 1u) - b0[e] - b1[e];  // P2: e = DReLU' - ([b]_0 + [b]_1)
-        }
-      }
-      {
-        uint32_t Ak0[16], Ak1[16];
-        chacha<R>(k02, j0 >> 3, L_A02, Ak0);
-        chacha<R>(k12, j0 >> 3, L_A12, Ak1);
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const ulonglong2 v0 = load2(a.x0, i0 + 2 * h, a.n), v1 = load2(a.x1, i0 + 2 * h, a.n);
-#pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            const int e = 2 * h + s;
-            const uint64_t a0 = u64_of(Ak0, e), a1 = u64_of(Ak1, e);
-            const uint64_t d = ((s ? v0.y : v0.x) - a0) + ((s ? v1.y : v1.x) - a1);  // opened d = x - a
-            y0[e] = d * ev[e] + d * b0[e] + ev[e] * a0;                          // P0: de + d[b]_0 + e[a]_0
-            y1[e] = d * b1[e] + ev[e] * a1 + (a0 + a1) * (b0[e] + b1[e]);        // P1: d[b]_1 + e[a]_1 + ab
-          }
-        }
-      }
-      {
-        uint32_t Ck[16];
-        chacha<R>(k02, j0 >> 3, L_C02, Ck);
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const ulonglong2 v0 = load2(a.x0, i0 + 2 * h, a.n), v1 = load2(a.x1, i0 + 2 * h, a.n);
-#pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            const int e = 2 * h + s;
-            const uint64_t c0v = u64_of(Ck, e);
-            const uint64_t t = (tbits >> e) & 1u;
-            const uint64_t in0 = y0[e] + c0v;  // ... + [c]_0
-            const uint64_t in1 = y1[e] - c0v;  // [c]_1 = ab - [c]_0 (P2)
-            const uint64_t x0v = s ? v0.y : v0.x, x1v = s ? v1.y : v1.x;
-            y0[e] = ((t ? x0v : 0ull) + (t ? 0ull - in0 : in0)) & kp.ymask;  // t[x] + (1-2t)(...)
-            y1[e] = ((t ? x1v : 0ull) + (t ? 0ull - in1 : in1)) & kp.ymask;
-          }
-        }
+// Wide tape (any p <= 257, 3..8 slots): one seed01 block per element.
+template <int R, bool RELU>
+__global__ void __launch_bounds__(TPB, 2) k_fused_w(FusedArgs a, KP kp, Key k01, Key k02, Key k12) {
+  const uint64_t ngroups = (a.n + 7) >> 3;
+  for (uint64_t g = (uint64_t)blockIdx.x * TPB + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB) {
+    const uint64_t i0 = g << 3;
+    const uint64_t j0 = a.base + i0;
+    const uint32_t cnt = (uint32_t)min((uint64_t)8, a.n - i0);
+    uint32_t zbits = 0, tbits = 0;
+#pragma unroll 1
+    for (int e = 0; e < 8; ++e) {
+      const uint64_t xa = (uint32_t)e < cnt ? __ldg(a.x0 + i0 + e) : 0ull;
+      const uint64_t xb = (uint32_t)e < cnt ? __ldg(a.x1 + i0 + e) : 0ull;
+      uint32_t B[16];
+      chacha<R>(k01, j0 + (uint64_t)e, L_TAPEW, B);
+      Tape tp;
+      decode_wide<R>(B, j0 + e, k01, kp, tp);
+      uint32_t W0[8], W1[8];
+      party_W_wide<0>(xa, kp, tp, W0);
+      party_W_wide<1>(xb, kp, tp, W1);
+      zbits |= zero_test(W0, W1, kp.p, kp.S) << e;
+      tbits |= tp.t << e;
+      if (a.w0lo != nullptr && (uint32_t)e < cnt) {
+        reinterpret_cast<uint64_t*>(a.w0lo)[i0 + e] = pack_lo(W0);
+        reinterpret_cast<uint64_t*>(a.w1lo)[i0 + e] = pack_lo(W1);
+        a.w0hi[i0 + e] = (uint8_t)pack_hi(W0);
+        a.w1hi[i0 + e] = (uint8_t)pack_hi(W1);
       }
     }
-    store8(a.y0 + i0, y0, cnt);
-    store8(a.y1 + i0, y1, cnt);
+    finish_group<R, RELU>(a, kp, k02, k12, i0, j0, cnt, zbits, tbits);
   }
 }
 
@@ -169,10 +201,10 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
   return dispatch_rounds(prm->rounds, [&](auto Rc) {
     constexpr int R = decltype(Rc)::value;
     if (prm->compact) {
-      auto fn = k_fused<R, true, RELU>;
+      auto fn = k_fused_c<R, RELU>;
       fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k01, k02, k12);
     } else {
-      auto fn = k_fused<R, false, RELU>;
+      auto fn = k_fused_w<R, RELU>;
       fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k01, k02, k12);
     }
     return check_launch();

@@ -87,6 +87,8 @@ KP make_kp(const bc_params* prm) {
   KP kp;
   kp.ymask = prm->ell == 64 ? ~0ull : ((1ull << prm->ell) - 1ull);
   kp.f = (uint32_t)prm->f;
+  kp.fsh = (uint32_t)prm->f & 31u;
+  kp.fhi = prm->f >= 32 ? 1u : 0u;
   kp.w = prm->w;
   kp.p = prm->p;
   kp.S = prm->slots;

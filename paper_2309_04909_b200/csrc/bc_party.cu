@@ -17,51 +17,107 @@ struct SendArgs {
   uint64_t n, base;
 };
 
-// Alg 7 steps 1-8 (and Alg 8's [d]_b) for one computing party.
-template <int R, bool COMPACT, int PARTY, bool RELU>
-__global__ void __launch_bounds__(TPB, 2) k_send(SendArgs a, KP kp, Key k01, Key ktr) {
+__device__ __forceinline__ void store_msg(const SendArgs& a, const KP& kp, const Key& ktr, uint64_t g, uint64_t i0,
+                                          uint64_t j0, uint32_t cnt, const uint64_t (&lo)[8], uint64_t hi,
+                                          uint32_t tb, int party, bool relu);
+
+// Alg 7 steps 1-8 (and Alg 8's [d]_b) for one computing party, compact tape.
+template <int R, int PARTY, bool RELU>
+__global__ void __launch_bounds__(TPB, 2) k_send_c(SendArgs a, KP kp, Key k01, Key ktr) {
+  __shared__ uint32_t sA[PERM_A], sB[PERM_B];
+  build_perm_tables(sA, sB);
+  __syncthreads();
+  const bool fhi = kp.fhi != 0;
   const uint64_t ngroups = (a.n + 7) >> 3;
   for (uint64_t g = (uint64_t)blockIdx.x * TPB + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB) {
     const uint64_t i0 = g << 3;
     const uint64_t j0 = a.base + i0;
     const uint32_t cnt = (uint32_t)min((uint64_t)8, a.n - i0);
-    uint64_t x[8], lo[8];
-    load8(a.x + i0, x, cnt);
+    uint64_t lo[8];
     uint32_t tb = 0;
     uint64_t hi = 0;
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
+      const ulonglong2 v = load2(a.x, i0 + 2 * h, a.n);
       uint32_t B[16];
-      if (COMPACT) tape_block<R, true>(k01, j0, h, B);
+      chacha<R>(k01, (j0 >> 1) + (uint64_t)h, L_TAPE, B);
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         const int e = 2 * h + s;
-        if (!COMPACT) tape_block<R, false>(k01, j0, e, B);
-        Tape tp;
-        decode<R, COMPACT>(B, COMPACT ? s : 0, j0 + e, k01, kp, tp);
+        const uint32_t* T = &B[8 * s];
+        TapeC tp;
+        decode_c<R>(T[0], T[1], T[2], T[3], T[4], T[5], T[6], j0 + (uint64_t)e, k01, sA, sB, tp);
         uint32_t W[8];
-        party_W<COMPACT, PARTY>(x[e], kp, tp, W);
+        elem_one<PARTY>(s ? v.y : v.x, tp, kp.fsh, fhi, W);
         lo[e] = pack_lo(W);
         hi |= (uint64_t)pack_hi(W) << (8 * e);
         tb |= tp.t << e;
       }
     }
-    store8(reinterpret_cast<uint64_t*>(a.lo) + i0, lo, cnt);
-    if (a.hi) {
-      if (cnt == 8) *reinterpret_cast<uint64_t*>(a.hi + i0) = hi;
-      else
-        for (uint32_t e = 0; e < cnt; ++e) a.hi[i0 + e] = (uint8_t)(hi >> (8 * e));
-    }
-    a.tbits[g] = (uint8_t)(tb & ((1u << cnt) - 1u));
+    store_msg(a, kp, ktr, g, i0, j0, cnt, lo, hi, tb, PARTY, false);
     if (RELU) {  // Alg 8 step 4: [d]_b = [x]_b - [a]_b
       uint32_t Ak[16];
       chacha<R>(ktr, j0 >> 3, PARTY == 0 ? L_A02 : L_A12, Ak);
-      uint64_t d[8];
+      uint64_t x[8], d[8];
+      load8(a.x + i0, x, cnt);
 #pragma unroll
       for (int e = 0; e < 8; ++e) d[e] = (x[e] - u64_of(Ak, e)) & kp.ymask;
       store8(a.dshare + i0, d, cnt);
     }
   }
+}
+
+// Wide tape.
+template <int R, int PARTY, bool RELU>
+__global__ void __launch_bounds__(TPB, 2) k_send_w(SendArgs a, KP kp, Key k01, Key ktr) {
+  const uint64_t ngroups = (a.n + 7) >> 3;
+  for (uint64_t g = (uint64_t)blockIdx.x * TPB + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB) {
+    const uint64_t i0 = g << 3;
+    const uint64_t j0 = a.base + i0;
+    const uint32_t cnt = (uint32_t)min((uint64_t)8, a.n - i0);
+    uint64_t lo[8];
+    uint32_t tb = 0;
+    uint64_t hi = 0;
+#pragma unroll 1
+    for (int e = 0; e < 8; ++e) {
+      const uint64_t xv = (uint32_t)e < cnt ? __ldg(a.x + i0 + e) : 0ull;
+      uint32_t B[16];
+      chacha<R>(k01, j0 + (uint64_t)e, L_TAPEW, B);
+      Tape tp;
+      decode_wide<R>(B, j0 + e, k01, kp, tp);
+      uint32_t W[8];
+      party_W_wide<PARTY>(xv, kp, tp, W);
+      const uint64_t l = pack_lo(W);
+      const uint64_t hbyte = pack_hi(W);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k == e) lo[k] = l;
+      hi |= hbyte << (8 * e);
+      tb |= tp.t << e;
+    }
+    store_msg(a, kp, ktr, g, i0, j0, cnt, lo, hi, tb, PARTY, false);
+    if (RELU) {
+      uint32_t Ak[16];
+      chacha<R>(ktr, j0 >> 3, PARTY == 0 ? L_A02 : L_A12, Ak);
+      uint64_t x[8], d[8];
+      load8(a.x + i0, x, cnt);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) d[e] = (x[e] - u64_of(Ak, e)) & kp.ymask;
+      store8(a.dshare + i0, d, cnt);
+    }
+  }
+}
+
+__device__ __forceinline__ void store_msg(const SendArgs& a, const KP& kp, const Key& ktr, uint64_t g, uint64_t i0,
+                                          uint64_t j0, uint32_t cnt, const uint64_t (&lo)[8], uint64_t hi,
+                                          uint32_t tb, int party, bool relu) {
+  store8(reinterpret_cast<uint64_t*>(a.lo) + i0, lo, cnt);
+  if (a.hi) {
+    if (cnt == 8) *reinterpret_cast<uint64_t*>(a.hi + i0) = hi;
+    else
+      for (uint32_t e = 0; e < cnt; ++e) a.hi[i0 + e] = (uint8_t)(hi >> (8 * e));
+  }
+  a.tbits[g] = (uint8_t)(tb & ((1u << cnt) - 1u));
 }
 
 struct HelperArgs {
@@ -227,11 +283,11 @@ int send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits,
     constexpr int R = decltype(Rc)::value;
     auto go = [&](auto fn) { fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k01, ktr); };
     if (prm->compact) {
-      if (party == 0) go(k_send<R, true, 0, RELU>);
-      else go(k_send<R, true, 1, RELU>);
+      if (party == 0) go(k_send_c<R, 0, RELU>);
+      else go(k_send_c<R, 1, RELU>);
     } else {
-      if (party == 0) go(k_send<R, false, 0, RELU>);
-      else go(k_send<R, false, 1, RELU>);
+      if (party == 0) go(k_send_w<R, 0, RELU>);
+      else go(k_send_w<R, 1, RELU>);
     }
     return check_launch();
   });
