@@ -24,7 +24,8 @@ from . import ring
 from .chacha import chacha_blocks, element_u32, element_u64, label_u64
 
 # Stream labels (domain separation of the seeds' keystreams).
-L_TAPE = label_u64(b"bc2.tape")    # seed01: 32 B/element (compact tape)
+L_TAPEA = label_u64(b"bc2.tpa1")  # seed01: 16 B/element (compact tape, part A)
+L_TAPEB = label_u64(b"bc2.tpb1")  # seed01:  8 B/element (compact tape, part B)
 L_TAPEW = label_u64(b"bc2.tapw")   # seed01: 64 B/element (wide tape)
 L_FALLBACK = label_u64(b"bc2.fb01")  # seed01: rejection fallback, counter j*256+k
 L_RESP = label_u64(b"bc2.resp")    # seed02: [DReLU']_0, 8 B/element
@@ -35,6 +36,7 @@ L_A12 = label_u64(b"bc2.ta12")     # seed12: [a]_1, 8 B/element
 L_B12 = label_u64(b"bc2.tb12")     # seed12: [b]_1, 8 B/element
 
 PERM_LIMIT_COMPACT = 53261 * 40320  # largest multiple of 8! below 2^31
+RHO_WORD_LIMIT = 253 * 257 ** 3     # largest multiple of 257^3 below 2^32
 
 
 @dataclass(frozen=True)
@@ -71,7 +73,7 @@ class Params:
 
     @property
     def compact(self) -> bool:
-        """Compact 32-B tape iff p = 257 and 8 slots (masks are exact bytes)."""
+        """Compact 24-B tape iff p = 257 and 8 slots (masks are exact bytes)."""
         return self.p == 257 and self.slots == 8
 
 
@@ -109,50 +111,78 @@ def tape(prm: Params, seed01: bytes, j) -> dict:
     Parity unpinned beyond the ChaCha vector (the layout is the spec's).
     """
     j = np.atleast_1d(np.asarray(j, dtype=np.uint64))
-    n, S, p = j.size, prm.slots, prm.p
     if prm.compact:
-        T = element_u32(seed01, L_TAPE, prm.rounds, j, 8)
-        t = (T[:, 0] >> np.uint32(31)).astype(np.uint64)
-        idx = (T[:, 0] & np.uint32(0x7FFFFFFF)).astype(np.uint64)
-        idx_ok = idx < np.uint64(PERM_LIMIT_COMPACT)
-        rbytes = np.ascontiguousarray(T[:, 1:3]).view(np.uint8).reshape(n, 8).astype(np.uint64)
-        r = rbytes + np.uint64(1)
-        r_ok = np.ones((n, S), dtype=bool)
-        u = np.ascontiguousarray(T[:, 3:7]).view("<u2").reshape(n, 8).astype(np.uint64)
-        perm_lim = PERM_LIMIT_COMPACT
-        mask_lim = None
-    else:
-        T = element_u32(seed01, L_TAPEW, prm.rounds, j, 16)
-        t = (T[:, 0] >> np.uint32(31)).astype(np.uint64)
-        idx = (T[:, 0] & np.uint32(0x7FFFFFFF)).astype(np.uint64)
-        perm_lim = ((1 << 31) // math.factorial(S)) * math.factorial(S)
-        idx_ok = idx < np.uint64(perm_lim)
-        um = np.ascontiguousarray(T[:, 1:5]).view("<u2").reshape(n, 8)[:, :S].astype(np.uint64)
-        mask_lim = (65536 // (p - 1)) * (p - 1)
-        r_ok = um < np.uint64(mask_lim)
-        r = np.uint64(1) + um % np.uint64(p - 1)
-        u = np.ascontiguousarray(T[:, 5:9]).view("<u2").reshape(n, 8).astype(np.uint64)
-    u = u[:, :S]
+        return _tape_compact(prm, seed01, j)
+    return _tape_wide(prm, seed01, j)
+
+
+def _tape_compact(prm: Params, seed01: bytes, j) -> dict:
+    """p = 257, 8 slots.  24 B per element from two regular streams:
+    part A (16 B at 16 j): T0 = t (bit 31) | perm index (bits 0..30, reject >= 53261*8!),
+                           T1, T2 = mask bytes, r_m = 1 + byte m (exactly uniform on Z_257^*),
+                           T3 = reshare word 0;
+    part B (8 B at 8 j):   T4, T5 = reshare words 1, 2.
+    Reshare word k (reject >= 253 * 257^3) holds rho_{3k}, rho_{3k+1}, rho_{3k+2}
+    as its base-257 digits, least significant first (rho_8 is unused)."""
+    n, S = j.size, prm.slots
+    A = element_u32(seed01, L_TAPEA, prm.rounds, j, 4)
+    Bw = element_u32(seed01, L_TAPEB, prm.rounds, j, 2)
+    t = (A[:, 0] >> np.uint32(31)).astype(np.uint64)
+    idx = (A[:, 0] & np.uint32(0x7FFFFFFF)).astype(np.uint64)
+    idx_ok = idx < np.uint64(PERM_LIMIT_COMPACT)
+    r = np.ascontiguousarray(A[:, 1:3]).view(np.uint8).reshape(n, 8).astype(np.uint64) + np.uint64(1)
+    words = np.stack([A[:, 3], Bw[:, 0], Bw[:, 1]], axis=1).astype(np.uint64)
+    words_ok = words < np.uint64(RHO_WORD_LIMIT)
+    for row in np.nonzero(~idx_ok | ~words_ok.all(axis=1))[0]:  # rare: fallback stream, in order
+        fb = _fallback_words(seed01, int(j[row]), prm.rounds)
+        if not idx_ok[row]:
+            v = next(fb) & 0x7FFFFFFF
+            while v >= PERM_LIMIT_COMPACT:
+                v = next(fb) & 0x7FFFFFFF
+            idx[row] = v
+        for k in range(3):
+            if not words_ok[row, k]:
+                v = next(fb)
+                while v >= RHO_WORD_LIMIT:
+                    v = next(fb)
+                words[row, k] = v
+    P = np.uint64(257)
+    digits = np.stack([(words // P ** np.uint64(i)) % P for i in range(3)], axis=2).reshape(n, 9)
+    return {"t": t, "k": _perm_swaps(idx, S), "r": r, "rho": digits[:, :8].copy()}
+
+
+def _tape_wide(prm: Params, seed01: bytes, j) -> dict:
+    """Any p <= 257, 3..8 slots.  64 B per element at 64 j (label bc2.tapw):
+    T0 = t | perm index (reject >= floor(2^31/S!) S!); T1..T4 = 8 u16 mask draws,
+    r_m = 1 + u mod (p-1) (reject >= floor(65536/(p-1))(p-1)); T5..T8 = 8 u16
+    reshare draws, rho_m = u mod p (reject >= floor(65536/p) p)."""
+    n, S, p = j.size, prm.slots, prm.p
+    T = element_u32(seed01, L_TAPEW, prm.rounds, j, 16)
+    t = (T[:, 0] >> np.uint32(31)).astype(np.uint64)
+    idx = (T[:, 0] & np.uint32(0x7FFFFFFF)).astype(np.uint64)
+    perm_lim = ((1 << 31) // math.factorial(S)) * math.factorial(S)
+    idx_ok = idx < np.uint64(perm_lim)
+    um = np.ascontiguousarray(T[:, 1:5]).view("<u2").reshape(n, 8)[:, :S].astype(np.uint64)
+    mask_lim = (65536 // (p - 1)) * (p - 1)
+    r_ok = um < np.uint64(mask_lim)
+    r = np.uint64(1) + um % np.uint64(p - 1)
+    u = np.ascontiguousarray(T[:, 5:9]).view("<u2").reshape(n, 8)[:, :S].astype(np.uint64)
     rho_lim = (65536 // p) * p
     rho_ok = u < np.uint64(rho_lim)
     rho = u % np.uint64(p)
-    r = r[:, :S].copy()
-
-    bad = np.nonzero(~idx_ok | ~r_ok.all(axis=1) | ~rho_ok.all(axis=1))[0]
-    for row in bad:  # rare: resample rejected draws from the fallback stream, in order
+    for row in np.nonzero(~idx_ok | ~r_ok.all(axis=1) | ~rho_ok.all(axis=1))[0]:
         fb = _fallback_words(seed01, int(j[row]), prm.rounds)
         if not idx_ok[row]:
             v = next(fb) & 0x7FFFFFFF
             while v >= perm_lim:
                 v = next(fb) & 0x7FFFFFFF
             idx[row] = v
-        if mask_lim is not None:
-            for m in range(S):
-                if not r_ok[row, m]:
+        for m in range(S):
+            if not r_ok[row, m]:
+                v = next(fb) & 0xFFFF
+                while v >= mask_lim:
                     v = next(fb) & 0xFFFF
-                    while v >= mask_lim:
-                        v = next(fb) & 0xFFFF
-                    r[row, m] = 1 + v % (p - 1)
+                r[row, m] = 1 + v % (p - 1)
         for m in range(S):
             if not rho_ok[row, m]:
                 v = next(fb) & 0xFFFF

@@ -81,9 +81,10 @@ def lib() -> ctypes.CDLL:
     """Load libbicoptor.so (built in-tree by __graft_entry__.build())."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise BicoptorError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
-        L = ctypes.CDLL(LIB_PATH)
+        path = os.environ.get("BICOPTOR_LIB", LIB_PATH)  # tuning experiments load a variant build
+        if not os.path.exists(path):
+            raise BicoptorError(f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(path)
         for name, (res, args) in _SIG.items():
             fn = getattr(L, name)
             fn.restype = res

@@ -39,19 +39,24 @@ def _digest(paths) -> str:
     return h.hexdigest()
 
 
-def build(verbose: bool = False, ptxas_v: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, ptxas_v: bool = False, force: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile and link.  `defines` / `out` are for tuning experiments (tools/variants.py);
+    the product library is built with neither."""
     headers = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(INCLUDE, "bicoptor.h"))
-    os.makedirs(OBJDIR, exist_ok=True)
-    stamp_file = os.path.join(OBJDIR, "stamp")
+    lib = out or LIB
+    objdir = OBJDIR if not defines else OBJDIR + "_" + hashlib.sha256(" ".join(defines).encode()).hexdigest()[:8]
+    os.makedirs(objdir, exist_ok=True)
+    stamp_file = os.path.join(objdir, "stamp")
     all_src = [os.path.join(CSRC, s) for s in SOURCES]
-    digest = _digest(headers + all_src)
-    if not force and os.path.exists(LIB) and os.path.exists(stamp_file) and open(stamp_file).read() == digest:
-        return LIB
+    digest = _digest(headers + all_src) + " ".join(defines) + lib
+    if not force and os.path.exists(lib) and os.path.exists(stamp_file) and open(stamp_file).read() == digest:
+        return lib
+    dflags = [f"-D{d}" for d in defines]
 
     def compile_one(src: str) -> str:
-        obj = os.path.join(OBJDIR, os.path.basename(src).replace(".cu", ".o"))
-        cmd = [nvcc()] + ARCH + FLAGS + (["-Xptxas", "-v"] if ptxas_v else []) + ["-c", src, "-o", obj]
+        obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
+        cmd = [nvcc()] + ARCH + FLAGS + dflags + (["-Xptxas", "-v"] if ptxas_v else []) + ["-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
@@ -61,13 +66,13 @@ def build(verbose: bool = False, ptxas_v: bool = False, force: bool = False) -> 
 
     with cf.ThreadPoolExecutor(max_workers=len(all_src)) as ex:
         objs = list(ex.map(compile_one, all_src))
-    cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs
+    cmd = [nvcc()] + ARCH + ["-shared", "-o", lib] + objs
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
     with open(stamp_file, "w") as f:
         f.write(digest)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -21,6 +21,10 @@
 namespace bc {
 
 constexpr int TPB = 256;
+#ifndef BC_FUSED_MINB
+#define BC_FUSED_MINB 2
+#endif
+constexpr int FUSED_MINB = BC_FUSED_MINB;  // resident CTAs per SM the fused kernels are compiled for
 
 __device__ __forceinline__ uint64_t u64_of(const uint32_t (&B)[16], int e) {
   return (uint64_t)B[2 * e] | ((uint64_t)B[2 * e + 1] << 32);

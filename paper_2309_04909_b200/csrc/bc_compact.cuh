@@ -4,7 +4,7 @@
 // balancing the ALU pipe (LOP3/SHF/PRMT/IADD3) against the FMA pipe (IMAD*).
 //
 // Per-element data flow (both computing parties; P2's zero test):
-//   tape   T0..T6 (7 of the element's 8 keystream words)
+//   tape   T0..T3 (part A, 16 B) and T4, T5 (part B, 8 B): DESIGN.md "PRG tape"
 //   t      = T0 >> 31                              (Alg 7 step 1)
 //   Pi     = Fisher-Yates digits of T0 & 0x7fffffff, evaluated as two table
 //            lookups (k7,k6,k5 | k4..k1) = (idx mod 336 | idx / 336 mod 120)
@@ -50,44 +50,50 @@ __device__ __forceinline__ void build_perm_tables(uint32_t* sA, uint32_t* sB) {
 struct TapeC {
   uint32_t t;          // blinding bit
   uint32_t selA, selB; // two-phase shuffle selectors (nibbles)
-  uint32_t r[4];       // 16-bit lanes: slot 2j -> lane 0 of r[j], slot 2j+1 -> lane 1
-  uint32_t a0[4];      // lanes of r_m + rho_m + 257      (P0 addend)
-  uint32_t a1[4];      // lanes of r_m - rho_m + 514      (P1 addend)
+  uint32_t rb[2];      // mask bytes r_m - 1, slot m = byte m
+  uint32_t rho[8];     // reshare digits rho_m in Z_257
 };
 
-// Halfword == 0xFFFF detector (exact as a boolean): haszero16(~w).
-__device__ __forceinline__ uint32_t has_ffff(uint32_t w) { return (0u - w - 0x00010002u) & w & 0x80008000u; }
+// x / 257 for any 32-bit x: floor(x * (2^40 + 1)/257 / 2^40) (exact).
+__device__ __forceinline__ uint32_t div257(uint32_t x) { return __umulhi(x, 0xFF00FF01u) >> 8; }
 
 template <int R>
-__device__ __forceinline__ void decode_c(uint32_t T0, uint32_t T1, uint32_t T2, uint32_t w3, uint32_t w4,
-                                         uint32_t w5, uint32_t w6, uint64_t j, const Key& k01,
-                                         const uint32_t* sA, const uint32_t* sB, TapeC& tp) {
+__device__ __noinline__ void fallback_c(uint32_t& idx, uint32_t& w0, uint32_t& w1, uint32_t& w2, uint64_t j, Key key) {
+  FbStream<R> fb;
+  fb.key = key; fb.j = j; fb.pos = 16; fb.kc = 0;
+  if (idx >= PERM_LIMIT_8) {
+    uint32_t v = fb.next() & 0x7FFFFFFFu;
+    while (v >= PERM_LIMIT_8) v = fb.next() & 0x7FFFFFFFu;
+    idx = v;
+  }
+  if (w0 >= RHO_WORD_LIMIT) { uint32_t v = fb.next(); while (v >= RHO_WORD_LIMIT) v = fb.next(); w0 = v; }
+  if (w1 >= RHO_WORD_LIMIT) { uint32_t v = fb.next(); while (v >= RHO_WORD_LIMIT) v = fb.next(); w1 = v; }
+  if (w2 >= RHO_WORD_LIMIT) { uint32_t v = fb.next(); while (v >= RHO_WORD_LIMIT) v = fb.next(); w2 = v; }
+}
+
+// Compact tape (24 B): T0 = t | perm index, T1, T2 = mask bytes, reshare words
+// w0 = T3 (part A), w1, w2 = T4, T5 (part B) holding rho_0..7 as base-257 digits.
+template <int R>
+__device__ __forceinline__ void decode_c(uint32_t T0, uint32_t T1, uint32_t T2, uint32_t w0, uint32_t w1,
+                                         uint32_t w2, uint64_t j, const Key& k01, const uint32_t* sA,
+                                         const uint32_t* sB, TapeC& tp) {
   tp.t = T0 >> 31;
   uint32_t idx = T0 & 0x7FFFFFFFu;
-  const uint32_t hz = has_ffff(w3) | has_ffff(w4) | has_ffff(w5) | has_ffff(w6);
-  if (__builtin_expect((hz != 0) | (idx >= PERM_LIMIT_8), 0)) {
-    Draws d;
-    d.idx = idx;
-    d.ur[0] = w3 & 0xFFFFu; d.ur[1] = w3 >> 16; d.ur[2] = w4 & 0xFFFFu; d.ur[3] = w4 >> 16;
-    d.ur[4] = w5 & 0xFFFFu; d.ur[5] = w5 >> 16; d.ur[6] = w6 & 0xFFFFu; d.ur[7] = w6 >> 16;
-    fallback<R>(d, j, k01, 8, PERM_LIMIT_8, 0, 65535u);
-    idx = d.idx;
-    w3 = d.ur[0] | (d.ur[1] << 16); w4 = d.ur[2] | (d.ur[3] << 16);
-    w5 = d.ur[4] | (d.ur[5] << 16); w6 = d.ur[6] | (d.ur[7] << 16);
-  }
+  if (__builtin_expect((idx >= PERM_LIMIT_8) | (w0 >= RHO_WORD_LIMIT) | (w1 >= RHO_WORD_LIMIT) |
+                       (w2 >= RHO_WORD_LIMIT), 0))
+    fallback_c<R>(idx, w0, w1, w2, j, k01);
   const uint32_t hiq = idx / (uint32_t)PERM_A;               // < 2^31 / 336
   tp.selA = sA[idx - hiq * (uint32_t)PERM_A];                // (idx mod 8!) mod 336 = idx mod 336
   tp.selB = sB[hiq % (uint32_t)PERM_B];                      // (idx mod 8!) / 336
-  const uint32_t U[4] = {w3, w4, w5, w6};
+  tp.rb[0] = T1;
+  tp.rb[1] = T2;
+  const uint32_t w[3] = {w0, w1, w2};
 #pragma unroll
-  for (int jj = 0; jj < 4; ++jj) {
-    // r_m - 1 bytes of T1 (slots 0..3) / T2 (slots 4..7) spread into 16-bit lanes
-    const uint32_t rb = __byte_perm(jj < 2 ? T1 : T2, 0u, (jj & 1) ? 0x4342u : 0x4140u);
-    const uint32_t L = U[jj] & 0x00FF00FFu;                  // low bytes l of the u16 draws
-    const uint32_t H = __byte_perm(U[jj], 0u, 0x4341u);      // high bytes h; rho = u mod 257 = l - h mod 257
-    tp.r[jj] = rb + 0x00010001u;
-    tp.a0[jj] = rb + L - H + 0x01020102u;                    // r + rho + 257, in [3, 768]
-    tp.a1[jj] = rb + H - L + 0x01020102u;                    // r - rho + 514, in [3, 768]
+  for (int k = 0; k < 3; ++k) {  // base-257 digits, least significant first
+    const uint32_t q1 = div257(w[k]), q2 = div257(q1);
+    tp.rho[3 * k] = w[k] - 257u * q1;
+    tp.rho[3 * k + 1] = q1 - 257u * q2;
+    if (k < 2) tp.rho[3 * k + 2] = q2 - 257u * div257(q2);
   }
 }
 
@@ -128,27 +134,36 @@ __device__ __forceinline__ void ladder_swar(uint32_t win, uint32_t& lo, uint32_t
   hi = (ce_hi & M) | ((co_hi << 8) & ~M);
 }
 
-// Step 6: both Fisher-Yates phases as PRMT byte gathers.
-__device__ __forceinline__ void shuffle_bytes(uint32_t& lo, uint32_t& hi, uint32_t selA, uint32_t selB) {
-  const uint32_t l1 = __byte_perm(lo, hi, selA), h1 = __byte_perm(lo, hi, selA >> 16);
-  lo = __byte_perm(l1, h1, selB);
-  hi = __byte_perm(l1, h1, selB >> 16);
+// prmt.b32 straight from PTX: our selector nibbles never set the sign-replicate
+// bit, so the masking __byte_perm adds is not needed.
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(s));
+  return d;
 }
 
-__device__ __forceinline__ uint32_t lane16(const uint32_t (&v)[4], int m) {
-  return (m & 1) ? (v[m >> 1] >> 16) : (v[m >> 1] & 0xFFFFu);
+// Step 6: both Fisher-Yates phases as PRMT byte gathers.
+__device__ __forceinline__ void shuffle_bytes(uint32_t& lo, uint32_t& hi, uint32_t selA, uint32_t selB) {
+  const uint32_t aH = __umulhi(selA, 1u << 16), bH = __umulhi(selB, 1u << 16);  // >> 16 on the FMA pipe
+  const uint32_t l1 = prmt(lo, hi, selA), h1 = prmt(lo, hi, aH);
+  lo = prmt(l1, h1, selB);
+  hi = prmt(l1, h1, bH);
 }
+
 __device__ __forceinline__ uint32_t mod257s(uint32_t x) {  // x < 2^18
   return x - 257u * __umulhi(x, 0xFF0100u);
 }
 
-// Steps 7-8 for one party: W_m = (c_m + 1) r_m +- rho_m (mod 257).
+// Steps 7-8 for one party: W_m = (c_m + 1) r_m +- rho_m (mod 257), with
+// r_m = rb_m + 1; the addend carries +257 / +514 so it stays positive.
 template <int PARTY>
 __device__ __forceinline__ void mask_slots(uint32_t lo, uint32_t hi, const TapeC& tp, uint32_t (&W)[8]) {
 #pragma unroll
   for (int m = 0; m < 8; ++m) {
     const uint32_t c = byte_of(m < 4 ? lo : hi, m & 3);
-    W[m] = mod257s(c * lane16(tp.r, m) + lane16(PARTY == 0 ? tp.a0 : tp.a1, m));
+    const uint32_t rb = byte_of(tp.rb[m >> 2], m & 3);
+    const uint32_t add = (PARTY == 0) ? rb + tp.rho[m] + 258u : rb - tp.rho[m] + 515u;
+    W[m] = mod257s(c * (rb + 1u) + add);
   }
 }
 
@@ -165,9 +180,9 @@ __device__ __forceinline__ uint32_t elem_both(uint64_t x0, uint64_t x1, const Ta
   uint32_t vmin = 0xFFFFFFFFu;
 #pragma unroll
   for (int m = 0; m < 8; ++m) {
-    const uint32_t r = lane16(tp.r, m);
-    const uint32_t w0 = mod257s(byte_of(m < 4 ? c_lo : c_hi, m & 3) * r + lane16(tp.a0, m));  // P0's message
-    const uint32_t w1 = mod257s(byte_of(m < 4 ? d_lo : d_hi, m & 3) * r + lane16(tp.a1, m));  // P1's message
+    const uint32_t rb = byte_of(tp.rb[m >> 2], m & 3), r = rb + 1u;
+    const uint32_t w0 = mod257s(byte_of(m < 4 ? c_lo : c_hi, m & 3) * r + (rb + tp.rho[m] + 258u));  // P0's message
+    const uint32_t w1 = mod257s(byte_of(m < 4 ? d_lo : d_hi, m & 3) * r + (rb - tp.rho[m] + 515u));  // P1's message
     if (KEEP_W) { W0[m] = w0; W1[m] = w1; }
     const uint32_t s = w0 + w1;                              // P2: w_m = W0 + W1 (mod 257)
     vmin = min(vmin, s - 257u * (s >> 8));                   // 0 iff s in {0, 257}; s <= 512

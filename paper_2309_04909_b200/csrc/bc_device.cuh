@@ -19,7 +19,8 @@ __host__ __device__ constexpr uint64_t lbl(const char (&s)[9]) {
   for (int i = 7; i >= 0; --i) v = (v << 8) | (uint64_t)(uint8_t)s[i];
   return v;
 }
-constexpr uint64_t L_TAPE = lbl("bc2.tape");   // seed01, 32 B / element (compact)
+constexpr uint64_t L_TAPEA = lbl("bc2.tpa1");  // seed01, 16 B / element (compact tape, part A)
+constexpr uint64_t L_TAPEB = lbl("bc2.tpb1");  // seed01,  8 B / element (compact tape, part B)
 constexpr uint64_t L_TAPEW = lbl("bc2.tapw");  // seed01, 64 B / element (wide)
 constexpr uint64_t L_FB = lbl("bc2.fb01");     // seed01, fallback, counter j*256+k
 constexpr uint64_t L_RESP = lbl("bc2.resp");   // seed02, [DReLU']_0
@@ -30,9 +31,12 @@ constexpr uint64_t L_A12 = lbl("bc2.ta12");    // seed12, [a]_1
 constexpr uint64_t L_B12 = lbl("bc2.tb12");    // seed12, [b]_1
 
 constexpr uint32_t PERM_LIMIT_8 = 53261u * 40320u;  // largest multiple of 8! below 2^31
+constexpr uint32_t RHO_WORD_LIMIT = 253u * 257u * 257u * 257u;  // largest multiple of 257^3 below 2^32
 
 struct Key {
   uint32_t k[8];
+  uint32_t m7;  // = 2^7, read from the kernel parameter bank so ptxas cannot strength-reduce
+                // rotl_fma's multiplies back into ALU shifts (LEA.HI / SHF)
 };
 
 // Kernel-side protocol constants (derived on the host from bc_params).
@@ -53,15 +57,30 @@ struct KP {
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t rotl(uint32_t v, int n) { return __funnelshift_l(v, v, n); }
 
+// rotl on the FMA pipe: (x << n) + (x >> (32-n)) = lo(x * 2^n) + hi(x * 2^n),
+// one IMAD.SHL and one IMAD.HI with addend.  ChaCha is xor/rotate heavy (ALU
+// pipe: LOP3, SHF) and add light (FMA pipe: IMAD.IADD); moving one of the four
+// rotations of each quarter round to the FMA pipe balances the two pipes.
+__device__ __forceinline__ uint32_t rotl_fma(uint32_t v, uint32_t two_n) { return __umulhi(v, two_n) + v * two_n; }
+
+#ifndef BC_ROT_FMA
+#define BC_ROT_FMA 0
+#endif
+#if BC_ROT_FMA
+#define BC_ROT7(b) rotl_fma(b, key.m7)
+#else
+#define BC_ROT7(b) rotl(b, 7)
+#endif
 #define BC_QR(a, b, c, d)          \
   a += b; d ^= a; d = rotl(d, 16); \
   c += d; b ^= c; b = rotl(b, 12); \
   a += b; d ^= a; d = rotl(d, 8);  \
-  c += d; b ^= c; b = rotl(b, 7);
+  c += d; b ^= c; b = BC_ROT7(b);
 
-// Double rounds are kept rolled by default: a full R = 20 unroll is ~1000
+// Double rounds are kept (mostly) rolled: a full R = 20 unroll is ~1000
 // instructions per call site and the fused kernel's call sites then overflow
-// the instruction cache (ncu: "no_instruction" was the top stall).
+// the instruction cache (ncu: "no_instruction" was the top stall).  Two
+// double rounds per iteration remove most loop-carried register moves.
 #ifndef BC_CHACHA_UNROLL
 #define BC_CHACHA_UNROLL 1
 #endif

@@ -94,10 +94,11 @@ __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, c
   store8(a.y1 + i0, y1, cnt);
 }
 
-// Compact tape (p = 257, 8 slots): 4 seed01 blocks per 8-element group, one
-// block per element pair; the pair loop is kept rolled (instruction cache).
-template <int R, bool RELU>
-__global__ void __launch_bounds__(TPB, 2) k_fused_c(FusedArgs a, KP kp, Key k01, Key k02, Key k12) {
+// Compact tape (p = 257, 8 slots): per 8-element group one part-B block
+// (8 B/element) and two part-A blocks (16 B/element, 4 elements each) -- 3
+// ChaCha blocks per 8 elements, none shared between threads.
+template <int R, bool RELU, bool TRANSCRIPT>
+__global__ void __launch_bounds__(TPB, FUSED_MINB) k_fused_c(FusedArgs a, KP kp, Key k01, Key k02, Key k12) {
   __shared__ uint32_t sA[PERM_A], sB[PERM_B];
   build_perm_tables(sA, sB);
   __syncthreads();
@@ -108,33 +109,36 @@ __global__ void __launch_bounds__(TPB, 2) k_fused_c(FusedArgs a, KP kp, Key k01,
     const uint64_t j0 = a.base + i0;
     const uint32_t cnt = (uint32_t)min((uint64_t)8, a.n - i0);
     uint32_t zbits = 0, tbits = 0;
+    uint32_t Bp[16];  // part B: words 2e, 2e+1 of element e (reshare words w1, w2)
+    chacha<R>(k01, j0 >> 3, L_TAPEB, Bp);
 #pragma unroll 1
-    for (int h = 0; h < 4; ++h) {
-      const ulonglong2 v0 = load2(a.x0, i0 + 2 * h, a.n), v1 = load2(a.x1, i0 + 2 * h, a.n);
-      uint32_t B[16];
-      chacha<R>(k01, (j0 >> 1) + (uint64_t)h, L_TAPE, B);
+    for (int hb = 0; hb < 2; ++hb) {
+      const uint64_t ib = i0 + 4 * hb;
+      const ulonglong2 u0 = load2(a.x0, ib, a.n), u1 = load2(a.x1, ib, a.n);
+      const ulonglong2 v0 = load2(a.x0, ib + 2, a.n), v1 = load2(a.x1, ib + 2, a.n);
+      uint32_t A[16];  // part A: words 4q..4q+3 of element 4 hb + q
+      chacha<R>(k01, (j0 >> 2) + (uint64_t)hb, L_TAPEA, A);
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const int e = 2 * h + s;
-        const uint32_t* T = &B[8 * s];
+      for (int q = 0; q < 4; ++q) {
+        const int e = 4 * hb + q;
         TapeC tp;
-        decode_c<R>(T[0], T[1], T[2], T[3], T[4], T[5], T[6], j0 + (uint64_t)e, k01, sA, sB, tp);
-        const uint64_t xa = s ? v0.y : v0.x, xb = s ? v1.y : v1.x;
-        uint32_t W0[8], W1[8], z;
-        if (a.w0lo != nullptr) {  // transcript of the P0/P1 -> P2 messages (uniform branch)
-          z = elem_both<true>(xa, xb, tp, kp.fsh, fhi, W0, W1);
-          if ((uint32_t)e < cnt) {
-            reinterpret_cast<uint64_t*>(a.w0lo)[i0 + e] = pack_lo(W0);
-            reinterpret_cast<uint64_t*>(a.w1lo)[i0 + e] = pack_lo(W1);
-            a.w0hi[i0 + e] = (uint8_t)pack_hi(W0);
-            a.w1hi[i0 + e] = (uint8_t)pack_hi(W1);
-          }
-        } else {
-          z = elem_both<false>(xa, xb, tp, kp.fsh, fhi, W0, W1);
+        decode_c<R>(A[4 * q], A[4 * q + 1], A[4 * q + 2], A[4 * q + 3], Bp[2 * q], Bp[2 * q + 1],
+                    j0 + (uint64_t)e, k01, sA, sB, tp);
+        const uint64_t xa = q == 0 ? u0.x : q == 1 ? u0.y : q == 2 ? v0.x : v0.y;
+        const uint64_t xb = q == 0 ? u1.x : q == 1 ? u1.y : q == 2 ? v1.x : v1.y;
+        uint32_t W0[8], W1[8];
+        const uint32_t z = elem_both<TRANSCRIPT>(xa, xb, tp, kp.fsh, fhi, W0, W1);
+        if (TRANSCRIPT && (uint32_t)e < cnt) {  // the P0/P1 -> P2 messages, wire format
+          reinterpret_cast<uint64_t*>(a.w0lo)[i0 + e] = pack_lo(W0);
+          reinterpret_cast<uint64_t*>(a.w1lo)[i0 + e] = pack_lo(W1);
+          a.w0hi[i0 + e] = (uint8_t)pack_hi(W0);
+          a.w1hi[i0 + e] = (uint8_t)pack_hi(W1);
         }
         zbits |= z << e;
         tbits |= tp.t << e;
       }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) Bp[k] = Bp[k + 8];  // elements 4..7 next
     }
     finish_group<R, RELU>(a, kp, k02, k12, i0, j0, cnt, zbits, tbits);
   }
@@ -201,7 +205,7 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
   return dispatch_rounds(prm->rounds, [&](auto Rc) {
     constexpr int R = decltype(Rc)::value;
     if (prm->compact) {
-      auto fn = k_fused_c<R, RELU>;
+      auto fn = tr ? k_fused_c<R, RELU, true> : k_fused_c<R, RELU, false>;
       fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k01, k02, k12);
     } else {
       auto fn = k_fused_w<R, RELU>;

@@ -104,6 +104,7 @@ KP make_kp(const bc_params* prm) {
 Key make_key(const uint8_t* s) {
   Key k;
   std::memcpy(k.k, s, 32);  // little-endian host: words are the LE u32 of the seed
+  k.m7 = 1u << 7;
   return k;
 }
 

@@ -36,19 +36,21 @@ __global__ void __launch_bounds__(TPB, 2) k_send_c(SendArgs a, KP kp, Key k01, K
     uint64_t lo[8];
     uint32_t tb = 0;
     uint64_t hi = 0;
+    uint32_t Bp[16];
+    chacha<R>(k01, j0 >> 3, L_TAPEB, Bp);
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      const ulonglong2 v = load2(a.x, i0 + 2 * h, a.n);
-      uint32_t B[16];
-      chacha<R>(k01, (j0 >> 1) + (uint64_t)h, L_TAPE, B);
+    for (int hb = 0; hb < 2; ++hb) {
+      const ulonglong2 u = load2(a.x, i0 + 4 * hb, a.n), v = load2(a.x, i0 + 4 * hb + 2, a.n);
+      uint32_t A[16];
+      chacha<R>(k01, (j0 >> 2) + (uint64_t)hb, L_TAPEA, A);
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const int e = 2 * h + s;
-        const uint32_t* T = &B[8 * s];
+      for (int q = 0; q < 4; ++q) {
+        const int e = 4 * hb + q;
         TapeC tp;
-        decode_c<R>(T[0], T[1], T[2], T[3], T[4], T[5], T[6], j0 + (uint64_t)e, k01, sA, sB, tp);
+        decode_c<R>(A[4 * q], A[4 * q + 1], A[4 * q + 2], A[4 * q + 3], Bp[8 * hb + 2 * q], Bp[8 * hb + 2 * q + 1],
+                    j0 + (uint64_t)e, k01, sA, sB, tp);
         uint32_t W[8];
-        elem_one<PARTY>(s ? v.y : v.x, tp, kp.fsh, fhi, W);
+        elem_one<PARTY>(q == 0 ? u.x : q == 1 ? u.y : q == 2 ? v.x : v.y, tp, kp.fsh, fhi, W);
         lo[e] = pack_lo(W);
         hi |= (uint64_t)pack_hi(W) << (8 * e);
         tb |= tp.t << e;

@@ -118,15 +118,12 @@ def test_fused_parity_with_transcript(api, kw, fn):
 
 
 def test_fused_rejection_fallback(api):
-    """Elements whose compact tape rejects (u16 reshare 65535 or perm index
-    >= 53261*8!) take the fallback stream; they must match the oracle too."""
-    from oracle.chacha import element_u32
+    """Elements whose compact tape rejects (a reshare word >= 253*257^3 or a
+    perm index >= 53261*8!) take the fallback stream; they must match the oracle too."""
+    from test_oracle_drelu import _compact_rejects
     kw = PARAMS[0]
     oprm = B.Params(**kw)
-    jj = np.arange(400000, dtype=np.uint64)
-    T = element_u32(SEEDS.s01, B.L_TAPE, oprm.rounds, jj, 8)
-    u = np.ascontiguousarray(T[:, 3:7]).view("<u2").reshape(-1, 8)
-    rej = np.nonzero((u == 65535).any(axis=1) | ((T[:, 0] & 0x7FFFFFFF) >= B.PERM_LIMIT_COMPACT))[0]
+    rej, _, _ = _compact_rejects(oprm, np.arange(400000, dtype=np.uint64))
     assert len(rej) >= 10
     for r in rej[:10]:
         base = int(r) - int(r) % 8

@@ -184,23 +184,46 @@ def test_tape_invariants():
             assert np.bincount(rb.astype(np.int64), minlength=257)[1:].min() > 0
 
 
+def _compact_rejects(prm, j):
+    """Elements whose compact tape has a rejected draw (perm index >= 53261*8!,
+    or a reshare word >= 253*257^3), recomputed from the raw keystream."""
+    from oracle.chacha import element_u32
+    A = element_u32(SEEDS.s01, B.L_TAPEA, prm.rounds, j, 4)
+    Bw = element_u32(SEEDS.s01, B.L_TAPEB, prm.rounds, j, 2)
+    bad = ((A[:, 0] & 0x7FFFFFFF) >= B.PERM_LIMIT_COMPACT) | (A[:, 3] >= B.RHO_WORD_LIMIT) | \
+        (Bw[:, 0] >= B.RHO_WORD_LIMIT) | (Bw[:, 1] >= B.RHO_WORD_LIMIT)
+    return np.nonzero(bad)[0], A, Bw
+
+
 def test_tape_fallback_path():
-    """Find elements whose compact tape rejects (u16 reshare draw = 65535 or
-    permutation index >= 53261*8!) and check the fallback decode stays in range
-    and matches a direct recomputation from the fallback stream."""
-    from oracle.chacha import element_u32, chacha_blocks
+    """Find elements whose compact tape rejects and check the fallback decode:
+    the first rejected reshare word is replaced by the first fallback word
+    below the limit, and its digits are what the decode returns."""
+    from oracle.chacha import chacha_blocks
     prm = B.Params()
-    j = np.arange(200000, dtype=np.uint64)
-    T = element_u32(SEEDS.s01, B.L_TAPE, prm.rounds, j, 8)
-    u = np.ascontiguousarray(T[:, 3:7]).view("<u2").reshape(-1, 8)
-    rej = np.nonzero((u == 65535).any(axis=1) | ((T[:, 0] & 0x7FFFFFFF) >= B.PERM_LIMIT_COMPACT))[0]
+    j = np.arange(40000, dtype=np.uint64)
+    rej, A, Bw = _compact_rejects(prm, j)
     assert len(rej) > 0
     tp = B.tape(prm, SEEDS.s01, j[rej])
-    for row, jj in enumerate(rej[:5]):
-        fb = chacha_blocks(SEEDS.s01, B.L_FALLBACK, [int(jj) * 256], prm.rounds)[0]
-        m = int(np.nonzero(u[jj] == 65535)[0][0]) if (u[jj] == 65535).any() else None
-        if m is not None and (T[jj, 0] & 0x7FFFFFFF) < B.PERM_LIMIT_COMPACT:
-            assert tp["rho"][row, m] == (int(fb[0]) & 0xFFFF) % 257
+    for row, jj in enumerate(rej[:8]):
+        words = [int(A[jj, 3]), int(Bw[jj, 0]), int(Bw[jj, 1])]
+        if (A[jj, 0] & 0x7FFFFFFF) >= B.PERM_LIMIT_COMPACT:
+            continue
+        k = next(i for i, w in enumerate(words) if w >= B.RHO_WORD_LIMIT)
+        fb = [int(w) for w in chacha_blocks(SEEDS.s01, B.L_FALLBACK, [int(jj) * 256], prm.rounds)[0]]
+        v = next(w for w in fb if w < B.RHO_WORD_LIMIT)
+        got = [int(tp["rho"][row, 3 * k + i]) for i in range(3) if 3 * k + i < 8]
+        assert got == [(v // 257 ** i) % 257 for i in range(3)][: len(got)]
+
+
+def test_reshare_digits_uniform():
+    """The base-257 digits of an accepted word are uniform on Z_257 (chi-square)."""
+    tp = B.tape(B.Params(), SEEDS.s01, np.arange(60000, dtype=np.uint64))
+    cnt = np.bincount(tp["rho"].ravel().astype(np.int64), minlength=257)
+    assert cnt.size == 257
+    exp = tp["rho"].size / 257
+    chi2 = float(((cnt - exp) ** 2 / exp).sum())
+    assert chi2 < 256 + 6 * math.sqrt(2 * 256)
 
 
 def test_mask_and_shuffle_preserve_zero_existence():
