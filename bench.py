@@ -37,8 +37,10 @@ import numpy as np  # noqa: E402
 N_PER_GPU = 1 << 24
 ELL, LX, F, MODE, ROUNDS = 64, 7, 24, "guard", 20
 METRIC = "DReLU & ReLU elements/s at ell=64 on 1/2/4/8 B200; % of HBM roofline"
-CHACHA_OPS_PER_BLOCK = {20: 976, 12: 592, 8: 400}   # R*4*12 word ops + 16 feed-forward adds
-BLOCKS_PER_ELEM = {"drelu": 0.625, "relu": 1.125}
+# ALU-pipe work of the PRG, the part of the path that cannot leave the ALU pipe:
+# per ChaCha_R block R/2 double rounds x 8 quarter rounds x (4 xor + 4 rotate).
+CHACHA_ALU_OPS_PER_BLOCK = {20: 640, 12: 384, 8: 256}
+BLOCKS_PER_ELEM = {"drelu": 0.5, "relu": 1.0}   # 3/8 (tape) + 1/8 (resp) or + 5/8 (triples)
 BYTES_PER_ELEM = {"drelu": 32, "relu": 32, "ladder": 16}  # algorithmic HBM bytes per element
 SM_COUNT_B200 = 148
 
@@ -289,7 +291,8 @@ def run_cuda(a):
     peaks = load_peaks()
     traffic = load_traffic()
     clk_mhz = peaks["sm_max_mhz"]
-    alu_peak = SM_COUNT_B200 * 4 * 32 * clk_mhz * 1e6 / 1e12  # Tops/s: 1 warp-instr/clk/SMSP
+    # ALU pipe (LOP3/SHF/PRMT/IADD3): 1 warp instruction per 2 clk per SMSP = 16 lanes/clk/SMSP
+    alu_peak = SM_COUNT_B200 * 4 * 16 * clk_mhz * 1e6 / 1e12  # Tops/s
 
     def roofline(kind, elems_per_s, launch_ms):
         bytes_ = BYTES_PER_ELEM[kind]
@@ -297,10 +300,12 @@ def run_cuda(a):
         out = {"hbm": {"achieved": hbm_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                        "frac": hbm_gbs / peaks["hbm_gbs"], "bytes_per_elem": bytes_}}
         if kind in BLOCKS_PER_ELEM:
-            ops = BLOCKS_PER_ELEM[kind] * CHACHA_OPS_PER_BLOCK[a.rounds]
+            ops = BLOCKS_PER_ELEM[kind] * CHACHA_ALU_OPS_PER_BLOCK[a.rounds]
             ach = elems_per_s / max(world, 1) * ops / 1e12
             out.update({"bound": "alu", "achieved": ach, "peak": alu_peak, "unit": "Tops/s", "frac": ach / alu_peak,
-                        "ops_per_elem": ops, "peak_note": f"148 SM x 4 SMSP x 32 lanes x 1 instr/clk x {clk_mhz:.0f} MHz ({peaks['src']} sm_max)"})
+                        "ops_per_elem": ops,
+                        "ops_note": "ChaCha xor+rotate word ops (ALU pipe) per element; protocol ops not counted",
+                        "peak_note": f"ALU pipe: 148 SM x 4 SMSP x 16 lanes/clk x {clk_mhz:.0f} MHz ({peaks['src']} sm_max)"})
         else:
             out.update({"bound": "hbm", "achieved": hbm_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                         "frac": hbm_gbs / peaks["hbm_gbs"]})

@@ -1,0 +1,192 @@
+"""Party-separated execution of Alg 7 / Alg 8: P0, P1, P2 in separate processes
+(one GPU each), messages over torch.distributed point-to-point (NCCL over
+NVLink on a GPU box).
+
+Roles: in a world of 3k ranks, rank r plays party r % 3 of triple r // 3; each
+triple owns its own element range (global index offset = triple * n), so k
+triples shard the batch with no cross-triple traffic.
+
+Messages per element (guard mode), Alg 7 / Alg 8:
+
+    DReLU  P0 -> P2  lo 8 B + hi 1 B          P1 -> P2  lo 8 B + hi 1 B
+           P2 -> P1  [D']_1 8 B               (P2 -> P0 [D']_0 8 B only if paper_literal;
+                                               otherwise P0 derives it from seed02, reading C12)
+    ReLU   P0 -> P2, P1 -> P2 as above        P0 <-> P1  [d]_b 8 B each way
+           P2 -> P0, P1  e 8 B                P2 -> P1  [c]_1 8 B (preprocessing, reading C20)
+
+The batch is processed in chunks; chunk k's local compute is issued while
+chunk k-1's messages are in flight (async isend/irecv; with NCCL the waits are
+stream-ordered, the host does not block).
+
+`compute` is the phase implementation: by default the CUDA kernels of
+`api` (bc_*_send/helper/finish).  Tests substitute a CPU implementation to
+exercise this transport logic with the gloo backend on machines without GPUs.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from . import api
+
+
+@dataclass
+class Role:
+    party: int      # 0, 1 (computing parties) or 2 (helper)
+    triple: int     # which P0/P1/P2 triple this rank belongs to
+    peers: tuple    # global ranks of (P0, P1, P2) of this triple
+
+    @staticmethod
+    def of(rank: int) -> "Role":
+        t = rank // 3
+        return Role(rank % 3, t, (3 * t, 3 * t + 1, 3 * t + 2))
+
+
+class CudaCompute:
+    """The product phase implementation: libbicoptor kernels on this rank's GPU."""
+
+    def __init__(self, device):
+        self.device = torch.device(device)
+        api.lib()
+
+    def empty(self, shape, dtype):
+        return torch.empty(shape, dtype=dtype, device=self.device)
+
+    drelu_send = staticmethod(api.drelu_send)
+    drelu_helper = staticmethod(api.drelu_helper)
+    drelu_finish = staticmethod(api.drelu_finish)
+    relu_send = staticmethod(api.relu_send)
+    relu_helper = staticmethod(api.relu_helper)
+    relu_finish = staticmethod(api.relu_finish)
+
+
+def _chunks(n: int, chunk: int):
+    chunk = max(8, (chunk // 8) * 8)  # chunk offsets stay multiples of 8 (elem_base rule)
+    return [(a, min(n, a + chunk)) for a in range(0, n, chunk)]
+
+
+class PartyRunner:
+    """Runs DReLU / ReLU for this rank's role over a batch of n elements."""
+
+    def __init__(self, prm: api.Params, seeds, n: int, chunk: int = 1 << 22, compute=None,
+                 group=None, paper_literal: bool = False, base: int | None = None):
+        self.rank = dist.get_rank()
+        self.role = Role.of(self.rank)
+        self.prm = prm
+        self.n = n
+        self.chunks = _chunks(n, chunk)
+        self.c = compute
+        self.group = group
+        self.paper_literal = paper_literal
+        self.base = self.role.triple * n if base is None else base
+        self.hi_needed = prm.c().p > 256
+        # seeds this party holds: P0 {01, 02}, P1 {01, 12}, P2 {02, 12}
+        held = {0: ("s01", "s02"), 1: ("s01", "s12"), 2: ("s02", "s12")}[self.role.party]
+        self.seed = {k: getattr(seeds, k) for k in held}
+        self.bytes_sent = 0
+
+    # -- messaging helpers ---------------------------------------------------------
+    def _isend(self, t, dst):
+        self.bytes_sent += t.numel() * t.element_size()
+        return dist.isend(t, self.role.peers[dst], group=self.group)
+
+    def _irecv(self, t, src):
+        return dist.irecv(t, self.role.peers[src], group=self.group)
+
+    @staticmethod
+    def _wait(works):
+        for w in works:
+            w.wait()
+
+    # -- DReLU (Alg 7) -----------------------------------------------------------------
+    def drelu(self, x=None):
+        """P0/P1: x is this party's share vector; returns its DReLU share.  P2: x=None, returns None."""
+        p, c = self.role.party, self.c
+        out = c.empty(self.n, torch.int64) if p < 2 else None
+        pending = []  # (chunk, state, works) whose round-2 messages are outstanding
+        for (a, b) in self.chunks:
+            m, base = b - a, self.base + a
+            if p < 2:
+                lo, hi, tb = c.drelu_send(p, x[a:b], self.prm, self.seed["s01"], base)   # steps 1-8
+                works = [self._isend(lo, 2)] + ([self._isend(hi, 2)] if self.hi_needed else [])
+                resp = None
+                if p == 1 or self.paper_literal:
+                    resp = c.empty(m, torch.int64)
+                    works.append(self._irecv(resp, 2))                                   # round 2
+                pending.append(((a, b), (tb, resp), works))
+            else:
+                lo0, lo1 = c.empty((m, 8), torch.uint8), c.empty((m, 8), torch.uint8)
+                hi0 = c.empty(m, torch.uint8) if self.hi_needed else None
+                hi1 = c.empty(m, torch.uint8) if self.hi_needed else None
+                rw = [self._irecv(lo0, 0), self._irecv(lo1, 1)]
+                if self.hi_needed:
+                    rw += [self._irecv(hi0, 0), self._irecv(hi1, 1)]
+                self._wait(rw)
+                r0, r1 = c.drelu_helper(lo0, hi0, lo1, hi1, self.prm, self.seed["s02"], base,
+                                        paper_literal=self.paper_literal)                 # steps 9-10
+                works = [self._isend(r1, 1)] + ([self._isend(r0, 0)] if self.paper_literal else [])
+                pending.append(((a, b), None, works))
+            if len(pending) > 1:
+                self._drelu_finish(*pending.pop(0), out)
+        while pending:
+            self._drelu_finish(*pending.pop(0), out)
+        return out
+
+    def _drelu_finish(self, rng, state, works, out):
+        self._wait(works)
+        if state is None:
+            return
+        (a, b), (tb, resp) = rng, state
+        seed02 = self.seed.get("s02") if resp is None else None
+        self.c.drelu_finish(self.role.party, tb, resp, self.prm, b - a, seed02, self.base + a, out=out[a:b])  # step 11
+
+    # -- ReLU (Alg 8) ------------------------------------------------------------------
+    def relu(self, x=None, with_c1: bool = True):
+        p, c = self.role.party, self.c
+        out = c.empty(self.n, torch.int64) if p < 2 else None
+        pending = []
+        for (a, b) in self.chunks:
+            m, base = b - a, self.base + a
+            if p < 2:
+                seed_tr = self.seed["s02"] if p == 0 else self.seed["s12"]
+                lo, hi, tb, d_own = c.relu_send(p, x[a:b], self.prm, self.seed["s01"], seed_tr, base)  # steps 1, 4
+                d_peer = c.empty(m, torch.int64)
+                e = c.empty(m, torch.int64)
+                c1 = c.empty(m, torch.int64) if p == 1 else None
+                works = [self._isend(lo, 2)] + ([self._isend(hi, 2)] if self.hi_needed else [])
+                # P0 <-> P1 open d = x - a; order the pair to avoid head-of-line deadlock on gloo
+                if p == 0:
+                    works += [self._isend(d_own, 1), self._irecv(d_peer, 1)]
+                else:
+                    works += [self._irecv(d_peer, 0), self._isend(d_own, 0)]
+                works.append(self._irecv(e, 2))
+                if p == 1:
+                    works.append(self._irecv(c1, 2))
+                pending.append(((a, b), (x[a:b], tb, d_own, d_peer, e, c1, seed_tr), works))
+            else:
+                lo0, lo1 = c.empty((m, 8), torch.uint8), c.empty((m, 8), torch.uint8)
+                hi0 = c.empty(m, torch.uint8) if self.hi_needed else None
+                hi1 = c.empty(m, torch.uint8) if self.hi_needed else None
+                rw = [self._irecv(lo0, 0), self._irecv(lo1, 1)]
+                if self.hi_needed:
+                    rw += [self._irecv(hi0, 0), self._irecv(hi1, 1)]
+                self._wait(rw)
+                e, c1 = c.relu_helper(lo0, hi0, lo1, hi1, self.prm, self.seed["s02"], self.seed["s12"], base)  # steps 2-3
+                works = [self._isend(e, 0), self._isend(e, 1), self._isend(c1, 1)]
+                pending.append(((a, b), None, works))
+            if len(pending) > 1:
+                self._relu_finish(*pending.pop(0), out)
+        while pending:
+            self._relu_finish(*pending.pop(0), out)
+        return out
+
+    def _relu_finish(self, rng, state, works, out):
+        self._wait(works)
+        if state is None:
+            return
+        (a, b) = rng
+        x, tb, d_own, d_peer, e, c1, seed_tr = state
+        self.c.relu_finish(self.role.party, x, tb, d_own, d_peer, e, c1, self.prm, seed_tr, self.base + a,
+                           out=out[a:b])  # steps 4-5

@@ -1,0 +1,76 @@
+"""Party-separated runtime (paper_2309_04909_b200.party) over torch.distributed
+with the gloo backend on CPU: 3 ranks (one triple) and 6 ranks (two triples),
+chunked, compared with the oracle's three-party functions.  The phase compute
+is the oracle-backed tests/party_cpu_compute.py; the CUDA phase kernels are
+checked separately on a GPU (test_gpu_parity.py)."""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, kind, n, chunk, mode, literal, outdir):
+    sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import synth
+    from paper_2309_04909_b200 import party
+    from paper_2309_04909_b200.api import Params
+    from party_cpu_compute import OracleCompute
+
+    class P(Params):  # the runner asks prm.c() for p; answer without the CUDA library
+        def c(self):
+            from oracle import bicoptor as B
+            o = B.Params(ell=self.ell, lx=self.lx, f=self.f, mode=self.mode, rounds=self.rounds)
+            return type("C", (), {"p": o.p})()
+
+    prm = P(ell=64, lx=7, f=24, mode=mode, rounds=8) if mode == "guard" else P(ell=16, lx=7, f=0, mode=mode, rounds=8)
+    role = party.Role.of(rank)
+    x, x0, x1 = synth.shares(n, prm.ell, prm.lx, prm.f, "D1", run=role.triple)
+    xs = torch.from_numpy((x0 if role.party == 0 else x1).view(np.int64))
+    runner = party.PartyRunner(prm, synth.seeds(0), n, chunk=chunk, compute=OracleCompute(), paper_literal=literal)
+    y = runner.drelu(xs if role.party < 2 else None) if kind == "drelu" else runner.relu(xs if role.party < 2 else None)
+    if y is not None:
+        np.save(os.path.join(outdir, f"y_{rank}.npy"), y.numpy().view(np.uint64))
+    np.save(os.path.join(outdir, f"bytes_{rank}.npy"), np.array([runner.bytes_sent]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind,world,mode,literal", [("drelu", 3, "guard", False), ("drelu", 3, "guard", True),
+                                                      ("relu", 3, "guard", False), ("relu", 6, "guard", False),
+                                                      ("drelu", 3, "literal", False)])
+def test_party_runtime_gloo(tmp_path, kind, world, mode, literal):
+    import synth
+    from oracle import bicoptor as B
+    n, chunk = 300, 128  # 3 chunks, the last one ragged
+    mp.start_processes(_worker, args=(world, _free_port(), kind, n, chunk, mode, literal, str(tmp_path)),
+                       nprocs=world, join=True, start_method="spawn")
+    ell, lx, f = (64, 7, 24) if mode == "guard" else (16, 7, 0)
+    o = B.Params(ell=ell, lx=lx, f=f, mode=mode, rounds=8)
+    for t in range(world // 3):
+        x, x0, x1 = synth.shares(n, ell, lx, f, "D1", run=t)
+        j = np.arange(n, dtype=np.uint64) + np.uint64(t * n)
+        ref = getattr(B, kind)(o, x0, x1, j, synth.seeds(0))
+        assert np.array_equal(np.load(tmp_path / f"y_{3 * t}.npy"), ref["y0"])
+        assert np.array_equal(np.load(tmp_path / f"y_{3 * t + 1}.npy"), ref["y1"])
+    # wire bytes per element: P0 -> P2 (ell_x+1) * ceil(log2 p) bits (Table 1)
+    b0 = int(np.load(tmp_path / "bytes_0.npy")[0])
+    per = 9 if mode == "guard" else 8
+    extra = (0 if kind == "drelu" else 8)  # ReLU: P0 also sends [d]_0 to P1
+    assert b0 == n * (per + extra)
