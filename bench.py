@@ -350,6 +350,8 @@ def run_cuda(a):
                                  "roofline": roofline("ladder", v_l, ms_l),
                                  "note": "one party, 8 B in + 8 B out per element (config 2 primitive)"}
         del v_lad
+        # ---- config 5: E2E-shaped ReLU layer streams (CUDA graph per network) ----
+        line["config5"] = relu_streams(api, prm, seeds, dev, stream, timed, world)
         # ---- e2e through the public API with pinned HOST buffers ----------------
         line["e2e"] = e2e(api, prm, seeds, x0h, x1h, base, dev, world, max_over_ranks, barrier, a)
     if rank == 0 and not a.no_extras:
@@ -359,6 +361,35 @@ def run_cuda(a):
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def relu_streams(api, prm, seeds, dev, stream, timed, world):
+    """BASELINE config 5: each network's ReLU layers at the paper's batch
+    (Table 7), one fused bc_relu per layer, replayed from a CUDA graph.  Inputs
+    are seeded shares generated on the device (torch RNG; input generation is
+    outside the timed region and holds none of the method's arithmetic)."""
+    import torch
+    from paper_2309_04909_b200 import stream as S
+    out = {}
+    g = torch.Generator(device=dev)
+    g.manual_seed(5)
+    for name in S.NETWORKS:
+        st = S.ReluStream(S.layer_sizes(name), prm, seeds, dev)
+        for x0, x1 in zip(st.x0, st.x1):
+            x = (torch.randn(x0.numel(), device=dev, generator=g) * 2 ** 26).round().to(torch.int64)
+            r = torch.randint(-2 ** 63, 2 ** 63 - 1, (x0.numel(),), device=dev, generator=g, dtype=torch.int64)
+            x0.copy_(x + r)   # [x]_0 = x + R, [x]_1 = -R  (int64 wraps mod 2^64)
+            x1.copy_(-r)
+        st.capture()
+        steps = 20
+        t_ms, _, _ = timed(st.replay, steps, 3)
+        ms = t_ms / steps
+        out[name] = {"relus": st.total, "layers": len(st.sizes), "ms_per_forward": ms,
+                     "relu_per_s": world * st.total / (ms * 1e-3), "launches_per_forward": len(st.sizes)}
+        del st
+        torch.cuda.empty_cache()
+    out["note"] = "per GPU, paper batch (Table 7: 240/60/1650); CUDA graph of one bc_relu per layer"
+    return out
 
 
 def e2e(api, prm, seeds, x0h, x1h, base, dev, world, max_over_ranks, barrier, a):

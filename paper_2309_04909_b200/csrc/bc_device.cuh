@@ -63,24 +63,30 @@ __device__ __forceinline__ uint32_t rotl(uint32_t v, int n) { return __funnelshi
 // rotations of each quarter round to the FMA pipe balances the two pipes.
 __device__ __forceinline__ uint32_t rotl_fma(uint32_t v, uint32_t two_n) { return __umulhi(v, two_n) + v * two_n; }
 
+// BC_ROT_FMA = how many of the 8 quarter rounds of a double round take their
+// rotate-by-7 on the FMA pipe (IMAD + IMAD.HI = 3 FMA issue slots, measured:
+// IMAD.HI runs at half rate) instead of the ALU pipe (SHF).  ChaCha is ALU
+// bound (xor + rotate), so moving a few rotates to the idle FMA pipe helps
+// until the FMA pipe saturates (tools/variants.py).
 #ifndef BC_ROT_FMA
 #define BC_ROT_FMA 0
 #endif
-#if BC_ROT_FMA
-#define BC_ROT7(b) rotl_fma(b, key.m7)
-#else
-#define BC_ROT7(b) rotl(b, 7)
-#endif
-#define BC_QR(a, b, c, d)          \
+#define BC_QR_ALU(a, b, c, d)      \
   a += b; d ^= a; d = rotl(d, 16); \
   c += d; b ^= c; b = rotl(b, 12); \
   a += b; d ^= a; d = rotl(d, 8);  \
-  c += d; b ^= c; b = BC_ROT7(b);
+  c += d; b ^= c; b = rotl(b, 7);
+#define BC_QR_FMA(a, b, c, d)      \
+  a += b; d ^= a; d = rotl(d, 16); \
+  c += d; b ^= c; b = rotl(b, 12); \
+  a += b; d ^= a; d = rotl(d, 8);  \
+  c += d; b ^= c; b = rotl_fma(b, key.m7);
+#define BC_QR_SEL(i, a, b, c, d) \
+  if ((i) < BC_ROT_FMA) { BC_QR_FMA(a, b, c, d) } else { BC_QR_ALU(a, b, c, d) }
 
 // Double rounds are kept (mostly) rolled: a full R = 20 unroll is ~1000
 // instructions per call site and the fused kernel's call sites then overflow
-// the instruction cache (ncu: "no_instruction" was the top stall).  Two
-// double rounds per iteration remove most loop-carried register moves.
+// the instruction cache (ncu: "no_instruction" was the top stall).
 #ifndef BC_CHACHA_UNROLL
 #define BC_CHACHA_UNROLL 1
 #endif
@@ -96,8 +102,9 @@ __device__ __forceinline__ void chacha(const Key& key, uint64_t ctr, uint64_t la
   uint32_t x12 = c0, x13 = c1, x14 = l0, x15 = l1;
 #pragma unroll kChachaUnroll
   for (int r = 0; r < R; r += 2) {
-    BC_QR(x0, x4, x8, x12) BC_QR(x1, x5, x9, x13) BC_QR(x2, x6, x10, x14) BC_QR(x3, x7, x11, x15)
-    BC_QR(x0, x5, x10, x15) BC_QR(x1, x6, x11, x12) BC_QR(x2, x7, x8, x13) BC_QR(x3, x4, x9, x14)
+    BC_QR_SEL(0, x0, x4, x8, x12) BC_QR_SEL(2, x1, x5, x9, x13) BC_QR_SEL(4, x2, x6, x10, x14)
+    BC_QR_SEL(6, x3, x7, x11, x15) BC_QR_SEL(1, x0, x5, x10, x15) BC_QR_SEL(3, x1, x6, x11, x12)
+    BC_QR_SEL(5, x2, x7, x8, x13) BC_QR_SEL(7, x3, x4, x9, x14)
   }
   o[0] = x0 + 0x61707865u; o[1] = x1 + 0x3320646eu; o[2] = x2 + 0x79622d32u; o[3] = x3 + 0x6b206574u;
   o[4] = x4 + key.k[0]; o[5] = x5 + key.k[1]; o[6] = x6 + key.k[2]; o[7] = x7 + key.k[3];

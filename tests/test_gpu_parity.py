@@ -281,3 +281,36 @@ def test_abi_errors(api):
         api.drelu(torch.zeros(8, dtype=torch.int64), torch.zeros(8, dtype=torch.int64), prm, SEEDS)
     y0, y1 = api.drelu(x[:0], x[16:16], prm, SEEDS)                # n = 0 is a no-op
     assert y0.numel() == 0
+
+
+# ---- config 5: E2E-shaped ReLU layer stream (CUDA graph) ---------------------------
+
+def test_relu_stream_graph_matches_eager_and_oracle(api):
+    """The CIFAR10_VGG16 ReLU layer sequence at batch 2: the captured CUDA graph
+    equals eager launches bit for bit, and sampled outputs of every layer match
+    the oracle at that layer's global index range."""
+    from paper_2309_04909_b200 import stream as S
+    kw = PARAMS[0]
+    prm = api.Params(**kw)
+    st = S.ReluStream(S.layer_sizes("CIFAR10_VGG16", batch=2), prm, SEEDS, DEV, base=1 << 32)
+    rng = np.random.default_rng(9)
+    xs = []
+    for i, n in enumerate(st.sizes):
+        x, x0, x1 = synth.shares(n, 64, 7, 24, "D2", run=i)
+        st.x0[i].copy_(dev(x0))
+        st.x1[i].copy_(dev(x1))
+        xs.append((x, x0, x1))
+    st.run_eager()
+    eager = [(y0.clone(), y1.clone()) for y0, y1 in zip(st.y0, st.y1)]
+    for y in st.y0 + st.y1:
+        y.zero_()
+    st.capture()
+    st.replay()
+    torch.cuda.synchronize()
+    oprm = B.Params(**kw)
+    for i, n in enumerate(st.sizes):
+        assert torch.equal(st.y0[i], eager[i][0]) and torch.equal(st.y1[i], eager[i][1])
+        idx = np.sort(rng.choice(n, min(n, 512), replace=False))
+        x, x0, x1 = xs[i]
+        ref = B.relu(oprm, x0[idx], x1[idx], idx.astype(np.uint64) + np.uint64(st.bases[i]), SEEDS)
+        assert np.array_equal(host(st.y0[i])[idx], ref["y0"]) and np.array_equal(host(st.y1[i])[idx], ref["y1"])

@@ -1,0 +1,90 @@
+// intpipe_bench.cu -- measured integer-pipe throughput on this GPU.
+//
+// Each kernel runs 8 independent dependency chains per thread of one SASS
+// instruction class, at full occupancy, and reports thread-ops per second.
+// The results set the ALU roofline denominators used in DESIGN.md / bench.py.
+//
+//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o intpipe_bench tools/intpipe_bench.cu
+//   ./intpipe_bench            -> one JSON line
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+constexpr int ITERS = 4096;
+constexpr int CH = 8;
+
+#define BODY(OP)                                                      \
+  uint32_t v[CH];                                                     \
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) v[c] = seed + c * 0x9E3779B9u + threadIdx.x; \
+  for (int i = 0; i < ITERS; ++i) {                                   \
+    _Pragma("unroll") for (int c = 0; c < CH; ++c) { OP; }            \
+  }                                                                   \
+  uint32_t acc = 0;                                                   \
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) acc ^= v[c];         \
+  if (acc == 0x12345678u) out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+
+__global__ void k_lop3(uint32_t* out, uint32_t seed, uint32_t k) {
+  BODY(asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(v[c]) : "r"(k), "r"(seed)))
+}
+__global__ void k_shf(uint32_t* out, uint32_t seed, uint32_t k) {
+  BODY(asm volatile("shf.l.wrap.b32 %0, %0, %0, 7;" : "+r"(v[c])))
+}
+__global__ void k_prmt(uint32_t* out, uint32_t seed, uint32_t k) {
+  BODY(asm volatile("prmt.b32 %0, %0, %1, 0x2103;" : "+r"(v[c]) : "r"(k)))
+}
+__global__ void k_iadd3(uint32_t* out, uint32_t seed, uint32_t k) {
+  BODY(asm volatile("add.u32 %0, %0, %1;" : "+r"(v[c]) : "r"(k)))
+}
+__global__ void k_imad(uint32_t* out, uint32_t seed, uint32_t k) {
+  BODY(asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(v[c]) : "r"(k), "r"(seed)))
+}
+__global__ void k_imadhi(uint32_t* out, uint32_t seed, uint32_t k) {
+  BODY(asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(v[c]) : "r"(k), "r"(seed)))
+}
+__global__ void k_mix_chacha(uint32_t* out, uint32_t seed, uint32_t k) {
+  // ChaCha-like: xor (LOP3), rotate (SHF), add (IMAD.IADD) in the 1:1:1 ratio
+  BODY({
+    asm volatile("add.u32 %0, %0, %1;" : "+r"(v[c]) : "r"(k));
+    asm volatile("xor.b32 %0, %0, %1;" : "+r"(v[c]) : "r"(seed));
+    asm volatile("shf.l.wrap.b32 %0, %0, %0, 12;" : "+r"(v[c]));
+  })
+}
+
+template <typename K>
+double rate(K kern, int ops_per_iter, int blocks, int threads) {
+  uint32_t* out;
+  cudaMalloc(&out, (size_t)blocks * threads * 4);
+  kern<<<blocks, threads>>>(out, 1u, 3u);
+  cudaDeviceSynchronize();
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  const int reps = 5;
+  for (int r = 0; r < reps; ++r) kern<<<blocks, threads>>>(out, 1u + r, 3u);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaFree(out);
+  const double ops = (double)reps * blocks * threads * ITERS * CH * ops_per_iter;
+  return ops / (ms * 1e-3) / 1e12;
+}
+
+int main() {
+  int dev = 0, sms = 0, clk = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
+  const int threads = 256, blocks = sms * 8;
+  printf("{\"sms\": %d, \"clock_khz_attr\": %d", sms, clk);
+  printf(", \"lop3_tops\": %.3f", rate(k_lop3, 1, blocks, threads));
+  printf(", \"shf_tops\": %.3f", rate(k_shf, 1, blocks, threads));
+  printf(", \"prmt_tops\": %.3f", rate(k_prmt, 1, blocks, threads));
+  printf(", \"iadd_tops\": %.3f", rate(k_iadd3, 1, blocks, threads));
+  printf(", \"imad_tops\": %.3f", rate(k_imad, 1, blocks, threads));
+  printf(", \"imad_hi_tops\": %.3f", rate(k_imadhi, 1, blocks, threads));
+  printf(", \"chacha_mix_tops\": %.3f", rate(k_mix_chacha, 3, blocks, threads));
+  printf("}\n");
+  return 0;
+}
