@@ -55,6 +55,10 @@ def parse():
     ap.add_argument("--rounds", type=int, default=ROUNDS)
     ap.add_argument("--no-extras", action="store_true", help="skip ReLU / ladder / variants / e2e / cpu legs")
     ap.add_argument("--only", choices=["drelu", "relu", "ladder"], help="profiling aid: launch one op steps+warmup times, print nothing")
+    ap.add_argument("--mode", default="sharded", choices=["sharded", "party"],
+                    help="party: config 4, P0/P1/P2 on distinct GPUs (needs >= 3 ranks), ReLU over NCCL P2P")
+    ap.add_argument("--party-n", type=int, default=1 << 26, help="elements per P0/P1/P2 triple (config 4)")
+    ap.add_argument("--chunk", type=int, default=1 << 22, help="party mode: elements per pipelined chunk")
     return ap.parse_args()
 
 
@@ -418,9 +422,80 @@ def e2e(api, prm, seeds, x0h, x1h, base, dev, world, max_over_ranks, barrier, a)
             "note": "api host pipeline: pinned x0,x1 -> HBM -> fused DReLU -> pinned y0,y1, wall clock, max over ranks"}
 
 
+def run_party(a):
+    """BASELINE config 4: ReLU with P0, P1, P2 on distinct GPUs, messages as NCCL
+    point-to-point over NVLink (paper_2309_04909_b200.party).  World = 3k ranks
+    (extra ranks idle); each triple owns party-n elements."""
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2309_04909_b200 import api, party
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world < 3:
+        if rank == 0:
+            print(json.dumps({"metric": "config4 party-separated ReLU elements/s", "mode": "party",
+                              "unavailable": f"needs >= 3 GPUs (one per party), have {world}"}))
+        return
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    k = world // 3
+    group = dist.new_group(list(range(3 * k)))
+    n = a.party_n
+    prm = api.Params(ell=ELL, lx=LX, f=F, mode=MODE, rounds=a.rounds)
+    seeds = synth.seeds(0)
+    t_ms, bytes_sent = 0.0, 0
+    if rank < 3 * k:
+        role = party.Role.of(rank)
+        xs = None
+        if role.party < 2:
+            x = synth.plaintext(n, ELL, LX, F, "D2", run=role.triple)
+            x0, x1 = synth.share(x, ELL, run=role.triple)
+            xs = torch.from_numpy((x0 if role.party == 0 else x1).view(np.int64)).to(dev)
+        runner = party.PartyRunner(prm, seeds, n, chunk=a.chunk, compute=party.CudaCompute(dev), group=group)
+        for _ in range(max(a.warmup, 2)):
+            runner.relu(xs)
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=group)
+        runner.bytes_sent = 0
+        steps = max(1, min(a.steps, 20))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            runner.relu(xs)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=group)
+        t_ms = e0.elapsed_time(e1) / steps
+        bytes_sent = runner.bytes_sent / steps
+    t = torch.tensor([t_ms, bytes_sent], dtype=torch.float64, device=dev)
+    tm = t.clone()
+    dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    per_rank = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in range(world)]
+    dist.all_gather(per_rank, t)
+    if rank == 0:
+        ms = float(tm[0])
+        egress = {f"P{p}": float(per_rank[p][1]) / n for p in range(3)}
+        print(json.dumps({
+            "metric": "config4 party-separated ReLU elements/s (P0,P1,P2 on distinct GPUs, NCCL P2P)",
+            "mode": "party", "value": k * n / (ms * 1e-3), "unit": "elements/s", "n_gpus": world, "triples": k,
+            "ms_per_step": ms, "steps": steps, "chunk": a.chunk, "higher_is_better": True, "dtype": "u64",
+            "config": {"workload": f"config4: ReLU ell={ELL} lx={LX} f={F} {MODE} ChaCha{a.rounds}, 2^{int(math.log2(n))} elements per triple"},
+            "wire_bytes_per_elem": egress,
+            "paper_one_pass_bits": 64, "guard_one_pass_bits": 72,
+            "p2_egress_GBs": float(per_rank[2][1]) / (ms * 1e-3) / 1e9}))
+    dist.destroy_process_group()
+
+
 if __name__ == "__main__":
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.mode == "party":
+        run_party(args)
     else:
         run_cuda(args)

@@ -14,9 +14,10 @@ Messages per element (guard mode), Alg 7 / Alg 8:
     ReLU   P0 -> P2, P1 -> P2 as above        P0 <-> P1  [d]_b 8 B each way
            P2 -> P0, P1  e 8 B                P2 -> P1  [c]_1 8 B (preprocessing, reading C20)
 
-The batch is processed in chunks; chunk k's local compute is issued while
-chunk k-1's messages are in flight (async isend/irecv; with NCCL the waits are
-stream-ordered, the host does not block).
+The batch is processed in chunks.  Each protocol round of a chunk is one
+batch_isend_irecv group; the round-2 receives of chunk k stay in flight while
+chunk k+1's local phase runs (with NCCL the waits are stream-ordered, the host
+does not block).
 
 `compute` is the phase implementation: by default the CUDA kernels of
 `api` (bc_*_send/helper/finish).  Tests substitute a CPU implementation to
@@ -88,12 +89,19 @@ class PartyRunner:
         self.bytes_sent = 0
 
     # -- messaging helpers ---------------------------------------------------------
-    def _isend(self, t, dst):
+    # Each protocol round of a chunk is posted as one batch_isend_irecv group
+    # (one NCCL group call on GPUs), so the order in which the three parties
+    # post their sends and receives cannot deadlock.
+    def _send(self, t, dst):
         self.bytes_sent += t.numel() * t.element_size()
-        return dist.isend(t, self.role.peers[dst], group=self.group)
+        return dist.P2POp(dist.isend, t, self.role.peers[dst], group=self.group)
 
-    def _irecv(self, t, src):
-        return dist.irecv(t, self.role.peers[src], group=self.group)
+    def _recv(self, t, src):
+        return dist.P2POp(dist.irecv, t, self.role.peers[src], group=self.group)
+
+    @staticmethod
+    def _post(ops):
+        return dist.batch_isend_irecv(ops) if ops else []
 
     @staticmethod
     def _wait(works):
@@ -110,24 +118,25 @@ class PartyRunner:
             m, base = b - a, self.base + a
             if p < 2:
                 lo, hi, tb = c.drelu_send(p, x[a:b], self.prm, self.seed["s01"], base)   # steps 1-8
-                works = [self._isend(lo, 2)] + ([self._isend(hi, 2)] if self.hi_needed else [])
+                ops = [self._send(lo, 2)] + ([self._send(hi, 2)] if self.hi_needed else [])
+                works = self._post(ops)                                                  # round 1
                 resp = None
                 if p == 1 or self.paper_literal:
                     resp = c.empty(m, torch.int64)
-                    works.append(self._irecv(resp, 2))                                   # round 2
+                    works += self._post([self._recv(resp, 2)])                           # round 2
                 pending.append(((a, b), (tb, resp), works))
             else:
                 lo0, lo1 = c.empty((m, 8), torch.uint8), c.empty((m, 8), torch.uint8)
                 hi0 = c.empty(m, torch.uint8) if self.hi_needed else None
                 hi1 = c.empty(m, torch.uint8) if self.hi_needed else None
-                rw = [self._irecv(lo0, 0), self._irecv(lo1, 1)]
+                ops = [self._recv(lo0, 0), self._recv(lo1, 1)]
                 if self.hi_needed:
-                    rw += [self._irecv(hi0, 0), self._irecv(hi1, 1)]
-                self._wait(rw)
+                    ops += [self._recv(hi0, 0), self._recv(hi1, 1)]
+                self._wait(self._post(ops))
                 r0, r1 = c.drelu_helper(lo0, hi0, lo1, hi1, self.prm, self.seed["s02"], base,
                                         paper_literal=self.paper_literal)                 # steps 9-10
-                works = [self._isend(r1, 1)] + ([self._isend(r0, 0)] if self.paper_literal else [])
-                pending.append(((a, b), None, works))
+                ops = [self._send(r1, 1)] + ([self._send(r0, 0)] if self.paper_literal else [])
+                pending.append(((a, b), None, self._post(ops)))
             if len(pending) > 1:
                 self._drelu_finish(*pending.pop(0), out)
         while pending:
@@ -155,27 +164,23 @@ class PartyRunner:
                 d_peer = c.empty(m, torch.int64)
                 e = c.empty(m, torch.int64)
                 c1 = c.empty(m, torch.int64) if p == 1 else None
-                works = [self._isend(lo, 2)] + ([self._isend(hi, 2)] if self.hi_needed else [])
-                # P0 <-> P1 open d = x - a; order the pair to avoid head-of-line deadlock on gloo
-                if p == 0:
-                    works += [self._isend(d_own, 1), self._irecv(d_peer, 1)]
-                else:
-                    works += [self._irecv(d_peer, 0), self._isend(d_own, 0)]
-                works.append(self._irecv(e, 2))
-                if p == 1:
-                    works.append(self._irecv(c1, 2))
+                # round 1: the message to P2 and the opening of d between P0 and P1
+                ops = [self._send(lo, 2)] + ([self._send(hi, 2)] if self.hi_needed else [])
+                ops += [self._send(d_own, 1 - p), self._recv(d_peer, 1 - p)]
+                works = self._post(ops)
+                # round 2: e (and [c]_1 for P1) from P2
+                works += self._post([self._recv(e, 2)] + ([self._recv(c1, 2)] if p == 1 else []))
                 pending.append(((a, b), (x[a:b], tb, d_own, d_peer, e, c1, seed_tr), works))
             else:
                 lo0, lo1 = c.empty((m, 8), torch.uint8), c.empty((m, 8), torch.uint8)
                 hi0 = c.empty(m, torch.uint8) if self.hi_needed else None
                 hi1 = c.empty(m, torch.uint8) if self.hi_needed else None
-                rw = [self._irecv(lo0, 0), self._irecv(lo1, 1)]
+                ops = [self._recv(lo0, 0), self._recv(lo1, 1)]
                 if self.hi_needed:
-                    rw += [self._irecv(hi0, 0), self._irecv(hi1, 1)]
-                self._wait(rw)
+                    ops += [self._recv(hi0, 0), self._recv(hi1, 1)]
+                self._wait(self._post(ops))
                 e, c1 = c.relu_helper(lo0, hi0, lo1, hi1, self.prm, self.seed["s02"], self.seed["s12"], base)  # steps 2-3
-                works = [self._isend(e, 0), self._isend(e, 1), self._isend(c1, 1)]
-                pending.append(((a, b), None, works))
+                pending.append(((a, b), None, self._post([self._send(e, 0), self._send(e, 1), self._send(c1, 1)])))
             if len(pending) > 1:
                 self._relu_finish(*pending.pop(0), out)
         while pending:

@@ -1,0 +1,35 @@
+"""Sweep the host-buffer pipeline (streams x chunks) and raw PCIe copy rates."""
+import os, sys, time, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import synth
+from paper_2309_04909_b200 import api, host as H
+n = 1 << 24
+dev = torch.device("cuda:0")
+x, x0h, x1h = synth.shares(n, 64, 7, 24, "D2")
+hx0 = torch.from_numpy(x0h.view(np.int64)).pin_memory(); hx1 = torch.from_numpy(x1h.view(np.int64)).pin_memory()
+hy0 = torch.empty(n, dtype=torch.int64).pin_memory(); hy1 = torch.empty(n, dtype=torch.int64).pin_memory()
+d = torch.empty(n, dtype=torch.int64, device=dev)
+out = {}
+def bw(fn, nbytes, reps=10):
+    fn(); torch.cuda.synchronize(); t = time.perf_counter()
+    for _ in range(reps): fn()
+    torch.cuda.synchronize(); return nbytes * reps / (time.perf_counter() - t) / 1e9
+out["h2d_GBs"] = bw(lambda: d.copy_(hx0, non_blocking=True), 8 * n)
+out["d2h_GBs"] = bw(lambda: hy0.copy_(d, non_blocking=True), 8 * n)
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+d2 = torch.empty_like(d)
+def both():
+    with torch.cuda.stream(s1): d.copy_(hx0, non_blocking=True)
+    with torch.cuda.stream(s2): hy0.copy_(d2, non_blocking=True)
+out["bidir_GBs_each"] = bw(both, 8 * n)
+prm, sd = api.Params(), synth.seeds(0)
+for streams in (2, 3, 4):
+    for chunks in (8, 16, 32):
+        ex = H.HostPipeline(n, dev, chunks=chunks, streams=streams)
+        for _ in range(2): ex.drelu(hx0, hx1, hy0, hy1, prm, sd)
+        torch.cuda.synchronize(); t = time.perf_counter()
+        for _ in range(10): ex.drelu(hx0, hx1, hy0, hy1, prm, sd)
+        torch.cuda.synchronize(); dt = (time.perf_counter() - t) / 10
+        out[f"s{streams}_c{chunks}"] = n / dt / 1e9
+print(json.dumps(out))
