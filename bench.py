@@ -354,6 +354,8 @@ def run_cuda(a):
                                  "roofline": roofline("ladder", v_l, ms_l),
                                  "note": "one party, 8 B in + 8 B out per element (config 2 primitive)"}
         del v_lad
+        # ---- every party's work unshared: the party-phase kernels chained on 1 GPU ----
+        line["party_chain_1gpu"] = party_chain(api, prm, seeds, x0, x1, base, dev, stream, timed, world, n)
         # ---- config 5: E2E-shaped ReLU layer streams (CUDA graph per network) ----
         line["config5"] = relu_streams(api, prm, seeds, dev, stream, timed, world)
         # ---- e2e through the public API with pinned HOST buffers ----------------
@@ -365,6 +367,41 @@ def run_cuda(a):
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def party_chain(api, prm, seeds, x0, x1, base, dev, stream, timed, world, n):
+    """The fused kernel expands seed01 once for both simulated computing parties.
+    In a deployment each party expands its own seeds; this leg runs the party
+    kernels back to back on one GPU (P0 send, P1 send, P2 helper, P0 finish, P1
+    finish), i.e. every party's PRG and arithmetic, no sharing."""
+    import torch
+    lo0, hi0, tb0 = api.msg_buffers(n, dev)
+    lo1, hi1, tb1 = api.msg_buffers(n, dev)
+    r1 = torch.empty(n, dtype=torch.int64, device=dev)
+    ya, yb = torch.empty_like(r1), torch.empty_like(r1)
+    d0, d1, e, c1 = (torch.empty_like(r1) for _ in range(4))
+
+    def drelu_chain():
+        api.drelu_send(0, x0, prm, seeds.s01, base, out=(lo0, hi0, tb0), stream=stream)
+        api.drelu_send(1, x1, prm, seeds.s01, base, out=(lo1, hi1, tb1), stream=stream)
+        api.drelu_helper(lo0, hi0, lo1, hi1, prm, seeds.s02, base, out=(None, r1), stream=stream)
+        api.drelu_finish(0, tb0, None, prm, n, seeds.s02, base, out=ya, stream=stream)
+        api.drelu_finish(1, tb1, r1, prm, n, None, base, out=yb, stream=stream)
+
+    def relu_chain():
+        api.relu_send(0, x0, prm, seeds.s01, seeds.s02, base, out=(lo0, hi0, tb0, d0), stream=stream)
+        api.relu_send(1, x1, prm, seeds.s01, seeds.s12, base, out=(lo1, hi1, tb1, d1), stream=stream)
+        api.relu_helper(lo0, hi0, lo1, hi1, prm, seeds.s02, seeds.s12, base, out=(e, c1), stream=stream)
+        api.relu_finish(0, x0, tb0, d0, d1, e, None, prm, seeds.s02, base, out=ya, stream=stream)
+        api.relu_finish(1, x1, tb1, d1, d0, e, c1, prm, seeds.s12, base, out=yb, stream=stream)
+
+    res = {}
+    for name, fn in (("drelu", drelu_chain), ("relu", relu_chain)):
+        t_ms, _, _ = timed(fn, 50, 3)
+        ms = t_ms / 50
+        res[name] = {"value": world * n / (ms * 1e-3), "unit": "elements/s", "ms_per_step": ms, "launches_per_step": 5}
+    res["note"] = "P0,P1 send + P2 helper + P0,P1 finish back to back on one GPU: all parties' work, nothing shared"
+    return res
 
 
 def relu_streams(api, prm, seeds, dev, stream, timed, world):

@@ -1,0 +1,29 @@
+"""compute-sanitizer memcheck / racecheck / initcheck over every C-ABI entry
+point on small ragged inputs (tools/sanitize_run.py)."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "initcheck"])
+def test_compute_sanitizer(tool):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(cs):
+        pytest.skip("compute-sanitizer not installed")
+    cmd = [cs, "--tool", tool, "--error-exitcode", "3"]
+    if tool == "initcheck":
+        cmd += ["--track-unused-memory", "no"]
+    r = subprocess.run(cmd + [sys.executable, os.path.join(ROOT, "tools", "sanitize_run.py")],
+                       capture_output=True, text=True, timeout=900)
+    tail = (r.stdout + r.stderr)[-3000:]
+    assert r.returncode == 0 and "sanitize_run ok" in r.stdout, tail
+    assert "ERROR SUMMARY: 0 errors" in r.stdout + r.stderr, tail

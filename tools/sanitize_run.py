@@ -1,0 +1,34 @@
+"""Exercise every C-ABI entry point once on small ragged inputs (for compute-sanitizer)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import synth
+from paper_2309_04909_b200 import api
+
+dev = "cuda:0"
+sd = synth.seeds(0)
+def t(a): return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).to(dev)
+for kw in (dict(), dict(ell=16, lx=7, f=0, mode="literal"), dict(ell=32, lx=5, f=3)):
+    prm = api.Params(**kw, rounds=8)
+    for n in (1, 13, 1003):
+        x, x0, x1 = synth.shares(n, prm.ell, prm.lx, prm.f, "D1")
+        a0, a1 = t(x0), t(x1)
+        tr = api.transcript_buffers(n, dev)
+        api.drelu(a0, a1, prm, sd, 8, transcript=tr)
+        api.relu(a0, a1, prm, sd, 8, transcript=tr)
+        api.drelu(a0, a1, prm, sd, 16)
+        api.relu(a0, a1, prm, sd, 16)
+        api.ladder_modswitch(0, a0, prm); api.ladder_modswitch(1, a1, prm)
+        api.trc(0, a0, prm.ell, 3, 1); api.trc(1, a1, prm.ell, 3, 1)
+        api.trc_prob(0, a0, prm.ell, 3); api.modswitch(1, a1, 7, 131)
+        lo0, hi0, tb0 = api.drelu_send(0, a0, prm, sd.s01, 8)
+        lo1, hi1, tb1 = api.drelu_send(1, a1, prm, sd.s01, 8)
+        r0, r1 = api.drelu_helper(lo0, hi0, lo1, hi1, prm, sd.s02, 8, paper_literal=True)
+        api.drelu_finish(0, tb0, None, prm, n, sd.s02, 8); api.drelu_finish(1, tb1, r1, prm, n, None, 8)
+        L0, H0, T0, d0 = api.relu_send(0, a0, prm, sd.s01, sd.s02, 8)
+        L1, H1, T1, d1 = api.relu_send(1, a1, prm, sd.s01, sd.s12, 8)
+        e, c1 = api.relu_helper(L0, H0, L1, H1, prm, sd.s02, sd.s12, 8)
+        api.relu_finish(0, a0, T0, d0, d1, e, None, prm, sd.s02, 8)
+        api.relu_finish(1, a1, T1, d1, d0, e, c1, prm, sd.s12, 8)
+torch.cuda.synchronize()
+print("sanitize_run ok")
