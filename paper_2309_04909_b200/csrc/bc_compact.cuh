@@ -19,9 +19,12 @@
 namespace bc {
 
 constexpr int PERM_A = 336;  // 8 * 7 * 6: digits k7, k6, k5
+
+
 constexpr int PERM_B = 120;  // 5 * 4 * 3 * 2: digits k4 .. k1
 
-// Nibble selectors of the two Fisher-Yates phases (built once per CTA in smem).
+// Nibble selectors of the two Fisher-Yates phases (built once per CTA in smem):
+// sA[0..335] / sA[336..671] = low / high halves of phase A, sB likewise (120).
 __device__ __forceinline__ uint32_t fy_swap(uint32_t sel, int m, uint32_t k) {
   const uint32_t a = (sel >> (4 * m)) & 15u, b = (sel >> (4 * k)) & 15u, d = a ^ b;
   return sel ^ (d << (4 * m)) ^ (d << (4 * k));
@@ -34,14 +37,16 @@ __device__ __forceinline__ void build_perm_tables(uint32_t* sA, uint32_t* sB) {
       sel = fy_swap(sel, 7, q % 8); q /= 8;
       sel = fy_swap(sel, 6, q % 7); q /= 7;
       sel = fy_swap(sel, 5, q % 6);
-      sA[i] = sel;
+      sA[i] = sel & 0xFFFFu;
+      sA[PERM_A + i] = sel >> 16;
     } else {           // swaps m = 4 .. 1 with the next mixed-radix digits
       uint32_t q = (uint32_t)(i - PERM_A);
       sel = fy_swap(sel, 4, q % 5); q /= 5;
       sel = fy_swap(sel, 3, q % 4); q /= 4;
       sel = fy_swap(sel, 2, q % 3); q /= 3;
       sel = fy_swap(sel, 1, q % 2);
-      sB[i - PERM_A] = sel;
+      sB[i - PERM_A] = sel & 0xFFFFu;
+      sB[PERM_B + i - PERM_A] = sel >> 16;
     }
   }
 }
@@ -49,7 +54,7 @@ __device__ __forceinline__ void build_perm_tables(uint32_t* sA, uint32_t* sB) {
 // Per-element randomness in the form the slot loop consumes.
 struct TapeC {
   uint32_t t;          // blinding bit
-  uint32_t selA, selB; // two-phase shuffle selectors (nibbles)
+  uint32_t sel[4];     // two-phase shuffle selectors: A lo, A hi, B lo, B hi
   uint32_t rb[2];      // mask bytes r_m - 1, slot m = byte m
   uint32_t rho[8];     // reshare digits rho_m in Z_257
 };
@@ -57,18 +62,23 @@ struct TapeC {
 // x / 257 for any 32-bit x: floor(x * (2^40 + 1)/257 / 2^40) (exact).
 __device__ __forceinline__ uint32_t div257(uint32_t x) { return __umulhi(x, 0xFF00FF01u) >> 8; }
 
+struct FbC {  // the draws a compact tape can reject, passed by value (registers, not local memory)
+  uint32_t idx, w0, w1, w2;
+};
+
 template <int R>
-__device__ __noinline__ void fallback_c(uint32_t& idx, uint32_t& w0, uint32_t& w1, uint32_t& w2, uint64_t j, Key key) {
+__device__ __noinline__ FbC fallback_c(FbC d, uint64_t j, Key key) {
   FbStream<R> fb;
   fb.key = key; fb.j = j; fb.pos = 16; fb.kc = 0;
-  if (idx >= PERM_LIMIT_8) {
+  if (d.idx >= PERM_LIMIT_8) {
     uint32_t v = fb.next() & 0x7FFFFFFFu;
     while (v >= PERM_LIMIT_8) v = fb.next() & 0x7FFFFFFFu;
-    idx = v;
+    d.idx = v;
   }
-  if (w0 >= RHO_WORD_LIMIT) { uint32_t v = fb.next(); while (v >= RHO_WORD_LIMIT) v = fb.next(); w0 = v; }
-  if (w1 >= RHO_WORD_LIMIT) { uint32_t v = fb.next(); while (v >= RHO_WORD_LIMIT) v = fb.next(); w1 = v; }
-  if (w2 >= RHO_WORD_LIMIT) { uint32_t v = fb.next(); while (v >= RHO_WORD_LIMIT) v = fb.next(); w2 = v; }
+  if (d.w0 >= RHO_WORD_LIMIT) { uint32_t v = fb.next(); while (v >= RHO_WORD_LIMIT) v = fb.next(); d.w0 = v; }
+  if (d.w1 >= RHO_WORD_LIMIT) { uint32_t v = fb.next(); while (v >= RHO_WORD_LIMIT) v = fb.next(); d.w1 = v; }
+  if (d.w2 >= RHO_WORD_LIMIT) { uint32_t v = fb.next(); while (v >= RHO_WORD_LIMIT) v = fb.next(); d.w2 = v; }
+  return d;
 }
 
 // Compact tape (24 B): T0 = t | perm index, T1, T2 = mask bytes, reshare words
@@ -80,11 +90,17 @@ __device__ __forceinline__ void decode_c(uint32_t T0, uint32_t T1, uint32_t T2, 
   tp.t = T0 >> 31;
   uint32_t idx = T0 & 0x7FFFFFFFu;
   if (__builtin_expect((idx >= PERM_LIMIT_8) | (w0 >= RHO_WORD_LIMIT) | (w1 >= RHO_WORD_LIMIT) |
-                       (w2 >= RHO_WORD_LIMIT), 0))
-    fallback_c<R>(idx, w0, w1, w2, j, k01);
+                       (w2 >= RHO_WORD_LIMIT), 0)) {
+    const FbC d = fallback_c<R>(FbC{idx, w0, w1, w2}, j, k01);
+    idx = d.idx; w0 = d.w0; w1 = d.w1; w2 = d.w2;
+  }
   const uint32_t hiq = idx / (uint32_t)PERM_A;               // < 2^31 / 336
-  tp.selA = sA[idx - hiq * (uint32_t)PERM_A];                // (idx mod 8!) mod 336 = idx mod 336
-  tp.selB = sB[hiq % (uint32_t)PERM_B];                      // (idx mod 8!) / 336
+  const uint32_t ia = idx - hiq * (uint32_t)PERM_A;          // (idx mod 8!) mod 336 = idx mod 336
+  const uint32_t ib = hiq % (uint32_t)PERM_B;                // (idx mod 8!) / 336
+  tp.sel[0] = sA[ia];
+  tp.sel[1] = sA[PERM_A + ia];
+  tp.sel[2] = sB[ib];
+  tp.sel[3] = sB[PERM_B + ib];
   tp.rb[0] = T1;
   tp.rb[1] = T2;
   const uint32_t w[3] = {w0, w1, w2};
@@ -118,8 +134,9 @@ __device__ __forceinline__ void ladder_swar(uint32_t win, uint32_t& lo, uint32_t
   constexpr uint32_t M = 0x00FF00FFu;
   const uint32_t e = win & 0x3FFFu;
   const uint32_t o = (win >> 1) & 0x3FFFu;
-  const uint32_t Elo = (e * KL) & M, Ehi = (__umulhi(e, KL) + e * 1024u) & M;
-  const uint32_t Olo = (o * KL) & M, Ohi = (__umulhi(o, KL) + o * 1024u) & M;
+  // high word of e * (KL + 2^42) for e < 2^14 is exactly (e >> 4) + (e << 10)
+  const uint32_t Elo = (e * KL) & M, Ehi = ((e >> 4) + (e << 10)) & M;
+  const uint32_t Olo = (o * KL) & M, Ohi = ((o >> 4) + (o << 10)) & M;
   const uint32_t Slo = __byte_perm(Elo, Ehi, 0x5432u), Shi = Ehi >> 16;  // E >> 16: a_2,a_4,a_6,0
   uint32_t ce_lo, ce_hi, co_lo, co_hi;
   if (PARTY == 0) {  // u_i + u_{i+1} - 2 (mod 256) = v'_i - 1 for P0
@@ -142,12 +159,12 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
   return d;
 }
 
-// Step 6: both Fisher-Yates phases as PRMT byte gathers.
-__device__ __forceinline__ void shuffle_bytes(uint32_t& lo, uint32_t& hi, uint32_t selA, uint32_t selB) {
-  const uint32_t aH = __umulhi(selA, 1u << 16), bH = __umulhi(selB, 1u << 16);  // >> 16 on the FMA pipe
-  const uint32_t l1 = prmt(lo, hi, selA), h1 = prmt(lo, hi, aH);
-  lo = prmt(l1, h1, selB);
-  hi = prmt(l1, h1, bH);
+// Step 6: both Fisher-Yates phases as PRMT byte gathers.  Selectors hold the
+// low (output bytes 0-3) and high (bytes 4-7) nibble halves in separate words.
+__device__ __forceinline__ void shuffle_bytes(uint32_t& lo, uint32_t& hi, const uint32_t (&sel)[4]) {
+  const uint32_t l1 = prmt(lo, hi, sel[0]), h1 = prmt(lo, hi, sel[1]);
+  lo = prmt(l1, h1, sel[2]);
+  hi = prmt(l1, h1, sel[3]);
 }
 
 __device__ __forceinline__ uint32_t mod257s(uint32_t x) {  // x < 2^18
@@ -175,18 +192,28 @@ __device__ __forceinline__ uint32_t elem_both(uint64_t x0, uint64_t x1, const Ta
   uint32_t c_lo, c_hi, d_lo, d_hi;
   ladder_swar<0>(window_of<0>(x0, tp.t, fsh, fhi), c_lo, c_hi);
   ladder_swar<1>(window_of<1>(x1, tp.t, fsh, fhi), d_lo, d_hi);
-  shuffle_bytes(c_lo, c_hi, tp.selA, tp.selB);
-  shuffle_bytes(d_lo, d_hi, tp.selA, tp.selB);
+  shuffle_bytes(c_lo, c_hi, tp.sel);
+  shuffle_bytes(d_lo, d_hi, tp.sel);
   uint32_t vmin = 0xFFFFFFFFu;
 #pragma unroll
   for (int m = 0; m < 8; ++m) {
-    const uint32_t rb = byte_of(tp.rb[m >> 2], m & 3), r = rb + 1u;
-    const uint32_t w0 = mod257s(byte_of(m < 4 ? c_lo : c_hi, m & 3) * r + (rb + tp.rho[m] + 258u));  // P0's message
-    const uint32_t w1 = mod257s(byte_of(m < 4 ? d_lo : d_hi, m & 3) * r + (rb - tp.rho[m] + 515u));  // P1's message
-    if (KEEP_W) { W0[m] = w0; W1[m] = w1; }
-    const uint32_t s = w0 + w1;                              // P2: w_m = W0 + W1 (mod 257)
-    vmin = min(vmin, s - 257u * (s >> 8));                   // 0 iff s in {0, 257}; s <= 512
+    const uint32_t rb = byte_of(tp.rb[m >> 2], m & 3);
+    const uint32_t r = rb + 1u, a0 = rb + tp.rho[m] + 258u, a1 = rb - tp.rho[m] + 515u;
+    // P0's and P1's messages as integers < 2^17 congruent to W0_m, W1_m (mod 257)
+    const uint32_t x0 = byte_of(m < 4 ? c_lo : c_hi, m & 3) * r + a0;   // (v'+1) r + rho + 257
+    const uint32_t x1 = byte_of(m < 4 ? d_lo : d_hi, m & 3) * r + a1;   // (v'+1) r - rho + 514
+    if (KEEP_W) {  // transcript: the wire format needs the reduced values
+      W0[m] = mod257s(x0);
+      W1[m] = mod257s(x1);
+      const uint32_t s = W0[m] + W1[m];
+      vmin = min(vmin, s - 257u * (s >> 8));                 // 0 iff s in {0, 257}
+    } else {
+      // P2: w_m = W0 + W1 = 0 (mod 257)  <=>  257 | (x0 + x1)  <=>
+      // (x0 + x1) * 257^-1 mod 2^32 <= floor((2^32-1)/257)   (exact for x0 + x1 < 2^19)
+      vmin = min(vmin, (x0 + x1) * 0xFF00FF01u);
+    }
   }
+  if (!KEEP_W) return vmin <= 16711935u;
   return vmin == 0u;
 }
 
@@ -194,7 +221,7 @@ template <int PARTY>
 __device__ __forceinline__ void elem_one(uint64_t x, const TapeC& tp, uint32_t fsh, bool fhi, uint32_t (&W)[8]) {
   uint32_t lo, hi;
   ladder_swar<PARTY>(window_of<PARTY>(x, tp.t, fsh, fhi), lo, hi);
-  shuffle_bytes(lo, hi, tp.selA, tp.selB);
+  shuffle_bytes(lo, hi, tp.sel);
   mask_slots<PARTY>(lo, hi, tp, W);
 }
 

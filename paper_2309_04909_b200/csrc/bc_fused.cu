@@ -99,7 +99,7 @@ __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, c
 // ChaCha blocks per 8 elements, none shared between threads.
 template <int R, bool RELU, bool TRANSCRIPT>
 __global__ void __launch_bounds__(TPB, FUSED_MINB) k_fused_c(FusedArgs a, KP kp, Key k01, Key k02, Key k12) {
-  __shared__ uint32_t sA[PERM_A], sB[PERM_B];
+  __shared__ uint32_t sA[2 * PERM_A], sB[2 * PERM_B];
   build_perm_tables(sA, sB);
   __syncthreads();
   const bool fhi = kp.fhi != 0;

@@ -24,7 +24,7 @@ __device__ __forceinline__ void store_msg(const SendArgs& a, const KP& kp, const
 // Alg 7 steps 1-8 (and Alg 8's [d]_b) for one computing party, compact tape.
 template <int R, int PARTY, bool RELU>
 __global__ void __launch_bounds__(TPB, 2) k_send_c(SendArgs a, KP kp, Key k01, Key ktr) {
-  __shared__ uint32_t sA[PERM_A], sB[PERM_B];
+  __shared__ uint32_t sA[2 * PERM_A], sB[2 * PERM_B];
   build_perm_tables(sA, sB);
   __syncthreads();
   const bool fhi = kp.fhi != 0;

@@ -41,13 +41,66 @@ __global__ void k_imad(uint32_t* out, uint32_t seed, uint32_t k) {
 __global__ void k_imadhi(uint32_t* out, uint32_t seed, uint32_t k) {
   BODY(asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(v[c]) : "r"(k), "r"(seed)))
 }
-__global__ void k_mix_chacha(uint32_t* out, uint32_t seed, uint32_t k) {
-  // ChaCha-like: xor (LOP3), rotate (SHF), add (IMAD.IADD) in the 1:1:1 ratio
-  BODY({
-    asm volatile("add.u32 %0, %0, %1;" : "+r"(v[c]) : "r"(k));
-    asm volatile("xor.b32 %0, %0, %1;" : "+r"(v[c]) : "r"(seed));
-    asm volatile("shf.l.wrap.b32 %0, %0, %0, 12;" : "+r"(v[c]));
-  })
+
+
+__global__ void k_mix_lop_imad(uint32_t* out, uint32_t seed, uint32_t k) {
+  // one LOP3 and one IMAD per chain per iteration, on separate chains (no dependency between them)
+  uint32_t v[CH], w[CH];
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) { v[c] = seed + c * 0x9E3779B9u + threadIdx.x; w[c] = v[c] ^ 0x55u; }
+  for (int i = 0; i < ITERS; ++i) {
+    _Pragma("unroll") for (int c = 0; c < CH; ++c) {
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(v[c]) : "r"(k), "r"(seed));
+      asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(w[c]) : "r"(k), "r"(seed));
+    }
+  }
+  uint32_t acc = 0;
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) acc ^= v[c] ^ w[c];
+  if (acc == 0x12345678u) out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+__global__ void k_mix_lop_imadhi(uint32_t* out, uint32_t seed, uint32_t k) {
+  uint32_t v[CH], w[CH];
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) { v[c] = seed + c * 0x9E3779B9u + threadIdx.x; w[c] = v[c] ^ 0x55u; }
+  for (int i = 0; i < ITERS; ++i) {
+    _Pragma("unroll") for (int c = 0; c < CH; ++c) {
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(v[c]) : "r"(k), "r"(seed));
+      asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(w[c]) : "r"(k), "r"(seed));
+    }
+  }
+  uint32_t acc = 0;
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) acc ^= v[c] ^ w[c];
+  if (acc == 0x12345678u) out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+__global__ void k_mix_xsa(uint32_t* out, uint32_t seed, uint32_t k) {
+  // ChaCha-like step: x = rotl(x ^ y, 7); y += x  (LOP3, SHF, IMAD.IADD) on 8 chains
+  uint32_t v[CH], w[CH];
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) { v[c] = seed + c * 0x9E3779B9u + threadIdx.x; w[c] = v[c] ^ 0x55u; }
+  for (int i = 0; i < ITERS; ++i) {
+    _Pragma("unroll") for (int c = 0; c < CH; ++c) {
+      asm volatile("xor.b32 %0, %0, %1;" : "+r"(v[c]) : "r"(w[c]));
+      asm volatile("shf.l.wrap.b32 %0, %0, %0, 7;" : "+r"(v[c]));
+      asm volatile("add.u32 %0, %0, %1;" : "+r"(w[c]) : "r"(v[c]));
+    }
+  }
+  uint32_t acc = 0;
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) acc ^= v[c] ^ w[c];
+  if (acc == 0x12345678u) out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
+__global__ void k_viadd(uint32_t* out, uint32_t seed, uint32_t k) {
+  BODY(asm volatile("add.u32 %0, %0, 0x3320646e;" : "+r"(v[c])))
+}
+__global__ void k_mix_lop_viadd(uint32_t* out, uint32_t seed, uint32_t k) {
+  uint32_t v[CH], w[CH];
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) { v[c] = seed + c * 0x9E3779B9u + threadIdx.x; w[c] = v[c] ^ 0x55u; }
+  for (int i = 0; i < ITERS; ++i) {
+    _Pragma("unroll") for (int c = 0; c < CH; ++c) {
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(v[c]) : "r"(k), "r"(seed));
+      asm volatile("add.u32 %0, %0, 0x3320646e;" : "+r"(w[c]));
+    }
+  }
+  uint32_t acc = 0;
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) acc ^= v[c] ^ w[c];
+  if (acc == 0x12345678u) out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
 template <typename K>
@@ -81,10 +134,13 @@ int main() {
   printf(", \"lop3_tops\": %.3f", rate(k_lop3, 1, blocks, threads));
   printf(", \"shf_tops\": %.3f", rate(k_shf, 1, blocks, threads));
   printf(", \"prmt_tops\": %.3f", rate(k_prmt, 1, blocks, threads));
-  printf(", \"iadd_tops\": %.3f", rate(k_iadd3, 1, blocks, threads));
   printf(", \"imad_tops\": %.3f", rate(k_imad, 1, blocks, threads));
   printf(", \"imad_hi_tops\": %.3f", rate(k_imadhi, 1, blocks, threads));
-  printf(", \"chacha_mix_tops\": %.3f", rate(k_mix_chacha, 3, blocks, threads));
+  printf(", \"viadd_tops\": %.3f", rate(k_viadd, 1, blocks, threads));
+  printf(", \"lop3+viadd_tops\": %.3f", rate(k_mix_lop_viadd, 2, blocks, threads));
+  printf(", \"lop3+imad_tops\": %.3f", rate(k_mix_lop_imad, 2, blocks, threads));
+  printf(", \"lop3+imadhi_tops\": %.3f", rate(k_mix_lop_imadhi, 2, blocks, threads));
+  printf(", \"xor_rot_add_tops\": %.3f", rate(k_mix_xsa, 3, blocks, threads));
   printf("}\n");
   return 0;
 }
