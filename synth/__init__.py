@@ -24,16 +24,19 @@ import numpy as np
 
 @dataclass(frozen=True)
 class Seeds:
-    """Pre-shared seeds seed01, seed02, seed12."""
+    """Pre-shared seeds seed01, seed02, seed12, and for the RSS variant
+    (Alg 9) seed012 (all three parties) and P2's private seed2."""
     s01: bytes
     s02: bytes
     s12: bytes
+    s012: bytes = b""
+    s2: bytes = b""
 
 
 def seeds(run: int = 0) -> Seeds:
-    """SHA-256("bicoptor/seedXY/run<k>") for the three party pairs."""
+    """SHA-256("bicoptor/<seed>/run<k>") for each seed."""
     h = lambda tag: hashlib.sha256(f"bicoptor/{tag}/run{run}".encode()).digest()
-    return Seeds(h("seed01"), h("seed02"), h("seed12"))
+    return Seeds(h("seed01"), h("seed02"), h("seed12"), h("seed012"), h("seed2"))
 
 
 def _mask(ell: int) -> np.uint64:
@@ -78,6 +81,18 @@ def share(x: np.ndarray, ell: int, run: int = 0):
         x0 = (x + R) & _mask(ell)
         x1 = (np.uint64(0) - R) & _mask(ell)
     return x0.astype(np.uint64), x1.astype(np.uint64)
+
+
+def rss_share(x: np.ndarray, ell: int, run: int = 0):
+    """Replicated 2-out-of-3 input sharing x = x_0 + x_1 + x_2 mod 2^ell with
+    x_0, x_1 uniform; party P_i holds (x_i, x_{i+1})."""
+    x = np.asarray(x, dtype=np.uint64)
+    rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence([0x7355, run, x.size, ell])))
+    x0 = rng.integers(0, np.iinfo(np.uint64).max, size=x.size, dtype=np.uint64, endpoint=True) & _mask(ell)
+    x1 = rng.integers(0, np.iinfo(np.uint64).max, size=x.size, dtype=np.uint64, endpoint=True) & _mask(ell)
+    with np.errstate(over="ignore"):
+        x2 = (x - x0 - x1) & _mask(ell)
+    return x0.astype(np.uint64), x1.astype(np.uint64), x2.astype(np.uint64)
 
 
 def shares(n: int, ell: int, lx: int, f: int, dist: str = "D1", run: int = 0):
