@@ -40,8 +40,10 @@ METRIC = "DReLU & ReLU elements/s at ell=64 on 1/2/4/8 B200; % of HBM roofline"
 # ALU-pipe work of the PRG, the part of the path that cannot leave the ALU pipe:
 # per ChaCha_R block R/2 double rounds x 8 quarter rounds x (4 xor + 4 rotate).
 CHACHA_ALU_OPS_PER_BLOCK = {20: 640, 12: 384, 8: 256}
-BLOCKS_PER_ELEM = {"drelu": 0.5, "relu": 1.0}   # 3/8 (tape) + 1/8 (resp) or + 5/8 (triples)
-BYTES_PER_ELEM = {"drelu": 32, "relu": 32, "ladder": 16}  # algorithmic HBM bytes per element
+BLOCKS_PER_ELEM = {"drelu": 0.5, "relu": 1.0,   # 3/8 (tape) + 1/8 (resp) or + 5/8 (triples)
+                   "drelu_rss": 1.5, "relu_rss": 1.875}  # RSS: 3/8 (tape) + 9/8 (preprocessing) (+ 3/8 ReLU zero share)
+BYTES_PER_ELEM = {"drelu": 32, "relu": 32, "ladder": 16,   # algorithmic HBM bytes per element
+                  "drelu_rss": 48, "relu_rss": 48}
 SM_COUNT_B200 = 148
 
 
@@ -54,7 +56,7 @@ def parse():
     ap.add_argument("--n", type=int, default=N_PER_GPU)
     ap.add_argument("--rounds", type=int, default=ROUNDS)
     ap.add_argument("--no-extras", action="store_true", help="skip ReLU / ladder / variants / e2e / cpu legs")
-    ap.add_argument("--only", choices=["drelu", "relu", "ladder"], help="profiling aid: launch one op steps+warmup times, print nothing")
+    ap.add_argument("--only", choices=["drelu", "relu", "ladder", "drelu_rss", "relu_rss"], help="profiling aid: launch one op steps+warmup times, print nothing")
     ap.add_argument("--mode", default="sharded", choices=["sharded", "party"],
                     help="party: config 4, P0/P1/P2 on distinct GPUs (needs >= 3 ranks), ReLU over NCCL P2P")
     ap.add_argument("--party-n", type=int, default=1 << 26, help="elements per P0/P1/P2 triple (config 4)")
@@ -293,7 +295,13 @@ def run_cuda(a):
 
     if a.only:  # profiling aid (ncu): just the launches, no timing output
         v_lad = torch.empty((n, 8), dtype=torch.uint8, device=dev)
-        op = {"drelu": lambda: api.drelu(x0, x1, prm, seeds, base, y0, y1, stream=stream),
+        if a.only.endswith("_rss"):
+            xs = [torch.from_numpy(v.view(np.int64)).to(dev) for v in synth.rss_share(x, ELL, run=rank)]
+            ys = tuple(torch.empty_like(xs[0]) for _ in range(3))
+            f_rss = getattr(api, a.only)
+        op = {"drelu_rss": lambda: f_rss(*xs, prm, seeds, base, out=ys, stream=stream),
+              "relu_rss": lambda: f_rss(*xs, prm, seeds, base, out=ys, stream=stream),
+              "drelu": lambda: api.drelu(x0, x1, prm, seeds, base, y0, y1, stream=stream),
               "relu": lambda: api.relu(x0, x1, prm, seeds, base, y0, y1, stream=stream),
               "ladder": lambda: api.ladder_modswitch(0, x0, prm, out=v_lad, stream=stream)}[a.only]
         for _ in range(a.warmup + a.steps):
@@ -371,6 +379,8 @@ def run_cuda(a):
         del v_lad
         # ---- every party's work unshared: the party-phase kernels chained on 1 GPU ----
         line["party_chain_1gpu"] = party_chain(api, prm, seeds, x0, x1, base, dev, stream, timed, world, n)
+        # ---- RSS variant (Alg 9): DReLU / ReLU on replicated shares of the same x ----
+        line["rss"] = rss_leg(api, prm, seeds, x, base, dev, stream, timed, world, n, roofline, rank)
         # ---- config 5: E2E-shaped ReLU layer streams (CUDA graph per network) ----
         line["config5"] = relu_streams(api, prm, seeds, dev, stream, timed, world)
         # ---- e2e through the public API with pinned HOST buffers ----------------
@@ -416,6 +426,24 @@ def party_chain(api, prm, seeds, x0, x1, base, dev, stream, timed, world, n):
         ms = t_ms / 50
         res[name] = {"value": world * n / (ms * 1e-3), "unit": "elements/s", "ms_per_step": ms, "launches_per_step": 5}
     res["note"] = "P0,P1 send + P2 helper + P0,P1 finish back to back on one GPU: all parties' work, nothing shared"
+    return res
+
+
+def rss_leg(api, prm, seeds, x, base, dev, stream, timed, world, n, roofline, rank):
+    """Alg 9 (RSS DReLU) and RSS ReLU, all three parties in one fused kernel, on
+    replicated shares of the headline batch."""
+    import torch
+    import synth
+    xs = [torch.from_numpy(v.view(np.int64)).to(dev) for v in synth.rss_share(x, ELL, run=rank)]
+    ys = tuple(torch.empty_like(xs[0]) for _ in range(3))
+    res = {}
+    for name in ("drelu_rss", "relu_rss"):
+        fn = getattr(api, name)
+        t_ms, _, _ = timed(lambda: fn(*xs, prm, seeds, base, out=ys, stream=stream), 50, 3)
+        ms = t_ms / 50
+        v = world * n / (ms * 1e-3)
+        res[name] = {"value": v, "unit": "elements/s", "ms_per_step": ms, "roofline": roofline(name, v, ms)}
+    del xs, ys
     return res
 
 

@@ -173,6 +173,35 @@ int bc_relu_finish(int party, const uint64_t *x, const uint8_t *tbits, const uin
                    size_t n, uint64_t elem_base, const bc_params *prm,
                    const uint8_t seed_tr[32], void *stream);
 
+/* ---- RSS variant (Alg 9; RSS ReLU P:1930-1931) -------------
+ *
+ * Replicated 3-party sharing x = x0 + x1 + x2 mod 2^ell (P_i holds
+ * components i and i+1).  All three parties simulated in one fused kernel:
+ * the preprocessing ([t] re-shared from seed012, [s], [u] = [s XOR t] by one
+ * RSS multiplication), Alg 7 on the bridged sharing (P0 input x0 + x1, P1
+ * input x2; Alg 9 online step 1), DReLU'' = s XOR DReLU' (step 3) and the
+ * output [DReLU] = DReLU'' + [u] - 2 DReLU''[u] (step 5; DReLU'' on component
+ * 0, reading C27).  bc_relu_rss adds the secret multiplication [x][DReLU]
+ * (reading C26: z_i = a_i b_i + a_i b_{i+1} + a_{i+1} b_i + g_i, g a zero
+ * sharing from seed02 / seed01 / seed12).  Stream labels: DESIGN.md C25.
+ *
+ * x0, x1, x2 (in) and y0, y1, y2 (out): n u64 components in [0, 2^ell),
+ * device memory, 16-B aligned, outputs disjoint from each other and from the
+ * inputs (BC_EALIAS).  seeds: the pairwise seeds; seed012: the seed of all
+ * three parties; seed2: P2's private seed (32 B each, host memory).  Only the
+ * compact tape (guard mode, p = 257) is supported (BC_EINVAL otherwise).
+ * Errors as bc_drelu; elem_base % 8 == 0; n = 0 is a no-op. */
+int bc_drelu_rss(const uint64_t *x0, const uint64_t *x1, const uint64_t *x2, uint64_t *y0,
+                 uint64_t *y1, uint64_t *y2, size_t n, uint64_t elem_base, const bc_params *prm,
+                 const bc_seeds *seeds, const uint8_t seed012[32], const uint8_t seed2[32],
+                 void *stream);
+
+/* RSS ReLU: [x][DReLU(x)]; arguments as bc_drelu_rss. */
+int bc_relu_rss(const uint64_t *x0, const uint64_t *x1, const uint64_t *x2, uint64_t *y0,
+                uint64_t *y1, uint64_t *y2, size_t n, uint64_t elem_base, const bc_params *prm,
+                const bc_seeds *seeds, const uint8_t seed012[32], const uint8_t seed2[32],
+                void *stream);
+
 /* Human-readable text for a BC_* code (static storage). */
 const char *bc_strerror(int code);
 

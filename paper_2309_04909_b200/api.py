@@ -71,6 +71,10 @@ _SIG = {
                                       ctypes.POINTER(bc_params), ctypes.c_char_p, ctypes.c_char_p, _P]),
     "bc_relu_finish": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64,
                                       ctypes.POINTER(bc_params), ctypes.c_char_p, _P]),
+    "bc_drelu_rss": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64, ctypes.POINTER(bc_params),
+                                    ctypes.POINTER(bc_seeds), ctypes.c_char_p, ctypes.c_char_p, _P]),
+    "bc_relu_rss": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64, ctypes.POINTER(bc_params),
+                                   ctypes.POINTER(bc_seeds), ctypes.c_char_p, ctypes.c_char_p, _P]),
 }
 EXPORTS = tuple(_SIG)
 
@@ -297,3 +301,30 @@ def relu_finish(party, x, tbits, d_own, d_peer, e, c1, prm: Params, seed_tr: byt
                                 _dev(d_peer, "d_peer"), _dev(e, "e"), _opt(c1, "c1"), _dev(y, "y"), n, elem_base,
                                 ctypes.byref(prm.c()), seed_tr, _stream(stream)), "bc_relu_finish")
     return y
+
+
+# ---- RSS variant (Alg 9) -------------------------------------------------------------
+
+def _rss(fn, what, x0, x1, x2, prm: Params, seeds, elem_base, out, stream):
+    n = x0.numel()
+    if x1.numel() != n or x2.numel() != n:
+        raise BicoptorError("x0, x1, x2 differ in length")
+    y0, y1, y2 = (torch.empty_like(x0), torch.empty_like(x1), torch.empty_like(x2)) if out is None else out
+    for name in ("s012", "s2"):
+        if len(getattr(seeds, name)) != 32:
+            raise BicoptorError(f"seeds.{name} must be 32 bytes")
+    cp, cs = prm.c(), seeds_struct(seeds)
+    _check(fn(_dev(x0, "x0"), _dev(x1, "x1"), _dev(x2, "x2"), _dev(y0, "y0"), _dev(y1, "y1"), _dev(y2, "y2"), n,
+              elem_base, ctypes.byref(cp), ctypes.byref(cs), seeds.s012, seeds.s2, _stream(stream)), what)
+    return y0, y1, y2
+
+
+def drelu_rss(x0, x1, x2, prm: Params, seeds, elem_base: int = 0, out=None, stream=None):
+    """Alg 9 (RSS DReLU), three parties in one fused kernel: returns (y0, y1, y2), sum = DReLU(x).
+    seeds carries s01, s02, s12, s012 and s2 (synth.Seeds)."""
+    return _rss(lib().bc_drelu_rss, "bc_drelu_rss", x0, x1, x2, prm, seeds, elem_base, out, stream)
+
+
+def relu_rss(x0, x1, x2, prm: Params, seeds, elem_base: int = 0, out=None, stream=None):
+    """RSS ReLU [x][DReLU(x)]: returns (y0, y1, y2), sum = ReLU(x)."""
+    return _rss(lib().bc_relu_rss, "bc_relu_rss", x0, x1, x2, prm, seeds, elem_base, out, stream)

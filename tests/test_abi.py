@@ -28,7 +28,7 @@ def test_header_declares_the_boundary():
     names = declared()
     for must in ("bc_params_init", "bc_trc", "bc_modswitch", "bc_ladder_modswitch", "bc_drelu", "bc_relu",
                  "bc_drelu_send", "bc_drelu_helper", "bc_drelu_finish", "bc_relu_send", "bc_relu_helper",
-                 "bc_relu_finish", "bc_strerror", "bc_trc_prob"):
+                 "bc_relu_finish", "bc_strerror", "bc_trc_prob", "bc_drelu_rss", "bc_relu_rss"):
         assert must in names
 
 
@@ -65,4 +65,4 @@ def test_errors_and_strerror(lib):
     assert b"window" in lib.bc_strerror(-2)
     # a NULL-pointer call is rejected on the host before any launch
     assert lib.bc_drelu(None, None, None, None, 8, 0, ctypes.byref(api.Params().c()), None, None, None) == -1
-    assert lib.bc_version() >= 100
+    assert lib.bc_version() >= 101

@@ -314,3 +314,67 @@ def test_relu_stream_graph_matches_eager_and_oracle(api):
         x, x0, x1 = xs[i]
         ref = B.relu(oprm, x0[idx], x1[idx], idx.astype(np.uint64) + np.uint64(st.bases[i]), SEEDS)
         assert np.array_equal(host(st.y0[i])[idx], ref["y0"]) and np.array_equal(host(st.y1[i])[idx], ref["y1"])
+
+
+# ---- RSS variant (Alg 9) ---------------------------------------------------------------
+
+RSS_PARAMS = [PARAMS[0], PARAMS[1], PARAMS[2], PARAMS[3]]
+
+
+@pytest.mark.parametrize("kw", RSS_PARAMS, ids=_ids)
+@pytest.mark.parametrize("fn", ["drelu_rss", "relu_rss"])
+def test_rss_parity(api, kw, fn):
+    """bc_drelu_rss / bc_relu_rss: all three output components bit-exact
+    against oracle.rss, ragged sizes and several element bases."""
+    from oracle import rss
+    oprm = B.Params(**kw)
+    prm = api.Params(**kw)
+    for n in SIZES:
+        for base in (0, 8, 1 << 40):
+            x = synth.plaintext(n, kw["ell"], kw["lx"], kw["f"], "D1", run=n)
+            xs = synth.rss_share(x, kw["ell"], run=n)
+            j = np.arange(n, dtype=np.uint64) + np.uint64(base)
+            ref = getattr(rss, fn)(oprm, *xs, j, SEEDS)
+            ys = getattr(api, fn)(*(dev(v) for v in xs), prm, SEEDS, elem_base=base)
+            for k in range(3):
+                assert np.array_equal(host(ys[k]), ref["y"][k]), (n, base, k)
+
+
+@pytest.mark.parametrize("fn", ["drelu_rss", "relu_rss"])
+def test_rss_full_size_sampled(api, fn):
+    """2^24 elements in one launch: oracle parity on a 2^13 sample; opened sign /
+    ReLU on every element the key bits determine."""
+    from oracle import rss
+    n = 1 << 24
+    kw = PARAMS[0]
+    x = synth.plaintext(n, 64, 7, 24, "D2")
+    xs = synth.rss_share(x, 64)
+    ys = [host(t) for t in getattr(api, fn)(*(dev(v) for v in xs), api.Params(**kw), SEEDS)]
+    idx = np.sort(np.random.default_rng(12).choice(n, 1 << 13, replace=False)).astype(np.uint64)
+    ref = getattr(rss, fn)(B.Params(**kw), *(v[idx] for v in xs), idx, SEEDS)
+    for k in range(3):
+        assert np.array_equal(ys[k][idx], ref["y"][k])
+    with np.errstate(over="ignore"):
+        y = ys[0] + ys[1] + ys[2]
+    s, valid = band_sign(x, 64, 7, 24)
+    want = s if fn == "drelu_rss" else relu_plain(x, 64, 7, 24)
+    assert np.array_equal(y[valid], want[valid])
+
+
+def test_rss_abi_errors(api):
+    import ctypes
+    L = api.lib()
+    cp, cs = api.Params().c(), api.seeds_struct(SEEDS)
+    t = [torch.zeros(16, dtype=torch.int64, device=DEV) for _ in range(6)]
+    p = [v.data_ptr() for v in t]
+    call = lambda *ptrs, n=16, base=0, prm=cp: L.bc_drelu_rss(*ptrs, n, base, ctypes.byref(prm), ctypes.byref(cs),  # noqa: E731
+                                                               SEEDS.s012, SEEDS.s2, None)
+    assert call(*p) == 0
+    assert call(*p, n=0) == 0
+    assert call(p[0], p[1], p[2], p[0], p[4], p[5]) == -5      # output aliases an input
+    assert call(p[0], p[1], p[2], p[3], p[3], p[5]) == -5      # outputs alias each other
+    assert call(p[0] + 8, *p[1:]) == -3                          # misaligned
+    assert call(*p, base=4) == -3
+    assert call(None, *p[1:]) == -1
+    wide = api.Params(ell=16, lx=7, f=0, mode="literal").c()
+    assert call(*p, prm=wide) == -1                              # compact tape only
