@@ -27,6 +27,8 @@ from .chacha import chacha_blocks, element_u32, element_u64, label_u64
 L_TAPEA = label_u64(b"bc2.tpa1")  # seed01: 16 B/element (compact tape, part A)
 L_TAPEB = label_u64(b"bc2.tpb1")  # seed01:  8 B/element (compact tape, part B)
 L_TAPEW = label_u64(b"bc2.tapw")   # seed01: 64 B/element (wide tape)
+L_TAPEL = label_u64(b"bc2.tpL1")   # seed01: 576 B/element (large tape, lx >= 8)
+L_FBL = label_u64(b"bc2.fbL1")     # seed01: large-tape fallback, u64 words, counter j*2^20+k
 L_FALLBACK = label_u64(b"bc2.fb01")  # seed01: rejection fallback, counter j*256+k
 L_RESP = label_u64(b"bc2.resp")    # seed02: [DReLU']_0, 8 B/element
 L_A02 = label_u64(b"bc2.ta02")     # seed02: [a]_0, 8 B/element
@@ -50,8 +52,8 @@ class Params:
     def __post_init__(self):
         if not (2 <= self.ell <= 64):
             raise ValueError("ell must be in [2, 64]")
-        if not (2 <= self.lx <= 7):
-            raise ValueError("lx must be in [2, 7] (at most 8 ladder slots)")
+        if not (2 <= self.lx <= 31):
+            raise ValueError("lx must be in [2, 31] (at most 32 ladder slots, p < 2^33)")
         if self.mode not in ("guard", "literal"):
             raise ValueError("mode must be 'guard' or 'literal'")
         if self.f < 0 or self.f + self.lx + self.w > self.ell:
@@ -75,6 +77,14 @@ class Params:
     def compact(self) -> bool:
         """Compact 24-B tape iff p = 257 and 8 slots (masks are exact bytes)."""
         return self.p == 257 and self.slots == 8
+
+    @property
+    def layout(self) -> str:
+        """PRG tape layout: "compact" (p = 257, 8 slots), "wide" (lx <= 7),
+        "large" (lx >= 8: up to 32 slots, p < 2^33; full precision lx = 31)."""
+        if self.compact:
+            return "compact"
+        return "wide" if self.lx <= 7 else "large"
 
 
 # --- PRG tape: t, Pi, r_m, rho_m for one element (Alg 7 steps 1, 6, 7, 8) -------------
@@ -111,8 +121,10 @@ def tape(prm: Params, seed01: bytes, j) -> dict:
     Parity unpinned beyond the ChaCha vector (the layout is the spec's).
     """
     j = np.atleast_1d(np.asarray(j, dtype=np.uint64))
-    if prm.compact:
+    if prm.layout == "compact":
         return _tape_compact(prm, seed01, j)
+    if prm.layout == "large":
+        return _tape_large(prm, seed01, j)
     return _tape_wide(prm, seed01, j)
 
 
@@ -192,6 +204,60 @@ def _tape_wide(prm: Params, seed01: bytes, j) -> dict:
     return {"t": t, "k": _perm_swaps(idx, S), "r": r, "rho": rho}
 
 
+def _fallback_u64(seed01: bytes, j: int, rounds: int):
+    """Sequential u64 words of ChaCha(seed01, L_FBL, counter = j*2^20 + k)."""
+    k = 0
+    while True:
+        blk = chacha_blocks(seed01, L_FBL, [(j << 20) + k], rounds)[0]
+        for i in range(8):
+            yield int(blk[2 * i]) | (int(blk[2 * i + 1]) << 32)
+        k += 1
+
+
+def _tape_large(prm: Params, seed01: bytes, j) -> dict:
+    """lx >= 8 (up to 32 slots, p < 2^33; the full-precision lx = 31 regime,
+    P:195).  576 B = 9 ChaCha blocks per element at 576 j (label bc2.tpL1):
+      block 0:    32 u16 h; t = h[0] & 1; the Fisher-Yates draw of slot m
+                  (m = S-1 .. 1) is h[S-m]: k_m = h mod (m+1), reject h >= floor(2^16/(m+1))(m+1);
+      blocks 1-4: 32 u64 mask draws u_m: r_m = 1 + u_m mod (p-1), reject u >= floor(2^64/(p-1))(p-1);
+      blocks 5-8: 32 u64 reshare draws u_m: rho_m = u_m mod p, reject u >= floor(2^64/p) p.
+    Slots m >= S leave their draws unused.  A rejected draw -- in the order
+    k_{S-1} .. k_1, r_0 .. r_{S-1}, rho_0 .. rho_{S-1} -- is replaced by the next
+    u64 of the fallback stream (its low 16 bits for a Fisher-Yates draw), repeated
+    until accepted (reading C10).  Returns r, rho as Python-int object arrays."""
+    n, S, p = j.size, prm.slots, prm.p
+    T = element_u32(seed01, L_TAPEL, prm.rounds, j, 144)
+    h = np.ascontiguousarray(T[:, :16]).view("<u2").reshape(n, 32).astype(np.int64)
+    U = np.ascontiguousarray(T[:, 16:]).view("<u8").reshape(n, 64)
+    t = (h[:, 0] & 1).astype(np.uint64)
+    k = np.zeros((n, S), dtype=np.int64)
+    hlim = {m: (65536 // (m + 1)) * (m + 1) for m in range(1, S)}
+    rlim, plim = ((1 << 64) // (p - 1)) * (p - 1), ((1 << 64) // p) * p
+    r = np.empty((n, S), dtype=object)
+    rho = np.empty((n, S), dtype=object)
+    for row in range(n):
+        fb = None
+        for m in range(S - 1, 0, -1):
+            d = int(h[row, S - m])
+            while d >= hlim[m]:
+                fb = fb or _fallback_u64(seed01, int(j[row]), prm.rounds)
+                d = next(fb) & 0xFFFF
+            k[row, m] = d % (m + 1)
+        for m in range(S):
+            u = int(U[row, m])
+            while u >= rlim:
+                fb = fb or _fallback_u64(seed01, int(j[row]), prm.rounds)
+                u = next(fb)
+            r[row, m] = 1 + u % (p - 1)
+        for m in range(S):
+            u = int(U[row, 32 + m])
+            while u >= plim:
+                fb = fb or _fallback_u64(seed01, int(j[row]), prm.rounds)
+                u = next(fb)
+            rho[row, m] = u % p
+    return {"t": t, "k": k, "r": r, "rho": rho}
+
+
 # --- Alg 7 steps 3-5: ladder, pairwise sums, modulo switch --------------------------
 
 def ladder(prm: Params, party: int, s) -> np.ndarray:
@@ -224,6 +290,8 @@ def ladder_modswitch(prm: Params, party: int, s) -> np.ndarray:
 def ladder_modswitch_bytes(prm: Params, party: int, s) -> np.ndarray:
     """Output format of bc_ladder_modswitch: byte m = v'_m - 1 (v' is never 0,
     see Alg 6), bytes S..7 zero.  (n, 8) uint8."""
+    if prm.slots > 8:
+        raise ValueError("the byte format holds at most 8 slots (lx <= 7)")
     vp = ladder_modswitch(prm, party, s)
     out = np.zeros((vp.shape[0], 8), dtype=np.uint8)
     out[:, : prm.slots] = (vp - np.uint64(1)).astype(np.uint8)
@@ -260,6 +328,11 @@ def drelu_send(prm: Params, party: int, xb, j, seed01: bytes) -> dict:
     s = np.where(t == 1, ring.neg(xb, prm.ell), xb).astype(np.uint64)       # steps 1-2
     vp = ladder_modswitch(prm, party, s)                                      # steps 3-5
     vp = shuffle(tp["k"], vp)                                                 # step 6
+    if prm.layout == "large":                                                 # p up to 2^33: exact ints
+        P = prm.p
+        wv = (vp.astype(object) * tp["r"]) % P                                # step 7
+        W = (wv + tp["rho"]) % P if party == 0 else (wv + P - tp["rho"]) % P  # step 8
+        return {"t": t, "W": W.astype(np.uint64)}
     P = np.uint64(prm.p)
     wv = (vp * tp["r"]) % P                                                   # step 7
     if party == 0:                                                            # step 8
@@ -386,6 +459,8 @@ def encode_msg(W: np.ndarray):
     element on the wire: 72 (guard, p=257) / 64 (literal, p=131)."""
     W = np.asarray(W, dtype=np.uint64)
     n, S = W.shape
+    if S > 8:
+        raise ValueError("the byte wire format holds at most 8 slots (lx <= 7)")
     lo = np.zeros((n, 8), dtype=np.uint8)
     lo[:, :S] = (W & np.uint64(0xFF)).astype(np.uint8)
     hi = np.zeros(n, dtype=np.uint8)
