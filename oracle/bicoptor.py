@@ -222,7 +222,7 @@ def _tape_large(prm: Params, seed01: bytes, j) -> dict:
       blocks 1-4: 32 u64 mask draws u_m: r_m = 1 + u_m mod (p-1), reject u >= floor(2^64/(p-1))(p-1);
       blocks 5-8: 32 u64 reshare draws u_m: rho_m = u_m mod p, reject u >= floor(2^64/p) p.
     Slots m >= S leave their draws unused.  A rejected draw -- in the order
-    k_{S-1} .. k_1, r_0 .. r_{S-1}, rho_0 .. rho_{S-1} -- is replaced by the next
+    k_{S-1} .. k_1, then r_0, rho_0, r_1, rho_1, .., r_{S-1}, rho_{S-1} -- is replaced by the next
     u64 of the fallback stream (its low 16 bits for a Fisher-Yates draw), repeated
     until accepted (reading C10).  Returns r, rho as Python-int object arrays."""
     n, S, p = j.size, prm.slots, prm.p
@@ -232,7 +232,7 @@ def _tape_large(prm: Params, seed01: bytes, j) -> dict:
     t = (h[:, 0] & 1).astype(np.uint64)
     k = np.zeros((n, S), dtype=np.int64)
     hlim = {m: (65536 // (m + 1)) * (m + 1) for m in range(1, S)}
-    rlim, plim = ((1 << 64) // (p - 1)) * (p - 1), ((1 << 64) // p) * p
+    rlim, plim = ((1 << 64) // (p - 1)) * (p - 1), ((1 << 64) // p) * p   # 2^64 when q | 2^64: no rejection
     r = np.empty((n, S), dtype=object)
     rho = np.empty((n, S), dtype=object)
     for row in range(n):
@@ -249,7 +249,6 @@ def _tape_large(prm: Params, seed01: bytes, j) -> dict:
                 fb = fb or _fallback_u64(seed01, int(j[row]), prm.rounds)
                 u = next(fb)
             r[row, m] = 1 + u % (p - 1)
-        for m in range(S):
             u = int(U[row, 32 + m])
             while u >= plim:
                 fb = fb or _fallback_u64(seed01, int(j[row]), prm.rounds)
