@@ -41,9 +41,10 @@ METRIC = "DReLU & ReLU elements/s at ell=64 on 1/2/4/8 B200; % of HBM roofline"
 # per ChaCha_R block R/2 double rounds x 8 quarter rounds x (4 xor + 4 rotate).
 CHACHA_ALU_OPS_PER_BLOCK = {20: 640, 12: 384, 8: 256}
 BLOCKS_PER_ELEM = {"drelu": 0.5, "relu": 1.0,   # 3/8 (tape) + 1/8 (resp) or + 5/8 (triples)
-                   "drelu_rss": 1.5, "relu_rss": 1.875}  # RSS: 3/8 (tape) + 9/8 (preprocessing) (+ 3/8 ReLU zero share)
+                   "drelu_rss": 1.5, "relu_rss": 1.875,  # RSS: 3/8 (tape) + 9/8 (preprocessing) (+ 3/8 ReLU zero share)
+                   "drelu_fp": 9.125, "relu_fp": 9.625}  # lx=31 large tape: 9 blocks + the finish streams
 BYTES_PER_ELEM = {"drelu": 32, "relu": 32, "ladder": 16,   # algorithmic HBM bytes per element
-                  "drelu_rss": 48, "relu_rss": 48}
+                  "drelu_rss": 48, "relu_rss": 48, "drelu_fp": 32, "relu_fp": 32}
 SM_COUNT_B200 = 148
 
 
@@ -56,7 +57,7 @@ def parse():
     ap.add_argument("--n", type=int, default=N_PER_GPU)
     ap.add_argument("--rounds", type=int, default=ROUNDS)
     ap.add_argument("--no-extras", action="store_true", help="skip ReLU / ladder / variants / e2e / cpu legs")
-    ap.add_argument("--only", choices=["drelu", "relu", "ladder", "drelu_rss", "relu_rss"], help="profiling aid: launch one op steps+warmup times, print nothing")
+    ap.add_argument("--only", choices=["drelu", "relu", "ladder", "drelu_rss", "relu_rss", "drelu_fp", "relu_fp"], help="profiling aid: launch one op steps+warmup times, print nothing")
     ap.add_argument("--mode", default="sharded", choices=["sharded", "party"],
                     help="party: config 4, P0/P1/P2 on distinct GPUs (needs >= 3 ranks), ReLU over NCCL P2P")
     ap.add_argument("--party-n", type=int, default=1 << 26, help="elements per P0/P1/P2 triple (config 4)")
@@ -294,6 +295,7 @@ def run_cuda(a):
         return max_over_ranks(total_ms), per, ck
 
     if a.only:  # profiling aid (ncu): just the launches, no timing output
+        pfp = api.Params(ell=ELL, lx=31, f=0, mode=MODE, rounds=a.rounds)
         v_lad = torch.empty((n, 8), dtype=torch.uint8, device=dev)
         if a.only.endswith("_rss"):
             xs = [torch.from_numpy(v.view(np.int64)).to(dev) for v in synth.rss_share(x, ELL, run=rank)]
@@ -301,6 +303,8 @@ def run_cuda(a):
             f_rss = getattr(api, a.only)
         op = {"drelu_rss": lambda: f_rss(*xs, prm, seeds, base, out=ys, stream=stream),
               "relu_rss": lambda: f_rss(*xs, prm, seeds, base, out=ys, stream=stream),
+              "drelu_fp": lambda: api.drelu(x0, x1, pfp, seeds, base, y0, y1, stream=stream),
+              "relu_fp": lambda: api.relu(x0, x1, pfp, seeds, base, y0, y1, stream=stream),
               "drelu": lambda: api.drelu(x0, x1, prm, seeds, base, y0, y1, stream=stream),
               "relu": lambda: api.relu(x0, x1, prm, seeds, base, y0, y1, stream=stream),
               "ladder": lambda: api.ladder_modswitch(0, x0, prm, out=v_lad, stream=stream)}[a.only]
@@ -381,6 +385,17 @@ def run_cuda(a):
         line["party_chain_1gpu"] = party_chain(api, prm, seeds, x0, x1, base, dev, stream, timed, world, n)
         # ---- RSS variant (Alg 9): DReLU / ReLU on replicated shares of the same x ----
         line["rss"] = rss_leg(api, prm, seeds, x, base, dev, stream, timed, world, n, roofline, rank)
+        # ---- full precision lx = 31, f = 0 (no key bits; large tape, p = 2^32 + 15) ----
+        pfp = api.Params(ell=ELL, lx=31, f=0, mode=MODE, rounds=a.rounds)
+        fp = {}
+        for name, fn in (("drelu_fp", api.drelu), ("relu_fp", api.relu)):
+            t_fp, _, _ = timed(lambda: fn(x0, x1, pfp, seeds, base, y0, y1, stream=stream), 10, 3)
+            ms_fp = t_fp / 10
+            v_fp = world * n / (ms_fp * 1e-3)
+            fp[name] = {"value": v_fp, "unit": "elements/s", "ms_per_step": ms_fp,
+                        "roofline": roofline(name, v_fp, ms_fp)}
+        fp["note"] = "lx=31, f=0, guard (w=32, p=2^32+15, 32 slots): the paper's full 5+26 precision, same batch"
+        line["full_precision"] = fp
         # ---- config 5: E2E-shaped ReLU layer streams (CUDA graph per network) ----
         line["config5"] = relu_streams(api, prm, seeds, dev, stream, timed, world)
         # ---- e2e through the public API with pinned HOST buffers ----------------

@@ -45,20 +45,30 @@ extern "C" {
 #define BC_MODE_GUARD   0 /* w = lx + 1, p = 257 at lx = 7 (default; reading C6) */
 #define BC_MODE_LITERAL 1 /* w = lx, the paper's Z_{2^lx} (64-bit wire)  */
 
+/* PRG tape layouts. */
+#define BC_TAPE_WIDE    0 /* lx <= 7, p <= 257 other than the compact case: 64 B / element */
+#define BC_TAPE_COMPACT 1 /* p = 257 and 8 slots (lx = 7 guard): 24 B / element            */
+#define BC_TAPE_LARGE   2 /* lx >= 8, up to 32 slots and p < 2^33: 576 B / element          */
+
 /* Protocol parameters (Alg 7 "Setting"; key bits, sec. 6.1).
  *   ell    ring bits, 2..64
- *   lx     key-bit width ell_x, 2..7 (lx + 1 <= 8 ladder slots)
- *   f      key-bit window offset: the ladder reads bits [f, f+lx+w) (reading C5;
+ *   lx     ladder width ell_x, 2..31 (lx + 1 ladder slots).  lx = 7 is the
+ *          paper's key-bit setting; lx = 31, f = 0 is its full 5+26
+ *          precision without key bits
+ *   f      window offset: the ladder reads bits [f, f+lx+w) (reading C5;
  *          f = 24 keeps 5+2 of the paper's 5+26 fixed point)
  *   mode   BC_MODE_GUARD / BC_MODE_LITERAL
  *   rounds ChaCha rounds 8, 12 or 20 (reading C19)
  * Derived by bc_params_init: w (window width), p (smallest prime > 2^w,
- * reading C7), slots = lx + 1, compact = (p == 257 && slots == 8): the 32-B
- * per-element PRG tape, else the 64-B tape. */
+ * reading C7; 2^32 + 15 at lx = 31 guard), slots = lx + 1, tape (BC_TAPE_*).
+ * Entry points that take a byte-plane message format (bc_ladder_modswitch,
+ * the party phases) need slots <= 8 and p <= 257 (BC_EINVAL otherwise);
+ * bc_drelu / bc_relu accept every tape. */
 typedef struct bc_params {
   int32_t ell, lx, f, mode, rounds;
-  uint32_t w, p, slots;
-  int32_t compact;
+  uint32_t w, slots;
+  int32_t tape;
+  uint64_t p;
 } bc_params;
 
 /* Pre-shared seeds seed01, seed02, seed12. */
@@ -69,8 +79,10 @@ typedef struct bc_seeds {
 } bc_seeds;
 
 /* Optional transcript of the simulated three-party run (bc_drelu / bc_relu):
- * the messages P0 and P1 send to P2 (Alg 7 step 8), in the wire format
- * of bc_drelu_send.  Any pointer may be NULL (that plane is not written). */
+ * the messages P0 and P1 send to P2 (Alg 7 step 8).  Compact and wide
+ * tapes: the wire format of bc_drelu_send, all four planes non-NULL.  Large
+ * tape: w0_lo and w1_lo are uint64_t[n][slots] (W_m in [0, p), 8-B aligned),
+ * w0_hi and w1_hi must be NULL. */
 typedef struct bc_transcript {
   uint8_t *w0_lo, *w0_hi, *w1_lo, *w1_hi;
 } bc_transcript;

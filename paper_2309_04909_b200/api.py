@@ -31,7 +31,10 @@ class BicoptorError(RuntimeError):
 class bc_params(ctypes.Structure):
     _fields_ = [("ell", ctypes.c_int32), ("lx", ctypes.c_int32), ("f", ctypes.c_int32),
                 ("mode", ctypes.c_int32), ("rounds", ctypes.c_int32), ("w", ctypes.c_uint32),
-                ("p", ctypes.c_uint32), ("slots", ctypes.c_uint32), ("compact", ctypes.c_int32)]
+                ("slots", ctypes.c_uint32), ("tape", ctypes.c_int32), ("p", ctypes.c_uint64)]
+
+
+TAPE = {0: "wide", 1: "compact", 2: "large"}
 
 
 class bc_seeds(ctypes.Structure):
@@ -196,15 +199,20 @@ def _fused(fn, what, x0, x1, prm, seeds, elem_base, y0, y1, transcript, stream):
     y1 = torch.empty_like(x1) if y1 is None else y1
     tr = None
     if transcript is not None:
-        tr = bc_transcript(*(_opt(transcript.get(k), k, 1) for k in ("w0_lo", "w0_hi", "w1_lo", "w1_hi")))
+        tr = bc_transcript(*(_opt(transcript.get(k), k, None) for k in ("w0_lo", "w0_hi", "w1_lo", "w1_hi")))
     cp, cs = prm.c(), seeds_struct(seeds)
     _check(fn(_dev(x0, "x0"), _dev(x1, "x1"), _dev(y0, "y0"), _dev(y1, "y1"), n, elem_base, ctypes.byref(cp),
               ctypes.byref(cs), ctypes.byref(tr) if tr is not None else None, _stream(stream)), what)
     return y0, y1
 
 
-def transcript_buffers(n: int, device) -> dict:
-    """Caller-owned buffers for the P0/P1 -> P2 message transcript."""
+def transcript_buffers(n: int, device, prm: "Params | None" = None) -> dict:
+    """Caller-owned buffers for the P0/P1 -> P2 message transcript (large tape:
+    W0, W1 as (n, slots) u64 planes; otherwise the byte wire format)."""
+    if prm is not None and prm.lx >= 8:
+        S = prm.lx + 1
+        return {"w0_lo": torch.empty((n, S), dtype=torch.int64, device=device),
+                "w1_lo": torch.empty((n, S), dtype=torch.int64, device=device)}
     return {"w0_lo": torch.empty((n, 8), dtype=torch.uint8, device=device),
             "w0_hi": torch.empty(n, dtype=torch.uint8, device=device),
             "w1_lo": torch.empty((n, 8), dtype=torch.uint8, device=device),

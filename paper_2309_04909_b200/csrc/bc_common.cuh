@@ -16,6 +16,7 @@
 
 #include "bc_compact.cuh"
 #include "bc_device.cuh"
+#include "bc_large.cuh"
 #include "bicoptor.h"
 
 namespace bc {
@@ -47,7 +48,8 @@ __device__ __forceinline__ uint64_t load_hi8(const uint8_t* hi, uint64_t i0, uin
 // ---- host utilities (bc_host.cu) ------------------------------------------
 namespace host {
 int check_launch();                                  // cudaGetLastError -> BC_OK / BC_ECUDA
-int grid_for(const void* fn, uint64_t nthreads_work);  // persistent grid size
+int grid_for(const void* fn, uint64_t nthreads_work, int tpb = TPB);  // persistent grid size
+KPL make_kpl(const bc_params* prm);                  // large-tape constants (p < 2^33)
 bool aligned16(const void* p);
 bool aligned8(const void* p);
 bool overlap(const void* a, size_t na, const void* b, size_t nb);

@@ -200,10 +200,11 @@ int bc_ladder_modswitch(int party, const uint64_t* x, uint8_t* v, size_t n, cons
   if (rc) return rc;
   if (n == 0) return BC_OK;  // no-op after parameter validation
   if (party != 0 && party != 1) return BC_EINVAL;
+  if (prm->tape == BC_TAPE_LARGE) return BC_EINVAL;  // byte format: slots <= 8, p <= 257
   if (!aligned16(x) || !aligned16(v)) return BC_EALIGN;
   if (overlap(x, n * 8, v, n * 8)) return BC_EALIAS;
   const KP kp = make_kp(prm);
-  const int compact = prm->compact;
+  const int compact = prm->tape == BC_TAPE_COMPACT;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint64_t* vo = reinterpret_cast<uint64_t*>(v);
   if (party == 0)

@@ -177,6 +177,40 @@ __global__ void __launch_bounds__(TPB, 2) k_fused_w(FusedArgs a, KP kp, Key k01,
   }
 }
 
+// Large tape (lx >= 8, up to 32 slots, p < 2^33): 9 seed01 blocks per element,
+// the 8 elements of a group in sequence, then the shared finish.
+constexpr int TPB_L = 128;
+
+template <int R, bool RELU, bool TRANSCRIPT>
+__global__ void __launch_bounds__(TPB_L) k_fused_l(FusedArgs a, KP kp, KPL kl, Key k01, Key k02, Key k12) {
+  __shared__ uint8_t sidx[32 * TPB_L];
+  __shared__ uint32_t magic[33], hlim[33];
+  for (uint32_t s = threadIdx.x; s < 33; s += blockDim.x) {
+    magic[s] = s >= 2 ? 0xFFFFFFFFu / s + 1u : 0u;  // ceil(2^32 / s)
+    hlim[s] = s >= 2 ? (65536u / s) * s : 0u;
+  }
+  __syncthreads();
+  uint8_t* idx = sidx + threadIdx.x;
+  const uint64_t ngroups = (a.n + 7) >> 3;
+  for (uint64_t g = (uint64_t)blockIdx.x * TPB_L + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB_L) {
+    const uint64_t i0 = g << 3;
+    const uint64_t j0 = a.base + i0;
+    const uint32_t cnt = (uint32_t)min((uint64_t)8, a.n - i0);
+    uint32_t zbits = 0, tbits = 0;
+#pragma unroll 1
+    for (uint32_t e = 0; e < cnt; ++e) {
+      const uint64_t i = i0 + e;
+      uint64_t* w0 = TRANSCRIPT ? reinterpret_cast<uint64_t*>(a.w0lo) + i * kl.S : nullptr;
+      uint64_t* w1 = TRANSCRIPT ? reinterpret_cast<uint64_t*>(a.w1lo) + i * kl.S : nullptr;
+      const uint32_t r =
+          elem_large<R, TRANSCRIPT, TPB_L>(__ldg(a.x0 + i), __ldg(a.x1 + i), j0 + e, k01, kl, idx, magic, hlim, w0, w1);
+      zbits |= (r & 1u) << e;
+      tbits |= (r >> 1) << e;
+    }
+    finish_group<R, RELU>(a, kp, k02, k12, i0, j0, cnt, zbits, tbits);
+  }
+}
+
 template <bool RELU>
 int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, size_t n, uint64_t base,
           const bc_params* prm, const bc_seeds* seeds, const bc_transcript* tr, void* stream) {
@@ -190,7 +224,18 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
       overlap(y1, nb, x1, nb))
     return BC_EALIAS;
   FusedArgs a{x0, x1, y0, y1, (uint64_t)n, base, nullptr, nullptr, nullptr, nullptr};
-  if (tr) {  // the transcript is all-or-nothing
+  const bool large = prm->tape == BC_TAPE_LARGE;
+  if (tr && large) {  // W planes as uint64_t[n][slots]
+    if (!tr->w0_lo || !tr->w1_lo || tr->w0_hi || tr->w1_hi) return BC_EINVAL;
+    if (!aligned8(tr->w0_lo) || !aligned8(tr->w1_lo)) return BC_EALIGN;
+    const size_t wb = n * prm->slots * 8;
+    if (overlap(tr->w0_lo, wb, tr->w1_lo, wb) || overlap(tr->w0_lo, wb, x0, nb) || overlap(tr->w0_lo, wb, x1, nb) ||
+        overlap(tr->w1_lo, wb, x0, nb) || overlap(tr->w1_lo, wb, x1, nb) || overlap(tr->w0_lo, wb, y0, nb) ||
+        overlap(tr->w0_lo, wb, y1, nb) || overlap(tr->w1_lo, wb, y0, nb) || overlap(tr->w1_lo, wb, y1, nb))
+      return BC_EALIAS;
+    a.w0lo = tr->w0_lo;
+    a.w1lo = tr->w1_lo;
+  } else if (tr) {  // the transcript is all-or-nothing
     if (!tr->w0_lo || !tr->w0_hi || !tr->w1_lo || !tr->w1_hi) return BC_EINVAL;
     if (!aligned8(tr->w0_lo) || !aligned8(tr->w1_lo)) return BC_EALIGN;
     a.w0lo = tr->w0_lo;
@@ -204,7 +249,11 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
   const uint64_t ngroups = (n + 7) / 8;
   return dispatch_rounds(prm->rounds, [&](auto Rc) {
     constexpr int R = decltype(Rc)::value;
-    if (prm->compact) {
+    if (large) {
+      const KPL kl = make_kpl(prm);
+      auto fn = tr ? k_fused_l<R, RELU, true> : k_fused_l<R, RELU, false>;
+      fn<<<grid_for((const void*)fn, ngroups, TPB_L), TPB_L, 0, st>>>(a, kp, kl, k01, k02, k12);
+    } else if (prm->tape == BC_TAPE_COMPACT) {
       auto fn = tr ? k_fused_c<R, RELU, true> : k_fused_c<R, RELU, false>;
       fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k01, k02, k12);
     } else {

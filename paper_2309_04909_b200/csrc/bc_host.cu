@@ -7,9 +7,9 @@
 namespace {
 thread_local int g_last_cuda = 0;
 
-bool is_prime(uint32_t v) {
+bool is_prime(uint64_t v) {
   if (v < 2) return false;
-  for (uint32_t d = 2; (uint64_t)d * d <= v; ++d)
+  for (uint64_t d = 2; d * d <= v; ++d)
     if (v % d == 0) return false;
   return true;
 }
@@ -34,7 +34,7 @@ int check_launch() {
 }
 
 // Persistent grid: min(#work blocks, #SM x resident blocks per SM), cached per (kernel, device).
-int grid_for(const void* fn, uint64_t nthreads_work) {
+int grid_for(const void* fn, uint64_t nthreads_work, int tpb) {
   struct Entry {
     const void* fn;
     int dev;
@@ -56,12 +56,12 @@ int grid_for(const void* fn, uint64_t nthreads_work) {
     if (!cap) {
       int sms = 0, occ = 0;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, TPB, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, tpb, 0);
       cap = std::max(1, sms) * std::max(1, occ);
       if (ncache < 512) cache[ncache++] = Entry{fn, dev, cap};
     }
   }
-  const uint64_t want = (nthreads_work + TPB - 1) / TPB;
+  const uint64_t want = (nthreads_work + (uint64_t)tpb - 1) / (uint64_t)tpb;
   return (int)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)cap));
 }
 
@@ -79,7 +79,7 @@ int check_params(const bc_params* prm) {
   bc_params ref;
   const int rc = bc_params_init(&ref, prm->ell, prm->lx, prm->f, prm->mode, prm->rounds);
   if (rc) return rc;
-  if (ref.w != prm->w || ref.p != prm->p || ref.slots != prm->slots || ref.compact != prm->compact) return BC_EINVAL;
+  if (ref.w != prm->w || ref.p != prm->p || ref.slots != prm->slots || ref.tape != prm->tape) return BC_EINVAL;
   return BC_OK;
 }
 
@@ -90,15 +90,43 @@ KP make_kp(const bc_params* prm) {
   kp.fsh = (uint32_t)prm->f & 31u;
   kp.fhi = prm->f >= 32 ? 1u : 0u;
   kp.w = prm->w;
-  kp.p = prm->p;
+  kp.p = (uint32_t)prm->p;  // only used by the p <= 257 tapes
   kp.S = prm->slots;
   kp.lx = (uint32_t)prm->lx;
-  kp.wmask = (1u << prm->w) - 1u;
-  kp.fact = factorial(prm->slots);
-  kp.perm_lim = (uint32_t)((0x80000000ull / kp.fact) * kp.fact);
-  kp.mask_lim = (65536u / (prm->p - 1u)) * (prm->p - 1u);
-  kp.rho_lim = (65536u / prm->p) * prm->p;
+  kp.wmask = (uint32_t)((1ull << prm->w) - 1ull);
+  if (prm->tape != BC_TAPE_LARGE) {
+    kp.fact = factorial(prm->slots);
+    kp.perm_lim = (uint32_t)((0x80000000ull / kp.fact) * kp.fact);
+    kp.mask_lim = (65536u / (kp.p - 1u)) * (kp.p - 1u);
+    kp.rho_lim = (65536u / kp.p) * kp.p;
+  }
   return kp;
+}
+
+KPL make_kpl(const bc_params* prm) {
+  using u128 = unsigned __int128;
+  KPL k{};
+  const uint64_t p = prm->p, q = p - 1;
+  k.ymask = prm->ell == 64 ? ~0ull : ((1ull << prm->ell) - 1ull);
+  k.wmask = (1ull << prm->w) - 1ull;
+  k.p = p;
+  uint64_t inv = p;  // p^-1 mod 2^64 by Newton (p odd: correct to 3 bits, doubling per step)
+  for (int i = 0; i < 5; ++i) inv *= 2ull - p * inv;
+  k.pinv = 0ull - inv;
+  const uint64_t r1 = (uint64_t)(((u128)1 << 64) % p);
+  k.r2 = (uint64_t)(((u128)r1 * r1) % p);
+  k.mu_p = ~0ull / p;
+  k.mu_q = ~0ull / q;
+  const u128 two64 = (u128)1 << 64;
+  const u128 pl = two64 / p * p, ql = two64 / q * q;
+  k.plim = pl == two64 ? 0ull : (uint64_t)pl;
+  k.qlim = ql == two64 ? 0ull : (uint64_t)ql;
+  k.two_w = (1ull << prm->w) % p;
+  k.off1 = p - (1ull << prm->w);
+  k.f = (uint32_t)prm->f;
+  k.w = prm->w;
+  k.S = prm->slots;
+  return k;
 }
 
 Key make_key(const uint8_t* s) {
@@ -113,7 +141,7 @@ Key make_key(const uint8_t* s) {
 
 extern "C" {
 
-int bc_version(void) { return 101; }
+int bc_version(void) { return 200; }
 
 int bc_last_cuda_error(void) { return g_last_cuda; }
 
@@ -131,12 +159,12 @@ const char* bc_strerror(int code) {
 
 int bc_params_init(bc_params* out, int ell, int lx, int f, int mode, int rounds) {
   if (!out) return BC_EINVAL;
-  if (ell < 2 || ell > 64 || lx < 2 || lx > 7 || f < 0 || (mode != BC_MODE_GUARD && mode != BC_MODE_LITERAL) ||
+  if (ell < 2 || ell > 64 || lx < 2 || lx > 31 || f < 0 || (mode != BC_MODE_GUARD && mode != BC_MODE_LITERAL) ||
       (rounds != 8 && rounds != 12 && rounds != 20))
     return BC_EINVAL;
   const uint32_t w = (uint32_t)(mode == BC_MODE_GUARD ? lx + 1 : lx);
   if ((uint64_t)f + (uint64_t)lx + w > (uint64_t)ell) return BC_ERANGE;
-  uint32_t p = (1u << w) + 1u;  // smallest prime > 2^w (reading C7)
+  uint64_t p = (1ull << w) + 1ull;  // smallest prime > 2^w (reading C7)
   while (!is_prime(p)) ++p;
   bc_params r;
   r.ell = ell;
@@ -147,7 +175,7 @@ int bc_params_init(bc_params* out, int ell, int lx, int f, int mode, int rounds)
   r.w = w;
   r.p = p;
   r.slots = (uint32_t)lx + 1u;
-  r.compact = (p == 257u && r.slots == 8u) ? 1 : 0;
+  r.tape = (p == 257u && r.slots == 8u) ? BC_TAPE_COMPACT : (lx <= 7 ? BC_TAPE_WIDE : BC_TAPE_LARGE);
   *out = r;
   return BC_OK;
 }

@@ -1,0 +1,159 @@
+// bc_large.cuh -- Alg 7 steps 1-9 for the large tape (lx >= 8: up to 32
+// ladder slots, p < 2^33).  Full precision lx = 31, f = 0 without key bits is
+// the paper's "31 * 31 ~ 1,000 bits" regime (Table 1).
+//
+// Per element: 9 ChaCha blocks from seed01 (large):
+//   block 0     t and the Fisher-Yates draws (u16, rejection),
+//   blocks 1-4  mask draws r_m (u64 -> 1 + u mod (p-1), rejection),
+//   blocks 5-8  reshare draws rho_m (u64 -> u mod p, rejection),
+// streamed in (r, rho) block pairs so at most 32 keystream words are live.
+// Arithmetic mod p: Montgomery products (R = 2^64) for W = v'r, Barrett
+// reductions for the draws.  The permutation is kept as a byte table per
+// thread in shared memory ([slot][thread], conflict-free) and applied by
+// evaluating slot m's source window v'_{Pi(m)} directly from the share.
+#pragma once
+#include <cstdint>
+
+#include "bc_device.cuh"
+
+namespace bc {
+
+constexpr uint64_t L_TAPEL = lbl("bc2.tpL1");  // seed01, 576 B / element (9 blocks at counter 9j + b)
+constexpr uint64_t L_FBL = lbl("bc2.fbL1");    // seed01, large-tape fallback: u64 words, counter j*2^20 + k
+
+struct KPL {
+  uint64_t ymask;     // 2^ell - 1
+  uint64_t wmask;     // 2^w - 1
+  uint64_t p;         // modulus, odd, < 2^33
+  uint64_t pinv;      // -p^-1 mod 2^64 (Montgomery)
+  uint64_t r2;        // 2^128 mod p
+  uint64_t mu_p;      // floor((2^64-1) / p)      (Barrett)
+  uint64_t mu_q;      // floor((2^64-1) / (p-1))
+  uint64_t plim;      // floor(2^64/p) p, 0 = no rejection (2^64)
+  uint64_t qlim;      // floor(2^64/(p-1)) (p-1), 0 = no rejection
+  uint64_t two_w;     // 2^w mod p (P0's image of 0, Alg 6)
+  uint64_t off1;      // p - 2^w   (P1's modswitch offset, Alg 6)
+  uint32_t f, w, S;
+};
+
+// a * b * 2^-64 mod p for a, b < p (REDC; t < 2p before the final subtraction).
+__device__ __forceinline__ uint64_t mont(uint64_t a, uint64_t b, const KPL& kp) {
+  const uint64_t lo = a * b, hi = __umul64hi(a, b);
+  const uint64_t m = lo * kp.pinv;
+  const uint64_t t = hi + __umul64hi(m, kp.p) + (lo != 0 ? 1ull : 0ull);
+  return t >= kp.p ? t - kp.p : t;
+}
+
+// u mod q with mu = floor((2^64-1)/q): the quotient estimate is low by at most 1.
+__device__ __forceinline__ uint64_t barrett(uint64_t u, uint64_t q, uint64_t mu) {
+  const uint64_t r = u - __umul64hi(u, mu) * q;
+  return r >= q ? r - q : r;
+}
+
+__device__ __forceinline__ bool accept64(uint64_t u, uint64_t lim) { return lim == 0 || u < lim; }
+
+// c-th u64 word of element j's fallback stream (rare path, kept out of line).
+template <int R>
+__device__ __noinline__ uint64_t fbl_word(Key k01, uint64_t j, uint32_t c) {
+  uint32_t B[16];
+  chacha<R>(k01, (j << 20) + (c >> 3), L_FBL, B);
+  const uint32_t e = c & 7u;
+  uint64_t v = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if ((uint32_t)i == e) v = (uint64_t)B[2 * i] | ((uint64_t)B[2 * i + 1] << 32);
+  return v;
+}
+
+// Ladder source slot i of Alg 7 steps 3-5 for both parties (s0, s1 blinded
+// shares, ns1 = -s1 mod 2^ell): returns P0's c'_i and P1's d'_i in [0, p).
+__device__ __forceinline__ void slot_values(uint64_t s0, uint64_t ns1, uint32_t i, const KPL& kp, uint64_t& c,
+                                            uint64_t& d) {
+  const uint32_t sh = kp.f + i;
+  const uint64_t a_i = (s0 >> sh) & kp.wmask;
+  const uint64_t b_i = (0ull - ((ns1 >> sh) & kp.wmask)) & kp.wmask;   // Alg 5, P1 (readings C3, C4)
+  uint64_t cv, dv;
+  if (i + 1 < kp.S) {
+    const uint64_t a_n = (s0 >> (sh + 1)) & kp.wmask;
+    const uint64_t b_n = (0ull - ((ns1 >> (sh + 1)) & kp.wmask)) & kp.wmask;
+    cv = (a_i + a_n - 1ull) & kp.wmask;                                  // step 4: P0 carries the -1 (C8)
+    dv = (b_i + b_n) & kp.wmask;
+  } else {
+    cv = (a_i - 1ull) & kp.wmask;
+    dv = b_i;
+  }
+  c = cv == 0 ? kp.two_w : cv;                                           // step 5 (Alg 6), P0
+  d = dv + kp.off1;                                                      //                 P1: p + d - 2^w
+}
+
+// Alg 7 steps 1-9 for element j with shares x0, x1: returns DReLU' (bit 0)
+// and t (bit 1).  idx: this thread's column of the [32][TPB] byte table.
+// magic[s] = ceil(2^32 / s), hlim[s] = floor(2^16 / s) s for s = 2..32.
+template <int R, bool TRANSCRIPT, int TPB_L>
+__device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_t j, const Key& k01, const KPL& kp,
+                                               uint8_t* idx, const uint32_t* magic, const uint32_t* hlim,
+                                               uint64_t* w0, uint64_t* w1) {
+  const uint32_t S = kp.S;
+  uint32_t fbc = 0;  // fallback words consumed
+  uint32_t t;
+  {
+    uint32_t B[16];
+    chacha<R>(k01, j * 9, L_TAPEL, B);
+    t = B[0] & 1u;
+#pragma unroll
+    for (uint32_t m = 0; m < 32; ++m) idx[m * TPB_L] = (uint8_t)m;
+    // step 6: Fisher-Yates, slot m = S-1 .. 1 draws h[S-m] (q = S - m)
+#pragma unroll
+    for (uint32_t q = 1; q < 32; ++q) {
+      if (q < S) {
+        const uint32_t m = S - q, s = m + 1;
+        uint32_t d = (B[q >> 1] >> (16 * (q & 1))) & 0xFFFFu;
+        while (d >= hlim[s]) d = (uint32_t)fbl_word<R>(k01, j, fbc++) & 0xFFFFu;
+        const uint32_t k = d - __umulhi(d, magic[s]) * s;
+        const uint8_t a = idx[m * TPB_L], b = idx[k * TPB_L];
+        idx[m * TPB_L] = b;
+        idx[k * TPB_L] = a;
+      }
+    }
+  }
+  // steps 1-2: blind both shares by (-1)^t
+  const uint64_t s0 = t ? (0ull - x0) & kp.ymask : x0 & kp.ymask;
+  const uint64_t s1 = t ? (0ull - x1) & kp.ymask : x1 & kp.ymask;
+  const uint64_t ns1 = (0ull - s1) & kp.ymask;
+  uint32_t z = 0;
+#pragma unroll 1
+  for (uint32_t b = 0; b < 4; ++b) {
+    if (8 * b >= S) break;
+    uint32_t Br[16], Bq[16];
+    chacha<R>(k01, j * 9 + 1 + b, L_TAPEL, Br);
+    chacha<R>(k01, j * 9 + 5 + b, L_TAPEL, Bq);
+#pragma unroll
+    for (uint32_t e = 0; e < 8; ++e) {
+      const uint32_t m = 8 * b + e;
+      if (m < S) {
+        uint64_t ur = (uint64_t)Br[2 * e] | ((uint64_t)Br[2 * e + 1] << 32);
+        while (!accept64(ur, kp.qlim)) ur = fbl_word<R>(k01, j, fbc++);
+        uint64_t uq = (uint64_t)Bq[2 * e] | ((uint64_t)Bq[2 * e + 1] << 32);
+        while (!accept64(uq, kp.plim)) uq = fbl_word<R>(k01, j, fbc++);
+        const uint64_t r = 1ull + barrett(ur, kp.p - 1ull, kp.mu_q);   // r_m in Z_p^*
+        const uint64_t rho = barrett(uq, kp.p, kp.mu_p);               // rho_m in Z_p
+        uint64_t c, d;
+        slot_values(s0, ns1, idx[m * TPB_L], kp, c, d);                // v'_{Pi(m)} of each party
+        const uint64_t rM = mont(r, kp.r2, kp);                        // r * 2^64 mod p
+        uint64_t W0 = mont(c, rM, kp) + rho;                           // step 7-8, P0: v'r + rho
+        W0 = W0 >= kp.p ? W0 - kp.p : W0;
+        uint64_t W1 = mont(d, rM, kp) + (kp.p - rho);                  //           P1: v'r - rho
+        W1 = W1 >= kp.p ? W1 - kp.p : W1;
+        if (TRANSCRIPT) {
+          w0[m] = W0;
+          w1[m] = W1;
+        }
+        const uint64_t sum = W0 + W1;                                  // step 9 (P2): w_m = 0 mod p?
+        z |= (sum == 0 || sum == kp.p) ? 1u : 0u;
+      }
+    }
+  }
+  return z | (t << 1);
+}
+
+}  // namespace bc

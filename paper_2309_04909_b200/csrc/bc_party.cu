@@ -268,6 +268,7 @@ int send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits,
   if (rc) return rc;
   if (n == 0) return BC_OK;  // no-op after parameter validation
   if ((party != 0 && party != 1) || !x || !lo || !tbits || !s01 || (RELU && (!dshare || !str))) return BC_EINVAL;
+  if (prm->tape == BC_TAPE_LARGE) return BC_EINVAL;  // byte-plane wire format: slots <= 8, p <= 257
   if (!hi && prm->p > 256) return BC_EINVAL;
   if (!aligned16(x) || !aligned16(lo) || (hi && !aligned8(hi)) || (RELU && !aligned16(dshare)) || (base & 7))
     return BC_EALIGN;
@@ -284,7 +285,7 @@ int send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits,
   return dispatch_rounds(prm->rounds, [&](auto Rc) {
     constexpr int R = decltype(Rc)::value;
     auto go = [&](auto fn) { fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k01, ktr); };
-    if (prm->compact) {
+    if (prm->tape == BC_TAPE_COMPACT) {
       if (party == 0) go(k_send_c<R, 0, RELU>);
       else go(k_send_c<R, 1, RELU>);
     } else {
@@ -303,6 +304,7 @@ int helper(const uint8_t* lo0, const uint8_t* hi0, const uint8_t* lo1, const uin
   if (rc) return rc;
   if (n == 0) return BC_OK;  // no-op after parameter validation
   if (!lo0 || !lo1 || !s02 || (RELU && (!s12 || !out0)) || (!RELU && !out1)) return BC_EINVAL;
+  if (prm->tape == BC_TAPE_LARGE) return BC_EINVAL;  // byte-plane wire format: slots <= 8, p <= 257
   if (prm->p > 256 && (!hi0 || !hi1)) return BC_EINVAL;
   if (!aligned16(lo0) || !aligned16(lo1) || (hi0 && !aligned8(hi0)) || (hi1 && !aligned8(hi1)) ||
       (out0 && !aligned16(out0)) || (out1 && !aligned16(out1)) || (base & 7))

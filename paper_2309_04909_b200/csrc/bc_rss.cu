@@ -166,7 +166,7 @@ int fused_rss(const uint64_t* x0, const uint64_t* x1, const uint64_t* x2, uint64
               const uint8_t* s2, void* stream) {
   const int rc = check_params(prm);
   if (rc) return rc;
-  if (!prm->compact) return BC_EINVAL;  // RSS path: compact tape (p = 257, 8 slots) only
+  if (prm->tape != BC_TAPE_COMPACT) return BC_EINVAL;  // RSS path: compact tape (p = 257, 8 slots) only
   if (n == 0) return BC_OK;
   if (!x0 || !x1 || !x2 || !y0 || !y1 || !y2 || !seeds || !s012 || !s2) return BC_EINVAL;
   if (!aligned16(x0) || !aligned16(x1) || !aligned16(x2) || !aligned16(y0) || !aligned16(y1) || !aligned16(y2) ||

@@ -43,7 +43,7 @@ def test_params_derivation_matches_oracle(lib):
     from oracle import bicoptor as B
     from paper_2309_04909_b200 import api
     for ell in (8, 16, 32, 64):
-        for lx in range(2, 8):
+        for lx in (2, 3, 5, 7, 8, 12, 15, 16, 30, 31, 32):
             for mode in ("guard", "literal"):
                 for f in (0, 1, 24):
                     try:
@@ -53,7 +53,7 @@ def test_params_derivation_matches_oracle(lib):
                             api.Params(ell=ell, lx=lx, f=f, mode=mode, rounds=12).c()
                         continue
                     c = api.Params(ell=ell, lx=lx, f=f, mode=mode, rounds=12).c()
-                    assert (c.w, c.p, c.slots, bool(c.compact)) == (o.w, o.p, o.slots, o.compact)
+                    assert (c.w, c.p, c.slots, api.TAPE[c.tape]) == (o.w, o.p, o.slots, o.layout)
 
 
 def test_errors_and_strerror(lib):
@@ -65,4 +65,5 @@ def test_errors_and_strerror(lib):
     assert b"window" in lib.bc_strerror(-2)
     # a NULL-pointer call is rejected on the host before any launch
     assert lib.bc_drelu(None, None, None, None, 8, 0, ctypes.byref(api.Params().c()), None, None, None) == -1
-    assert lib.bc_version() >= 101
+    assert lib.bc_version() >= 200
+    assert ctypes.sizeof(api.bc_params) == 40

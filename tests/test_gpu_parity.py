@@ -378,3 +378,94 @@ def test_rss_abi_errors(api):
     assert call(None, *p[1:]) == -1
     wide = api.Params(ell=16, lx=7, f=0, mode="literal").c()
     assert call(*p, prm=wide) == -1                              # compact tape only
+
+
+# ---- large tape: lx >= 8, full precision lx = 31 (NEXT #2) ------------------------------
+
+LARGE_PARAMS = [
+    dict(ell=64, lx=31, f=0, mode="guard", rounds=20),     # full 5+26 precision, p = 2^32 + 15
+    dict(ell=64, lx=31, f=0, mode="literal", rounds=12),   # the paper's Z_{2^31}, p = 2^31 + 11
+    dict(ell=24, lx=10, f=0, mode="guard", rounds=8),
+    dict(ell=20, lx=8, f=1, mode="guard", rounds=20),
+    dict(ell=40, lx=15, f=3, mode="guard", rounds=8),      # p = 65537: p - 1 = 2^16, no mask rejection
+]
+
+
+@pytest.mark.parametrize("kw", LARGE_PARAMS, ids=_ids)
+@pytest.mark.parametrize("fn", ["drelu", "relu"])
+def test_large_parity_with_transcript(api, kw, fn):
+    oprm = B.Params(**kw)
+    prm = api.Params(**kw)
+    for n in (1, 7, 9, 203):
+        for base in (0, 1 << 40):
+            x, x0, x1 = synth.shares(n, kw["ell"], kw["lx"], kw["f"], "D1", run=n)
+            j = np.arange(n, dtype=np.uint64) + np.uint64(base)
+            ref = getattr(B, fn)(oprm, x0, x1, j, SEEDS)
+            tr = api.transcript_buffers(n, DEV, prm)
+            y0, y1 = getattr(api, fn)(dev(x0), dev(x1), prm, SEEDS, elem_base=base, transcript=tr)
+            assert np.array_equal(host(y0), ref["y0"]), (n, base)
+            assert np.array_equal(host(y1), ref["y1"]), (n, base)
+            assert np.array_equal(host(tr["w0_lo"]), ref["W0"]) and np.array_equal(host(tr["w1_lo"]), ref["W1"])
+
+
+def test_large_fallback_elements(api):
+    """Elements whose Fisher-Yates draws reject (~0.35 % at 32 slots) take the
+    fallback stream; they must match the oracle, messages included."""
+    from test_oracle_fullprec import _raw_perm_rejects
+    kw = LARGE_PARAMS[0]
+    oprm, prm = B.Params(**kw), api.Params(**kw)
+    rej, _ = _raw_perm_rejects(oprm, np.arange(8000, dtype=np.uint64))
+    rows = np.nonzero(rej)[0][:8]
+    assert len(rows) >= 5
+    for r in rows:
+        base = int(r) - int(r) % 8
+        x, x0, x1 = synth.shares(16, 64, 31, 0, "D2", run=int(r))
+        j = np.arange(16, dtype=np.uint64) + np.uint64(base)
+        for fn in ("drelu", "relu"):
+            ref = getattr(B, fn)(oprm, x0, x1, j, SEEDS)
+            tr = api.transcript_buffers(16, DEV, prm)
+            y0, y1 = getattr(api, fn)(dev(x0), dev(x1), prm, SEEDS, elem_base=base, transcript=tr)
+            assert np.array_equal(host(y0), ref["y0"]) and np.array_equal(host(y1), ref["y1"])
+            assert np.array_equal(host(tr["w0_lo"]), ref["W0"])
+
+
+@pytest.mark.parametrize("fn", ["drelu", "relu"])
+def test_full_precision_full_size_sampled(api, fn):
+    """lx = 31, f = 0, 2^24 elements in the launch the bench times: oracle parity on
+    a 2^10 sample; opened sign / ReLU on every nonzero element."""
+    n = 1 << 24
+    kw = LARGE_PARAMS[0]
+    x, x0, x1 = synth.shares(n, 64, 7, 24, "D2")          # the bench batch: |x| < 2^31
+    y0, y1 = getattr(api, fn)(dev(x0), dev(x1), api.Params(**kw), SEEDS)
+    g0, g1 = host(y0), host(y1)
+    idx = np.sort(np.random.default_rng(13).choice(n, 1 << 10, replace=False)).astype(np.uint64)
+    ref = getattr(B, fn)(B.Params(**kw), x0[idx], x1[idx], idx, SEEDS)
+    assert np.array_equal(g0[idx], ref["y0"]) and np.array_equal(g1[idx], ref["y1"])
+    with np.errstate(over="ignore"):
+        y = g0 + g1
+    s, valid = band_sign(x, 64, 31, 0)
+    want = s if fn == "drelu" else relu_plain(x, 64, 31, 0)
+    assert np.array_equal(y[valid], want[valid])
+
+
+def test_large_abi_errors(api):
+    import ctypes
+    L = api.lib()
+    cp = api.Params(ell=64, lx=31, f=0).c()
+    assert cp.p == 2**32 + 15 and cp.slots == 32 and api.TAPE[cp.tape] == "large"
+    t = torch.zeros(16, dtype=torch.int64, device=DEV)
+    v = torch.zeros((16, 8), dtype=torch.uint8, device=DEV)
+    # byte-plane formats hold at most 8 slots
+    assert L.bc_ladder_modswitch(0, t.data_ptr(), v.data_ptr(), 16, ctypes.byref(cp), None) == -1
+    assert L.bc_drelu_send(0, t.data_ptr(), v.data_ptr(), v.data_ptr(), v.data_ptr(), 16, 0, ctypes.byref(cp),
+                           SEEDS.s01, None) == -1
+    # large transcript: u64 planes, hi planes must be NULL
+    w = [torch.zeros((16, 32), dtype=torch.int64, device=DEV) for _ in range(2)]
+    ys = [torch.zeros(16, dtype=torch.int64, device=DEV) for _ in range(3)]
+    cs = api.seeds_struct(SEEDS)
+    bad = api.bc_transcript(w[0].data_ptr(), v.data_ptr(), w[1].data_ptr(), None)
+    assert L.bc_drelu(t.data_ptr(), ys[2].data_ptr(), ys[0].data_ptr(), ys[1].data_ptr(), 16, 0, ctypes.byref(cp),
+                      ctypes.byref(cs), ctypes.byref(bad), None) == -1
+    ok = api.bc_transcript(w[0].data_ptr(), None, w[1].data_ptr(), None)
+    assert L.bc_drelu(t.data_ptr(), ys[2].data_ptr(), ys[0].data_ptr(), ys[1].data_ptr(), 16, 0, ctypes.byref(cp),
+                      ctypes.byref(cs), ctypes.byref(ok), None) == 0
