@@ -219,7 +219,10 @@ def _tape_large(prm: Params, seed01: bytes, j) -> dict:
     P:195).  576 B = 9 ChaCha blocks per element at 576 j (label bc2.tpL1):
       block 0:    32 u16 h; t = h[0] & 1; the Fisher-Yates draw of slot m
                   (m = S-1 .. 1) is h[S-m]: k_m = h mod (m+1), reject h >= floor(2^16/(m+1))(m+1);
-      blocks 1-4: 32 u64 mask draws u_m: r_m = 1 + u_m mod (p-1), reject u >= floor(2^64/(p-1))(p-1);
+      blocks 1-4: 32 u64 mask draws u_m: r_m = (1 + u_m mod (p-1)) * 2^-64 mod p,
+                  reject u >= floor(2^64/(p-1))(p-1) -- multiplying by the unit 2^-64 is a
+                  bijection of Z_p^*, so r_m is still uniform on Z_p^* (the draw is the
+                  mask's Montgomery form, which is what a Montgomery multiplier consumes);
       blocks 5-8: 32 u64 reshare draws u_m: rho_m = u_m mod p, reject u >= floor(2^64/p) p.
     Slots m >= S leave their draws unused.  A rejected draw -- in the order
     k_{S-1} .. k_1, then r_0, rho_0, r_1, rho_1, .., r_{S-1}, rho_{S-1} -- is replaced by the next
@@ -233,6 +236,7 @@ def _tape_large(prm: Params, seed01: bytes, j) -> dict:
     k = np.zeros((n, S), dtype=np.int64)
     hlim = {m: (65536 // (m + 1)) * (m + 1) for m in range(1, S)}
     rlim, plim = ((1 << 64) // (p - 1)) * (p - 1), ((1 << 64) // p) * p   # 2^64 when q | 2^64: no rejection
+    rinv = pow(2, -64, p)                                                  # 2^-64 mod p
     r = np.empty((n, S), dtype=object)
     rho = np.empty((n, S), dtype=object)
     for row in range(n):
@@ -248,7 +252,7 @@ def _tape_large(prm: Params, seed01: bytes, j) -> dict:
             while u >= rlim:
                 fb = fb or _fallback_u64(seed01, int(j[row]), prm.rounds)
                 u = next(fb)
-            r[row, m] = 1 + u % (p - 1)
+            r[row, m] = (1 + u % (p - 1)) * rinv % p
             u = int(U[row, 32 + m])
             while u >= plim:
                 fb = fb or _fallback_u64(seed01, int(j[row]), prm.rounds)
