@@ -184,6 +184,7 @@ constexpr int TPB_L = 128;
 template <int R, bool RELU, bool TRANSCRIPT>
 __global__ void __launch_bounds__(TPB_L) k_fused_l(FusedArgs a, KP kp, KPL kl, Key k01, Key k02, Key k12) {
   __shared__ uint8_t sidx[32 * TPB_L];
+  __shared__ uint32_t sstg[32 * TPB_L];
   __shared__ uint32_t magic[33], hlim[33];
   for (uint32_t s = threadIdx.x; s < 33; s += blockDim.x) {
     magic[s] = s >= 2 ? 0xFFFFFFFFu / s + 1u : 0u;  // ceil(2^32 / s)
@@ -191,6 +192,7 @@ __global__ void __launch_bounds__(TPB_L) k_fused_l(FusedArgs a, KP kp, KPL kl, K
   }
   __syncthreads();
   uint8_t* idx = sidx + threadIdx.x;
+  uint32_t* stg = sstg + threadIdx.x;
   const uint64_t ngroups = (a.n + 7) >> 3;
   for (uint64_t g = (uint64_t)blockIdx.x * TPB_L + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB_L) {
     const uint64_t i0 = g << 3;
@@ -203,7 +205,7 @@ __global__ void __launch_bounds__(TPB_L) k_fused_l(FusedArgs a, KP kp, KPL kl, K
       uint64_t* w0 = TRANSCRIPT ? reinterpret_cast<uint64_t*>(a.w0lo) + i * kl.S : nullptr;
       uint64_t* w1 = TRANSCRIPT ? reinterpret_cast<uint64_t*>(a.w1lo) + i * kl.S : nullptr;
       const uint32_t r =
-          elem_large<R, TRANSCRIPT, TPB_L>(__ldg(a.x0 + i), __ldg(a.x1 + i), j0 + e, k01, kl, idx, magic, hlim, w0, w1);
+          elem_large<R, TRANSCRIPT, TPB_L>(__ldg(a.x0 + i), __ldg(a.x1 + i), j0 + e, k01, kl, idx, stg, magic, hlim, w0, w1);
       zbits |= (r & 1u) << e;
       tbits |= (r >> 1) << e;
     }

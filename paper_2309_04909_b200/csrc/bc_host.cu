@@ -113,8 +113,6 @@ KPL make_kpl(const bc_params* prm) {
   uint64_t inv = p;  // p^-1 mod 2^64 by Newton (p odd: correct to 3 bits, doubling per step)
   for (int i = 0; i < 5; ++i) inv *= 2ull - p * inv;
   k.pinv = 0ull - inv;
-  const uint64_t r1 = (uint64_t)(((u128)1 << 64) % p);
-  k.r2 = (uint64_t)(((u128)r1 * r1) % p);
   k.mu_p = ~0ull / p;
   k.mu_q = ~0ull / q;
   const u128 two64 = (u128)1 << 64;

@@ -4,13 +4,14 @@
 //
 // Per element: 9 ChaCha blocks from seed01 (large):
 //   block 0     t and the Fisher-Yates draws (u16, rejection),
-//   blocks 1-4  mask draws r_m (u64 -> 1 + u mod (p-1), rejection),
+//   blocks 1-4  mask draws (u64 -> rM = 1 + u mod (p-1), rejection); the mask
+//               is r_m = rM 2^-64 mod p, i.e. rM is its Montgomery form,
 //   blocks 5-8  reshare draws rho_m (u64 -> u mod p, rejection),
 // streamed in (r, rho) block pairs so at most 32 keystream words are live.
-// Arithmetic mod p: Montgomery products (R = 2^64) for W = v'r, Barrett
-// reductions for the draws.  The permutation is kept as a byte table per
-// thread in shared memory ([slot][thread], conflict-free) and applied by
-// evaluating slot m's source window v'_{Pi(m)} directly from the share.
+// Arithmetic mod p: one Montgomery product (R = 2^64) per party and slot,
+// W = REDC(v' rM) = v' r; Barrett reductions for the draws.  The permutation
+// is a byte table per thread in shared memory ([slot][thread]) and is applied
+// by evaluating slot m's source window v'_{Pi(m)} directly from the share.
 #pragma once
 #include <cstdint>
 
@@ -26,7 +27,6 @@ struct KPL {
   uint64_t wmask;     // 2^w - 1
   uint64_t p;         // modulus, odd, < 2^33
   uint64_t pinv;      // -p^-1 mod 2^64 (Montgomery)
-  uint64_t r2;        // 2^128 mod p
   uint64_t mu_p;      // floor((2^64-1) / p)      (Barrett)
   uint64_t mu_q;      // floor((2^64-1) / (p-1))
   uint64_t plim;      // floor(2^64/p) p, 0 = no rejection (2^64)
@@ -87,12 +87,14 @@ __device__ __forceinline__ void slot_values(uint64_t s0, uint64_t ns1, uint32_t 
 }
 
 // Alg 7 steps 1-9 for element j with shares x0, x1: returns DReLU' (bit 0)
-// and t (bit 1).  idx: this thread's column of the [32][TPB] byte table.
-// magic[s] = ceil(2^32 / s), hlim[s] = floor(2^16 / s) s for s = 2..32.
+// and t (bit 1).  idx: this thread's column of a [32][TPB_L] byte table (the
+// permutation); stg: its column of a [32][TPB_L] word table (keystream staging,
+// so the Fisher-Yates and slot loops stay rolled: the kernel must fit the
+// instruction cache).  magic[s] = ceil(2^32 / s), hlim[s] = floor(2^16 / s) s.
 template <int R, bool TRANSCRIPT, int TPB_L>
 __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_t j, const Key& k01, const KPL& kp,
-                                               uint8_t* idx, const uint32_t* magic, const uint32_t* hlim,
-                                               uint64_t* w0, uint64_t* w1) {
+                                               uint8_t* idx, uint32_t* stg, const uint32_t* magic,
+                                               const uint32_t* hlim, uint64_t* w0, uint64_t* w1) {
   const uint32_t S = kp.S;
   uint32_t fbc = 0;  // fallback words consumed
   uint32_t t;
@@ -101,20 +103,20 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
     chacha<R>(k01, j * 9, L_TAPEL, B);
     t = B[0] & 1u;
 #pragma unroll
-    for (uint32_t m = 0; m < 32; ++m) idx[m * TPB_L] = (uint8_t)m;
-    // step 6: Fisher-Yates, slot m = S-1 .. 1 draws h[S-m] (q = S - m)
-#pragma unroll
-    for (uint32_t q = 1; q < 32; ++q) {
-      if (q < S) {
-        const uint32_t m = S - q, s = m + 1;
-        uint32_t d = (B[q >> 1] >> (16 * (q & 1))) & 0xFFFFu;
-        while (d >= hlim[s]) d = (uint32_t)fbl_word<R>(k01, j, fbc++) & 0xFFFFu;
-        const uint32_t k = d - __umulhi(d, magic[s]) * s;
-        const uint8_t a = idx[m * TPB_L], b = idx[k * TPB_L];
-        idx[m * TPB_L] = b;
-        idx[k * TPB_L] = a;
-      }
-    }
+    for (int w = 0; w < 16; ++w) stg[w * TPB_L] = B[w];
+  }
+#pragma unroll 4
+  for (uint32_t m = 0; m < 32; ++m) idx[m * TPB_L] = (uint8_t)m;
+  // step 6: Fisher-Yates, slot m = S-1 .. 1 draws h[S-m]
+#pragma unroll 1
+  for (uint32_t q = 1; q < S; ++q) {
+    const uint32_t m = S - q, s = m + 1;
+    uint32_t d = (stg[(q >> 1) * TPB_L] >> (16 * (q & 1))) & 0xFFFFu;
+    while (d >= hlim[s]) d = (uint32_t)fbl_word<R>(k01, j, fbc++) & 0xFFFFu;
+    const uint32_t k = d - __umulhi(d, magic[s]) * s;
+    const uint8_t a = idx[m * TPB_L], b = idx[k * TPB_L];
+    idx[m * TPB_L] = b;
+    idx[k * TPB_L] = a;
   }
   // steps 1-2: blind both shares by (-1)^t
   const uint64_t s0 = t ? (0ull - x0) & kp.ymask : x0 & kp.ymask;
@@ -122,35 +124,37 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
   const uint64_t ns1 = (0ull - s1) & kp.ymask;
   uint32_t z = 0;
 #pragma unroll 1
-  for (uint32_t b = 0; b < 4; ++b) {
-    if (8 * b >= S) break;
-    uint32_t Br[16], Bq[16];
-    chacha<R>(k01, j * 9 + 1 + b, L_TAPEL, Br);
-    chacha<R>(k01, j * 9 + 5 + b, L_TAPEL, Bq);
+  for (uint32_t b = 0; 8 * b < S; ++b) {
+    // mask block 1+b -> rows 0..15, reshare block 5+b -> rows 16..31
+#pragma unroll 1
+    for (uint32_t h = 0; h < 2; ++h) {
+      uint32_t B[16];
+      chacha<R>(k01, j * 9 + 1 + b + 4 * h, L_TAPEL, B);
 #pragma unroll
-    for (uint32_t e = 0; e < 8; ++e) {
-      const uint32_t m = 8 * b + e;
-      if (m < S) {
-        uint64_t ur = (uint64_t)Br[2 * e] | ((uint64_t)Br[2 * e + 1] << 32);
-        while (!accept64(ur, kp.qlim)) ur = fbl_word<R>(k01, j, fbc++);
-        uint64_t uq = (uint64_t)Bq[2 * e] | ((uint64_t)Bq[2 * e + 1] << 32);
-        while (!accept64(uq, kp.plim)) uq = fbl_word<R>(k01, j, fbc++);
-        const uint64_t r = 1ull + barrett(ur, kp.p - 1ull, kp.mu_q);   // r_m in Z_p^*
-        const uint64_t rho = barrett(uq, kp.p, kp.mu_p);               // rho_m in Z_p
-        uint64_t c, d;
-        slot_values(s0, ns1, idx[m * TPB_L], kp, c, d);                // v'_{Pi(m)} of each party
-        const uint64_t rM = mont(r, kp.r2, kp);                        // r * 2^64 mod p
-        uint64_t W0 = mont(c, rM, kp) + rho;                           // step 7-8, P0: v'r + rho
-        W0 = W0 >= kp.p ? W0 - kp.p : W0;
-        uint64_t W1 = mont(d, rM, kp) + (kp.p - rho);                  //           P1: v'r - rho
-        W1 = W1 >= kp.p ? W1 - kp.p : W1;
-        if (TRANSCRIPT) {
-          w0[m] = W0;
-          w1[m] = W1;
-        }
-        const uint64_t sum = W0 + W1;                                  // step 9 (P2): w_m = 0 mod p?
-        z |= (sum == 0 || sum == kp.p) ? 1u : 0u;
+      for (int w = 0; w < 16; ++w) stg[(16 * h + w) * TPB_L] = B[w];
+    }
+    const uint32_t mend = min(S, 8 * b + 8);
+#pragma unroll 1
+    for (uint32_t m = 8 * b; m < mend; ++m) {
+      const uint32_t e = 2 * (m - 8 * b);
+      uint64_t ur = (uint64_t)stg[e * TPB_L] | ((uint64_t)stg[(e + 1) * TPB_L] << 32);
+      while (!accept64(ur, kp.qlim)) ur = fbl_word<R>(k01, j, fbc++);
+      uint64_t uq = (uint64_t)stg[(16 + e) * TPB_L] | ((uint64_t)stg[(17 + e) * TPB_L] << 32);
+      while (!accept64(uq, kp.plim)) uq = fbl_word<R>(k01, j, fbc++);
+      const uint64_t rM = 1ull + barrett(ur, kp.p - 1ull, kp.mu_q);  // r_m = rM 2^-64 (Montgomery form)
+      const uint64_t rho = barrett(uq, kp.p, kp.mu_p);               // rho_m in Z_p
+      uint64_t c, d;
+      slot_values(s0, ns1, idx[m * TPB_L], kp, c, d);                // v'_{Pi(m)} of each party
+      uint64_t W0 = mont(c, rM, kp) + rho;                           // steps 7-8, P0: v'r + rho
+      W0 = W0 >= kp.p ? W0 - kp.p : W0;
+      uint64_t W1 = mont(d, rM, kp) + (kp.p - rho);                  //            P1: v'r - rho
+      W1 = W1 >= kp.p ? W1 - kp.p : W1;
+      if (TRANSCRIPT) {
+        w0[m] = W0;
+        w1[m] = W1;
       }
+      const uint64_t sum = W0 + W1;                                  // step 9 (P2): w_m = 0 mod p?
+      z |= (sum == 0 || sum == kp.p) ? 1u : 0u;
     }
   }
   return z | (t << 1);
