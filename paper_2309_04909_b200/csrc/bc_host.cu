@@ -112,13 +112,14 @@ KPL make_kpl(const bc_params* prm) {
   k.p = p;
   uint64_t inv = p;  // p^-1 mod 2^64 by Newton (p odd: correct to 3 bits, doubling per step)
   for (int i = 0; i < 5; ++i) inv *= 2ull - p * inv;
-  k.pinv = 0ull - inv;
+  k.pinv = inv;
   k.mu_p = ~0ull / p;
   k.mu_q = ~0ull / q;
   const u128 two64 = (u128)1 << 64;
   const u128 pl = two64 / p * p, ql = two64 / q * q;
-  k.plim = pl == two64 ? 0ull : (uint64_t)pl;
-  k.qlim = ql == two64 ? 0ull : (uint64_t)ql;
+  k.plim = (uint64_t)(pl - 1);  // accept u <= lim - 1; 2^64 - 1 when p | 2^64 (nothing rejects)
+  k.qlim = (uint64_t)(ql - 1);
+  k.wm32 = (uint32_t)((1ull << prm->w) - 1ull);
   k.two_w = (1ull << prm->w) % p;
   k.off1 = p - (1ull << prm->w);
   k.f = (uint32_t)prm->f;

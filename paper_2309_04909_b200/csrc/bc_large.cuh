@@ -26,22 +26,23 @@ struct KPL {
   uint64_t ymask;     // 2^ell - 1
   uint64_t wmask;     // 2^w - 1
   uint64_t p;         // modulus, odd, < 2^33
-  uint64_t pinv;      // -p^-1 mod 2^64 (Montgomery)
+  uint64_t pinv;      // p^-1 mod 2^64 (Montgomery, subtractive REDC)
   uint64_t mu_p;      // floor((2^64-1) / p)      (Barrett)
   uint64_t mu_q;      // floor((2^64-1) / (p-1))
-  uint64_t plim;      // floor(2^64/p) p, 0 = no rejection (2^64)
-  uint64_t qlim;      // floor(2^64/(p-1)) (p-1), 0 = no rejection
+  uint64_t plim;      // floor(2^64/p) p - 1: accept u <= plim (2^64 - 1 when nothing rejects)
+  uint64_t qlim;      // floor(2^64/(p-1)) (p-1) - 1
   uint64_t two_w;     // 2^w mod p (P0's image of 0, Alg 6)
   uint64_t off1;      // p - 2^w   (P1's modswitch offset, Alg 6)
+  uint32_t wm32;      // 2^w - 1 as 32 bits (w <= 32)
   uint32_t f, w, S;
 };
 
-// a * b * 2^-64 mod p for a, b < p (REDC; t < 2p before the final subtraction).
+// a * b * 2^-64 mod p for a, b < p.  Subtractive REDC: m = lo p^-1 makes
+// lo - lo(m p) = 0 exactly, so (ab - mp) / 2^64 = hi - hi(mp), in (-p, p).
 __device__ __forceinline__ uint64_t mont(uint64_t a, uint64_t b, const KPL& kp) {
   const uint64_t lo = a * b, hi = __umul64hi(a, b);
-  const uint64_t m = lo * kp.pinv;
-  const uint64_t t = hi + __umul64hi(m, kp.p) + (lo != 0 ? 1ull : 0ull);
-  return t >= kp.p ? t - kp.p : t;
+  const uint64_t mh = __umul64hi(lo * kp.pinv, kp.p);
+  return hi >= mh ? hi - mh : hi - mh + kp.p;
 }
 
 // u mod q with mu = floor((2^64-1)/q): the quotient estimate is low by at most 1.
@@ -50,7 +51,7 @@ __device__ __forceinline__ uint64_t barrett(uint64_t u, uint64_t q, uint64_t mu)
   return r >= q ? r - q : r;
 }
 
-__device__ __forceinline__ bool accept64(uint64_t u, uint64_t lim) { return lim == 0 || u < lim; }
+__device__ __forceinline__ bool accept64(uint64_t u, uint64_t lim_m1) { return u <= lim_m1; }
 
 // c-th u64 word of element j's fallback stream (rare path, kept out of line).
 template <int R>
@@ -65,25 +66,25 @@ __device__ __noinline__ uint64_t fbl_word(Key k01, uint64_t j, uint32_t c) {
   return v;
 }
 
-// Ladder source slot i of Alg 7 steps 3-5 for both parties (s0, s1 blinded
-// shares, ns1 = -s1 mod 2^ell): returns P0's c'_i and P1's d'_i in [0, p).
-__device__ __forceinline__ void slot_values(uint64_t s0, uint64_t ns1, uint32_t i, const KPL& kp, uint64_t& c,
+// Ladder source slot i of Alg 7 steps 3-5 for both parties.  s0f = s0 >> f
+// and n1f = ((-s1) mod 2^ell) >> f (the blinded shares with the key-bit
+// offset applied once per element), so window i is bits [i, i+w) of a 64-bit
+// value with i + w <= 64 - f: one 32-bit funnel shift (i <= 31, w <= 32).
+// Returns P0's c'_i and P1's d'_i in [0, p).
+__device__ __forceinline__ void slot_values(uint64_t s0f, uint64_t n1f, uint32_t i, const KPL& kp, uint64_t& c,
                                             uint64_t& d) {
-  const uint32_t sh = kp.f + i;
-  const uint64_t a_i = (s0 >> sh) & kp.wmask;
-  const uint64_t b_i = (0ull - ((ns1 >> sh) & kp.wmask)) & kp.wmask;   // Alg 5, P1 (readings C3, C4)
-  uint64_t cv, dv;
-  if (i + 1 < kp.S) {
-    const uint64_t a_n = (s0 >> (sh + 1)) & kp.wmask;
-    const uint64_t b_n = (0ull - ((ns1 >> (sh + 1)) & kp.wmask)) & kp.wmask;
-    cv = (a_i + a_n - 1ull) & kp.wmask;                                  // step 4: P0 carries the -1 (C8)
-    dv = (b_i + b_n) & kp.wmask;
-  } else {
-    cv = (a_i - 1ull) & kp.wmask;
-    dv = b_i;
-  }
-  c = cv == 0 ? kp.two_w : cv;                                           // step 5 (Alg 6), P0
-  d = dv + kp.off1;                                                      //                 P1: p + d - 2^w
+  const uint32_t l0 = (uint32_t)s0f, h0 = (uint32_t)(s0f >> 32);
+  const uint32_t l1 = (uint32_t)n1f, h1 = (uint32_t)(n1f >> 32);
+  const uint32_t wm = kp.wm32;
+  const uint32_t nm = i + 1 < kp.S ? wm : 0u;                          // slot lx has no successor
+  const uint32_t a_i = __funnelshift_r(l0, h0, i) & wm;
+  const uint32_t a_n = __funnelshift_rc(l0, h0, i + 1) & nm;
+  const uint32_t b_i = (0u - (__funnelshift_r(l1, h1, i) & wm)) & wm;  // Alg 5, P1 (readings C3, C4)
+  const uint32_t b_n = (0u - (__funnelshift_rc(l1, h1, i + 1) & nm)) & wm;
+  const uint32_t cv = (a_i + a_n - 1u) & wm;                           // step 4: P0 carries the -1 (C8)
+  const uint32_t dv = (b_i + b_n) & wm;
+  c = cv == 0 ? kp.two_w : (uint64_t)cv;                               // step 5 (Alg 6), P0
+  d = (uint64_t)dv + kp.off1;                                          //                 P1: p + d - 2^w
 }
 
 // Alg 7 steps 1-9 for element j with shares x0, x1: returns DReLU' (bit 0)
@@ -121,7 +122,7 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
   // steps 1-2: blind both shares by (-1)^t
   const uint64_t s0 = t ? (0ull - x0) & kp.ymask : x0 & kp.ymask;
   const uint64_t s1 = t ? (0ull - x1) & kp.ymask : x1 & kp.ymask;
-  const uint64_t ns1 = (0ull - s1) & kp.ymask;
+  const uint64_t s0f = s0 >> kp.f, n1f = ((0ull - s1) & kp.ymask) >> kp.f;
   uint32_t z = 0;
 #pragma unroll 1
   for (uint32_t b = 0; 8 * b < S; ++b) {
@@ -144,7 +145,7 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
       const uint64_t rM = 1ull + barrett(ur, kp.p - 1ull, kp.mu_q);  // r_m = rM 2^-64 (Montgomery form)
       const uint64_t rho = barrett(uq, kp.p, kp.mu_p);               // rho_m in Z_p
       uint64_t c, d;
-      slot_values(s0, ns1, idx[m * TPB_L], kp, c, d);                // v'_{Pi(m)} of each party
+      slot_values(s0f, n1f, idx[m * TPB_L], kp, c, d);                // v'_{Pi(m)} of each party
       uint64_t W0 = mont(c, rM, kp) + rho;                           // steps 7-8, P0: v'r + rho
       W0 = W0 >= kp.p ? W0 - kp.p : W0;
       uint64_t W1 = mont(d, rM, kp) + (kp.p - rho);                  //            P1: v'r - rho
