@@ -396,6 +396,8 @@ def run_cuda(a):
                         "roofline": roofline(name, v_fp, ms_fp)}
         fp["note"] = "lx=31, f=0, guard (w=32, p=2^32+15, 32 slots): the paper's full 5+26 precision, same batch"
         line["full_precision"] = fp
+        # ---- truncation study (NEXT #3): exact e1 counting, Alg 3 vs mult-then-trc ----
+        line["trunc_study"] = trunc_leg(api, seeds, x0, x1, y0, y1, base, dev, stream, timed, world, n)
         # ---- config 5: E2E-shaped ReLU layer streams (CUDA graph per network) ----
         line["config5"] = relu_streams(api, prm, seeds, dev, stream, timed, world)
         # ---- e2e through the public API with pinned HOST buffers ----------------
@@ -459,6 +461,26 @@ def rss_leg(api, prm, seeds, x, base, dev, stream, timed, world, n, roofline, ra
         v = world * n / (ms * 1e-3)
         res[name] = {"value": v, "unit": "elements/s", "ms_per_step": ms, "roofline": roofline(name, v, ms)}
     del xs, ys
+    return res
+
+
+def trunc_leg(api, seeds, x0, x1, y0, y1, base, dev, stream, timed, world, n):
+    """Sec. 4-5 kernels: bc_trc_count (every mask of a range against a list of
+    x, classified exact / e0 / e1) and the fixed-point product in both orders
+    (ABY3 truncation, ell = 64, f = 26: the paper's Piranha setting)."""
+    import torch
+    res = {}
+    xs = torch.arange(1, 4097, dtype=torch.int64, device=dev) << 40       # 4096 band inputs at ell = 64
+    counts = torch.zeros((4096, 3), dtype=torch.int64, device=dev)
+    m = 1 << 20
+    t_ms, _, _ = timed(lambda: api.trc_count("secureml", xs, 64, 26, 0, m, counts=counts, stream=stream), 5, 3)
+    res["trc_count"] = {"value": world * 4096 * m / (t_ms / 5 * 1e-3), "unit": "protocol evaluations/s",
+                        "ms_per_step": t_ms / 5, "note": "Alg 1 on 4096 inputs x 2^20 masks, classified (C30)"}
+    z0, z1 = torch.empty_like(x0), torch.empty_like(x1)
+    for order in ("mul_then_trc", "trc_then_mul"):
+        t_ms, _, _ = timed(lambda: api.mul_trc(order, "aby3", x0, x1, y0, y1, 64, 26, seeds, base, out=(z0, z1),
+                                               stream=stream), 20, 3)
+        res[order] = {"value": world * n / (t_ms / 20 * 1e-3), "unit": "products/s", "ms_per_step": t_ms / 20}
     return res
 
 

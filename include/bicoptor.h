@@ -214,6 +214,48 @@ int bc_relu_rss(const uint64_t *x0, const uint64_t *x1, const uint64_t *x2, uint
                 const bc_seeds *seeds, const uint8_t seed012[32], const uint8_t seed2[32],
                 void *stream);
 
+/* ---- truncation study (sec. 3-5) --------------------
+ *
+ * Probabilistic truncation of prior work and its error e1 (sec. 4),
+ * the deterministic Alg 4 for comparison, and Alg 3 "truncate-then-multiply"
+ * (sec. 5.2).  Two parties simulated on one GPU; the preprocessing
+ * comes from the seeds with P2 as the dealer (readings C29, C31). */
+#define BC_TRC_SECUREML 1 /* Alg 1, non-interactive probabilistic */
+#define BC_TRC_ABY3     2 /* Alg 2, interactive probabilistic      */
+#define BC_TRC_DET      4 /* Alg 4, deterministic, Z_{2^(ell-k)}   */
+#define BC_MUL_THEN_TRC 0 /* z = x y, then trc(z, f)                           */
+#define BC_TRC_THEN_MUL 1 /* Alg 3: trc(x, floor(f/2)) trc(y, ceil(f/2))        */
+
+/* Alg 2 (ABY3) for both parties: alpha = x + r is opened ([x]_i + [r]_i, the
+ * paper's footnote P:341), y0 = alpha/2^k - [r']_0 (P0 adds the public term,
+ * C29), y1 = -[r']_1.  r, r' = cut(r, k) preprocessed from seed02 / seed12,
+ * truncation instance q (0 or 1) selecting the labels.  y0 + y1 = trc(x, k) up
+ * to e0, or e1 when x + r wraps.  Arrays as bc_drelu; 2 <= ell <= 64,
+ * 0 <= k < ell, rounds 8 / 12 / 20. */
+int bc_trc_aby3(const uint64_t *x0, const uint64_t *x1, uint64_t *y0, uint64_t *y1, size_t n,
+                uint64_t elem_base, int ell, int k, int rounds, int q, const bc_seeds *seeds,
+                void *stream);
+
+/* Exact e1 counting (sec. 4).  For each plaintext x[i] (i < nx; device
+ * uint64_t, 8-B aligned) and each mask m in [m_base, m_base + m_count) (taken
+ * mod 2^ell), run alg on the shares -- Alg 1 / Alg 4: [x]_0 = x + m, [x]_1 = -m;
+ * Alg 2: r = m -- and add the class of the reconstruction (reading C30:
+ * exact, e0 = the one-bit error, e1 = anything else) to counts[i][0..2]
+ * (uint64_t[nx][3], accumulated: the caller zeroes it).  Over all 2^ell masks
+ * Alg 1 / Alg 2 give e1 = xi for every x (C18); Alg 4 gives none (Theorem
+ * newcut2).  1 <= k < ell <= 64. */
+int bc_trc_count(int alg, const uint64_t *x, size_t nx, int ell, int k, uint64_t m_base,
+                 uint64_t m_count, uint64_t *counts, void *stream);
+
+/* Secure fixed-point multiplication z = x y / 2^f for both parties (a Beaver
+ * product, triple from seed02 / seed12 by P2, C31), in the order given:
+ * BC_MUL_THEN_TRC (truncate the product) or BC_TRC_THEN_MUL (Alg 3: truncate
+ * the operands by floor(f/2) and ceil(f/2), then multiply), each truncation
+ * Alg 1 or Alg 2 (alg).  Arrays as bc_drelu; 0 <= f < ell. */
+int bc_mul_trc(int order, int alg, const uint64_t *x0, const uint64_t *x1, const uint64_t *y0,
+               const uint64_t *y1, uint64_t *z0, uint64_t *z1, size_t n, uint64_t elem_base,
+               int ell, int f, int rounds, const bc_seeds *seeds, void *stream);
+
 /* Human-readable text for a BC_* code (static storage). */
 const char *bc_strerror(int code);
 

@@ -74,6 +74,12 @@ _SIG = {
                                       ctypes.POINTER(bc_params), ctypes.c_char_p, ctypes.c_char_p, _P]),
     "bc_relu_finish": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64,
                                       ctypes.POINTER(bc_params), ctypes.c_char_p, _P]),
+    "bc_trc_aby3": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
+                                   ctypes.c_int, ctypes.c_int, ctypes.POINTER(bc_seeds), _P]),
+    "bc_trc_count": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_uint64,
+                                    ctypes.c_uint64, _P, _P]),
+    "bc_mul_trc": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64,
+                                  ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(bc_seeds), _P]),
     "bc_drelu_rss": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64, ctypes.POINTER(bc_params),
                                     ctypes.POINTER(bc_seeds), ctypes.c_char_p, ctypes.c_char_p, _P]),
     "bc_relu_rss": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64, ctypes.POINTER(bc_params),
@@ -336,3 +342,39 @@ def drelu_rss(x0, x1, x2, prm: Params, seeds, elem_base: int = 0, out=None, stre
 def relu_rss(x0, x1, x2, prm: Params, seeds, elem_base: int = 0, out=None, stream=None):
     """RSS ReLU [x][DReLU(x)]: returns (y0, y1, y2), sum = ReLU(x)."""
     return _rss(lib().bc_relu_rss, "bc_relu_rss", x0, x1, x2, prm, seeds, elem_base, out, stream)
+
+
+# ---- truncation study (sec. 3-5) ---------------------------------------------------------
+
+TRC_ALG = {"secureml": 1, "aby3": 2, "det": 4}
+MUL_ORDER = {"mul_then_trc": 0, "trc_then_mul": 1}
+
+
+def trc_aby3(x0, x1, ell: int, k: int, seeds, elem_base: int = 0, q: int = 0, rounds: int = 20, out=None,
+             stream=None):
+    """Alg 2 (ABY3) for both parties: returns (y0, y1), y0 + y1 = trc(x, k) (probabilistic)."""
+    y0, y1 = (torch.empty_like(x0), torch.empty_like(x1)) if out is None else out
+    cs = seeds_struct(seeds)
+    _check(lib().bc_trc_aby3(_dev(x0, "x0"), _dev(x1, "x1"), _dev(y0, "y0"), _dev(y1, "y1"), x0.numel(), elem_base,
+                             ell, k, rounds, q, ctypes.byref(cs), _stream(stream)), "bc_trc_aby3")
+    return y0, y1
+
+
+def trc_count(alg: str, x, ell: int, k: int, m_base: int = 0, m_count: int | None = None, counts=None, stream=None):
+    """Exact e1 counting: counts[i] += (#exact, #e0, #e1) over masks [m_base, m_base + m_count)."""
+    m_count = (1 << ell) if m_count is None else m_count
+    counts = torch.zeros((x.numel(), 3), dtype=torch.int64, device=x.device) if counts is None else counts
+    _check(lib().bc_trc_count(TRC_ALG[alg], _dev(x, "x"), x.numel(), ell, k, m_base, m_count, _dev(counts, "counts"),
+                              _stream(stream)), "bc_trc_count")
+    return counts
+
+
+def mul_trc(order: str, alg: str, x0, x1, y0, y1, ell: int, f: int, seeds, elem_base: int = 0, rounds: int = 20,
+            out=None, stream=None):
+    """Fixed-point product x y / 2^f in the given order (Alg 3 = "trc_then_mul"): returns (z0, z1)."""
+    z0, z1 = (torch.empty_like(x0), torch.empty_like(x1)) if out is None else out
+    cs = seeds_struct(seeds)
+    _check(lib().bc_mul_trc(MUL_ORDER[order], TRC_ALG[alg], _dev(x0, "x0"), _dev(x1, "x1"), _dev(y0, "y0"),
+                            _dev(y1, "y1"), _dev(z0, "z0"), _dev(z1, "z1"), x0.numel(), elem_base, ell, f, rounds,
+                            ctypes.byref(cs), _stream(stream)), "bc_mul_trc")
+    return z0, z1

@@ -469,3 +469,86 @@ def test_large_abi_errors(api):
     ok = api.bc_transcript(w[0].data_ptr(), None, w[1].data_ptr(), None)
     assert L.bc_drelu(t.data_ptr(), ys[2].data_ptr(), ys[0].data_ptr(), ys[1].data_ptr(), 16, 0, ctypes.byref(cp),
                       ctypes.byref(cs), ctypes.byref(ok), None) == 0
+
+
+# ---- truncation study (NEXT #3) ----------------------------------------------------------
+
+@pytest.mark.parametrize("ell,k", [(64, 26), (64, 13), (32, 5), (16, 0)])
+@pytest.mark.parametrize("q", [0, 1])
+def test_trc_aby3_parity(api, ell, k, q):
+    from oracle import trunc
+    for n in SIZES:
+        for base in (0, 1 << 40):
+            x, x0, x1 = synth.shares(n, ell, 5, min(k, ell - 7), "D1", run=n + q)
+            j = np.arange(n, dtype=np.uint64) + np.uint64(base)
+            r0, r1 = trunc.trc_aby3(x0, x1, trunc.aby3_pre(ell, k, j, SEEDS, 20, q), k, ell)
+            y0, y1 = api.trc_aby3(dev(x0), dev(x1), ell, k, SEEDS, elem_base=base, q=q)
+            assert np.array_equal(host(y0), r0) and np.array_equal(host(y1), r1), (n, base)
+
+
+@pytest.mark.parametrize("order", ["mul_then_trc", "trc_then_mul"])
+@pytest.mark.parametrize("alg", ["secureml", "aby3"])
+@pytest.mark.parametrize("ell,f,rounds", [(64, 26, 20), (32, 13, 8)])
+def test_mul_trc_parity(api, order, alg, ell, f, rounds):
+    from oracle import trunc
+    for n in (1, 9, 1000):
+        X = synth.plaintext(n, ell, 5, f, "D1", run=1)
+        Y = synth.plaintext(n, ell, 5, f, "D1", run=2)
+        x0, x1 = synth.share(X, ell, run=3)
+        y0, y1 = synth.share(Y, ell, run=4)
+        j = np.arange(n, dtype=np.uint64) + np.uint64(64)
+        ref = getattr(trunc, order)(alg, x0, x1, y0, y1, f, ell, j, SEEDS, rounds)
+        z0, z1 = api.mul_trc(order, alg, dev(x0), dev(x1), dev(y0), dev(y1), ell, f, SEEDS, elem_base=64,
+                             rounds=rounds)
+        assert np.array_equal(host(z0), ref[0]) and np.array_equal(host(z1), ref[1])
+
+
+def test_trc_count_exhaustive_ell12(api):
+    """Every band x (|x| < 2^10) against all 2^12 masks, three algorithms: the
+    GPU counts equal the oracle's brute force, and the e1 counts are xi (Alg 1,
+    Alg 2) and 0 (Alg 4)."""
+    from oracle import trunc
+    ell, k = 12, 4
+    xi = np.arange(1, 1 << 10, dtype=np.uint64)
+    xs = np.concatenate([xi, np.uint64(1 << ell) - xi])
+    xis = np.concatenate([xi, xi])
+    for alg in ("secureml", "aby3", "det"):
+        got = api.trc_count(alg, dev(xs), ell, k).cpu().numpy()
+        ref = np.stack([trunc.count_masks(alg, int(x), k, ell) for x in xs])
+        assert np.array_equal(got, ref), alg
+        assert np.array_equal(got[:, 2], xis if alg != "det" else np.zeros_like(xis))
+
+
+def test_trc_count_ell24_closed_forms_and_ranges(api):
+    """ell = 24, all 2^24 masks for a sample of x: e1 = xi (Alg 1), and Alg 4's
+    one-bit error count is (xi mod 2^k) 2^(ell-k); two half-range calls add up
+    to one full-range call."""
+    ell, k = 24, 7
+    rng = np.random.default_rng(5)
+    xi = rng.integers(1, 1 << 21, 64).astype(np.uint64)
+    xs = np.concatenate([xi, np.uint64(1 << ell) - xi])
+    xis = np.concatenate([xi, xi])
+    c1 = api.trc_count("secureml", dev(xs), ell, k).cpu().numpy()
+    assert np.array_equal(c1[:, 2], xis.astype(np.int64)) and np.all(c1.sum(axis=1) == 1 << ell)
+    cd = api.trc_count("det", dev(xs), ell, k).cpu().numpy()
+    assert np.all(cd[:, 2] == 0)
+    assert np.array_equal(cd[:, 1], ((xis % (1 << k)) * (1 << (ell - k))).astype(np.int64))
+    half = api.trc_count("aby3", dev(xs), ell, k, 0, 1 << 23)
+    api.trc_count("aby3", dev(xs), ell, k, 1 << 23, 1 << 23, counts=half)
+    assert np.array_equal(half.cpu().numpy(), api.trc_count("aby3", dev(xs), ell, k).cpu().numpy())
+
+
+def test_trunc_abi_errors(api):
+    L = api.lib()
+    t = [torch.zeros(16, dtype=torch.int64, device=DEV) for _ in range(6)]
+    p = [v.data_ptr() for v in t]
+    import ctypes
+    cs = api.seeds_struct(SEEDS)
+    assert L.bc_trc_aby3(p[0], p[1], p[2], p[3], 16, 0, 64, 64, 20, 0, ctypes.byref(cs), None) == -1   # k >= ell
+    assert L.bc_trc_aby3(p[0], p[1], p[2], p[3], 16, 0, 64, 26, 20, 2, ctypes.byref(cs), None) == -1   # q
+    assert L.bc_trc_aby3(p[0], p[1], p[0], p[3], 16, 0, 64, 26, 20, 0, ctypes.byref(cs), None) == -5   # alias
+    assert L.bc_mul_trc(1, 4, p[0], p[1], p[2], p[3], p[4], p[5], 16, 0, 64, 26, 20, ctypes.byref(cs), None) == -1
+    assert L.bc_mul_trc(2, 1, p[0], p[1], p[2], p[3], p[4], p[5], 16, 0, 64, 26, 20, ctypes.byref(cs), None) == -1
+    assert L.bc_mul_trc(0, 1, p[0], p[1], p[2], p[3], p[4], p[5], 16, 4, 64, 26, 20, ctypes.byref(cs), None) == -3
+    assert L.bc_trc_count(3, p[0], 16, 64, 4, 0, 10, p[1], None) == -1
+    assert L.bc_trc_count(1, p[0], 16, 64, 0, 0, 10, p[1], None) == -1   # k >= 1
