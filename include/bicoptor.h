@@ -132,6 +132,27 @@ int bc_relu(const uint64_t *x0, const uint64_t *x1, uint64_t *y0, uint64_t *y1, 
             uint64_t elem_base, const bc_params *prm, const bc_seeds *seeds,
             const bc_transcript *tr, void *stream);
 
+/* ---- host-buffer entry points (end to end) ------------------------------
+ *
+ * bc_drelu / bc_relu on shares that live in HOST memory: x0, x1 (in) and y0,
+ * y1 (out) are host arrays of n uint64_t (pinned memory recommended; pageable
+ * works but serialises the copies).  The batch is processed in chunks of
+ * `chunk` elements (a positive multiple of 8): H2D copy, the fused kernel
+ * (elem_base + chunk offset, so the result equals one bc_drelu over the whole
+ * batch), D2H copy, pipelined over a ring of 3 library-owned CUDA streams so
+ * both PCIe directions overlap each other and the kernels.  ws is a caller-
+ * owned DEVICE workspace of ws_bytes >= bc_host_workspace_bytes(chunk), 16-B
+ * aligned.  Ordered after prior work on `stream`; unlike every other entry
+ * point the call is synchronous: the host outputs are complete on return.
+ * Errors as bc_drelu (BC_EINVAL for a short workspace or a bad chunk). */
+size_t bc_host_workspace_bytes(size_t chunk);
+int bc_drelu_host(const uint64_t *x0, const uint64_t *x1, uint64_t *y0, uint64_t *y1, size_t n,
+                  uint64_t elem_base, const bc_params *prm, const bc_seeds *seeds, void *ws,
+                  size_t ws_bytes, size_t chunk, void *stream);
+int bc_relu_host(const uint64_t *x0, const uint64_t *x1, uint64_t *y0, uint64_t *y1, size_t n,
+                 uint64_t elem_base, const bc_params *prm, const bc_seeds *seeds, void *ws,
+                 size_t ws_bytes, size_t chunk, void *stream);
+
 /* ---- party-separated phases (each party on its own device; the caller moves
  * the message buffers, e.g. with NCCL send/recv) --------------------------- */
 

@@ -74,6 +74,11 @@ _SIG = {
                                       ctypes.POINTER(bc_params), ctypes.c_char_p, ctypes.c_char_p, _P]),
     "bc_relu_finish": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64,
                                       ctypes.POINTER(bc_params), ctypes.c_char_p, _P]),
+    "bc_host_workspace_bytes": (ctypes.c_size_t, [ctypes.c_size_t]),
+    "bc_drelu_host": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64, ctypes.POINTER(bc_params),
+                                     ctypes.POINTER(bc_seeds), _P, ctypes.c_size_t, ctypes.c_size_t, _P]),
+    "bc_relu_host": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64, ctypes.POINTER(bc_params),
+                                    ctypes.POINTER(bc_seeds), _P, ctypes.c_size_t, ctypes.c_size_t, _P]),
     "bc_trc_aby3": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
                                    ctypes.c_int, ctypes.c_int, ctypes.POINTER(bc_seeds), _P]),
     "bc_trc_count": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_uint64,
@@ -233,6 +238,45 @@ def drelu(x0, x1, prm: Params, seeds, elem_base: int = 0, y0=None, y1=None, tran
 def relu(x0, x1, prm: Params, seeds, elem_base: int = 0, y0=None, y1=None, transcript=None, stream=None):
     """Alg 8 with all three parties in one fused kernel: returns (y0, y1), y0 + y1 = ReLU(x)."""
     return _fused(lib().bc_relu, "bc_relu", x0, x1, prm, seeds, elem_base, y0, y1, transcript, stream)
+
+
+# ---- host-buffer entry points (end to end) -------------------------------------------
+
+def _host(t, name):
+    if not isinstance(t, torch.Tensor) or t.is_cuda:
+        raise BicoptorError(f"{name} must be a host tensor")
+    if not t.is_contiguous() or t.element_size() != 8:
+        raise BicoptorError(f"{name} must be contiguous with 8-byte elements")
+    return t.data_ptr()
+
+
+def host_workspace(chunk: int, device) -> torch.Tensor:
+    """Device workspace for drelu_host / relu_host at this chunk size."""
+    nbytes = lib().bc_host_workspace_bytes(chunk)
+    return torch.empty(nbytes // 8, dtype=torch.int64, device=device)
+
+
+def _host_call(fn, what, hx0, hx1, hy0, hy1, prm, seeds, elem_base, ws, chunk, stream):
+    n = hx0.numel()
+    if hx1.numel() != n or hy0.numel() != n or hy1.numel() != n:
+        raise BicoptorError("host buffers differ in length")
+    cp, cs = prm.c(), seeds_struct(seeds)
+    _check(fn(_host(hx0, "x0"), _host(hx1, "x1"), _host(hy0, "y0"), _host(hy1, "y1"), n, elem_base,
+              ctypes.byref(cp), ctypes.byref(cs), _dev(ws, "ws", None), ws.numel() * ws.element_size(), chunk,
+              _stream(stream)), what)
+    return hy0, hy1
+
+
+def drelu_host(hx0, hx1, hy0, hy1, prm: Params, seeds, ws, chunk: int = 1 << 20, elem_base: int = 0, stream=None):
+    """bc_drelu_host: host shares in (pinned recommended), host shares out; synchronous."""
+    return _host_call(lib().bc_drelu_host, "bc_drelu_host", hx0, hx1, hy0, hy1, prm, seeds, elem_base, ws, chunk,
+                      stream)
+
+
+def relu_host(hx0, hx1, hy0, hy1, prm: Params, seeds, ws, chunk: int = 1 << 20, elem_base: int = 0, stream=None):
+    """bc_relu_host: as drelu_host for ReLU."""
+    return _host_call(lib().bc_relu_host, "bc_relu_host", hx0, hx1, hy0, hy1, prm, seeds, elem_base, ws, chunk,
+                      stream)
 
 
 # ---- party-separated phases ---------------------------------------------------------

@@ -552,3 +552,43 @@ def test_trunc_abi_errors(api):
     assert L.bc_mul_trc(0, 1, p[0], p[1], p[2], p[3], p[4], p[5], 16, 4, 64, 26, 20, ctypes.byref(cs), None) == -3
     assert L.bc_trc_count(3, p[0], 16, 64, 4, 0, 10, p[1], None) == -1
     assert L.bc_trc_count(1, p[0], 16, 64, 0, 0, 10, p[1], None) == -1   # k >= 1
+
+
+# ---- host-buffer entry points (e2e) ----------------------------------------------------
+
+@pytest.mark.parametrize("fn", ["drelu", "relu"])
+def test_host_entry_matches_oracle(api, fn):
+    """bc_drelu_host / bc_relu_host on pinned host buffers: ragged chunks and a
+    ragged tail, bit-exact against the oracle (and so against the device path)."""
+    kw = PARAMS[0]
+    n, base = 5003, 1 << 20
+    x, x0, x1 = synth.shares(n, 64, 7, 24, "D1", run=9)
+    j = np.arange(n, dtype=np.uint64) + np.uint64(base)
+    ref = getattr(B, fn)(B.Params(**kw), x0, x1, j, SEEDS)
+    hx0 = torch.from_numpy(x0.view(np.int64)).pin_memory()
+    hx1 = torch.from_numpy(x1.view(np.int64)).pin_memory()
+    for chunk in (8, 1024, 1 << 20):
+        hy0 = torch.zeros(n, dtype=torch.int64).pin_memory()
+        hy1 = torch.zeros(n, dtype=torch.int64).pin_memory()
+        ws = api.host_workspace(chunk, DEV)
+        getattr(api, fn + "_host")(hx0, hx1, hy0, hy1, api.Params(**kw), SEEDS, ws, chunk, base)
+        assert np.array_equal(hy0.numpy().view(np.uint64), ref["y0"]), chunk
+        assert np.array_equal(hy1.numpy().view(np.uint64), ref["y1"]), chunk
+
+
+def test_host_entry_errors(api):
+    import ctypes
+    L = api.lib()
+    cp, cs = api.Params().c(), api.seeds_struct(SEEDS)
+    h = [torch.zeros(64, dtype=torch.int64).pin_memory() for _ in range(4)]
+    p = [t.data_ptr() for t in h]
+    ws = api.host_workspace(64, DEV)
+    nb = ws.numel() * 8
+    assert L.bc_host_workspace_bytes(64) == nb == 3 * 4 * 64 * 8
+    call = lambda *a, chunk=64, wsb=nb, base=0: L.bc_drelu_host(*a, 64, base, ctypes.byref(cp), ctypes.byref(cs),  # noqa: E731
+                                                                 ws.data_ptr(), wsb, chunk, None)
+    assert call(*p) == 0
+    assert call(*p, chunk=12) == -1          # not a multiple of 8
+    assert call(*p, wsb=nb - 8) == -1        # workspace too small
+    assert call(*p, base=4) == -3
+    assert call(p[0], p[1], p[0], p[3]) == -5

@@ -1,4 +1,4 @@
-"""Sweep the host-buffer pipeline (streams x chunks) and raw PCIe copy rates."""
+"""Sweep the native host-buffer pipeline (chunk sizes) and raw PCIe copy rates."""
 import os, sys, time, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -24,12 +24,11 @@ def both():
     with torch.cuda.stream(s2): hy0.copy_(d2, non_blocking=True)
 out["bidir_GBs_each"] = bw(both, 8 * n)
 prm, sd = api.Params(), synth.seeds(0)
-for streams in (2, 3, 4):
-    for chunks in (8, 16, 32):
-        ex = H.HostPipeline(n, dev, chunks=chunks, streams=streams)
-        for _ in range(2): ex.drelu(hx0, hx1, hy0, hy1, prm, sd)
-        torch.cuda.synchronize(); t = time.perf_counter()
-        for _ in range(10): ex.drelu(hx0, hx1, hy0, hy1, prm, sd)
-        torch.cuda.synchronize(); dt = (time.perf_counter() - t) / 10
-        out[f"s{streams}_c{chunks}"] = n / dt / 1e9
+for chunk in (1 << 18, 1 << 19, 1 << 20, 1 << 21, 1 << 22):
+    ex = H.HostPipeline(dev, chunk=chunk)
+    for _ in range(2): ex.drelu(hx0, hx1, hy0, hy1, prm, sd)
+    torch.cuda.synchronize(); t = time.perf_counter()
+    for _ in range(10): ex.drelu(hx0, hx1, hy0, hy1, prm, sd)
+    torch.cuda.synchronize(); dt = (time.perf_counter() - t) / 10
+    out[f"chunk{chunk}"] = n / dt / 1e9
 print(json.dumps(out))
