@@ -19,9 +19,7 @@ def test_compute_sanitizer(tool):
     cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
     if not os.path.exists(cs):
         pytest.skip("compute-sanitizer not installed")
-    cmd = [cs, "--tool", tool, "--error-exitcode", "3"]
-    if tool == "initcheck":
-        cmd += ["--track-unused-memory", "no"]
+    cmd = [cs, "--tool", tool, "--error-exitcode", "3"]  # initcheck: unused-memory tracking is off by default
     r = subprocess.run(cmd + [sys.executable, os.path.join(ROOT, "tools", "sanitize_run.py")],
                        capture_output=True, text=True, timeout=900)
     tail = (r.stdout + r.stderr)[-3000:]

@@ -30,5 +30,25 @@ for kw in (dict(), dict(ell=16, lx=7, f=0, mode="literal"), dict(ell=32, lx=5, f
         e, c1 = api.relu_helper(L0, H0, L1, H1, prm, sd.s02, sd.s12, 8)
         api.relu_finish(0, a0, T0, d0, d1, e, None, prm, sd.s02, 8)
         api.relu_finish(1, a1, T1, d1, d0, e, c1, prm, sd.s12, 8)
+# RSS variant (Alg 9), large tape (lx = 31), truncation study, host-buffer entry
+prm = api.Params(rounds=8)
+for n in (1, 13, 1003):
+    x = synth.plaintext(n, 64, 7, 24, "D1")
+    xs = [t(v) for v in synth.rss_share(x, 64)]
+    api.drelu_rss(*xs, prm, sd, 8)
+    api.relu_rss(*xs, prm, sd, 8)
+    x, x0, x1 = synth.shares(n, 64, 7, 24, "D1")
+    a0, a1 = t(x0), t(x1)
+    big = api.Params(ell=64, lx=31, f=0, rounds=8)
+    tr = api.transcript_buffers(n, dev, big)
+    api.drelu(a0, a1, big, sd, 8, transcript=tr)
+    api.relu(a0, a1, big, sd, 8)
+    api.trc_aby3(a0, a1, 64, 26, sd, 8, q=1, rounds=8)
+    api.mul_trc("trc_then_mul", "aby3", a0, a1, a0, a1, 64, 26, sd, 8, rounds=8)
+    api.mul_trc("mul_then_trc", "secureml", a0, a1, a0, a1, 64, 26, sd, 8, rounds=8)
+    api.trc_count("det", a0, 64, 26, 0, 1000)
+    hx0, hx1 = torch.from_numpy(x0.view(np.int64)).pin_memory(), torch.from_numpy(x1.view(np.int64)).pin_memory()
+    hy0, hy1 = torch.empty(n, dtype=torch.int64).pin_memory(), torch.empty(n, dtype=torch.int64).pin_memory()
+    api.drelu_host(hx0, hx1, hy0, hy1, prm, sd, api.host_workspace(512, dev), 512, 8)
 torch.cuda.synchronize()
 print("sanitize_run ok")
