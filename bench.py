@@ -443,6 +443,17 @@ def party_chain(api, prm, seeds, x0, x1, base, dev, stream, timed, world, n):
         ms = t_ms / 50
         res[name] = {"value": world * n / (ms * 1e-3), "unit": "elements/s", "ms_per_step": ms, "launches_per_step": 5}
     res["note"] = "P0,P1 send + P2 helper + P0,P1 finish back to back on one GPU: all parties' work, nothing shared"
+    # the messages these kernels exchange, per element (DESIGN.md sec. 4 wire format) vs Table 1
+    slots, pbits = LX + 1, 9 if MODE == "guard" else 8
+    res["wire_bytes_per_elem"] = {
+        "drelu": {"P0->P2": slots * pbits / 8, "P1->P2": slots * pbits / 8, "P2->P1": 8.0},
+        "relu": {"P0->P2": slots * pbits / 8, "P1->P2": slots * pbits / 8, "P0<->P1 (d)": 8.0,
+                 "P2->P0,P1 (e)": 8.0, "P2->P1 ([c]_1, preprocessing)": 8.0},
+        "one_pass_bits_per_party": slots * pbits,
+        "paper_one_pass_bits_per_party": (LX + 1) * (LX + 1),
+        "note": "Table 1 counts (lx+1)^2 = 64 bits in the paper's literal domain; guard mode (reading C6) "
+                "sends lx+1 slots of ceil(log2 257) = 9 bits = 72",
+    }
     return res
 
 
