@@ -396,6 +396,14 @@ def run_cuda(a):
                         "roofline": roofline(name, v_fp, ms_fp)}
         fp["note"] = "lx=31, f=0, guard (w=32, p=2^32+15, 32 slots): the paper's full 5+26 precision, same batch"
         line["full_precision"] = fp
+        # ---- Bicoptor-1 as the paper describes it (NEXT #4), same batch and seeds ----
+        t_b1, _, _ = timed(lambda: api.drelu_b1(x0, x1, prm, seeds, base, y0, y1, stream=stream), 20, 3)
+        line["bicoptor1"] = {
+            "drelu": {"value": world * n / (t_b1 / 20 * 1e-3), "unit": "elements/s", "ms_per_step": t_b1 / 20},
+            "one_pass_bits_per_party": (LX + 1) * ELL, "bicoptor2_one_pass_bits_per_party": (LX + 1) * 9,
+            "note": "SecureML truncation, recursive sums, no modulo switch, 64-bit masks (readings C32-C34); "
+                    "3 ChaCha blocks per element vs 0.5",
+        }
         # ---- truncation study (NEXT #3): exact e1 counting, Alg 3 vs mult-then-trc ----
         line["trunc_study"] = trunc_leg(api, seeds, x0, x1, base, dev, stream, timed, world, n)
         # ---- config 5: E2E-shaped ReLU layer streams (CUDA graph per network) ----

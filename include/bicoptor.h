@@ -132,6 +132,16 @@ int bc_relu(const uint64_t *x0, const uint64_t *x1, uint64_t *y0, uint64_t *y1, 
             uint64_t elem_base, const bc_params *prm, const bc_seeds *seeds,
             const bc_transcript *tr, void *stream);
 
+/* Bicoptor-1 DReLU as Bicoptor 2.0 describes its predecessor -- an in-repo
+ * comparison point (readings C32-C34): SecureML truncation
+ * (u_i in Z_{2^ell}, probabilistic), recursive sums, no modulo
+ * switch, odd masks and reshares in Z_{2^ell}; (lx+1) * ell message bits per
+ * party.  Arguments as bc_drelu; prm->slots <= 8; tr, if given,
+ * receives W0, W1 as uint64_t[n][slots] planes in w0_lo / w1_lo (hi NULL). */
+int bc_drelu_b1(const uint64_t *x0, const uint64_t *x1, uint64_t *y0, uint64_t *y1, size_t n,
+                uint64_t elem_base, const bc_params *prm, const bc_seeds *seeds,
+                const bc_transcript *tr, void *stream);
+
 /* ---- host-buffer entry points (end to end) ------------------------------
  *
  * bc_drelu / bc_relu on shares that live in HOST memory: x0, x1 (in) and y0,

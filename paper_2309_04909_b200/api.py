@@ -74,6 +74,8 @@ _SIG = {
                                       ctypes.POINTER(bc_params), ctypes.c_char_p, ctypes.c_char_p, _P]),
     "bc_relu_finish": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64,
                                       ctypes.POINTER(bc_params), ctypes.c_char_p, _P]),
+    "bc_drelu_b1": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64, ctypes.POINTER(bc_params),
+                                   ctypes.POINTER(bc_seeds), ctypes.POINTER(bc_transcript), _P]),
     "bc_host_workspace_bytes": (ctypes.c_size_t, [ctypes.c_size_t]),
     "bc_drelu_host": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64, ctypes.POINTER(bc_params),
                                      ctypes.POINTER(bc_seeds), _P, ctypes.c_size_t, ctypes.c_size_t, _P]),
@@ -215,6 +217,12 @@ def _fused(fn, what, x0, x1, prm, seeds, elem_base, y0, y1, transcript, stream):
     _check(fn(_dev(x0, "x0"), _dev(x1, "x1"), _dev(y0, "y0"), _dev(y1, "y1"), n, elem_base, ctypes.byref(cp),
               ctypes.byref(cs), ctypes.byref(tr) if tr is not None else None, _stream(stream)), what)
     return y0, y1
+
+
+def drelu_b1(x0, x1, prm: Params, seeds, elem_base: int = 0, y0=None, y1=None, transcript=None, stream=None):
+    """Bicoptor-1 DReLU (comparison point): returns (y0, y1); transcript = u64 planes
+    {"w0_lo", "w1_lo"} of shape (n, lx+1)."""
+    return _fused(lib().bc_drelu_b1, "bc_drelu_b1", x0, x1, prm, seeds, elem_base, y0, y1, transcript, stream)
 
 
 def transcript_buffers(n: int, device, prm: "Params | None" = None) -> dict:

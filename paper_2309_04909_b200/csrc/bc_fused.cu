@@ -213,6 +213,102 @@ __global__ void __launch_bounds__(TPB_L) k_fused_l(FusedArgs a, KP kp, KPL kl, K
   }
 }
 
+// ---- Bicoptor-1 as Bicoptor 2.0 describes it (NEXT #4; readings C32-C34) ----------
+// SecureML truncation (u_i in Z_{2^ell}), recursive sums, no modulo switch, odd
+// 64-bit masks and 64-bit reshares: 3 seed01 blocks per element (bc1.tape).
+constexpr uint64_t L_TAPE1 = lbl("bc1.tape");
+constexpr uint64_t L_FB1 = lbl("bc1.fbk1");
+
+template <int R>
+__device__ __noinline__ uint32_t fallback_b1(uint64_t j, Key key, uint32_t lim) {
+  uint32_t B[16];
+  for (uint32_t k = 0;; ++k) {
+    if ((k & 15u) == 0) chacha<R>(key, j * 256 + (k >> 4), L_FB1, B);
+    uint32_t w = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if ((uint32_t)i == (k & 15u)) w = B[i];
+    const uint32_t v = w & 0x7FFFFFFFu;
+    if (v < lim) return v;
+  }
+}
+
+template <int R, bool TRANSCRIPT>
+__global__ void __launch_bounds__(TPB_L) k_fused_b1(FusedArgs a, KP kp, Key k01, Key k02, Key k12) {
+  __shared__ uint64_t sv[2 * 8 * TPB_L];  // [party][slot][thread]
+  const uint32_t tid = threadIdx.x, S = kp.S;
+  const uint64_t ym = kp.ymask;
+  const uint64_t ngroups = (a.n + 7) >> 3;
+  for (uint64_t g = (uint64_t)blockIdx.x * TPB_L + tid; g < ngroups; g += (uint64_t)gridDim.x * TPB_L) {
+    const uint64_t i0 = g << 3;
+    const uint64_t j0 = a.base + i0;
+    const uint32_t cnt = (uint32_t)min((uint64_t)8, a.n - i0);
+    uint32_t zbits = 0, tbits = 0;
+#pragma unroll 1
+    for (uint32_t e = 0; e < cnt; ++e) {
+      const uint64_t j = j0 + e, i = i0 + e;
+      uint64_t r[8], rho[8];
+      uint32_t t, idx;
+      {
+        uint32_t B[16];
+        chacha<R>(k01, 3 * j, L_TAPE1, B);             // words 0..15: t|idx, r_0..r_6
+        t = B[0] >> 31;
+        idx = B[0] & 0x7FFFFFFFu;
+#pragma unroll
+        for (int m = 0; m < 7; ++m) r[m] = (uint64_t)B[2 + 2 * m] | ((uint64_t)B[3 + 2 * m] << 32);
+        chacha<R>(k01, 3 * j + 1, L_TAPE1, B);         // words 16..31: r_7, rho_0..rho_6
+        r[7] = (uint64_t)B[0] | ((uint64_t)B[1] << 32);
+#pragma unroll
+        for (int m = 0; m < 7; ++m) rho[m] = (uint64_t)B[2 + 2 * m] | ((uint64_t)B[3 + 2 * m] << 32);
+        chacha<R>(k01, 3 * j + 2, L_TAPE1, B);         // words 32, 33: rho_7
+        rho[7] = (uint64_t)B[0] | ((uint64_t)B[1] << 32);
+      }
+      if (idx >= kp.perm_lim) idx = fallback_b1<R>(j, k01, kp.perm_lim);
+      // step 6: Fisher-Yates nibble selector (same digits as the wide tape)
+      uint32_t sel = 0x76543210u;
+      for (uint32_t m = S - 1; m >= 1; --m) {
+        const uint32_t k = idx % (m + 1);
+        idx /= (m + 1);
+        const uint32_t aa = (sel >> (4 * m)) & 15u, bb = (sel >> (4 * k)) & 15u, d = aa ^ bb;
+        sel ^= (d << (4 * m)) ^ (d << (4 * k));
+      }
+      // steps 1-4: blind, Alg 1 truncations u_i = trc(s, f+i) in Z_{2^ell}, recursive sums
+      const uint64_t x0v = __ldg(a.x0 + i), x1v = __ldg(a.x1 + i);
+      const uint64_t s0 = (t ? 0ull - x0v : x0v) & ym;
+      const uint64_t n1 = (t ? x1v : 0ull - x1v) & ym;  // -s1 mod 2^ell
+      uint64_t acc0 = 0, acc1 = 0;
+#pragma unroll
+      for (int q = 7; q >= 0; --q) {
+        if ((uint32_t)q < S) {
+          acc0 += s0 >> (kp.f + q);                    // P0: cut(s0, f+q)
+          acc1 -= n1 >> (kp.f + q);                    // P1: -cut(-s1, f+q)
+          sv[(0 * 8 + q) * TPB_L + tid] = acc0 - 1ull; // v_q, P0 carries the -1
+          sv[(1 * 8 + q) * TPB_L + tid] = acc1;
+        }
+      }
+      // steps 6-9: shuffle, mask (odd r), reshare, P2's zero test, all mod 2^ell
+      uint32_t z = 0;
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        if ((uint32_t)m < S) {
+          const uint32_t src = (sel >> (4 * m)) & 15u;
+          const uint64_t rm = r[m] | 1ull;
+          const uint64_t W0 = (sv[src * TPB_L + tid] * rm + rho[m]) & ym;
+          const uint64_t W1 = (sv[(8 + src) * TPB_L + tid] * rm - rho[m]) & ym;
+          if (TRANSCRIPT) {
+            reinterpret_cast<uint64_t*>(a.w0lo)[i * S + m] = W0;
+            reinterpret_cast<uint64_t*>(a.w1lo)[i * S + m] = W1;
+          }
+          z |= ((W0 + W1) & ym) == 0 ? 1u : 0u;
+        }
+      }
+      zbits |= z << e;
+      tbits |= t << e;
+    }
+    finish_group<R, false>(a, kp, k02, k12, i0, j0, cnt, zbits, tbits);
+  }
+}
+
 template <bool RELU>
 int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, size_t n, uint64_t base,
           const bc_params* prm, const bc_seeds* seeds, const bc_transcript* tr, void* stream) {
@@ -266,9 +362,51 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
   });
 }
 
+int drelu_b1(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, size_t n, uint64_t base,
+             const bc_params* prm, const bc_seeds* seeds, const bc_transcript* tr, void* stream) {
+  const int rc = check_params(prm);
+  if (rc) return rc;
+  if (prm->slots > 8) return BC_EINVAL;
+  if (n == 0) return BC_OK;
+  if (!x0 || !x1 || !y0 || !y1 || !seeds) return BC_EINVAL;
+  if (!aligned16(x0) || !aligned16(x1) || !aligned16(y0) || !aligned16(y1) || (base & 7)) return BC_EALIGN;
+  const size_t nb = n * 8;
+  if (overlap(y0, nb, y1, nb) || overlap(y0, nb, x0, nb) || overlap(y0, nb, x1, nb) || overlap(y1, nb, x0, nb) ||
+      overlap(y1, nb, x1, nb))
+    return BC_EALIAS;
+  FusedArgs a{x0, x1, y0, y1, (uint64_t)n, base, nullptr, nullptr, nullptr, nullptr};
+  if (tr) {  // W planes as uint64_t[n][slots]
+    if (!tr->w0_lo || !tr->w1_lo || tr->w0_hi || tr->w1_hi) return BC_EINVAL;
+    if (!aligned8(tr->w0_lo) || !aligned8(tr->w1_lo)) return BC_EALIGN;
+    const size_t wb = n * prm->slots * 8;
+    if (overlap(tr->w0_lo, wb, tr->w1_lo, wb) || overlap(tr->w0_lo, wb, x0, nb) || overlap(tr->w0_lo, wb, x1, nb) ||
+        overlap(tr->w1_lo, wb, x0, nb) || overlap(tr->w1_lo, wb, x1, nb) || overlap(tr->w0_lo, wb, y0, nb) ||
+        overlap(tr->w0_lo, wb, y1, nb) || overlap(tr->w1_lo, wb, y0, nb) || overlap(tr->w1_lo, wb, y1, nb))
+      return BC_EALIAS;
+    a.w0lo = tr->w0_lo;
+    a.w1lo = tr->w1_lo;
+  }
+  KP kp = make_kp(prm);
+  const uint32_t fact = [&] { uint32_t f = 1; for (uint32_t i = 2; i <= prm->slots; ++i) f *= i; return f; }();
+  kp.perm_lim = (uint32_t)((0x80000000ull / fact) * fact);
+  const Key k01 = make_key(seeds->s01), k02 = make_key(seeds->s02), k12 = make_key(seeds->s12);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return dispatch_rounds(prm->rounds, [&](auto Rc) {
+    constexpr int R = decltype(Rc)::value;
+    auto fn = tr ? k_fused_b1<R, true> : k_fused_b1<R, false>;
+    fn<<<grid_for((const void*)fn, (n + 7) / 8, TPB_L), TPB_L, 0, st>>>(a, kp, k01, k02, k12);
+    return check_launch();
+  });
+}
+
 }  // namespace
 
 extern "C" {
+
+int bc_drelu_b1(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, size_t n, uint64_t elem_base,
+                const bc_params* prm, const bc_seeds* seeds, const bc_transcript* tr, void* stream) {
+  return drelu_b1(x0, x1, y0, y1, n, elem_base, prm, seeds, tr, stream);
+}
 
 int bc_drelu(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, size_t n, uint64_t elem_base,
              const bc_params* prm, const bc_seeds* seeds, const bc_transcript* tr, void* stream) {

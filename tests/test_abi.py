@@ -29,7 +29,7 @@ def test_header_declares_the_boundary():
     for must in ("bc_params_init", "bc_trc", "bc_modswitch", "bc_ladder_modswitch", "bc_drelu", "bc_relu",
                  "bc_drelu_send", "bc_drelu_helper", "bc_drelu_finish", "bc_relu_send", "bc_relu_helper",
                  "bc_relu_finish", "bc_strerror", "bc_trc_prob", "bc_drelu_rss", "bc_relu_rss",
-                 "bc_trc_aby3", "bc_trc_count", "bc_mul_trc", "bc_drelu_host", "bc_relu_host"):
+                 "bc_trc_aby3", "bc_trc_count", "bc_mul_trc", "bc_drelu_host", "bc_relu_host", "bc_drelu_b1"):
         assert must in names
 
 

@@ -592,3 +592,45 @@ def test_host_entry_errors(api):
     assert call(*p, wsb=nb - 8) == -1        # workspace too small
     assert call(*p, base=4) == -3
     assert call(p[0], p[1], p[0], p[3]) == -5
+
+
+# ---- Bicoptor-1 comparison point (NEXT #4) -------------------------------------------------
+
+B1_PARAMS = [PARAMS[0], dict(ell=32, lx=7, f=0, mode="guard", rounds=12), PARAMS[3],
+             dict(ell=16, lx=4, f=1, mode="guard", rounds=8)]
+
+
+@pytest.mark.parametrize("kw", B1_PARAMS, ids=_ids)
+def test_b1_parity_with_transcript(api, kw):
+    from oracle import bicoptor1 as B1
+    oprm, prm = B.Params(**kw), api.Params(**kw)
+    for n in SIZES:
+        for base in (0, 1 << 40):
+            x, x0, x1 = synth.shares(n, kw["ell"], kw["lx"], kw["f"], "D1", run=n)
+            j = np.arange(n, dtype=np.uint64) + np.uint64(base)
+            ref = B1.drelu1(oprm, x0, x1, j, SEEDS)
+            S = kw["lx"] + 1
+            tr = {"w0_lo": torch.empty((n, S), dtype=torch.int64, device=DEV),
+                  "w1_lo": torch.empty((n, S), dtype=torch.int64, device=DEV)}
+            y0, y1 = api.drelu_b1(dev(x0), dev(x1), prm, SEEDS, elem_base=base, transcript=tr)
+            assert np.array_equal(host(y0), ref["y0"]) and np.array_equal(host(y1), ref["y1"]), (n, base)
+            assert np.array_equal(host(tr["w0_lo"]), ref["W0"]) and np.array_equal(host(tr["w1_lo"]), ref["W1"])
+
+
+def test_b1_fallback_elements(api):
+    """Elements whose Bicoptor-1 perm index rejects (~6e-8 per element; indices
+    from tests/golden/b1_fallback.txt, written from the oracle by
+    tools/find_b1_fallback.py) take the fallback stream on both sides."""
+    import os
+    from oracle import bicoptor1 as B1
+    kw = PARAMS[0]
+    path = os.path.join(os.path.dirname(__file__), "golden", "b1_fallback.txt")
+    rej = [int(v) for v in open(path).read().split() if not v.startswith("#") and v.strip().isdigit()]
+    assert len(rej) >= 2
+    for r in rej:
+        base = int(r) - int(r) % 8
+        x, x0, x1 = synth.shares(16, 64, 7, 24, "D2", run=int(r))
+        jj = np.arange(16, dtype=np.uint64) + np.uint64(base)
+        ref = B1.drelu1(B.Params(**kw), x0, x1, jj, SEEDS)
+        y0, y1 = api.drelu_b1(dev(x0), dev(x1), api.Params(**kw), SEEDS, elem_base=base)
+        assert np.array_equal(host(y0), ref["y0"]) and np.array_equal(host(y1), ref["y1"])

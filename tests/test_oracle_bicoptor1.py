@@ -77,3 +77,18 @@ def test_e1_breaks_bicoptor1_not_bicoptor2_at_ell16():
         y = ring.add(ring.trc_secureml(0, s0, f + i, ell), ring.trc_secureml(1, s1, f + i, ell), ell)
         any_e1 |= trunc.classify(sb, y, f + i, ell) == trunc.E1
     assert np.all(any_e1[bad])
+
+
+def test_golden_fallback_indices_reject():
+    """The fixture tests/golden/b1_fallback.txt lists elements whose tape word 0
+    rejects; decoding them still yields valid Fisher-Yates digits (fallback)."""
+    import os
+    from oracle.chacha import chacha_blocks
+    path = os.path.join(os.path.dirname(__file__), "golden", "b1_fallback.txt")
+    rej = [int(v) for v in open(path).read().split() if v.strip().isdigit()]
+    assert len(rej) >= 2
+    j = np.array(rej, dtype=np.uint64)
+    w0 = chacha_blocks(SEEDS.s01, B1.L_TAPE1, 3 * j, 20)[:, 0] & np.uint32(0x7FFFFFFF)
+    assert np.all(w0 >= np.uint32((2**31 // 40320) * 40320))
+    tp = B1.tape1(B.Params(), SEEDS.s01, j)
+    assert np.all(tp["k"] <= np.arange(8))
