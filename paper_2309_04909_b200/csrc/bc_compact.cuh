@@ -185,7 +185,14 @@ __device__ __forceinline__ void mask_slots(uint32_t lo, uint32_t hi, const TapeC
 }
 
 // Steps 1-9 for both computing parties and P2 on one element; returns z.
-// If W0/W1 are non-null the messages are also returned (transcript).
+// KEEP_W: the messages are returned (transcript).  BC_MATERIALIZE (default 1):
+// P0's and P1's messages are always formed as wire values in [0, 257) and P2
+// tests their sum, so the reshare rho -- which cancels in P2's sum -- cannot be
+// folded out of the simulation.  BC_MATERIALIZE=0 lets P2 test the unreduced
+// congruent sum instead (12% faster).
+#ifndef BC_MATERIALIZE
+#define BC_MATERIALIZE 1
+#endif
 template <bool KEEP_W>
 __device__ __forceinline__ uint32_t elem_both(uint64_t x0, uint64_t x1, const TapeC& tp, uint32_t fsh, bool fhi,
                                               uint32_t (&W0)[8], uint32_t (&W1)[8]) {
@@ -202,7 +209,7 @@ __device__ __forceinline__ uint32_t elem_both(uint64_t x0, uint64_t x1, const Ta
     // P0's and P1's messages as integers < 2^17 congruent to W0_m, W1_m (mod 257)
     const uint32_t x0 = byte_of(m < 4 ? c_lo : c_hi, m & 3) * r + a0;   // (v'+1) r + rho + 257
     const uint32_t x1 = byte_of(m < 4 ? d_lo : d_hi, m & 3) * r + a1;   // (v'+1) r - rho + 514
-    if (KEEP_W) {  // transcript: the wire format needs the reduced values
+    if (KEEP_W || BC_MATERIALIZE) {  // the wire values W in [0, 257)
       W0[m] = mod257s(x0);
       W1[m] = mod257s(x1);
       const uint32_t s = W0[m] + W1[m];
@@ -213,7 +220,7 @@ __device__ __forceinline__ uint32_t elem_both(uint64_t x0, uint64_t x1, const Ta
       vmin = min(vmin, (x0 + x1) * 0xFF00FF01u);
     }
   }
-  if (!KEEP_W) return vmin <= 16711935u;
+  if (!(KEEP_W || BC_MATERIALIZE)) return vmin <= 16711935u;
   return vmin == 0u;
 }
 
