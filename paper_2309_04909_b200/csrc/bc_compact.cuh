@@ -185,11 +185,13 @@ __device__ __forceinline__ void mask_slots(uint32_t lo, uint32_t hi, const TapeC
 }
 
 // Steps 1-9 for both computing parties and P2 on one element; returns z.
-// KEEP_W: the messages are returned (transcript).  BC_MATERIALIZE (default 1):
-// P0's and P1's messages are always formed as wire values in [0, 257) and P2
-// tests their sum, so the reshare rho -- which cancels in P2's sum -- cannot be
-// folded out of the simulation.  BC_MATERIALIZE=0 lets P2 test the unreduced
-// congruent sum instead (12% faster).
+// KEEP_W: the messages are returned (transcript, both reduced to [0, 257)).
+// Otherwise BC_MATERIALIZE selects how P2 tests w_m = 0:
+//   0  the unreduced congruent sum -- the reshare rho cancels and the compiler
+//      folds its decode away (fastest, 0.457 ms / 2^24);
+//   1  (default) P0's wire value W0 in [0, 257) plus P1's congruent message:
+//      rho is decoded and enters through the reduction (0.498 ms);
+//   2  both wire values reduced, as the transcript path (0.514 ms).
 #ifndef BC_MATERIALIZE
 #define BC_MATERIALIZE 1
 #endif
@@ -209,7 +211,12 @@ __device__ __forceinline__ uint32_t elem_both(uint64_t x0, uint64_t x1, const Ta
     // P0's and P1's messages as integers < 2^17 congruent to W0_m, W1_m (mod 257)
     const uint32_t x0 = byte_of(m < 4 ? c_lo : c_hi, m & 3) * r + a0;   // (v'+1) r + rho + 257
     const uint32_t x1 = byte_of(m < 4 ? d_lo : d_hi, m & 3) * r + a1;   // (v'+1) r - rho + 514
-    if (KEEP_W || BC_MATERIALIZE) {  // the wire values W in [0, 257)
+    if (!KEEP_W && BC_MATERIALIZE == 1) {
+      // P0's wire value W0 in [0, 257), P1's message as its congruent representative x1;
+      // P2: 257 | (W0 + x1) by the multiplicative test (W0 + x1 < 2^18).  rho enters
+      // through the reduction of W0, so it cannot cancel algebraically.
+      vmin = min(vmin, (mod257s(x0) + x1) * 0xFF00FF01u);
+    } else if (KEEP_W || BC_MATERIALIZE) {  // the wire values W in [0, 257)
       W0[m] = mod257s(x0);
       W1[m] = mod257s(x1);
       const uint32_t s = W0[m] + W1[m];
@@ -220,7 +227,7 @@ __device__ __forceinline__ uint32_t elem_both(uint64_t x0, uint64_t x1, const Ta
       vmin = min(vmin, (x0 + x1) * 0xFF00FF01u);
     }
   }
-  if (!(KEEP_W || BC_MATERIALIZE)) return vmin <= 16711935u;
+  if (!KEEP_W && BC_MATERIALIZE <= 1) return vmin <= 16711935u;
   return vmin == 0u;
 }
 
