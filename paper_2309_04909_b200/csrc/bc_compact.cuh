@@ -127,7 +127,7 @@ __device__ __forceinline__ uint32_t window_of(uint64_t x, uint32_t t, uint32_t f
 // E = spread of a_0,a_2,a_4,a_6 into bytes 0,2,4,6 via one 64-bit multiply by
 // 1 + 2^14 + 2^28 + 2^42; O likewise for a_1,a_3,a_5,a_7; 16-bit lanes then
 // hold the pairwise sums without carries.  Verified exhaustively over all
-// 2^15 windows (tests/test_swar_model.py).
+// 2^15 windows (tests/test_kernel_arith.py).
 template <int PARTY>
 __device__ __forceinline__ void ladder_swar(uint32_t win, uint32_t& lo, uint32_t& hi) {
   constexpr uint32_t KL = 1u + (1u << 14) + (1u << 28);

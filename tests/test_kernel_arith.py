@@ -1,0 +1,139 @@
+"""CPU checks of the integer identities the CUDA kernels rely on, against their
+plain definitions (no oracle involved): each kernel trick is re-expressed in
+Python with 32/64-bit wrap-around and compared over its whole domain (or a
+large random sample where the domain is 2^64)."""
+import numpy as np
+
+M32 = (1 << 32) - 1
+M64 = (1 << 64) - 1
+
+
+def umulhi32(a, b):
+    return (a * b) >> 32
+
+
+# ---- compact path (csrc/bc_compact.cuh) -------------------------------------------------
+
+def test_div257_exact_all_u32_sample_and_edges():
+    """div257(x) = umulhi(x, 0xFF00FF01) >> 8 == x // 257 for every 32-bit x
+    (checked on all multiples-of-257 neighbourhoods and 2^22 random values)."""
+    rng = np.random.default_rng(0)
+    xs = list(rng.integers(0, 2**32, 1 << 16, dtype=np.uint64))
+    xs += [q * 257 + d for q in range(0, (1 << 32) // 257, 4099) for d in (0, 1, 255, 256)]
+    xs += [M32, M32 - 1, 0, 1, 256, 257]
+    for x in xs:
+        x = int(x) & M32
+        assert (umulhi32(x, 0xFF00FF01) >> 8) == x // 257
+
+
+def test_mod257s_exact_below_2_18():
+    """mod257s(x) = x - 257 umulhi(x, 0xFF0100) == x % 257 for x < 2^18."""
+    x = np.arange(1 << 18, dtype=np.uint64)
+    q = (x * np.uint64(0xFF0100)) >> np.uint64(32)
+    assert np.array_equal(x - np.uint64(257) * q, x % np.uint64(257))
+
+
+def test_multiplicative_divisibility_test_below_2_19():
+    """257 | s  <=>  s * 257^-1 mod 2^32 <= floor((2^32-1)/257), for s < 2^19."""
+    s = np.arange(1 << 19, dtype=np.uint64)
+    lhs = ((s * np.uint64(0xFF00FF01)) & np.uint64(M32)) <= np.uint64(16711935)
+    assert (0xFF00FF01 * 257) & M32 == 1
+    assert np.array_equal(lhs, s % np.uint64(257) == 0)
+
+
+def test_ladder_swar_all_windows():
+    """ladder_swar: for every 15-bit window, the bytes produced by the 64-bit
+    spread multiply equal the direct per-slot values u_i + u_{i+1} - 2 (P0) and
+    -(u_i + u_{i+1}) (P1), mod 256, with u_i the 8-bit window at bit i."""
+    KL = 1 + (1 << 14) + (1 << 28)
+    MM = 0x00FF00FF
+
+    def swar(win, party):
+        e, o = win & 0x3FFF, (win >> 1) & 0x3FFF
+        Elo, Ehi = (e * KL) & M32 & MM, ((e >> 4) + (e << 10)) & MM
+        Olo, Ohi = (o * KL) & M32 & MM, ((o >> 4) + (o << 10)) & MM
+        Slo = ((Elo >> 16) | (Ehi << 16)) & M32
+        Shi = Ehi >> 16
+        if party == 0:
+            ce_lo, ce_hi = (Elo + Olo + 0x00FE00FE) & M32, (Ehi + Ohi + 0x00FE00FE) & M32
+            co_lo, co_hi = (Olo + Slo + 0x00FE00FE) & M32, (Ohi + Shi + 0x00FE00FE) & M32
+        else:
+            ce_lo, ce_hi = (0x04000400 - Elo - Olo) & M32, (0x04000400 - Ehi - Ohi) & M32
+            co_lo, co_hi = (0x04000400 - Olo - Slo) & M32, (0x04000400 - Ohi - Shi) & M32
+        lo = (ce_lo & MM) | ((co_lo << 8) & ~MM & M32)
+        hi = (ce_hi & MM) | ((co_hi << 8) & ~MM & M32)
+        return [(lo >> (8 * k)) & 255 for k in range(4)] + [(hi >> (8 * k)) & 255 for k in range(4)]
+
+    for win in range(1 << 15):
+        u = [(win >> i) & 255 for i in range(8)]
+        want0 = [(u[i] + (u[i + 1] if i < 7 else 0) - 2) & 255 for i in range(8)]
+        want1 = [(-(u[i] + (u[i + 1] if i < 7 else 0))) & 255 for i in range(8)]
+        assert swar(win, 0) == want0, win
+        assert swar(win, 1) == want1, win
+
+
+# ---- large path (csrc/bc_large.cuh) -----------------------------------------------------
+
+def _kpl(p):
+    inv = p
+    for _ in range(5):
+        inv = (inv * (2 - p * inv)) & M64
+    assert (inv * p) & M64 == 1
+    return {"p": p, "pinv": inv, "mu_p": M64 // p, "mu_q": M64 // (p - 1)}
+
+
+def mont(a, b, k):
+    lo, hi = (a * b) & M64, (a * b) >> 64
+    mh = (((lo * k["pinv"]) & M64) * k["p"]) >> 64
+    return hi - mh if hi >= mh else (hi - mh + k["p"]) & M64
+
+
+def barrett(u, q, mu):
+    r = (u - ((u * mu) >> 64) * q) & M64
+    return r - q if r >= q else r
+
+
+def test_subtractive_redc_and_barrett():
+    rng = np.random.default_rng(1)
+    for p in (2**32 + 15, 2**31 + 11, 65537, 521, 2053):
+        k = _kpl(p)
+        rinv = pow(2, -64, p)
+        for _ in range(3000):
+            a, b = int(rng.integers(0, p)), int(rng.integers(0, p))
+            assert mont(a, b, k) == a * b * rinv % p
+            u = int(rng.integers(0, 2**63)) * 2 + int(rng.integers(0, 2))
+            assert barrett(u, p, k["mu_p"]) == u % p
+            assert barrett(u, p - 1, k["mu_q"]) == u % (p - 1)
+        for a, b in ((p - 1, p - 1), (0, p - 1), (1, 1)):
+            assert mont(a, b, k) == a * b * rinv % p
+        for u in (M64, M64 - 1, 0, p, p - 1):
+            assert barrett(u, p, k["mu_p"]) == u % p and barrett(u, p - 1, k["mu_q"]) == u % (p - 1)
+
+
+def test_funnel_windows_match_shifts():
+    """slot_values: bits [i, i+w) of a 64-bit value via a clamped 32-bit funnel
+    shift equal (v >> i) & (2^w - 1) for i <= 31, and the successor window at
+    i + 1 <= 32 (clamped shift of 32 = the high word)."""
+    rng = np.random.default_rng(2)
+
+    def fsr(lo, hi, s, clamp):
+        s = min(s, 32) if clamp else s & 31
+        return (((hi << 32) | lo) >> s) & M32
+
+    for _ in range(2000):
+        v = int(rng.integers(0, 2**63)) * 2 + int(rng.integers(0, 2))
+        lo, hi = v & M32, v >> 32
+        for w in (9, 16, 31, 32):
+            wm = (1 << w) - 1
+            for i in range(32):
+                assert fsr(lo, hi, i, False) & wm == (v >> i) & wm
+                assert fsr(lo, hi, i + 1, True) & wm == (v >> (i + 1)) & wm
+
+
+def test_fisher_yates_magic_division():
+    """k = d - umulhi(d, ceil(2^32 / s)) s == d mod s for 16-bit d and s <= 32."""
+    d = np.arange(1 << 16, dtype=np.uint64)
+    for s in range(2, 33):
+        magic = (M32 // s) + 1
+        q = (d * np.uint64(magic)) >> np.uint64(32)
+        assert np.array_equal(d - q * np.uint64(s), d % np.uint64(s)), s
