@@ -63,6 +63,53 @@ class CudaCompute:
     relu_finish = staticmethod(api.relu_finish)
 
 
+class StagedCudaCompute:
+    """The libbicoptor phase kernels with host-resident messages: every phase
+    copies its inputs to this rank's GPU, runs the kernel there and returns host
+    tensors, so the messages can travel over a host transport (gloo over TCP:
+    parties on separate machines, the paper's LAN / WAN setting).
+    With NCCL use CudaCompute: the messages then stay in device memory."""
+
+    def __init__(self, device):
+        self.device = torch.device(device)
+        api.lib()
+
+    @staticmethod
+    def empty(shape, dtype):
+        return torch.empty(shape, dtype=dtype)
+
+    def _d(self, t):
+        return None if t is None else t.to(self.device, non_blocking=False)
+
+    @staticmethod
+    def _h(*ts):
+        out = tuple(None if t is None else t.cpu() for t in ts)
+        return out if len(out) > 1 else out[0]
+
+    def drelu_send(self, party, x, prm, seed01, base):
+        return self._h(*api.drelu_send(party, self._d(x), prm, seed01, base))
+
+    def drelu_helper(self, lo0, hi0, lo1, hi1, prm, seed02, base, paper_literal=False):
+        return self._h(*api.drelu_helper(self._d(lo0), self._d(hi0), self._d(lo1), self._d(hi1), prm, seed02, base,
+                                         paper_literal=paper_literal))
+
+    def drelu_finish(self, party, tbits, resp, prm, n, seed02, base, out):
+        out.copy_(api.drelu_finish(party, self._d(tbits), self._d(resp), prm, n, seed02, base).cpu())
+        return out
+
+    def relu_send(self, party, x, prm, seed01, seed_tr, base):
+        return self._h(*api.relu_send(party, self._d(x), prm, seed01, seed_tr, base))
+
+    def relu_helper(self, lo0, hi0, lo1, hi1, prm, seed02, seed12, base):
+        return self._h(*api.relu_helper(self._d(lo0), self._d(hi0), self._d(lo1), self._d(hi1), prm, seed02, seed12,
+                                        base))
+
+    def relu_finish(self, party, x, tbits, d_own, d_peer, e, c1, prm, seed_tr, base, out):
+        out.copy_(api.relu_finish(party, self._d(x), self._d(tbits), self._d(d_own), self._d(d_peer), self._d(e),
+                                  self._d(c1), prm, seed_tr, base).cpu())
+        return out
+
+
 def _chunks(n: int, chunk: int):
     chunk = max(8, (chunk // 8) * 8)  # chunk offsets stay multiples of 8 (elem_base rule)
     return [(a, min(n, a + chunk)) for a in range(0, n, chunk)]
