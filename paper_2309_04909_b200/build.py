@@ -45,7 +45,9 @@ def build(verbose: bool = False, ptxas_v: bool = False, force: bool = False, def
     headers = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(INCLUDE, "bicoptor.h"))
     lib = out or LIB
-    objdir = OBJDIR if not defines else OBJDIR + "_" + hashlib.sha256(" ".join(defines).encode()).hexdigest()[:8]
+    # variant builds (compile-time knobs) keep their objects beside the variant libraries
+    objdir = OBJDIR if not defines else os.path.join(os.path.dirname(OBJDIR), "variants",
+                                                     "obj_" + hashlib.sha256(" ".join(defines).encode()).hexdigest()[:8])
     os.makedirs(objdir, exist_ok=True)
     stamp_file = os.path.join(objdir, "stamp")
     all_src = [os.path.join(CSRC, s) for s in SOURCES]
