@@ -62,6 +62,9 @@ def parse():
                     help="party: config 4, P0/P1/P2 on distinct GPUs (needs >= 3 ranks), ReLU over NCCL P2P")
     ap.add_argument("--party-n", type=int, default=1 << 26, help="elements per P0/P1/P2 triple (config 4)")
     ap.add_argument("--chunk", type=int, default=1 << 22, help="party mode: elements per pipelined chunk")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
+                    help="party mode: NCCL P2P (party.PartyRunner) or peer memory (peer.PeerPartyRunner: the "
+                         "phase kernels store each message into the receiver's HBM over NVLink, CUDA IPC)")
     return ap.parse_args()
 
 
@@ -585,6 +588,9 @@ def run_party(a):
     dist.init_process_group("nccl", device_id=dev)
     k = world // 3
     group = dist.new_group(list(range(3 * k)))
+    # peer transport: doorbells / credits / IPC handles over a gloo group per triple
+    gloo_triples = [dist.new_group([3 * t, 3 * t + 1, 3 * t + 2], backend="gloo") for t in range(k)] \
+        if a.transport == "peer" else None
     n = a.party_n
     prm = api.Params(ell=ELL, lx=LX, f=F, mode=MODE, rounds=a.rounds)
     seeds = synth.seeds(0)
@@ -596,22 +602,34 @@ def run_party(a):
             x = synth.plaintext(n, ELL, LX, F, "D2", run=role.triple)
             x0, x1 = synth.share(x, ELL, run=role.triple)
             xs = torch.from_numpy((x0 if role.party == 0 else x1).view(np.int64)).to(dev)
-        runner = party.PartyRunner(prm, seeds, n, chunk=a.chunk, compute=party.CudaCompute(dev), group=group)
+        if a.transport == "peer":
+            from paper_2309_04909_b200 import peer
+            runner = peer.PeerPartyRunner("relu", prm, seeds, n, chunk=a.chunk, backend=peer.CudaIpcBackend(dev),
+                                          group=gloo_triples[role.triple])
+            step = lambda: runner.run(xs)  # noqa: E731
+            # egress per step: P0/P1 message + [d]_b; P2 e to both + [c]_1 (the kernels' peer stores)
+            wire = {0: 9 + 8, 1: 9 + 8, 2: 8 + 8 + 8}[role.party] * n
+        else:
+            runner = party.PartyRunner(prm, seeds, n, chunk=a.chunk, compute=party.CudaCompute(dev), group=group)
+            step = lambda: runner.relu(xs)  # noqa: E731
         for _ in range(max(a.warmup, 2)):
-            runner.relu(xs)
+            step()
         torch.cuda.synchronize(dev)
         dist.barrier(group=group)
-        runner.bytes_sent = 0
+        if a.transport == "nccl":
+            runner.bytes_sent = 0
         steps = max(1, min(a.steps, 20))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(steps):
-            runner.relu(xs)
+            step()
         e1.record()
         torch.cuda.synchronize(dev)
         dist.barrier(group=group)
         t_ms = e0.elapsed_time(e1) / steps
-        bytes_sent = runner.bytes_sent / steps
+        bytes_sent = runner.bytes_sent / steps if a.transport == "nccl" else wire
+        if a.transport == "peer":
+            runner.close()
     t = torch.tensor([t_ms, bytes_sent], dtype=torch.float64, device=dev)
     tm = t.clone()
     dist.all_reduce(tm, op=dist.ReduceOp.MAX)
@@ -621,8 +639,9 @@ def run_party(a):
         ms = float(tm[0])
         egress = {f"P{p}": float(per_rank[p][1]) / n for p in range(3)}
         print(json.dumps({
-            "metric": "config4 party-separated ReLU elements/s (P0,P1,P2 on distinct GPUs, NCCL P2P)",
-            "mode": "party", "value": k * n / (ms * 1e-3), "unit": "elements/s", "n_gpus": world, "triples": k,
+            "metric": f"config4 party-separated ReLU elements/s (P0,P1,P2 on distinct GPUs, "
+                      f"{'NCCL P2P' if a.transport == 'nccl' else 'peer-memory stores from the phase kernels'})",
+            "mode": "party", "transport": a.transport, "value": k * n / (ms * 1e-3), "unit": "elements/s", "n_gpus": world, "triples": k,
             "ms_per_step": ms, "steps": steps, "chunk": a.chunk, "higher_is_better": True, "dtype": "u64",
             "config": {"workload": f"config4: ReLU ell={ELL} lx={LX} f={F} {MODE} ChaCha{a.rounds}, 2^{int(math.log2(n))} elements per triple"},
             "wire_bytes_per_elem": egress,

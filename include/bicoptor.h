@@ -61,9 +61,10 @@ extern "C" {
  *   rounds ChaCha rounds 8, 12 or 20 (reading C19)
  * Derived by bc_params_init: w (window width), p (smallest prime > 2^w,
  * reading C7; 2^32 + 15 at lx = 31 guard), slots = lx + 1, tape (BC_TAPE_*).
- * Entry points that take a byte-plane message format (bc_ladder_modswitch,
- * the party phases) need slots <= 8 and p <= 257 (BC_EINVAL otherwise);
- * bc_drelu / bc_relu accept every tape. */
+ * bc_ladder_modswitch (a byte-plane format) needs slots <= 8 and p <= 257
+ * (BC_EINVAL otherwise); the party phases use byte planes for those and
+ * uint32 planes for the large tape (bc_drelu_send); bc_drelu / bc_relu accept
+ * every tape. */
 typedef struct bc_params {
   int32_t ell, lx, f, mode, rounds;
   uint32_t w, slots;
@@ -171,7 +172,12 @@ int bc_relu_host(const uint64_t *x0, const uint64_t *x1, uint64_t *y0, uint64_t 
  * uint8_t[n] (bit m = bit 8 of W_m; may be NULL when p <= 256), plus the
  * party's blinding bits tbits: uint8_t[(n+7)/8] (bit i%8 of byte i/8 = t_i),
  * kept locally for the finish phase.  (lx+1)*ceil(log2 p) bits per element:
- * 72 in guard mode, 64 literal (Table 1). */
+ * 72 in guard mode, 64 literal (Table 1).
+ * Large tape (lx >= 8, S = lx+1 <= 32 slots, p < 2^33): lo is
+ * uint32_t[n][S] (low 32 bits of W_m) and hi is uint32_t[n] (bit m = bit 32
+ * of W_m; may be NULL when p < 2^32): 33 S bits per element, 1,056 at the
+ * full precision lx = 31 (the paper's "31 * 31 ~ 1,000 bits").  The
+ * helper (bc_drelu_helper, bc_relu_helper[_to]) takes the same planes. */
 int bc_drelu_send(int party, const uint64_t *x, uint8_t *lo, uint8_t *hi, uint8_t *tbits,
                   size_t n, uint64_t elem_base, const bc_params *prm, const uint8_t seed01[32],
                   void *stream);
@@ -215,6 +221,40 @@ int bc_relu_finish(int party, const uint64_t *x, const uint8_t *tbits, const uin
                    const uint64_t *d_peer, const uint64_t *e, const uint64_t *c1, uint64_t *y,
                    size_t n, uint64_t elem_base, const bc_params *prm,
                    const uint8_t seed_tr[32], void *stream);
+
+/* Peer-memory variants of the ReLU phases (the transport of
+ * paper_2309_04909_b200/peer.py).  As bc_relu_send, and
+ * [d]_b is stored a second time into dshare_peer (nullable): a device pointer
+ * that may be the other computing party's receive buffer mapped into this
+ * process by bc_ipc_open (on another GPU: a peer mapping, the stores travel
+ * over NVLink).  dshare_peer must be 16-B aligned and must not overlap x or
+ * dshare (BC_EALIAS is checked in this process's address space only). */
+int bc_relu_send_to(int party, const uint64_t *x, uint8_t *lo, uint8_t *hi, uint8_t *tbits,
+                    uint64_t *dshare, uint64_t *dshare_peer, size_t n, uint64_t elem_base,
+                    const bc_params *prm, const uint8_t seed01[32], const uint8_t seed_tr[32],
+                    void *stream);
+
+/* As bc_relu_helper, with e stored to e0 (P0's copy) and, if e1 != NULL, a
+ * second time to e1 (P1's copy): Alg 8 step 3 sends e to both computing
+ * parties.  e1 != NULL requires e0 != NULL (BC_EINVAL). */
+int bc_relu_helper_to(const uint8_t *lo0, const uint8_t *hi0, const uint8_t *lo1,
+                      const uint8_t *hi1, uint64_t *e0, uint64_t *e1, uint64_t *c1, size_t n,
+                      uint64_t elem_base, const bc_params *prm, const uint8_t seed02[32],
+                      const uint8_t seed12[32], void *stream);
+
+/* ---- peer memory (CUDA IPC) -------------------------------------------------
+ * Host-only plumbing for the peer-memory transport; no kernel is launched.
+ * bc_ipc_export: handle (64 B, caller-owned host memory) of the device
+ * allocation that contains dptr, and dptr's byte offset inside it (allocators
+ * sub-allocate, so the handle names the whole allocation).  bc_ipc_open maps
+ * a handle exported by ANOTHER process into this one (*base = the mapping of
+ * the allocation's first byte; peer access is enabled lazily when the
+ * allocation lives on another GPU); bc_ipc_close unmaps it.  The exporter
+ * keeps the allocation alive until every importer has closed it.  Errors:
+ * BC_EINVAL for NULL arguments, BC_ECUDA otherwise (bc_last_cuda_error). */
+int bc_ipc_export(const void *dptr, uint8_t handle[64], uint64_t *offset);
+int bc_ipc_open(const uint8_t handle[64], void **base);
+int bc_ipc_close(void *base);
 
 /* ---- RSS variant (Alg 9; RSS ReLU P:1930-1931) -------------
  *

@@ -74,6 +74,13 @@ _SIG = {
                                       ctypes.POINTER(bc_params), ctypes.c_char_p, ctypes.c_char_p, _P]),
     "bc_relu_finish": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64,
                                       ctypes.POINTER(bc_params), ctypes.c_char_p, _P]),
+    "bc_relu_send_to": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64,
+                                       ctypes.POINTER(bc_params), ctypes.c_char_p, ctypes.c_char_p, _P]),
+    "bc_relu_helper_to": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64,
+                                         ctypes.POINTER(bc_params), ctypes.c_char_p, ctypes.c_char_p, _P]),
+    "bc_ipc_export": (ctypes.c_int, [_P, ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint64)]),
+    "bc_ipc_open": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "bc_ipc_close": (ctypes.c_int, [_P]),
     "bc_drelu_b1": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64, ctypes.POINTER(bc_params),
                                    ctypes.POINTER(bc_seeds), ctypes.POINTER(bc_transcript), _P]),
     "bc_host_workspace_bytes": (ctypes.c_size_t, [ctypes.c_size_t]),
@@ -289,9 +296,22 @@ def relu_host(hx0, hx1, hy0, hy1, prm: Params, seeds, ws, chunk: int = 1 << 20, 
 
 # ---- party-separated phases ---------------------------------------------------------
 
-def msg_buffers(n: int, device):
-    lo = torch.empty((n, 8), dtype=torch.uint8, device=device)
-    hi = torch.empty(n, dtype=torch.uint8, device=device)
+def wire_format(prm: Params) -> dict:
+    """Per-element shape and dtype of the message planes to P2 (include/bicoptor.h,
+    bc_drelu_send): byte planes lo (8 B) + hi (1 B) for slots <= 8, p <= 257; for
+    the large tape lo = S low words (uint32) + hi = one word of bit-32 flags.
+    "hi" is None when every W_m fits the lo plane."""
+    c = prm.c()
+    if c.tape == 2:  # large
+        return {"lo": ((c.slots,), torch.int32), "hi": ((), torch.int32) if c.p > 0xFFFFFFFF else None}
+    return {"lo": ((8,), torch.uint8), "hi": ((), torch.uint8) if c.p > 256 else None}
+
+
+def msg_buffers(n: int, device, prm: "Params | None" = None):
+    fmt = wire_format(prm if prm is not None else Params())
+    (los, lot), hi_f = fmt["lo"], fmt["hi"]
+    lo = torch.empty((n,) + los, dtype=lot, device=device)
+    hi = torch.empty(n, dtype=(hi_f[1] if hi_f else lot), device=device)
     tb = torch.empty((n + 7) // 8, dtype=torch.uint8, device=device)
     return lo, hi, tb
 
@@ -299,8 +319,8 @@ def msg_buffers(n: int, device):
 def drelu_send(party, x, prm: Params, seed01: bytes, elem_base=0, out=None, stream=None):
     """Alg 7 steps 1-8 for P0/P1: returns (lo, hi, tbits)."""
     n = x.numel()
-    lo, hi, tb = msg_buffers(n, x.device) if out is None else out
-    _check(lib().bc_drelu_send(party, _dev(x, "x"), _dev(lo, "lo", 1), _dev(hi, "hi", 1), _dev(tb, "tbits", 1), n,
+    lo, hi, tb = msg_buffers(n, x.device, prm) if out is None else out
+    _check(lib().bc_drelu_send(party, _dev(x, "x"), _dev(lo, "lo", None), _opt(hi, "hi", None), _dev(tb, "tbits", 1), n,
                                elem_base, ctypes.byref(prm.c()), seed01, _stream(stream)), "bc_drelu_send")
     return lo, hi, tb
 
@@ -314,7 +334,8 @@ def drelu_helper(lo0, hi0, lo1, hi1, prm: Params, seed02: bytes, elem_base=0, pa
         r1 = torch.empty(n, dtype=torch.int64, device=lo0.device)
     else:
         r0, r1 = out
-    _check(lib().bc_drelu_helper(_dev(lo0, "lo0", 1), _opt(hi0, "hi0", 1), _dev(lo1, "lo1", 1), _opt(hi1, "hi1", 1),
+    _check(lib().bc_drelu_helper(_dev(lo0, "lo0", None), _opt(hi0, "hi0", None), _dev(lo1, "lo1", None),
+                                 _opt(hi1, "hi1", None),
                                  _opt(r0, "resp0"), _dev(r1, "resp1"), n, elem_base, ctypes.byref(prm.c()), seed02,
                                  _stream(stream)), "bc_drelu_helper")
     return r0, r1
@@ -329,32 +350,47 @@ def drelu_finish(party, tbits, resp, prm: Params, n: int, seed02: bytes | None =
     return y
 
 
-def relu_send(party, x, prm: Params, seed01: bytes, seed_tr: bytes, elem_base=0, out=None, stream=None):
-    """Alg 8 steps 1, 4 for P0/P1: returns (lo, hi, tbits, dshare)."""
+def relu_send(party, x, prm: Params, seed01: bytes, seed_tr: bytes, elem_base=0, out=None, d_peer=None,
+              stream=None):
+    """Alg 8 steps 1, 4 for P0/P1: returns (lo, hi, tbits, dshare).  d_peer: a second
+    destination of dshare (bc_relu_send_to), e.g. the other party's mapped inbox."""
     n = x.numel()
     if out is None:
-        lo, hi, tb = msg_buffers(n, x.device)
+        lo, hi, tb = msg_buffers(n, x.device, prm)
         d = torch.empty_like(x)
     else:
         lo, hi, tb, d = out
-    _check(lib().bc_relu_send(party, _dev(x, "x"), _dev(lo, "lo", 1), _dev(hi, "hi", 1), _dev(tb, "tbits", 1),
-                              _dev(d, "dshare"), n, elem_base, ctypes.byref(prm.c()), seed01, seed_tr,
-                              _stream(stream)), "bc_relu_send")
+    if d_peer is None:
+        _check(lib().bc_relu_send(party, _dev(x, "x"), _dev(lo, "lo", None), _opt(hi, "hi", None),
+                                  _dev(tb, "tbits", 1),
+                                  _dev(d, "dshare"), n, elem_base, ctypes.byref(prm.c()), seed01, seed_tr,
+                                  _stream(stream)), "bc_relu_send")
+    else:
+        _check(lib().bc_relu_send_to(party, _dev(x, "x"), _dev(lo, "lo", None), _opt(hi, "hi", None),
+                                     _dev(tb, "tbits", 1), _dev(d, "dshare"), _dev(d_peer, "d_peer"), n, elem_base,
+                                     ctypes.byref(prm.c()), seed01, seed_tr, _stream(stream)), "bc_relu_send_to")
     return lo, hi, tb, d
 
 
 def relu_helper(lo0, hi0, lo1, hi1, prm: Params, seed02: bytes, seed12: bytes, elem_base=0, with_c1=True, out=None,
-                stream=None):
-    """Alg 8 steps 2-3 for P2: returns (e, c1 or None)."""
+                e_dup=None, stream=None):
+    """Alg 8 steps 2-3 for P2: returns (e, c1 or None).  e_dup: a second destination of
+    e (bc_relu_helper_to), e.g. P1's mapped inbox while e goes to P0's."""
     n = lo0.shape[0]
     if out is None:
         e = torch.empty(n, dtype=torch.int64, device=lo0.device)
         c1 = torch.empty(n, dtype=torch.int64, device=lo0.device) if with_c1 else None
     else:
         e, c1 = out
-    _check(lib().bc_relu_helper(_dev(lo0, "lo0", 1), _opt(hi0, "hi0", 1), _dev(lo1, "lo1", 1), _opt(hi1, "hi1", 1),
-                                _dev(e, "e"), _opt(c1, "c1"), n, elem_base, ctypes.byref(prm.c()), seed02, seed12,
-                                _stream(stream)), "bc_relu_helper")
+    if e_dup is None:
+        _check(lib().bc_relu_helper(_dev(lo0, "lo0", None), _opt(hi0, "hi0", None), _dev(lo1, "lo1", None),
+                                    _opt(hi1, "hi1", None), _dev(e, "e"), _opt(c1, "c1"), n, elem_base,
+                                    ctypes.byref(prm.c()), seed02, seed12, _stream(stream)), "bc_relu_helper")
+    else:
+        _check(lib().bc_relu_helper_to(_dev(lo0, "lo0", None), _opt(hi0, "hi0", None), _dev(lo1, "lo1", None),
+                                       _opt(hi1, "hi1", None), _dev(e, "e"), _dev(e_dup, "e_dup"), _opt(c1, "c1"), n,
+                                       elem_base, ctypes.byref(prm.c()), seed02, seed12, _stream(stream)),
+               "bc_relu_helper_to")
     return e, c1
 
 
@@ -367,6 +403,42 @@ def relu_finish(party, x, tbits, d_own, d_peer, e, c1, prm: Params, seed_tr: byt
                                 _dev(d_peer, "d_peer"), _dev(e, "e"), _opt(c1, "c1"), _dev(y, "y"), n, elem_base,
                                 ctypes.byref(prm.c()), seed_tr, _stream(stream)), "bc_relu_finish")
     return y
+
+
+# ---- peer memory (CUDA IPC) ----------------------------------------------------------
+
+def ipc_export(t: torch.Tensor) -> tuple[bytes, int]:
+    """(64-B handle of the allocation holding t, byte offset of t in it)."""
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_uint64()
+    _check(lib().bc_ipc_export(_dev(t, "t", None), h, ctypes.byref(off)), "bc_ipc_export")
+    return h.raw, off.value
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map a peer process's allocation; returns the base address in this process."""
+    base = ctypes.c_void_p()
+    _check(lib().bc_ipc_open(handle, ctypes.byref(base)), "bc_ipc_open")
+    return base.value
+
+
+def ipc_close(base: int) -> None:
+    _check(lib().bc_ipc_close(base), "bc_ipc_close")
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of raw device memory (a mapped peer buffer)."""
+
+    def __init__(self, ptr: int, shape, dtype: torch.dtype):
+        typestr = {torch.int64: "<i8", torch.int32: "<i4", torch.uint8: "|u1"}[dtype]
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def tensor_at(ptr: int, shape, dtype: torch.dtype) -> torch.Tensor:
+    """A tensor aliasing device memory at ptr (no copy, no ownership).  Its device is the
+    one that owns the memory (a peer GPU for a peer mapping); only its address is used."""
+    return torch.as_tensor(_CudaArray(ptr, shape, dtype))
 
 
 # ---- RSS variant (Alg 9) -------------------------------------------------------------

@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 OBJDIR = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libbicoptor.so")
-SOURCES = ["bc_host.cu", "bc_elem.cu", "bc_party.cu", "bc_fused.cu", "bc_rss.cu", "bc_trunc.cu", "bc_hostpipe.cu"]
+SOURCES = ["bc_host.cu", "bc_elem.cu", "bc_party.cu", "bc_fused.cu", "bc_rss.cu", "bc_trunc.cu", "bc_hostpipe.cu", "bc_ipc.cu"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC]

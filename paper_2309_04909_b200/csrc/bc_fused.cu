@@ -179,17 +179,14 @@ __global__ void __launch_bounds__(TPB, 2) k_fused_w(FusedArgs a, KP kp, Key k01,
 
 // Large tape (lx >= 8, up to 32 slots, p < 2^33): 9 seed01 blocks per element,
 // the 8 elements of a group in sequence, then the shared finish.
-constexpr int TPB_L = 128;
+constexpr int TPB_L = TPB_LARGE;
 
 template <int R, bool RELU, bool TRANSCRIPT>
 __global__ void __launch_bounds__(TPB_L) k_fused_l(FusedArgs a, KP kp, KPL kl, Key k01, Key k02, Key k12) {
   __shared__ uint8_t sidx[32 * TPB_L];
   __shared__ uint32_t sstg[32 * TPB_L];
   __shared__ uint32_t magic[33], hlim[33];
-  for (uint32_t s = threadIdx.x; s < 33; s += blockDim.x) {
-    magic[s] = s >= 2 ? 0xFFFFFFFFu / s + 1u : 0u;  // ceil(2^32 / s)
-    hlim[s] = s >= 2 ? (65536u / s) * s : 0u;
-  }
+  large_tables(magic, hlim);
   __syncthreads();
   uint8_t* idx = sidx + threadIdx.x;
   uint32_t* stg = sstg + threadIdx.x;

@@ -24,6 +24,14 @@ uint32_t factorial(uint32_t s) {
 namespace bc {
 namespace host {
 
+int cuda_rc(cudaError_t e) {
+  if (e != cudaSuccess) {
+    g_last_cuda = (int)e;
+    return BC_ECUDA;
+  }
+  return BC_OK;
+}
+
 int check_launch() {
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

@@ -87,17 +87,27 @@ __device__ __forceinline__ void slot_values(uint64_t s0f, uint64_t n1f, uint32_t
   d = (uint64_t)dv + kp.off1;                                          //                 P1: p + d - 2^w
 }
 
-// Alg 7 steps 1-9 for element j with shares x0, x1: returns DReLU' (bit 0)
-// and t (bit 1).  idx: this thread's column of a [32][TPB_L] byte table (the
-// permutation); stg: its column of a [32][TPB_L] word table (keystream staging,
-// so the Fisher-Yates and slot loops stay rolled: the kernel must fit the
-// instruction cache).  magic[s] = ceil(2^32 / s), hlim[s] = floor(2^16 / s) s.
-template <int R, bool TRANSCRIPT, int TPB_L>
-__device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_t j, const Key& k01, const KPL& kp,
-                                               uint8_t* idx, uint32_t* stg, const uint32_t* magic,
-                                               const uint32_t* hlim, uint64_t* w0, uint64_t* w1) {
+constexpr int TPB_LARGE = 128;  // threads per CTA of the large-tape kernels (shared tables are [32][TPB_LARGE])
+
+// Per-CTA constant tables of the Fisher-Yates draws: magic[s] = ceil(2^32 / s),
+// hlim[s] = floor(2^16 / s) s (the u16 rejection limit), s = 2..32.
+__device__ __forceinline__ void large_tables(uint32_t* magic, uint32_t* hlim) {
+  for (uint32_t s = threadIdx.x; s < 33; s += blockDim.x) {
+    magic[s] = s >= 2 ? 0xFFFFFFFFu / s + 1u : 0u;
+    hlim[s] = s >= 2 ? (65536u / s) * s : 0u;
+  }
+}
+
+// Block 0 of element j's tape: t and step 6's Fisher-Yates permutation into
+// this thread's idx column.  idx: this thread's column of a [32][TPB_L] byte
+// table; stg: its column of a [32][TPB_L] word table (keystream staging, so the
+// Fisher-Yates and slot loops stay rolled: the kernel must fit the instruction
+// cache).  magic[s] = ceil(2^32 / s), hlim[s] = floor(2^16 / s) s.  fbc counts
+// the fallback words consumed.  Returns t.
+template <int R, int TPB_L>
+__device__ __forceinline__ uint32_t large_perm(uint64_t j, const Key& k01, const KPL& kp, uint8_t* idx, uint32_t* stg,
+                                               const uint32_t* magic, const uint32_t* hlim, uint32_t& fbc) {
   const uint32_t S = kp.S;
-  uint32_t fbc = 0;  // fallback words consumed
   uint32_t t;
   {
     uint32_t B[16];
@@ -119,6 +129,44 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
     idx[m * TPB_L] = b;
     idx[k * TPB_L] = a;
   }
+  return t;
+}
+
+// Mask and reshare draws of slot m (blocks 1+b and 5+b staged in stg rows 0..31):
+// rM = Montgomery form of r_m, rho = rho_m.
+template <int R, int TPB_L>
+__device__ __forceinline__ void large_draws(uint32_t m, uint32_t b, uint64_t j, const Key& k01, const KPL& kp,
+                                            const uint32_t* stg, uint32_t& fbc, uint64_t& rM, uint64_t& rho) {
+  const uint32_t e = 2 * (m - 8 * b);
+  uint64_t ur = (uint64_t)stg[e * TPB_L] | ((uint64_t)stg[(e + 1) * TPB_L] << 32);
+  while (!accept64(ur, kp.qlim)) ur = fbl_word<R>(k01, j, fbc++);
+  uint64_t uq = (uint64_t)stg[(16 + e) * TPB_L] | ((uint64_t)stg[(17 + e) * TPB_L] << 32);
+  while (!accept64(uq, kp.plim)) uq = fbl_word<R>(k01, j, fbc++);
+  rM = 1ull + barrett(ur, kp.p - 1ull, kp.mu_q);  // r_m = rM 2^-64 (Montgomery form)
+  rho = barrett(uq, kp.p, kp.mu_p);               // rho_m in Z_p
+}
+
+template <int R, int TPB_L>
+__device__ __forceinline__ void large_stage(uint32_t b, uint64_t j, const Key& k01, uint32_t* stg) {
+  // mask block 1+b -> rows 0..15, reshare block 5+b -> rows 16..31
+#pragma unroll 1
+  for (uint32_t h = 0; h < 2; ++h) {
+    uint32_t B[16];
+    chacha<R>(k01, j * 9 + 1 + b + 4 * h, L_TAPEL, B);
+#pragma unroll
+    for (int w = 0; w < 16; ++w) stg[(16 * h + w) * TPB_L] = B[w];
+  }
+}
+
+// Alg 7 steps 1-9 for element j with shares x0, x1 (both computing parties and
+// P2's zero test): returns DReLU' (bit 0) and t (bit 1).
+template <int R, bool TRANSCRIPT, int TPB_L>
+__device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_t j, const Key& k01, const KPL& kp,
+                                               uint8_t* idx, uint32_t* stg, const uint32_t* magic,
+                                               const uint32_t* hlim, uint64_t* w0, uint64_t* w1) {
+  const uint32_t S = kp.S;
+  uint32_t fbc = 0;  // fallback words consumed
+  const uint32_t t = large_perm<R, TPB_L>(j, k01, kp, idx, stg, magic, hlim, fbc);
   // steps 1-2: blind both shares by (-1)^t
   const uint64_t s0 = t ? (0ull - x0) & kp.ymask : x0 & kp.ymask;
   const uint64_t s1 = t ? (0ull - x1) & kp.ymask : x1 & kp.ymask;
@@ -126,24 +174,12 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
   uint32_t z = 0;
 #pragma unroll 1
   for (uint32_t b = 0; 8 * b < S; ++b) {
-    // mask block 1+b -> rows 0..15, reshare block 5+b -> rows 16..31
-#pragma unroll 1
-    for (uint32_t h = 0; h < 2; ++h) {
-      uint32_t B[16];
-      chacha<R>(k01, j * 9 + 1 + b + 4 * h, L_TAPEL, B);
-#pragma unroll
-      for (int w = 0; w < 16; ++w) stg[(16 * h + w) * TPB_L] = B[w];
-    }
+    large_stage<R, TPB_L>(b, j, k01, stg);
     const uint32_t mend = min(S, 8 * b + 8);
 #pragma unroll 1
     for (uint32_t m = 8 * b; m < mend; ++m) {
-      const uint32_t e = 2 * (m - 8 * b);
-      uint64_t ur = (uint64_t)stg[e * TPB_L] | ((uint64_t)stg[(e + 1) * TPB_L] << 32);
-      while (!accept64(ur, kp.qlim)) ur = fbl_word<R>(k01, j, fbc++);
-      uint64_t uq = (uint64_t)stg[(16 + e) * TPB_L] | ((uint64_t)stg[(17 + e) * TPB_L] << 32);
-      while (!accept64(uq, kp.plim)) uq = fbl_word<R>(k01, j, fbc++);
-      const uint64_t rM = 1ull + barrett(ur, kp.p - 1ull, kp.mu_q);  // r_m = rM 2^-64 (Montgomery form)
-      const uint64_t rho = barrett(uq, kp.p, kp.mu_p);               // rho_m in Z_p
+      uint64_t rM, rho;
+      large_draws<R, TPB_L>(m, b, j, k01, kp, stg, fbc, rM, rho);
       uint64_t c, d;
       slot_values(s0f, n1f, idx[m * TPB_L], kp, c, d);                // v'_{Pi(m)} of each party
       uint64_t W0 = mont(c, rM, kp) + rho;                           // steps 7-8, P0: v'r + rho
@@ -159,6 +195,53 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
     }
   }
   return z | (t << 1);
+}
+
+// Alg 7 steps 1-8 for ONE computing party (the party-separated send phase):
+// the message W_m, m < S, as 32-bit low words lo[m] and bit m of the returned
+// high-bit word (bit 32 of W_m; p < 2^33).  Returns t in bit 32 of the result.
+template <int R, int PARTY, int TPB_L>
+__device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, const Key& k01, const KPL& kp,
+                                                     uint8_t* idx, uint32_t* stg, const uint32_t* magic,
+                                                     const uint32_t* hlim, uint32_t* lo) {
+  const uint32_t S = kp.S;
+  uint32_t fbc = 0;
+  const uint32_t t = large_perm<R, TPB_L>(j, k01, kp, idx, stg, magic, hlim, fbc);
+  const uint64_t s = t ? (0ull - x) & kp.ymask : x & kp.ymask;                  // steps 1-2
+  // P0 reads windows of s, P1 of (-s) mod 2^ell (Alg 5, readings C3, C4)
+  const uint64_t sf = (PARTY == 0 ? s : (0ull - s) & kp.ymask) >> kp.f;
+  uint32_t hib = 0;
+#pragma unroll 1
+  for (uint32_t b = 0; 8 * b < S; ++b) {
+    large_stage<R, TPB_L>(b, j, k01, stg);
+    const uint32_t mend = min(S, 8 * b + 8);
+#pragma unroll 1
+    for (uint32_t m = 8 * b; m < mend; ++m) {
+      uint64_t rM, rho;
+      large_draws<R, TPB_L>(m, b, j, k01, kp, stg, fbc, rM, rho);
+      uint64_t c, d;
+      slot_values(sf, sf, idx[m * TPB_L], kp, c, d);                  // one of the two is this party's
+      uint64_t W = PARTY == 0 ? mont(c, rM, kp) + rho : mont(d, rM, kp) + (kp.p - rho);  // steps 7-8
+      W = W >= kp.p ? W - kp.p : W;
+      lo[m] = (uint32_t)W;
+      hib |= (uint32_t)(W >> 32) << m;
+    }
+  }
+  return (uint64_t)hib | ((uint64_t)t << 32);
+}
+
+// Step 9 on the wire values of one element: any (W0_m + W1_m) mod p == 0.
+__device__ __forceinline__ uint32_t zero_test_large(const uint32_t* lo0, uint32_t hi0, const uint32_t* lo1,
+                                                    uint32_t hi1, const KPL& kp) {
+  uint32_t z = 0;
+#pragma unroll 1
+  for (uint32_t m = 0; m < kp.S; ++m) {
+    const uint64_t W0 = (uint64_t)__ldg(lo0 + m) | ((uint64_t)((hi0 >> m) & 1u) << 32);
+    const uint64_t W1 = (uint64_t)__ldg(lo1 + m) | ((uint64_t)((hi1 >> m) & 1u) << 32);
+    const uint64_t sum = W0 + W1;
+    z |= (sum == 0 || sum == kp.p) ? 1u : 0u;
+  }
+  return z;
 }
 
 }  // namespace bc

@@ -14,12 +14,28 @@ struct SendArgs {
   uint8_t* hi;
   uint8_t* tbits;
   uint64_t* dshare;
+  uint64_t* dpeer;  // nullable: second destination of [d]_b (the other computing party's inbox)
   uint64_t n, base;
 };
 
 __device__ __forceinline__ void store_msg(const SendArgs& a, const KP& kp, const Key& ktr, uint64_t g, uint64_t i0,
                                           uint64_t j0, uint32_t cnt, const uint64_t (&lo)[8], uint64_t hi,
                                           uint32_t tb, int party, bool relu);
+
+// Alg 8 step 4 (first half): [d]_b = [x]_b - [a]_b for the group's 8
+// elements, stored locally and (peer transport) into the other party's inbox.
+template <int R, int PARTY>
+__device__ __forceinline__ void send_dshare(const SendArgs& a, const KP& kp, const Key& ktr, uint64_t i0, uint64_t j0,
+                                            uint32_t cnt) {
+  uint32_t Ak[16];
+  chacha<R>(ktr, j0 >> 3, PARTY == 0 ? L_A02 : L_A12, Ak);
+  uint64_t x[8], d[8];
+  load8(a.x + i0, x, cnt);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) d[e] = (x[e] - u64_of(Ak, e)) & kp.ymask;
+  store8(a.dshare + i0, d, cnt);
+  if (a.dpeer) store8(a.dpeer + i0, d, cnt);  // the opening of d, stored straight into the peer
+}
 
 // Alg 7 steps 1-8 (and Alg 8's [d]_b) for one computing party, compact tape.
 template <int R, int PARTY, bool RELU>
@@ -57,15 +73,7 @@ __global__ void __launch_bounds__(TPB, 2) k_send_c(SendArgs a, KP kp, Key k01, K
       }
     }
     store_msg(a, kp, ktr, g, i0, j0, cnt, lo, hi, tb, PARTY, false);
-    if (RELU) {  // Alg 8 step 4: [d]_b = [x]_b - [a]_b
-      uint32_t Ak[16];
-      chacha<R>(ktr, j0 >> 3, PARTY == 0 ? L_A02 : L_A12, Ak);
-      uint64_t x[8], d[8];
-      load8(a.x + i0, x, cnt);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) d[e] = (x[e] - u64_of(Ak, e)) & kp.ymask;
-      store8(a.dshare + i0, d, cnt);
-    }
+    if (RELU) send_dshare<R, PARTY>(a, kp, ktr, i0, j0, cnt);
   }
 }
 
@@ -98,15 +106,41 @@ __global__ void __launch_bounds__(TPB, 2) k_send_w(SendArgs a, KP kp, Key k01, K
       tb |= tp.t << e;
     }
     store_msg(a, kp, ktr, g, i0, j0, cnt, lo, hi, tb, PARTY, false);
-    if (RELU) {
-      uint32_t Ak[16];
-      chacha<R>(ktr, j0 >> 3, PARTY == 0 ? L_A02 : L_A12, Ak);
-      uint64_t x[8], d[8];
-      load8(a.x + i0, x, cnt);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) d[e] = (x[e] - u64_of(Ak, e)) & kp.ymask;
-      store8(a.dshare + i0, d, cnt);
+    if (RELU) send_dshare<R, PARTY>(a, kp, ktr, i0, j0, cnt);
+  }
+}
+
+// Large tape (lx >= 8: up to 32 slots, p < 2^33).  Wire format: lo =
+// uint32_t[n][S] (low 32 bits of W_m), hi = uint32_t[n] (bit m = bit 32 of
+// W_m; NULL when p < 2^32): 33 S bits per element, 132 B at lx = 31 guard.
+template <int R, int PARTY, bool RELU>
+__global__ void __launch_bounds__(TPB_LARGE) k_send_l(SendArgs a, KP kp, KPL kl, Key k01, Key ktr) {
+  __shared__ uint8_t sidx[32 * TPB_LARGE];
+  __shared__ uint32_t sstg[32 * TPB_LARGE];
+  __shared__ uint32_t magic[33], hlim[33];
+  large_tables(magic, hlim);
+  __syncthreads();
+  uint8_t* idx = sidx + threadIdx.x;
+  uint32_t* stg = sstg + threadIdx.x;
+  uint32_t* lo = reinterpret_cast<uint32_t*>(a.lo);
+  uint32_t* hi = reinterpret_cast<uint32_t*>(a.hi);
+  const uint64_t ngroups = (a.n + 7) >> 3;
+  for (uint64_t g = (uint64_t)blockIdx.x * TPB_LARGE + threadIdx.x; g < ngroups;
+       g += (uint64_t)gridDim.x * TPB_LARGE) {
+    const uint64_t i0 = g << 3;
+    const uint64_t j0 = a.base + i0;
+    const uint32_t cnt = (uint32_t)min((uint64_t)8, a.n - i0);
+    uint32_t tb = 0;
+#pragma unroll 1
+    for (uint32_t e = 0; e < cnt; ++e) {
+      const uint64_t i = i0 + e;
+      const uint64_t r = elem_large_party<R, PARTY, TPB_LARGE>(__ldg(a.x + i), j0 + e, k01, kl, idx, stg, magic,
+                                                               hlim, lo + i * kl.S);
+      if (hi) hi[i] = (uint32_t)r;
+      tb |= (uint32_t)(r >> 32) << e;
     }
+    a.tbits[g] = (uint8_t)tb;
+    if (RELU) send_dshare<R, PARTY>(a, kp, ktr, i0, j0, cnt);
   }
 }
 
@@ -124,10 +158,54 @@ __device__ __forceinline__ void store_msg(const SendArgs& a, const KP& kp, const
 
 struct HelperArgs {
   const uint8_t *lo0, *hi0, *lo1, *hi1;
-  uint64_t* out0;  // DReLU: resp0 (nullable)   ReLU: e
-  uint64_t* out1;  // DReLU: resp1              ReLU: c1 (nullable)
+  uint64_t* out0;   // DReLU: resp0 (nullable)   ReLU: e
+  uint64_t* out0b;  // nullable: second destination of out0 (ReLU: e to P1 as well as P0)
+  uint64_t* out1;   // DReLU: resp1              ReLU: c1 (nullable)
   uint64_t n, base;
 };
+
+// P2's response for a group with zero-test bits zbits: Alg 7 step 10 ([D']_0
+// from seed02, [D']_1 = DReLU' - [D']_0), or Alg 8 steps 2-3 (e = DReLU' - b and
+// [c]_1 = ab - [c]_0 from the triple seeds).
+template <int R, bool RELU>
+__device__ __forceinline__ void helper_respond(const HelperArgs& a, const KP& kp, const Key& k02, const Key& k12,
+                                               uint64_t i0, uint64_t j0, uint32_t cnt, uint32_t zbits) {
+  uint64_t o0[8], o1[8];
+  if (!RELU) {
+    uint32_t Q[16];
+    chacha<R>(k02, j0 >> 3, L_RESP, Q);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint64_t q = u64_of(Q, e) & kp.ymask;
+      o0[e] = q;
+      o1[e] = (((zbits >> e) & 1u) - q) & kp.ymask;
+    }
+  } else {
+    uint32_t Bk0[16], Bk1[16];
+    chacha<R>(k02, j0 >> 3, L_B02, Bk0);
+    chacha<R>(k12, j0 >> 3, L_B12, Bk1);
+    uint64_t bsum[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      bsum[e] = u64_of(Bk0, e) + u64_of(Bk1, e);
+      o0[e] = (((zbits >> e) & 1u) - bsum[e]) & kp.ymask;  // e = DReLU' - b
+    }
+    if (a.out1) {  // [c]_1 = ([a]_0 + [a]_1)([b]_0 + [b]_1) - [c]_0
+      uint32_t Ak0[16], Ak1[16];
+      chacha<R>(k02, j0 >> 3, L_A02, Ak0);
+      chacha<R>(k12, j0 >> 3, L_A12, Ak1);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o1[e] = (u64_of(Ak0, e) + u64_of(Ak1, e)) * bsum[e];
+      uint32_t Ck[16];
+      chacha<R>(k02, j0 >> 3, L_C02, Ck);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o1[e] = (o1[e] - u64_of(Ck, e)) & kp.ymask;
+    }
+  }
+  if (a.out0) store8(a.out0 + i0, o0, cnt);
+  if (a.out0b) store8(a.out0b + i0, o0, cnt);
+  if (a.out1) store8(a.out1 + i0, o1, cnt);
+}
 
 // P2: Alg 7 steps 9-10, or Alg 8 steps 2-3 with the triple's [c]_1.
 template <int R, bool RELU>
@@ -149,40 +227,30 @@ __global__ void __launch_bounds__(TPB, 2) k_helper(HelperArgs a, KP kp, Key k02,
       unpack_W(l1[e], (uint32_t)(h1 >> (8 * e)) & 0xFFu, W1);
       zbits |= zero_test(W0, W1, kp.p, kp.S) << e;
     }
-    uint64_t o0[8], o1[8];
-    if (!RELU) {  // step 10: [D']_0 from seed02, [D']_1 = D' - [D']_0
-      uint32_t Q[16];
-      chacha<R>(k02, j0 >> 3, L_RESP, Q);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const uint64_t q = u64_of(Q, e) & kp.ymask;
-        o0[e] = q;
-        o1[e] = (((zbits >> e) & 1u) - q) & kp.ymask;
-      }
-    } else {
-      uint32_t Bk0[16], Bk1[16];
-      chacha<R>(k02, j0 >> 3, L_B02, Bk0);
-      chacha<R>(k12, j0 >> 3, L_B12, Bk1);
-      uint64_t bsum[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        bsum[e] = u64_of(Bk0, e) + u64_of(Bk1, e);
-        o0[e] = (((zbits >> e) & 1u) - bsum[e]) & kp.ymask;  // e = DReLU' - b
-      }
-      if (a.out1) {  // [c]_1 = ([a]_0 + [a]_1)([b]_0 + [b]_1) - [c]_0
-        uint32_t Ak0[16], Ak1[16];
-        chacha<R>(k02, j0 >> 3, L_A02, Ak0);
-        chacha<R>(k12, j0 >> 3, L_A12, Ak1);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o1[e] = (u64_of(Ak0, e) + u64_of(Ak1, e)) * bsum[e];
-        uint32_t Ck[16];
-        chacha<R>(k02, j0 >> 3, L_C02, Ck);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o1[e] = (o1[e] - u64_of(Ck, e)) & kp.ymask;
-      }
+    helper_respond<R, RELU>(a, kp, k02, k12, i0, j0, cnt, zbits);
+  }
+}
+
+// P2 on the large-tape wire format (see k_send_l).
+template <int R, bool RELU>
+__global__ void __launch_bounds__(TPB, 2) k_helper_l(HelperArgs a, KP kp, KPL kl, Key k02, Key k12) {
+  const uint32_t* lo0 = reinterpret_cast<const uint32_t*>(a.lo0);
+  const uint32_t* lo1 = reinterpret_cast<const uint32_t*>(a.lo1);
+  const uint32_t* hi0 = reinterpret_cast<const uint32_t*>(a.hi0);
+  const uint32_t* hi1 = reinterpret_cast<const uint32_t*>(a.hi1);
+  const uint64_t ngroups = (a.n + 7) >> 3;
+  for (uint64_t g = (uint64_t)blockIdx.x * TPB + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB) {
+    const uint64_t i0 = g << 3;
+    const uint64_t j0 = a.base + i0;
+    const uint32_t cnt = (uint32_t)min((uint64_t)8, a.n - i0);
+    uint32_t zbits = 0;
+#pragma unroll 1
+    for (uint32_t e = 0; e < cnt; ++e) {  // step 9
+      const uint64_t i = i0 + e;
+      zbits |= zero_test_large(lo0 + i * kl.S, hi0 ? __ldg(hi0 + i) : 0u, lo1 + i * kl.S, hi1 ? __ldg(hi1 + i) : 0u,
+                               kl) << e;
     }
-    if (a.out0) store8(a.out0 + i0, o0, cnt);
-    if (a.out1) store8(a.out1 + i0, o1, cnt);
+    helper_respond<R, RELU>(a, kp, k02, k12, i0, j0, cnt, zbits);
   }
 }
 
@@ -262,21 +330,26 @@ __global__ void __launch_bounds__(TPB, 2) k_finish(FinishArgs a, KP kp, Key ks) 
 }
 
 template <bool RELU>
-int send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits, uint64_t* dshare, size_t n,
-         uint64_t base, const bc_params* prm, const uint8_t* s01, const uint8_t* str, void* stream) {
+int send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits, uint64_t* dshare, uint64_t* dpeer,
+         size_t n, uint64_t base, const bc_params* prm, const uint8_t* s01, const uint8_t* str, void* stream) {
   const int rc = check_params(prm);
   if (rc) return rc;
   if (n == 0) return BC_OK;  // no-op after parameter validation
   if ((party != 0 && party != 1) || !x || !lo || !tbits || !s01 || (RELU && (!dshare || !str))) return BC_EINVAL;
-  if (prm->tape == BC_TAPE_LARGE) return BC_EINVAL;  // byte-plane wire format: slots <= 8, p <= 257
-  if (!hi && prm->p > 256) return BC_EINVAL;
-  if (!aligned16(x) || !aligned16(lo) || (hi && !aligned8(hi)) || (RELU && !aligned16(dshare)) || (base & 7))
+  const bool large = prm->tape == BC_TAPE_LARGE;
+  if (!hi && prm->p > (large ? 0xFFFFFFFFull : 256ull)) return BC_EINVAL;  // the high-bit plane is needed
+  if (!RELU && dpeer) return BC_EINVAL;
+  if (!aligned16(x) || !aligned16(lo) || (hi && !aligned8(hi)) || (RELU && !aligned16(dshare)) ||
+      (dpeer && !aligned16(dpeer)) || (base & 7))
     return BC_EALIGN;
   const size_t nb = n * 8;
-  if (overlap(lo, nb, x, nb) || overlap(hi, n, x, nb) || overlap(tbits, (n + 7) / 8, x, nb) ||
-      (RELU && overlap(dshare, nb, x, nb)))
+  const size_t nlo = large ? n * prm->slots * 4 : nb, nhi = large ? n * 4 : n;  // wire planes (bytes)
+  if (overlap(lo, nlo, x, nb) || overlap(hi, nhi, x, nb) || overlap(tbits, (n + 7) / 8, x, nb) ||
+      overlap(lo, nlo, hi, nhi) || overlap(lo, nlo, tbits, (n + 7) / 8) || overlap(hi, nhi, tbits, (n + 7) / 8) ||
+      (RELU && (overlap(dshare, nb, x, nb) || overlap(dshare, nb, lo, nlo) || overlap(dshare, nb, hi, nhi))) ||
+      overlap(dpeer, nb, x, nb) || overlap(dpeer, nb, dshare, nb))
     return BC_EALIAS;
-  SendArgs a{x, lo, hi, tbits, dshare, (uint64_t)n, base};
+  SendArgs a{x, lo, hi, tbits, dshare, dpeer, (uint64_t)n, base};
   const KP kp = make_kp(prm);
   const Key k01 = make_key(s01);
   const Key ktr = RELU ? make_key(str) : Key{};
@@ -285,7 +358,11 @@ int send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits,
   return dispatch_rounds(prm->rounds, [&](auto Rc) {
     constexpr int R = decltype(Rc)::value;
     auto go = [&](auto fn) { fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k01, ktr); };
-    if (prm->tape == BC_TAPE_COMPACT) {
+    if (large) {
+      const KPL kl = make_kpl(prm);
+      auto fn = party == 0 ? k_send_l<R, 0, RELU> : k_send_l<R, 1, RELU>;
+      fn<<<grid_for((const void*)fn, ngroups, TPB_LARGE), TPB_LARGE, 0, st>>>(a, kp, kl, k01, ktr);
+    } else if (prm->tape == BC_TAPE_COMPACT) {
       if (party == 0) go(k_send_c<R, 0, RELU>);
       else go(k_send_c<R, 1, RELU>);
     } else {
@@ -298,23 +375,27 @@ int send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits,
 
 template <bool RELU>
 int helper(const uint8_t* lo0, const uint8_t* hi0, const uint8_t* lo1, const uint8_t* hi1, uint64_t* out0,
-           uint64_t* out1, size_t n, uint64_t base, const bc_params* prm, const uint8_t* s02, const uint8_t* s12,
+           uint64_t* out0b, uint64_t* out1, size_t n, uint64_t base, const bc_params* prm, const uint8_t* s02, const uint8_t* s12,
            void* stream) {
   const int rc = check_params(prm);
   if (rc) return rc;
   if (n == 0) return BC_OK;  // no-op after parameter validation
   if (!lo0 || !lo1 || !s02 || (RELU && (!s12 || !out0)) || (!RELU && !out1)) return BC_EINVAL;
-  if (prm->tape == BC_TAPE_LARGE) return BC_EINVAL;  // byte-plane wire format: slots <= 8, p <= 257
-  if (prm->p > 256 && (!hi0 || !hi1)) return BC_EINVAL;
+  const bool large = prm->tape == BC_TAPE_LARGE;
+  if (prm->p > (large ? 0xFFFFFFFFull : 256ull) && (!hi0 || !hi1)) return BC_EINVAL;
   if (!aligned16(lo0) || !aligned16(lo1) || (hi0 && !aligned8(hi0)) || (hi1 && !aligned8(hi1)) ||
-      (out0 && !aligned16(out0)) || (out1 && !aligned16(out1)) || (base & 7))
+      (out0 && !aligned16(out0)) || (out0b && !aligned16(out0b)) || (out1 && !aligned16(out1)) || (base & 7))
     return BC_EALIGN;
+  if (out0b && !out0) return BC_EINVAL;
   const size_t nb = n * 8;
-  if (overlap(out0, nb, lo0, nb) || overlap(out0, nb, lo1, nb) || overlap(out1, nb, lo0, nb) ||
-      overlap(out1, nb, lo1, nb) || overlap(out0, nb, out1, nb) || overlap(out0, nb, hi0, n) ||
-      overlap(out0, nb, hi1, n) || overlap(out1, nb, hi0, n) || overlap(out1, nb, hi1, n))
+  const size_t nlo = large ? n * prm->slots * 4 : nb, nhi = large ? n * 4 : n;  // wire planes (bytes)
+  if (overlap(out0, nb, lo0, nlo) || overlap(out0, nb, lo1, nlo) || overlap(out1, nb, lo0, nlo) ||
+      overlap(out1, nb, lo1, nlo) || overlap(out0, nb, out1, nb) || overlap(out0, nb, hi0, nhi) ||
+      overlap(out0, nb, hi1, nhi) || overlap(out1, nb, hi0, nhi) || overlap(out1, nb, hi1, nhi) ||
+      overlap(out0b, nb, out0, nb) || overlap(out0b, nb, out1, nb) || overlap(out0b, nb, lo0, nlo) ||
+      overlap(out0b, nb, lo1, nlo) || overlap(out0b, nb, hi0, nhi) || overlap(out0b, nb, hi1, nhi))
     return BC_EALIAS;
-  HelperArgs a{lo0, hi0, lo1, hi1, out0, out1, (uint64_t)n, base};
+  HelperArgs a{lo0, hi0, lo1, hi1, out0, out0b, out1, (uint64_t)n, base};
   const KP kp = make_kp(prm);
   const Key k02 = make_key(s02);
   const Key k12 = RELU ? make_key(s12) : Key{};
@@ -322,8 +403,13 @@ int helper(const uint8_t* lo0, const uint8_t* hi0, const uint8_t* lo1, const uin
   const uint64_t ngroups = (n + 7) / 8;
   return dispatch_rounds(prm->rounds, [&](auto Rc) {
     constexpr int R = decltype(Rc)::value;
-    auto fn = k_helper<R, RELU>;
-    fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k02, k12);
+    if (large) {
+      auto fn = k_helper_l<R, RELU>;
+      fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, make_kpl(prm), k02, k12);
+    } else {
+      auto fn = k_helper<R, RELU>;
+      fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k02, k12);
+    }
     return check_launch();
   });
 }
@@ -365,13 +451,13 @@ extern "C" {
 
 int bc_drelu_send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits, size_t n,
                   uint64_t elem_base, const bc_params* prm, const uint8_t seed01[32], void* stream) {
-  return send<false>(party, x, lo, hi, tbits, nullptr, n, elem_base, prm, seed01, nullptr, stream);
+  return send<false>(party, x, lo, hi, tbits, nullptr, nullptr, n, elem_base, prm, seed01, nullptr, stream);
 }
 
 int bc_drelu_helper(const uint8_t* lo0, const uint8_t* hi0, const uint8_t* lo1, const uint8_t* hi1, uint64_t* resp0,
                     uint64_t* resp1, size_t n, uint64_t elem_base, const bc_params* prm, const uint8_t seed02[32],
                     void* stream) {
-  return helper<false>(lo0, hi0, lo1, hi1, resp0, resp1, n, elem_base, prm, seed02, nullptr, stream);
+  return helper<false>(lo0, hi0, lo1, hi1, resp0, nullptr, resp1, n, elem_base, prm, seed02, nullptr, stream);
 }
 
 int bc_drelu_finish(int party, const uint8_t* tbits, const uint64_t* resp, uint64_t* y, size_t n, uint64_t elem_base,
@@ -382,13 +468,25 @@ int bc_drelu_finish(int party, const uint8_t* tbits, const uint64_t* resp, uint6
 int bc_relu_send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits, uint64_t* dshare, size_t n,
                  uint64_t elem_base, const bc_params* prm, const uint8_t seed01[32], const uint8_t seed_tr[32],
                  void* stream) {
-  return send<true>(party, x, lo, hi, tbits, dshare, n, elem_base, prm, seed01, seed_tr, stream);
+  return send<true>(party, x, lo, hi, tbits, dshare, nullptr, n, elem_base, prm, seed01, seed_tr, stream);
+}
+
+int bc_relu_send_to(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits, uint64_t* dshare,
+                    uint64_t* dshare_peer, size_t n, uint64_t elem_base, const bc_params* prm,
+                    const uint8_t seed01[32], const uint8_t seed_tr[32], void* stream) {
+  return send<true>(party, x, lo, hi, tbits, dshare, dshare_peer, n, elem_base, prm, seed01, seed_tr, stream);
 }
 
 int bc_relu_helper(const uint8_t* lo0, const uint8_t* hi0, const uint8_t* lo1, const uint8_t* hi1, uint64_t* e,
                    uint64_t* c1, size_t n, uint64_t elem_base, const bc_params* prm, const uint8_t seed02[32],
                    const uint8_t seed12[32], void* stream) {
-  return helper<true>(lo0, hi0, lo1, hi1, e, c1, n, elem_base, prm, seed02, seed12, stream);
+  return helper<true>(lo0, hi0, lo1, hi1, e, nullptr, c1, n, elem_base, prm, seed02, seed12, stream);
+}
+
+int bc_relu_helper_to(const uint8_t* lo0, const uint8_t* hi0, const uint8_t* lo1, const uint8_t* hi1, uint64_t* e0,
+                      uint64_t* e1, uint64_t* c1, size_t n, uint64_t elem_base, const bc_params* prm,
+                      const uint8_t seed02[32], const uint8_t seed12[32], void* stream) {
+  return helper<true>(lo0, hi0, lo1, hi1, e0, e1, c1, n, elem_base, prm, seed02, seed12, stream);
 }
 
 int bc_relu_finish(int party, const uint64_t* x, const uint8_t* tbits, const uint64_t* d_own, const uint64_t* d_peer,

@@ -129,13 +129,22 @@ class PartyRunner:
         self.group = group
         self.paper_literal = paper_literal
         self.base = self.role.triple * n if base is None else base
-        self.hi_needed = prm.c().p > 256
+        self.fmt = api.wire_format(prm)  # byte planes (p <= 257) or uint32 planes (large tape)
+        self.hi_needed = self.fmt["hi"] is not None
         # seeds this party holds: P0 {01, 02}, P1 {01, 12}, P2 {02, 12}
         held = {0: ("s01", "s02"), 1: ("s01", "s12"), 2: ("s02", "s12")}[self.role.party]
         self.seed = {k: getattr(seeds, k) for k in held}
         self.bytes_sent = 0
 
     # -- messaging helpers ---------------------------------------------------------
+    def _msg_bufs(self, m):
+        """P2's receive buffers for one chunk: lo0, hi0, lo1, hi1 (hi None if unused)."""
+        (los, lot), hf = self.fmt["lo"], self.fmt["hi"]
+        lo0, lo1 = self.c.empty((m,) + los, lot), self.c.empty((m,) + los, lot)
+        hi0 = self.c.empty(m, hf[1]) if hf else None
+        hi1 = self.c.empty(m, hf[1]) if hf else None
+        return lo0, hi0, lo1, hi1
+
     # Each protocol round of a chunk is posted as one batch_isend_irecv group
     # (one NCCL group call on GPUs), so the order in which the three parties
     # post their sends and receives cannot deadlock.
@@ -173,9 +182,7 @@ class PartyRunner:
                     works += self._post([self._recv(resp, 2)])                           # round 2
                 pending.append(((a, b), (tb, resp), works))
             else:
-                lo0, lo1 = c.empty((m, 8), torch.uint8), c.empty((m, 8), torch.uint8)
-                hi0 = c.empty(m, torch.uint8) if self.hi_needed else None
-                hi1 = c.empty(m, torch.uint8) if self.hi_needed else None
+                lo0, hi0, lo1, hi1 = self._msg_bufs(m)
                 ops = [self._recv(lo0, 0), self._recv(lo1, 1)]
                 if self.hi_needed:
                     ops += [self._recv(hi0, 0), self._recv(hi1, 1)]
@@ -219,9 +226,7 @@ class PartyRunner:
                 works += self._post([self._recv(e, 2)] + ([self._recv(c1, 2)] if p == 1 else []))
                 pending.append(((a, b), (x[a:b], tb, d_own, d_peer, e, c1, seed_tr), works))
             else:
-                lo0, lo1 = c.empty((m, 8), torch.uint8), c.empty((m, 8), torch.uint8)
-                hi0 = c.empty(m, torch.uint8) if self.hi_needed else None
-                hi1 = c.empty(m, torch.uint8) if self.hi_needed else None
+                lo0, hi0, lo1, hi1 = self._msg_bufs(m)
                 ops = [self._recv(lo0, 0), self._recv(lo1, 1)]
                 if self.hi_needed:
                     ops += [self._recv(hi0, 0), self._recv(hi1, 1)]

@@ -37,10 +37,22 @@ def _unpack_bits(b, n):
 
 
 def _decode_msg(lo, hi, S):
-    W = lo[:, :S].astype(np.uint64)
+    """Inverse of B.encode_msg (byte planes) / B.encode_msg_large (uint32 planes)."""
+    lo = np.asarray(lo)
+    bit = np.uint64(8 if lo.dtype.itemsize == 1 else 32)
+    W = lo[:, :S].view(np.uint8 if bit == 8 else np.uint32).astype(np.uint64)
     if hi is not None:
-        W |= ((hi[:, None].astype(np.uint64) >> np.arange(S, dtype=np.uint64)) & np.uint64(1)) << np.uint64(8)
+        h = np.asarray(hi).view(np.uint8 if bit == 8 else np.uint32).astype(np.uint64)
+        W |= ((h[:, None] >> np.arange(S, dtype=np.uint64)) & np.uint64(1)) << bit
     return W
+
+
+def _encode(o, W):
+    if o.layout == "large":
+        lo, hi = B.encode_msg_large(W)
+        return torch.from_numpy(lo.view(np.int32)), torch.from_numpy(hi.view(np.int32))
+    lo, hi = B.encode_msg(W)
+    return torch.from_numpy(lo), torch.from_numpy(hi)
 
 
 class OracleCompute:
@@ -53,8 +65,8 @@ class OracleCompute:
     def drelu_send(self, party, x, prm, seed01, base):
         o = _prm(prm)
         m = B.drelu_send(o, party, _np(x), _j(base, x.numel()), seed01)
-        lo, hi = B.encode_msg(m["W"])
-        return torch.from_numpy(lo), torch.from_numpy(hi), torch.from_numpy(_pack_bits(m["t"]))
+        lo, hi = _encode(o, m["W"])
+        return lo, hi, torch.from_numpy(_pack_bits(m["t"]))
 
     def drelu_helper(self, lo0, hi0, lo1, hi1, prm, seed02, base, paper_literal=False):
         o = _prm(prm)
@@ -78,8 +90,8 @@ class OracleCompute:
     def relu_send(self, party, x, prm, seed01, seed_tr, base):
         o = _prm(prm)
         m = B.relu_send(o, party, _np(x), _j(base, x.numel()), seed01, seed_tr)
-        lo, hi = B.encode_msg(m["W"])
-        return torch.from_numpy(lo), torch.from_numpy(hi), torch.from_numpy(_pack_bits(m["t"])), _t64(m["d"])
+        lo, hi = _encode(o, m["W"])
+        return lo, hi, torch.from_numpy(_pack_bits(m["t"])), _t64(m["d"])
 
     def relu_helper(self, lo0, hi0, lo1, hi1, prm, seed02, seed12, base):
         o = _prm(prm)

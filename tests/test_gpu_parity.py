@@ -232,10 +232,28 @@ def test_config2_ladder_full_size_sampled(api):
 
 # ---- party-separated phases on one device ------------------------------------------
 
-@pytest.mark.parametrize("kw", [PARAMS[0], PARAMS[4], PARAMS[5]], ids=_ids)
+def _wire(oprm, W):
+    """The oracle's message in the kernels' wire format (byte or uint32 planes)."""
+    if oprm.layout == "large":
+        return B.encode_msg_large(W)
+    return B.encode_msg(W)
+
+
+def _np_plane(t):
+    a = t.cpu().numpy()
+    return a.view(np.uint32) if a.dtype == np.int32 else a
+
+
+PARTY_PARAMS = [PARAMS[0], PARAMS[4], PARAMS[5],
+                dict(ell=64, lx=31, f=0, mode="guard", rounds=20),     # full precision: uint32 + bit-32 planes
+                dict(ell=64, lx=31, f=0, mode="literal", rounds=8),    # p = 2^31 + 11: no bit-32 plane
+                dict(ell=24, lx=10, f=0, mode="guard", rounds=8)]
+
+
+@pytest.mark.parametrize("kw", PARTY_PARAMS, ids=_ids)
 def test_party_phases_match_oracle_and_fused(api, kw):
     oprm, prm = B.Params(**kw), api.Params(**kw)
-    n, base = 4099, 1 << 20
+    n, base = (4099 if oprm.layout != "large" else 523), 1 << 20
     x, x0, x1 = synth.shares(n, kw["ell"], kw["lx"], kw["f"], "D1")
     j = np.arange(n, dtype=np.uint64) + np.uint64(base)
     t0, t1 = dev(x0), dev(x1)
@@ -243,8 +261,14 @@ def test_party_phases_match_oracle_and_fused(api, kw):
     lo0, hi0, tb0 = api.drelu_send(0, t0, prm, SEEDS.s01, base)
     lo1, hi1, tb1 = api.drelu_send(1, t1, prm, SEEDS.s01, base)
     m0 = B.drelu_send(oprm, 0, x0, j, SEEDS.s01)
-    el0, eh0 = B.encode_msg(m0["W"])
-    assert np.array_equal(lo0.cpu().numpy(), el0) and np.array_equal(hi0.cpu().numpy(), eh0)
+    m1 = B.drelu_send(oprm, 1, x1, j, SEEDS.s01)
+    for lo, hi, m in ((lo0, hi0, m0), (lo1, hi1, m1)):
+        el, eh = _wire(oprm, m["W"])
+        assert np.array_equal(_np_plane(lo), el)
+        if api.wire_format(prm)["hi"] is not None:
+            assert np.array_equal(_np_plane(hi), eh)
+        else:
+            assert not eh.any()
     r0, r1 = api.drelu_helper(lo0, hi0, lo1, hi1, prm, SEEDS.s02, base, paper_literal=True)
     ya = api.drelu_finish(0, tb0, None, prm, n, SEEDS.s02, base)
     yb = api.drelu_finish(0, tb0, r0, prm, n, None, base)
@@ -257,6 +281,11 @@ def test_party_phases_match_oracle_and_fused(api, kw):
     e, c1 = api.relu_helper(L0, H0, L1, H1, prm, SEEDS.s02, SEEDS.s12, base)
     ref = B.relu(oprm, x0, x1, j, SEEDS)
     assert np.array_equal(host(d0), ref["d0"]) and np.array_equal(host(e), ref["e"]) and np.array_equal(host(c1), ref["c1"])
+    # the peer-transport entry points store d and e a second time, bit for bit
+    dp, ed = torch.empty_like(d0), torch.empty_like(e)
+    api.relu_send(0, t0, prm, SEEDS.s01, SEEDS.s02, base, d_peer=dp)
+    api.relu_helper(L0, H0, L1, H1, prm, SEEDS.s02, SEEDS.s12, base, e_dup=ed)
+    assert torch.equal(dp, d0) and torch.equal(ed, e)
     z0 = api.relu_finish(0, t0, T0, d0, d1, e, None, prm, SEEDS.s02, base)
     z1 = api.relu_finish(1, t1, T1, d1, d0, e, c1, prm, SEEDS.s12, base)
     g0, g1 = api.relu(t0, t1, prm, SEEDS, elem_base=base)
@@ -457,8 +486,12 @@ def test_large_abi_errors(api):
     v = torch.zeros((16, 8), dtype=torch.uint8, device=DEV)
     # byte-plane formats hold at most 8 slots
     assert L.bc_ladder_modswitch(0, t.data_ptr(), v.data_ptr(), 16, ctypes.byref(cp), None) == -1
-    assert L.bc_drelu_send(0, t.data_ptr(), v.data_ptr(), v.data_ptr(), v.data_ptr(), 16, 0, ctypes.byref(cp),
+    # large-tape wire format: uint32 planes; at p = 2^32 + 15 the bit-32 plane is required
+    lo32 = torch.zeros((16, 32), dtype=torch.int32, device=DEV)
+    assert L.bc_drelu_send(0, t.data_ptr(), lo32.data_ptr(), None, v.data_ptr(), 16, 0, ctypes.byref(cp),
                            SEEDS.s01, None) == -1
+    assert L.bc_drelu_helper(lo32.data_ptr(), None, lo32.data_ptr(), None, None, t.data_ptr(), 16, 0,
+                             ctypes.byref(cp), SEEDS.s02, None) == -1
     # large transcript: u64 planes, hi planes must be NULL
     w = [torch.zeros((16, 32), dtype=torch.int64, device=DEV) for _ in range(2)]
     ys = [torch.zeros(16, dtype=torch.int64, device=DEV) for _ in range(3)]

@@ -14,6 +14,14 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+# "guard": compact tape, byte wire planes; "literal": p = 131 (no high-bit plane);
+# "large": lx = 10 large tape, uint32 low-word plane only (p = 2053); "large_full": the paper's
+# full precision lx = 31 (p = 2^32 + 15: low words and the bit-32 plane); "large_literal": p = 2^31 + 11
+CONFIGS = {"guard": dict(ell=64, lx=7, f=24, mode="guard", rounds=8),
+           "literal": dict(ell=16, lx=7, f=0, mode="literal", rounds=8),
+           "large": dict(ell=24, lx=10, f=0, mode="guard", rounds=8),
+           "large_full": dict(ell=64, lx=31, f=0, mode="guard", rounds=8),
+           "large_literal": dict(ell=64, lx=31, f=0, mode="literal", rounds=8)}
 
 
 def _free_port():
@@ -37,9 +45,10 @@ def _worker(rank, world, port, kind, n, chunk, mode, literal, outdir):
         def c(self):
             from oracle import bicoptor as B
             o = B.Params(ell=self.ell, lx=self.lx, f=self.f, mode=self.mode, rounds=self.rounds)
-            return type("C", (), {"p": o.p})()
+            return type("C", (), {"p": o.p, "slots": o.slots,
+                                  "tape": {"wide": 0, "compact": 1, "large": 2}[o.layout]})()
 
-    prm = P(ell=64, lx=7, f=24, mode=mode, rounds=8) if mode == "guard" else P(ell=16, lx=7, f=0, mode=mode, rounds=8)
+    prm = P(**CONFIGS[mode])
     role = party.Role.of(rank)
     x, x0, x1 = synth.shares(n, prm.ell, prm.lx, prm.f, "D1", run=role.triple)
     xs = torch.from_numpy((x0 if role.party == 0 else x1).view(np.int64))
@@ -54,15 +63,17 @@ def _worker(rank, world, port, kind, n, chunk, mode, literal, outdir):
 
 @pytest.mark.parametrize("kind,world,mode,literal", [("drelu", 3, "guard", False), ("drelu", 3, "guard", True),
                                                       ("relu", 3, "guard", False), ("relu", 6, "guard", False),
-                                                      ("drelu", 3, "literal", False)])
+                                                      ("drelu", 3, "literal", False), ("relu", 3, "large", False),
+                                                      ("drelu", 3, "large_full", True),
+                                                      ("drelu", 3, "large_literal", False)])
 def test_party_runtime_gloo(tmp_path, kind, world, mode, literal):
     import synth
     from oracle import bicoptor as B
     n, chunk = 300, 128  # 3 chunks, the last one ragged
     mp.start_processes(_worker, args=(world, _free_port(), kind, n, chunk, mode, literal, str(tmp_path)),
                        nprocs=world, join=True, start_method="spawn")
-    ell, lx, f = (64, 7, 24) if mode == "guard" else (16, 7, 0)
-    o = B.Params(ell=ell, lx=lx, f=f, mode=mode, rounds=8)
+    o = B.Params(**CONFIGS[mode])
+    ell, lx, f = o.ell, o.lx, o.f
     for t in range(world // 3):
         x, x0, x1 = synth.shares(n, ell, lx, f, "D1", run=t)
         j = np.arange(n, dtype=np.uint64) + np.uint64(t * n)
@@ -71,6 +82,7 @@ def test_party_runtime_gloo(tmp_path, kind, world, mode, literal):
         assert np.array_equal(np.load(tmp_path / f"y_{3 * t + 1}.npy"), ref["y1"])
     # wire bytes per element: P0 -> P2 (ell_x+1) * ceil(log2 p) bits (Table 1)
     b0 = int(np.load(tmp_path / "bytes_0.npy")[0])
-    per = 9 if mode == "guard" else 8
+    # wire bytes per element: byte planes 8 + 1 (guard) / 8 (literal); uint32 planes 4 S (+ 4 with the bit-32 plane)
+    per = {"guard": 9, "literal": 8, "large": 11 * 4, "large_full": 32 * 4 + 4, "large_literal": 32 * 4}[mode]
     extra = (0 if kind == "drelu" else 8)  # ReLU: P0 also sends [d]_0 to P1
     assert b0 == n * (per + extra)
