@@ -413,7 +413,7 @@ def run_cuda(a):
         line["config5"] = relu_streams(api, prm, seeds, dev, stream, timed, world)
         # ---- e2e through the public API with pinned HOST buffers ----------------
         line["e2e"] = e2e(api, prm, seeds, x0h, x1h, base, dev, world, max_over_ranks, barrier, a)
-    if rank == 0 and not a.no_extras:
+    if rank == 0 and world == 1 and not a.no_extras:  # the CPU baseline: rank 0 at N=1 only
         rate, cores, sample = oracle_rate("drelu", a.rounds)
         line["cpu_baseline"] = {"value": rate, "unit": "elements/s", "cores": cores, "kind": "oracle", "sample": sample}
     if rank == 0:

@@ -21,10 +21,14 @@ struct FusedArgs {
 };
 
 // ---- shared finish: Alg 7 steps 10-11, or Alg 8 (triple, e, d, Beaver combine) ----
-template <int R, bool RELU>
+// FULL (ell = 64): every value is already reduced mod 2^ell, the masks fold away.
+// The sign (1 - 2t) is applied as a 64-bit multiply (FMA pipe) rather than as
+// negate-and-select (ALU pipe, which the ChaCha rounds saturate).
+template <int R, bool RELU, bool FULL>
 __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, const Key& k02, const Key& k12,
                                              uint64_t i0, uint64_t j0, uint32_t cnt, uint32_t zbits,
                                              uint32_t tbits) {
+  const uint64_t ym = FULL ? ~0ull : kp.ymask;
   uint64_t y0[8], y1[8];
   if (!RELU) {
     // Alg 7 step 10: P2 reshares DReLU' ([D']_0 from seed02); step 11: P0/P1 unblind.
@@ -33,10 +37,10 @@ __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, c
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const uint64_t z = (zbits >> e) & 1u, t = (tbits >> e) & 1u;
-      const uint64_t q = u64_of(Q, e) & kp.ymask;  // [D']_0
-      const uint64_t d1 = (z - q) & kp.ymask;      // [D']_1 = D' - [D']_0
-      y0[e] = t ? ((1ull - q) & kp.ymask) : q;     // t + (1-2t)[D']_0
-      y1[e] = t ? ((0ull - d1) & kp.ymask) : d1;   // (1-2t)[D']_1
+      const uint64_t sgn = 1ull - 2ull * t;  // 1 - 2t (mod 2^64)
+      const uint64_t q = u64_of(Q, e);       // [D']_0 (mod 2^ell)
+      y0[e] = (t + sgn * q) & ym;            // t + (1-2t)[D']_0
+      y1[e] = (sgn * (z - q)) & ym;          // (1-2t)[D']_1, [D']_1 = D' - [D']_0
     }
   } else {
     // Alg 8: triple from seed02 / seed12, e from P2, d opened by P0/P1, combine.
@@ -84,8 +88,9 @@ __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, c
           const uint64_t in0 = y0[e] + c0v;  // ... + [c]_0
           const uint64_t in1 = y1[e] - c0v;  // [c]_1 = ab - [c]_0 (P2)
           const uint64_t x0v = s ? v0.y : v0.x, x1v = s ? v1.y : v1.x;
-          y0[e] = ((t ? x0v : 0ull) + (t ? 0ull - in0 : in0)) & kp.ymask;  // t[x] + (1-2t)(...)
-          y1[e] = ((t ? x1v : 0ull) + (t ? 0ull - in1 : in1)) & kp.ymask;
+          const uint64_t sgn = 1ull - 2ull * t;
+          y0[e] = (t * x0v + sgn * in0) & ym;  // t[x] + (1-2t)(...)
+          y1[e] = (t * x1v + sgn * in1) & ym;
         }
       }
     }
@@ -97,7 +102,7 @@ __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, c
 // Compact tape (p = 257, 8 slots): per 8-element group one part-B block
 // (8 B/element) and two part-A blocks (16 B/element, 4 elements each) -- 3
 // ChaCha blocks per 8 elements, none shared between threads.
-template <int R, bool RELU, bool TRANSCRIPT>
+template <int R, bool RELU, bool TRANSCRIPT, bool FULL>
 __global__ void __launch_bounds__(TPB, FUSED_MINB) k_fused_c(FusedArgs a, KP kp, Key k01, Key k02, Key k12) {
   __shared__ uint32_t sA[2 * PERM_A], sB[2 * PERM_B];
   build_perm_tables(sA, sB);
@@ -140,7 +145,7 @@ __global__ void __launch_bounds__(TPB, FUSED_MINB) k_fused_c(FusedArgs a, KP kp,
 #pragma unroll
       for (int k = 0; k < 8; ++k) Bp[k] = Bp[k + 8];  // elements 4..7 next
     }
-    finish_group<R, RELU>(a, kp, k02, k12, i0, j0, cnt, zbits, tbits);
+    finish_group<R, RELU, FULL>(a, kp, k02, k12, i0, j0, cnt, zbits, tbits);
   }
 }
 
@@ -173,7 +178,7 @@ __global__ void __launch_bounds__(TPB, 2) k_fused_w(FusedArgs a, KP kp, Key k01,
         a.w1hi[i0 + e] = (uint8_t)pack_hi(W1);
       }
     }
-    finish_group<R, RELU>(a, kp, k02, k12, i0, j0, cnt, zbits, tbits);
+    finish_group<R, RELU, false>(a, kp, k02, k12, i0, j0, cnt, zbits, tbits);
   }
 }
 
@@ -206,7 +211,7 @@ __global__ void __launch_bounds__(TPB_L) k_fused_l(FusedArgs a, KP kp, KPL kl, K
       zbits |= (r & 1u) << e;
       tbits |= (r >> 1) << e;
     }
-    finish_group<R, RELU>(a, kp, k02, k12, i0, j0, cnt, zbits, tbits);
+    finish_group<R, RELU, false>(a, kp, k02, k12, i0, j0, cnt, zbits, tbits);
   }
 }
 
@@ -302,7 +307,7 @@ __global__ void __launch_bounds__(TPB_L) k_fused_b1(FusedArgs a, KP kp, Key k01,
       zbits |= z << e;
       tbits |= t << e;
     }
-    finish_group<R, false>(a, kp, k02, k12, i0, j0, cnt, zbits, tbits);
+    finish_group<R, false, false>(a, kp, k02, k12, i0, j0, cnt, zbits, tbits);
   }
 }
 
@@ -349,7 +354,8 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
       auto fn = tr ? k_fused_l<R, RELU, true> : k_fused_l<R, RELU, false>;
       fn<<<grid_for((const void*)fn, ngroups, TPB_L), TPB_L, 0, st>>>(a, kp, kl, k01, k02, k12);
     } else if (prm->tape == BC_TAPE_COMPACT) {
-      auto fn = tr ? k_fused_c<R, RELU, true> : k_fused_c<R, RELU, false>;
+      auto fn = tr ? k_fused_c<R, RELU, true, false>
+                   : (prm->ell == 64 ? k_fused_c<R, RELU, false, true> : k_fused_c<R, RELU, false, false>);
       fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k01, k02, k12);
     } else {
       auto fn = k_fused_w<R, RELU>;
