@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--rounds", type=int, default=ROUNDS)
     ap.add_argument("--no-extras", action="store_true", help="skip ReLU / ladder / variants / e2e / cpu legs")
     ap.add_argument("--only", choices=["drelu", "relu", "ladder", "drelu_rss", "relu_rss", "drelu_fp", "relu_fp"], help="profiling aid: launch one op steps+warmup times, print nothing")
+    ap.add_argument("--op", default="drelu", choices=["drelu", "relu"],
+                    help="tuning aid (tools/variants.py): the op of the headline timing with --no-extras")
     ap.add_argument("--mode", default="sharded", choices=["sharded", "party"],
                     help="party: config 4, P0/P1/P2 on distinct GPUs (needs >= 3 ranks), ReLU over NCCL P2P")
     ap.add_argument("--party-n", type=int, default=1 << 26, help="elements per P0/P1/P2 triple (config 4)")
@@ -318,7 +320,8 @@ def run_cuda(a):
 
     # ---- headline: fused DReLU ------------------------------------------------
     ck = Clocks(local)
-    t_ms, per, clocks = timed(lambda: api.drelu(x0, x1, prm, seeds, base, y0, y1, stream=stream),
+    head = api.relu if a.op == "relu" else api.drelu
+    t_ms, per, clocks = timed(lambda: head(x0, x1, prm, seeds, base, y0, y1, stream=stream),
                               a.steps, max(a.warmup, 3), clocks=ck)
     ms = t_ms / a.steps
     value = world * n / (ms * 1e-3)
@@ -353,7 +356,7 @@ def run_cuda(a):
         "warmup": max(a.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded; shares of D2 activations)",
         "config": workload_config(a),
-        "roofline": roofline("drelu", value, ms),
+        "roofline": roofline(a.op, value, ms),
         "gpu_launches": a.steps,
         "clocks": clocks,
     }

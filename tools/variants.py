@@ -1,7 +1,8 @@
 """Build and time tuning variants of the fused kernel (compile-time knobs).
 
     python tools/variants.py build           # here (CPU): builds paper_2309_04909_b200/variants/*.so
-    python tools/variants.py time            # on the GPU box: times each variant (DReLU, R20 and R8)
+    python tools/variants.py time            # on the GPU box: times each variant (DReLU, R20 and R8;
+                                             # VARIANT_OP=relu times ReLU instead)
 """
 import itertools
 import json
@@ -40,7 +41,8 @@ if __name__ == "__main__":
             out = {}
             for R in (20, 8):
                 r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--no-extras", "--steps", "300",
-                                    "--rounds", str(R)], capture_output=True, text=True,
+                                    "--rounds", str(R)] + (["--op", os.environ["VARIANT_OP"]] if "VARIANT_OP" in os.environ else []),
+                                   capture_output=True, text=True,
                                    env={**os.environ, "BICOPTOR_LIB": lib})
                 try:
                     out[f"R{R}_ms"] = json.loads(r.stdout.strip().splitlines()[-1])["ms_per_step"]
