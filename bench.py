@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--rounds", type=int, default=ROUNDS)
     ap.add_argument("--no-extras", action="store_true", help="skip ReLU / ladder / variants / e2e / cpu legs")
     ap.add_argument("--only", choices=["drelu", "relu", "ladder", "drelu_rss", "relu_rss", "drelu_fp", "relu_fp"], help="profiling aid: launch one op steps+warmup times, print nothing")
-    ap.add_argument("--op", default="drelu", choices=["drelu", "relu"],
+    ap.add_argument("--op", default="drelu", choices=["drelu", "relu", "drelu_fp", "relu_fp"],
                     help="tuning aid (tools/variants.py): the op of the headline timing with --no-extras")
     ap.add_argument("--mode", default="sharded", choices=["sharded", "party"],
                     help="party: config 4, P0/P1/P2 on distinct GPUs (needs >= 3 ranks), ReLU over NCCL P2P")
@@ -301,7 +301,9 @@ def run_cuda(a):
 
     if a.only:  # profiling aid (ncu): just the launches, no timing output
         pfp = api.Params(ell=ELL, lx=31, f=0, mode=MODE, rounds=a.rounds)
-        v_lad = torch.empty((n, 8), dtype=torch.uint8, device=dev)
+        if a.only == "ladder":  # config 2's size, as the bench leg times it
+            x_c2 = x0.repeat(((1 << 28) + n - 1) // n)[:1 << 28]
+            v_lad = torch.empty((1 << 28, 8), dtype=torch.uint8, device=dev)
         if a.only.endswith("_rss"):
             xs = [torch.from_numpy(v.view(np.int64)).to(dev) for v in synth.rss_share(x, ELL, run=rank)]
             ys = tuple(torch.empty_like(xs[0]) for _ in range(3))
@@ -312,7 +314,7 @@ def run_cuda(a):
               "relu_fp": lambda: api.relu(x0, x1, pfp, seeds, base, y0, y1, stream=stream),
               "drelu": lambda: api.drelu(x0, x1, prm, seeds, base, y0, y1, stream=stream),
               "relu": lambda: api.relu(x0, x1, prm, seeds, base, y0, y1, stream=stream),
-              "ladder": lambda: api.ladder_modswitch(0, x0, prm, out=v_lad, stream=stream)}[a.only]
+              "ladder": lambda: api.ladder_modswitch(0, x_c2, prm, out=v_lad, stream=stream)}[a.only]
         for _ in range(a.warmup + a.steps):
             op()
         torch.cuda.synchronize(dev)
@@ -320,8 +322,9 @@ def run_cuda(a):
 
     # ---- headline: fused DReLU ------------------------------------------------
     ck = Clocks(local)
-    head = api.relu if a.op == "relu" else api.drelu
-    t_ms, per, clocks = timed(lambda: head(x0, x1, prm, seeds, base, y0, y1, stream=stream),
+    head = api.relu if a.op.startswith("relu") else api.drelu
+    hprm = prm if not a.op.endswith("_fp") else api.Params(ell=ELL, lx=31, f=0, mode=MODE, rounds=a.rounds)
+    t_ms, per, clocks = timed(lambda: head(x0, x1, hprm, seeds, base, y0, y1, stream=stream),
                               a.steps, max(a.warmup, 3), clocks=ck)
     ms = t_ms / a.steps
     value = world * n / (ms * 1e-3)
@@ -378,15 +381,18 @@ def run_cuda(a):
             tr_, _, _ = timed(lambda: api.relu(x0, x1, pr, seeds, base, y0, y1, stream=stream), 50, 3)
             var[f"chacha{R}"] = {"drelu": world * n / (tv / 50 * 1e-3), "relu": world * n / (tr_ / 50 * 1e-3)}
         line["variants"] = var
-        # ---- config 2: ladder + modswitch (Alg 7 steps 3-5), HBM-bound ---------
-        v_lad = torch.empty((n, 8), dtype=torch.uint8, device=dev)
-        tl, _, _ = timed(lambda: api.ladder_modswitch(0, x0, prm, out=v_lad, stream=stream), 100, 5)
-        ms_l = tl / 100
-        v_l = world * n / (ms_l * 1e-3)
-        line["trc_modswitch"] = {"value": v_l, "unit": "elements/s", "ms_per_step": ms_l,
+        # ---- config 2: ladder + modswitch (Alg 7 steps 3-5), HBM-bound, at config 2's 2^28 ----
+        n2 = 1 << 28
+        x_c2 = x0.repeat((n2 + n - 1) // n)[:n2]  # the headline batch's shares tiled to 2^28 (2 GiB)
+        v_lad = torch.empty((n2, 8), dtype=torch.uint8, device=dev)
+        tl, _, _ = timed(lambda: api.ladder_modswitch(0, x_c2, prm, out=v_lad, stream=stream), 20, 3)
+        ms_l = tl / 20
+        v_l = world * n2 / (ms_l * 1e-3)
+        line["trc_modswitch"] = {"value": v_l, "unit": "elements/s", "ms_per_step": ms_l, "n_per_gpu": n2,
                                  "roofline": roofline("ladder", v_l, ms_l),
-                                 "note": "one party, 8 B in + 8 B out per element (config 2 primitive)"}
-        del v_lad
+                                 "note": "config 2: one party, 8 B in + 8 B out per element, 2^28 elements "
+                                         "(the headline batch's shares tiled)"}
+        del v_lad, x_c2
         # ---- every party's work unshared: the party-phase kernels chained on 1 GPU ----
         line["party_chain_1gpu"] = party_chain(api, prm, seeds, x0, x1, base, dev, stream, timed, world, n)
         # ---- RSS variant (Alg 9): DReLU / ReLU on replicated shares of the same x ----

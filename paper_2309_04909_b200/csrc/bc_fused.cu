@@ -185,9 +185,12 @@ __global__ void __launch_bounds__(TPB, 2) k_fused_w(FusedArgs a, KP kp, Key k01,
 // Large tape (lx >= 8, up to 32 slots, p < 2^33): 9 seed01 blocks per element,
 // the 8 elements of a group in sequence, then the shared finish.
 constexpr int TPB_L = TPB_LARGE;
+#ifndef BC_LARGE_MINB
+#define BC_LARGE_MINB 1  // resident CTAs per SM the large-tape kernel is compiled for (register cap)
+#endif
 
 template <int R, bool RELU, bool TRANSCRIPT>
-__global__ void __launch_bounds__(TPB_L) k_fused_l(FusedArgs a, KP kp, KPL kl, Key k01, Key k02, Key k12) {
+__global__ void __launch_bounds__(TPB_L, BC_LARGE_MINB) k_fused_l(FusedArgs a, KP kp, KPL kl, Key k01, Key k02, Key k12) {
   __shared__ uint8_t sidx[32 * TPB_L];
   __shared__ uint32_t sstg[32 * TPB_L];
   __shared__ uint32_t magic[33], hlim[33];

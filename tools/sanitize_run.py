@@ -43,6 +43,18 @@ for n in (1, 13, 1003):
     tr = api.transcript_buffers(n, dev, big)
     api.drelu(a0, a1, big, sd, 8, transcript=tr)
     api.relu(a0, a1, big, sd, 8)
+    for pk in (big, api.Params(ell=64, lx=31, f=0, mode="literal", rounds=8), api.Params(ell=24, lx=10, f=0, rounds=8)):
+        x, x0, x1 = synth.shares(n, pk.ell, pk.lx, pk.f, "D1")   # party phases on the uint32 wire planes
+        b0, b1 = t(x0), t(x1)
+        lo0, hi0, tb0 = api.drelu_send(0, b0, pk, sd.s01, 8)
+        lo1, hi1, tb1 = api.drelu_send(1, b1, pk, sd.s01, 8)
+        r0, r1 = api.drelu_helper(lo0, hi0, lo1, hi1, pk, sd.s02, 8, paper_literal=True)
+        api.drelu_finish(1, tb1, r1, pk, n, None, 8)
+        dp = torch.empty_like(b0)
+        L0, H0, T0, d0 = api.relu_send(0, b0, pk, sd.s01, sd.s02, 8, d_peer=dp)
+        L1, H1, T1, d1 = api.relu_send(1, b1, pk, sd.s01, sd.s12, 8)
+        e, c1 = api.relu_helper(L0, H0, L1, H1, pk, sd.s02, sd.s12, 8, e_dup=torch.empty_like(b0))
+        api.relu_finish(1, b1, T1, d1, dp, e, c1, pk, sd.s12, 8)
     api.trc_aby3(a0, a1, 64, 26, sd, 8, q=1, rounds=8)
     api.mul_trc("trc_then_mul", "aby3", a0, a1, a0, a1, 64, 26, sd, 8, rounds=8)
     api.mul_trc("mul_then_trc", "secureml", a0, a1, a0, a1, 64, 26, sd, 8, rounds=8)
