@@ -241,9 +241,17 @@ def run_cuda(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BENCH_SHARE_GPU=1 (testing the N>1 code path on a 1-GPU box): every rank on cuda:0, gloo
+    # for the barriers and the max over ranks.  Its numbers are not measurements.
+    share = os.environ.get("BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     api.lib()
@@ -255,7 +263,7 @@ def run_cuda(a):
     def max_over_ranks(v: float) -> float:
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if share else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -592,9 +600,17 @@ def run_party(a):
             print(json.dumps({"metric": "config4 party-separated ReLU elements/s", "mode": "party",
                               "unavailable": f"needs >= 3 GPUs (one per party), have {world}"}))
         return
+    share = os.environ.get("BENCH_SHARE_GPU") == "1"  # testing aid, see run_cuda: every rank on cuda:0, gloo
+    if share:
+        local = 0
+        if a.transport != "peer":
+            raise SystemExit("BENCH_SHARE_GPU=1 needs --transport peer (NCCL cannot put two ranks on one GPU)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    if share:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
     k = world // 3
     group = dist.new_group(list(range(3 * k)))
     # peer transport: doorbells / credits / IPC handles over a gloo group per triple
@@ -639,10 +655,11 @@ def run_party(a):
         bytes_sent = runner.bytes_sent / steps if a.transport == "nccl" else wire
         if a.transport == "peer":
             runner.close()
-    t = torch.tensor([t_ms, bytes_sent], dtype=torch.float64, device=dev)
+    rdev = "cpu" if share else dev
+    t = torch.tensor([t_ms, bytes_sent], dtype=torch.float64, device=rdev)
     tm = t.clone()
     dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-    per_rank = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in range(world)]
+    per_rank = [torch.zeros(2, dtype=torch.float64, device=rdev) for _ in range(world)]
     dist.all_gather(per_rank, t)
     if rank == 0:
         ms = float(tm[0])
