@@ -470,6 +470,34 @@ def party_chain(api, prm, seeds, x0, x1, base, dev, stream, timed, world, n):
         t_ms, _, _ = timed(fn, 50, 3)
         ms = t_ms / 50
         res[name] = {"value": world * n / (ms * 1e-3), "unit": "elements/s", "ms_per_step": ms, "launches_per_step": 5}
+    # each party's kernels alone (inputs left in place by the chains above): what one GPU per party
+    # would run per step in config 4.  The rate of a P0/P1/P2 triple on three GPUs is bounded by the
+    # slowest party, transfers overlapped -- a projection from measured kernels, not a 3-GPU run.
+    per = {}
+    for name, calls in (
+            ("drelu", {"P0": lambda: (api.drelu_send(0, x0, prm, seeds.s01, base, out=(lo0, hi0, tb0), stream=stream),
+                                      api.drelu_finish(0, tb0, None, prm, n, seeds.s02, base, out=ya, stream=stream)),
+                       "P1": lambda: (api.drelu_send(1, x1, prm, seeds.s01, base, out=(lo1, hi1, tb1), stream=stream),
+                                      api.drelu_finish(1, tb1, r1, prm, n, None, base, out=yb, stream=stream)),
+                       "P2": lambda: api.drelu_helper(lo0, hi0, lo1, hi1, prm, seeds.s02, base, out=(None, r1),
+                                                      stream=stream)}),
+            ("relu", {"P0": lambda: (api.relu_send(0, x0, prm, seeds.s01, seeds.s02, base, out=(lo0, hi0, tb0, d0),
+                                                   stream=stream),
+                                     api.relu_finish(0, x0, tb0, d0, d1, e, None, prm, seeds.s02, base, out=ya,
+                                                     stream=stream)),
+                      "P1": lambda: (api.relu_send(1, x1, prm, seeds.s01, seeds.s12, base, out=(lo1, hi1, tb1, d1),
+                                                   stream=stream),
+                                     api.relu_finish(1, x1, tb1, d1, d0, e, c1, prm, seeds.s12, base, out=yb,
+                                                     stream=stream)),
+                      "P2": lambda: api.relu_helper(lo0, hi0, lo1, hi1, prm, seeds.s02, seeds.s12, base,
+                                                    out=(e, c1), stream=stream)})):
+        ms_p = {}
+        for pty, fn in calls.items():
+            t_p, _, _ = timed(fn, 30, 3)
+            ms_p[pty] = t_p / 30
+        per[name] = {"ms_per_party": ms_p,
+                     "projected_triple_elements_per_s": n / (max(ms_p.values()) * 1e-3)}
+    res["per_party"] = per
     res["note"] = "P0,P1 send + P2 helper + P0,P1 finish back to back on one GPU: all parties' work, nothing shared"
     # the messages these kernels exchange, per element (DESIGN.md sec. 4 wire format) vs Table 1
     slots, pbits = LX + 1, 9 if MODE == "guard" else 8
