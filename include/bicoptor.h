@@ -19,7 +19,9 @@
  *   - elem_base is the global index of element 0 of this call; every PRG draw
  *     is addressed by global index j = elem_base + i, so a batch split into
  *     shards (or chunks) gives bit-identical results to one call.  It must be
- *     a multiple of 8 (BC_EALIGN).
+ *     a multiple of 8 (BC_EALIGN), and elem_base + n <= BC_MAX_INDEX = 2^44
+ *     (BC_ERANGE): the stream counters (j * 9 + b for the large tape, j * 2^20
+ *     + k for its fallback stream) then never wrap.
  *   - Seeds are 32-byte keys passed by value; a party-phase call takes only the
  *     seeds that party holds: P0 {seed01, seed02}, P1 {seed01, seed12},
  *     P2 {seed02, seed12}.
@@ -37,10 +39,13 @@ extern "C" {
 
 #define BC_OK 0
 #define BC_EINVAL (-1)   /* bad parameter (party id, ell, lx, mode, rounds, NULL) */
-#define BC_ERANGE (-2)   /* key-bit window does not fit: need f + lx + w <= ell  */
+#define BC_ERANGE (-2)   /* key-bit window does not fit: need f + lx + w <= ell,
+                            or elem_base + n > BC_MAX_INDEX                      */
 #define BC_EALIGN (-3)   /* pointer not 16-B aligned, or elem_base % 8 != 0      */
 #define BC_ECUDA  (-4)   /* CUDA launch error (bc_last_cuda_error() has the code) */
 #define BC_EALIAS (-5)   /* an output overlaps an input                          */
+
+#define BC_MAX_INDEX ((uint64_t)1 << 44) /* bound on global element indices (elem_base + n) */
 
 #define BC_MODE_GUARD   0 /* w = lx + 1, p = 257 at lx = 7 (default; reading C6) */
 #define BC_MODE_LITERAL 1 /* w = lx, the paper's Z_{2^lx} (64-bit wire)  */

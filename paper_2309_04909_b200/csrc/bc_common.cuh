@@ -54,6 +54,7 @@ KPL make_kpl(const bc_params* prm);                  // large-tape constants (p 
 bool aligned16(const void* p);
 bool aligned8(const void* p);
 bool overlap(const void* a, size_t na, const void* b, size_t nb);
+bool index_range_ok(uint64_t base, size_t n);       // [base, base + n) within [0, BC_MAX_INDEX]
 int check_params(const bc_params* prm);              // re-derives and compares
 KP make_kp(const bc_params* prm);
 Key make_key(const uint8_t* s);

@@ -322,6 +322,7 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
   if (n == 0) return BC_OK;  // no-op after parameter validation
   if (!x0 || !x1 || !y0 || !y1 || !seeds) return BC_EINVAL;
   if (!aligned16(x0) || !aligned16(x1) || !aligned16(y0) || !aligned16(y1) || (base & 7)) return BC_EALIGN;
+  if (!index_range_ok(base, n)) return BC_ERANGE;  // global indices j < BC_MAX_INDEX
   const size_t nb = n * 8;
   if (overlap(y0, nb, y1, nb) || overlap(y0, nb, x0, nb) || overlap(y0, nb, x1, nb) || overlap(y1, nb, x0, nb) ||
       overlap(y1, nb, x1, nb))
@@ -376,6 +377,7 @@ int drelu_b1(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1,
   if (n == 0) return BC_OK;
   if (!x0 || !x1 || !y0 || !y1 || !seeds) return BC_EINVAL;
   if (!aligned16(x0) || !aligned16(x1) || !aligned16(y0) || !aligned16(y1) || (base & 7)) return BC_EALIGN;
+  if (!index_range_ok(base, n)) return BC_ERANGE;  // global indices j < BC_MAX_INDEX
   const size_t nb = n * 8;
   if (overlap(y0, nb, y1, nb) || overlap(y0, nb, x0, nb) || overlap(y0, nb, x1, nb) || overlap(y1, nb, x0, nb) ||
       overlap(y1, nb, x1, nb))

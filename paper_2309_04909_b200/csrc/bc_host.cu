@@ -82,6 +82,8 @@ bool overlap(const void* a, size_t na, const void* b, size_t nb) {
   return x < y + nb && y < x + na;
 }
 
+bool index_range_ok(uint64_t base, size_t n) { return base <= BC_MAX_INDEX && (uint64_t)n <= BC_MAX_INDEX - base; }
+
 int check_params(const bc_params* prm) {
   if (!prm) return BC_EINVAL;
   bc_params ref;
@@ -156,7 +158,7 @@ const char* bc_strerror(int code) {
   switch (code) {
     case BC_OK: return "ok";
     case BC_EINVAL: return "invalid parameter";
-    case BC_ERANGE: return "key-bit window does not fit: need f + lx + w <= ell";
+    case BC_ERANGE: return "key-bit window does not fit (need f + lx + w <= ell), or elem_base + n > BC_MAX_INDEX";
     case BC_EALIGN: return "pointer misaligned (16 B for u64 arrays) or elem_base not a multiple of 8";
     case BC_ECUDA: return "CUDA launch error (see bc_last_cuda_error)";
     case BC_EALIAS: return "output overlaps an input";

@@ -57,6 +57,7 @@ int host_run(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1,
   if (n == 0) return BC_OK;
   if (!x0 || !x1 || !y0 || !y1 || !seeds || !ws || chunk == 0 || (chunk & 7)) return BC_EINVAL;
   if (!aligned16(ws) || (base & 7)) return BC_EALIGN;
+  if (!index_range_ok(base, n)) return BC_ERANGE;  // global indices j < BC_MAX_INDEX
   if (ws_bytes < NS * slot_bytes(chunk)) return BC_EINVAL;
   const size_t nb = n * 8;
   if (overlap(y0, nb, x0, nb) || overlap(y0, nb, x1, nb) || overlap(y1, nb, x0, nb) || overlap(y1, nb, x1, nb) ||

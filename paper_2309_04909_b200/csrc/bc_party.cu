@@ -342,6 +342,7 @@ int send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits,
   if (!aligned16(x) || !aligned16(lo) || (hi && !aligned8(hi)) || (RELU && !aligned16(dshare)) ||
       (dpeer && !aligned16(dpeer)) || (base & 7))
     return BC_EALIGN;
+  if (!index_range_ok(base, n)) return BC_ERANGE;  // global indices j < BC_MAX_INDEX
   const size_t nb = n * 8;
   const size_t nlo = large ? n * prm->slots * 4 : nb, nhi = large ? n * 4 : n;  // wire planes (bytes)
   if (overlap(lo, nlo, x, nb) || overlap(hi, nhi, x, nb) || overlap(tbits, (n + 7) / 8, x, nb) ||
@@ -386,6 +387,7 @@ int helper(const uint8_t* lo0, const uint8_t* hi0, const uint8_t* lo1, const uin
   if (!aligned16(lo0) || !aligned16(lo1) || (hi0 && !aligned8(hi0)) || (hi1 && !aligned8(hi1)) ||
       (out0 && !aligned16(out0)) || (out0b && !aligned16(out0b)) || (out1 && !aligned16(out1)) || (base & 7))
     return BC_EALIGN;
+  if (!index_range_ok(base, n)) return BC_ERANGE;  // global indices j < BC_MAX_INDEX
   if (out0b && !out0) return BC_EINVAL;
   const size_t nb = n * 8;
   const size_t nlo = large ? n * prm->slots * 4 : nb, nhi = large ? n * 4 : n;  // wire planes (bytes)
@@ -427,6 +429,7 @@ int finish(int party, const uint64_t* x, const uint8_t* tbits, const uint64_t* r
   if (!aligned16(y) || (resp && !aligned16(resp)) || (x && !aligned16(x)) || (d_own && !aligned16(d_own)) ||
       (d_peer && !aligned16(d_peer)) || (c1 && !aligned16(c1)) || (base & 7))
     return BC_EALIGN;
+  if (!index_range_ok(base, n)) return BC_ERANGE;  // global indices j < BC_MAX_INDEX
   const size_t nb = n * 8;
   if (overlap(y, nb, resp, nb) || overlap(y, nb, x, nb) || overlap(y, nb, d_own, nb) || overlap(y, nb, d_peer, nb) ||
       overlap(y, nb, c1, nb) || overlap(y, nb, tbits, (n + 7) / 8))

@@ -172,6 +172,7 @@ int fused_rss(const uint64_t* x0, const uint64_t* x1, const uint64_t* x2, uint64
   if (!aligned16(x0) || !aligned16(x1) || !aligned16(x2) || !aligned16(y0) || !aligned16(y1) || !aligned16(y2) ||
       (base & 7))
     return BC_EALIGN;
+  if (!index_range_ok(base, n)) return BC_ERANGE;  // global indices j < BC_MAX_INDEX
   const size_t nb = n * 8;
   const void* ins[3] = {x0, x1, x2};
   const void* outs[3] = {y0, y1, y2};

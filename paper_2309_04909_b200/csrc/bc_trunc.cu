@@ -226,6 +226,7 @@ int bc_trc_aby3(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* 
   if (n == 0) return BC_OK;
   if (!x0 || !x1 || !y0 || !y1 || !seeds) return BC_EINVAL;
   if (!aligned16(x0) || !aligned16(x1) || !aligned16(y0) || !aligned16(y1) || (elem_base & 7)) return BC_EALIGN;
+  if (!index_range_ok(elem_base, n)) return BC_ERANGE;  // global indices j < BC_MAX_INDEX
   const size_t nb = n * 8;
   if (overlap(y0, nb, y1, nb) || overlap(y0, nb, x0, nb) || overlap(y0, nb, x1, nb) || overlap(y1, nb, x0, nb) ||
       overlap(y1, nb, x1, nb))
@@ -253,6 +254,7 @@ int bc_mul_trc(int order, int alg, const uint64_t* x0, const uint64_t* x1, const
   if (!aligned16(x0) || !aligned16(x1) || !aligned16(y0) || !aligned16(y1) || !aligned16(z0) || !aligned16(z1) ||
       (elem_base & 7))
     return BC_EALIGN;
+  if (!index_range_ok(elem_base, n)) return BC_ERANGE;  // global indices j < BC_MAX_INDEX
   const size_t nb = n * 8;
   const void* ins[4] = {x0, x1, y0, y1};
   if (overlap(z0, nb, z1, nb)) return BC_EALIAS;

@@ -667,3 +667,56 @@ def test_b1_fallback_elements(api):
         ref = B1.drelu1(B.Params(**kw), x0, x1, jj, SEEDS)
         y0, y1 = api.drelu_b1(dev(x0), dev(x1), api.Params(**kw), SEEDS, elem_base=base)
         assert np.array_equal(host(y0), ref["y0"]) and np.array_equal(host(y1), ref["y1"])
+
+
+# ---- the top of the index domain (BC_MAX_INDEX = 2^44) ------------------------------------
+
+HIGH_PARAMS = [PARAMS[0], PARAMS[4], PARAMS[5], dict(ell=64, lx=31, f=0, mode="guard", rounds=8)]
+
+
+@pytest.mark.parametrize("kw", HIGH_PARAMS, ids=_ids)
+def test_high_global_indices(api, kw):
+    """Elements at the top of the index domain: every stream counter carries
+    into its high word (compact part A counter j/4 ~ 2^42, large tape 9j ~ 2^47,
+    fallback j 2^20 ~ 2^64), fused and party kernels bit-exact with the oracle;
+    one element more is BC_ERANGE."""
+    oprm, prm = B.Params(**kw), api.Params(**kw)
+    n = 203 if oprm.layout == "large" else 2051
+    base = ((1 << 44) - n) // 8 * 8
+    x, x0, x1 = synth.shares(n, kw["ell"], kw["lx"], kw["f"], "D1")
+    j = np.arange(n, dtype=np.uint64) + np.uint64(base)
+    for fn in ("drelu", "relu"):
+        y0, y1 = getattr(api, fn)(dev(x0), dev(x1), prm, SEEDS, elem_base=base)
+        ref = getattr(B, fn)(oprm, x0, x1, j, SEEDS)
+        assert np.array_equal(host(y0), ref["y0"]) and np.array_equal(host(y1), ref["y1"]), fn
+    lo0, hi0, tb0 = api.drelu_send(0, dev(x0), prm, SEEDS.s01, base)
+    lo1, hi1, tb1 = api.drelu_send(1, dev(x1), prm, SEEDS.s01, base)
+    _, r1 = api.drelu_helper(lo0, hi0, lo1, hi1, prm, SEEDS.s02, base)
+    y1 = api.drelu_finish(1, tb1, r1, prm, n, None, base)
+    assert np.array_equal(host(y1), B.drelu(oprm, x0, x1, j, SEEDS)["y1"])
+    with pytest.raises(api.BicoptorError, match=r"\[-2\]"):
+        api.drelu(dev(x0), dev(x1), prm, SEEDS, elem_base=base + 8 * ((n + 15) // 8))
+    with pytest.raises(api.BicoptorError, match=r"\[-2\]"):
+        api.drelu_send(0, dev(x0), prm, SEEDS.s01, 1 << 44)
+
+
+def test_high_global_indices_rss_b1_trunc(api):
+    from oracle import bicoptor1 as B1, rss, trunc
+    n = 1003
+    base = ((1 << 44) - n) // 8 * 8
+    j = np.arange(n, dtype=np.uint64) + np.uint64(base)
+    kw = PARAMS[0]
+    oprm, prm = B.Params(**kw), api.Params(**kw)
+    x = synth.plaintext(n, 64, 7, 24, "D1")
+    xs = synth.rss_share(x, 64)
+    ys = api.drelu_rss(*(dev(v) for v in xs), prm, SEEDS, base)
+    ref = rss.drelu_rss(oprm, *xs, j, SEEDS)
+    for k in range(3):
+        assert np.array_equal(host(ys[k]), ref["y"][k])
+    x, x0, x1 = synth.shares(n, 64, 7, 24, "D1")
+    y0, y1 = api.drelu_b1(dev(x0), dev(x1), prm, SEEDS, base)
+    r1 = B1.drelu1(oprm, x0, x1, j, SEEDS)
+    assert np.array_equal(host(y0), r1["y0"]) and np.array_equal(host(y1), r1["y1"])
+    z0, z1 = api.trc_aby3(dev(x0), dev(x1), 64, 26, SEEDS, elem_base=base, q=1)
+    t0, t1 = trunc.trc_aby3(x0, x1, trunc.aby3_pre(64, 26, j, SEEDS, 20, 1), 26, 64)
+    assert np.array_equal(host(z0), t0) and np.array_equal(host(z1), t1)
