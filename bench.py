@@ -379,6 +379,20 @@ def run_cuda(a):
         ms_r = t_ms_r / max(a.steps // 2, 5)
         v_r = world * n / (ms_r * 1e-3)
         line["relu"] = {"value": v_r, "unit": "elements/s", "ms_per_step": ms_r, "roofline": roofline("relu", v_r, ms_r)}
+        # ---- DReLU across batch sizes: launch-bound small batches to config 3's 2^27 asymptote ----
+        sweep = {}
+        for lg in (16, 20, 22, 27):
+            m = 1 << lg
+            xs0 = x0.repeat((m + n - 1) // n)[:m] if m > n else x0[:m]
+            xs1 = x1.repeat((m + n - 1) // n)[:m] if m > n else x1[:m]
+            ys0, ys1 = torch.empty_like(xs0), torch.empty_like(xs1)
+            reps = max(5, min(200, (1 << 28) // m))
+            tv, _, _ = timed(lambda: api.drelu(xs0, xs1, prm, seeds, base, ys0, ys1, stream=stream), reps, 3)
+            sweep[f"2^{lg}"] = world * m / (tv / reps * 1e-3)
+            del xs0, xs1, ys0, ys1
+        sweep["2^24"] = value
+        line["drelu_batch_sweep"] = {"unit": "elements/s", **dict(sorted(sweep.items(), key=lambda kv: int(kv[0][2:]))),
+                                     "note": "2^27: the headline batch's shares tiled; smaller batches are prefixes"}
         # ---- ChaCha round-count variants of DReLU --------------------------------
         var = {}
         for R in (12, 8):
