@@ -720,3 +720,32 @@ def test_high_global_indices_rss_b1_trunc(api):
     z0, z1 = api.trc_aby3(dev(x0), dev(x1), 64, 26, SEEDS, elem_base=base, q=1)
     t0, t1 = trunc.trc_aby3(x0, x1, trunc.aby3_pre(64, 26, j, SEEDS, 20, 1), 26, 64)
     assert np.array_equal(host(z0), t0) and np.array_equal(host(z1), t1)
+
+
+# ---- the largest batch one call takes in this suite: n > 2^31 -------------------------------
+
+@pytest.mark.parametrize("fn", ["drelu", "relu"])
+def test_max_size_over_2pow31_sampled(api, fn):
+    """n = 2^31 + 13 elements in one call (64 GiB of shares and outputs): no
+    32-bit index or size overflow anywhere on the path.  Oracle parity on a
+    seeded sample that includes the first and last groups and the 2^31 and
+    2^32-element boundaries of the byte offsets."""
+    if torch.cuda.get_device_properties(0).total_memory < (96 << 30):
+        pytest.skip("needs > 96 GiB of device memory")
+    n = (1 << 31) + 13
+    g = torch.Generator(device=DEV).manual_seed(2024)
+    x0 = torch.randint(-(1 << 63), (1 << 63) - 1, (n,), dtype=torch.int64, device=DEV, generator=g)
+    x1 = torch.randint(-(1 << 63), (1 << 63) - 1, (n,), dtype=torch.int64, device=DEV, generator=g)
+    kw = PARAMS[0]
+    y0, y1 = getattr(api, fn)(x0, x1, api.Params(**kw), SEEDS)
+    rng = np.random.default_rng(17)
+    idx = np.unique(np.concatenate([np.arange(16), n - 1 - np.arange(16), (1 << 28) + np.arange(-8, 8),
+                                    (1 << 29) + np.arange(-8, 8), (1 << 31) + np.arange(-8, 8),
+                                    rng.choice(n, 4096, replace=False)]))
+    ti = torch.from_numpy(idx.astype(np.int64)).to(DEV)
+    s0, s1 = host(x0[ti]), host(x1[ti])
+    g0, g1 = host(y0[ti]), host(y1[ti])
+    del x0, x1, y0, y1
+    torch.cuda.empty_cache()
+    ref = getattr(B, fn)(B.Params(**kw), s0, s1, idx.astype(np.uint64), SEEDS)
+    assert np.array_equal(g0, ref["y0"]) and np.array_equal(g1, ref["y1"])
