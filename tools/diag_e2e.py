@@ -24,7 +24,7 @@ def both():
     with torch.cuda.stream(s2): hy0.copy_(d2, non_blocking=True)
 out["bidir_GBs_each"] = bw(both, 8 * n)
 prm, sd = api.Params(), synth.seeds(0)
-for chunk in (1 << 18, 1 << 19, 1 << 20, 1 << 21, 1 << 22):
+for chunk in (1 << 19, 1 << 20, 1 << 21, 1 << 22, 1 << 23):
     ex = H.HostPipeline(dev, chunk=chunk)
     for _ in range(2): ex.drelu(hx0, hx1, hy0, hy1, prm, sd)
     torch.cuda.synchronize(); t = time.perf_counter()
