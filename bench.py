@@ -57,7 +57,9 @@ def parse():
     ap.add_argument("--n", type=int, default=N_PER_GPU)
     ap.add_argument("--rounds", type=int, default=ROUNDS)
     ap.add_argument("--no-extras", action="store_true", help="skip ReLU / ladder / variants / e2e / cpu legs")
-    ap.add_argument("--only", choices=["drelu", "relu", "ladder", "drelu_rss", "relu_rss", "drelu_fp", "relu_fp"], help="profiling aid: launch one op steps+warmup times, print nothing")
+    ap.add_argument("--only", choices=["drelu", "relu", "ladder", "drelu_rss", "relu_rss", "drelu_fp", "relu_fp",
+                                       "party_drelu", "party_relu"],
+                    help="profiling aid: launch one op steps+warmup times, print nothing")
     ap.add_argument("--op", default="drelu", choices=["drelu", "relu", "drelu_fp", "relu_fp"],
                     help="tuning aid (tools/variants.py): the op of the headline timing with --no-extras")
     ap.add_argument("--mode", default="sharded", choices=["sharded", "party"],
@@ -312,11 +314,30 @@ def run_cuda(a):
         if a.only == "ladder":  # config 2's size, as the bench leg times it
             x_c2 = x0.repeat(((1 << 28) + n - 1) // n)[:1 << 28]
             v_lad = torch.empty((1 << 28, 8), dtype=torch.uint8, device=dev)
+        if a.only.startswith("party_"):  # the five party-phase kernels of one step, chained
+            lo0, hi0, tb0 = api.msg_buffers(n, dev)
+            lo1, hi1, tb1 = api.msg_buffers(n, dev)
+            r1, d0, d1, e, c1 = (torch.empty_like(y0) for _ in range(5))
         if a.only.endswith("_rss"):
             xs = [torch.from_numpy(v.view(np.int64)).to(dev) for v in synth.rss_share(x, ELL, run=rank)]
             ys = tuple(torch.empty_like(xs[0]) for _ in range(3))
             f_rss = getattr(api, a.only)
-        op = {"drelu_rss": lambda: f_rss(*xs, prm, seeds, base, out=ys, stream=stream),
+        def party_drelu():
+            api.drelu_send(0, x0, prm, seeds.s01, base, out=(lo0, hi0, tb0), stream=stream)
+            api.drelu_send(1, x1, prm, seeds.s01, base, out=(lo1, hi1, tb1), stream=stream)
+            api.drelu_helper(lo0, hi0, lo1, hi1, prm, seeds.s02, base, out=(None, r1), stream=stream)
+            api.drelu_finish(0, tb0, None, prm, n, seeds.s02, base, out=y0, stream=stream)
+            api.drelu_finish(1, tb1, r1, prm, n, None, base, out=y1, stream=stream)
+
+        def party_relu():
+            api.relu_send(0, x0, prm, seeds.s01, seeds.s02, base, out=(lo0, hi0, tb0, d0), stream=stream)
+            api.relu_send(1, x1, prm, seeds.s01, seeds.s12, base, out=(lo1, hi1, tb1, d1), stream=stream)
+            api.relu_helper(lo0, hi0, lo1, hi1, prm, seeds.s02, seeds.s12, base, out=(e, c1), stream=stream)
+            api.relu_finish(0, x0, tb0, d0, d1, e, None, prm, seeds.s02, base, out=y0, stream=stream)
+            api.relu_finish(1, x1, tb1, d1, d0, e, c1, prm, seeds.s12, base, out=y1, stream=stream)
+
+        op = {"party_drelu": party_drelu, "party_relu": party_relu,
+              "drelu_rss": lambda: f_rss(*xs, prm, seeds, base, out=ys, stream=stream),
               "relu_rss": lambda: f_rss(*xs, prm, seeds, base, out=ys, stream=stream),
               "drelu_fp": lambda: api.drelu(x0, x1, pfp, seeds, base, y0, y1, stream=stream),
               "relu_fp": lambda: api.relu(x0, x1, pfp, seeds, base, y0, y1, stream=stream),

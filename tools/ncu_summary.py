@@ -1,6 +1,7 @@
 """Summarise ncu captures into profiles/ (committed evidence).
 
     python tools/ncu_summary.py <round-tag> gpurun_out/prof_<op>.ncu-rep ... [--launches gpurun_out/launches.csv]
+                                [--out DIR]   (default profiles/; on the GPU box write under gpurun_out/)
 
 Writes profiles/<tag>_<op>.txt (key counters, stall reasons) per report,
 profiles/<tag>_launches.txt (per-launch durations and each kernel's share),
@@ -99,10 +100,18 @@ def launches(tag, path):
 
 if __name__ == "__main__":
     tag = sys.argv[1]
+    args = sys.argv[2:]
+    if "--out" in args:
+        i = args.index("--out")
+        PROF = os.path.abspath(args[i + 1])
+        args = args[:i] + args[i + 2:]
     os.makedirs(PROF, exist_ok=True)
     tj = os.path.join(PROF, "ncu_traffic.json")
-    traffic = json.load(open(tj)) if os.path.exists(tj) else {}
-    args = sys.argv[2:]
+    if not os.path.exists(tj) and os.path.exists(os.path.join(ROOT, "profiles", "ncu_traffic.json")):
+        tj_src = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    else:
+        tj_src = tj
+    traffic = json.load(open(tj_src)) if os.path.exists(tj_src) else {}
     if "--launches" in args:
         i = args.index("--launches")
         launches(tag, args[i + 1])

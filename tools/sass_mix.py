@@ -48,7 +48,7 @@ def main():
     si, ti = h.index("Source"), h.index("Thread Instructions Executed")
     by_op, by_pipe = Counter(), Counter()
     for r in rows[hdr + 1:]:
-        if len(r) <= ti or not r[ti].strip():
+        if len(r) <= ti or not r[ti].strip() or r[0] == "Address":  # reports with several kernels repeat the header
             continue
         text = r[si].strip()
         if text.startswith("@"):
