@@ -11,6 +11,7 @@ torch.uint64) holding Z_{2^ell} values bit for bit.
 from __future__ import annotations
 
 import ctypes
+import functools
 import os
 from dataclasses import dataclass
 
@@ -173,12 +174,29 @@ def _stream(stream) -> int | None:
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
+def _on_input_device(fn):
+    """Run the call with the device of its first CUDA tensor argument current, so
+    the library launches (and allocates outputs) where the inputs live, whatever
+    device the caller has current.  The first tensor argument of every entry is
+    local memory (an input share, a local inbox, the workspace); outputs may be
+    peer mappings (peer.py)."""
+    @functools.wraps(fn)
+    def run(*args, **kw):
+        for a in list(args) + list(kw.values()):
+            if isinstance(a, torch.Tensor) and a.is_cuda:
+                with torch.cuda.device(a.device):
+                    return fn(*args, **kw)
+        return fn(*args, **kw)
+    return run
+
+
 def empty_u64(n: int, device) -> torch.Tensor:
     return torch.empty(n, dtype=torch.int64, device=device)
 
 
 # ---- elementwise primitives --------------------------------------------------------
 
+@_on_input_device
 def trc(party: int, x: torch.Tensor, ell: int, k1: int, k2: int = 0, out=None, stream=None) -> torch.Tensor:
     """Alg 4 / Alg 5 deterministic truncation of one party's share."""
     out = torch.empty_like(x) if out is None else out
@@ -186,6 +204,7 @@ def trc(party: int, x: torch.Tensor, ell: int, k1: int, k2: int = 0, out=None, s
     return out
 
 
+@_on_input_device
 def trc_prob(party: int, x: torch.Tensor, ell: int, k: int, out=None, stream=None) -> torch.Tensor:
     """Alg 1 SecureML probabilistic truncation of one party's share."""
     out = torch.empty_like(x) if out is None else out
@@ -193,6 +212,7 @@ def trc_prob(party: int, x: torch.Tensor, ell: int, k: int, out=None, stream=Non
     return out
 
 
+@_on_input_device
 def modswitch(party: int, x: torch.Tensor, lp: int, p: int, out=None, stream=None) -> torch.Tensor:
     """Alg 6 modulo switch Z_{2^lp} -> Z_p of one party's share (uint32 out, in int32 storage)."""
     out = torch.empty(x.numel(), dtype=torch.int32, device=x.device) if out is None else out
@@ -201,6 +221,7 @@ def modswitch(party: int, x: torch.Tensor, lp: int, p: int, out=None, stream=Non
     return out
 
 
+@_on_input_device
 def ladder_modswitch(party: int, x: torch.Tensor, prm: Params, out=None, stream=None) -> torch.Tensor:
     """Alg 7 steps 3-5 on one party's share: (n, 8) uint8, byte m = v'_m - 1."""
     out = torch.empty((x.numel(), 8), dtype=torch.uint8, device=x.device) if out is None else out
@@ -226,6 +247,7 @@ def _fused(fn, what, x0, x1, prm, seeds, elem_base, y0, y1, transcript, stream):
     return y0, y1
 
 
+@_on_input_device
 def drelu_b1(x0, x1, prm: Params, seeds, elem_base: int = 0, y0=None, y1=None, transcript=None, stream=None):
     """Bicoptor-1 DReLU (comparison point): returns (y0, y1); transcript = u64 planes
     {"w0_lo", "w1_lo"} of shape (n, lx+1)."""
@@ -245,11 +267,13 @@ def transcript_buffers(n: int, device, prm: "Params | None" = None) -> dict:
             "w1_hi": torch.empty(n, dtype=torch.uint8, device=device)}
 
 
+@_on_input_device
 def drelu(x0, x1, prm: Params, seeds, elem_base: int = 0, y0=None, y1=None, transcript=None, stream=None):
     """Alg 7 with all three parties in one fused kernel: returns (y0, y1), y0 + y1 = DReLU(x)."""
     return _fused(lib().bc_drelu, "bc_drelu", x0, x1, prm, seeds, elem_base, y0, y1, transcript, stream)
 
 
+@_on_input_device
 def relu(x0, x1, prm: Params, seeds, elem_base: int = 0, y0=None, y1=None, transcript=None, stream=None):
     """Alg 8 with all three parties in one fused kernel: returns (y0, y1), y0 + y1 = ReLU(x)."""
     return _fused(lib().bc_relu, "bc_relu", x0, x1, prm, seeds, elem_base, y0, y1, transcript, stream)
@@ -282,12 +306,14 @@ def _host_call(fn, what, hx0, hx1, hy0, hy1, prm, seeds, elem_base, ws, chunk, s
     return hy0, hy1
 
 
+@_on_input_device
 def drelu_host(hx0, hx1, hy0, hy1, prm: Params, seeds, ws, chunk: int = 1 << 20, elem_base: int = 0, stream=None):
     """bc_drelu_host: host shares in (pinned recommended), host shares out; synchronous."""
     return _host_call(lib().bc_drelu_host, "bc_drelu_host", hx0, hx1, hy0, hy1, prm, seeds, elem_base, ws, chunk,
                       stream)
 
 
+@_on_input_device
 def relu_host(hx0, hx1, hy0, hy1, prm: Params, seeds, ws, chunk: int = 1 << 20, elem_base: int = 0, stream=None):
     """bc_relu_host: as drelu_host for ReLU."""
     return _host_call(lib().bc_relu_host, "bc_relu_host", hx0, hx1, hy0, hy1, prm, seeds, elem_base, ws, chunk,
@@ -316,6 +342,7 @@ def msg_buffers(n: int, device, prm: "Params | None" = None):
     return lo, hi, tb
 
 
+@_on_input_device
 def drelu_send(party, x, prm: Params, seed01: bytes, elem_base=0, out=None, stream=None):
     """Alg 7 steps 1-8 for P0/P1: returns (lo, hi, tbits)."""
     n = x.numel()
@@ -325,6 +352,7 @@ def drelu_send(party, x, prm: Params, seed01: bytes, elem_base=0, out=None, stre
     return lo, hi, tb
 
 
+@_on_input_device
 def drelu_helper(lo0, hi0, lo1, hi1, prm: Params, seed02: bytes, elem_base=0, paper_literal=False, out=None,
                  stream=None):
     """Alg 7 steps 9-10 for P2: returns (resp0 or None, resp1)."""
@@ -341,6 +369,7 @@ def drelu_helper(lo0, hi0, lo1, hi1, prm: Params, seed02: bytes, elem_base=0, pa
     return r0, r1
 
 
+@_on_input_device
 def drelu_finish(party, tbits, resp, prm: Params, n: int, seed02: bytes | None = None, elem_base=0, out=None,
                  stream=None):
     """Alg 7 step 11 for P0/P1 (P0 may pass resp=None and seed02)."""
@@ -350,6 +379,7 @@ def drelu_finish(party, tbits, resp, prm: Params, n: int, seed02: bytes | None =
     return y
 
 
+@_on_input_device
 def relu_send(party, x, prm: Params, seed01: bytes, seed_tr: bytes, elem_base=0, out=None, d_peer=None,
               stream=None):
     """Alg 8 steps 1, 4 for P0/P1: returns (lo, hi, tbits, dshare).  d_peer: a second
@@ -372,6 +402,7 @@ def relu_send(party, x, prm: Params, seed01: bytes, seed_tr: bytes, elem_base=0,
     return lo, hi, tb, d
 
 
+@_on_input_device
 def relu_helper(lo0, hi0, lo1, hi1, prm: Params, seed02: bytes, seed12: bytes, elem_base=0, with_c1=True, out=None,
                 e_dup=None, stream=None):
     """Alg 8 steps 2-3 for P2: returns (e, c1 or None).  e_dup: a second destination of
@@ -394,6 +425,7 @@ def relu_helper(lo0, hi0, lo1, hi1, prm: Params, seed02: bytes, seed12: bytes, e
     return e, c1
 
 
+@_on_input_device
 def relu_finish(party, x, tbits, d_own, d_peer, e, c1, prm: Params, seed_tr: bytes, elem_base=0, out=None,
                 stream=None):
     """Alg 8 steps 4-5 for P0/P1."""
@@ -457,12 +489,14 @@ def _rss(fn, what, x0, x1, x2, prm: Params, seeds, elem_base, out, stream):
     return y0, y1, y2
 
 
+@_on_input_device
 def drelu_rss(x0, x1, x2, prm: Params, seeds, elem_base: int = 0, out=None, stream=None):
     """Alg 9 (RSS DReLU), three parties in one fused kernel: returns (y0, y1, y2), sum = DReLU(x).
     seeds carries s01, s02, s12, s012 and s2 (synth.Seeds)."""
     return _rss(lib().bc_drelu_rss, "bc_drelu_rss", x0, x1, x2, prm, seeds, elem_base, out, stream)
 
 
+@_on_input_device
 def relu_rss(x0, x1, x2, prm: Params, seeds, elem_base: int = 0, out=None, stream=None):
     """RSS ReLU [x][DReLU(x)]: returns (y0, y1, y2), sum = ReLU(x)."""
     return _rss(lib().bc_relu_rss, "bc_relu_rss", x0, x1, x2, prm, seeds, elem_base, out, stream)
@@ -474,6 +508,7 @@ TRC_ALG = {"secureml": 1, "aby3": 2, "det": 4}
 MUL_ORDER = {"mul_then_trc": 0, "trc_then_mul": 1}
 
 
+@_on_input_device
 def trc_aby3(x0, x1, ell: int, k: int, seeds, elem_base: int = 0, q: int = 0, rounds: int = 20, out=None,
              stream=None):
     """Alg 2 (ABY3) for both parties: returns (y0, y1), y0 + y1 = trc(x, k) (probabilistic)."""
@@ -484,6 +519,7 @@ def trc_aby3(x0, x1, ell: int, k: int, seeds, elem_base: int = 0, q: int = 0, ro
     return y0, y1
 
 
+@_on_input_device
 def trc_count(alg: str, x, ell: int, k: int, m_base: int = 0, m_count: int | None = None, counts=None, stream=None):
     """Exact e1 counting: counts[i] += (#exact, #e0, #e1) over masks [m_base, m_base + m_count)."""
     m_count = (1 << ell) if m_count is None else m_count
@@ -493,6 +529,7 @@ def trc_count(alg: str, x, ell: int, k: int, m_base: int = 0, m_count: int | Non
     return counts
 
 
+@_on_input_device
 def mul_trc(order: str, alg: str, x0, x1, y0, y1, ell: int, f: int, seeds, elem_base: int = 0, rounds: int = 20,
             out=None, stream=None):
     """Fixed-point product x y / 2^f in the given order (Alg 3 = "trc_then_mul"): returns (z0, z1)."""
