@@ -42,7 +42,7 @@ METRIC = "DReLU & ReLU elements/s at ell=64 on 1/2/4/8 B200; % of HBM roofline"
 CHACHA_ALU_OPS_PER_BLOCK = {20: 640, 12: 384, 8: 256}
 BLOCKS_PER_ELEM = {"drelu": 0.5, "relu": 1.0,   # 3/8 (tape) + 1/8 (resp) or + 5/8 (triples)
                    "drelu_rss": 1.5, "relu_rss": 1.875,  # RSS: 3/8 (tape) + 9/8 (preprocessing) (+ 3/8 ReLU zero share)
-                   "drelu_fp": 9.125, "relu_fp": 9.625}  # lx=31 large tape: 9 blocks + the finish streams
+                   "drelu_fp": 7.125, "relu_fp": 7.625}  # lx=31 large tape: 7 blocks + the finish streams
 BYTES_PER_ELEM = {"drelu": 32, "relu": 32, "ladder": 16,   # algorithmic HBM bytes per element
                   "drelu_rss": 48, "relu_rss": 48, "drelu_fp": 32, "relu_fp": 32}
 SM_COUNT_B200 = 148

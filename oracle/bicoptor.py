@@ -27,8 +27,8 @@ from .chacha import chacha_blocks, element_u32, element_u64, label_u64
 L_TAPEA = label_u64(b"bc2.tpa1")  # seed01: 16 B/element (compact tape, part A)
 L_TAPEB = label_u64(b"bc2.tpb1")  # seed01:  8 B/element (compact tape, part B)
 L_TAPEW = label_u64(b"bc2.tapw")   # seed01: 64 B/element (wide tape)
-L_TAPEL = label_u64(b"bc2.tpL1")   # seed01: 576 B/element (large tape, lx >= 8)
-L_FBL = label_u64(b"bc2.fbL1")     # seed01: large-tape fallback, u64 words, counter j*2^20+k
+L_TAPEL = label_u64(b"bc2.tpL2")   # seed01: 448 B/element (large tape, lx >= 8; 48-bit draws)
+L_FBL = label_u64(b"bc2.fbL2")     # seed01: large-tape fallback, u64 words, counter j*2^20+k
 L_FALLBACK = label_u64(b"bc2.fb01")  # seed01: rejection fallback, counter j*256+k
 L_RESP = label_u64(b"bc2.resp")    # seed02: [DReLU']_0, 8 B/element
 L_A02 = label_u64(b"bc2.ta02")     # seed02: [a]_0, 8 B/element
@@ -216,27 +216,42 @@ def _fallback_u64(seed01: bytes, j: int, rounds: int):
 
 def _tape_large(prm: Params, seed01: bytes, j) -> dict:
     """lx >= 8 (up to 32 slots, p < 2^33; the full-precision lx = 31 regime,
-    P:195).  576 B = 9 ChaCha blocks per element at 576 j (label bc2.tpL1):
+    P:195).  448 B = 7 ChaCha blocks per element at 448 j (label bc2.tpL2):
       block 0:    32 u16 h; t = h[0] & 1; the Fisher-Yates draw of slot m
                   (m = S-1 .. 1) is h[S-m]: k_m = h mod (m+1), reject h >= floor(2^16/(m+1))(m+1);
-      blocks 1-4: 32 u64 mask draws u_m: r_m = (1 + u_m mod (p-1)) * 2^-64 mod p,
-                  reject u >= floor(2^64/(p-1))(p-1) -- multiplying by the unit 2^-64 is a
-                  bijection of Z_p^*, so r_m is still uniform on Z_p^* (the draw is the
-                  mask's Montgomery form, which is what a Montgomery multiplier consumes);
-      blocks 5-8: 32 u64 reshare draws u_m: rho_m = u_m mod p, reject u >= floor(2^64/p) p.
+      blocks 1-6: 48-bit little-endian draws in groups of 8 slots, 96 B per group g = m div 8:
+                  the mask draw u of slot m at byte 96 g + 6 (m mod 8), its reshare draw at
+                  96 g + 48 + 6 (m mod 8) (bytes counted from the start of block 1);
+                  r_m = (1 + u mod (p-1)) * 2^-64 mod p, reject u >= floor(2^48/(p-1))(p-1) --
+                  multiplying by the unit 2^-64 is a bijection of Z_p^*, so r_m is still uniform
+                  on Z_p^* (the draw is the mask's Montgomery form, which is what a Montgomery
+                  multiplier consumes); rho_m = u mod p, reject u >= floor(2^48/p) p.
+    48 bits carry a 33-bit value with a rejection probability below 2^-15 per draw; the
+    tape is 7 blocks instead of the 9 that 64-bit draws take (reading C28).
     Slots m >= S leave their draws unused.  A rejected draw -- in the order
     k_{S-1} .. k_1, then r_0, rho_0, r_1, rho_1, .., r_{S-1}, rho_{S-1} -- is replaced by the next
-    u64 of the fallback stream (its low 16 bits for a Fisher-Yates draw), repeated
-    until accepted (reading C10).  Returns r, rho as Python-int object arrays."""
+    u64 of the fallback stream (its low 16 bits for a Fisher-Yates draw, its low 48 bits for a
+    mask or reshare draw), repeated until accepted (reading C10).  Returns r, rho as Python-int
+    object arrays."""
     n, S, p = j.size, prm.slots, prm.p
-    T = element_u32(seed01, L_TAPEL, prm.rounds, j, 144)
+    T = element_u32(seed01, L_TAPEL, prm.rounds, j, 112)
     h = np.ascontiguousarray(T[:, :16]).view("<u2").reshape(n, 32).astype(np.int64)
-    U = np.ascontiguousarray(T[:, 16:]).view("<u8").reshape(n, 64)
+    D = np.ascontiguousarray(T[:, 16:]).view(np.uint8).reshape(n, 384)
+
+    def draw48(off):  # (n,) little-endian 48-bit values at byte offset off
+        v = np.zeros(n, dtype=np.uint64)
+        for b in range(6):
+            v |= D[:, off + b].astype(np.uint64) << np.uint64(8 * b)
+        return v
+
+    U = np.stack([draw48(96 * (m // 8) + 6 * (m % 8)) for m in range(32)]
+                 + [draw48(96 * (m // 8) + 48 + 6 * (m % 8)) for m in range(32)], axis=1)
     t = (h[:, 0] & 1).astype(np.uint64)
     k = np.zeros((n, S), dtype=np.int64)
     hlim = {m: (65536 // (m + 1)) * (m + 1) for m in range(1, S)}
-    rlim, plim = ((1 << 64) // (p - 1)) * (p - 1), ((1 << 64) // p) * p   # 2^64 when q | 2^64: no rejection
-    rinv = pow(2, -64, p)                                                  # 2^-64 mod p
+    rlim, plim = ((1 << 48) // (p - 1)) * (p - 1), ((1 << 48) // p) * p  # 2^48 when q | 2^48: no rejection
+    m48 = (1 << 48) - 1
+    rinv = pow(2, -64, p)                                                 # 2^-64 mod p
     r = np.empty((n, S), dtype=object)
     rho = np.empty((n, S), dtype=object)
     for row in range(n):
@@ -251,12 +266,12 @@ def _tape_large(prm: Params, seed01: bytes, j) -> dict:
             u = int(U[row, m])
             while u >= rlim:
                 fb = fb or _fallback_u64(seed01, int(j[row]), prm.rounds)
-                u = next(fb)
+                u = next(fb) & m48
             r[row, m] = (1 + u % (p - 1)) * rinv % p
             u = int(U[row, 32 + m])
             while u >= plim:
                 fb = fb or _fallback_u64(seed01, int(j[row]), prm.rounds)
-                u = next(fb)
+                u = next(fb) & m48
             rho[row, m] = u % p
     return {"t": t, "k": k, "r": r, "rho": rho}
 

@@ -192,7 +192,7 @@ constexpr int TPB_L = TPB_LARGE;
 template <int R, bool RELU, bool TRANSCRIPT>
 __global__ void __launch_bounds__(TPB_L, BC_LARGE_MINB) k_fused_l(FusedArgs a, KP kp, KPL kl, Key k01, Key k02, Key k12) {
   __shared__ uint8_t sidx[32 * TPB_L];
-  __shared__ uint32_t sstg[32 * TPB_L];
+  __shared__ uint32_t sstg[LARGE_STG_ROWS * TPB_L];
   __shared__ uint32_t magic[33], hlim[33];
   large_tables(magic, hlim);
   __syncthreads();

@@ -125,9 +125,9 @@ KPL make_kpl(const bc_params* prm) {
   k.pinv = inv;
   k.mu_p = ~0ull / p;
   k.mu_q = ~0ull / q;
-  const u128 two64 = (u128)1 << 64;
-  const u128 pl = two64 / p * p, ql = two64 / q * q;
-  k.plim = (uint64_t)(pl - 1);  // accept u <= lim - 1; 2^64 - 1 when p | 2^64 (nothing rejects)
+  const u128 two48 = (u128)1 << 48;  // the large tape's draws are 48-bit
+  const u128 pl = two48 / p * p, ql = two48 / q * q;
+  k.plim = (uint64_t)(pl - 1);  // accept u <= lim - 1; 2^48 - 1 when q | 2^48 (nothing rejects)
   k.qlim = (uint64_t)(ql - 1);
   k.wm32 = (uint32_t)((1ull << prm->w) - 1ull);
   k.two_w = (1ull << prm->w) % p;

@@ -2,12 +2,12 @@
 // ladder slots, p < 2^33).  Full precision lx = 31, f = 0 without key bits is
 // the paper's "31 * 31 ~ 1,000 bits" regime (Table 1).
 //
-// Per element: 9 ChaCha blocks from seed01 (large):
+// Per element: 7 ChaCha blocks from seed01 (large):
 //   block 0     t and the Fisher-Yates draws (u16, rejection),
-//   blocks 1-4  mask draws (u64 -> rM = 1 + u mod (p-1), rejection); the mask
-//               is r_m = rM 2^-64 mod p, i.e. rM is its Montgomery form,
-//   blocks 5-8  reshare draws rho_m (u64 -> u mod p, rejection),
-// streamed in (r, rho) block pairs so at most 32 keystream words are live.
+//   blocks 1-6  48-bit draws, 96 B per group of 8 slots: 8 masks (u -> rM = 1 +
+//               u mod (p-1), rejection; the mask is r_m = rM 2^-64 mod p, i.e. rM
+//               is its Montgomery form), then 8 reshares (u -> rho_m = u mod p),
+// streamed 3 blocks (two slot groups) at a time through shared memory.
 // Arithmetic mod p: one Montgomery product (R = 2^64) per party and slot,
 // W = REDC(v' rM) = v' r; Barrett reductions for the draws.  The permutation
 // is a byte table per thread in shared memory ([slot][thread]) and is applied
@@ -19,8 +19,10 @@
 
 namespace bc {
 
-constexpr uint64_t L_TAPEL = lbl("bc2.tpL1");  // seed01, 576 B / element (9 blocks at counter 9j + b)
-constexpr uint64_t L_FBL = lbl("bc2.fbL1");    // seed01, large-tape fallback: u64 words, counter j*2^20 + k
+constexpr uint64_t L_TAPEL = lbl("bc2.tpL2");  // seed01, 448 B / element (7 blocks at counter 7j + b)
+constexpr uint64_t L_FBL = lbl("bc2.fbL2");    // seed01, large-tape fallback: u64 words, counter j*2^20 + k
+constexpr uint32_t LARGE_STG_ROWS = 48;         // keystream words staged per thread (3 blocks)
+constexpr uint64_t DRAW48 = (1ull << 48) - 1ull;
 
 struct KPL {
   uint64_t ymask;     // 2^ell - 1
@@ -111,7 +113,7 @@ __device__ __forceinline__ uint32_t large_perm(uint64_t j, const Key& k01, const
   uint32_t t;
   {
     uint32_t B[16];
-    chacha<R>(k01, j * 9, L_TAPEL, B);
+    chacha<R>(k01, j * 7, L_TAPEL, B);
     t = B[0] & 1u;
 #pragma unroll
     for (int w = 0; w < 16; ++w) stg[w * TPB_L] = B[w];
@@ -132,29 +134,38 @@ __device__ __forceinline__ uint32_t large_perm(uint64_t j, const Key& k01, const
   return t;
 }
 
-// Mask and reshare draws of slot m (blocks 1+b and 5+b staged in stg rows 0..31):
-// rM = Montgomery form of r_m, rho = rho_m.
+// 48-bit little-endian draw at byte offset `byte` (even) of the staged words.
+template <int TPB_L>
+__device__ __forceinline__ uint64_t draw48(const uint32_t* stg, uint32_t byte) {
+  const uint32_t w = byte >> 2, sh = (byte & 3u) * 8u;  // sh is 0 or 16
+  const uint32_t a = stg[w * TPB_L], b = stg[(w + 1) * TPB_L];
+  return (uint64_t)__funnelshift_r(a, b, sh) | ((uint64_t)((b >> sh) & 0xFFFFu) << 32);
+}
+
+// Mask and reshare draws of slot m (its 16-slot pair of groups staged by
+// large_stage): rM = Montgomery form of r_m, rho = rho_m.  Group g = m / 8 holds
+// 8 mask draws then 8 reshare draws, 6 B each (96 B per group).
 template <int R, int TPB_L>
-__device__ __forceinline__ void large_draws(uint32_t m, uint32_t b, uint64_t j, const Key& k01, const KPL& kp,
+__device__ __forceinline__ void large_draws(uint32_t m, uint64_t j, const Key& k01, const KPL& kp,
                                             const uint32_t* stg, uint32_t& fbc, uint64_t& rM, uint64_t& rho) {
-  const uint32_t e = 2 * (m - 8 * b);
-  uint64_t ur = (uint64_t)stg[e * TPB_L] | ((uint64_t)stg[(e + 1) * TPB_L] << 32);
-  while (!accept64(ur, kp.qlim)) ur = fbl_word<R>(k01, j, fbc++);
-  uint64_t uq = (uint64_t)stg[(16 + e) * TPB_L] | ((uint64_t)stg[(17 + e) * TPB_L] << 32);
-  while (!accept64(uq, kp.plim)) uq = fbl_word<R>(k01, j, fbc++);
+  const uint32_t gbyte = 96u * ((m >> 3) & 1u) + 6u * (m & 7u);
+  uint64_t ur = draw48<TPB_L>(stg, gbyte);
+  while (!accept64(ur, kp.qlim)) ur = fbl_word<R>(k01, j, fbc++) & DRAW48;
+  uint64_t uq = draw48<TPB_L>(stg, gbyte + 48u);
+  while (!accept64(uq, kp.plim)) uq = fbl_word<R>(k01, j, fbc++) & DRAW48;
   rM = 1ull + barrett(ur, kp.p - 1ull, kp.mu_q);  // r_m = rM 2^-64 (Montgomery form)
   rho = barrett(uq, kp.p, kp.mu_p);               // rho_m in Z_p
 }
 
+// Blocks 1 + 3h .. 3 + 3h (slot groups 2h, 2h + 1) into staged rows 0..47.
 template <int R, int TPB_L>
-__device__ __forceinline__ void large_stage(uint32_t b, uint64_t j, const Key& k01, uint32_t* stg) {
-  // mask block 1+b -> rows 0..15, reshare block 5+b -> rows 16..31
+__device__ __forceinline__ void large_stage(uint32_t h, uint64_t j, const Key& k01, uint32_t* stg) {
 #pragma unroll 1
-  for (uint32_t h = 0; h < 2; ++h) {
+  for (uint32_t b = 0; b < 3; ++b) {
     uint32_t B[16];
-    chacha<R>(k01, j * 9 + 1 + b + 4 * h, L_TAPEL, B);
+    chacha<R>(k01, j * 7 + 1 + 3 * h + b, L_TAPEL, B);
 #pragma unroll
-    for (int w = 0; w < 16; ++w) stg[(16 * h + w) * TPB_L] = B[w];
+    for (int w = 0; w < 16; ++w) stg[(16 * b + w) * TPB_L] = B[w];
   }
 }
 
@@ -173,13 +184,13 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
   const uint64_t s0f = s0 >> kp.f, n1f = ((0ull - s1) & kp.ymask) >> kp.f;
   uint32_t z = 0;
 #pragma unroll 1
-  for (uint32_t b = 0; 8 * b < S; ++b) {
-    large_stage<R, TPB_L>(b, j, k01, stg);
-    const uint32_t mend = min(S, 8 * b + 8);
+  for (uint32_t h = 0; 16 * h < S; ++h) {
+    large_stage<R, TPB_L>(h, j, k01, stg);
+    const uint32_t mend = min(S, 16 * h + 16);
 #pragma unroll 1
-    for (uint32_t m = 8 * b; m < mend; ++m) {
+    for (uint32_t m = 16 * h; m < mend; ++m) {
       uint64_t rM, rho;
-      large_draws<R, TPB_L>(m, b, j, k01, kp, stg, fbc, rM, rho);
+      large_draws<R, TPB_L>(m, j, k01, kp, stg, fbc, rM, rho);
       uint64_t c, d;
       slot_values(s0f, n1f, idx[m * TPB_L], kp, c, d);                // v'_{Pi(m)} of each party
       uint64_t W0 = mont(c, rM, kp) + rho;                           // steps 7-8, P0: v'r + rho
@@ -212,13 +223,13 @@ __device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, con
   const uint64_t sf = (PARTY == 0 ? s : (0ull - s) & kp.ymask) >> kp.f;
   uint32_t hib = 0;
 #pragma unroll 1
-  for (uint32_t b = 0; 8 * b < S; ++b) {
-    large_stage<R, TPB_L>(b, j, k01, stg);
-    const uint32_t mend = min(S, 8 * b + 8);
+  for (uint32_t h = 0; 16 * h < S; ++h) {
+    large_stage<R, TPB_L>(h, j, k01, stg);
+    const uint32_t mend = min(S, 16 * h + 16);
 #pragma unroll 1
-    for (uint32_t m = 8 * b; m < mend; ++m) {
+    for (uint32_t m = 16 * h; m < mend; ++m) {
       uint64_t rM, rho;
-      large_draws<R, TPB_L>(m, b, j, k01, kp, stg, fbc, rM, rho);
+      large_draws<R, TPB_L>(m, j, k01, kp, stg, fbc, rM, rho);
       uint64_t c, d;
       slot_values(sf, sf, idx[m * TPB_L], kp, c, d);                  // one of the two is this party's
       uint64_t W = PARTY == 0 ? mont(c, rM, kp) + rho : mont(d, rM, kp) + (kp.p - rho);  // steps 7-8

@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(TPB, 2) k_send_w(SendArgs a, KP kp, Key k01, K
 template <int R, int PARTY, bool RELU>
 __global__ void __launch_bounds__(TPB_LARGE) k_send_l(SendArgs a, KP kp, KPL kl, Key k01, Key ktr) {
   __shared__ uint8_t sidx[32 * TPB_LARGE];
-  __shared__ uint32_t sstg[32 * TPB_LARGE];
+  __shared__ uint32_t sstg[LARGE_STG_ROWS * TPB_LARGE];
   __shared__ uint32_t magic[33], hlim[33];
   large_tables(magic, hlim);
   __syncthreads();

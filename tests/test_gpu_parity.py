@@ -438,14 +438,18 @@ def test_large_parity_with_transcript(api, kw, fn):
 
 
 def test_large_fallback_elements(api):
-    """Elements whose Fisher-Yates draws reject (~0.35 % at 32 slots) take the
-    fallback stream; they must match the oracle, messages included."""
-    from test_oracle_fullprec import _raw_perm_rejects
+    """Elements whose Fisher-Yates draws reject (~0.35 % at 32 slots) or whose
+    48-bit mask / reshare draws reject (< 2^-15 per draw) take the fallback
+    stream; they must match the oracle, messages included."""
+    from test_oracle_fullprec import _raw_draw_rejects, _raw_perm_rejects
     kw = LARGE_PARAMS[0]
     oprm, prm = B.Params(**kw), api.Params(**kw)
     rej, _ = _raw_perm_rejects(oprm, np.arange(8000, dtype=np.uint64))
-    rows = np.nonzero(rej)[0][:8]
+    rows = list(np.nonzero(rej)[0][:8])
     assert len(rows) >= 5
+    drej = np.nonzero(_raw_draw_rejects(oprm, np.arange(3000, dtype=np.uint64)))[0]  # a 48-bit draw rejects
+    assert len(drej) >= 1
+    rows += list(drej[:3])
     for r in rows:
         base = int(r) - int(r) % 8
         x, x0, x1 = synth.shares(16, 64, 31, 0, "D2", run=int(r))

@@ -18,13 +18,33 @@ SEEDS = synth.seeds(0)
 
 def _raw_perm_rejects(prm, j):
     """Rows with a rejected Fisher-Yates draw, from the raw keystream."""
-    T = element_u32(SEEDS.s01, B.L_TAPEL, prm.rounds, j, 144)
+    T = element_u32(SEEDS.s01, B.L_TAPEL, prm.rounds, j, 112)
     h = np.ascontiguousarray(T[:, :16]).view("<u2").reshape(-1, 32).astype(np.int64)
     S = prm.slots
     rej = np.zeros(j.size, dtype=bool)
     for m in range(1, S):
         rej |= h[:, S - m] >= (65536 // (m + 1)) * (m + 1)
     return rej, h
+
+
+def _raw_draws(prm, j):
+    """The 48-bit mask and reshare draws of slots 0..31 straight from the keystream
+    bytes (tape layout of DESIGN.md sec. 4, written out independently of the oracle)."""
+    T = element_u32(SEEDS.s01, B.L_TAPEL, prm.rounds, j, 112)
+    D = np.ascontiguousarray(T[:, 16:]).view(np.uint8).reshape(-1, 384).astype(object)
+    r = np.array([[sum(int(D[i, 96 * (m // 8) + 6 * (m % 8) + b]) << (8 * b) for b in range(6)) for m in range(32)]
+                  for i in range(j.size)], dtype=object)
+    rho = np.array([[sum(int(D[i, 96 * (m // 8) + 48 + 6 * (m % 8) + b]) << (8 * b) for b in range(6))
+                     for m in range(32)] for i in range(j.size)], dtype=object)
+    return r, rho
+
+
+def _raw_draw_rejects(prm, j):
+    """Rows with a rejected 48-bit mask or reshare draw among the first S slots."""
+    r, rho = _raw_draws(prm, j)
+    p, S = prm.p, prm.slots
+    rl, pl = ((1 << 48) // (p - 1)) * (p - 1), ((1 << 48) // p) * p
+    return np.array([any(r[i, m] >= rl or rho[i, m] >= pl for m in range(S)) for i in range(j.size)])
 
 
 def test_params_full_precision():
@@ -70,6 +90,27 @@ def test_large_tape_invariants_and_fallback():
     for m in range(1, S):
         assert np.array_equal(tp["k"][direct, m], h[direct, S - m] % (m + 1))
     assert np.all(tp["k"][rej] <= np.arange(S))
+    # the 48-bit draws: r_m (Montgomery form) and rho_m from the raw bytes where nothing rejects
+    jd = np.arange(64, dtype=np.uint64)
+    ur, uq = _raw_draws(prm, jd)
+    tpd = B.tape(prm, SEEDS.s01, jd)
+    rinv = pow(2, -64, p)
+    for i in np.nonzero(~_raw_draw_rejects(prm, jd))[0][:40]:
+        for m in range(S):
+            assert tpd["r"][i, m] == (1 + ur[i, m] % (p - 1)) * rinv % p
+            assert tpd["rho"][i, m] == uq[i, m] % p
+
+
+def test_large_tape_48bit_draw_rejections():
+    """A 48-bit draw rejects with probability < 2^-15 (p - 1, p ~ 2^32): the rows that
+    reject are found from the raw bytes, and the oracle's values there still lie in
+    range (they came from the fallback stream)."""
+    prm = B.Params(ell=64, lx=31, f=0, rounds=8)
+    j = np.arange(3000, dtype=np.uint64)
+    rej = _raw_draw_rejects(prm, j)
+    assert 1 <= rej.sum() <= 15                      # expected 3000 * 64 * ~2^-16.5 ~ 2.1
+    tp = B.tape(prm, SEEDS.s01, j[rej])
+    assert all(1 <= int(v) < prm.p for v in np.ravel(tp["r"])) and all(0 <= int(v) < prm.p for v in np.ravel(tp["rho"]))
 
 
 @pytest.mark.parametrize("ell,lx,f", [(24, 10, 0), (20, 8, 1)])
