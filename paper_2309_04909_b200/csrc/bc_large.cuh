@@ -149,10 +149,14 @@ template <int R, int TPB_L>
 __device__ __forceinline__ void large_draws(uint32_t m, uint64_t j, const Key& k01, const KPL& kp,
                                             const uint32_t* stg, uint32_t& fbc, uint64_t& rM, uint64_t& rho) {
   const uint32_t gbyte = 96u * ((m >> 3) & 1u) + 6u * (m & 7u);
+  // a draw can reject only if its high 16 bits reach the limit's (probability ~2^-16):
+  // one 32-bit compare on the common path, the exact test behind it
   uint64_t ur = draw48<TPB_L>(stg, gbyte);
-  while (!accept64(ur, kp.qlim)) ur = fbl_word<R>(k01, j, fbc++) & DRAW48;
+  if (__builtin_expect((uint32_t)(ur >> 32) >= (uint32_t)(kp.qlim >> 32), 0))
+    while (!accept64(ur, kp.qlim)) ur = fbl_word<R>(k01, j, fbc++) & DRAW48;
   uint64_t uq = draw48<TPB_L>(stg, gbyte + 48u);
-  while (!accept64(uq, kp.plim)) uq = fbl_word<R>(k01, j, fbc++) & DRAW48;
+  if (__builtin_expect((uint32_t)(uq >> 32) >= (uint32_t)(kp.plim >> 32), 0))
+    while (!accept64(uq, kp.plim)) uq = fbl_word<R>(k01, j, fbc++) & DRAW48;
   rM = 1ull + barrett(ur, kp.p - 1ull, kp.mu_q);  // r_m = rM 2^-64 (Montgomery form)
   rho = barrett(uq, kp.p, kp.mu_p);               // rho_m in Z_p
 }
@@ -196,13 +200,19 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
       uint64_t W0 = mont(c, rM, kp) + rho;                           // steps 7-8, P0: v'r + rho
       W0 = W0 >= kp.p ? W0 - kp.p : W0;
       uint64_t W1 = mont(d, rM, kp) + (kp.p - rho);                  //            P1: v'r - rho
-      W1 = W1 >= kp.p ? W1 - kp.p : W1;
       if (TRANSCRIPT) {
+        W1 = W1 >= kp.p ? W1 - kp.p : W1;
         w0[m] = W0;
         w1[m] = W1;
+        const uint64_t sum = W0 + W1;                                // step 9 (P2): w_m = 0 mod p?
+        z |= (sum == 0 || sum == kp.p) ? 1u : 0u;
+      } else {
+        // P0's wire value W0 in [0, p) and P1's message as its congruent representative
+        // in (0, 2p] (as the compact path, BC_MATERIALIZE=1): W0 + W1 in (0, 3p), and
+        // w_m = 0 mod p iff the sum is p or 2p.  rho enters through W0's reduction.
+        const uint64_t sum = W0 + W1;
+        z |= (sum == kp.p || sum == 2 * kp.p) ? 1u : 0u;
       }
-      const uint64_t sum = W0 + W1;                                  // step 9 (P2): w_m = 0 mod p?
-      z |= (sum == 0 || sum == kp.p) ? 1u : 0u;
     }
   }
   return z | (t << 1);
