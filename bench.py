@@ -127,7 +127,7 @@ def oracle_rate(fn: str, rounds: int, budget_s: float = 12.0):
                               f"({fn}, D2), oracle.bicoptor.{fn} (numpy)")
 
 
-def run_reference(a, budget_s: float = 120.0):
+def run_reference(a, budget_s: float | None = None):
     """The reference arm for this tier: the oracle, as it stands, on the host
     cores (tier framing 4).  One process pool; each step is a bounded sample of
     the bench workload (per worker a slice of m elements at distinct global
@@ -137,6 +137,8 @@ def run_reference(a, budget_s: float = 120.0):
         return
     import concurrent.futures as cf
     cores = min(os.cpu_count() or 1, 16)
+    if budget_s is None:  # BENCH_REF_BUDGET_S: tests shrink the run (default ~2 minutes of CPU work)
+        budget_s = float(os.environ.get("BENCH_REF_BUDGET_S", "120"))
     cnt, dt = _oracle_chunk((0, 4096, "drelu", a.rounds))      # one core, calibration
     per_core = cnt / dt
     total = max(a.warmup, 3) + a.steps
