@@ -149,21 +149,43 @@ def test_sharding_is_bit_identical(api):
             assert torch.equal(s0, y0[a:b]) and torch.equal(s1, y1[a:b])
 
 
-def test_config1_exhaustive_ell16(api):
-    """Config 1: DReLU at ell=16, all key bits (lx=7, f=0), every x in Z_{2^16}
-    once (masks from the synthetic generator): bit-exact against the oracle for
-    all 65536 inputs; reconstructed sign exact on the band."""
-    kw = dict(ell=16, lx=7, f=0, mode="guard", rounds=20)
-    oprm = B.Params(**kw)
+@pytest.mark.parametrize("mode,f", [("guard", 0), ("literal", 0), ("guard", 1)])
+def test_config1_exhaustive_ell16(api, mode, f):
+    """Config 1: DReLU at ell=16, all key bits (lx=7), every x in Z_{2^16} once
+    (masks from the synthetic generator), guard and literal mode and the f=1
+    variant.  Seed set 0: bit-exact against the oracle for all
+    65536 inputs.  64 seed sets: the reconstructed sign is exact on every in-band
+    x (guard), or wrong only on the analytic false-positive set (literal, reading
+    C6), and oracle parity holds on a sample of each set."""
+    kw = dict(ell=16, lx=7, f=f, mode=mode, rounds=20)
+    oprm, prm = B.Params(**kw), api.Params(**kw)
     x = np.arange(1 << 16, dtype=np.uint64)
-    x0, x1 = synth.share(x, 16)
     j = np.arange(x.size, dtype=np.uint64)
-    ref = B.drelu(oprm, x0, x1, j, SEEDS)
-    y0, y1 = api.drelu(dev(x0), dev(x1), api.Params(**kw), SEEDS)
-    assert np.array_equal(host(y0), ref["y0"]) and np.array_equal(host(y1), ref["y1"])
-    y = (host(y0) + host(y1)) & np.uint64(0xFFFF)
-    s, valid = band_sign(x, 16, 7, 0)
-    assert valid.sum() == 254 and np.array_equal(y[valid], s[valid])
+    s, valid = band_sign(x, 16, 7, f)
+    assert valid.sum() == 2 * ((1 << (f + 7)) - (1 << f))
+    from test_oracle_drelu import _literal_fp_set
+    fp = _literal_fp_set(16, 7, f) if mode == "literal" else set()
+    xi = np.minimum(x, np.uint64(1 << 16) - x)
+    allowed = valid & np.isin(xi, np.array(sorted(fp), dtype=np.uint64))
+    wrong = np.zeros(x.size, dtype=np.int64)
+    rng = np.random.default_rng(21)
+    for run in range(64):
+        sd = synth.seeds(run)
+        x0, x1 = synth.share(x, 16, run=run)
+        y0, y1 = api.drelu(dev(x0), dev(x1), prm, sd)
+        g0, g1 = host(y0), host(y1)
+        if run == 0:
+            ref = B.drelu(oprm, x0, x1, j, sd)
+            assert np.array_equal(g0, ref["y0"]) and np.array_equal(g1, ref["y1"])
+        else:
+            idx = np.sort(rng.choice(x.size, 256, replace=False)).astype(np.uint64)
+            ref = B.drelu(oprm, x0[idx], x1[idx], idx, sd)
+            assert np.array_equal(g0[idx], ref["y0"]) and np.array_equal(g1[idx], ref["y1"]), run
+        y = (g0 + g1) & np.uint64(0xFFFF)
+        wrong += (valid & (y != s)).astype(np.int64)
+    assert not np.any(wrong[valid & ~allowed]), "misclassified outside the analytic set"
+    if mode == "literal":
+        assert wrong[allowed].sum() > 0      # the literal domain does err there (C6)
 
 
 def test_config1_all_masks_sign(api):
