@@ -83,3 +83,54 @@ def test_random_parameters(api, case):
     ref = B.drelu(o, x0, x1, j, SEEDS)
     assert np.array_equal(host(api.drelu_finish(0, tb0, r0, prm, n, None, base)), ref["y0"])
     assert np.array_equal(host(api.drelu_finish(1, tb1, r1, prm, n, None, base)), ref["y1"])
+
+
+@pytest.mark.parametrize("case", list(range(40)))
+def test_random_widened_rows(api, case):
+    """The widened rows under random parameters: RSS DReLU / ReLU (compact tape:
+    lx = 7 guard, random ell and f), the Bicoptor-1 comparison (slots <= 8), the
+    ABY3 truncation and the two fixed-point product orders."""
+    from oracle import bicoptor1 as B1, rss, trunc
+    rng = np.random.default_rng(5000 + case)
+    n = int(rng.integers(1, 2000))
+    base = int(rng.integers(0, 1 << 40)) // 8 * 8
+    j = np.arange(n, dtype=np.uint64) + np.uint64(base)
+    rounds = int(rng.choice([8, 12, 20]))
+    ell = int(rng.integers(16, 65))
+    f = int(rng.integers(0, ell - 15 + 1))
+    o = B.Params(ell=ell, lx=7, f=f, mode="guard", rounds=rounds)
+    prm = api.Params(ell=ell, lx=7, f=f, mode="guard", rounds=rounds)
+    x = synth.plaintext(n, ell, 7, f, ["D1", "D2"][rng.integers(2)], run=case)
+    xs = synth.rss_share(x, ell, run=case)
+    fn = ["drelu_rss", "relu_rss"][case % 2]
+    ys = getattr(api, fn)(*(dev(v) for v in xs), prm, SEEDS, elem_base=base)
+    ref = getattr(rss, fn)(o, *xs, j, SEEDS)
+    for k in range(3):
+        assert np.array_equal(host(ys[k]), ref["y"][k]), (fn, ell, f, n, base, k)
+    # Bicoptor-1 on random small ladders
+    lx = int(rng.integers(2, 8))
+    f1 = int(rng.integers(0, 64 - 2 * lx))
+    o1 = B.Params(ell=64, lx=lx, f=f1, mode="guard", rounds=rounds)
+    x, x0, x1 = synth.shares(n, 64, lx, f1, "D1", run=case)
+    y0, y1 = api.drelu_b1(dev(x0), dev(x1), api.Params(ell=64, lx=lx, f=f1, mode="guard", rounds=rounds), SEEDS,
+                          elem_base=base)
+    r1 = B1.drelu1(o1, x0, x1, j, SEEDS)
+    assert np.array_equal(host(y0), r1["y0"]) and np.array_equal(host(y1), r1["y1"]), ("b1", lx, f1)
+    # truncation: ABY3 (Alg 2) and the product orders (Alg 3 vs mult-then-trc)
+    k = int(rng.integers(0, ell - 6))
+    q = int(rng.integers(2))
+    x, x0, x1 = synth.shares(n, ell, 5, min(k, ell - 7), "D1", run=case + 1)
+    t0, t1 = api.trc_aby3(dev(x0), dev(x1), ell, k, SEEDS, elem_base=base, q=q, rounds=rounds)
+    e0, e1 = trunc.trc_aby3(x0, x1, trunc.aby3_pre(ell, k, j, SEEDS, rounds, q), k, ell)
+    assert np.array_equal(host(t0), e0) and np.array_equal(host(t1), e1), ("aby3", ell, k, q)
+    order = ["mul_then_trc", "trc_then_mul"][rng.integers(2)]
+    alg = ["secureml", "aby3"][rng.integers(2)]
+    ff = int(rng.integers(1, max(2, ell // 3)))
+    X = synth.plaintext(n, ell, 5, min(ff, ell - 7), "D1", run=case + 2)
+    Y = synth.plaintext(n, ell, 5, min(ff, ell - 7), "D1", run=case + 3)
+    a0, a1 = synth.share(X, ell, run=case + 4)
+    b0, b1 = synth.share(Y, ell, run=case + 5)
+    z0, z1 = api.mul_trc(order, alg, dev(a0), dev(a1), dev(b0), dev(b1), ell, ff, SEEDS, elem_base=base,
+                         rounds=rounds)
+    ref = getattr(trunc, order)(alg, a0, a1, b0, b1, ff, ell, j, SEEDS, rounds)
+    assert np.array_equal(host(z0), ref[0]) and np.array_equal(host(z1), ref[1]), (order, alg, ell, ff)
