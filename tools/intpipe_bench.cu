@@ -103,6 +103,69 @@ __global__ void k_mix_lop_viadd(uint32_t* out, uint32_t seed, uint32_t k) {
   if (acc == 0x12345678u) out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
+__global__ void k_imadwide(uint32_t* out, uint32_t seed, uint32_t k) {
+  uint32_t v[CH];
+  uint64_t w[CH];
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) { v[c] = seed + c * 0x9E3779B9u + threadIdx.x; w[c] = v[c]; }
+  for (int i = 0; i < ITERS; ++i) {
+    _Pragma("unroll") for (int c = 0; c < CH; ++c)
+      asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(w[c]) : "r"(v[c]), "r"(k));
+  }
+  uint32_t acc = 0;
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) acc ^= (uint32_t)w[c] ^ (uint32_t)(w[c] >> 32);
+  if (acc == 0x12345678u) out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+__global__ void k_mix_lop_imadwide(uint32_t* out, uint32_t seed, uint32_t k) {
+  uint32_t v[CH];
+  uint64_t w[CH];
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) { v[c] = seed + c * 0x9E3779B9u + threadIdx.x; w[c] = v[c] ^ 0x55u; }
+  for (int i = 0; i < ITERS; ++i) {
+    _Pragma("unroll") for (int c = 0; c < CH; ++c) {
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(v[c]) : "r"(k), "r"(seed));
+      asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(w[c]) : "r"(seed), "r"(k));
+    }
+  }
+  uint32_t acc = 0;
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) acc ^= v[c] ^ (uint32_t)w[c] ^ (uint32_t)(w[c] >> 32);
+  if (acc == 0x12345678u) out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+__global__ void k_mix_xsa_wide(uint32_t* out, uint32_t seed, uint32_t k) {
+  // the ChaCha-like step of k_mix_xsa with the rotate on the FMA pipe:
+  // x ^= y; t = x * 2^7 (64-bit); x = lo(t) + hi(t); y += x
+  uint32_t v[CH], w[CH];
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) { v[c] = seed + c * 0x9E3779B9u + threadIdx.x; w[c] = v[c] ^ 0x55u; }
+  for (int i = 0; i < ITERS; ++i) {
+    _Pragma("unroll") for (int c = 0; c < CH; ++c) {
+      asm volatile("xor.b32 %0, %0, %1;" : "+r"(v[c]) : "r"(w[c]));
+      asm volatile("{ .reg .b64 t; .reg .b32 lo, hi; mul.wide.u32 t, %0, 128; mov.b64 {lo, hi}, t; add.u32 %0, lo, hi; }"
+                   : "+r"(v[c]));
+      asm volatile("add.u32 %0, %0, %1;" : "+r"(w[c]) : "r"(v[c]));
+    }
+  }
+  uint32_t acc = 0;
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) acc ^= v[c] ^ w[c];
+  if (acc == 0x12345678u) out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+__global__ void k_mix_xsa_half(uint32_t* out, uint32_t seed, uint32_t k) {
+  // half the chains rotate with SHF (ALU), half with the 64-bit multiply (FMA pipe)
+  uint32_t v[CH], w[CH];
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) { v[c] = seed + c * 0x9E3779B9u + threadIdx.x; w[c] = v[c] ^ 0x55u; }
+  for (int i = 0; i < ITERS; ++i) {
+    _Pragma("unroll") for (int c = 0; c < CH; ++c) {
+      asm volatile("xor.b32 %0, %0, %1;" : "+r"(v[c]) : "r"(w[c]));
+      if (c & 1)
+        asm volatile("{ .reg .b64 t; .reg .b32 lo, hi; mul.wide.u32 t, %0, 128; mov.b64 {lo, hi}, t; add.u32 %0, lo, hi; }"
+                     : "+r"(v[c]));
+      else
+        asm volatile("shf.l.wrap.b32 %0, %0, %0, 7;" : "+r"(v[c]));
+      asm volatile("add.u32 %0, %0, %1;" : "+r"(w[c]) : "r"(v[c]));
+    }
+  }
+  uint32_t acc = 0;
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) acc ^= v[c] ^ w[c];
+  if (acc == 0x12345678u) out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
 template <typename K>
 double rate(K kern, int ops_per_iter, int blocks, int threads) {
   uint32_t* out;
@@ -141,6 +204,11 @@ int main() {
   printf(", \"lop3+imad_tops\": %.3f", rate(k_mix_lop_imad, 2, blocks, threads));
   printf(", \"lop3+imadhi_tops\": %.3f", rate(k_mix_lop_imadhi, 2, blocks, threads));
   printf(", \"xor_rot_add_tops\": %.3f", rate(k_mix_xsa, 3, blocks, threads));
+  printf(", \"imad_wide_tops\": %.3f", rate(k_imadwide, 1, blocks, threads));
+  printf(", \"lop3+imadwide_tops\": %.3f", rate(k_mix_lop_imadwide, 2, blocks, threads));
+  // the two ChaCha-like variants in the same unit as xor_rot_add: 3 algorithmic ops per step
+  printf(", \"xor_rotwide_add_tops\": %.3f", rate(k_mix_xsa_wide, 3, blocks, threads));
+  printf(", \"xor_rot_add_half_wide_tops\": %.3f", rate(k_mix_xsa_half, 3, blocks, threads));
   printf("}\n");
   return 0;
 }
