@@ -260,19 +260,15 @@ def run_cuda(a):
     torch.cuda.set_device(dev)
     api.lib()
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
+    from paper_2309_04909_b200 import shard
+
+    barrier = shard.barrier
 
     def max_over_ranks(v: float) -> float:
-        if world == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device="cpu" if share else dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return shard.max_over_ranks(v, "cpu" if share else dev)
 
     n = a.n
-    base = rank * n
+    base = shard.elem_base(rank, n)
     seeds = synth.seeds(0)
     prm = api.Params(ell=ELL, lx=LX, f=F, mode=MODE, rounds=a.rounds)
     x = synth.plaintext(n, ELL, LX, F, "D2", run=rank)
