@@ -447,6 +447,7 @@ def run_cuda(a):
             v_fp = world * n / (ms_fp * 1e-3)
             fp[name] = {"value": v_fp, "unit": "elements/s", "ms_per_step": ms_fp,
                         "roofline": roofline(name, v_fp, ms_fp)}
+        fp["party_chain_1gpu"] = party_chain(api, pfp, seeds, x0, x1, base, dev, stream, timed, world, n)
         fp["note"] = "lx=31, f=0, guard (w=32, p=2^32+15, 32 slots): the paper's full 5+26 precision, same batch"
         line["full_precision"] = fp
         # ---- Bicoptor-1 as the paper describes it (NEXT #4), same batch and seeds ----
@@ -478,8 +479,8 @@ def party_chain(api, prm, seeds, x0, x1, base, dev, stream, timed, world, n):
     kernels back to back on one GPU (P0 send, P1 send, P2 helper, P0 finish, P1
     finish), i.e. every party's PRG and arithmetic, no sharing."""
     import torch
-    lo0, hi0, tb0 = api.msg_buffers(n, dev)
-    lo1, hi1, tb1 = api.msg_buffers(n, dev)
+    lo0, hi0, tb0 = api.msg_buffers(n, dev, prm)
+    lo1, hi1, tb1 = api.msg_buffers(n, dev, prm)
     r1 = torch.empty(n, dtype=torch.int64, device=dev)
     ya, yb = torch.empty_like(r1), torch.empty_like(r1)
     d0, d1, e, c1 = (torch.empty_like(r1) for _ in range(4))
@@ -499,9 +500,10 @@ def party_chain(api, prm, seeds, x0, x1, base, dev, stream, timed, world, n):
         api.relu_finish(1, x1, tb1, d1, d0, e, c1, prm, seeds.s12, base, out=yb, stream=stream)
 
     res = {}
+    reps = 50 if prm.lx <= 7 else 5
     for name, fn in (("drelu", drelu_chain), ("relu", relu_chain)):
-        t_ms, _, _ = timed(fn, 50, 3)
-        ms = t_ms / 50
+        t_ms, _, _ = timed(fn, reps, 3)
+        ms = t_ms / reps
         res[name] = {"value": world * n / (ms * 1e-3), "unit": "elements/s", "ms_per_step": ms, "launches_per_step": 5}
     # each party's kernels alone (inputs left in place by the chains above): what one GPU per party
     # would run per step in config 4.  The rate of a P0/P1/P2 triple on three GPUs is bounded by the
@@ -526,12 +528,17 @@ def party_chain(api, prm, seeds, x0, x1, base, dev, stream, timed, world, n):
                                                     out=(e, c1), stream=stream)})):
         ms_p = {}
         for pty, fn in calls.items():
-            t_p, _, _ = timed(fn, 30, 3)
-            ms_p[pty] = t_p / 30
+            t_p, _, _ = timed(fn, 3 * reps // 5, 3)
+            ms_p[pty] = t_p / (3 * reps // 5)
         per[name] = {"ms_per_party": ms_p,
                      "projected_triple_elements_per_s": n / (max(ms_p.values()) * 1e-3)}
     res["per_party"] = per
     res["note"] = "P0,P1 send + P2 helper + P0,P1 finish back to back on one GPU: all parties' work, nothing shared"
+    if prm.lx > 7:  # large tape: uint32 planes, 33 S bits (guard, p > 2^32)
+        S = prm.lx + 1
+        res["wire_bytes_per_elem"] = {"P0->P2": 4 * S + (4 if prm.mode == "guard" else 0),
+                                      "paper_one_pass_bits_per_party": S * S}
+        return res
     # the messages these kernels exchange, per element (DESIGN.md sec. 4 wire format) vs Table 1
     slots, pbits = LX + 1, 9 if MODE == "guard" else 8
     res["wire_bytes_per_elem"] = {

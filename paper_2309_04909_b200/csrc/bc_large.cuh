@@ -251,18 +251,4 @@ __device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, con
   return (uint64_t)hib | ((uint64_t)t << 32);
 }
 
-// Step 9 on the wire values of one element: any (W0_m + W1_m) mod p == 0.
-__device__ __forceinline__ uint32_t zero_test_large(const uint32_t* lo0, uint32_t hi0, const uint32_t* lo1,
-                                                    uint32_t hi1, const KPL& kp) {
-  uint32_t z = 0;
-#pragma unroll 1
-  for (uint32_t m = 0; m < kp.S; ++m) {
-    const uint64_t W0 = (uint64_t)__ldg(lo0 + m) | ((uint64_t)((hi0 >> m) & 1u) << 32);
-    const uint64_t W1 = (uint64_t)__ldg(lo1 + m) | ((uint64_t)((hi1 >> m) & 1u) << 32);
-    const uint64_t sum = W0 + W1;
-    z |= (sum == 0 || sum == kp.p) ? 1u : 0u;
-  }
-  return z;
-}
-
 }  // namespace bc
