@@ -61,6 +61,10 @@ struct TapeC {
 
 // x / 257 for any 32-bit x: floor(x * (2^40 + 1)/257 / 2^40) (exact).
 __device__ __forceinline__ uint32_t div257(uint32_t x) { return __umulhi(x, 0xFF00FF01u) >> 8; }
+// x / 257 for x < 2^24 with one IMAD.HI and no shift: umulhi(x, ceil(2^32 / 257)); the
+// magic overshoots 2^32/257 by 1/8, harmless while x / 8 / 2^32 < 1/257, i.e. x < 2^27
+// (tests/test_kernel_arith.py, exhaustive below 2^24).
+__device__ __forceinline__ uint32_t div257s(uint32_t x) { return __umulhi(x, 0xFF0100u); }
 
 struct FbC {  // the draws a compact tape can reject, passed by value (registers, not local memory)
   uint32_t idx, w0, w1, w2;
@@ -89,8 +93,7 @@ __device__ __forceinline__ void decode_c(uint32_t T0, uint32_t T1, uint32_t T2, 
                                          const uint32_t* sB, TapeC& tp) {
   tp.t = T0 >> 31;
   uint32_t idx = T0 & 0x7FFFFFFFu;
-  if (__builtin_expect((idx >= PERM_LIMIT_8) | (w0 >= RHO_WORD_LIMIT) | (w1 >= RHO_WORD_LIMIT) |
-                       (w2 >= RHO_WORD_LIMIT), 0)) {
+  if (__builtin_expect((idx >= PERM_LIMIT_8) | (max(w0, max(w1, w2)) >= RHO_WORD_LIMIT), 0)) {
     const FbC d = fallback_c<R>(FbC{idx, w0, w1, w2}, j, k01);
     idx = d.idx; w0 = d.w0; w1 = d.w1; w2 = d.w2;
   }
@@ -106,10 +109,10 @@ __device__ __forceinline__ void decode_c(uint32_t T0, uint32_t T1, uint32_t T2, 
   const uint32_t w[3] = {w0, w1, w2};
 #pragma unroll
   for (int k = 0; k < 3; ++k) {  // base-257 digits, least significant first
-    const uint32_t q1 = div257(w[k]), q2 = div257(q1);
+    const uint32_t q1 = div257(w[k]), q2 = div257s(q1);  // q1 < 2^24, q2 < 2^16
     tp.rho[3 * k] = w[k] - 257u * q1;
     tp.rho[3 * k + 1] = q1 - 257u * q2;
-    if (k < 2) tp.rho[3 * k + 2] = q2 - 257u * div257(q2);
+    if (k < 2) tp.rho[3 * k + 2] = q2 - 257u * div257s(q2);
   }
 }
 

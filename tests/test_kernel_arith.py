@@ -14,6 +14,15 @@ def umulhi32(a, b):
 
 # ---- compact path (csrc/bc_compact.cuh) -------------------------------------------------
 
+def test_div257s_exact_below_2pow24():
+    """div257s(x) = umulhi(x, 0xFF0100) == x // 257 for every x < 2^24 (the
+    kernel applies it to quotients q1 = w // 257 < 2^24 and q2 < 2^16)."""
+    x = np.arange(1 << 24, dtype=np.uint64)
+    assert np.array_equal((x * np.uint64(0xFF0100)) >> np.uint64(32), x // np.uint64(257))
+    x = np.array([(1 << 27) - 1, (1 << 27) - 257, (1 << 26) + 12345], dtype=np.uint64)   # the stated bound
+    assert np.array_equal((x * np.uint64(0xFF0100)) >> np.uint64(32), x // np.uint64(257))
+
+
 def test_div257_exact_all_u32_sample_and_edges():
     """div257(x) = umulhi(x, 0xFF00FF01) >> 8 == x // 257 for every 32-bit x
     (checked on all multiples-of-257 neighbourhoods and 2^22 random values)."""
