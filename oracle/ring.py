@@ -41,6 +41,8 @@ def neg(a, ell: int):
     """-a mod 2^ell."""
     if _is_arr(a):
         return (np.uint64(0) - a.astype(np.uint64)) & np.uint64(mask(ell))
+    if isinstance(a, np.integer):  # exact in Python ints, back to the operand's kind
+        return np.uint64((-int(a)) & mask(ell))
     return (-a) & mask(ell)
 
 
