@@ -178,11 +178,13 @@ int bc_relu_host(const uint64_t *x0, const uint64_t *x1, uint64_t *y0, uint64_t 
  * party's blinding bits tbits: uint8_t[(n+7)/8] (bit i%8 of byte i/8 = t_i),
  * kept locally for the finish phase.  (lx+1)*ceil(log2 p) bits per element:
  * 72 in guard mode, 64 literal (Table 1).
- * Large tape (lx >= 8, S = lx+1 <= 32 slots, p < 2^33): lo is
- * uint32_t[n][S] (low 32 bits of W_m) and hi is uint32_t[n] (bit m = bit 32
- * of W_m; may be NULL when p < 2^32): 33 S bits per element, 1,056 at the
- * full precision lx = 31 (the paper's "31 * 31 ~ 1,000 bits").  The
- * helper (bc_drelu_helper, bc_relu_helper[_to]) takes the same planes. */
+ * Large tape (lx >= 8, S = lx+1 <= 32 slots, p < 2^33): lo is the
+ * slot-major plane uint32_t[S][n] (lo[m n + i] = low 32 bits of element i's
+ * W_m, so a warp's stores and loads of one slot are contiguous) and hi is
+ * uint32_t[n] (bit m = bit 32 of W_m; may be NULL when p < 2^32): 33 S bits
+ * per element, 1,056 at the full precision lx = 31 (the paper's "31 * 31 ~
+ * 1,000 bits").  The helper (bc_drelu_helper, bc_relu_helper[_to])
+ * takes the same planes. */
 int bc_drelu_send(int party, const uint64_t *x, uint8_t *lo, uint8_t *hi, uint8_t *tbits,
                   size_t n, uint64_t elem_base, const bc_params *prm, const uint8_t seed01[32],
                   void *stream);

@@ -489,12 +489,13 @@ def encode_msg(W: np.ndarray):
 
 def encode_msg_large(W: np.ndarray):
     """Large-tape wire format (lx >= 8, up to 32 slots, p < 2^33):
-    low-word plane (n, S) of uint32 = W_m mod 2^32, and a high-bit plane (n,)
-    of uint32 with bit m = bit 32 of W_m.  33 S bits per element: 1,056 at the
-    paper's full precision lx = 31 ("31 * 31 ~ 1,000 bits")."""
+    slot-major low-word plane (S, n) of uint32, row m = W_m mod 2^32 of every
+    element, and a high-bit plane (n,) of uint32 with bit m = bit 32 of W_m.
+    33 S bits per element: 1,056 at the paper's full precision lx = 31
+    ("31 * 31 ~ 1,000 bits", P:195)."""
     W = np.asarray(W, dtype=np.uint64)
     n, S = W.shape
-    lo = (W & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    lo = np.ascontiguousarray((W & np.uint64(0xFFFFFFFF)).astype(np.uint32).T)
     hi = np.zeros(n, dtype=np.uint32)
     for m in range(S):
         hi |= ((W[:, m] >> np.uint64(32)) & np.uint64(1)).astype(np.uint32) << np.uint32(m)

@@ -325,18 +325,28 @@ def relu_host(hx0, hx1, hy0, hy1, prm: Params, seeds, ws, chunk: int = 1 << 20, 
 def wire_format(prm: Params) -> dict:
     """Per-element shape and dtype of the message planes to P2 (include/bicoptor.h,
     bc_drelu_send): byte planes lo (8 B) + hi (1 B) for slots <= 8, p <= 257; for
-    the large tape lo = S low words (uint32) + hi = one word of bit-32 flags.
-    "hi" is None when every W_m fits the lo plane."""
+    the large tape lo = S low words (uint32, stored slot-major: an (S, n) plane) +
+    hi = one word of bit-32 flags.  "hi" is None when every W_m fits the lo plane."""
     c = prm.c()
-    if c.tape == 2:  # large
-        return {"lo": ((c.slots,), torch.int32), "hi": ((), torch.int32) if c.p > 0xFFFFFFFF else None}
-    return {"lo": ((8,), torch.uint8), "hi": ((), torch.uint8) if c.p > 256 else None}
+    if c.tape == 2:  # large: the lo plane is slot-major, (S, n)
+        return {"lo": ((c.slots,), torch.int32), "hi": ((), torch.int32) if c.p > 0xFFFFFFFF else None,
+                "slot_major": True}
+    return {"lo": ((8,), torch.uint8), "hi": ((), torch.uint8) if c.p > 256 else None, "slot_major": False}
+
+
+def lo_plane(buf: torch.Tensor, m: int, fmt: dict) -> torch.Tensor:
+    """The lo plane of m elements inside a buffer sized for more: the first m rows of
+    an element-major plane, or an (S, m) view of the first S m words of a slot-major one."""
+    if fmt.get("slot_major"):
+        S = fmt["lo"][0][0]
+        return buf.reshape(-1)[:S * m].view(S, m)
+    return buf[:m]
 
 
 def msg_buffers(n: int, device, prm: "Params | None" = None):
     fmt = wire_format(prm if prm is not None else Params())
     (los, lot), hi_f = fmt["lo"], fmt["hi"]
-    lo = torch.empty((n,) + los, dtype=lot, device=device)
+    lo = torch.empty((los[0], n) if fmt["slot_major"] else (n,) + los, dtype=lot, device=device)
     hi = torch.empty(n, dtype=(hi_f[1] if hi_f else lot), device=device)
     tb = torch.empty((n + 7) // 8, dtype=torch.uint8, device=device)
     return lo, hi, tb
@@ -356,7 +366,7 @@ def drelu_send(party, x, prm: Params, seed01: bytes, elem_base=0, out=None, stre
 def drelu_helper(lo0, hi0, lo1, hi1, prm: Params, seed02: bytes, elem_base=0, paper_literal=False, out=None,
                  stream=None):
     """Alg 7 steps 9-10 for P2: returns (resp0 or None, resp1)."""
-    n = lo0.shape[0]
+    n = lo0.shape[1] if wire_format(prm)["slot_major"] else lo0.shape[0]  # (S, n) or (n, 8)
     if out is None:
         r0 = torch.empty(n, dtype=torch.int64, device=lo0.device) if paper_literal else None
         r1 = torch.empty(n, dtype=torch.int64, device=lo0.device)
@@ -407,7 +417,7 @@ def relu_helper(lo0, hi0, lo1, hi1, prm: Params, seed02: bytes, seed12: bytes, e
                 e_dup=None, stream=None):
     """Alg 8 steps 2-3 for P2: returns (e, c1 or None).  e_dup: a second destination of
     e (bc_relu_helper_to), e.g. P1's mapped inbox while e goes to P0's."""
-    n = lo0.shape[0]
+    n = lo0.shape[1] if wire_format(prm)["slot_major"] else lo0.shape[0]  # (S, n) or (n, 8)
     if out is None:
         e = torch.empty(n, dtype=torch.int64, device=lo0.device)
         c1 = torch.empty(n, dtype=torch.int64, device=lo0.device) if with_c1 else None

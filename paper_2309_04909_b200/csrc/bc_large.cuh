@@ -219,12 +219,13 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
 }
 
 // Alg 7 steps 1-8 for ONE computing party (the party-separated send phase):
-// the message W_m, m < S, as 32-bit low words lo[m] and bit m of the returned
-// high-bit word (bit 32 of W_m; p < 2^33).  Returns t in bit 32 of the result.
+// the message W_m, m < S, as 32-bit low words lo[m * stride] (slot-major wire
+// planes) and bit m of the returned high-bit word (bit 32 of W_m; p < 2^33).
+// Returns t in bit 32 of the result.
 template <int R, int PARTY, int TPB_L>
 __device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, const Key& k01, const KPL& kp,
                                                      uint8_t* idx, uint32_t* stg, const uint32_t* magic,
-                                                     const uint32_t* hlim, uint32_t* lo) {
+                                                     const uint32_t* hlim, uint32_t* lo, uint64_t stride) {
   const uint32_t S = kp.S;
   uint32_t fbc = 0;
   const uint32_t t = large_perm<R, TPB_L>(j, k01, kp, idx, stg, magic, hlim, fbc);
@@ -244,7 +245,7 @@ __device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, con
       slot_values(sf, sf, idx[m * TPB_L], kp, c, d);                  // one of the two is this party's
       uint64_t W = PARTY == 0 ? mont(c, rM, kp) + rho : mont(d, rM, kp) + (kp.p - rho);  // steps 7-8
       W = W >= kp.p ? W - kp.p : W;
-      lo[m] = (uint32_t)W;
+      lo[m * stride] = (uint32_t)W;
       hib |= (uint32_t)(W >> 32) << m;
     }
   }

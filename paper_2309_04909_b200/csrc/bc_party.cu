@@ -110,9 +110,14 @@ __global__ void __launch_bounds__(TPB, 2) k_send_w(SendArgs a, KP kp, Key k01, K
   }
 }
 
-// Large tape (lx >= 8: up to 32 slots, p < 2^33).  Wire format: lo =
-// uint32_t[n][S] (low 32 bits of W_m), hi = uint32_t[n] (bit m = bit 32 of
-// W_m; NULL when p < 2^32): 33 S bits per element, 132 B at lx = 31 guard.
+// Large tape (lx >= 8: up to 32 slots, p < 2^33).  Wire format, slot-major:
+// lo = uint32_t[S][n] (word m of element i at lo[m n + i]: the low 32 bits of
+// W_m), hi = uint32_t[n] (bit m = bit 32 of W_m; NULL when p < 2^32): 33 S
+// bits per element, 132 B at lx = 31 guard.  A warp owns 256 consecutive
+// elements: first lane l computes elements base + 32 e + l (e = 0..7), so the
+// stores of slot m are 128 coalesced bytes (over NVLink in the peer
+// transport) and the blinding bits come out of one ballot per 32 elements;
+// then (ReLU) lane l computes [d]_b for its group of 8 (send_dshare).
 template <int R, int PARTY, bool RELU>
 __global__ void __launch_bounds__(TPB_LARGE) k_send_l(SendArgs a, KP kp, KPL kl, Key k01, Key ktr) {
   __shared__ uint8_t sidx[32 * TPB_LARGE];
@@ -124,23 +129,32 @@ __global__ void __launch_bounds__(TPB_LARGE) k_send_l(SendArgs a, KP kp, KPL kl,
   uint32_t* stg = sstg + threadIdx.x;
   uint32_t* lo = reinterpret_cast<uint32_t*>(a.lo);
   uint32_t* hi = reinterpret_cast<uint32_t*>(a.hi);
-  const uint64_t ngroups = (a.n + 7) >> 3;
-  for (uint64_t g = (uint64_t)blockIdx.x * TPB_LARGE + threadIdx.x; g < ngroups;
-       g += (uint64_t)gridDim.x * TPB_LARGE) {
-    const uint64_t i0 = g << 3;
-    const uint64_t j0 = a.base + i0;
-    const uint32_t cnt = (uint32_t)min((uint64_t)8, a.n - i0);
-    uint32_t tb = 0;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t ngroups = (a.n + 7) >> 3, nbytes = ngroups;
+  const uint64_t warps = (uint64_t)gridDim.x * (TPB_LARGE / 32);
+  for (uint64_t wb = ((uint64_t)blockIdx.x * (TPB_LARGE / 32) + threadIdx.x / 32) * 256; wb < a.n;
+       wb += warps * 256) {
 #pragma unroll 1
-    for (uint32_t e = 0; e < cnt; ++e) {
-      const uint64_t i = i0 + e;
-      const uint64_t r = elem_large_party<R, PARTY, TPB_LARGE>(__ldg(a.x + i), j0 + e, k01, kl, idx, stg, magic,
-                                                               hlim, lo + i * kl.S);
-      if (hi) hi[i] = (uint32_t)r;
-      tb |= (uint32_t)(r >> 32) << e;
+    for (uint32_t e = 0; e < 8; ++e) {
+      const uint64_t i = wb + 32 * e + lane;
+      uint32_t tb = 0;
+      if (i < a.n) {
+        const uint64_t r = elem_large_party<R, PARTY, TPB_LARGE>(__ldg(a.x + i), a.base + i, k01, kl, idx, stg,
+                                                                 magic, hlim, lo + i, a.n);
+        if (hi) hi[i] = (uint32_t)r;
+        tb = (uint32_t)(r >> 32);
+      }
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, tb != 0u);  // t of elements wb + 32 e + 0..31
+      const uint64_t byte = (wb + 32 * e) / 8 + lane;
+      if (lane < 4 && byte < nbytes) a.tbits[byte] = (uint8_t)(bal >> (8 * lane));
     }
-    a.tbits[g] = (uint8_t)tb;
-    if (RELU) send_dshare<R, PARTY>(a, kp, ktr, i0, j0, cnt);
+    if (RELU) {
+      const uint64_t g = wb / 8 + lane;
+      if (g < ngroups) {
+        const uint64_t i0 = g << 3;
+        send_dshare<R, PARTY>(a, kp, ktr, i0, a.base + i0, (uint32_t)min((uint64_t)8, a.n - i0));
+      }
+    }
   }
 }
 
@@ -231,14 +245,13 @@ __global__ void __launch_bounds__(TPB, 2) k_helper(HelperArgs a, KP kp, Key k02,
   }
 }
 
-// P2 on the large-tape wire format (see k_send_l).  The message rows are S
-// words per element: a warp reads each row coalesced (lane m reads slot m of
-// P0's and P1's rows), tests its slot, and a ballot gives the element's
-// DReLU'; the warp walks the 32 groups it owns, 8 elements (32 loads per
-// lane in flight) at a time, then every lane answers for its own group
-// (helper_respond).
+// P2 on the large-tape wire format (slot-major, see k_send_l).  A warp owns
+// 256 consecutive elements: lane l tests elements base + 32 e + l, reading
+// slot m of both messages as 128 coalesced bytes per warp, 8 slots' loads in
+// flight at a time; a ballot per 32 elements hands each lane the DReLU' byte
+// of its own group of 8, for which it then answers (helper_respond).
 #ifndef BC_HELPER_L_MINB
-#define BC_HELPER_L_MINB 3  // measured: 2.18 ms (3) vs 2.86 (2), 2.29 (4) per 2^24 for the DReLU helper
+#define BC_HELPER_L_MINB 2
 #endif
 template <int R, bool RELU>
 __global__ void __launch_bounds__(TPB, BC_HELPER_L_MINB) k_helper_l(HelperArgs a, KP kp, KPL kl, Key k02, Key k12) {
@@ -247,38 +260,41 @@ __global__ void __launch_bounds__(TPB, BC_HELPER_L_MINB) k_helper_l(HelperArgs a
   const uint32_t* hi0 = reinterpret_cast<const uint32_t*>(a.hi0);
   const uint32_t* hi1 = reinterpret_cast<const uint32_t*>(a.hi1);
   const uint32_t lane = threadIdx.x & 31u, S = kl.S;
-  const uint64_t ngroups = (a.n + 7) >> 3;
+  const uint64_t n = a.n, ngroups = (n + 7) >> 3;
   const uint64_t warps = (uint64_t)gridDim.x * (TPB / 32);
-  for (uint64_t wb = ((uint64_t)blockIdx.x * (TPB / 32) + threadIdx.x / 32) * 32; wb < ngroups; wb += warps * 32) {
-    const uint64_t g = wb + lane;  // this lane's group
-    const uint64_t gend = min(ngroups, wb + 32);
+  for (uint64_t wb = ((uint64_t)blockIdx.x * (TPB / 32) + threadIdx.x / 32) * 256; wb < n; wb += warps * 256) {
     uint32_t zbits = 0;
 #pragma unroll 1
-    for (uint64_t q = wb; q < gend; ++q) {  // warp-uniform: step 9 for the 8 elements of group q
-      uint32_t l0[8], l1[8], h0[8], h1[8];
+    for (uint32_t e = 0; e < 8; ++e) {
+      const uint64_t i = wb + 32 * e + lane;
+      bool z = false;
+      if (i < n) {  // step 9: any (W0_m + W1_m) mod p == 0
+        const uint32_t h0 = hi0 ? __ldg(hi0 + i) : 0u, h1 = hi1 ? __ldg(hi1 + i) : 0u;
+#pragma unroll 1
+        for (uint32_t m0 = 0; m0 < S; m0 += 8) {
+          uint32_t l0[8], l1[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {  // all loads first: 32 in flight per lane
-        const uint64_t i = q * 8 + e;
-        const bool ok = i < a.n && lane < S;
-        l0[e] = ok ? __ldg(lo0 + i * S + lane) : 0u;
-        l1[e] = ok ? __ldg(lo1 + i * S + lane) : 0u;
-        h0[e] = (ok && hi0) ? __ldg(hi0 + i) : 0u;
-        h1[e] = (ok && hi1) ? __ldg(hi1 + i) : 0u;
-      }
-      uint32_t zq = 0;
+          for (uint32_t k = 0; k < 8; ++k) {
+            const bool ok = m0 + k < S;
+            l0[k] = ok ? __ldg(lo0 + (m0 + k) * n + i) : 1u;  // absent slots: W0 + W1 = 2, never 0 or p
+            l1[k] = ok ? __ldg(lo1 + (m0 + k) * n + i) : 1u;
+          }
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const uint64_t W0 = (uint64_t)l0[e] | ((uint64_t)((h0[e] >> lane) & 1u) << 32);
-        const uint64_t W1 = (uint64_t)l1[e] | ((uint64_t)((h1[e] >> lane) & 1u) << 32);
-        const uint64_t sum = W0 + W1;
-        const bool z = lane < S && q * 8 + e < a.n && (sum == 0 || sum == kl.p);
-        zq |= (__ballot_sync(0xFFFFFFFFu, z) != 0u ? 1u : 0u) << e;
+          for (uint32_t k = 0; k < 8; ++k) {
+            const uint64_t W0 = (uint64_t)l0[k] | ((uint64_t)((h0 >> (m0 + k)) & 1u) << 32);
+            const uint64_t W1 = (uint64_t)l1[k] | ((uint64_t)((h1 >> (m0 + k)) & 1u) << 32);
+            const uint64_t sum = W0 + W1;
+            z |= sum == 0 || sum == kl.p;
+          }
+        }
       }
-      if (q == g) zbits = zq;
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, z);  // elements wb + 32 e + 0..31
+      if ((lane >> 2) == e) zbits = (bal >> (8 * (lane & 3u))) & 0xFFu;
     }
+    const uint64_t g = wb / 8 + lane;
     if (g < ngroups) {
       const uint64_t i0 = g << 3;
-      helper_respond<R, RELU>(a, kp, k02, k12, i0, a.base + i0, (uint32_t)min((uint64_t)8, a.n - i0), zbits);
+      helper_respond<R, RELU>(a, kp, k02, k12, i0, a.base + i0, (uint32_t)min((uint64_t)8, n - i0), zbits);
     }
   }
 }

@@ -140,7 +140,8 @@ class PartyRunner:
     def _msg_bufs(self, m):
         """P2's receive buffers for one chunk: lo0, hi0, lo1, hi1 (hi None if unused)."""
         (los, lot), hf = self.fmt["lo"], self.fmt["hi"]
-        lo0, lo1 = self.c.empty((m,) + los, lot), self.c.empty((m,) + los, lot)
+        shape = (los[0], m) if self.fmt["slot_major"] else (m,) + los
+        lo0, lo1 = self.c.empty(shape, lot), self.c.empty(shape, lot)
         hi0 = self.c.empty(m, hf[1]) if hf else None
         hi1 = self.c.empty(m, hf[1]) if hf else None
         return lo0, hi0, lo1, hi1

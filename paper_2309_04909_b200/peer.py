@@ -183,7 +183,8 @@ class PeerPartyRunner:
         self.g = group
         self.literal = paper_literal and kind == "drelu"
         self.base = self.role.triple * n if base is None else base
-        fmt = api.wire_format(prm)  # byte planes (p <= 257) or uint32 planes (large tape)
+        fmt = api.wire_format(prm)  # byte planes (p <= 257) or slot-major uint32 planes (large tape)
+        self.fmt = fmt
         self.hi_needed = fmt["hi"] is not None
         held = {0: ("s01", "s02"), 1: ("s01", "s12"), 2: ("s02", "s12")}[self.role.party]
         self.seed = {k: getattr(seeds, k) for k in held}
@@ -227,9 +228,12 @@ class PeerPartyRunner:
             self._works.pop(0).wait()
 
     def _send_out(self, d, m):
-        lo = d["lo"][:m]
+        lo = api.lo_plane(d["lo"], m, self.fmt)
         hi = d["hi"][:m] if self.hi_needed else self.hi_scratch[:m]
         return lo, hi
+
+    def _lo_in(self, src, m):
+        return api.lo_plane(src["lo"], m, self.fmt)
 
     @staticmethod
     def _hi_in(src, m):
@@ -258,7 +262,7 @@ class PeerPartyRunner:
                 s0, s1 = L["A"].wait(seq, be, g), L["B"].wait(seq, be, g)
                 r1 = L["C"].acquire(seq, be, g)["resp"][:m]
                 r0 = L["D"].acquire(seq, be, g)["resp"][:m] if self.literal else None
-                c.drelu_helper(s0["lo"][:m], self._hi_in(s0, m), s1["lo"][:m], self._hi_in(s1, m), self.prm,
+                c.drelu_helper(self._lo_in(s0, m), self._hi_in(s0, m), self._lo_in(s1, m), self._hi_in(s1, m), self.prm,
                                self.seed["s02"], base, paper_literal=self.literal, out=(r0, r1))     # steps 9-10
                 L["A"].release(seq, be, g, W)
                 L["B"].release(seq, be, g, W)
@@ -299,7 +303,7 @@ class PeerPartyRunner:
                 s0, s1 = L["A"].wait(seq, be, g), L["B"].wait(seq, be, g)
                 e0 = L["G"].acquire(seq, be, g)["e"][:m]
                 h = L["H"].acquire(seq, be, g)
-                c.relu_helper(s0["lo"][:m], self._hi_in(s0, m), s1["lo"][:m], self._hi_in(s1, m), self.prm,
+                c.relu_helper(self._lo_in(s0, m), self._hi_in(s0, m), self._lo_in(s1, m), self._hi_in(s1, m), self.prm,
                               self.seed["s02"], self.seed["s12"], base, out=(e0, h["c1"][:m]),
                               e_dup=h["e"][:m])                                                     # steps 2-3
                 L["A"].release(seq, be, g, W)

@@ -37,10 +37,11 @@ def _unpack_bits(b, n):
 
 
 def _decode_msg(lo, hi, S):
-    """Inverse of B.encode_msg (byte planes) / B.encode_msg_large (uint32 planes)."""
+    """Inverse of B.encode_msg (byte planes, (n, 8)) / B.encode_msg_large (slot-major
+    uint32 planes, (S, n))."""
     lo = np.asarray(lo)
     bit = np.uint64(8 if lo.dtype.itemsize == 1 else 32)
-    W = lo[:, :S].view(np.uint8 if bit == 8 else np.uint32).astype(np.uint64)
+    W = (lo[:, :S] if bit == 8 else lo.view(np.uint32).T).astype(np.uint64)
     if hi is not None:
         h = np.asarray(hi).view(np.uint8 if bit == 8 else np.uint32).astype(np.uint64)
         W |= ((h[:, None] >> np.arange(S, dtype=np.uint64)) & np.uint64(1)) << bit
@@ -70,9 +71,9 @@ class OracleCompute:
 
     def drelu_helper(self, lo0, hi0, lo1, hi1, prm, seed02, base, paper_literal=False):
         o = _prm(prm)
-        n = lo0.shape[0]
         W0 = _decode_msg(_np(lo0), None if hi0 is None else _np(hi0), o.slots)
         W1 = _decode_msg(_np(lo1), None if hi1 is None else _np(hi1), o.slots)
+        n = W0.shape[0]
         h = B.drelu_helper(o, W0, W1, _j(base, n), seed02)
         return (_t64(h["D0"]) if paper_literal else None), _t64(h["D1"])
 
@@ -95,9 +96,9 @@ class OracleCompute:
 
     def relu_helper(self, lo0, hi0, lo1, hi1, prm, seed02, seed12, base):
         o = _prm(prm)
-        n = lo0.shape[0]
         W0 = _decode_msg(_np(lo0), None if hi0 is None else _np(hi0), o.slots)
         W1 = _decode_msg(_np(lo1), None if hi1 is None else _np(hi1), o.slots)
+        n = W0.shape[0]
         h = B.relu_helper(o, W0, W1, _j(base, n), seed02, seed12)
         return _t64(h["e"]), _t64(h["c1"])
 
