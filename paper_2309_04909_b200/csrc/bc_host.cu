@@ -125,6 +125,13 @@ KPL make_kpl(const bc_params* prm) {
   k.pinv = inv;
   k.mu_p = ~0ull / p;
   k.mu_q = ~0ull / q;
+  k.qinv_p = 1.0 / (double)p;
+  k.qoff_p = -(4503599627370496.0 + (double)((p - 1) / 2));
+  k.s_q = 0;
+  while (((q >> k.s_q) & 1ull) == 0) ++k.s_q;
+  const uint64_t qo = q >> k.s_q;  // odd part of p - 1
+  k.qinv_q = 1.0 / (double)qo;
+  k.qoff_q = -(4503599627370496.0 + (double)((qo - 1) / 2));
   const u128 two48 = (u128)1 << 48;  // the large tape's draws are 48-bit
   const u128 pl = two48 / p * p, ql = two48 / q * q;
   k.plim = (uint64_t)(pl - 1);  // accept u <= lim - 1; 2^48 - 1 when q | 2^48 (nothing rejects)

@@ -146,3 +146,36 @@ def test_fisher_yates_magic_division():
         magic = (M32 // s) + 1
         q = (d * np.uint64(magic)) >> np.uint64(32)
         assert np.array_equal(d - q * np.uint64(s), d % np.uint64(s)), s
+
+
+def _fp_quotient(v, qo):
+    """The kernel's fpmod48 quotient, emulated exactly: vd = v - (qo-1)/2 (exact in
+    binary64), then RN(vd * RN(1/qo) + 1.5 * 2^52), whose grid at that magnitude is
+    the integers: round half to even of the exact rational."""
+    from fractions import Fraction
+    vd = Fraction(v) - Fraction(qo - 1, 2)
+    x = vd * Fraction(1.0 / qo) + Fraction(3 << 51)
+    fl = x.numerator // x.denominator
+    rem = x - fl
+    r = fl + (1 if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and fl % 2) else 0)
+    return r - (3 << 51)
+
+
+def test_fpmod48_quotient_exact():
+    """floor(u / q) = floor(v / q'), v = u >> s, q = q' 2^s (q' odd), and the binary64
+    quotient the large-tape kernel uses (BC_LARGE_FPMOD) is exactly floor(v / q') for
+    every draw u < 2^48: the moduli of every large-tape setting (p and p - 1 for
+    w = 9..32), random draws and the draws next to multiples of q and to 2^48."""
+    from oracle.ring import prime_above
+    rng = np.random.default_rng(7)
+    for w in range(9, 33):
+        p = prime_above(w)
+        for q in (p, p - 1):
+            s = (q & -q).bit_length() - 1
+            qo = q >> s
+            us = [0, 1, q - 1, q, q + 1, (1 << 48) - 1, ((1 << 48) // q) * q - 1, ((1 << 48) // q) * q - 2]
+            us += [int(v) for v in rng.integers(0, 1 << 48, size=40, dtype=np.uint64)]
+            k = [int(v) for v in rng.integers(1, (1 << 48) // q, size=20, dtype=np.uint64)]
+            us += [m * q + d for m in k for d in (-1, 0, 1, q // 2, q - 1) if 0 <= m * q + d < (1 << 48)]
+            for u in us:
+                assert _fp_quotient(u >> s, qo) == u // q, (w, q, u)
