@@ -1,6 +1,8 @@
 // bc_party.cu -- party-separated phases of Alg 7 / Alg 8: send (P0, P1),
-// helper (P2), finish (P0, P1).  Each party runs its phase on its own device;
-// the caller moves the message buffers (NCCL send/recv over NVLink).
+// helper (P2), finish (P0, P1).  Each party runs its phase on its own device.
+// The message buffers are whatever the caller passes: staging buffers it then
+// moves (NCCL send/recv, party.py) or the receiving party's inbox mapped into
+// this process (peer.py), in which case the kernel's stores are the transfer.
 #include "bc_common.cuh"
 
 using namespace bc;
