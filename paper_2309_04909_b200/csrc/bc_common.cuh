@@ -58,6 +58,7 @@ bool index_range_ok(uint64_t base, size_t n);       // [base, base + n) within [
 int check_params(const bc_params* prm);              // re-derives and compares
 KP make_kp(const bc_params* prm);
 Key make_key(const uint8_t* s);
+KeyPre make_keypre(const uint8_t* s, uint64_t label);  // chacha_pre's first-round precomputation
 
 template <typename F>
 int dispatch_rounds(int rounds, F&& f) {

@@ -112,6 +112,38 @@ __device__ __forceinline__ void chacha(const Key& key, uint64_t ctr, uint64_t la
   o[12] = x12 + c0; o[13] = x13 + c1; o[14] = x14 + l0; o[15] = x15 + l1;
 }
 
+// A (key, label) pair with the two column quarter rounds of the first round
+// that involve neither counter word already applied (columns 2 and 3: words
+// 2, 6, 10, 14 and 3, 7, 11, 15 are constants, key and label).  Computed on
+// the host per (seed, stream label); the kernel reads it from the parameter
+// bank, so the first round costs two quarter rounds instead of four.
+struct KeyPre {
+  uint32_t k[8];
+  uint32_t l0, l1;
+  uint32_t c[8];  // x2, x6, x10, x14, x3, x7, x11, x15 after the first column round
+};
+
+template <int R>
+__device__ __forceinline__ void chacha_pre(const KeyPre& P, uint64_t ctr, uint32_t (&o)[16]) {
+  uint32_t x0 = 0x61707865u, x1 = 0x3320646eu;
+  uint32_t x4 = P.k[0], x5 = P.k[1], x8 = P.k[4], x9 = P.k[5];
+  const uint32_t c0 = (uint32_t)ctr, c1 = (uint32_t)(ctr >> 32);
+  uint32_t x12 = c0, x13 = c1;
+  BC_QR_ALU(x0, x4, x8, x12) BC_QR_ALU(x1, x5, x9, x13)
+  uint32_t x2 = P.c[0], x6 = P.c[1], x10 = P.c[2], x14 = P.c[3];
+  uint32_t x3 = P.c[4], x7 = P.c[5], x11 = P.c[6], x15 = P.c[7];
+  BC_QR_ALU(x0, x5, x10, x15) BC_QR_ALU(x1, x6, x11, x12) BC_QR_ALU(x2, x7, x8, x13) BC_QR_ALU(x3, x4, x9, x14)
+#pragma unroll kChachaUnroll
+  for (int r = 2; r < R; r += 2) {
+    BC_QR_ALU(x0, x4, x8, x12) BC_QR_ALU(x1, x5, x9, x13) BC_QR_ALU(x2, x6, x10, x14) BC_QR_ALU(x3, x7, x11, x15)
+    BC_QR_ALU(x0, x5, x10, x15) BC_QR_ALU(x1, x6, x11, x12) BC_QR_ALU(x2, x7, x8, x13) BC_QR_ALU(x3, x4, x9, x14)
+  }
+  o[0] = x0 + 0x61707865u; o[1] = x1 + 0x3320646eu; o[2] = x2 + 0x79622d32u; o[3] = x3 + 0x6b206574u;
+  o[4] = x4 + P.k[0]; o[5] = x5 + P.k[1]; o[6] = x6 + P.k[2]; o[7] = x7 + P.k[3];
+  o[8] = x8 + P.k[4]; o[9] = x9 + P.k[5]; o[10] = x10 + P.k[6]; o[11] = x11 + P.k[7];
+  o[12] = x12 + c0; o[13] = x13 + c1; o[14] = x14 + P.l0; o[15] = x15 + P.l1;
+}
+
 // ---------------------------------------------------------------------------
 // Small helpers
 // ---------------------------------------------------------------------------

@@ -20,20 +20,41 @@ struct FusedArgs {
   uint8_t *w0lo, *w0hi, *w1lo, *w1hi;
 };
 
+// Every stream of the fused kernels with its first-round precomputation
+// (KeyPre, chacha_pre); BC_CHACHA_PRE = 0 runs the plain block function.
+struct PreKeys {
+  KeyPre tpa, tpb, resp, a02, b02, c02, a12, b12;
+};
+#ifndef BC_CHACHA_PRE
+#define BC_CHACHA_PRE 1
+#endif
+// PRE: use the precomputation at this call site.  Measured (tools/variants.py):
+// DReLU 0.490 -> 0.484 ms / 2^24; ReLU 0.860 -> 0.880 (the peeled first double
+// round at its seven call sites costs more instruction cache than it saves), so
+// the ReLU kernels keep the plain block function.
+template <int R, bool PRE>
+__device__ __forceinline__ void stream_blk(const KeyPre& P, const Key& k, uint64_t label, uint64_t ctr,
+                                           uint32_t (&o)[16]) {
+  if (PRE && BC_CHACHA_PRE)
+    chacha_pre<R>(P, ctr, o);
+  else
+    chacha<R>(k, ctr, label, o);
+}
+
 // ---- shared finish: Alg 7 steps 10-11, or Alg 8 (triple, e, d, Beaver combine) ----
 // FULL (ell = 64): every value is already reduced mod 2^ell, the masks fold away.
 // The sign (1 - 2t) is applied as a 64-bit multiply (FMA pipe) rather than as
 // negate-and-select (ALU pipe, which the ChaCha rounds saturate).
 template <int R, bool RELU, bool FULL>
 __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, const Key& k02, const Key& k12,
-                                             uint64_t i0, uint64_t j0, uint32_t cnt, uint32_t zbits,
-                                             uint32_t tbits) {
+                                             const PreKeys& pk, uint64_t i0, uint64_t j0, uint32_t cnt,
+                                             uint32_t zbits, uint32_t tbits) {
   const uint64_t ym = FULL ? ~0ull : kp.ymask;
   uint64_t y0[8], y1[8];
   if (!RELU) {
     // Alg 7 step 10: P2 reshares DReLU' ([D']_0 from seed02); step 11: P0/P1 unblind.
     uint32_t Q[16];
-    chacha<R>(k02, j0 >> 3, L_RESP, Q);
+    stream_blk<R, true>(pk.resp, k02, L_RESP, j0 >> 3, Q);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const uint64_t z = (zbits >> e) & 1u, t = (tbits >> e) & 1u;
@@ -47,10 +68,10 @@ __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, c
     uint64_t b0[8], b1[8], ev[8];
     {
       uint32_t Bk[16];
-      chacha<R>(k02, j0 >> 3, L_B02, Bk);
+      stream_blk<R, false>(pk.b02, k02, L_B02, j0 >> 3, Bk);
 #pragma unroll
       for (int e = 0; e < 8; ++e) b0[e] = u64_of(Bk, e);
-      chacha<R>(k12, j0 >> 3, L_B12, Bk);
+      stream_blk<R, false>(pk.b12, k12, L_B12, j0 >> 3, Bk);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         b1[e] = u64_of(Bk, e);
@@ -59,8 +80,8 @@ __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, c
     }
     {
       uint32_t Ak0[16], Ak1[16];
-      chacha<R>(k02, j0 >> 3, L_A02, Ak0);
-      chacha<R>(k12, j0 >> 3, L_A12, Ak1);
+      stream_blk<R, false>(pk.a02, k02, L_A02, j0 >> 3, Ak0);
+      stream_blk<R, false>(pk.a12, k12, L_A12, j0 >> 3, Ak1);
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
         const ulonglong2 v0 = load2(a.x0, i0 + 2 * h, a.n), v1 = load2(a.x1, i0 + 2 * h, a.n);
@@ -76,7 +97,7 @@ __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, c
     }
     {
       uint32_t Ck[16];
-      chacha<R>(k02, j0 >> 3, L_C02, Ck);
+      stream_blk<R, false>(pk.c02, k02, L_C02, j0 >> 3, Ck);
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
         const ulonglong2 v0 = load2(a.x0, i0 + 2 * h, a.n), v1 = load2(a.x1, i0 + 2 * h, a.n);
@@ -103,7 +124,7 @@ __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, c
 // (8 B/element) and two part-A blocks (16 B/element, 4 elements each) -- 3
 // ChaCha blocks per 8 elements, none shared between threads.
 template <int R, bool RELU, bool TRANSCRIPT, bool FULL>
-__global__ void __launch_bounds__(TPB, FUSED_MINB) k_fused_c(FusedArgs a, KP kp, Key k01, Key k02, Key k12) {
+__global__ void __launch_bounds__(TPB, FUSED_MINB) k_fused_c(FusedArgs a, KP kp, Key k01, Key k02, Key k12, PreKeys pk) {
   __shared__ uint32_t sA[2 * PERM_A], sB[2 * PERM_B];
   build_perm_tables(sA, sB);
   __syncthreads();
@@ -115,14 +136,14 @@ __global__ void __launch_bounds__(TPB, FUSED_MINB) k_fused_c(FusedArgs a, KP kp,
     const uint32_t cnt = (uint32_t)min((uint64_t)8, a.n - i0);
     uint32_t zbits = 0, tbits = 0;
     uint32_t Bp[16];  // part B: words 2e, 2e+1 of element e (reshare words w1, w2)
-    chacha<R>(k01, j0 >> 3, L_TAPEB, Bp);
+    stream_blk<R, !RELU>(pk.tpb, k01, L_TAPEB, j0 >> 3, Bp);
 #pragma unroll 1
     for (int hb = 0; hb < 2; ++hb) {
       const uint64_t ib = i0 + 4 * hb;
       const ulonglong2 u0 = load2(a.x0, ib, a.n), u1 = load2(a.x1, ib, a.n);
       const ulonglong2 v0 = load2(a.x0, ib + 2, a.n), v1 = load2(a.x1, ib + 2, a.n);
       uint32_t A[16];  // part A: words 4q..4q+3 of element 4 hb + q
-      chacha<R>(k01, (j0 >> 2) + (uint64_t)hb, L_TAPEA, A);
+      stream_blk<R, !RELU>(pk.tpa, k01, L_TAPEA, (j0 >> 2) + (uint64_t)hb, A);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int e = 4 * hb + q;
@@ -145,13 +166,13 @@ __global__ void __launch_bounds__(TPB, FUSED_MINB) k_fused_c(FusedArgs a, KP kp,
 #pragma unroll
       for (int k = 0; k < 8; ++k) Bp[k] = Bp[k + 8];  // elements 4..7 next
     }
-    finish_group<R, RELU, FULL>(a, kp, k02, k12, i0, j0, cnt, zbits, tbits);
+    finish_group<R, RELU, FULL>(a, kp, k02, k12, pk, i0, j0, cnt, zbits, tbits);
   }
 }
 
 // Wide tape (any p <= 257, 3..8 slots): one seed01 block per element.
 template <int R, bool RELU>
-__global__ void __launch_bounds__(TPB, 2) k_fused_w(FusedArgs a, KP kp, Key k01, Key k02, Key k12) {
+__global__ void __launch_bounds__(TPB, 2) k_fused_w(FusedArgs a, KP kp, Key k01, Key k02, Key k12, PreKeys pk) {
   const uint64_t ngroups = (a.n + 7) >> 3;
   for (uint64_t g = (uint64_t)blockIdx.x * TPB + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB) {
     const uint64_t i0 = g << 3;
@@ -178,7 +199,7 @@ __global__ void __launch_bounds__(TPB, 2) k_fused_w(FusedArgs a, KP kp, Key k01,
         a.w1hi[i0 + e] = (uint8_t)pack_hi(W1);
       }
     }
-    finish_group<R, RELU, false>(a, kp, k02, k12, i0, j0, cnt, zbits, tbits);
+    finish_group<R, RELU, false>(a, kp, k02, k12, pk, i0, j0, cnt, zbits, tbits);
   }
 }
 
@@ -190,7 +211,7 @@ constexpr int TPB_L = TPB_LARGE;
 #endif
 
 template <int R, bool RELU, bool TRANSCRIPT>
-__global__ void __launch_bounds__(TPB_L, BC_LARGE_MINB) k_fused_l(FusedArgs a, KP kp, KPL kl, Key k01, Key k02, Key k12) {
+__global__ void __launch_bounds__(TPB_L, BC_LARGE_MINB) k_fused_l(FusedArgs a, KP kp, KPL kl, Key k01, Key k02, Key k12, PreKeys pk) {
   __shared__ uint8_t sidx[32 * TPB_L];
   __shared__ uint32_t sstg[LARGE_STG_ROWS * TPB_L];
   __shared__ uint32_t magic[33], hlim[33];
@@ -214,7 +235,7 @@ __global__ void __launch_bounds__(TPB_L, BC_LARGE_MINB) k_fused_l(FusedArgs a, K
       zbits |= (r & 1u) << e;
       tbits |= (r >> 1) << e;
     }
-    finish_group<R, RELU, false>(a, kp, k02, k12, i0, j0, cnt, zbits, tbits);
+    finish_group<R, RELU, false>(a, kp, k02, k12, pk, i0, j0, cnt, zbits, tbits);
   }
 }
 
@@ -239,7 +260,7 @@ __device__ __noinline__ uint32_t fallback_b1(uint64_t j, Key key, uint32_t lim) 
 }
 
 template <int R, bool TRANSCRIPT>
-__global__ void __launch_bounds__(TPB_L) k_fused_b1(FusedArgs a, KP kp, Key k01, Key k02, Key k12) {
+__global__ void __launch_bounds__(TPB_L) k_fused_b1(FusedArgs a, KP kp, Key k01, Key k02, Key k12, PreKeys pk) {
   __shared__ uint64_t sv[2 * 8 * TPB_L];  // [party][slot][thread]
   const uint32_t tid = threadIdx.x, S = kp.S;
   const uint64_t ym = kp.ymask;
@@ -310,7 +331,7 @@ __global__ void __launch_bounds__(TPB_L) k_fused_b1(FusedArgs a, KP kp, Key k01,
       zbits |= z << e;
       tbits |= t << e;
     }
-    finish_group<R, false, false>(a, kp, k02, k12, i0, j0, cnt, zbits, tbits);
+    finish_group<R, false, false>(a, kp, k02, k12, pk, i0, j0, cnt, zbits, tbits);
   }
 }
 
@@ -349,6 +370,10 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
   }
   const KP kp = make_kp(prm);
   const Key k01 = make_key(seeds->s01), k02 = make_key(seeds->s02), k12 = make_key(seeds->s12);
+  const PreKeys pk{make_keypre(seeds->s01, L_TAPEA), make_keypre(seeds->s01, L_TAPEB),
+                   make_keypre(seeds->s02, L_RESP),  make_keypre(seeds->s02, L_A02),
+                   make_keypre(seeds->s02, L_B02),   make_keypre(seeds->s02, L_C02),
+                   make_keypre(seeds->s12, L_A12),   make_keypre(seeds->s12, L_B12)};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint64_t ngroups = (n + 7) / 8;
   return dispatch_rounds(prm->rounds, [&](auto Rc) {
@@ -356,14 +381,14 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
     if (large) {
       const KPL kl = make_kpl(prm);
       auto fn = tr ? k_fused_l<R, RELU, true> : k_fused_l<R, RELU, false>;
-      fn<<<grid_for((const void*)fn, ngroups, TPB_L), TPB_L, 0, st>>>(a, kp, kl, k01, k02, k12);
+      fn<<<grid_for((const void*)fn, ngroups, TPB_L), TPB_L, 0, st>>>(a, kp, kl, k01, k02, k12, pk);
     } else if (prm->tape == BC_TAPE_COMPACT) {
       auto fn = tr ? k_fused_c<R, RELU, true, false>
                    : (prm->ell == 64 ? k_fused_c<R, RELU, false, true> : k_fused_c<R, RELU, false, false>);
-      fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k01, k02, k12);
+      fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k01, k02, k12, pk);
     } else {
       auto fn = k_fused_w<R, RELU>;
-      fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k01, k02, k12);
+      fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k01, k02, k12, pk);
     }
     return check_launch();
   });
@@ -398,11 +423,15 @@ int drelu_b1(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1,
   const uint32_t fact = [&] { uint32_t f = 1; for (uint32_t i = 2; i <= prm->slots; ++i) f *= i; return f; }();
   kp.perm_lim = (uint32_t)((0x80000000ull / fact) * fact);
   const Key k01 = make_key(seeds->s01), k02 = make_key(seeds->s02), k12 = make_key(seeds->s12);
+  const PreKeys pk{make_keypre(seeds->s01, L_TAPEA), make_keypre(seeds->s01, L_TAPEB),
+                   make_keypre(seeds->s02, L_RESP),  make_keypre(seeds->s02, L_A02),
+                   make_keypre(seeds->s02, L_B02),   make_keypre(seeds->s02, L_C02),
+                   make_keypre(seeds->s12, L_A12),   make_keypre(seeds->s12, L_B12)};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   return dispatch_rounds(prm->rounds, [&](auto Rc) {
     constexpr int R = decltype(Rc)::value;
     auto fn = tr ? k_fused_b1<R, true> : k_fused_b1<R, false>;
-    fn<<<grid_for((const void*)fn, (n + 7) / 8, TPB_L), TPB_L, 0, st>>>(a, kp, k01, k02, k12);
+    fn<<<grid_for((const void*)fn, (n + 7) / 8, TPB_L), TPB_L, 0, st>>>(a, kp, k01, k02, k12, pk);
     return check_launch();
   });
 }

@@ -145,6 +145,27 @@ KPL make_kpl(const bc_params* prm) {
   return k;
 }
 
+KeyPre make_keypre(const uint8_t* s, uint64_t label) {
+  KeyPre p;
+  std::memcpy(p.k, s, 32);
+  p.l0 = (uint32_t)label;
+  p.l1 = (uint32_t)(label >> 32);
+  auto rotl = [](uint32_t v, int n) { return (v << n) | (v >> (32 - n)); };
+  auto qr = [&](uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {  // RFC 8439 sec. 2.1
+    a += b; d ^= a; d = rotl(d, 16);
+    c += d; b ^= c; b = rotl(b, 12);
+    a += b; d ^= a; d = rotl(d, 8);
+    c += d; b ^= c; b = rotl(b, 7);
+  };
+  uint32_t x2 = 0x79622d32u, x6 = p.k[2], x10 = p.k[6], x14 = p.l0;
+  uint32_t x3 = 0x6b206574u, x7 = p.k[3], x11 = p.k[7], x15 = p.l1;
+  qr(x2, x6, x10, x14);
+  qr(x3, x7, x11, x15);
+  const uint32_t c[8] = {x2, x6, x10, x14, x3, x7, x11, x15};
+  std::memcpy(p.c, c, sizeof c);
+  return p;
+}
+
 Key make_key(const uint8_t* s) {
   Key k;
   std::memcpy(k.k, s, 32);  // little-endian host: words are the LE u32 of the seed
