@@ -28,9 +28,9 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, kind, n, chunk, slots, literal, runs, outdir):
+def _worker(rank, world, port, kind, n, chunk, slots, literal, runs, outdir, kw=None):
     try:
-        _work(rank, world, port, kind, n, chunk, slots, literal, runs, outdir)
+        _work(rank, world, port, kind, n, chunk, slots, literal, runs, outdir, kw)
     except BaseException:
         import traceback
         with open(os.path.join(outdir, f"err_{rank}.txt"), "w") as f:
@@ -38,16 +38,17 @@ def _worker(rank, world, port, kind, n, chunk, slots, literal, runs, outdir):
         raise
 
 
-def _work(rank, world, port, kind, n, chunk, slots, literal, runs, outdir):
+def _work(rank, world, port, kind, n, chunk, slots, literal, runs, outdir, kw=None):
     sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     import synth
     from paper_2309_04909_b200 import api, peer
-    prm = api.Params(ell=64, lx=7, f=24, mode="guard", rounds=20)
+    kw = kw or dict(ell=64, lx=7, f=24, mode="guard", rounds=20)
+    prm = api.Params(**kw)
     role = peer.Role.of(rank)
-    x, x0, x1 = synth.shares(n, 64, 7, 24, "D1", run=role.triple)
+    x, x0, x1 = synth.shares(n, kw["ell"], kw["lx"], kw["f"], "D1", run=role.triple)
     xs = torch.from_numpy((x0 if role.party == 0 else x1).view(np.int64)).cuda()
     runner = peer.PeerPartyRunner(kind, prm, synth.seeds(0), n, chunk=chunk, slots=slots,
                                   backend=peer.CudaIpcBackend("cuda:0"), group=dist.group.WORLD,
@@ -67,9 +68,9 @@ def _work(rank, world, port, kind, n, chunk, slots, literal, runs, outdir):
     dist.destroy_process_group()
 
 
-def _run(tmp_path, kind, n, chunk, slots, literal, runs):
+def _run(tmp_path, kind, n, chunk, slots, literal, runs, kw=None):
     try:
-        mp.start_processes(_worker, args=(3, _free_port(), kind, n, chunk, slots, literal, runs, str(tmp_path)),
+        mp.start_processes(_worker, args=(3, _free_port(), kind, n, chunk, slots, literal, runs, str(tmp_path), kw),
                            nprocs=3, join=True, start_method="spawn")
     except Exception:
         errs = "".join(f"--- rank {r}\n" + open(tmp_path / f"err_{r}.txt").read()
@@ -102,3 +103,13 @@ def test_party_peer_large_vs_fused(tmp_path, kind):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     _run(tmp_path, kind, (1 << 22) + 13, 1 << 20, 2, False, runs=3)  # 5 chunks x 3 runs: the rings keep turning
+
+
+@pytest.mark.parametrize("kind", ["drelu", "relu"])
+def test_party_peer_full_precision(tmp_path, kind):
+    """The large tape through the peer transport: lx = 31 full precision (p = 2^32 + 15),
+    slot-major uint32 planes with the bit-32 plane stored into P2's inbox."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    kw = dict(ell=64, lx=31, f=0, mode="guard", rounds=8)
+    _run(tmp_path, kind, 2003, 512, 2, kind == "drelu", 2, kw)
