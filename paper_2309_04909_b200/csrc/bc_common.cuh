@@ -49,7 +49,7 @@ __device__ __forceinline__ uint64_t load_hi8(const uint8_t* hi, uint64_t i0, uin
 namespace host {
 int check_launch();                                  // cudaGetLastError -> BC_OK / BC_ECUDA
 int cuda_rc(cudaError_t e);                          // records e for bc_last_cuda_error
-int grid_for(const void* fn, uint64_t nthreads_work, int tpb = TPB);  // persistent grid size
+int grid_for(const void* fn, uint64_t nthreads_work, int tpb = TPB, size_t smem = 0);  // persistent grid size
 KPL make_kpl(const bc_params* prm);                  // large-tape constants (p < 2^33)
 bool aligned16(const void* p);
 bool aligned8(const void* p);

@@ -42,7 +42,7 @@ int check_launch() {
 }
 
 // Persistent grid: min(#work blocks, #SM x resident blocks per SM), cached per (kernel, device).
-int grid_for(const void* fn, uint64_t nthreads_work, int tpb) {
+int grid_for(const void* fn, uint64_t nthreads_work, int tpb, size_t smem) {
   struct Entry {
     const void* fn;
     int dev;
@@ -64,7 +64,7 @@ int grid_for(const void* fn, uint64_t nthreads_work, int tpb) {
     if (!cap) {
       int sms = 0, occ = 0;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, tpb, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, tpb, smem);
       cap = std::max(1, sms) * std::max(1, occ);
       if (ncache < 512) cache[ncache++] = Entry{fn, dev, cap};
     }
