@@ -340,7 +340,9 @@ const char *bc_strerror(int code);
 /* cudaError_t of the most recent BC_ECUDA on this thread (0 if none). */
 int bc_last_cuda_error(void);
 
-/* Library ABI version (major * 100 + minor). */
+/* Library ABI version (major * 100 + minor).  3.00: the large-tape party
+ * phases (slot-major uint32 wire planes), bc_relu_send_to / bc_relu_helper_to,
+ * bc_ipc_*, BC_MAX_INDEX, and the 7-block large tape bc2.tpL2 (2.00: 9 blocks). */
 int bc_version(void);
 
 #ifdef __cplusplus

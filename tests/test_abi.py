@@ -66,5 +66,5 @@ def test_errors_and_strerror(lib):
     assert b"window" in lib.bc_strerror(-2)
     # a NULL-pointer call is rejected on the host before any launch
     assert lib.bc_drelu(None, None, None, None, 8, 0, ctypes.byref(api.Params().c()), None, None, None) == -1
-    assert lib.bc_version() >= 200
+    assert lib.bc_version() >= 300
     assert ctypes.sizeof(api.bc_params) == 40
