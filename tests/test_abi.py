@@ -68,3 +68,22 @@ def test_errors_and_strerror(lib):
     assert lib.bc_drelu(None, None, None, None, 8, 0, ctypes.byref(api.Params().c()), None, None, None) == -1
     assert lib.bc_version() >= 300
     assert ctypes.sizeof(api.bc_params) == 40
+
+
+def test_host_only_entry_points_validate_without_a_gpu(lib):
+    """The peer-memory plumbing refuses NULL arguments before touching CUDA, and
+    parameter derivation rejects windows that do not fit (BC_ERANGE) -- no device needed."""
+    import ctypes
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_uint64()
+    base = ctypes.c_void_p()
+    assert lib.bc_ipc_export(None, h, ctypes.byref(off)) == -1
+    assert lib.bc_ipc_export(ctypes.c_void_p(16), None, ctypes.byref(off)) == -1
+    assert lib.bc_ipc_open(None, ctypes.byref(base)) == -1
+    assert lib.bc_ipc_open(h, None) == -1
+    assert lib.bc_ipc_close(None) == -1
+    from paper_2309_04909_b200 import api
+    p = api.bc_params()
+    assert lib.bc_params_init(ctypes.byref(p), 64, 31, 2, 0, 20) == -2     # 2 + 31 + 32 > 64
+    assert lib.bc_params_init(ctypes.byref(p), 64, 31, 0, 0, 20) == 0
+    assert p.tape == 2 and p.slots == 32 and p.p == 2**32 + 15
