@@ -18,7 +18,10 @@ using namespace bc::host;
 
 namespace {
 
-constexpr int NS = 3;
+#ifndef BC_HOST_NS
+#define BC_HOST_NS 3
+#endif
+constexpr int NS = BC_HOST_NS;  // streams (and workspace chunk slots) in the ring
 constexpr int MAX_DEV = 64;
 
 struct Ring {

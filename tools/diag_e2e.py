@@ -32,3 +32,27 @@ for chunk in (1 << 19, 1 << 20, 1 << 21, 1 << 22, 1 << 23):
     torch.cuda.synchronize(); dt = (time.perf_counter() - t) / 10
     out[f"chunk{chunk}"] = n / dt / 1e9
 print(json.dumps(out))
+
+# the same chunked schedule with copies only (no kernel): the PCIe-side bound of the pipeline
+def copy_only(chunk, ns=3):
+    streams = [torch.cuda.Stream() for _ in range(ns)]
+    bufs = [[torch.empty(chunk, dtype=torch.int64, device=dev) for _ in range(4)] for _ in range(ns)]
+    def run():
+        for c, a in enumerate(range(0, n, chunk)):
+            m = min(chunk, n - a)
+            s = streams[c % ns]
+            b = bufs[c % ns]
+            with torch.cuda.stream(s):
+                b[0][:m].copy_(hx0[a:a + m], non_blocking=True)
+                b[1][:m].copy_(hx1[a:a + m], non_blocking=True)
+                hy0[a:a + m].copy_(b[2][:m], non_blocking=True)
+                hy1[a:a + m].copy_(b[3][:m], non_blocking=True)
+        torch.cuda.synchronize()
+    run()
+    t = time.perf_counter()
+    for _ in range(10):
+        run()
+    return n / ((time.perf_counter() - t) / 10) / 1e9
+out2 = {f"copy_only_chunk{c}": copy_only(c) for c in (1 << 20, 1 << 21, 1 << 22)}
+out2["copy_only_chunk2M_4streams"] = copy_only(1 << 21, 4)
+print(json.dumps(out2))
