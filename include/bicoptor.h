@@ -169,6 +169,21 @@ int bc_relu_host(const uint64_t *x0, const uint64_t *x1, uint64_t *y0, uint64_t 
                  uint64_t elem_base, const bc_params *prm, const bc_seeds *seeds, void *ws,
                  size_t ws_bytes, size_t chunk, void *stream);
 
+/* Asynchronous forms of the two calls above: enqueue only.  The chunks are not
+ * ordered after the caller's earlier stream work (the host inputs must be
+ * ready when called); the caller's stream waits for every chunk, so
+ * synchronising it makes the host outputs complete.  Consecutive calls with
+ * the same workspace pipeline into each other: a serving loop keeps both PCIe
+ * directions busy across requests instead of filling and draining per call.
+ * The host buffers of a call must not be reused before that point. */
+int bc_drelu_host_async(const uint64_t *x0, const uint64_t *x1, uint64_t *y0, uint64_t *y1,
+                        size_t n, uint64_t elem_base, const bc_params *prm,
+                        const bc_seeds *seeds, void *ws, size_t ws_bytes, size_t chunk,
+                        void *stream);
+int bc_relu_host_async(const uint64_t *x0, const uint64_t *x1, uint64_t *y0, uint64_t *y1,
+                       size_t n, uint64_t elem_base, const bc_params *prm, const bc_seeds *seeds,
+                       void *ws, size_t ws_bytes, size_t chunk, void *stream);
+
 /* ---- party-separated phases (each party on its own device; the caller moves
  * the message buffers, e.g. with NCCL send/recv) --------------------------- */
 

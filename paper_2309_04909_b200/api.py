@@ -89,6 +89,12 @@ _SIG = {
                                      ctypes.POINTER(bc_seeds), _P, ctypes.c_size_t, ctypes.c_size_t, _P]),
     "bc_relu_host": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64, ctypes.POINTER(bc_params),
                                     ctypes.POINTER(bc_seeds), _P, ctypes.c_size_t, ctypes.c_size_t, _P]),
+    "bc_drelu_host_async": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64,
+                                           ctypes.POINTER(bc_params), ctypes.POINTER(bc_seeds), _P, ctypes.c_size_t,
+                                           ctypes.c_size_t, _P]),
+    "bc_relu_host_async": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64,
+                                          ctypes.POINTER(bc_params), ctypes.POINTER(bc_seeds), _P, ctypes.c_size_t,
+                                          ctypes.c_size_t, _P]),
     "bc_trc_aby3": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
                                    ctypes.c_int, ctypes.c_int, ctypes.POINTER(bc_seeds), _P]),
     "bc_trc_count": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_uint64,
@@ -307,17 +313,20 @@ def _host_call(fn, what, hx0, hx1, hy0, hy1, prm, seeds, elem_base, ws, chunk, s
 
 
 @_on_input_device
-def drelu_host(hx0, hx1, hy0, hy1, prm: Params, seeds, ws, chunk: int = 1 << 20, elem_base: int = 0, stream=None):
-    """bc_drelu_host: host shares in (pinned recommended), host shares out; synchronous."""
-    return _host_call(lib().bc_drelu_host, "bc_drelu_host", hx0, hx1, hy0, hy1, prm, seeds, elem_base, ws, chunk,
-                      stream)
+def drelu_host(hx0, hx1, hy0, hy1, prm: Params, seeds, ws, chunk: int = 1 << 20, elem_base: int = 0, stream=None,
+               sync: bool = True):
+    """bc_drelu_host: host shares in (pinned recommended), host shares out; synchronous.
+    sync=False: bc_drelu_host_async, enqueue only (synchronise the stream before reading)."""
+    fn, what = (lib().bc_drelu_host, "bc_drelu_host") if sync else (lib().bc_drelu_host_async, "bc_drelu_host_async")
+    return _host_call(fn, what, hx0, hx1, hy0, hy1, prm, seeds, elem_base, ws, chunk, stream)
 
 
 @_on_input_device
-def relu_host(hx0, hx1, hy0, hy1, prm: Params, seeds, ws, chunk: int = 1 << 20, elem_base: int = 0, stream=None):
+def relu_host(hx0, hx1, hy0, hy1, prm: Params, seeds, ws, chunk: int = 1 << 20, elem_base: int = 0, stream=None,
+              sync: bool = True):
     """bc_relu_host: as drelu_host for ReLU."""
-    return _host_call(lib().bc_relu_host, "bc_relu_host", hx0, hx1, hy0, hy1, prm, seeds, elem_base, ws, chunk,
-                      stream)
+    fn, what = (lib().bc_relu_host, "bc_relu_host") if sync else (lib().bc_relu_host_async, "bc_relu_host_async")
+    return _host_call(fn, what, hx0, hx1, hy0, hy1, prm, seeds, elem_base, ws, chunk, stream)
 
 
 # ---- party-separated phases ---------------------------------------------------------

@@ -9,6 +9,7 @@
 // what makes a workspace of NS chunk slots sufficient.  Device memory is the
 // caller's workspace; the streams and events are created once per device and
 // cached (the only library-owned CUDA objects).
+#include <atomic>
 #include <mutex>
 
 #include "bc_common.cuh"
@@ -29,6 +30,7 @@ struct Ring {
   cudaStream_t s[NS];
   cudaEvent_t ev[NS];
   cudaEvent_t start;
+  std::atomic<uint64_t> next{0};  // chunk rotation continues across calls (async calls pipeline evenly)
 };
 
 std::mutex g_ring_mu;
@@ -52,7 +54,12 @@ int ring_for(int dev, Ring** out) {
 
 size_t slot_bytes(size_t chunk) { return 4 * chunk * sizeof(uint64_t); }
 
-template <bool RELU>
+// SYNC: order after the caller's stream and return with the host outputs
+// complete.  Otherwise (the _async entries) only enqueue: consecutive calls
+// share the ring streams, so call k+1's copies overlap call k's tail (chunk c
+// always runs on stream c % NS, and stream order keeps each workspace slot's
+// uses apart); the caller's stream is made to wait for every chunk.
+template <bool RELU, bool SYNC>
 int host_run(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, size_t n, uint64_t base,
              const bc_params* prm, const bc_seeds* seeds, void* ws, size_t ws_bytes, size_t chunk, void* stream) {
   const int rc = check_params(prm);
@@ -72,14 +79,19 @@ int host_run(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1,
   const int rr = ring_for(dev, &ring);
   if (rr) return rr;
   cudaStream_t caller = static_cast<cudaStream_t>(stream);
-  // order after the caller's prior work on `stream`
-  cudaEventRecord(ring->start, caller);
-  for (int i = 0; i < NS; ++i) cudaStreamWaitEvent(ring->s[i], ring->start, 0);
+  if (SYNC) {  // order after the caller's prior work on `stream`
+    cudaEventRecord(ring->start, caller);
+    for (int i = 0; i < NS; ++i) cudaStreamWaitEvent(ring->s[i], ring->start, 0);
+  }
   uint8_t* wsb = static_cast<uint8_t*>(ws);
+  // chunk -> stream (and workspace slot) by a rotation that continues across calls, so
+  // back-to-back async calls spread evenly over the ring; stream order keeps each slot's uses apart
+  const uint64_t nchunks = (n + chunk - 1) / chunk;
+  const uint64_t c0 = ring->next.fetch_add(nchunks);
   size_t c = 0;
   for (size_t a = 0; a < n; a += chunk, ++c) {
     const size_t m = (n - a < chunk) ? n - a : chunk;
-    const int k = (int)(c % NS);
+    const int k = (int)((c0 + c) % NS);
     cudaStream_t s = ring->s[k];
     uint64_t* bx0 = reinterpret_cast<uint64_t*>(wsb + k * slot_bytes(chunk));
     uint64_t* bx1 = bx0 + chunk;
@@ -98,8 +110,9 @@ int host_run(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1,
     cudaEventRecord(ring->ev[i], ring->s[i]);
     cudaStreamWaitEvent(caller, ring->ev[i], 0);
   }
-  for (int i = 0; i < NS; ++i)
-    if (cudaStreamSynchronize(ring->s[i]) != cudaSuccess) return check_launch();
+  if (SYNC)
+    for (int i = 0; i < NS; ++i)
+      if (cudaStreamSynchronize(ring->s[i]) != cudaSuccess) return check_launch();
   return check_launch();
 }
 
@@ -112,13 +125,25 @@ size_t bc_host_workspace_bytes(size_t chunk) { return NS * slot_bytes((chunk + 7
 int bc_drelu_host(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, size_t n, uint64_t elem_base,
                   const bc_params* prm, const bc_seeds* seeds, void* ws, size_t ws_bytes, size_t chunk,
                   void* stream) {
-  return host_run<false>(x0, x1, y0, y1, n, elem_base, prm, seeds, ws, ws_bytes, chunk, stream);
+  return host_run<false, true>(x0, x1, y0, y1, n, elem_base, prm, seeds, ws, ws_bytes, chunk, stream);
+}
+
+int bc_drelu_host_async(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, size_t n,
+                        uint64_t elem_base, const bc_params* prm, const bc_seeds* seeds, void* ws, size_t ws_bytes,
+                        size_t chunk, void* stream) {
+  return host_run<false, false>(x0, x1, y0, y1, n, elem_base, prm, seeds, ws, ws_bytes, chunk, stream);
 }
 
 int bc_relu_host(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, size_t n, uint64_t elem_base,
                  const bc_params* prm, const bc_seeds* seeds, void* ws, size_t ws_bytes, size_t chunk,
                  void* stream) {
-  return host_run<true>(x0, x1, y0, y1, n, elem_base, prm, seeds, ws, ws_bytes, chunk, stream);
+  return host_run<true, true>(x0, x1, y0, y1, n, elem_base, prm, seeds, ws, ws_bytes, chunk, stream);
+}
+
+int bc_relu_host_async(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, size_t n,
+                       uint64_t elem_base, const bc_params* prm, const bc_seeds* seeds, void* ws, size_t ws_bytes,
+                       size_t chunk, void* stream) {
+  return host_run<true, false>(x0, x1, y0, y1, n, elem_base, prm, seeds, ws, ws_bytes, chunk, stream);
 }
 
 }  // extern "C"

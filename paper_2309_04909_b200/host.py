@@ -24,12 +24,14 @@ class HostPipeline:
             if t.is_cuda or not t.is_pinned():
                 raise api.BicoptorError("HostPipeline expects pinned host tensors")
 
-    def drelu(self, hx0, hx1, hy0, hy1, prm, seeds, base: int = 0):
+    def drelu(self, hx0, hx1, hy0, hy1, prm, seeds, base: int = 0, sync: bool = True):
+        """sync=False enqueues only (a serving loop: consecutive requests pipeline into
+        each other); torch.cuda.synchronize(device) then completes the host outputs."""
         self._pinned(hx0, hx1, hy0, hy1)
         with torch.cuda.device(self.dev):
-            return api.drelu_host(hx0, hx1, hy0, hy1, prm, seeds, self.ws, self.chunk, base)
+            return api.drelu_host(hx0, hx1, hy0, hy1, prm, seeds, self.ws, self.chunk, base, sync=sync)
 
-    def relu(self, hx0, hx1, hy0, hy1, prm, seeds, base: int = 0):
+    def relu(self, hx0, hx1, hy0, hy1, prm, seeds, base: int = 0, sync: bool = True):
         self._pinned(hx0, hx1, hy0, hy1)
         with torch.cuda.device(self.dev):
-            return api.relu_host(hx0, hx1, hy0, hy1, prm, seeds, self.ws, self.chunk, base)
+            return api.relu_host(hx0, hx1, hy0, hy1, prm, seeds, self.ws, self.chunk, base, sync=sync)

@@ -635,6 +635,32 @@ def test_host_entry_matches_oracle(api, fn):
         assert np.array_equal(hy1.numpy().view(np.uint64), ref["y1"]), chunk
 
 
+@pytest.mark.parametrize("fn", ["drelu", "relu"])
+def test_host_entry_async_back_to_back(api, fn):
+    """bc_*_host_async: three requests enqueued back to back on one workspace (they
+    pipeline through the same stream ring), then one synchronisation; each request's
+    outputs bit-exact with the oracle."""
+    kw = PARAMS[0]
+    n, chunk = 3001, 512
+    reqs = []
+    for r in range(3):
+        base = (r + 1) << 16
+        x, x0, x1 = synth.shares(n, 64, 7, 24, "D1", run=20 + r)
+        hx0 = torch.from_numpy(x0.view(np.int64)).pin_memory()
+        hx1 = torch.from_numpy(x1.view(np.int64)).pin_memory()
+        hy0 = torch.zeros(n, dtype=torch.int64).pin_memory()
+        hy1 = torch.zeros(n, dtype=torch.int64).pin_memory()
+        reqs.append((base, x0, x1, hx0, hx1, hy0, hy1))
+    ws = api.host_workspace(chunk, DEV)
+    for base, _, _, hx0, hx1, hy0, hy1 in reqs:
+        getattr(api, fn + "_host")(hx0, hx1, hy0, hy1, api.Params(**kw), SEEDS, ws, chunk, base, sync=False)
+    torch.cuda.synchronize()
+    for base, x0, x1, _, _, hy0, hy1 in reqs:
+        ref = getattr(B, fn)(B.Params(**kw), x0, x1, np.arange(n, dtype=np.uint64) + np.uint64(base), SEEDS)
+        assert np.array_equal(hy0.numpy().view(np.uint64), ref["y0"])
+        assert np.array_equal(hy1.numpy().view(np.uint64), ref["y1"])
+
+
 def test_host_entry_errors(api):
     import ctypes
     L = api.lib()

@@ -31,6 +31,14 @@ for chunk in (1 << 19, 1 << 20, 1 << 21, 1 << 22, 1 << 23):
     for _ in range(10): ex.drelu(hx0, hx1, hy0, hy1, prm, sd)
     torch.cuda.synchronize(); dt = (time.perf_counter() - t) / 10
     out[f"chunk{chunk}"] = n / dt / 1e9
+for rep in range(2):
+    for chunk in (1 << 20, 1 << 21, 1 << 22, 1 << 23):  # the async entry, back to back (bench e2e)
+        ex = H.HostPipeline(dev, chunk=chunk)
+        for _ in range(2): ex.drelu(hx0, hx1, hy0, hy1, prm, sd, sync=False)
+        torch.cuda.synchronize(); t = time.perf_counter()
+        for _ in range(40): ex.drelu(hx0, hx1, hy0, hy1, prm, sd, sync=False)
+        torch.cuda.synchronize(); dt = (time.perf_counter() - t) / 40
+        out[f"async_chunk{chunk}_rep{rep}"] = n / dt / 1e9
 print(json.dumps(out))
 
 # the same chunked schedule with copies only (no kernel): the PCIe-side bound of the pipeline
