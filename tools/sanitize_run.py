@@ -62,5 +62,9 @@ for n in (1, 13, 1003):
     hx0, hx1 = torch.from_numpy(x0.view(np.int64)).pin_memory(), torch.from_numpy(x1.view(np.int64)).pin_memory()
     hy0, hy1 = torch.empty(n, dtype=torch.int64).pin_memory(), torch.empty(n, dtype=torch.int64).pin_memory()
     api.drelu_host(hx0, hx1, hy0, hy1, prm, sd, api.host_workspace(512, dev), 512, 8)
+    wsa = api.host_workspace(64, dev)
+    api.relu_host(hx0, hx1, hy0, hy1, prm, sd, wsa, 64, 8, sync=False)   # two async requests pipelined
+    api.drelu_host(hx0, hx1, hy0, hy1, prm, sd, wsa, 64, 8, sync=False)
+    torch.cuda.synchronize()
 torch.cuda.synchronize()
 print("sanitize_run ok")
