@@ -67,6 +67,22 @@ def _worker(rank, world, port, kind, n, chunk, slots, mode, literal, runs, outdi
     dist.destroy_process_group()
 
 
+def test_peer_runtime_gloo_single_chunk_many_slots(tmp_path):
+    """One chunk (n < chunk) through 4 ring slots, three runs: the credits that are
+    never needed inside a run are still collected at close()."""
+    import synth
+    from oracle import bicoptor as B
+    n, chunk, runs = 37, 64, 3
+    mp.start_processes(_worker, args=(3, _free_port(), "relu", n, chunk, 4, "guard", False, runs, str(tmp_path)),
+                       nprocs=3, join=True, start_method="spawn")
+    o = B.Params(**CONFIGS["guard"])
+    x, x0, x1 = synth.shares(n, o.ell, o.lx, o.f, "D1", run=0)
+    ref = B.relu(o, x0, x1, np.arange(n, dtype=np.uint64), synth.seeds(0))
+    for r in range(runs):
+        assert np.array_equal(np.load(tmp_path / f"y_0_{r}.npy"), ref["y0"])
+        assert np.array_equal(np.load(tmp_path / f"y_1_{r}.npy"), ref["y1"])
+
+
 @pytest.mark.parametrize("kind,world,slots,mode,literal", [
     ("drelu", 3, 2, "guard", False), ("drelu", 3, 3, "guard", True), ("relu", 3, 2, "guard", False),
     ("relu", 6, 2, "guard", False), ("drelu", 3, 2, "literal", False), ("relu", 3, 3, "literal", False),
