@@ -60,7 +60,7 @@ def parse():
     ap.add_argument("--only", choices=["drelu", "relu", "ladder", "drelu_rss", "relu_rss", "drelu_fp", "relu_fp",
                                        "party_drelu", "party_relu"],
                     help="profiling aid: launch one op steps+warmup times, print nothing")
-    ap.add_argument("--op", default="drelu", choices=["drelu", "relu", "drelu_fp", "relu_fp"],
+    ap.add_argument("--op", default="drelu", choices=["drelu", "relu", "drelu_fp", "relu_fp", "drelu_rss", "relu_rss"],
                     help="tuning aid (tools/variants.py): the op of the headline timing with --no-extras")
     ap.add_argument("--mode", default="sharded", choices=["sharded", "party"],
                     help="party: config 4, P0/P1/P2 on distinct GPUs (needs >= 3 ranks), ReLU over NCCL P2P")
@@ -351,8 +351,13 @@ def run_cuda(a):
     ck = Clocks(local)
     head = api.relu if a.op.startswith("relu") else api.drelu
     hprm = prm if not a.op.endswith("_fp") else api.Params(ell=ELL, lx=31, f=0, mode=MODE, rounds=a.rounds)
-    t_ms, per, clocks = timed(lambda: head(x0, x1, hprm, seeds, base, y0, y1, stream=stream),
-                              a.steps, max(a.warmup, 3), clocks=ck)
+    step = lambda: head(x0, x1, hprm, seeds, base, y0, y1, stream=stream)  # noqa: E731
+    if a.op.endswith("_rss"):  # tuning aid: the RSS kernels on replicated shares of the same x
+        xr = [torch.from_numpy(v.view(np.int64)).to(dev) for v in synth.rss_share(x, ELL, run=rank)]
+        yr = tuple(torch.empty_like(xr[0]) for _ in range(3))
+        f_rss = getattr(api, a.op)
+        step = lambda: f_rss(*xr, prm, seeds, base, out=yr, stream=stream)  # noqa: E731
+    t_ms, per, clocks = timed(step, a.steps, max(a.warmup, 3), clocks=ck)
     ms = t_ms / a.steps
     value = world * n / (ms * 1e-3)
     peaks = load_peaks()

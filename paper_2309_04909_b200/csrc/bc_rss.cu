@@ -21,7 +21,12 @@ using namespace bc::host;
 
 namespace {
 
-constexpr int TPB_RSS = 128;
+#ifndef BC_TPB_RSS
+#define BC_TPB_RSS 128
+#endif
+// threads per CTA: the staged preprocessing keystream is 576 B per thread (DReLU),
+// so the CTA size sets how many CTAs fit in shared memory
+constexpr int TPB_RSS = BC_TPB_RSS;
 
 constexpr uint64_t L_RA0 = lbl("bc2.ra00"), L_RA1 = lbl("bc2.ra01"), L_RA2 = lbl("bc2.ra02");  // seed012: alpha_k
 constexpr uint64_t L_RS01 = lbl("bc2.rs01");   // seed012: [s]_1

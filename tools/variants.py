@@ -2,7 +2,8 @@
 
     python tools/variants.py build           # here (CPU): builds paper_2309_04909_b200/variants/*.so
     python tools/variants.py time            # on the GPU box: times each variant (DReLU, R20 and R8;
-                                             # VARIANT_OP=relu|drelu_fp|relu_fp times that op instead)
+                                             # VARIANT_OP=relu|drelu_fp|relu_fp|drelu_rss|relu_rss
+                                             # times that op instead)
 """
 import itertools
 import json
