@@ -337,23 +337,25 @@ __global__ void __launch_bounds__(TPB, 2) k_finish(FinishArgs a, KP kp, Key ks) 
         y[e] = PARTY == 0 ? (t ? (1ull - d) & kp.ymask : d) : (t ? (0ull - d) & kp.ymask : d);
       }
     } else {  // Alg 8 steps 4-5
-      uint64_t x[8], ev[8], acc[8];
+      // [a]_b is not regenerated: the send phase published [d]_b = [x]_b - [a]_b, so
+      // [a]_b = [x]_b - [d]_b (mod 2^ell) from the two vectors this phase reads anyway,
+      // one ChaCha block per 8 elements fewer than drawing it again from the triple stream
+      uint64_t x[8], ev[8], acc[8], own[8];
       load8(a.x + i0, x, cnt);
       load8(a.resp + i0, ev, cnt);
       {
         uint64_t dp[8];
-        load8(a.d_own + i0, acc, cnt);
+        load8(a.d_own + i0, own, cnt);
         load8(a.d_peer + i0, dp, cnt);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] += dp[e];  // d = [d]_0 + [d]_1 (opened)
+        for (int e = 0; e < 8; ++e) acc[e] = own[e] + dp[e];  // d = [d]_0 + [d]_1 (opened)
       }
-      uint32_t Ak[16], Bk[16];
-      chacha<R>(ks, j0 >> 3, PARTY == 0 ? L_A02 : L_A12, Ak);
+      uint32_t Bk[16];
       chacha<R>(ks, j0 >> 3, PARTY == 0 ? L_B02 : L_B12, Bk);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const uint64_t d = acc[e];
-        acc[e] = d * u64_of(Bk, e) + ev[e] * u64_of(Ak, e) + (PARTY == 0 ? d * ev[e] : 0ull);
+        const uint64_t d = acc[e], ab = x[e] - own[e];  // [a]_b
+        acc[e] = d * u64_of(Bk, e) + ev[e] * ab + (PARTY == 0 ? d * ev[e] : 0ull);
       }
       if (PARTY == 0) {
         uint32_t Ck[16];
