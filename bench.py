@@ -515,8 +515,8 @@ def party_chain(api, prm, seeds, x0, x1, base, dev, stream, timed, world, n):
     # slowest party, transfers overlapped -- a projection from measured kernels, not a 3-GPU run.
     per = {}
     for name, calls in (
-            ("drelu", {"P0": lambda: (api.drelu_send(0, x0, prm, seeds.s01, base, out=(lo0, hi0, tb0), stream=stream),
-                                      api.drelu_finish(0, tb0, None, prm, n, seeds.s02, base, out=ya, stream=stream)),
+            ("drelu", {"P0": lambda: api.drelu_send(0, x0, prm, seeds.s01, base, out=(lo0, hi0, None), stream=stream,
+                                                    y=ya, seed02=seeds.s02),   # one kernel (bc_drelu_send_p0)
                        "P1": lambda: (api.drelu_send(1, x1, prm, seeds.s01, base, out=(lo1, hi1, tb1), stream=stream),
                                       api.drelu_finish(1, tb1, r1, prm, n, None, base, out=yb, stream=stream)),
                        "P2": lambda: api.drelu_helper(lo0, hi0, lo1, hi1, prm, seeds.s02, base, out=(None, r1),

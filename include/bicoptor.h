@@ -204,6 +204,16 @@ int bc_drelu_send(int party, const uint64_t *x, uint8_t *lo, uint8_t *hi, uint8_
                   size_t n, uint64_t elem_base, const bc_params *prm, const uint8_t seed01[32],
                   void *stream);
 
+/* P0's whole DReLU in the transport where P0 derives [D']_0 from seed02 itself
+ * (reading C12; P2 answers only P1): Alg 7 steps 1-8 as bc_drelu_send for
+ * party 0, and steps 10-11 in the same kernel, y[i] = t + (1-2t) q with q the
+ * seed02 response stream (the value bc_drelu_finish would compute).  y:
+ * uint64_t[n], 16-B aligned; tbits may be NULL (it is not needed afterwards).
+ * BC_EINVAL for y == NULL or seed02 == NULL. */
+int bc_drelu_send_p0(const uint64_t *x, uint8_t *lo, uint8_t *hi, uint8_t *tbits, uint64_t *y,
+                     size_t n, uint64_t elem_base, const bc_params *prm, const uint8_t seed01[32],
+                     const uint8_t seed02[32], void *stream);
+
 /* Alg 7 steps 9-10 for P2: zero test of w = W0 + W1 mod p, then
  * reshare DReLU' in Z_{2^ell}: [D']_0 = seed02 stream value (P0 can derive
  * it; written to resp0 only if resp0 != NULL, the paper-literal transport,

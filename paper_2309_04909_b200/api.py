@@ -65,6 +65,8 @@ _SIG = {
                                ctypes.POINTER(bc_seeds), ctypes.POINTER(bc_transcript), _P]),
     "bc_drelu_send": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64,
                                      ctypes.POINTER(bc_params), ctypes.c_char_p, _P]),
+    "bc_drelu_send_p0": (ctypes.c_int, [_P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64,
+                                        ctypes.POINTER(bc_params), ctypes.c_char_p, ctypes.c_char_p, _P]),
     "bc_drelu_helper": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64,
                                        ctypes.POINTER(bc_params), ctypes.c_char_p, _P]),
     "bc_drelu_finish": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64,
@@ -362,12 +364,21 @@ def msg_buffers(n: int, device, prm: "Params | None" = None):
 
 
 @_on_input_device
-def drelu_send(party, x, prm: Params, seed01: bytes, elem_base=0, out=None, stream=None):
-    """Alg 7 steps 1-8 for P0/P1: returns (lo, hi, tbits)."""
+def drelu_send(party, x, prm: Params, seed01: bytes, elem_base=0, out=None, stream=None, y=None, seed02=None):
+    """Alg 7 steps 1-8 for P0/P1: returns (lo, hi, tbits).  With y (P0 only, and seed02):
+    bc_drelu_send_p0, P0's output share computed in the same kernel (reading C12)."""
     n = x.numel()
     lo, hi, tb = msg_buffers(n, x.device, prm) if out is None else out
-    _check(lib().bc_drelu_send(party, _dev(x, "x"), _dev(lo, "lo", None), _opt(hi, "hi", None), _dev(tb, "tbits", 1), n,
-                               elem_base, ctypes.byref(prm.c()), seed01, _stream(stream)), "bc_drelu_send")
+    if y is None:
+        _check(lib().bc_drelu_send(party, _dev(x, "x"), _dev(lo, "lo", None), _opt(hi, "hi", None),
+                                   _dev(tb, "tbits", 1), n, elem_base, ctypes.byref(prm.c()), seed01,
+                                   _stream(stream)), "bc_drelu_send")
+    else:
+        if party != 0 or seed02 is None:
+            raise BicoptorError("drelu_send with y: P0 only, and seed02 is needed")
+        _check(lib().bc_drelu_send_p0(_dev(x, "x"), _dev(lo, "lo", None), _opt(hi, "hi", None), _opt(tb, "tbits", 1),
+                                      _dev(y, "y"), n, elem_base, ctypes.byref(prm.c()), seed01, seed02,
+                                      _stream(stream)), "bc_drelu_send_p0")
     return lo, hi, tb
 
 

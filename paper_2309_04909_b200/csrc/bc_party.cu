@@ -17,8 +17,25 @@ struct SendArgs {
   uint8_t* tbits;
   uint64_t* dshare;
   uint64_t* dpeer;  // nullable: second destination of [d]_b (the other computing party's inbox)
+  uint64_t* y0;     // nullable (DReLU, P0): P0's output share, computed in the same kernel
   uint64_t n, base;
 };
+
+// Alg 7 steps 10-11 for P0 inside its send kernel (the transport in which P0
+// derives [D']_0 from seed02 itself, reading C12): y0 = t + (1-2t) q.
+template <int R>
+__device__ __forceinline__ void send_finish_p0(const SendArgs& a, const KP& kp, const Key& k02, uint64_t i0,
+                                               uint64_t j0, uint32_t cnt, uint32_t tb) {
+  uint32_t Q[16];
+  chacha<R>(k02, j0 >> 3, L_RESP, Q);
+  uint64_t y[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const uint64_t t = (tb >> e) & 1u;
+    y[e] = (t + (1ull - 2ull * t) * u64_of(Q, e)) & kp.ymask;
+  }
+  store8(a.y0 + i0, y, cnt);
+}
 
 __device__ __forceinline__ void store_msg(const SendArgs& a, const KP& kp, const Key& ktr, uint64_t g, uint64_t i0,
                                           uint64_t j0, uint32_t cnt, const uint64_t (&lo)[8], uint64_t hi,
@@ -76,6 +93,7 @@ __global__ void __launch_bounds__(TPB, 2) k_send_c(SendArgs a, KP kp, Key k01, K
     }
     store_msg(a, kp, ktr, g, i0, j0, cnt, lo, hi, tb, PARTY, false);
     if (RELU) send_dshare<R, PARTY>(a, kp, ktr, i0, j0, cnt);
+    if (!RELU && PARTY == 0 && a.y0) send_finish_p0<R>(a, kp, ktr, i0, j0, cnt, tb);
   }
 }
 
@@ -109,6 +127,7 @@ __global__ void __launch_bounds__(TPB, 2) k_send_w(SendArgs a, KP kp, Key k01, K
     }
     store_msg(a, kp, ktr, g, i0, j0, cnt, lo, hi, tb, PARTY, false);
     if (RELU) send_dshare<R, PARTY>(a, kp, ktr, i0, j0, cnt);
+    if (!RELU && PARTY == 0 && a.y0) send_finish_p0<R>(a, kp, ktr, i0, j0, cnt, tb);
   }
 }
 
@@ -136,6 +155,7 @@ __global__ void __launch_bounds__(TPB_LARGE) k_send_l(SendArgs a, KP kp, KPL kl,
   const uint64_t warps = (uint64_t)gridDim.x * (TPB_LARGE / 32);
   for (uint64_t wb = ((uint64_t)blockIdx.x * (TPB_LARGE / 32) + threadIdx.x / 32) * 256; wb < a.n;
        wb += warps * 256) {
+    uint32_t tgroup = 0;
 #pragma unroll 1
     for (uint32_t e = 0; e < 8; ++e) {
       const uint64_t i = wb + 32 * e + lane;
@@ -148,7 +168,15 @@ __global__ void __launch_bounds__(TPB_LARGE) k_send_l(SendArgs a, KP kp, KPL kl,
       }
       const uint32_t bal = __ballot_sync(0xFFFFFFFFu, tb != 0u);  // t of elements wb + 32 e + 0..31
       const uint64_t byte = (wb + 32 * e) / 8 + lane;
-      if (lane < 4 && byte < nbytes) a.tbits[byte] = (uint8_t)(bal >> (8 * lane));
+      if (lane < 4 && byte < nbytes && a.tbits) a.tbits[byte] = (uint8_t)(bal >> (8 * lane));
+      if ((lane >> 2) == e) tgroup = (bal >> (8 * (lane & 3u))) & 0xFFu;  // t bits of lane's group
+    }
+    if (!RELU && PARTY == 0 && a.y0) {
+      const uint64_t g = wb / 8 + lane;
+      if (g < ngroups) {
+        const uint64_t i0 = g << 3;
+        send_finish_p0<R>(a, kp, ktr, i0, a.base + i0, (uint32_t)min((uint64_t)8, a.n - i0), tgroup);
+      }
     }
     if (RELU) {
       const uint64_t g = wb / 8 + lane;
@@ -169,7 +197,7 @@ __device__ __forceinline__ void store_msg(const SendArgs& a, const KP& kp, const
     else
       for (uint32_t e = 0; e < cnt; ++e) a.hi[i0 + e] = (uint8_t)(hi >> (8 * e));
   }
-  a.tbits[g] = (uint8_t)(tb & ((1u << cnt) - 1u));
+  if (a.tbits) a.tbits[g] = (uint8_t)(tb & ((1u << cnt) - 1u));
 }
 
 struct HelperArgs {
@@ -380,11 +408,15 @@ __global__ void __launch_bounds__(TPB, 2) k_finish(FinishArgs a, KP kp, Key ks) 
 
 template <bool RELU>
 int send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits, uint64_t* dshare, uint64_t* dpeer,
-         size_t n, uint64_t base, const bc_params* prm, const uint8_t* s01, const uint8_t* str, void* stream) {
+         size_t n, uint64_t base, const bc_params* prm, const uint8_t* s01, const uint8_t* str, void* stream,
+         uint64_t* y0 = nullptr) {
   const int rc = check_params(prm);
   if (rc) return rc;
   if (n == 0) return BC_OK;  // no-op after parameter validation
-  if ((party != 0 && party != 1) || !x || !lo || !tbits || !s01 || (RELU && (!dshare || !str))) return BC_EINVAL;
+  if ((party != 0 && party != 1) || !x || !lo || (!tbits && !y0) || !s01 || (RELU && (!dshare || !str)))
+    return BC_EINVAL;
+  if (y0 && (RELU || party != 0 || !str)) return BC_EINVAL;  // P0's DReLU output needs seed02 (in str)
+  if (y0 && !aligned16(y0)) return BC_EALIGN;
   const bool large = prm->tape == BC_TAPE_LARGE;
   if (!hi && prm->p > (large ? 0xFFFFFFFFull : 256ull)) return BC_EINVAL;  // the high-bit plane is needed
   if (!RELU && dpeer) return BC_EINVAL;
@@ -397,12 +429,13 @@ int send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits,
   if (overlap(lo, nlo, x, nb) || overlap(hi, nhi, x, nb) || overlap(tbits, (n + 7) / 8, x, nb) ||
       overlap(lo, nlo, hi, nhi) || overlap(lo, nlo, tbits, (n + 7) / 8) || overlap(hi, nhi, tbits, (n + 7) / 8) ||
       (RELU && (overlap(dshare, nb, x, nb) || overlap(dshare, nb, lo, nlo) || overlap(dshare, nb, hi, nhi))) ||
-      overlap(dpeer, nb, x, nb) || overlap(dpeer, nb, dshare, nb))
+      overlap(dpeer, nb, x, nb) || overlap(dpeer, nb, dshare, nb) || overlap(y0, nb, x, nb) ||
+      overlap(y0, nb, lo, nlo) || overlap(y0, nb, hi, nhi) || overlap(y0, nb, tbits, (n + 7) / 8))
     return BC_EALIAS;
-  SendArgs a{x, lo, hi, tbits, dshare, dpeer, (uint64_t)n, base};
+  SendArgs a{x, lo, hi, tbits, dshare, dpeer, y0, (uint64_t)n, base};
   const KP kp = make_kp(prm);
   const Key k01 = make_key(s01);
-  const Key ktr = RELU ? make_key(str) : Key{};
+  const Key ktr = (RELU || y0) ? make_key(str) : Key{};  // triple seed (ReLU) or seed02 (P0's DReLU output)
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint64_t ngroups = (n + 7) / 8;
   return dispatch_rounds(prm->rounds, [&](auto Rc) {
@@ -504,6 +537,13 @@ extern "C" {
 int bc_drelu_send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits, size_t n,
                   uint64_t elem_base, const bc_params* prm, const uint8_t seed01[32], void* stream) {
   return send<false>(party, x, lo, hi, tbits, nullptr, nullptr, n, elem_base, prm, seed01, nullptr, stream);
+}
+
+int bc_drelu_send_p0(const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits, uint64_t* y, size_t n,
+                     uint64_t elem_base, const bc_params* prm, const uint8_t seed01[32], const uint8_t seed02[32],
+                     void* stream) {
+  if (!y) return BC_EINVAL;
+  return send<false>(0, x, lo, hi, tbits, nullptr, nullptr, n, elem_base, prm, seed01, seed02, stream, y);
 }
 
 int bc_drelu_helper(const uint8_t* lo0, const uint8_t* hi0, const uint8_t* lo1, const uint8_t* hi1, uint64_t* resp0,

@@ -250,12 +250,15 @@ class PeerPartyRunner:
                 link = L["A"] if p == 0 else L["B"]
                 dst = link.acquire(seq, be, g)
                 tb = self.tb[a // 8:(b + 7) // 8]
-                c.drelu_send(p, x[a:b], self.prm, self.seed["s01"], base, out=(*self._send_out(dst, m), tb))  # steps 1-8
-                link.publish(seq, be, g, W)
                 if p == 1 or self.literal:
+                    c.drelu_send(p, x[a:b], self.prm, self.seed["s01"], base,
+                                 out=(*self._send_out(dst, m), tb))                                  # steps 1-8
+                    link.publish(seq, be, g, W)
                     lag.append((k, seq, a, b, tb))
-                else:  # P0 derives [D']_0 from seed02 (reading C12): nothing to wait for
-                    c.drelu_finish(0, tb, None, self.prm, m, self.seed["s02"], base, out=out[a:b])
+                else:  # P0 derives [D']_0 from seed02 (reading C12): steps 1-8 and 10-11 in one kernel
+                    c.drelu_send(0, x[a:b], self.prm, self.seed["s01"], base, out=(*self._send_out(dst, m), None),
+                                 y=out[a:b], seed02=self.seed["s02"])
+                    link.publish(seq, be, g, W)
                 if len(lag) > 1:
                     self._drelu_finish(*lag.pop(0), out)
             else:

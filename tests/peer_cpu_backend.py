@@ -63,11 +63,14 @@ class FileBackend:
 
 
 class OracleApiCompute(OracleCompute):
-    def drelu_send(self, party, x, prm, seed01, base, out):
+    def drelu_send(self, party, x, prm, seed01, base, out, y=None, seed02=None):
         lo, hi, tb = super().drelu_send(party, x, prm, seed01, base)
         out[0].copy_(lo)
         out[1].copy_(hi)
-        out[2].copy_(tb)
+        if out[2] is not None:
+            out[2].copy_(tb)
+        if y is not None:  # bc_drelu_send_p0: P0's output share in the same call
+            self.drelu_finish(0, tb, None, prm, x.numel(), seed02, base, y)
         return out
 
     def drelu_helper(self, lo0, hi0, lo1, hi1, prm, seed02, base, paper_literal=False, out=None):

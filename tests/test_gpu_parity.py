@@ -297,6 +297,11 @@ def test_party_phases_match_oracle_and_fused(api, kw):
     y1 = api.drelu_finish(1, tb1, r1, prm, n, None, base)
     f0, f1 = api.drelu(t0, t1, prm, SEEDS, elem_base=base)
     assert torch.equal(ya, f0) and torch.equal(yb, f0) and torch.equal(y1, f1)
+    # P0's send with its output in the same kernel (bc_drelu_send_p0): same message, same share
+    yp = torch.empty_like(t0)
+    lp, hp, _ = api.drelu_send(0, t0, prm, SEEDS.s01, base, out=(*api.msg_buffers(n, DEV, prm)[:2], None),
+                               y=yp, seed02=SEEDS.s02)
+    assert torch.equal(yp, f0) and torch.equal(lp, lo0) and (api.wire_format(prm)["hi"] is None or torch.equal(hp, hi0))
     # ReLU
     L0, H0, T0, d0 = api.relu_send(0, t0, prm, SEEDS.s01, SEEDS.s02, base)
     L1, H1, T1, d1 = api.relu_send(1, t1, prm, SEEDS.s01, SEEDS.s12, base)

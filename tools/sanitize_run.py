@@ -25,6 +25,7 @@ for kw in (dict(), dict(ell=16, lx=7, f=0, mode="literal"), dict(ell=32, lx=5, f
         lo1, hi1, tb1 = api.drelu_send(1, a1, prm, sd.s01, 8)
         r0, r1 = api.drelu_helper(lo0, hi0, lo1, hi1, prm, sd.s02, 8, paper_literal=True)
         api.drelu_finish(0, tb0, None, prm, n, sd.s02, 8); api.drelu_finish(1, tb1, r1, prm, n, None, 8)
+        api.drelu_send(0, a0, prm, sd.s01, 8, out=(lo0, hi0, None), y=torch.empty_like(a0), seed02=sd.s02)
         L0, H0, T0, d0 = api.relu_send(0, a0, prm, sd.s01, sd.s02, 8)
         L1, H1, T1, d1 = api.relu_send(1, a1, prm, sd.s01, sd.s12, 8)
         e, c1 = api.relu_helper(L0, H0, L1, H1, prm, sd.s02, sd.s12, 8)
@@ -50,6 +51,7 @@ for n in (1, 13, 1003):
         lo1, hi1, tb1 = api.drelu_send(1, b1, pk, sd.s01, 8)
         r0, r1 = api.drelu_helper(lo0, hi0, lo1, hi1, pk, sd.s02, 8, paper_literal=True)
         api.drelu_finish(1, tb1, r1, pk, n, None, 8)
+        api.drelu_send(0, b0, pk, sd.s01, 8, out=(lo0, hi0, None), y=torch.empty_like(b0), seed02=sd.s02)
         dp = torch.empty_like(b0)
         L0, H0, T0, d0 = api.relu_send(0, b0, pk, sd.s01, sd.s02, 8, d_peer=dp)
         L1, H1, T1, d1 = api.relu_send(1, b1, pk, sd.s01, sd.s12, 8)
