@@ -4,6 +4,8 @@ and the party phases compared element by element with the oracle, messages
 included.  Complements the hand-picked cases of test_gpu_parity.py with
 combinations nobody chose (odd ell, windows touching the top bit, ragged n,
 large bases)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -42,7 +44,7 @@ def _draw(rng):
             continue
 
 
-CASES = list(range(120))
+CASES = list(range(int(os.environ.get("BC_FUZZ_CASES", "120"))))  # BC_FUZZ_CASES: longer sweeps
 
 
 @pytest.fixture(scope="module")
@@ -85,7 +87,7 @@ def test_random_parameters(api, case):
     assert np.array_equal(host(api.drelu_finish(1, tb1, r1, prm, n, None, base)), ref["y1"])
 
 
-@pytest.mark.parametrize("case", list(range(40)))
+@pytest.mark.parametrize("case", list(range(int(os.environ.get("BC_FUZZ_CASES", "120")) // 3)))
 def test_random_widened_rows(api, case):
     """The widened rows under random parameters: RSS DReLU / ReLU (compact tape:
     lx = 7 guard, random ell and f), the Bicoptor-1 comparison (slots <= 8), the
