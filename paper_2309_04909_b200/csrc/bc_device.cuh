@@ -49,6 +49,9 @@ struct KP {
   uint32_t fact;       // S!
   uint32_t mask_lim;   // floor(65536 / (p-1)) * (p-1)
   uint32_t rho_lim;    // floor(65536 / p) * p
+  // magic multipliers of the wide tape's runtime divisions (exact for the ranges used):
+  uint32_t mag_p, mag_q;   // ceil(2^32 / p), ceil(2^32 / (p-1)): x / d = umulhi(x, mag) for x < 2^16
+  uint32_t mag_f, sh_f;    // ceil(2^(31+l) / S!), l - 1 (l = ceil(log2 S!)): x / S! = umulhi(x, mag_f) >> sh_f, x < 2^31
 };
 
 // ---------------------------------------------------------------------------
@@ -265,13 +268,18 @@ __device__ __forceinline__ void decode_wide(const uint32_t* T, uint64_t j, const
     d.ur[m] = (T[5 + m / 2] >> (16 * (m & 1))) & 0xFFFFu;
     if ((uint32_t)m < kp.S) bad |= (d.um[m] >= kp.mask_lim) | (d.ur[m] >= kp.rho_lim);
   }
-  if (__builtin_expect(bad, 0)) fallback<R>(d, j, k01, kp.S, kp.perm_lim, kp.mask_lim, kp.rho_lim);
-#pragma unroll
-  for (int m = 0; m < 8; ++m) {
-    tp.r[m] = 1u + d.um[m] % (kp.p - 1u);
-    tp.rho[m] = d.ur[m] % kp.p;
+  if (__builtin_expect(bad, 0)) {  // the addressable copy lives on the rare path only
+    Draws f = d;
+    fallback<R>(f, j, k01, kp.S, kp.perm_lim, kp.mask_lim, kp.rho_lim);
+    d = f;
   }
-  tp.sel = perm_sel_rt(d.idx % kp.fact, kp.S);
+  const uint32_t q = kp.p - 1u;
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {  // draws < 2^16: one IMAD.HI per division (magics from the host)
+    tp.r[m] = 1u + d.um[m] - q * __umulhi(d.um[m], kp.mag_q);
+    tp.rho[m] = d.ur[m] - kp.p * __umulhi(d.ur[m], kp.mag_p);
+  }
+  tp.sel = perm_sel_rt(d.idx - kp.fact * (__umulhi(d.idx, kp.mag_f) >> kp.sh_f), kp.S);
 }
 
 // ---------------------------------------------------------------------------

@@ -109,6 +109,14 @@ KP make_kp(const bc_params* prm) {
     kp.perm_lim = (uint32_t)((0x80000000ull / kp.fact) * kp.fact);
     kp.mask_lim = (65536u / (kp.p - 1u)) * (kp.p - 1u);
     kp.rho_lim = (65536u / kp.p) * kp.p;
+    // x / d for x < 2^16, d <= 257: ceil(2^32 / d) overshoots 2^32/d by e < 1, and x e / 2^32 < 1/d
+    kp.mag_p = (uint32_t)(((1ull << 32) + kp.p - 1) / kp.p);
+    kp.mag_q = (uint32_t)(((1ull << 32) + kp.p - 2) / (kp.p - 1u));
+    // x / S! for x < 2^31 (round-up method, l = ceil(log2 S!)): m = ceil(2^(31+l) / S!) < 2^32
+    uint32_t l = 0;
+    while ((1ull << l) < kp.fact) ++l;
+    kp.mag_f = (uint32_t)(((1ull << (31 + l)) + kp.fact - 1) / kp.fact);
+    kp.sh_f = l - 1;
   }
   return kp;
 }

@@ -179,3 +179,30 @@ def test_fpmod48_quotient_exact():
             us += [m * q + d for m in k for d in (-1, 0, 1, q // 2, q - 1) if 0 <= m * q + d < (1 << 48)]
             for u in us:
                 assert _fp_quotient(u >> s, qo) == u // q, (w, q, u)
+
+
+def test_wide_tape_magic_divisions():
+    """The wide tape's runtime divisions by host-computed magics (KP::mag_p, mag_q,
+    mag_f): x / d = umulhi(x, ceil(2^32/d)) for every 16-bit draw and every d = p, p-1
+    of a wide-tape setting (w = 2..8); x / S! = umulhi(x, ceil(2^(31+l)/S!)) >> (l-1)
+    for 31-bit indices (l = ceil(log2 S!)), sampled plus the multiples' edges."""
+    import math
+    from oracle.ring import prime_above
+    x16 = np.arange(1 << 16, dtype=np.uint64)
+    for w in range(2, 9):
+        p = prime_above(w)
+        for d in (p, p - 1):
+            mag = np.uint64(((1 << 32) + d - 1) // d)
+            assert np.array_equal((x16 * mag) >> np.uint64(32), x16 // np.uint64(d)), (w, d)
+    rng = np.random.default_rng(3)
+    for S in range(3, 9):
+        f = math.factorial(S)
+        l = (f - 1).bit_length()
+        mag = ((1 << (31 + l)) + f - 1) // f
+        assert mag < (1 << 32)
+        xs = np.concatenate([rng.integers(0, 1 << 31, 100000, dtype=np.uint64),
+                             np.array([0, f - 1, f, (1 << 31) - 1], dtype=np.uint64),
+                             np.arange(1, 2000, dtype=np.uint64) * np.uint64(f) - np.uint64(1)])
+        xs = xs[xs < (1 << 31)]
+        q = ((xs * np.uint64(mag)) >> np.uint64(32)) >> np.uint64(l - 1)
+        assert np.array_equal(q, xs // np.uint64(f)), S
