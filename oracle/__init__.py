@@ -15,7 +15,12 @@ Modules
   chacha    -- RFC 8439 ChaCha block function and keystream addressing (the
                PRG the paper leaves unnamed; reading C19 in DESIGN.md).
   ring      -- cut / LT / Alg 1, 4, 5 truncation / Alg 6 modulo switch.
-  bicoptor  -- Alg 7 UBL DReLU, Alg 8 UBL ReLU, per party and composed.
+  bicoptor  -- Alg 7 UBL DReLU, Alg 8 UBL ReLU, per party and composed; the
+               compact, wide and large (full precision) tapes; wire formats.
+  rss       -- Alg 9 RSS DReLU and the RSS ReLU.
+  trunc     -- the truncation study: Alg 1 / 2 e0-e1 classes, exact mask counting,
+               Alg 3 trc-then-mult against mult-then-trc.
+  bicoptor1 -- Bicoptor-1's DReLU as Bicoptor 2.0 describes it.
 
 Pins (what fixes each function independently of itself) are listed in
 DESIGN.md section "Oracle and its pins"; functions without one say
