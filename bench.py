@@ -45,7 +45,7 @@ BLOCKS_PER_ELEM = {"drelu": 0.5, "relu": 1.0,   # 3/8 (tap
                    "drelu_fp": 7.125, "relu_fp": 7.625}  # lx=31 large tape: 7 blocks + the finish streams
 BYTES_PER_ELEM = {"drelu": 32, "relu": 32, "ladder": 16,   # algorithmic HBM bytes per element
                   "drelu_rss": 48, "relu_rss": 48, "drelu_fp": 32, "relu_fp": 32}
-SM_COUNT_B200 = 148
+SM_COUNT_B200 = 148  # nominal; the roofline uses the device's own count
 
 
 def parse():
@@ -364,7 +364,8 @@ def run_cuda(a):
     traffic = load_traffic()
     clk_mhz = peaks["sm_max_mhz"]
     # ALU pipe (LOP3/SHF/PRMT/IADD3): 1 warp instruction per 2 clk per SMSP = 16 lanes/clk/SMSP
-    alu_peak = SM_COUNT_B200 * 4 * 16 * clk_mhz * 1e6 / 1e12  # Tops/s
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count or SM_COUNT_B200
+    alu_peak = sms * 4 * 16 * clk_mhz * 1e6 / 1e12  # Tops/s
 
     def roofline(kind, elems_per_s, launch_ms):
         bytes_ = BYTES_PER_ELEM[kind]
@@ -377,7 +378,7 @@ def run_cuda(a):
             out.update({"bound": "alu", "achieved": ach, "peak": alu_peak, "unit": "Tops/s", "frac": ach / alu_peak,
                         "ops_per_elem": ops,
                         "ops_note": "ChaCha xor+rotate word ops (ALU pipe) per element; protocol ops not counted",
-                        "peak_note": f"ALU pipe: 148 SM x 4 SMSP x 16 lanes/clk x {clk_mhz:.0f} MHz ({peaks['src']} sm_max)"})
+                        "peak_note": f"ALU pipe: {sms} SM x 4 SMSP x 16 lanes/clk x {clk_mhz:.0f} MHz ({peaks['src']} sm_max)"})
         else:
             out.update({"bound": "hbm", "achieved": hbm_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                         "frac": hbm_gbs / peaks["hbm_gbs"]})
