@@ -291,6 +291,11 @@ __device__ __forceinline__ void decode_wide(const uint32_t* T, uint64_t j, const
 //   6   shuffle: PRMT with the permutation selector
 //   7-8 W_m = v'_m r_m + rho_m (P0) / v'_m r_m - rho_m (P1)  mod p
 // ---------------------------------------------------------------------------
+// x mod p for x < 2^24 by the host's magic (KP::mag_p = ceil(2^32 / p), p <= 257): exact.
+__device__ __forceinline__ uint32_t modp_small(uint32_t x, const KP& kp) {
+  return x - kp.p * __umulhi(x, kp.mag_p);
+}
+
 template <int PARTY>
 __device__ __forceinline__ void party_W_wide(uint64_t x, const KP& kp, const Tape& tp, uint32_t (&W)[8]) {
   const uint64_t nx = 0ull - x;
@@ -311,8 +316,8 @@ __device__ __forceinline__ void party_W_wide(uint64_t x, const KP& kp, const Tap
       const uint32_t nxt = ((uint32_t)i < kp.lx) ? u[i + 1] : 0u;
       uint32_t vi = (u[i] + nxt - (PARTY == 0 ? 1u : 0u)) & kp.wmask;  // step 4
       uint32_t vp;                                                      // step 5 (Alg 6)
-      if (PARTY == 0) vp = (vi == 0) ? ((1u << kp.w) % kp.p) : vi % kp.p;
-      else vp = (kp.p + vi - (1u << kp.w)) % kp.p;
+      if (PARTY == 0) vp = (vi == 0) ? modp_small(1u << kp.w, kp) : modp_small(vi, kp);
+      else vp = modp_small(kp.p + vi - (1u << kp.w), kp);
       e = vp - 1u;
     }
     if (i < 4) bytes_lo |= e << (8 * i); else bytes_hi |= e << (8 * (i - 4));
@@ -323,7 +328,7 @@ __device__ __forceinline__ void party_W_wide(uint64_t x, const KP& kp, const Tap
   for (int m = 0; m < 8; ++m) {
     const uint32_t c = byte_of(m < 4 ? P_lo : P_hi, m & 3) + 1u;
     const uint32_t rr = (PARTY == 0) ? tp.rho[m] : (kp.p - tp.rho[m]);
-    W[m] = ((uint32_t)m < kp.S) ? (c * tp.r[m] + rr) % kp.p : 0u;
+    W[m] = ((uint32_t)m < kp.S) ? modp_small(c * tp.r[m] + rr, kp) : 0u;  // < 257 * 257 + 257
   }
 }
 

@@ -115,8 +115,8 @@ __device__ __forceinline__ uint64_t ladder_bytes(uint64_t x, const KP& kp, bool 
       const uint32_t nxt = ((uint32_t)i < kp.lx) ? u[i + 1] : 0u;
       const uint32_t vi = (u[i] + nxt - (PARTY == 0 ? 1u : 0u)) & kp.wmask;
       uint32_t vp;
-      if (PARTY == 0) vp = (vi == 0) ? ((1u << kp.w) % kp.p) : vi % kp.p;
-      else vp = (kp.p + vi - (1u << kp.w)) % kp.p;
+      if (PARTY == 0) vp = (vi == 0) ? modp_small(1u << kp.w, kp) : modp_small(vi, kp);
+      else vp = modp_small(kp.p + vi - (1u << kp.w), kp);
       out |= (uint64_t)(vp - 1u) << (8 * i);
     }
   }
