@@ -264,3 +264,48 @@ def test_party_composition_matches_drelu():
     lo, hi = B.encode_msg(m0["W"])
     back = lo[:, :8].astype(np.uint64) | ((hi[:, None] >> np.arange(8, dtype=np.uint8)) & 1).astype(np.uint64) << np.uint64(8)
     assert np.array_equal(back, m0["W"])
+
+
+def test_compact_lit_tape_raw_draws():
+    """Compact literal tape (p = 131, 8 slots, layout spec DESIGN.md §4): re-read the
+    32 keystream bytes of each element from whole ChaCha blocks (element j = bytes
+    [32 j, 32 j + 32) of the bc2.tpl1 stream), take the 14-bit draws as bit strings,
+    and check r_m = 1 + u mod 130 and rho_m = u mod 131 on unrejected elements; on a
+    rejected element the rejected draw is replaced by the first fallback word whose
+    low 14 bits fall below the limit."""
+    from oracle.chacha import chacha_blocks
+    prm = B.Params(ell=16, lx=7, f=0, mode="literal")
+    assert prm.layout == "compact_lit" and prm.p == 131
+    n = 4000
+    blocks = chacha_blocks(SEEDS.s01, B.L_TAPECL, list(range(n // 2)), prm.rounds)
+    raw = np.asarray(blocks, dtype="<u4").tobytes()
+    tp = B.tape(prm, SEEDS.s01, np.arange(n, dtype=np.uint64))
+    ok_rows, rej = 0, []
+    for jj in range(n):
+        e = raw[32 * jj: 32 * jj + 32]
+        w0 = int.from_bytes(e[:4], "little")
+        bits = "".join(format(b, "08b")[::-1] for b in e[4:])  # LSB-first bit string of D
+        u = [int(bits[14 * i: 14 * i + 14][::-1], 2) for i in range(16)]
+        assert int(tp["t"][jj]) == w0 >> 31
+        if (w0 & 0x7FFFFFFF) >= 53261 * 40320 or any(v >= 16380 for v in u[:8]) or \
+                any(v >= 16375 for v in u[8:]):
+            rej.append((jj, u, w0))
+            continue
+        ok_rows += 1
+        assert [int(v) for v in tp["r"][jj]] == [1 + v % 130 for v in u[:8]]
+        assert [int(v) for v in tp["rho"][jj]] == [v % 131 for v in u[8:]]
+    assert ok_rows > 3000 and rej
+    # a rejected draw (index accepted, exactly one draw rejected) takes the fallback stream
+    for jj, u, w0 in rej:
+        bad = [i for i, v in enumerate(u) if v >= (16380 if i < 8 else 16375)]
+        if (w0 & 0x7FFFFFFF) >= 53261 * 40320 or len(bad) != 1:
+            continue
+        i = bad[0]
+        lim = 16380 if i < 8 else 16375
+        fb = [int(w) & 0x3FFF for w in chacha_blocks(SEEDS.s01, B.L_FALLBACK, [jj * 256], prm.rounds)[0]]
+        v = next(w for w in fb if w < lim)
+        got = int(tp["r"][jj, i]) if i < 8 else int(tp["rho"][jj, i - 8])
+        assert got == (1 + v % 130 if i < 8 else v % 131)
+        break
+    else:
+        pytest.fail("no single-rejection element found")
