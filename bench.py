@@ -432,7 +432,7 @@ def run_cuda(a):
         pl = api.Params(ell=ELL, lx=LX, f=F, mode="literal", rounds=a.rounds)
         tl_, _, _ = timed(lambda: api.drelu(x0, x1, pl, seeds, base, y0, y1, stream=stream), 50, 3)
         var["literal"] = {"drelu": world * n / (tl_ / 50 * 1e-3),
-                          "note": "mode=literal (w = lx = 7, p = 131): wide tape, 64 B of keystream per element"}
+                          "note": "mode=literal (w = lx = 7, p = 131): compact literal tape, 32 B of keystream per element"}
         line["variants"] = var
         # ---- config 2: ladder + modswitch (Alg 7 steps 3-5), HBM-bound, at config 2's 2^28 ----
         n2 = 1 << 28

@@ -53,7 +53,8 @@ extern "C" {
 /* PRG tape layouts. */
 #define BC_TAPE_WIDE    0 /* lx <= 7, p <= 257 other than the compact case: 64 B / element */
 #define BC_TAPE_COMPACT 1 /* p = 257 and 8 slots (lx = 7 guard): 24 B / element            */
-#define BC_TAPE_LARGE   2 /* lx >= 8, up to 32 slots and p < 2^33: 576 B / element          */
+#define BC_TAPE_LARGE   2 /* lx >= 8, up to 32 slots and p < 2^33: 448 B / element          */
+#define BC_TAPE_COMPACT_LIT 3 /* p = 131 and 8 slots (lx = 7 literal): 32 B / element, 14-bit draws */
 
 /* Protocol parameters (Alg 7 "Setting"; key bits, sec. 6.1).
  *   ell    ring bits, 2..64

@@ -22,6 +22,7 @@ __host__ __device__ constexpr uint64_t lbl(const char (&s)[9]) {
 constexpr uint64_t L_TAPEA = lbl("bc2.tpa1");  // seed01, 16 B / element (compact tape, part A)
 constexpr uint64_t L_TAPEB = lbl("bc2.tpb1");  // seed01,  8 B / element (compact tape, part B)
 constexpr uint64_t L_TAPEW = lbl("bc2.tapw");  // seed01, 64 B / element (wide)
+constexpr uint64_t L_TAPECL = lbl("bc2.tpl1"); // seed01, 32 B / element (compact literal: p = 131, 8 slots)
 constexpr uint64_t L_FB = lbl("bc2.fb01");     // seed01, fallback, counter j*256+k
 constexpr uint64_t L_RESP = lbl("bc2.resp");   // seed02, [DReLU']_0
 constexpr uint64_t L_A02 = lbl("bc2.ta02");    // seed02, [a]_0
@@ -217,7 +218,8 @@ struct Draws {  // raw draws of one element: perm index, 8 mask u16, 8 reshare u
 
 template <int R>
 __device__ __noinline__ void fallback(Draws& d, uint64_t j, Key key, uint32_t S, uint32_t perm_lim,
-                                      uint32_t mask_lim /*0: masks never rejected*/, uint32_t rho_lim) {
+                                      uint32_t mask_lim /*0: masks never rejected*/, uint32_t rho_lim,
+                                      uint32_t dmask /*draw width: 0xFFFF wide, 0x3FFF compact literal*/) {
   FbStream<R> fb;
   fb.key = key; fb.j = j; fb.pos = 16; fb.kc = 0;
   if (d.idx >= perm_lim) {
@@ -228,15 +230,15 @@ __device__ __noinline__ void fallback(Draws& d, uint64_t j, Key key, uint32_t S,
   if (mask_lim) {
     for (uint32_t m = 0; m < S; ++m)
       if (d.um[m] >= mask_lim) {
-        uint32_t v = fb.next() & 0xFFFFu;
-        while (v >= mask_lim) v = fb.next() & 0xFFFFu;
+        uint32_t v = fb.next() & dmask;
+        while (v >= mask_lim) v = fb.next() & dmask;
         d.um[m] = v;
       }
   }
   for (uint32_t m = 0; m < S; ++m)
     if (d.ur[m] >= rho_lim) {
-      uint32_t v = fb.next() & 0xFFFFu;
-      while (v >= rho_lim) v = fb.next() & 0xFFFFu;
+      uint32_t v = fb.next() & dmask;
+      while (v >= rho_lim) v = fb.next() & dmask;
       d.ur[m] = v;
     }
 }
@@ -270,7 +272,7 @@ __device__ __forceinline__ void decode_wide(const uint32_t* T, uint64_t j, const
   }
   if (__builtin_expect(bad, 0)) {  // the addressable copy lives on the rare path only
     Draws f = d;
-    fallback<R>(f, j, k01, kp.S, kp.perm_lim, kp.mask_lim, kp.rho_lim);
+    fallback<R>(f, j, k01, kp.S, kp.perm_lim, kp.mask_lim, kp.rho_lim, 0xFFFFu);
     d = f;
   }
   const uint32_t q = kp.p - 1u;
@@ -280,6 +282,39 @@ __device__ __forceinline__ void decode_wide(const uint32_t* T, uint64_t j, const
     tp.rho[m] = d.ur[m] - kp.p * __umulhi(d.ur[m], kp.mag_p);
   }
   tp.sel = perm_sel_rt(d.idx - kp.fact * (__umulhi(d.idx, kp.mag_f) >> kp.sh_f), kp.S);
+}
+
+// Compact literal tape (p = 131, 8 slots; the paper-literal domain at lx = 7): 32 B per element,
+// two elements per block (label bc2.tpl1); T[0..7] = keystream bytes [32 j, 32 j + 32).
+//   T0: t | perm index (reject >= floor(2^31/8!) 8!)
+//   T1..T7 as one 224-bit little-endian D: u_i = (D >> 14 i) & 0x3FFF, i < 8 masks
+//   (r_m = 1 + u mod 130, reject >= 16380), i >= 8 reshares (rho_m = u mod 131, reject >= 16375).
+// KP carries the 14-bit limits (make_kp); the fallback stream yields low-14-bit draws.
+template <int R>
+__device__ __forceinline__ void decode_cl(const uint32_t* T, uint64_t j, const Key& k01, const KP& kp, Tape& tp) {
+  Draws d;
+  tp.t = T[0] >> 31;
+  d.idx = T[0] & 0x7FFFFFFFu;
+  bool bad = d.idx >= kp.perm_lim;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int bit = 14 * i, w = bit >> 5, sh = bit & 31;
+    const uint32_t nxt = w < 6 ? T[2 + w] : 0u;
+    const uint32_t v = __funnelshift_r(T[1 + w], nxt, sh) & 0x3FFFu;
+    if (i < 8) { d.um[i] = v; bad |= v >= kp.mask_lim; }
+    else { d.ur[i - 8] = v; bad |= v >= kp.rho_lim; }
+  }
+  if (__builtin_expect(bad, 0)) {
+    Draws f = d;
+    fallback<R>(f, j, k01, 8u, kp.perm_lim, kp.mask_lim, kp.rho_lim, 0x3FFFu);
+    d = f;
+  }
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {  // draws < 2^14: the 16-bit magics are exact
+    tp.r[m] = 1u + d.um[m] - 130u * __umulhi(d.um[m], kp.mag_q);
+    tp.rho[m] = d.ur[m] - 131u * __umulhi(d.ur[m], kp.mag_p);
+  }
+  tp.sel = perm_sel_rt(d.idx - kp.fact * (__umulhi(d.idx, kp.mag_f) >> kp.sh_f), 8u);
 }
 
 // ---------------------------------------------------------------------------

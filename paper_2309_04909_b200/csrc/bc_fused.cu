@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(TPB, FUSED_MINB) k_fused_c(FusedArgs a, KP kp,
 }
 
 // Wide tape (any p <= 257, 3..8 slots): one seed01 block per element.
-template <int R, bool RELU>
+template <int R, bool RELU, bool CL>
 __global__ void __launch_bounds__(TPB, 2) k_fused_w(FusedArgs a, KP kp, Key k01, Key k02, Key k12, PreKeys pk) {
   const uint64_t ngroups = (a.n + 7) >> 3;
   for (uint64_t g = (uint64_t)blockIdx.x * TPB + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB) {
@@ -179,14 +179,19 @@ __global__ void __launch_bounds__(TPB, 2) k_fused_w(FusedArgs a, KP kp, Key k01,
     const uint64_t j0 = a.base + i0;
     const uint32_t cnt = (uint32_t)min((uint64_t)8, a.n - i0);
     uint32_t zbits = 0, tbits = 0;
+    uint32_t B[16];
 #pragma unroll 1
     for (int e = 0; e < 8; ++e) {
       const uint64_t xa = (uint32_t)e < cnt ? __ldg(a.x0 + i0 + e) : 0ull;
       const uint64_t xb = (uint32_t)e < cnt ? __ldg(a.x1 + i0 + e) : 0ull;
-      uint32_t B[16];
-      chacha<R>(k01, j0 + (uint64_t)e, L_TAPEW, B);
       Tape tp;
-      decode_wide<R>(B, j0 + e, k01, kp, tp);
+      if constexpr (CL) {  // one block holds elements 2i, 2i+1 (j0 is a multiple of 8)
+        if ((e & 1) == 0) chacha<R>(k01, (j0 + (uint64_t)e) >> 1, L_TAPECL, B);
+        decode_cl<R>(B + 8 * (e & 1), j0 + e, k01, kp, tp);
+      } else {
+        chacha<R>(k01, j0 + (uint64_t)e, L_TAPEW, B);
+        decode_wide<R>(B, j0 + e, k01, kp, tp);
+      }
       uint32_t W0[8], W1[8];
       party_W_wide<0>(xa, kp, tp, W0);
       party_W_wide<1>(xb, kp, tp, W1);
@@ -387,7 +392,7 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
                    : (prm->ell == 64 ? k_fused_c<R, RELU, false, true> : k_fused_c<R, RELU, false, false>);
       fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k01, k02, k12, pk);
     } else {
-      auto fn = k_fused_w<R, RELU>;
+      auto fn = prm->tape == BC_TAPE_COMPACT_LIT ? k_fused_w<R, RELU, true> : k_fused_w<R, RELU, false>;
       fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k01, k02, k12, pk);
     }
     return check_launch();

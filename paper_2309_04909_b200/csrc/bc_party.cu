@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(TPB, 2) k_send_c(SendArgs a, KP kp, Key k01, K
 }
 
 // Wide tape.
-template <int R, int PARTY, bool RELU>
+template <int R, int PARTY, bool RELU, bool CL>
 __global__ void __launch_bounds__(TPB, 2) k_send_w(SendArgs a, KP kp, Key k01, Key ktr) {
   const uint64_t ngroups = (a.n + 7) >> 3;
   for (uint64_t g = (uint64_t)blockIdx.x * TPB + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB) {
@@ -108,13 +108,18 @@ __global__ void __launch_bounds__(TPB, 2) k_send_w(SendArgs a, KP kp, Key k01, K
     uint64_t lo[8];
     uint32_t tb = 0;
     uint64_t hi = 0;
+    uint32_t B[16];
 #pragma unroll 1
     for (int e = 0; e < 8; ++e) {
       const uint64_t xv = (uint32_t)e < cnt ? __ldg(a.x + i0 + e) : 0ull;
-      uint32_t B[16];
-      chacha<R>(k01, j0 + (uint64_t)e, L_TAPEW, B);
       Tape tp;
-      decode_wide<R>(B, j0 + e, k01, kp, tp);
+      if constexpr (CL) {  // one block holds elements 2i, 2i+1 (j0 is a multiple of 8)
+        if ((e & 1) == 0) chacha<R>(k01, (j0 + (uint64_t)e) >> 1, L_TAPECL, B);
+        decode_cl<R>(B + 8 * (e & 1), j0 + e, k01, kp, tp);
+      } else {
+        chacha<R>(k01, j0 + (uint64_t)e, L_TAPEW, B);
+        decode_wide<R>(B, j0 + e, k01, kp, tp);
+      }
       uint32_t W[8];
       party_W_wide<PARTY>(xv, kp, tp, W);
       const uint64_t l = pack_lo(W);
@@ -448,9 +453,12 @@ int send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits,
     } else if (prm->tape == BC_TAPE_COMPACT) {
       if (party == 0) go(k_send_c<R, 0, RELU>);
       else go(k_send_c<R, 1, RELU>);
+    } else if (prm->tape == BC_TAPE_COMPACT_LIT) {
+      if (party == 0) go(k_send_w<R, 0, RELU, true>);
+      else go(k_send_w<R, 1, RELU, true>);
     } else {
-      if (party == 0) go(k_send_w<R, 0, RELU>);
-      else go(k_send_w<R, 1, RELU>);
+      if (party == 0) go(k_send_w<R, 0, RELU, false>);
+      else go(k_send_w<R, 1, RELU, false>);
     }
     return check_launch();
   });
