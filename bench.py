@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--rounds", type=int, default=ROUNDS)
     ap.add_argument("--no-extras", action="store_true", help="skip ReLU / ladder / variants / e2e / cpu legs")
     ap.add_argument("--only", choices=["drelu", "relu", "ladder", "drelu_rss", "relu_rss", "drelu_fp", "relu_fp",
-                                       "party_drelu", "party_relu"],
+                                       "drelu_literal", "party_drelu", "party_relu"],
                     help="profiling aid: launch one op steps+warmup times, print nothing")
     ap.add_argument("--op", default="drelu", choices=["drelu", "relu", "drelu_fp", "relu_fp", "drelu_rss", "relu_rss"],
                     help="tuning aid (tools/variants.py): the op of the headline timing with --no-extras")
@@ -309,6 +309,7 @@ def run_cuda(a):
 
     if a.only:  # profiling aid (ncu): just the launches, no timing output
         pfp = api.Params(ell=ELL, lx=31, f=0, mode=MODE, rounds=a.rounds)
+        plit = api.Params(ell=ELL, lx=LX, f=F, mode="literal", rounds=a.rounds)
         if a.only == "ladder":  # config 2's size, as the bench leg times it
             x_c2 = x0.repeat(((1 << 28) + n - 1) // n)[:1 << 28]
             v_lad = torch.empty((1 << 28, 8), dtype=torch.uint8, device=dev)
@@ -338,6 +339,7 @@ def run_cuda(a):
               "drelu_rss": lambda: f_rss(*xs, prm, seeds, base, out=ys, stream=stream),
               "relu_rss": lambda: f_rss(*xs, prm, seeds, base, out=ys, stream=stream),
               "drelu_fp": lambda: api.drelu(x0, x1, pfp, seeds, base, y0, y1, stream=stream),
+              "drelu_literal": lambda: api.drelu(x0, x1, plit, seeds, base, y0, y1, stream=stream),
               "relu_fp": lambda: api.relu(x0, x1, pfp, seeds, base, y0, y1, stream=stream),
               "drelu": lambda: api.drelu(x0, x1, prm, seeds, base, y0, y1, stream=stream),
               "relu": lambda: api.relu(x0, x1, prm, seeds, base, y0, y1, stream=stream),
