@@ -55,6 +55,20 @@ struct KP {
   uint32_t mag_f, sh_f;    // ceil(2^(31+l) / S!), l - 1 (l = ceil(log2 S!)): x / S! = umulhi(x, mag_f) >> sh_f, x < 2^31
 };
 
+// The compact literal domain is one fixed parameter set (w = lx = 7, p = 131, 8 slots): its
+// kernels overwrite the runtime fields with literals so that every mod-p step compiles to
+// constants.  make_kp derives the same values on the host; the literal parity tests cover both.
+__device__ __forceinline__ KP kp_literal(const KP& kp) {
+  KP k = kp;
+  k.w = 7u; k.lx = 7u; k.p = 131u; k.S = 8u; k.wmask = 127u;
+  k.fact = 40320u; k.perm_lim = 53261u * 40320u; k.mask_lim = 126u * 130u; k.rho_lim = 125u * 131u;
+  k.mag_p = (uint32_t)(((1ull << 32) + 130ull) / 131ull);
+  k.mag_q = (uint32_t)(((1ull << 32) + 129ull) / 130ull);
+  k.mag_f = (uint32_t)(((1ull << 47) + 40319ull) / 40320ull);  // l = ceil(log2 8!) = 16
+  k.sh_f = 15u;
+  return k;
+}
+
 // ---------------------------------------------------------------------------
 // ChaCha_R block (RFC 8439 sec. 2.3), words 12-13 = 64-bit counter, 14-15 =
 // 64-bit label.  The key lives in the constant bank.

@@ -172,26 +172,30 @@ __global__ void __launch_bounds__(TPB, FUSED_MINB) k_fused_c(FusedArgs a, KP kp,
 
 // Wide tape (any p <= 257, 3..8 slots): one seed01 block per element.
 template <int R, bool RELU, bool CL>
-__global__ void __launch_bounds__(TPB, 2) k_fused_w(FusedArgs a, KP kp, Key k01, Key k02, Key k12, PreKeys pk) {
+__global__ void __launch_bounds__(TPB, 2) k_fused_w(FusedArgs a, KP kp_, Key k01, Key k02, Key k12, PreKeys pk) {
+  const KP kp = CL ? kp_literal(kp_) : kp_;
   const uint64_t ngroups = (a.n + 7) >> 3;
   for (uint64_t g = (uint64_t)blockIdx.x * TPB + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB) {
     const uint64_t i0 = g << 3;
     const uint64_t j0 = a.base + i0;
     const uint32_t cnt = (uint32_t)min((uint64_t)8, a.n - i0);
     uint32_t zbits = 0, tbits = 0;
-    uint32_t B[16];
+    constexpr int STEP = CL ? 2 : 1;  // elements per seed01 block
 #pragma unroll 1
-    for (int e = 0; e < 8; ++e) {
+    for (int e2 = 0; e2 < 8; e2 += STEP) {
+      uint32_t B[16];
+      if constexpr (CL)  // one block holds elements 2i, 2i+1 (j0 is a multiple of 8); pk.tpa: bc2.tpl1
+        stream_blk<R, !RELU>(pk.tpa, k01, L_TAPECL, (j0 + (uint64_t)e2) >> 1, B);
+      else
+        chacha<R>(k01, j0 + (uint64_t)e2, L_TAPEW, B);
+#pragma unroll
+    for (int h = 0; h < STEP; ++h) {  // static offsets into B keep it in registers
+      const int e = e2 + h;
       const uint64_t xa = (uint32_t)e < cnt ? __ldg(a.x0 + i0 + e) : 0ull;
       const uint64_t xb = (uint32_t)e < cnt ? __ldg(a.x1 + i0 + e) : 0ull;
       Tape tp;
-      if constexpr (CL) {  // one block holds elements 2i, 2i+1 (j0 is a multiple of 8)
-        if ((e & 1) == 0) chacha<R>(k01, (j0 + (uint64_t)e) >> 1, L_TAPECL, B);
-        decode_cl<R>(B + 8 * (e & 1), j0 + e, k01, kp, tp);
-      } else {
-        chacha<R>(k01, j0 + (uint64_t)e, L_TAPEW, B);
-        decode_wide<R>(B, j0 + e, k01, kp, tp);
-      }
+      if constexpr (CL) decode_cl<R>(B + 8 * h, j0 + e, k01, kp, tp);
+      else decode_wide<R>(B, j0 + e, k01, kp, tp);
       uint32_t W0[8], W1[8];
       party_W_wide<0>(xa, kp, tp, W0);
       party_W_wide<1>(xb, kp, tp, W1);
@@ -203,6 +207,7 @@ __global__ void __launch_bounds__(TPB, 2) k_fused_w(FusedArgs a, KP kp, Key k01,
         a.w0hi[i0 + e] = (uint8_t)pack_hi(W0);
         a.w1hi[i0 + e] = (uint8_t)pack_hi(W1);
       }
+    }
     }
     finish_group<R, RELU, false>(a, kp, k02, k12, pk, i0, j0, cnt, zbits, tbits);
   }
@@ -375,7 +380,8 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
   }
   const KP kp = make_kp(prm);
   const Key k01 = make_key(seeds->s01), k02 = make_key(seeds->s02), k12 = make_key(seeds->s12);
-  const PreKeys pk{make_keypre(seeds->s01, L_TAPEA), make_keypre(seeds->s01, L_TAPEB),
+  const uint64_t tape_a = prm->tape == BC_TAPE_COMPACT_LIT ? L_TAPECL : L_TAPEA;  // the slot the tape kernel reads
+  const PreKeys pk{make_keypre(seeds->s01, tape_a), make_keypre(seeds->s01, L_TAPEB),
                    make_keypre(seeds->s02, L_RESP),  make_keypre(seeds->s02, L_A02),
                    make_keypre(seeds->s02, L_B02),   make_keypre(seeds->s02, L_C02),
                    make_keypre(seeds->s12, L_A12),   make_keypre(seeds->s12, L_B12)};

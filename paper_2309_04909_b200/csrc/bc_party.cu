@@ -99,7 +99,8 @@ __global__ void __launch_bounds__(TPB, 2) k_send_c(SendArgs a, KP kp, Key k01, K
 
 // Wide tape.
 template <int R, int PARTY, bool RELU, bool CL>
-__global__ void __launch_bounds__(TPB, 2) k_send_w(SendArgs a, KP kp, Key k01, Key ktr) {
+__global__ void __launch_bounds__(TPB, 2) k_send_w(SendArgs a, KP kp_, Key k01, Key ktr) {
+  const KP kp = CL ? kp_literal(kp_) : kp_;
   const uint64_t ngroups = (a.n + 7) >> 3;
   for (uint64_t g = (uint64_t)blockIdx.x * TPB + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB) {
     const uint64_t i0 = g << 3;
@@ -108,18 +109,21 @@ __global__ void __launch_bounds__(TPB, 2) k_send_w(SendArgs a, KP kp, Key k01, K
     uint64_t lo[8];
     uint32_t tb = 0;
     uint64_t hi = 0;
-    uint32_t B[16];
+    constexpr int STEP = CL ? 2 : 1;  // elements per seed01 block
 #pragma unroll 1
-    for (int e = 0; e < 8; ++e) {
+    for (int e2 = 0; e2 < 8; e2 += STEP) {
+      uint32_t B[16];
+      if constexpr (CL)  // one block holds elements 2i, 2i+1 (j0 is a multiple of 8)
+        chacha<R>(k01, (j0 + (uint64_t)e2) >> 1, L_TAPECL, B);
+      else
+        chacha<R>(k01, j0 + (uint64_t)e2, L_TAPEW, B);
+#pragma unroll
+    for (int h = 0; h < STEP; ++h) {  // static offsets into B keep it in registers
+      const int e = e2 + h;
       const uint64_t xv = (uint32_t)e < cnt ? __ldg(a.x + i0 + e) : 0ull;
       Tape tp;
-      if constexpr (CL) {  // one block holds elements 2i, 2i+1 (j0 is a multiple of 8)
-        if ((e & 1) == 0) chacha<R>(k01, (j0 + (uint64_t)e) >> 1, L_TAPECL, B);
-        decode_cl<R>(B + 8 * (e & 1), j0 + e, k01, kp, tp);
-      } else {
-        chacha<R>(k01, j0 + (uint64_t)e, L_TAPEW, B);
-        decode_wide<R>(B, j0 + e, k01, kp, tp);
-      }
+      if constexpr (CL) decode_cl<R>(B + 8 * h, j0 + e, k01, kp, tp);
+      else decode_wide<R>(B, j0 + e, k01, kp, tp);
       uint32_t W[8];
       party_W_wide<PARTY>(xv, kp, tp, W);
       const uint64_t l = pack_lo(W);
@@ -129,6 +133,7 @@ __global__ void __launch_bounds__(TPB, 2) k_send_w(SendArgs a, KP kp, Key k01, K
         if (k == e) lo[k] = l;
       hi |= hbyte << (8 * e);
       tb |= tp.t << e;
+    }
     }
     store_msg(a, kp, ktr, g, i0, j0, cnt, lo, hi, tb, PARTY, false);
     if (RELU) send_dshare<R, PARTY>(a, kp, ktr, i0, j0, cnt);
