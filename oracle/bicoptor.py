@@ -27,7 +27,7 @@ from .chacha import chacha_blocks, element_u32, element_u64, label_u64
 L_TAPEA = label_u64(b"bc2.tpa1")  # seed01: 16 B/element (compact tape, part A)
 L_TAPEB = label_u64(b"bc2.tpb1")  # seed01:  8 B/element (compact tape, part B)
 L_TAPEW = label_u64(b"bc2.tapw")   # seed01: 64 B/element (wide tape)
-L_TAPECL = label_u64(b"bc2.tpl1")  # seed01: 32 B/element (compact literal tape: p = 131, 8 slots)
+L_TAPECL = label_u64(b"bc2.tpl2")  # seed01: 32 B/element (compact literal tape: p = 131, 8 slots, 28-bit pair draws)
 L_TAPEL = label_u64(b"bc2.tpL2")   # seed01: 448 B/element (large tape, lx >= 8; 48-bit draws)
 L_FBL = label_u64(b"bc2.fbL2")     # seed01: large-tape fallback, u64 words, counter j*2^20+k
 L_FALLBACK = label_u64(b"bc2.fb01")  # seed01: rejection fallback, counter j*256+k
@@ -171,26 +171,27 @@ def _tape_compact(prm: Params, seed01: bytes, j) -> dict:
 
 def _tape_compact_lit(prm: Params, seed01: bytes, j) -> dict:
     """p = 131, 8 slots (the paper-literal domain Z_{2^7} at lx = 7).  32 B per element
-    at 32 j (label bc2.tpl1, two elements per ChaCha block):
+    at 32 j (label bc2.tpl2, two elements per ChaCha block):
     T0 = t (bit 31) | perm index (bits 0..30, reject >= 53261*8!);
-    T1..T7 = 224 bits, read as one little-endian integer D, holding sixteen 14-bit
-    draws u_i = (D >> 14 i) & 0x3FFF: i < 8 are masks, r_m = 1 + u mod 130 (reject
-    u >= 126*130 = 16380), i >= 8 are reshares, rho_m = u mod 131 (reject u >= 125*131
-    = 16375).  A rejected draw takes the next word of the fallback stream (its low
-    31 bits for the index, low 14 bits for a draw), in the order index, masks,
-    reshares (reading C10)."""
+    T1..T7 = 224 bits, read as one little-endian integer D, holding eight 28-bit
+    draws u_m = (D >> 28 m) & (2^28 - 1), one per slot.  A draw is a pair in
+    Z_130 x Z_131: reject u >= 15762*17030, else x = u mod 17030, the mask
+    r_m = 1 + x mod 130 and the reshare rho_m = floor(x / 130) (x < 130*131, so
+    rho_m < 131; the pair (x mod 130, x div 130) is uniform on Z_130 x Z_131).
+    A rejected draw takes the next word of the fallback stream (its low 31 bits for
+    the index, low 28 bits for a draw), in the order index, slots 0..7 (reading C10)."""
     n, S, p = j.size, 8, 131
     T = element_u32(seed01, L_TAPECL, prm.rounds, j, 8).astype(np.uint64)
     t = T[:, 0] >> np.uint64(31)
     idx = T[:, 0] & np.uint64(0x7FFFFFFF)
     idx_ok = idx < np.uint64(PERM_LIMIT_COMPACT)
     D = [sum(int(T[i, w]) << (32 * (w - 1)) for w in range(1, 8)) for i in range(n)]
-    u = np.array([[(d >> (14 * k)) & 0x3FFF for k in range(16)] for d in D], dtype=np.uint64).reshape(n, 16)
-    mask_lim, rho_lim = 126 * 130, 125 * 131
-    r_ok, rho_ok = u[:, :8] < np.uint64(mask_lim), u[:, 8:] < np.uint64(rho_lim)
-    r = np.uint64(1) + u[:, :8] % np.uint64(p - 1)
-    rho = u[:, 8:] % np.uint64(p)
-    for row in np.nonzero(~idx_ok | ~r_ok.all(axis=1) | ~rho_ok.all(axis=1))[0]:
+    u = np.array([[(d >> (28 * m)) & 0xFFFFFFF for m in range(S)] for d in D], dtype=np.uint64).reshape(n, S)
+    pair = (p - 1) * p
+    lim = ((1 << 28) // pair) * pair
+    ok = u < np.uint64(lim)
+    x = u % np.uint64(pair)
+    for row in np.nonzero(~idx_ok | ~ok.all(axis=1))[0]:
         fb = _fallback_words(seed01, int(j[row]), prm.rounds)
         if not idx_ok[row]:
             v = next(fb) & 0x7FFFFFFF
@@ -198,17 +199,13 @@ def _tape_compact_lit(prm: Params, seed01: bytes, j) -> dict:
                 v = next(fb) & 0x7FFFFFFF
             idx[row] = v
         for m in range(S):
-            if not r_ok[row, m]:
-                v = next(fb) & 0x3FFF
-                while v >= mask_lim:
-                    v = next(fb) & 0x3FFF
-                r[row, m] = 1 + v % (p - 1)
-        for m in range(S):
-            if not rho_ok[row, m]:
-                v = next(fb) & 0x3FFF
-                while v >= rho_lim:
-                    v = next(fb) & 0x3FFF
-                rho[row, m] = v % p
+            if not ok[row, m]:
+                v = next(fb) & 0xFFFFFFF
+                while v >= lim:
+                    v = next(fb) & 0xFFFFFFF
+                x[row, m] = v % pair
+    r = np.uint64(1) + x % np.uint64(p - 1)
+    rho = x // np.uint64(p - 1)
     return {"t": t, "k": _perm_swaps(idx, S), "r": r, "rho": rho}
 
 

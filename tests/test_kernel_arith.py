@@ -206,3 +206,18 @@ def test_wide_tape_magic_divisions():
         xs = xs[xs < (1 << 31)]
         q = ((xs * np.uint64(mag)) >> np.uint64(32)) >> np.uint64(l - 1)
         assert np.array_equal(q, xs // np.uint64(f)), S
+
+
+def test_compact_literal_pair_division():
+    """decode_cl (csrc/bc_device.cuh): u / 17030 = umulhi(u, ceil(2^46/17030)) >> 14 for
+    every 28-bit u (exhaustive), and x div 130 by the 16-bit magic for x < 17030."""
+    pair = 130 * 131
+    mag = ((1 << 46) + pair - 1) // pair
+    assert mag <= M32
+    for c in range(16):
+        u = np.arange(c << 24, (c + 1) << 24, dtype=np.uint64)
+        q = ((u * np.uint64(mag)) >> np.uint64(32)) >> np.uint64(14)
+        assert np.array_equal(q, u // np.uint64(pair))
+    x = np.arange(pair, dtype=np.uint64)
+    mq = ((1 << 32) + 129) // 130
+    assert np.array_equal((x * np.uint64(mq)) >> np.uint64(32), x // np.uint64(130))
