@@ -22,7 +22,7 @@ __host__ __device__ constexpr uint64_t lbl(const char (&s)[9]) {
 constexpr uint64_t L_TAPEA = lbl("bc2.tpa1");  // seed01, 16 B / element (compact tape, part A)
 constexpr uint64_t L_TAPEB = lbl("bc2.tpb1");  // seed01,  8 B / element (compact tape, part B)
 constexpr uint64_t L_TAPEW = lbl("bc2.tapw");  // seed01, 64 B / element (wide)
-constexpr uint64_t L_TAPECL = lbl("bc2.tpl1"); // seed01, 32 B / element (compact literal: p = 131, 8 slots)
+constexpr uint64_t L_TAPECL = lbl("bc2.tpl2"); // seed01, 32 B / element (compact literal: p = 131, 8 slots)
 constexpr uint64_t L_FB = lbl("bc2.fb01");     // seed01, fallback, counter j*256+k
 constexpr uint64_t L_RESP = lbl("bc2.resp");   // seed02, [DReLU']_0
 constexpr uint64_t L_A02 = lbl("bc2.ta02");    // seed02, [a]_0
@@ -61,7 +61,7 @@ struct KP {
 __device__ __forceinline__ KP kp_literal(const KP& kp) {
   KP k = kp;
   k.w = 7u; k.lx = 7u; k.p = 131u; k.S = 8u; k.wmask = 127u;
-  k.fact = 40320u; k.perm_lim = 53261u * 40320u; k.mask_lim = 126u * 130u; k.rho_lim = 125u * 131u;
+  k.fact = 40320u; k.perm_lim = 53261u * 40320u;
   k.mag_p = (uint32_t)(((1ull << 32) + 130ull) / 131ull);
   k.mag_q = (uint32_t)(((1ull << 32) + 129ull) / 130ull);
   k.mag_f = (uint32_t)(((1ull << 47) + 40319ull) / 40320ull);  // l = ceil(log2 8!) = 16
@@ -299,11 +299,15 @@ __device__ __forceinline__ void decode_wide(const uint32_t* T, uint64_t j, const
 }
 
 // Compact literal tape (p = 131, 8 slots; the paper-literal domain at lx = 7): 32 B per element,
-// two elements per block (label bc2.tpl1); T[0..7] = keystream bytes [32 j, 32 j + 32).
+// two elements per block (label bc2.tpl2); T[0..7] = keystream bytes [32 j, 32 j + 32).
 //   T0: t | perm index (reject >= floor(2^31/8!) 8!)
-//   T1..T7 as one 224-bit little-endian D: u_i = (D >> 14 i) & 0x3FFF, i < 8 masks
-//   (r_m = 1 + u mod 130, reject >= 16380), i >= 8 reshares (rho_m = u mod 131, reject >= 16375).
-// KP carries the 14-bit limits (make_kp); the fallback stream yields low-14-bit draws.
+//   T1..T7 as one 224-bit little-endian D: u_m = (D >> 28 m) & (2^28 - 1), one draw per slot,
+//   reject u >= 15762 * 17030; x = u mod 17030 (= 130 * 131), r_m = 1 + x mod 130, rho_m = x div 130.
+// The fallback stream yields low-28-bit draws (fallback() with the reshare loop disabled).
+constexpr uint32_t CL_PAIR = 130u * 131u;
+constexpr uint32_t CL_LIM = ((1u << 28) / CL_PAIR) * CL_PAIR;
+constexpr uint32_t CL_MAG = (uint32_t)(((1ull << 46) + CL_PAIR - 1) / CL_PAIR);  // u / 17030 = umulhi(u, M) >> 14, u < 2^28
+
 template <int R>
 __device__ __forceinline__ void decode_cl(const uint32_t* T, uint64_t j, const Key& k01, const KP& kp, Tape& tp) {
   Draws d;
@@ -311,22 +315,24 @@ __device__ __forceinline__ void decode_cl(const uint32_t* T, uint64_t j, const K
   d.idx = T[0] & 0x7FFFFFFFu;
   bool bad = d.idx >= kp.perm_lim;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int bit = 14 * i, w = bit >> 5, sh = bit & 31;
+  for (int m = 0; m < 8; ++m) {
+    const int bit = 28 * m, w = bit >> 5, sh = bit & 31;
     const uint32_t nxt = w < 6 ? T[2 + w] : 0u;
-    const uint32_t v = __funnelshift_r(T[1 + w], nxt, sh) & 0x3FFFu;
-    if (i < 8) { d.um[i] = v; bad |= v >= kp.mask_lim; }
-    else { d.ur[i - 8] = v; bad |= v >= kp.rho_lim; }
+    d.um[m] = __funnelshift_r(T[1 + w], nxt, sh) & 0x0FFFFFFFu;
+    d.ur[m] = 0u;
+    bad |= d.um[m] >= CL_LIM;
   }
   if (__builtin_expect(bad, 0)) {
     Draws f = d;
-    fallback<R>(f, j, k01, 8u, kp.perm_lim, kp.mask_lim, kp.rho_lim, 0x3FFFu);
+    fallback<R>(f, j, k01, 8u, kp.perm_lim, CL_LIM, 1u, 0x0FFFFFFFu);
     d = f;
   }
 #pragma unroll
-  for (int m = 0; m < 8; ++m) {  // draws < 2^14: the 16-bit magics are exact
-    tp.r[m] = 1u + d.um[m] - 130u * __umulhi(d.um[m], kp.mag_q);
-    tp.rho[m] = d.ur[m] - 131u * __umulhi(d.ur[m], kp.mag_p);
+  for (int m = 0; m < 8; ++m) {
+    const uint32_t x = d.um[m] - CL_PAIR * (__umulhi(d.um[m], CL_MAG) >> 14);
+    const uint32_t q = __umulhi(x, kp.mag_q);  // x div 130, exact for x < 2^16
+    tp.r[m] = 1u + x - 130u * q;
+    tp.rho[m] = q;
   }
   tp.sel = perm_sel_rt(d.idx - kp.fact * (__umulhi(d.idx, kp.mag_f) >> kp.sh_f), 8u);
 }

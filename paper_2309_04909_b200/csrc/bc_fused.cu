@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(TPB, 2) k_fused_w(FusedArgs a, KP kp_, Key k01
 #pragma unroll 1
     for (int e2 = 0; e2 < 8; e2 += STEP) {
       uint32_t B[16];
-      if constexpr (CL)  // one block holds elements 2i, 2i+1 (j0 is a multiple of 8); pk.tpa: bc2.tpl1
+      if constexpr (CL)  // one block holds elements 2i, 2i+1 (j0 is a multiple of 8); pk.tpa: bc2.tpl2
         stream_blk<R, !RELU>(pk.tpa, k01, L_TAPECL, (j0 + (uint64_t)e2) >> 1, B);
       else
         chacha<R>(k01, j0 + (uint64_t)e2, L_TAPEW, B);

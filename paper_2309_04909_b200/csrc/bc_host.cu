@@ -107,9 +107,8 @@ KP make_kp(const bc_params* prm) {
   if (prm->tape != BC_TAPE_LARGE) {
     kp.fact = factorial(prm->slots);
     kp.perm_lim = (uint32_t)((0x80000000ull / kp.fact) * kp.fact);
-    const uint32_t span = prm->tape == BC_TAPE_COMPACT_LIT ? 16384u : 65536u;  // 14- or 16-bit draws
-    kp.mask_lim = (span / (kp.p - 1u)) * (kp.p - 1u);
-    kp.rho_lim = (span / kp.p) * kp.p;
+    kp.mask_lim = (65536u / (kp.p - 1u)) * (kp.p - 1u);  // wide tape (the compact literal tape has its own)
+    kp.rho_lim = (65536u / kp.p) * kp.p;
     // x / d for x < 2^16, d <= 257: ceil(2^32 / d) overshoots 2^32/d by e < 1, and x e / 2^32 < 1/d
     kp.mag_p = (uint32_t)(((1ull << 32) + kp.p - 1) / kp.p);
     kp.mag_q = (uint32_t)(((1ull << 32) + kp.p - 2) / (kp.p - 1u));
