@@ -16,7 +16,7 @@ Modules
                PRG the paper leaves unnamed; reading C19 in DESIGN.md).
   ring      -- cut / LT / Alg 1, 4, 5 truncation / Alg 6 modulo switch.
   bicoptor  -- Alg 7 UBL DReLU, Alg 8 UBL ReLU, per party and composed; the
-               compact, wide and large (full precision) tapes; wire formats.
+               compact, pair and large (full precision) tapes; wire formats.
   rss       -- Alg 9 RSS DReLU and the RSS ReLU.
   trunc     -- the truncation study: Alg 1 / 2 e0-e1 classes, exact mask counting,
                Alg 3 trc-then-mult against mult-then-trc.

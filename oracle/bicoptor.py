@@ -26,8 +26,7 @@ from .chacha import chacha_blocks, element_u32, element_u64, label_u64
 # Stream labels (domain separation of the seeds' keystreams).
 L_TAPEA = label_u64(b"bc2.tpa1")  # seed01: 16 B/element (compact tape, part A)
 L_TAPEB = label_u64(b"bc2.tpb1")  # seed01:  8 B/element (compact tape, part B)
-L_TAPEW = label_u64(b"bc2.tapw")   # seed01: 64 B/element (wide tape)
-L_TAPECL = label_u64(b"bc2.tpl2")  # seed01: 32 B/element (compact literal tape: p = 131, 8 slots, 28-bit pair draws)
+L_TAPEP = label_u64(b"bc2.tpp1")   # seed01: 32 B/element (pair tape: p <= 131, 28-bit (r, rho) draws)
 L_TAPEL = label_u64(b"bc2.tpL2")   # seed01: 448 B/element (large tape, lx >= 8; 48-bit draws)
 L_FBL = label_u64(b"bc2.fbL2")     # seed01: large-tape fallback, u64 words, counter j*2^20+k
 L_FALLBACK = label_u64(b"bc2.fb01")  # seed01: rejection fallback, counter j*256+k
@@ -81,14 +80,15 @@ class Params:
 
     @property
     def layout(self) -> str:
-        """PRG tape layout: "compact" (p = 257, 8 slots), "compact_lit" (p = 131,
-        8 slots: the paper-literal domain at lx = 7), "wide" (other lx <= 7),
+        """PRG tape layout: "compact" (p = 257, 8 slots), "pair" (other lx <= 7, p <= 131),
+        "compact_lit" (the pair tape's p = 131, 8-slot case: the paper-literal domain at
+        lx = 7, which the kernels compile with constant parameters),
         "large" (lx >= 8: up to 32 slots, p < 2^33; full precision lx = 31)."""
         if self.compact:
             return "compact"
         if self.p == 131 and self.slots == 8:
             return "compact_lit"
-        return "wide" if self.lx <= 7 else "large"
+        return "pair" if self.lx <= 7 else "large"
 
 
 # --- PRG tape: t, Pi, r_m, rho_m for one element (Alg 7 steps 1, 6, 7, 8) -------------
@@ -129,9 +129,7 @@ def tape(prm: Params, seed01: bytes, j) -> dict:
         return _tape_compact(prm, seed01, j)
     if prm.layout == "large":
         return _tape_large(prm, seed01, j)
-    if prm.layout == "compact_lit":
-        return _tape_compact_lit(prm, seed01, j)
-    return _tape_wide(prm, seed01, j)
+    return _tape_pair(prm, seed01, j)  # "pair" and its p = 131, 8-slot case "compact_lit"
 
 
 def _tape_compact(prm: Params, seed01: bytes, j) -> dict:
@@ -169,22 +167,25 @@ def _tape_compact(prm: Params, seed01: bytes, j) -> dict:
     return {"t": t, "k": _perm_swaps(idx, S), "r": r, "rho": digits[:, :8].copy()}
 
 
-def _tape_compact_lit(prm: Params, seed01: bytes, j) -> dict:
-    """p = 131, 8 slots (the paper-literal domain Z_{2^7} at lx = 7).  32 B per element
-    at 32 j (label bc2.tpl2, two elements per ChaCha block):
-    T0 = t (bit 31) | perm index (bits 0..30, reject >= 53261*8!);
-    T1..T7 = 224 bits, read as one little-endian integer D, holding eight 28-bit
-    draws u_m = (D >> 28 m) & (2^28 - 1), one per slot.  A draw is a pair in
-    Z_130 x Z_131: reject u >= 15762*17030, else x = u mod 17030, the mask
-    r_m = 1 + x mod 130 and the reshare rho_m = floor(x / 130) (x < 130*131, so
-    rho_m < 131; the pair (x mod 130, x div 130) is uniform on Z_130 x Z_131).
-    A rejected draw takes the next word of the fallback stream (its low 31 bits for
-    the index, low 28 bits for a draw), in the order index, slots 0..7 (reading C10)."""
-    n, S, p = j.size, 8, 131
-    T = element_u32(seed01, L_TAPECL, prm.rounds, j, 8).astype(np.uint64)
+def _tape_pair(prm: Params, seed01: bytes, j) -> dict:
+    """Any p <= 131 with 3..8 slots (every lx <= 7 domain but the compact one; at
+    lx = 7 literal, p = 131 and 8 slots).  32 B per element at 32 j (label bc2.tpp1,
+    two elements per ChaCha block):
+    T0 = t (bit 31) | perm index (bits 0..30, reject >= floor(2^31/S!) S!);
+    T1..T7 = 224 bits, read as one little-endian integer D, holding up to eight
+    28-bit draws u_m = (D >> 28 m) & (2^28 - 1), one per slot m < S.  A draw is a
+    pair in Z_{p-1} x Z_p: with d = (p-1) p, reject u >= floor(2^28/d) d, else
+    x = u mod d, the mask r_m = 1 + x mod (p-1) and the reshare rho_m = x div (p-1)
+    (the pair (x mod (p-1), x div (p-1)) is uniform on Z_{p-1} x Z_p).  A rejected
+    draw takes the next word of the fallback stream (its low 31 bits for the index,
+    low 28 bits for a draw), in the order index, slots 0..S-1 (reading C10)."""
+    n, S, p = j.size, prm.slots, prm.p
+    fact = math.factorial(S)
+    perm_lim = ((1 << 31) // fact) * fact
+    T = element_u32(seed01, L_TAPEP, prm.rounds, j, 8).astype(np.uint64)
     t = T[:, 0] >> np.uint64(31)
     idx = T[:, 0] & np.uint64(0x7FFFFFFF)
-    idx_ok = idx < np.uint64(PERM_LIMIT_COMPACT)
+    idx_ok = idx < np.uint64(perm_lim)
     D = [sum(int(T[i, w]) << (32 * (w - 1)) for w in range(1, 8)) for i in range(n)]
     u = np.array([[(d >> (28 * m)) & 0xFFFFFFF for m in range(S)] for d in D], dtype=np.uint64).reshape(n, S)
     pair = (p - 1) * p
@@ -195,7 +196,7 @@ def _tape_compact_lit(prm: Params, seed01: bytes, j) -> dict:
         fb = _fallback_words(seed01, int(j[row]), prm.rounds)
         if not idx_ok[row]:
             v = next(fb) & 0x7FFFFFFF
-            while v >= PERM_LIMIT_COMPACT:
+            while v >= perm_lim:
                 v = next(fb) & 0x7FFFFFFF
             idx[row] = v
         for m in range(S):
@@ -206,47 +207,6 @@ def _tape_compact_lit(prm: Params, seed01: bytes, j) -> dict:
                 x[row, m] = v % pair
     r = np.uint64(1) + x % np.uint64(p - 1)
     rho = x // np.uint64(p - 1)
-    return {"t": t, "k": _perm_swaps(idx, S), "r": r, "rho": rho}
-
-
-def _tape_wide(prm: Params, seed01: bytes, j) -> dict:
-    """Any p <= 257, 3..8 slots.  64 B per element at 64 j (label bc2.tapw):
-    T0 = t | perm index (reject >= floor(2^31/S!) S!); T1..T4 = 8 u16 mask draws,
-    r_m = 1 + u mod (p-1) (reject >= floor(65536/(p-1))(p-1)); T5..T8 = 8 u16
-    reshare draws, rho_m = u mod p (reject >= floor(65536/p) p)."""
-    n, S, p = j.size, prm.slots, prm.p
-    T = element_u32(seed01, L_TAPEW, prm.rounds, j, 16)
-    t = (T[:, 0] >> np.uint32(31)).astype(np.uint64)
-    idx = (T[:, 0] & np.uint32(0x7FFFFFFF)).astype(np.uint64)
-    perm_lim = ((1 << 31) // math.factorial(S)) * math.factorial(S)
-    idx_ok = idx < np.uint64(perm_lim)
-    um = np.ascontiguousarray(T[:, 1:5]).view("<u2").reshape(n, 8)[:, :S].astype(np.uint64)
-    mask_lim = (65536 // (p - 1)) * (p - 1)
-    r_ok = um < np.uint64(mask_lim)
-    r = np.uint64(1) + um % np.uint64(p - 1)
-    u = np.ascontiguousarray(T[:, 5:9]).view("<u2").reshape(n, 8)[:, :S].astype(np.uint64)
-    rho_lim = (65536 // p) * p
-    rho_ok = u < np.uint64(rho_lim)
-    rho = u % np.uint64(p)
-    for row in np.nonzero(~idx_ok | ~r_ok.all(axis=1) | ~rho_ok.all(axis=1))[0]:
-        fb = _fallback_words(seed01, int(j[row]), prm.rounds)
-        if not idx_ok[row]:
-            v = next(fb) & 0x7FFFFFFF
-            while v >= perm_lim:
-                v = next(fb) & 0x7FFFFFFF
-            idx[row] = v
-        for m in range(S):
-            if not r_ok[row, m]:
-                v = next(fb) & 0xFFFF
-                while v >= mask_lim:
-                    v = next(fb) & 0xFFFF
-                r[row, m] = 1 + v % (p - 1)
-        for m in range(S):
-            if not rho_ok[row, m]:
-                v = next(fb) & 0xFFFF
-                while v >= rho_lim:
-                    v = next(fb) & 0xFFFF
-                rho[row, m] = v % p
     return {"t": t, "k": _perm_swaps(idx, S), "r": r, "rho": rho}
 
 

@@ -182,7 +182,7 @@ def test_fpmod48_quotient_exact():
 
 
 def test_wide_tape_magic_divisions():
-    """The wide tape's runtime divisions by host-computed magics (KP::mag_p, mag_q,
+    """The pair tape's runtime divisions by host-computed magics (KP::mag_p, mag_q,
     mag_f): x / d = umulhi(x, ceil(2^32/d)) for every 16-bit draw and every d = p, p-1
     of a wide-tape setting (w = 2..8); x / S! = umulhi(x, ceil(2^(31+l)/S!)) >> (l-1)
     for 31-bit indices (l = ceil(log2 S!)), sampled plus the multiples' edges."""
@@ -221,3 +221,23 @@ def test_compact_literal_pair_division():
     x = np.arange(pair, dtype=np.uint64)
     mq = ((1 << 32) + 129) // 130
     assert np.array_equal((x * np.uint64(mq)) >> np.uint64(32), x // np.uint64(130))
+
+
+def test_pair_tape_runtime_magic():
+    """decode_pair (csrc/bc_device.cuh) with make_kp's runtime magic: for every prime the
+    pair tape serves (p = prime above 2^w, w = 2..7), d = (p-1) p is not a power of two,
+    M = ceil(2^(32+k)/d) < 2^32 with k = floor(log2 d), the bound u e < 2^(32+k) holds
+    for u < 2^28 (so u div d is exact everywhere), and a sample plus the edges agree."""
+    from oracle.ring import prime_above
+    rng = np.random.default_rng(5)
+    for w in range(2, 8):
+        p = prime_above(w)
+        d = (p - 1) * p
+        assert d & (d - 1) and d < 1 << 16
+        k = d.bit_length() - 1
+        mag = ((1 << (32 + k)) + d - 1) // d
+        assert mag <= M32 and ((1 << 28) - 1) * (mag * d - (1 << (32 + k))) < 1 << (32 + k)
+        u = np.concatenate([rng.integers(0, 1 << 28, 1 << 20, dtype=np.uint64),
+                            np.arange(d * 3, dtype=np.uint64), np.arange((1 << 28) - d * 3, 1 << 28, dtype=np.uint64)])
+        q = ((u * np.uint64(mag)) >> np.uint64(32)) >> np.uint64(k)
+        assert np.array_equal(q, u // np.uint64(d)), p

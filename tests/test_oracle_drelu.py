@@ -266,21 +266,28 @@ def test_party_composition_matches_drelu():
     assert np.array_equal(back, m0["W"])
 
 
-def test_compact_lit_tape_raw_draws():
-    """Compact literal tape (p = 131, 8 slots, layout spec DESIGN.md §4): re-read the
-    32 keystream bytes of each element from whole ChaCha blocks (element j = bytes
-    [32 j, 32 j + 32) of the bc2.tpl2 stream), take the 28-bit draws as bit strings,
-    and check r_m = 1 + (u mod 17030) mod 130 and rho_m = (u mod 17030) div 130 on
+@pytest.mark.parametrize("kw,layout", [(dict(ell=16, lx=7, f=0, mode="literal"), "compact_lit"),
+                                       (dict(ell=32, lx=5, f=3, mode="guard"), "pair"),
+                                       (dict(ell=12, lx=3, f=1, mode="literal"), "pair")])
+def test_pair_tape_raw_draws(kw, layout):
+    """Pair tape (p <= 131, layout spec DESIGN.md §4): re-read the 32 keystream bytes
+    of each element from whole ChaCha blocks (element j = bytes [32 j, 32 j + 32) of
+    the bc2.tpp1 stream), take the 28-bit draws as bit strings, and check
+    r_m = 1 + (u mod d) mod (p-1) and rho_m = (u mod d) div (p-1), d = (p-1) p, on
     unrejected elements; on a rejected element the rejected draw is replaced by the
     first fallback word whose low 28 bits fall below the limit.  Also: the pair
-    (r, rho) covers Z_131^* x Z_131 uniformly (chi-square)."""
+    (r, rho) covers Z_p^* x Z_p uniformly (chi-square)."""
     from oracle.chacha import chacha_blocks
-    prm = B.Params(ell=16, lx=7, f=0, mode="literal")
-    assert prm.layout == "compact_lit" and prm.p == 131
-    lim = 15762 * 17030
-    assert lim <= 1 << 28 < lim + 17030
+    prm = B.Params(**kw)
+    S, p = prm.slots, prm.p
+    assert prm.layout == layout and p <= 131
+    d = (p - 1) * p
+    lim = ((1 << 28) // d) * d
+    assert lim <= 1 << 28 < lim + d
+    fact = math.factorial(S)
+    plim = ((1 << 31) // fact) * fact
     n = 4000
-    blocks = chacha_blocks(SEEDS.s01, B.L_TAPECL, list(range(n // 2)), prm.rounds)
+    blocks = chacha_blocks(SEEDS.s01, B.L_TAPEP, list(range(n // 2)), prm.rounds)
     raw = np.asarray(blocks, dtype="<u4").tobytes()
     tp = B.tape(prm, SEEDS.s01, np.arange(n, dtype=np.uint64))
     ok_rows = 0
@@ -288,37 +295,40 @@ def test_compact_lit_tape_raw_draws():
         e = raw[32 * jj: 32 * jj + 32]
         w0 = int.from_bytes(e[:4], "little")
         bits = "".join(format(b, "08b")[::-1] for b in e[4:])  # LSB-first bit string of D
-        u = [int(bits[28 * i: 28 * i + 28][::-1], 2) for i in range(8)]
+        u = [int(bits[28 * i: 28 * i + 28][::-1], 2) for i in range(S)]
         assert int(tp["t"][jj]) == w0 >> 31
-        if (w0 & 0x7FFFFFFF) >= 53261 * 40320 or any(v >= lim for v in u):
+        if (w0 & 0x7FFFFFFF) >= plim or any(v >= lim for v in u):
             continue
         ok_rows += 1
-        assert [int(v) for v in tp["r"][jj]] == [1 + (v % 17030) % 130 for v in u]
-        assert [int(v) for v in tp["rho"][jj]] == [(v % 17030) // 130 for v in u]
-    assert ok_rows > 3990
-    # rejected draws (rate 3.2e-5 per draw): search a wider range from the raw words
+        assert [int(v) for v in tp["r"][jj]] == [1 + (v % d) % (p - 1) for v in u]
+        assert [int(v) for v in tp["rho"][jj]] == [(v % d) // (p - 1) for v in u]
+    assert ok_rows > 3980
+    # rejected draws: search a wider range from the raw words
     jr = np.arange(1 << 15, dtype=np.uint64)
-    T = np.asarray(chacha_blocks(SEEDS.s01, B.L_TAPECL, list(range(1 << 14)), prm.rounds), dtype="<u4")
+    T = np.asarray(chacha_blocks(SEEDS.s01, B.L_TAPEP, list(range(1 << 14)), prm.rounds), dtype="<u4")
     T = T.reshape(-1, 8)
     found = 0
     for jj in range(T.shape[0]):
-        if (int(T[jj, 0]) & 0x7FFFFFFF) >= 53261 * 40320:
+        if (int(T[jj, 0]) & 0x7FFFFFFF) >= plim:
             continue
         D = sum(int(T[jj, w]) << (32 * (w - 1)) for w in range(1, 8))
-        bad = [m for m in range(8) if ((D >> (28 * m)) & 0xFFFFFFF) >= lim]
+        bad = [m for m in range(S) if ((D >> (28 * m)) & 0xFFFFFFF) >= lim]
         if len(bad) != 1:
             continue
         m = bad[0]
         fb = [int(w) & 0xFFFFFFF for w in chacha_blocks(SEEDS.s01, B.L_FALLBACK, [jj * 256], prm.rounds)[0]]
-        x = next(w for w in fb if w < lim) % 17030
+        x = next(w for w in fb if w < lim) % d
         got = B.tape(prm, SEEDS.s01, jr[jj:jj + 1])
-        assert (int(got["r"][0, m]), int(got["rho"][0, m])) == (1 + x % 130, x // 130)
+        assert (int(got["r"][0, m]), int(got["rho"][0, m])) == (1 + x % (p - 1), x // (p - 1))
         found += 1
-    assert found >= 1
+        if found >= 3:
+            break
+    expected = (1 << 15) * S * ((1 << 28) - lim) / (1 << 28)
+    assert found >= 1 or expected < 3   # p = 11: 2^28 - lim = 6, no rejection in range
     tp = B.tape(prm, SEEDS.s01, np.arange(60000, dtype=np.uint64))
-    cells = ((tp["r"] - 1) * 131 + tp["rho"]).ravel().astype(np.int64)
-    cnt = np.bincount(cells, minlength=17030)
-    assert cnt.size == 17030 and tp["r"].min() >= 1 and tp["rho"].max() <= 130
-    exp = cells.size / 17030
+    cells = ((tp["r"] - 1) * p + tp["rho"]).ravel().astype(np.int64)
+    cnt = np.bincount(cells, minlength=d)
+    assert cnt.size == d and tp["r"].min() >= 1 and tp["rho"].max() <= p - 1
+    exp = cells.size / d
     chi2 = float(((cnt - exp) ** 2 / exp).sum())
-    assert chi2 < 17029 + 6 * math.sqrt(2 * 17029)
+    assert chi2 < (d - 1) + 6 * math.sqrt(2 * (d - 1))

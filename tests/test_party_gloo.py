@@ -46,7 +46,7 @@ def _worker(rank, world, port, kind, n, chunk, mode, literal, outdir):
             from oracle import bicoptor as B
             o = B.Params(ell=self.ell, lx=self.lx, f=self.f, mode=self.mode, rounds=self.rounds)
             return type("C", (), {"p": o.p, "slots": o.slots,
-                                  "tape": {"wide": 0, "compact": 1, "large": 2, "compact_lit": 3}[o.layout]})()
+                                  "tape": {"pair": 0, "compact": 1, "large": 2, "compact_lit": 3}[o.layout]})()
 
     prm = P(**CONFIGS[mode])
     role = party.Role.of(rank)
