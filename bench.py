@@ -430,11 +430,11 @@ def run_cuda(a):
             tr_, _, _ = timed(lambda: api.relu(x0, x1, pr, seeds, base, y0, y1, stream=stream), 50, 3)
             var[f"chacha{R}"] = {"drelu": world * n / (tv / 50 * 1e-3), "relu": world * n / (tr_ / 50 * 1e-3)}
         # the paper-literal domain Z_{2^lx} (p = 131, 64-bit messages; reading C6: it mis-signs a band of
-        # negatives, so guard mode is the default): the wide tape, one ChaCha block per element
+        # negatives, so guard mode is the default): the pair tape, one ChaCha block per two elements
         pl = api.Params(ell=ELL, lx=LX, f=F, mode="literal", rounds=a.rounds)
         tl_, _, _ = timed(lambda: api.drelu(x0, x1, pl, seeds, base, y0, y1, stream=stream), 50, 3)
         var["literal"] = {"drelu": world * n / (tl_ / 50 * 1e-3),
-                          "note": "mode=literal (w = lx = 7, p = 131): compact literal tape, 32 B of keystream per element"}
+                          "note": "mode=literal (w = lx = 7, p = 131): pair tape (28-bit (r, rho) draws), 32 B of keystream per element"}
         line["variants"] = var
         # ---- config 2: ladder + modswitch (Alg 7 steps 3-5), HBM-bound, at config 2's 2^28 ----
         n2 = 1 << 28

@@ -51,10 +51,10 @@ extern "C" {
 #define BC_MODE_LITERAL 1 /* w = lx, the paper's Z_{2^lx} (64-bit wire)  */
 
 /* PRG tape layouts. */
-#define BC_TAPE_WIDE    0 /* lx <= 7, p <= 257 other than the compact case: 64 B / element */
+#define BC_TAPE_PAIR    0 /* lx <= 7, p <= 131 (other than the cases below): 32 B / element, 28-bit (r, rho) draws */
 #define BC_TAPE_COMPACT 1 /* p = 257 and 8 slots (lx = 7 guard): 24 B / element            */
 #define BC_TAPE_LARGE   2 /* lx >= 8, up to 32 slots and p < 2^33: 448 B / element          */
-#define BC_TAPE_COMPACT_LIT 3 /* p = 131 and 8 slots (lx = 7 literal): 32 B / element, 14-bit draws */
+#define BC_TAPE_COMPACT_LIT 3 /* p = 131 and 8 slots (lx = 7 literal): the pair tape, kernels with constant parameters */
 
 /* Protocol parameters (Alg 7 "Setting"; key bits, sec. 6.1).
  *   ell    ring bits, 2..64
@@ -86,7 +86,7 @@ typedef struct bc_seeds {
 } bc_seeds;
 
 /* Optional transcript of the simulated three-party run (bc_drelu / bc_relu):
- * the messages P0 and P1 send to P2 (Alg 7 step 8).  Compact and wide
+ * the messages P0 and P1 send to P2 (Alg 7 step 8).  Compact and pair
  * tapes: the wire format of bc_drelu_send, all four planes non-NULL.  Large
  * tape: w0_lo and w1_lo are uint64_t[n][slots] (W_m in [0, p), 8-B aligned),
  * w0_hi and w1_hi must be NULL. */

@@ -35,7 +35,7 @@ class bc_params(ctypes.Structure):
                 ("slots", ctypes.c_uint32), ("tape", ctypes.c_int32), ("p", ctypes.c_uint64)]
 
 
-TAPE = {0: "wide", 1: "compact", 2: "large", 3: "compact_lit"}
+TAPE = {0: "pair", 1: "compact", 2: "large", 3: "compact_lit"}
 
 
 class bc_seeds(ctypes.Structure):

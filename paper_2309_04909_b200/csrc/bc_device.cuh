@@ -21,8 +21,7 @@ __host__ __device__ constexpr uint64_t lbl(const char (&s)[9]) {
 }
 constexpr uint64_t L_TAPEA = lbl("bc2.tpa1");  // seed01, 16 B / element (compact tape, part A)
 constexpr uint64_t L_TAPEB = lbl("bc2.tpb1");  // seed01,  8 B / element (compact tape, part B)
-constexpr uint64_t L_TAPEW = lbl("bc2.tapw");  // seed01, 64 B / element (wide)
-constexpr uint64_t L_TAPECL = lbl("bc2.tpl2"); // seed01, 32 B / element (compact literal: p = 131, 8 slots)
+constexpr uint64_t L_TAPEP = lbl("bc2.tpp1");  // seed01, 32 B / element (pair tape: p <= 131, 28-bit (r, rho) draws)
 constexpr uint64_t L_FB = lbl("bc2.fb01");     // seed01, fallback, counter j*256+k
 constexpr uint64_t L_RESP = lbl("bc2.resp");   // seed02, [DReLU']_0
 constexpr uint64_t L_A02 = lbl("bc2.ta02");    // seed02, [a]_0
@@ -48,9 +47,9 @@ struct KP {
   uint32_t wmask;      // 2^w - 1
   uint32_t perm_lim;   // floor(2^31 / S!) * S!
   uint32_t fact;       // S!
-  uint32_t mask_lim;   // floor(65536 / (p-1)) * (p-1)
-  uint32_t rho_lim;    // floor(65536 / p) * p
-  // magic multipliers of the wide tape's runtime divisions (exact for the ranges used):
+  // pair tape: d = (p-1) p, one 28-bit draw per slot, u / d = umulhi(u, pair_mag) >> pair_sh for u < 2^28
+  uint32_t pair_d, pair_lim, pair_mag, pair_sh;  // d, floor(2^28 / d) d, ceil(2^(32+k) / d), k = floor(log2 d)
+  // magic multipliers of the runtime divisions (exact for the ranges used):
   uint32_t mag_p, mag_q;   // ceil(2^32 / p), ceil(2^32 / (p-1)): x / d = umulhi(x, mag) for x < 2^16
   uint32_t mag_f, sh_f;    // ceil(2^(31+l) / S!), l - 1 (l = ceil(log2 S!)): x / S! = umulhi(x, mag_f) >> sh_f, x < 2^31
 };
@@ -62,6 +61,8 @@ __device__ __forceinline__ KP kp_literal(const KP& kp) {
   KP k = kp;
   k.w = 7u; k.lx = 7u; k.p = 131u; k.S = 8u; k.wmask = 127u;
   k.fact = 40320u; k.perm_lim = 53261u * 40320u;
+  k.pair_d = 130u * 131u; k.pair_lim = 15762u * 17030u;
+  k.pair_mag = (uint32_t)(((1ull << 46) + 17029ull) / 17030ull); k.pair_sh = 14u;
   k.mag_p = (uint32_t)(((1ull << 32) + 130ull) / 131ull);
   k.mag_q = (uint32_t)(((1ull << 32) + 129ull) / 130ull);
   k.mag_f = (uint32_t)(((1ull << 47) + 40319ull) / 40320ull);  // l = ceil(log2 8!) = 16
@@ -233,7 +234,7 @@ struct Draws {  // raw draws of one element: perm index, 8 mask u16, 8 reshare u
 template <int R>
 __device__ __noinline__ void fallback(Draws& d, uint64_t j, Key key, uint32_t S, uint32_t perm_lim,
                                       uint32_t mask_lim /*0: masks never rejected*/, uint32_t rho_lim,
-                                      uint32_t dmask /*draw width: 0xFFFF wide, 0x3FFF compact literal*/) {
+                                      uint32_t dmask /*draw width: 2^28 - 1 for the pair tape*/) {
   FbStream<R> fb;
   fb.key = key; fb.j = j; fb.pos = 16; fb.kc = 0;
   if (d.idx >= perm_lim) {
@@ -268,48 +269,15 @@ struct Tape {
   uint32_t rho[8];   // reshare rho_m in Z_p (step 8)
 };
 
-// Wide tape: 16 words T[0..15] = keystream bytes [64 j, 64 j + 64).
+// Pair tape (every lx <= 7 domain but the compact one: p <= 131, 3..8 slots): 32 B per element,
+// two elements per block (label bc2.tpp1); T[0..7] = keystream bytes [32 j, 32 j + 32).
 //   T0: t | perm index (reject >= floor(2^31/S!) S!)
-//   T1..T4: u16 m = mask draw, r_m = 1 + u mod (p-1) (reject >= floor(65536/(p-1))(p-1))
-//   T5..T8: u16 m = reshare draw, rho_m = u mod p (reject >= floor(65536/p) p)
+//   T1..T7 as one 224-bit little-endian D: u_m = (D >> 28 m) & (2^28 - 1), one draw per slot m < S,
+//   reject u >= floor(2^28/d) d (d = (p-1) p); x = u mod d, r_m = 1 + x mod (p-1), rho_m = x div (p-1).
+// The fallback stream yields low-28-bit draws (fallback() with the reshare loop disabled).  The
+// compact literal kernels (p = 131, 8 slots) pass kp_literal(kp), so the same code compiles to constants.
 template <int R>
-__device__ __forceinline__ void decode_wide(const uint32_t* T, uint64_t j, const Key& k01, const KP& kp, Tape& tp) {
-  Draws d;
-  tp.t = T[0] >> 31;
-  d.idx = T[0] & 0x7FFFFFFFu;
-  bool bad = d.idx >= kp.perm_lim;
-#pragma unroll
-  for (int m = 0; m < 8; ++m) {
-    d.um[m] = (T[1 + m / 2] >> (16 * (m & 1))) & 0xFFFFu;
-    d.ur[m] = (T[5 + m / 2] >> (16 * (m & 1))) & 0xFFFFu;
-    if ((uint32_t)m < kp.S) bad |= (d.um[m] >= kp.mask_lim) | (d.ur[m] >= kp.rho_lim);
-  }
-  if (__builtin_expect(bad, 0)) {  // the addressable copy lives on the rare path only
-    Draws f = d;
-    fallback<R>(f, j, k01, kp.S, kp.perm_lim, kp.mask_lim, kp.rho_lim, 0xFFFFu);
-    d = f;
-  }
-  const uint32_t q = kp.p - 1u;
-#pragma unroll
-  for (int m = 0; m < 8; ++m) {  // draws < 2^16: one IMAD.HI per division (magics from the host)
-    tp.r[m] = 1u + d.um[m] - q * __umulhi(d.um[m], kp.mag_q);
-    tp.rho[m] = d.ur[m] - kp.p * __umulhi(d.ur[m], kp.mag_p);
-  }
-  tp.sel = perm_sel_rt(d.idx - kp.fact * (__umulhi(d.idx, kp.mag_f) >> kp.sh_f), kp.S);
-}
-
-// Compact literal tape (p = 131, 8 slots; the paper-literal domain at lx = 7): 32 B per element,
-// two elements per block (label bc2.tpl2); T[0..7] = keystream bytes [32 j, 32 j + 32).
-//   T0: t | perm index (reject >= floor(2^31/8!) 8!)
-//   T1..T7 as one 224-bit little-endian D: u_m = (D >> 28 m) & (2^28 - 1), one draw per slot,
-//   reject u >= 15762 * 17030; x = u mod 17030 (= 130 * 131), r_m = 1 + x mod 130, rho_m = x div 130.
-// The fallback stream yields low-28-bit draws (fallback() with the reshare loop disabled).
-constexpr uint32_t CL_PAIR = 130u * 131u;
-constexpr uint32_t CL_LIM = ((1u << 28) / CL_PAIR) * CL_PAIR;
-constexpr uint32_t CL_MAG = (uint32_t)(((1ull << 46) + CL_PAIR - 1) / CL_PAIR);  // u / 17030 = umulhi(u, M) >> 14, u < 2^28
-
-template <int R>
-__device__ __forceinline__ void decode_cl(const uint32_t* T, uint64_t j, const Key& k01, const KP& kp, Tape& tp) {
+__device__ __forceinline__ void decode_pair(const uint32_t* T, uint64_t j, const Key& k01, const KP& kp, Tape& tp) {
   Draws d;
   tp.t = T[0] >> 31;
   d.idx = T[0] & 0x7FFFFFFFu;
@@ -320,21 +288,22 @@ __device__ __forceinline__ void decode_cl(const uint32_t* T, uint64_t j, const K
     const uint32_t nxt = w < 6 ? T[2 + w] : 0u;
     d.um[m] = __funnelshift_r(T[1 + w], nxt, sh) & 0x0FFFFFFFu;
     d.ur[m] = 0u;
-    bad |= d.um[m] >= CL_LIM;
+    bad |= ((uint32_t)m < kp.S) & (d.um[m] >= kp.pair_lim);
   }
   if (__builtin_expect(bad, 0)) {
     Draws f = d;
-    fallback<R>(f, j, k01, 8u, kp.perm_lim, CL_LIM, 1u, 0x0FFFFFFFu);
+    fallback<R>(f, j, k01, kp.S, kp.perm_lim, kp.pair_lim, 1u, 0x0FFFFFFFu);
     d = f;
   }
+  const uint32_t q1 = kp.p - 1u;
 #pragma unroll
   for (int m = 0; m < 8; ++m) {
-    const uint32_t x = d.um[m] - CL_PAIR * (__umulhi(d.um[m], CL_MAG) >> 14);
-    const uint32_t q = __umulhi(x, kp.mag_q);  // x div 130, exact for x < 2^16
-    tp.r[m] = 1u + x - 130u * q;
+    const uint32_t x = d.um[m] - kp.pair_d * (__umulhi(d.um[m], kp.pair_mag) >> kp.pair_sh);
+    const uint32_t q = __umulhi(x, kp.mag_q);  // x div (p-1), exact for x < 2^16
+    tp.r[m] = 1u + x - q1 * q;
     tp.rho[m] = q;
   }
-  tp.sel = perm_sel_rt(d.idx - kp.fact * (__umulhi(d.idx, kp.mag_f) >> kp.sh_f), 8u);
+  tp.sel = perm_sel_rt(d.idx - kp.fact * (__umulhi(d.idx, kp.mag_f) >> kp.sh_f), kp.S);
 }
 
 // ---------------------------------------------------------------------------
@@ -352,7 +321,7 @@ __device__ __forceinline__ uint32_t modp_small(uint32_t x, const KP& kp) {
 }
 
 template <int PARTY>
-__device__ __forceinline__ void party_W_wide(uint64_t x, const KP& kp, const Tape& tp, uint32_t (&W)[8]) {
+__device__ __forceinline__ void party_W_rt(uint64_t x, const KP& kp, const Tape& tp, uint32_t (&W)[8]) {
   const uint64_t nx = 0ull - x;
   const uint64_t v = (PARTY == 0) ? (tp.t ? nx : x) : (tp.t ? x : nx);
   const uint32_t win = (uint32_t)(v >> kp.f);

@@ -180,25 +180,20 @@ __global__ void __launch_bounds__(TPB, 2) k_fused_w(FusedArgs a, KP kp_, Key k01
     const uint64_t j0 = a.base + i0;
     const uint32_t cnt = (uint32_t)min((uint64_t)8, a.n - i0);
     uint32_t zbits = 0, tbits = 0;
-    constexpr int STEP = CL ? 2 : 1;  // elements per seed01 block
 #pragma unroll 1
-    for (int e2 = 0; e2 < 8; e2 += STEP) {
+    for (int e2 = 0; e2 < 8; e2 += 2) {  // one seed01 block holds elements e2, e2 + 1 (j0 is a multiple of 8)
       uint32_t B[16];
-      if constexpr (CL)  // one block holds elements 2i, 2i+1 (j0 is a multiple of 8); pk.tpa: bc2.tpl2
-        stream_blk<R, !RELU>(pk.tpa, k01, L_TAPECL, (j0 + (uint64_t)e2) >> 1, B);
-      else
-        chacha<R>(k01, j0 + (uint64_t)e2, L_TAPEW, B);
+      stream_blk<R, !RELU>(pk.tpa, k01, L_TAPEP, (j0 + (uint64_t)e2) >> 1, B);  // pk.tpa: bc2.tpp1
 #pragma unroll
-    for (int h = 0; h < STEP; ++h) {  // static offsets into B keep it in registers
+    for (int h = 0; h < 2; ++h) {  // static offsets into B keep it in registers
       const int e = e2 + h;
       const uint64_t xa = (uint32_t)e < cnt ? __ldg(a.x0 + i0 + e) : 0ull;
       const uint64_t xb = (uint32_t)e < cnt ? __ldg(a.x1 + i0 + e) : 0ull;
       Tape tp;
-      if constexpr (CL) decode_cl<R>(B + 8 * h, j0 + e, k01, kp, tp);
-      else decode_wide<R>(B, j0 + e, k01, kp, tp);
+      decode_pair<R>(B + 8 * h, j0 + e, k01, kp, tp);
       uint32_t W0[8], W1[8];
-      party_W_wide<0>(xa, kp, tp, W0);
-      party_W_wide<1>(xb, kp, tp, W1);
+      party_W_rt<0>(xa, kp, tp, W0);
+      party_W_rt<1>(xb, kp, tp, W1);
       zbits |= zero_test(W0, W1, kp.p, kp.S) << e;
       tbits |= tp.t << e;
       if (a.w0lo != nullptr && (uint32_t)e < cnt) {
@@ -300,7 +295,7 @@ __global__ void __launch_bounds__(TPB_L) k_fused_b1(FusedArgs a, KP kp, Key k01,
         rho[7] = (uint64_t)B[0] | ((uint64_t)B[1] << 32);
       }
       if (idx >= kp.perm_lim) idx = fallback_b1<R>(j, k01, kp.perm_lim);
-      // step 6: Fisher-Yates nibble selector (same digits as the wide tape)
+      // step 6: Fisher-Yates nibble selector (same digits as the pair tape)
       uint32_t sel = 0x76543210u;
       for (uint32_t m = S - 1; m >= 1; --m) {
         const uint32_t k = idx % (m + 1);
@@ -380,7 +375,7 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
   }
   const KP kp = make_kp(prm);
   const Key k01 = make_key(seeds->s01), k02 = make_key(seeds->s02), k12 = make_key(seeds->s12);
-  const uint64_t tape_a = prm->tape == BC_TAPE_COMPACT_LIT ? L_TAPECL : L_TAPEA;  // the slot the tape kernel reads
+  const uint64_t tape_a = prm->tape == BC_TAPE_COMPACT ? L_TAPEA : L_TAPEP;  // the stream the tape kernel reads
   const PreKeys pk{make_keypre(seeds->s01, tape_a), make_keypre(seeds->s01, L_TAPEB),
                    make_keypre(seeds->s02, L_RESP),  make_keypre(seeds->s02, L_A02),
                    make_keypre(seeds->s02, L_B02),   make_keypre(seeds->s02, L_C02),

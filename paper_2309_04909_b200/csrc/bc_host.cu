@@ -107,8 +107,12 @@ KP make_kp(const bc_params* prm) {
   if (prm->tape != BC_TAPE_LARGE) {
     kp.fact = factorial(prm->slots);
     kp.perm_lim = (uint32_t)((0x80000000ull / kp.fact) * kp.fact);
-    kp.mask_lim = (65536u / (kp.p - 1u)) * (kp.p - 1u);  // wide tape (the compact literal tape has its own)
-    kp.rho_lim = (65536u / kp.p) * kp.p;
+    // pair tape (p <= 131): d = (p-1) p < 2^15; with k = floor(log2 d), M = ceil(2^(32+k) / d) < 2^32
+    // (d is never a power of two) overshoots by e < d, and u e < 2^28 2^(k+1) < 2^(32+k): exact for u < 2^28
+    kp.pair_d = (kp.p - 1u) * kp.p;
+    kp.pair_lim = ((1u << 28) / kp.pair_d) * kp.pair_d;
+    kp.pair_sh = 31u - (uint32_t)__builtin_clz(kp.pair_d);
+    kp.pair_mag = (uint32_t)(((1ull << (32 + kp.pair_sh)) + kp.pair_d - 1) / kp.pair_d);
     // x / d for x < 2^16, d <= 257: ceil(2^32 / d) overshoots 2^32/d by e < 1, and x e / 2^32 < 1/d
     kp.mag_p = (uint32_t)(((1ull << 32) + kp.p - 1) / kp.p);
     kp.mag_q = (uint32_t)(((1ull << 32) + kp.p - 2) / (kp.p - 1u));
@@ -222,7 +226,7 @@ int bc_params_init(bc_params* out, int ell, int lx, int f, int mode, int rounds)
   r.slots = (uint32_t)lx + 1u;
   r.tape = (p == 257u && r.slots == 8u)   ? BC_TAPE_COMPACT
            : (p == 131u && r.slots == 8u) ? BC_TAPE_COMPACT_LIT
-           : (lx <= 7 ? BC_TAPE_WIDE : BC_TAPE_LARGE);
+           : (lx <= 7 ? BC_TAPE_PAIR : BC_TAPE_LARGE);
   *out = r;
   return BC_OK;
 }

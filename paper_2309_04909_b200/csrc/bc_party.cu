@@ -109,23 +109,18 @@ __global__ void __launch_bounds__(TPB, 2) k_send_w(SendArgs a, KP kp_, Key k01, 
     uint64_t lo[8];
     uint32_t tb = 0;
     uint64_t hi = 0;
-    constexpr int STEP = CL ? 2 : 1;  // elements per seed01 block
 #pragma unroll 1
-    for (int e2 = 0; e2 < 8; e2 += STEP) {
+    for (int e2 = 0; e2 < 8; e2 += 2) {  // one seed01 block holds elements e2, e2 + 1 (j0 is a multiple of 8)
       uint32_t B[16];
-      if constexpr (CL)  // one block holds elements 2i, 2i+1 (j0 is a multiple of 8)
-        chacha<R>(k01, (j0 + (uint64_t)e2) >> 1, L_TAPECL, B);
-      else
-        chacha<R>(k01, j0 + (uint64_t)e2, L_TAPEW, B);
+      chacha<R>(k01, (j0 + (uint64_t)e2) >> 1, L_TAPEP, B);
 #pragma unroll
-    for (int h = 0; h < STEP; ++h) {  // static offsets into B keep it in registers
+    for (int h = 0; h < 2; ++h) {  // static offsets into B keep it in registers
       const int e = e2 + h;
       const uint64_t xv = (uint32_t)e < cnt ? __ldg(a.x + i0 + e) : 0ull;
       Tape tp;
-      if constexpr (CL) decode_cl<R>(B + 8 * h, j0 + e, k01, kp, tp);
-      else decode_wide<R>(B, j0 + e, k01, kp, tp);
+      decode_pair<R>(B + 8 * h, j0 + e, k01, kp, tp);
       uint32_t W[8];
-      party_W_wide<PARTY>(xv, kp, tp, W);
+      party_W_rt<PARTY>(xv, kp, tp, W);
       const uint64_t l = pack_lo(W);
       const uint64_t hbyte = pack_hi(W);
 #pragma unroll
