@@ -127,12 +127,19 @@ __device__ __forceinline__ uint32_t window_of(uint64_t x, uint32_t t, uint32_t f
 }
 
 // Steps 3-5 for the 8 windows at once: bytes v'_i - 1 (P0) / v'_i - 1 (P1).
+#ifndef BC_ADD_FMA
+#define BC_ADD_FMA 2  // 0: off; 1: the mask offsets (DReLU only); 2: also the ladder sums
+#endif
+// a + b as a multiply-add a * one + b with one = 1 read from the parameter bank (KP::one):
+// ptxas cannot fold it back into an ALU-pipe IADD3, so it issues on the FMA pipe
+__device__ __forceinline__ uint32_t add_fma(uint32_t a, uint32_t b, uint32_t one) { return a * one + b; }
+
 // E = spread of a_0,a_2,a_4,a_6 into bytes 0,2,4,6 via one 64-bit multiply by
 // 1 + 2^14 + 2^28 + 2^42; O likewise for a_1,a_3,a_5,a_7; 16-bit lanes then
 // hold the pairwise sums without carries.  Verified exhaustively over all
 // 2^15 windows (tests/test_kernel_arith.py).
-template <int PARTY>
-__device__ __forceinline__ void ladder_swar(uint32_t win, uint32_t& lo, uint32_t& hi) {
+template <int PARTY, bool ADDF = false>
+__device__ __forceinline__ void ladder_swar(uint32_t win, uint32_t& lo, uint32_t& hi, uint32_t one = 1u) {
   constexpr uint32_t KL = 1u + (1u << 14) + (1u << 28);
   constexpr uint32_t M = 0x00FF00FFu;
   const uint32_t e = win & 0x3FFFu;
@@ -142,9 +149,17 @@ __device__ __forceinline__ void ladder_swar(uint32_t win, uint32_t& lo, uint32_t
   const uint32_t Olo = (o * KL) & M, Ohi = ((o >> 4) + (o << 10)) & M;
   const uint32_t Slo = __byte_perm(Elo, Ehi, 0x5432u), Shi = Ehi >> 16;  // E >> 16: a_2,a_4,a_6,0
   uint32_t ce_lo, ce_hi, co_lo, co_hi;
-  if (PARTY == 0) {  // u_i + u_{i+1} - 2 (mod 256) = v'_i - 1 for P0
+  if (PARTY == 0 && ADDF && BC_ADD_FMA >= 2) {  // the same sums, one add of each on the FMA pipe
+    const uint32_t Oc_lo = Olo + 0x00FE00FEu, Oc_hi = Ohi + 0x00FE00FEu;
+    ce_lo = Elo * one + Oc_lo; ce_hi = Ehi * one + Oc_hi;
+    co_lo = Slo * one + Oc_lo; co_hi = Shi * one + Oc_hi;
+  } else if (PARTY == 0) {  // u_i + u_{i+1} - 2 (mod 256) = v'_i - 1 for P0
     ce_lo = Elo + Olo + 0x00FE00FEu; ce_hi = Ehi + Ohi + 0x00FE00FEu;
     co_lo = Olo + Slo + 0x00FE00FEu; co_hi = Ohi + Shi + 0x00FE00FEu;
+  } else if (ADDF && BC_ADD_FMA >= 2) {
+    const uint32_t Oc_lo = 0x04000400u - Olo, Oc_hi = 0x04000400u - Ohi;
+    ce_lo = Oc_lo - Elo * one; ce_hi = Oc_hi - Ehi * one;
+    co_lo = Oc_lo - Slo * one; co_hi = Oc_hi - Shi * one;
   } else {           // -(B_i + B_{i+1}) (mod 256) = v'_i - 1 for P1
     ce_lo = 0x04000400u - Elo - Olo; ce_hi = 0x04000400u - Ehi - Ohi;
     co_lo = 0x04000400u - Olo - Slo; co_hi = 0x04000400u - Ohi - Shi;
@@ -198,19 +213,27 @@ __device__ __forceinline__ void mask_slots(uint32_t lo, uint32_t hi, const TapeC
 #ifndef BC_MATERIALIZE
 #define BC_MATERIALIZE 1
 #endif
-template <bool KEEP_W>
-__device__ __forceinline__ uint32_t elem_both(uint64_t x0, uint64_t x1, const TapeC& tp, uint32_t fsh, bool fhi,
+template <bool KEEP_W, bool ADDF = false>
+__device__ __forceinline__ uint32_t elem_both(uint64_t x0, uint64_t x1, const TapeC& tp, uint32_t fsh, bool fhi, uint32_t one,
                                               uint32_t (&W0)[8], uint32_t (&W1)[8]) {
   uint32_t c_lo, c_hi, d_lo, d_hi;
-  ladder_swar<0>(window_of<0>(x0, tp.t, fsh, fhi), c_lo, c_hi);
-  ladder_swar<1>(window_of<1>(x1, tp.t, fsh, fhi), d_lo, d_hi);
+  ladder_swar<0, ADDF>(window_of<0>(x0, tp.t, fsh, fhi), c_lo, c_hi, one);
+  ladder_swar<1, ADDF>(window_of<1>(x1, tp.t, fsh, fhi), d_lo, d_hi, one);
   shuffle_bytes(c_lo, c_hi, tp.sel);
   shuffle_bytes(d_lo, d_hi, tp.sel);
   uint32_t vmin = 0xFFFFFFFFu;
 #pragma unroll
   for (int m = 0; m < 8; ++m) {
     const uint32_t rb = byte_of(tp.rb[m >> 2], m & 3);
-    const uint32_t r = rb + 1u, a0 = rb + tp.rho[m] + 258u, a1 = rb - tp.rho[m] + 515u;
+    const uint32_t r = rb + 1u;
+    uint32_t a0, a1;
+    if (ADDF && BC_ADD_FMA >= 1) {  // the offsets as IMADs (FMA pipe; the ALU pipe is the bound)
+      a0 = add_fma(rb, tp.rho[m] + 258u, one);
+      a1 = add_fma(rb, 515u - tp.rho[m], one);
+    } else {
+      a0 = rb + tp.rho[m] + 258u;
+      a1 = rb - tp.rho[m] + 515u;
+    }
     // P0's and P1's messages as integers < 2^17 congruent to W0_m, W1_m (mod 257)
     const uint32_t x0 = byte_of(m < 4 ? c_lo : c_hi, m & 3) * r + a0;   // (v'+1) r + rho + 257
     const uint32_t x1 = byte_of(m < 4 ? d_lo : d_hi, m & 3) * r + a1;   // (v'+1) r - rho + 514

@@ -52,6 +52,7 @@ struct KP {
   // magic multipliers of the runtime divisions (exact for the ranges used):
   uint32_t mag_p, mag_q;   // ceil(2^32 / p), ceil(2^32 / (p-1)): x / d = umulhi(x, mag) for x < 2^16
   uint32_t mag_f, sh_f;    // ceil(2^(31+l) / S!), l - 1 (l = ceil(log2 S!)): x / S! = umulhi(x, mag_f) >> sh_f, x < 2^31
+  uint32_t one;            // = 1, opaque to ptxas (add_fma: a * one + b stays an IMAD on the FMA pipe)
 };
 
 // The compact literal domain is one fixed parameter set (w = lx = 7, p = 131, 8 slots): its

@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(TPB, FUSED_MINB) k_fused_c(FusedArgs a, KP kp,
         const uint64_t xa = q == 0 ? u0.x : q == 1 ? u0.y : q == 2 ? v0.x : v0.y;
         const uint64_t xb = q == 0 ? u1.x : q == 1 ? u1.y : q == 2 ? v1.x : v1.y;
         uint32_t W0[8], W1[8];
-        const uint32_t z = elem_both<TRANSCRIPT>(xa, xb, tp, kp.fsh, fhi, W0, W1);
+        const uint32_t z = elem_both<TRANSCRIPT, !RELU>(xa, xb, tp, kp.fsh, fhi, kp.one, W0, W1);
         if (TRANSCRIPT && (uint32_t)e < cnt) {  // the P0/P1 -> P2 messages, wire format
           reinterpret_cast<uint64_t*>(a.w0lo)[i0 + e] = pack_lo(W0);
           reinterpret_cast<uint64_t*>(a.w1lo)[i0 + e] = pack_lo(W1);

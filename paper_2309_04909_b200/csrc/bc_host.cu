@@ -104,6 +104,7 @@ KP make_kp(const bc_params* prm) {
   kp.S = prm->slots;
   kp.lx = (uint32_t)prm->lx;
   kp.wmask = (uint32_t)((1ull << prm->w) - 1ull);
+  kp.one = 1u;
   if (prm->tape != BC_TAPE_LARGE) {
     kp.fact = factorial(prm->slots);
     kp.perm_lim = (uint32_t)((0x80000000ull / kp.fact) * kp.fact);

@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(TPB_RSS) k_fused_rss(RssArgs a, KP kp, RssKeys
         const uint64_t xa = q == 0 ? p0.x + p1.x : q == 1 ? p0.y + p1.y : q == 2 ? q0.x + q1.x : q0.y + q1.y;
         const uint64_t xb = q == 0 ? p2.x : q == 1 ? p2.y : q == 2 ? q2.x : q2.y;
         uint32_t W0[8], W1[8];
-        zbits |= elem_both<false>(xa, xb, tp, kp.fsh, fhi, W0, W1) << e;
+        zbits |= elem_both<false>(xa, xb, tp, kp.fsh, fhi, kp.one, W0, W1) << e;
         tbits |= tp.t << e;
       }
 #pragma unroll
