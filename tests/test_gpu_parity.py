@@ -135,6 +135,31 @@ def test_fused_rejection_fallback(api):
             assert np.array_equal(host(y0), ref["y0"]) and np.array_equal(host(y1), ref["y1"])
 
 
+@pytest.mark.parametrize("kw", [PARAMS[4], PARAMS[5]], ids=_ids)
+def test_pair_tape_rejection_fallback(api, kw):
+    """Elements whose pair tape rejects a 28-bit draw (p = 131: 2.6e-4 per element,
+    p = 67: 5e-5) take the fallback stream; fused DReLU / ReLU and both parties'
+    send kernels must match the oracle on them (found from the raw keystream)."""
+    from test_oracle_drelu import _pair_rejects
+    oprm, prm = B.Params(**kw), api.Params(**kw)
+    rej = _pair_rejects(oprm, 1 << 14 if oprm.p == 131 else 1 << 16)
+    assert len(rej) >= 3
+    for r in rej[:6]:
+        base = r - r % 8
+        x, x0, x1 = synth.shares(64, kw["ell"], kw["lx"], kw["f"], "D2", run=r)
+        j = np.arange(64, dtype=np.uint64) + np.uint64(base)
+        for fn in ("drelu", "relu"):
+            ref = getattr(B, fn)(oprm, x0, x1, j, SEEDS)
+            y0, y1 = getattr(api, fn)(dev(x0), dev(x1), prm, SEEDS, elem_base=base)
+            assert np.array_equal(host(y0), ref["y0"]) and np.array_equal(host(y1), ref["y1"]), (fn, r)
+        for party, xs in ((0, x0), (1, x1)):
+            lo, hi, _ = api.drelu_send(party, dev(xs), prm, SEEDS.s01, base)
+            el, eh = _wire(oprm, B.drelu_send(oprm, party, xs, j, SEEDS.s01)["W"])
+            assert np.array_equal(_np_plane(lo), el), (party, r)
+            if api.wire_format(prm)["hi"] is not None:
+                assert np.array_equal(_np_plane(hi), eh), (party, r)
+
+
 def test_sharding_is_bit_identical(api):
     """elem_base addresses every PRG draw by global index: four shards equal one call."""
     kw = PARAMS[0]

@@ -332,3 +332,22 @@ def test_pair_tape_raw_draws(kw, layout):
     exp = cells.size / d
     chi2 = float(((cnt - exp) ** 2 / exp).sum())
     assert chi2 < (d - 1) + 6 * math.sqrt(2 * (d - 1))
+
+
+def _pair_rejects(prm, nblocks):
+    """Elements (of the first 2 * nblocks) whose pair tape takes the fallback stream:
+    the perm index >= floor(2^31/S!) S! or a 28-bit draw >= floor(2^28/d) d, found
+    from the raw keystream words."""
+    from oracle.chacha import chacha_blocks
+    S, p = prm.slots, prm.p
+    d = (p - 1) * p
+    lim = ((1 << 28) // d) * d
+    fact = math.factorial(S)
+    plim = ((1 << 31) // fact) * fact
+    T = np.asarray(chacha_blocks(SEEDS.s01, B.L_TAPEP, list(range(nblocks)), prm.rounds), dtype="<u4").reshape(-1, 8)
+    out = []
+    for jj in range(T.shape[0]):
+        D = sum(int(T[jj, w]) << (32 * (w - 1)) for w in range(1, 8))
+        if (int(T[jj, 0]) & 0x7FFFFFFF) >= plim or any(((D >> (28 * m)) & 0xFFFFFFF) >= lim for m in range(S)):
+            out.append(jj)
+    return out
