@@ -368,7 +368,9 @@ int bc_last_cuda_error(void);
 
 /* Library ABI version (major * 100 + minor).  3.00: the large-tape party
  * phases (slot-major uint32 wire planes), bc_relu_send_to / bc_relu_helper_to,
- * bc_ipc_*, BC_MAX_INDEX, and the 7-block large tape bc2.tpL2 (2.00: 9 blocks). */
+ * bc_ipc_*, BC_MAX_INDEX, and the 7-block large tape bc2.tpL2 (2.00: 9 blocks).
+ * 3.01: the 32-B pair tape bc2.tpp1 (BC_TAPE_PAIR, BC_TAPE_COMPACT_LIT) replaces the
+ * 64-B wide tape: every lx <= 7 domain but the compact one draws different keystream. */
 int bc_version(void);
 
 #ifdef __cplusplus

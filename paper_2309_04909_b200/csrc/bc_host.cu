@@ -191,7 +191,7 @@ Key make_key(const uint8_t* s) {
 
 extern "C" {
 
-int bc_version(void) { return 300; }
+int bc_version(void) { return 301; }
 
 int bc_last_cuda_error(void) { return g_last_cuda; }
 
