@@ -130,6 +130,9 @@ __device__ __forceinline__ uint32_t window_of(uint64_t x, uint32_t t, uint32_t f
 #ifndef BC_ADD_FMA
 #define BC_ADD_FMA 2  // 0: off; 1: the mask offsets (DReLU only); 2: also the ladder sums
 #endif
+#ifndef BC_ADD_FMA_SEND
+#define BC_ADD_FMA_SEND 0  // the same in the compact party send kernels (k_send_c)
+#endif
 // a + b as a multiply-add a * one + b with one = 1 read from the parameter bank (KP::one):
 // ptxas cannot fold it back into an ALU-pipe IADD3, so it issues on the FMA pipe
 __device__ __forceinline__ uint32_t add_fma(uint32_t a, uint32_t b, uint32_t one) { return a * one + b; }
@@ -191,13 +194,14 @@ __device__ __forceinline__ uint32_t mod257s(uint32_t x) {  // x < 2^18
 
 // Steps 7-8 for one party: W_m = (c_m + 1) r_m +- rho_m (mod 257), with
 // r_m = rb_m + 1; the addend carries +257 / +514 so it stays positive.
-template <int PARTY>
-__device__ __forceinline__ void mask_slots(uint32_t lo, uint32_t hi, const TapeC& tp, uint32_t (&W)[8]) {
+template <int PARTY, bool ADDF = false>
+__device__ __forceinline__ void mask_slots(uint32_t lo, uint32_t hi, const TapeC& tp, uint32_t (&W)[8], uint32_t one) {
 #pragma unroll
   for (int m = 0; m < 8; ++m) {
     const uint32_t c = byte_of(m < 4 ? lo : hi, m & 3);
     const uint32_t rb = byte_of(tp.rb[m >> 2], m & 3);
-    const uint32_t add = (PARTY == 0) ? rb + tp.rho[m] + 258u : rb - tp.rho[m] + 515u;
+    const uint32_t off = (PARTY == 0) ? tp.rho[m] + 258u : 515u - tp.rho[m];
+    const uint32_t add = ADDF ? add_fma(rb, off, one) : rb + off;
     W[m] = mod257s(c * (rb + 1u) + add);
   }
 }
@@ -257,12 +261,13 @@ __device__ __forceinline__ uint32_t elem_both(uint64_t x0, uint64_t x1, const Ta
   return vmin == 0u;
 }
 
-template <int PARTY>
-__device__ __forceinline__ void elem_one(uint64_t x, const TapeC& tp, uint32_t fsh, bool fhi, uint32_t (&W)[8]) {
+template <int PARTY, bool ADDF = false>
+__device__ __forceinline__ void elem_one(uint64_t x, const TapeC& tp, uint32_t fsh, bool fhi, uint32_t (&W)[8],
+                                         uint32_t one = 1u) {
   uint32_t lo, hi;
-  ladder_swar<PARTY>(window_of<PARTY>(x, tp.t, fsh, fhi), lo, hi);
+  ladder_swar<PARTY, ADDF>(window_of<PARTY>(x, tp.t, fsh, fhi), lo, hi, one);
   shuffle_bytes(lo, hi, tp.sel);
-  mask_slots<PARTY>(lo, hi, tp, W);
+  mask_slots<PARTY, ADDF>(lo, hi, tp, W, one);
 }
 
 }  // namespace bc

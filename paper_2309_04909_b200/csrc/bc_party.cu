@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(TPB, 2) k_send_c(SendArgs a, KP kp, Key k01, K
         decode_c<R>(A[4 * q], A[4 * q + 1], A[4 * q + 2], A[4 * q + 3], Bp[8 * hb + 2 * q], Bp[8 * hb + 2 * q + 1],
                     j0 + (uint64_t)e, k01, sA, sB, tp);
         uint32_t W[8];
-        elem_one<PARTY>(q == 0 ? u.x : q == 1 ? u.y : q == 2 ? v.x : v.y, tp, kp.fsh, fhi, W);
+        elem_one<PARTY, BC_ADD_FMA_SEND != 0>(q == 0 ? u.x : q == 1 ? u.y : q == 2 ? v.x : v.y, tp, kp.fsh, fhi, W, kp.one);
         lo[e] = pack_lo(W);
         hi |= (uint64_t)pack_hi(W) << (8 * e);
         tb |= tp.t << e;

@@ -14,9 +14,11 @@ from paper_2309_04909_b200 import api  # noqa: E402
 
 n = 1 << 24
 dev = torch.device("cuda:0")
-prm = api.Params(ell=64, lx=31, f=0, mode="guard", rounds=20)
+LX = int(os.environ.get("TIME_LX", "31"))  # 7: the compact tape (f = 24)
+F = 24 if LX == 7 else 0
+prm = api.Params(ell=64, lx=LX, f=F, mode="guard", rounds=20)
 sd = synth.seeds(0)
-x, x0, x1 = synth.shares(n, 64, 31, 0, "D2")
+x, x0, x1 = synth.shares(n, 64, LX, F, "D2")
 t0 = torch.from_numpy(x0.view(np.int64)).to(dev)
 t1 = torch.from_numpy(x1.view(np.int64)).to(dev)
 lo0, hi0, tb0 = api.drelu_send(0, t0, prm, sd.s01)
@@ -36,7 +38,11 @@ def ms(fn, reps=10):
     return a.elapsed_time(b) / reps
 
 
+ya, d0 = torch.empty_like(t0), torch.empty_like(t0)
 out = {"send_p0": ms(lambda: api.drelu_send(0, t0, prm, sd.s01, out=(lo0, hi0, tb0)), 3),
+       "send_p1": ms(lambda: api.drelu_send(1, t1, prm, sd.s01, out=(lo1, hi1, tb1)), 3),
+       "send_p0_y": ms(lambda: api.drelu_send(0, t0, prm, sd.s01, out=(lo0, hi0, None), y=ya, seed02=sd.s02), 3),
+       "relu_send_p0": ms(lambda: api.relu_send(0, t0, prm, sd.s01, sd.s02, out=(lo0, hi0, tb0, d0)), 3),
        "helper_drelu": ms(lambda: api.drelu_helper(lo0, hi0, lo1, hi1, prm, sd.s02, out=(None, r1))),
        "helper_relu": ms(lambda: api.relu_helper(lo0, hi0, lo1, hi1, prm, sd.s02, sd.s12, out=(e, c1)))}
 print(json.dumps(out))

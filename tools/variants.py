@@ -14,7 +14,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2309_04909_b200", "variants")
-KNOBS = {"BC_ADD_FMA": [0, 1, 2]}  # knobs in csrc/: also BC_MATERIALIZE, BC_FUSED_MINB, BC_ROT_FMA, BC_CHACHA_UNROLL
+KNOBS = {"BC_ADD_FMA_SEND": [0, 1]}  # knobs in csrc/: also BC_ADD_FMA, BC_MATERIALIZE, BC_FUSED_MINB, BC_ROT_FMA, BC_CHACHA_UNROLL
 
 
 def variants():
