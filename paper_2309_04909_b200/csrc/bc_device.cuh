@@ -341,8 +341,9 @@ __device__ __forceinline__ void party_W_rt(uint64_t x, const KP& kp, const Tape&
       const uint32_t nxt = ((uint32_t)i < kp.lx) ? u[i + 1] : 0u;
       uint32_t vi = (u[i] + nxt - (PARTY == 0 ? 1u : 0u)) & kp.wmask;  // step 4
       uint32_t vp;                                                      // step 5 (Alg 6)
-      if (PARTY == 0) vp = (vi == 0) ? modp_small(1u << kp.w, kp) : modp_small(vi, kp);
-      else vp = modp_small(kp.p + vi - (1u << kp.w), kp);
+      // p > 2^w (C7), so both values already lie in [1, p): no reduction needed
+      if (PARTY == 0) vp = (vi == 0) ? (1u << kp.w) : vi;
+      else vp = kp.p + vi - (1u << kp.w);
       e = vp - 1u;
     }
     if (i < 4) bytes_lo |= e << (8 * i); else bytes_hi |= e << (8 * (i - 4));
