@@ -92,76 +92,102 @@ def load_traffic():
 
 
 # ---------------------------------------------------------------------------
-# CPU oracle leg (cpu_baseline / --impl reference): the oracle as it stands,
-# on a bounded sample, in a process pool over the host cores.
+# CPU oracle legs (cpu_baseline / --impl reference): the scalar C oracle
+# (oracle/c/bicoptor_ref.c, OpenMP) as it stands, on a bounded sample of the
+# bench workload; the numpy oracle alongside for reference.
 # ---------------------------------------------------------------------------
+def _workload_slice(lo: int, hi: int):
+    """Elements lo .. hi - 1 of the bench workload (D2 activations, run 0 sharing)."""
+    import synth
+    x = synth.plaintext(hi - lo, ELL, LX, F, "D2", run=lo)
+    return synth.share(x, ELL, run=lo)
+
+
+def cref_rate(relu: bool, rounds: int, threads: int, budget_s: float):
+    """Elements/s of the C oracle on `threads` host threads (0 = all): calibrate on a
+    small slice, then time one call on a slice sized to about budget_s seconds."""
+    from oracle import bicoptor as B, cref
+    import synth
+    prm = B.Params(ell=ELL, lx=LX, f=F, mode=MODE, rounds=rounds)
+    sd = synth.seeds(0)
+    m = 1 << 14
+    x0, x1 = _workload_slice(0, m)
+    t0 = time.perf_counter()
+    cref.fused(prm, x0, x1, 0, sd, relu=relu, threads=threads)
+    per_s = m / max(time.perf_counter() - t0, 1e-6)
+    m = int(min(1 << 24, max(1 << 14, per_s * budget_s)))
+    x0, x1 = _workload_slice(0, m)
+    t0 = time.perf_counter()
+    cref.fused(prm, x0, x1, 0, sd, relu=relu, threads=threads)
+    return m / (time.perf_counter() - t0), m
+
+
 def _oracle_chunk(args):
-    """One worker: generate its slice of the workload, then time only the oracle call."""
+    """One numpy-oracle worker: generate its slice of the workload, then time only the oracle call."""
     lo, hi, fn, rounds = args
     import synth
     from oracle import bicoptor as B
     prm = B.Params(ell=ELL, lx=LX, f=F, mode=MODE, rounds=rounds)
-    x = synth.plaintext(hi - lo, ELL, LX, F, "D2", run=lo)   # this worker's slice only
-    x0, x1 = synth.share(x, ELL, run=lo)
+    x0, x1 = _workload_slice(lo, hi)
     j = np.arange(lo, hi, dtype=np.uint64)
     t0 = time.perf_counter()
     getattr(B, fn)(prm, x0, x1, j, synth.seeds(0))
     return hi - lo, time.perf_counter() - t0
 
 
-def oracle_rate(fn: str, rounds: int, budget_s: float = 12.0):
-    """Elements/s of the numpy oracle on the host cores for the bench workload:
-    one process per core, each timing the oracle on its own slice; rate = all
-    elements / slowest worker."""
-    import concurrent.futures as cf
-    cores = min(os.cpu_count() or 1, 16)
-    cnt, dt = _oracle_chunk((0, 4096, fn, rounds))   # calibrate on one core
-    per = max(4096, int(cnt / dt * budget_s))
-    per = 1 << int(math.log2(per))
-    tasks = [(k * per, (k + 1) * per, fn, rounds) for k in range(cores)]
-    with cf.ProcessPoolExecutor(max_workers=cores) as ex:
-        res = list(ex.map(_oracle_chunk, tasks))
-    done = sum(r[0] for r in res)
-    dt = max(r[1] for r in res)
-    return done / dt, cores, (f"{cores} processes x 2^{int(math.log2(per))} elements of the bench workload "
-                              f"({fn}, D2), oracle.bicoptor.{fn} (numpy)")
+def cpu_baseline(rounds: int):
+    """The oracle timed on the host cores (rank 0 at N=1 only): the C oracle single-threaded
+    and on all nproc threads (value), plus the numpy oracle on one core."""
+    from oracle import cref
+    nproc = os.cpu_count() or 1
+    threads = cref.threads()
+    r1, m1 = cref_rate(False, rounds, 1, 4.0)
+    rn, mn = cref_rate(False, rounds, 0, 4.0)
+    rr, mr = cref_rate(True, rounds, 0, 3.0)
+    cnt, dt = _oracle_chunk((0, 1 << 13, "drelu", rounds))
+    return {"value": rn, "unit": "elements/s", "cores": threads, "kind": "oracle",
+            "sample": f"C oracle (oracle/c/bicoptor_ref.c, gcc -O2 -fopenmp), DReLU on the bench workload: "
+                      f"{mn} elements on {threads} threads (nproc {nproc}); 1 thread: {m1} elements",
+            "nproc": nproc, "single_thread": r1, "relu_all_threads": rr,
+            "numpy_oracle_one_core": cnt / dt}
 
 
 def run_reference(a, budget_s: float | None = None):
-    """The reference arm for this tier: the oracle, as it stands, on the host
-    cores (tier framing 4).  One process pool; each step is a bounded sample of
-    the bench workload (per worker a slice of m elements at distinct global
-    offsets), sized so warmup + steps fit in about budget_s seconds."""
+    """The reference arm for this tier: the C oracle, as it stands, on all host cores
+    (tier framing 4).  Each step is a bounded sample of the bench workload (a fresh
+    slice of m elements at its own global offset), sized so warmup + steps fit in
+    about budget_s seconds."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import concurrent.futures as cf
-    cores = min(os.cpu_count() or 1, 16)
-    if budget_s is None:  # BENCH_REF_BUDGET_S: tests shrink the run (default ~2 minutes of CPU work)
-        budget_s = float(os.environ.get("BENCH_REF_BUDGET_S", "120"))
-    cnt, dt = _oracle_chunk((0, 4096, "drelu", a.rounds))      # one core, calibration
-    per_core = cnt / dt
+    from oracle import bicoptor as B, cref
+    import synth
+    if budget_s is None:  # BENCH_REF_BUDGET_S: tests shrink the run (default ~1 minute of CPU work)
+        budget_s = float(os.environ.get("BENCH_REF_BUDGET_S", "60"))
+    threads = cref.threads()
+    prm = B.Params(ell=ELL, lx=LX, f=F, mode=MODE, rounds=a.rounds)
+    sd = synth.seeds(0)
+    per_s, _ = cref_rate(False, a.rounds, 0, 0.5)
     total = max(a.warmup, 3) + a.steps
-    m = int(per_core * budget_s / total)
-    m = max(64, min(1 << 20, 1 << max(6, int(math.log2(max(m, 64))))))
-    times, step_vals = [], []
-    with cf.ProcessPoolExecutor(max_workers=cores) as ex:
-        for s in range(total):
-            tasks = [((s * cores + k) * m, (s * cores + k + 1) * m, "drelu", a.rounds) for k in range(cores)]
-            t0 = time.perf_counter()
-            res = list(ex.map(_oracle_chunk, tasks))
-            wall = time.perf_counter() - t0
-            if s >= total - a.steps:
-                times.append(wall)
-                step_vals.append(sum(r[0] for r in res) / max(r[1] for r in res))
-    value = float(np.median(step_vals))
-    sample = f"{cores} processes x {m} elements per step of the bench workload (drelu, D2), oracle.bicoptor.drelu (numpy)"
+    m = int(max(1 << 12, min(1 << 24, per_s * budget_s / total)))
+    times, vals = [], []
+    for s in range(total):
+        x0, x1 = _workload_slice(s * m, (s + 1) * m)
+        t0 = time.perf_counter()
+        cref.fused(prm, x0, x1, s * m, sd, threads=0)
+        dt = time.perf_counter() - t0
+        if s >= total - a.steps:
+            times.append(dt)
+            vals.append(m / dt)
+    value = float(np.median(vals))
+    sample = (f"C oracle (oracle/c/bicoptor_ref.c, OpenMP) on {threads} threads (nproc {os.cpu_count()}): "
+              f"{m} elements of the bench workload (DReLU, D2) per step")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": a.gpus,
         "steps": a.steps, "warmup": max(a.warmup, 3), "ms_per_step": 1e3 * float(np.mean(times)),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": workload_config(a),
-        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": threads, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -479,8 +505,7 @@ def run_cuda(a):
         # ---- e2e through the public API with pinned HOST buffers ----------------
         line["e2e"] = e2e(api, prm, seeds, x0h, x1h, base, dev, world, max_over_ranks, barrier, a)
     if rank == 0 and world == 1 and not a.no_extras:  # the CPU baseline: rank 0 at N=1 only
-        rate, cores, sample = oracle_rate("drelu", a.rounds)
-        line["cpu_baseline"] = {"value": rate, "unit": "elements/s", "cores": cores, "kind": "oracle", "sample": sample}
+        line["cpu_baseline"] = cpu_baseline(a.rounds)
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

@@ -51,6 +51,7 @@ int check_launch();                                  // cudaGetLastError -> BC_O
 int cuda_rc(cudaError_t e);                          // records e for bc_last_cuda_error
 int grid_for(const void* fn, uint64_t nthreads_work, int tpb = TPB, size_t smem = 0);  // persistent grid size
 KPL make_kpl(const bc_params* prm);                  // large-tape constants (p < 2^33)
+int allow_smem(const void* fn, size_t bytes);       // dynamic shared memory above 48 KB (cached)
 bool aligned16(const void* p);
 bool aligned8(const void* p);
 bool overlap(const void* a, size_t na, const void* b, size_t nb);

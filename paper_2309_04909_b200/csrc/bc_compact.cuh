@@ -15,6 +15,7 @@
 //   z      = [exists m: W0_m + W1_m in {0, 257}]                     (step 9)
 #pragma once
 #include "bc_device.cuh"
+#include "bc_tables.cuh"
 
 namespace bc {
 
@@ -114,6 +115,29 @@ __device__ __forceinline__ void decode_c(uint32_t T0, uint32_t T1, uint32_t T2, 
     tp.rho[3 * k + 1] = q1 - 257u * q2;
     if (k < 2) tp.rho[3 * k + 2] = q2 - 257u * div257s(q2);
   }
+}
+
+// The compact tape for the table kernels: the permutation as its index mod 8!
+// (the selector is looked up in shared memory), the reshare digits as above.
+template <int R>
+__device__ __forceinline__ uint32_t decode_t(uint32_t T0, uint32_t w0, uint32_t w1, uint32_t w2, uint64_t j,
+                                             const Key& k01, uint32_t (&rho)[8]) {
+  uint32_t idx = T0 & 0x7FFFFFFFu;
+  if (__builtin_expect((idx >= PERM_LIMIT_8) | (max(w0, max(w1, w2)) >= RHO_WORD_LIMIT), 0)) {
+    const FbC d = fallback_c<R>(FbC{idx, w0, w1, w2}, j, k01);
+    idx = d.idx; w0 = d.w0; w1 = d.w1; w2 = d.w2;
+  }
+  // idx mod 8! = idx - 40320 floor((idx >> 7) / 315); umulhi(x, ceil(2^32 / 315)) is exact for x < 2^24
+  const uint32_t ix = idx - 40320u * __umulhi(idx >> 7, 13634817u);
+  const uint32_t w[3] = {w0, w1, w2};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {  // base-257 digits, least significant first
+    const uint32_t q1 = div257(w[k]), q2 = div257s(q1);  // q1 < 2^24, q2 < 2^16
+    rho[3 * k] = w[k] - 257u * q1;
+    rho[3 * k + 1] = q1 - 257u * q2;
+    if (k < 2) rho[3 * k + 2] = q2 - 257u * div257s(q2);
+  }
+  return ix;
 }
 
 // Windows of the party's blinded share: bits [f, f+32) of (-1)^t x (P0) or of
@@ -259,6 +283,178 @@ __device__ __forceinline__ uint32_t elem_both(uint64_t x0, uint64_t x1, const Ta
   }
   if (!KEEP_W && BC_MATERIALIZE <= 1) return vmin <= 16711935u;
   return vmin == 0u;
+}
+
+// ---------------------------------------------------------------------------
+// Table-driven variant (bc_tables.cuh; one CTA of 512 threads per SM holds the
+// 210 KB of tables in shared memory).  Per element the ladder of each party is
+// two shared-memory lookups instead of the SWAR arithmetic, and the shuffle is
+// one lookup of the full 8! selector and one PRMT per output word.
+// ---------------------------------------------------------------------------
+// Window bits [f, f+32) of v (only [f, f+15) are used); FHI: f >= 32, fsh = f mod 32.
+template <bool FHI>
+__device__ __forceinline__ uint32_t win_at(uint64_t v, uint32_t fsh) {
+  const uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
+  return FHI ? (hi >> fsh) : __funnelshift_r(lo, hi, fsh);
+}
+
+// Byte offsets into the ladder sub-tables: 4 * (win mod 2^12), 4 * ((win >> 4) mod 2^11).
+__device__ __forceinline__ uint32_t lad_lo_off(uint32_t win) { return (win << 2) & 0x3FFCu; }
+__device__ __forceinline__ uint32_t lad_hi_off(uint32_t win) { return (win >> 2) & 0x1FFCu; }
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t saddr) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(saddr));
+  return v;
+}
+#ifndef BC_SELH_LDS
+#define BC_SELH_LDS 1
+#endif
+#ifndef BC_EXTRACT_DP4A
+#define BC_EXTRACT_DP4A 0
+#endif
+
+// Steps 1-9 for both computing parties and P2, table form.  sbase: shared-window
+// address of the tables (kPermSel at 0, kLadder after it).  ix: perm index mod 8!.
+// Returns z; the messages as in elem_both.
+template <bool KEEP_W, bool FHI>
+__device__ __forceinline__ uint32_t elem_both_t(uint64_t x0, uint64_t x1, uint32_t t, uint32_t ix, const uint32_t (&rb)[2],
+                                                const uint32_t (&rho)[8], uint32_t sbase, uint32_t fsh, uint32_t one,
+                                                uint32_t (&W0)[8], uint32_t (&W1)[8]) {
+  // steps 1-3: P0 windows (-1)^t x_0, P1 windows -(-1)^t x_1 (Alg 5 on -s_1, reading C3)
+  const uint64_t v0 = t ? 0ull - x0 : x0;
+  const uint64_t v1 = t ? x1 : 0ull - x1;
+  const uint32_t wn0 = win_at<FHI>(v0, fsh), wn1 = win_at<FHI>(v1, fsh);
+  constexpr uint32_t LAD = 4u * kPermN;
+  // steps 3-5: ladder, pairwise sums and modulo switch as bytes v'_i - 1 (table)
+  const uint32_t c_lo = lds_u32(sbase + LAD + 4u * kLadP0Lo + lad_lo_off(wn0));
+  const uint32_t c_hi = lds_u32(sbase + LAD + 4u * kLadP0Hi + lad_hi_off(wn0));
+  const uint32_t d_lo = lds_u32(sbase + LAD + 4u * kLadP1Lo + lad_lo_off(wn1));
+  const uint32_t d_hi = lds_u32(sbase + LAD + 4u * kLadP1Hi + lad_hi_off(wn1));
+  // step 6: the permutation as one selector (nibble m = source slot of slot m)
+  const uint32_t sel = lds_u32(sbase + ix * 4u);
+#if BC_SELH_LDS
+  const uint32_t selh = lds_u16(sbase + ix * 4u + 2u);  // the high selector half as a second load (LSU, not ALU)
+#else
+  const uint32_t selh = sel >> 16;
+#endif
+  const uint32_t C_lo = prmt(c_lo, c_hi, sel), C_hi = prmt(c_lo, c_hi, selh);
+  const uint32_t D_lo = prmt(d_lo, d_hi, sel), D_hi = prmt(d_lo, d_hi, selh);
+  uint32_t vmin = 0xFFFFFFFFu;
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+#if BC_EXTRACT_DP4A  // byte extraction as a dot product with a unit byte vector (IDP.4A, FMA pipe)
+    const uint32_t unit = 1u << (8 * (m & 3));
+    const uint32_t rbm = __dp4a(rb[m >> 2], unit, 0u);
+    const uint32_t r = __dp4a(rb[m >> 2], unit, 1u);
+    const uint32_t cm = __dp4a(m < 4 ? C_lo : C_hi, unit, 0u), dm = __dp4a(m < 4 ? D_lo : D_hi, unit, 0u);
+#else
+    const uint32_t rbm = byte_of(rb[m >> 2], m & 3);
+    const uint32_t r = rbm + 1u;
+    const uint32_t cm = byte_of(m < 4 ? C_lo : C_hi, m & 3), dm = byte_of(m < 4 ? D_lo : D_hi, m & 3);
+#endif
+    // steps 7-8: P0's and P1's messages as integers congruent to W0_m, W1_m (mod 257)
+    const uint32_t a0 = add_fma(rbm, rho[m] + 258u, one);            // r + rho + 257
+    const uint32_t a1 = add_fma(rbm, 515u - rho[m], one);            // r - rho + 514
+    const uint32_t xm0 = cm * r + a0;                                 // (v'+1) r + rho + 257
+    const uint32_t xm1 = dm * r + a1;                                 // (v'+1) r - rho + 514
+    if (!KEEP_W && BC_MATERIALIZE == 1) {
+      // P0's wire value W0 in [0, 257), P1's congruent message; P2: 257 | (W0 + x1), the sum on the FMA pipe
+      vmin = min(vmin, add_fma(mod257s(xm0), xm1, one) * 0xFF00FF01u);
+    } else if (KEEP_W || BC_MATERIALIZE) {
+      W0[m] = mod257s(xm0);
+      W1[m] = mod257s(xm1);
+      vmin = min(vmin, add_fma(W0[m], W1[m], one) * 0xFF00FF01u);  // 257 | s iff s in {0, 257}
+    } else {
+      vmin = min(vmin, add_fma(xm0, xm1, one) * 0xFF00FF01u);
+    }
+  }
+  return vmin <= 16711935u;  // some s_m divisible by 257: s * 257^-1 mod 2^32 <= floor((2^32-1)/257)
+}
+
+// ---- v2 of the table kernel's slot arithmetic (BC_TBL_V2) ----------------------------
+// The reshare enters as congruent offsets decoded straight from the digit quotients:
+//   P0: x0_m = (v'_m) r_m + o0_m, o0_m = rho_m + 257 k  (k >= 0; < 2^24)
+//   P1: x1_m = (v'_m) r_m + o1_m, o1_m = 257 K - rho_m  (> 0;     < 2^25)
+// with rho_{3k} = w - 257 q1 (reduced), rho_{3k+1} = q1 - 257 q2 (== q1), rho_{3k+2}
+// = q2 mod 257 (== q2), q1 = w div 257, q2 = q1 div 257.  The bytes v'-1 and r-1 are
+// extracted with the +1 folded in: dp4a(word, unit byte vector, 1) = byte + 1 (IDP.4A,
+// FMA pipe).  W0 = x0 mod 257 (< 2^25: div257s exact); P2 tests 257 | (W0 + x1).
+#ifndef BC_TBL_V2
+#define BC_TBL_V2 0
+#endif
+template <int R>
+__device__ __forceinline__ uint32_t decode_t2(uint32_t T0, uint32_t w0, uint32_t w1, uint32_t w2, uint64_t j,
+                                              const Key& k01, uint32_t (&o0)[8], uint32_t (&o1)[8]) {
+  uint32_t idx = T0 & 0x7FFFFFFFu;
+  if (__builtin_expect((idx >= PERM_LIMIT_8) | (max(w0, max(w1, w2)) >= RHO_WORD_LIMIT), 0)) {
+    const FbC d = fallback_c<R>(FbC{idx, w0, w1, w2}, j, k01);
+    idx = d.idx; w0 = d.w0; w1 = d.w1; w2 = d.w2;
+  }
+  const uint32_t ix = idx - 40320u * __umulhi(idx >> 7, 13634817u);
+  const uint32_t w[3] = {w0, w1, w2};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const uint32_t q1 = div257(w[k]);                       // < 2^24
+    o0[3 * k] = w[k] - 257u * q1;                           // rho_{3k}, reduced
+    o1[3 * k] = 257u * q1 + (257u - w[k]);                  // 257 - rho_{3k} > 0
+    o0[3 * k + 1] = q1;                                     // == rho_{3k+1} (mod 257)
+    o1[3 * k + 1] = 16842752u - q1;                         // 257 * 2^16 - q1 > 0
+    if (k < 2) {
+      const uint32_t q2 = div257s(q1);                      // < 2^16
+      o0[3 * k + 2] = q2;                                   // == rho_{3k+2}
+      o1[3 * k + 2] = 65792u - q2;                          // 257 * 256 - q2 > 0
+    }
+  }
+  return ix;
+}
+
+template <bool KEEP_W, bool FHI>
+__device__ __forceinline__ uint32_t elem_both_t2(uint64_t x0, uint64_t x1, uint32_t t, uint32_t ix, const uint32_t (&rb)[2],
+                                                 const uint32_t (&o0)[8], const uint32_t (&o1)[8], uint32_t sbase,
+                                                 uint32_t fsh, uint32_t one, uint32_t (&W0)[8], uint32_t (&W1)[8]) {
+  const uint64_t v0 = t ? 0ull - x0 : x0;
+  const uint64_t v1 = t ? x1 : 0ull - x1;
+  const uint32_t wn0 = win_at<FHI>(v0, fsh), wn1 = win_at<FHI>(v1, fsh);
+  const uint32_t four = one * 4u;  // opaque: the low offsets as IMAD (FMA pipe) + LOP3
+  constexpr uint32_t LAD = 4u * kPermN;
+  const uint32_t c_lo = lds_u32(sbase + LAD + 4u * kLadP0Lo + ((wn0 * four) & 0x3FFCu));
+  const uint32_t c_hi = lds_u32(sbase + LAD + 4u * kLadP0Hi + lad_hi_off(wn0));
+  const uint32_t d_lo = lds_u32(sbase + LAD + 4u * kLadP1Lo + ((wn1 * four) & 0x3FFCu));
+  const uint32_t d_hi = lds_u32(sbase + LAD + 4u * kLadP1Hi + lad_hi_off(wn1));
+  const uint32_t sel = lds_u32(sbase + ix * 4u);
+#if BC_SELH_LDS
+  const uint32_t selh = lds_u16(sbase + ix * 4u + 2u);
+#else
+  const uint32_t selh = sel >> 16;
+#endif
+  const uint32_t C_lo = prmt(c_lo, c_hi, sel), C_hi = prmt(c_lo, c_hi, selh);
+  const uint32_t D_lo = prmt(d_lo, d_hi, sel), D_hi = prmt(d_lo, d_hi, selh);
+  uint32_t vmin = 0xFFFFFFFFu;
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const uint32_t unit = 1u << (8 * (m & 3));
+    const uint32_t r = __dp4a(rb[m >> 2], unit, 1u);                  // r_m = 1 + mask byte
+    const uint32_t c1 = __dp4a(m < 4 ? C_lo : C_hi, unit, 1u);        // v'_m (P0)
+    const uint32_t d1 = __dp4a(m < 4 ? D_lo : D_hi, unit, 1u);        // v'_m (P1)
+    const uint32_t xm0 = c1 * r + o0[m];                              // == W0_m (mod 257)
+    const uint32_t xm1 = d1 * r + o1[m];                              // == W1_m (mod 257)
+    if (KEEP_W || BC_MATERIALIZE == 2) {
+      W0[m] = mod257s(xm0);
+      W1[m] = mod257s(xm1);
+      vmin = min(vmin, add_fma(W0[m], W1[m], one) * 0xFF00FF01u);
+    } else if (BC_MATERIALIZE == 1) {
+      vmin = min(vmin, add_fma(mod257s(xm0), xm1, one) * 0xFF00FF01u);
+    } else {
+      vmin = min(vmin, add_fma(xm0, xm1, one) * 0xFF00FF01u);
+    }
+  }
+  return vmin <= 16711935u;
 }
 
 template <int PARTY, bool ADDF = false>

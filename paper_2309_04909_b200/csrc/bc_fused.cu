@@ -170,6 +170,80 @@ __global__ void __launch_bounds__(TPB, FUSED_MINB) k_fused_c(FusedArgs a, KP kp,
   }
 }
 
+// Compact tape, table form (bc_tables.cuh): one CTA of TPB_T threads per SM with
+// the 210 KB of ladder and permutation tables in shared memory.  Same tape, same
+// thread mapping and the same finish as k_fused_c.
+#ifndef BC_FUSED_TABLES
+#define BC_FUSED_TABLES 1  // 0: the SWAR kernel k_fused_c for the compact tape
+#endif
+constexpr int TPB_T = 512;
+constexpr size_t kTabBytes = sizeof(uint32_t) * kTabWords;
+__device__ constexpr CompactTables kTables{};
+
+__device__ __forceinline__ void load_tables(uint32_t* s) {
+  const uint4* g = reinterpret_cast<const uint4*>(kTables.w);
+  uint4* d = reinterpret_cast<uint4*>(s);
+  for (int i = threadIdx.x; i < kTabWords / 4; i += blockDim.x) d[i] = g[i];
+}
+
+template <int R, bool RELU, bool TRANSCRIPT, bool FULL, bool FHI>
+__global__ void __launch_bounds__(TPB_T, 1) k_fused_t(FusedArgs a, KP kp, Key k01, Key k02, Key k12, PreKeys pk) {
+  extern __shared__ uint4 smem_t[];
+  uint32_t* tabs = reinterpret_cast<uint32_t*>(smem_t);
+  load_tables(tabs);
+  __syncthreads();
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tabs);
+  const uint64_t ngroups = (a.n + 7) >> 3;
+  for (uint64_t g = (uint64_t)blockIdx.x * TPB_T + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB_T) {
+    const uint64_t i0 = g << 3;
+    const uint64_t j0 = a.base + i0;
+    const uint32_t cnt = (uint32_t)min((uint64_t)8, a.n - i0);
+    uint32_t zbits = 0, tbits = 0;
+    uint32_t Bp[16];  // part B: words 2e, 2e+1 of element e (reshare words w1, w2)
+    stream_blk<R, !RELU>(pk.tpb, k01, L_TAPEB, j0 >> 3, Bp);
+#pragma unroll 1
+    for (int hb = 0; hb < 2; ++hb) {
+      const uint64_t ib = i0 + 4 * hb;
+      const ulonglong2 u0 = load2(a.x0, ib, a.n), u1 = load2(a.x1, ib, a.n);
+      const ulonglong2 v0 = load2(a.x0, ib + 2, a.n), v1 = load2(a.x1, ib + 2, a.n);
+      uint32_t A[16];  // part A: words 4q..4q+3 of element 4 hb + q
+      stream_blk<R, !RELU>(pk.tpa, k01, L_TAPEA, (j0 >> 2) + (uint64_t)hb, A);
+      const uint32_t bit0 = 1u << (4 * hb);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = 4 * hb + q;
+        const uint32_t T0 = A[4 * q];
+        const uint32_t t = T0 >> 31;
+        const uint32_t rb[2] = {A[4 * q + 1], A[4 * q + 2]};
+        const uint64_t xa = q == 0 ? u0.x : q == 1 ? u0.y : q == 2 ? v0.x : v0.y;
+        const uint64_t xb = q == 0 ? u1.x : q == 1 ? u1.y : q == 2 ? v1.x : v1.y;
+        uint32_t W0[8], W1[8];
+#if BC_TBL_V2
+        uint32_t o0[8], o1[8];
+        const uint32_t ix = decode_t2<R>(T0, A[4 * q + 3], Bp[2 * q], Bp[2 * q + 1], j0 + (uint64_t)e, k01, o0, o1);
+        const uint32_t z = elem_both_t2<TRANSCRIPT, FHI>(xa, xb, t, ix, rb, o0, o1, sbase, kp.fsh, kp.one, W0, W1);
+#else
+        uint32_t rho[8];
+        const uint32_t ix = decode_t<R>(T0, A[4 * q + 3], Bp[2 * q], Bp[2 * q + 1], j0 + (uint64_t)e, k01, rho);
+        const uint32_t z = elem_both_t<TRANSCRIPT, FHI>(xa, xb, t, ix, rb, rho, sbase, kp.fsh, kp.one, W0, W1);
+#endif
+        if (TRANSCRIPT && (uint32_t)e < cnt) {  // the P0/P1 -> P2 messages, wire format
+          reinterpret_cast<uint64_t*>(a.w0lo)[i0 + e] = pack_lo(W0);
+          reinterpret_cast<uint64_t*>(a.w1lo)[i0 + e] = pack_lo(W1);
+          a.w0hi[i0 + e] = (uint8_t)pack_hi(W0);
+          a.w1hi[i0 + e] = (uint8_t)pack_hi(W1);
+        }
+        const uint32_t bit = bit0 << q;
+        zbits = z * bit + zbits;   // IMADs: the bit masks on the FMA pipe
+        tbits = t * bit + tbits;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) Bp[k] = Bp[k + 8];  // elements 4..7 next
+    }
+    finish_group<R, RELU, FULL>(a, kp, k02, k12, pk, i0, j0, cnt, zbits, tbits);
+  }
+}
+
 // Wide tape (any p <= 257, 3..8 slots): one seed01 block per element.
 template <int R, bool RELU, bool CL>
 __global__ void __launch_bounds__(TPB, 2) k_fused_w(FusedArgs a, KP kp_, Key k01, Key k02, Key k12, PreKeys pk) {
@@ -388,6 +462,14 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
       const KPL kl = make_kpl(prm);
       auto fn = tr ? k_fused_l<R, RELU, true> : k_fused_l<R, RELU, false>;
       fn<<<grid_for((const void*)fn, ngroups, TPB_L), TPB_L, 0, st>>>(a, kp, kl, k01, k02, k12, pk);
+    } else if (prm->tape == BC_TAPE_COMPACT && BC_FUSED_TABLES) {
+      const bool fhi = kp.fhi != 0;
+      auto fn = tr ? (fhi ? k_fused_t<R, RELU, true, false, true> : k_fused_t<R, RELU, true, false, false>)
+                   : prm->ell == 64 ? (fhi ? k_fused_t<R, RELU, false, true, true> : k_fused_t<R, RELU, false, true, false>)
+                                    : (fhi ? k_fused_t<R, RELU, false, false, true> : k_fused_t<R, RELU, false, false, false>);
+      const int rc = allow_smem((const void*)fn, kTabBytes);
+      if (rc) return rc;
+      fn<<<grid_for((const void*)fn, ngroups, TPB_T, kTabBytes), TPB_T, kTabBytes, st>>>(a, kp, k01, k02, k12, pk);
     } else if (prm->tape == BC_TAPE_COMPACT) {
       auto fn = tr ? k_fused_c<R, RELU, true, false>
                    : (prm->ell == 64 ? k_fused_c<R, RELU, false, true> : k_fused_c<R, RELU, false, false>);

@@ -73,6 +73,26 @@ int grid_for(const void* fn, uint64_t nthreads_work, int tpb, size_t smem) {
   return (int)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)cap));
 }
 
+// Opt-in to more than 48 KB of dynamic shared memory, once per (kernel, device).
+int allow_smem(const void* fn, size_t bytes) {
+  struct Entry {
+    const void* fn;
+    int dev;
+  };
+  static std::mutex mu;
+  static Entry done[256];
+  static int ndone = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  for (int i = 0; i < ndone; ++i)
+    if (done[i].fn == fn && done[i].dev == dev) return BC_OK;
+  const int rc = cuda_rc(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  if (rc) return rc;
+  if (ndone < 256) done[ndone++] = Entry{fn, dev};
+  return BC_OK;
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 bool aligned8(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7u) == 0; }
 

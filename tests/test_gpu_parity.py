@@ -46,6 +46,8 @@ PARAMS = [
     dict(ell=16, lx=7, f=0, mode="literal", rounds=20),   # paper-literal Z_{2^7}, p = 131 (compact literal tape)
     dict(ell=32, lx=5, f=3, mode="guard", rounds=20),     # p = 67, 6 slots (pair tape)
     dict(ell=12, lx=3, f=1, mode="literal", rounds=8),    # p = 11, 4 slots
+    dict(ell=64, lx=7, f=24, mode="literal", rounds=20),  # the bench's paper-literal variant (p = 131, pair tape)
+    dict(ell=64, lx=7, f=40, mode="guard", rounds=20),    # compact tape with the window in the high word (f >= 32)
 ]
 SIZES = [1, 7, 8, 9, 1000, 4099]
 

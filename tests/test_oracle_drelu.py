@@ -60,24 +60,44 @@ def _pattern_ok(useq, pos, M):
     return all(v == 0 for v in useq[last + 1:]) and all(useq[i] == one for i in range(idx[0], last + 1))
 
 
-def test_ladder_pattern_theorem_exhaustive_ell12():
-    """thm:pattern0 + lmm:pattern3-5: every in-band xi in [1, 2^lx), every mask R in
-    Z_{2^12}: the opened ladder (beyond the first lambda-1 windows) is a run of
-    +-1 followed by zeros."""
-    ell, lx = 12, 5
+def _pattern_ok_rows(u, pos, M):
+    """_pattern_ok on every row of u at once (numpy): some entry equals the run value,
+    the entries from the first to the last run value are all the run value, and every
+    entry after the last one is 0."""
+    one = 1 if pos else M - 1
+    S = u.shape[1]
+    isone = u == one
+    has = isone.any(axis=1)
+    first = np.argmax(isone, axis=1)
+    last = S - 1 - np.argmax(isone[:, ::-1], axis=1)
+    col = np.arange(S)[None, :]
+    in_run = (col >= first[:, None]) & (col <= last[:, None])
+    after = col > last[:, None]
+    return has & np.all(~in_run | isone, axis=1) & np.all(~after | (u == 0), axis=1)
+
+
+@pytest.mark.parametrize("ell,lx", [(12, 5), (16, 7)])
+def test_ladder_pattern_theorem_exhaustive_all_masks(ell, lx):
+    """thm:pattern0 + lmm:pattern3-5: every in-band xi in [1, 2^lx) of both
+    signs and EVERY mask R in Z_{2^ell} (all 2^ell sharings [x]_0 = x + R, [x]_1 = -R):
+    the opened ladder (beyond the first lambda-1 windows) is a run of +-1 followed by
+    zeros.  At ell = 16, lx = 7 that is 254 x 65,536 = 16.6 M ladders."""
     prm = B.Params(ell=ell, lx=lx, f=0, mode="guard")
     M = 1 << prm.w
     R = np.arange(1 << ell, dtype=np.uint64)
     mk = np.uint64((1 << ell) - 1)
+    x1 = (np.uint64(0) - R) & mk
+    u1 = B.ladder(prm, 1, x1)
     for xi in range(1, 1 << lx):
         lam = xi.bit_length()
         for neg in (False, True):
             x = np.uint64(((-xi) if neg else xi) % (1 << ell))
-            x0 = (x + R) & mk
-            x1 = (np.uint64(0) - R) & mk
-            u = (B.ladder(prm, 0, x0) + B.ladder(prm, 1, x1)) % np.uint64(M)
-            for row in u[:: 97]:
-                assert _pattern_ok(row[lam - 1:].tolist(), not neg, M), (xi, neg, row)
+            u = (B.ladder(prm, 0, (x + R) & mk) + u1) % np.uint64(M)
+            ok = _pattern_ok_rows(u[:, lam - 1:], not neg, M)
+            assert ok.all(), (xi, neg, u[~ok][:3])
+            # the scalar reading of the theorem agrees with the vectorised one on a sample
+            for row in u[:: 4099]:
+                assert _pattern_ok(row[lam - 1:].tolist(), not neg, M)
 
 
 def _run(prm, x, run=0):
@@ -351,3 +371,120 @@ def _pair_rejects(prm, nblocks):
         if (int(T[jj, 0]) & 0x7FFFFFFF) >= plim or any(((D >> (28 * m)) & 0xFFFFFFF) >= lim for m in range(S)):
             out.append(jj)
     return out
+
+
+def _openssl_keystream(key: bytes, label: int, nblocks: int, ctr0: int = 0) -> bytes:
+    """nblocks ChaCha20 blocks of the stream (key, label) from block counter ctr0, by the
+    `cryptography` package (OpenSSL): an implementation independent of oracle.chacha.
+    DESIGN.md sec. 4 layout: words 12-13 = 64-bit counter, 14-15 = label; OpenSSL's
+    16-byte IV is words 12-15 (counter < 2^32 here, so word 13 = 0)."""
+    algorithms = pytest.importorskip("cryptography.hazmat.primitives.ciphers.algorithms")
+    from cryptography.hazmat.primitives.ciphers import Cipher
+    iv = ctr0.to_bytes(4, "little") + bytes(4) + label.to_bytes(8, "little")
+    return Cipher(algorithms.ChaCha20(key, iv), mode=None).encryptor().update(bytes(64 * nblocks))
+
+
+def test_compact_tape_raw_keystream():
+    """The compact tape (p = 257, 8 slots) re-read from whole ChaCha20
+    blocks of OpenSSL's keystream, byte by byte, for 8,192 elements: part A = bytes
+    [16 j, 16 j + 16) of bc2.tpa1, part B = bytes [8 j, 8 j + 8) of bc2.tpb1.  For every
+    accepted element: t = bit 31 of T0; the Fisher-Yates digits k_m of (T0 mod 2^31) mod 8!
+    (m = 7..1, k_m = q mod (m+1), q //= m+1); r_m = 1 + byte m of T1 T2; rho_{3k+i} =
+    digit i (least significant first) of reshare word k in base 257.  Elements whose draws
+    reject take the fallback stream bc2.fb01 (counter 256 j): checked on the first ones."""
+    prm = B.Params()
+    n = 8192
+    ka = _openssl_keystream(SEEDS.s01, B.L_TAPEA, n * 16 // 64)
+    kb = _openssl_keystream(SEEDS.s01, B.L_TAPEB, n * 8 // 64)
+    tp = B.tape(prm, SEEDS.s01, np.arange(n, dtype=np.uint64))
+    u32 = lambda b, o: int.from_bytes(b[o:o + 4], "little")
+    accepted, rejected = 0, []
+    for j in range(n):
+        a, b = ka[16 * j: 16 * j + 16], kb[8 * j: 8 * j + 8]
+        T0 = u32(a, 0)
+        words = [u32(a, 12), u32(b, 0), u32(b, 4)]
+        assert int(tp["t"][j]) == T0 >> 31
+        if (T0 & 0x7FFFFFFF) >= 53261 * 40320 or max(words) >= 253 * 257 ** 3:
+            rejected.append(j)
+            continue
+        accepted += 1
+        q = (T0 & 0x7FFFFFFF) % 40320
+        for m in range(7, 0, -1):
+            assert int(tp["k"][j, m]) == q % (m + 1)
+            q //= m + 1
+        assert [int(v) for v in tp["r"][j]] == [1 + a[4 + m] for m in range(8)]
+        digits = [(w // 257 ** i) % 257 for w in words for i in range(3)][:8]
+        assert [int(v) for v in tp["rho"][j]] == digits
+    assert accepted >= 8000
+    # the rejected ones: replay the fallback rule from the raw fallback keystream
+    for j in rejected[:4]:
+        a, b = ka[16 * j: 16 * j + 16], kb[8 * j: 8 * j + 8]
+        fb = _openssl_keystream(SEEDS.s01, B.L_FALLBACK, 4, ctr0=256 * j)
+        fw = iter(u32(fb, 4 * i) for i in range(64))
+        idx = u32(a, 0) & 0x7FFFFFFF
+        if idx >= 53261 * 40320:
+            idx = next(fw) & 0x7FFFFFFF
+            while idx >= 53261 * 40320:
+                idx = next(fw) & 0x7FFFFFFF
+        words = [u32(a, 12), u32(b, 0), u32(b, 4)]
+        for k in range(3):
+            while words[k] >= 253 * 257 ** 3:
+                words[k] = next(fw)
+        q = idx % 40320
+        for m in range(7, 0, -1):
+            assert int(tp["k"][j, m]) == q % (m + 1)
+            q //= m + 1
+        assert [int(v) for v in tp["rho"][j]] == [(w // 257 ** i) % 257 for w in words for i in range(3)][:8]
+
+
+@pytest.mark.parametrize("S", [2, 3, 5, 8])
+def test_perm_swaps_is_literal_fisher_yates(S):
+    """Reading C9: for every index q in [0, S!) the oracle's swap partners and
+    shuffle equal a literal Fisher-Yates on a Python list (for m = S-1 .. 1: k = q mod
+    (m+1), q //= m+1, swap v[m] and v[k]); and the S! indices give S! distinct
+    permutations (Fisher-Yates with k_m uniform on [0, m] is a bijection onto S_S)."""
+    fact = math.factorial(S)
+    idx = np.arange(fact, dtype=np.uint64)
+    k = B._perm_swaps(idx, S)
+    got = B.shuffle(k, np.tile(np.arange(S, dtype=np.uint64), (fact, 1)))
+    seen = set()
+    for q0 in range(fact):
+        v, q = list(range(S)), q0
+        for m in range(S - 1, 0, -1):
+            km = q % (m + 1)
+            q //= m + 1
+            assert int(k[q0, m]) == km
+            v[m], v[km] = v[km], v[m]
+        assert got[q0].tolist() == v
+        seen.add(tuple(v))
+    assert len(seen) == fact
+    # indices past S! wrap (the tape reduces the 31-bit draw mod S! first)
+    assert np.array_equal(B._perm_swaps(idx + np.uint64(fact), S), k)
+
+
+def test_fault_one_message_byte_breaks_exactly_that_element():
+    """Sec. 5 fault injection on the oracle (Alg 7 step 9): P2's zero test reads
+    the reshared messages.  Changing one slot of P0's message of one element flips that
+    element's DReLU' -- and only that element's outputs differ from the fault-free run.
+    Element a: a slot with w_m = 0 is the only zero, W0_m += 1 removes it (1 -> 0).
+    Element b: no zero, W0_m := -W1_m mod p creates one (0 -> 1)."""
+    prm = B.Params()
+    n = 4000
+    x, x0, x1 = synth.shares(n, 64, 7, 24, "D2")
+    j = np.arange(n, dtype=np.uint64)
+    m0, m1 = B.drelu_send(prm, 0, x0, j, SEEDS.s01), B.drelu_send(prm, 1, x1, j, SEEDS.s01)
+    ref = B.drelu(prm, x0, x1, j, SEEDS)
+    w = (m0["W"] + m1["W"]) % np.uint64(prm.p)
+    nz = (w == 0).sum(axis=1)
+    a = int(np.nonzero(nz == 1)[0][0])
+    b = int(np.nonzero(nz == 0)[0][0])
+    for e, make in ((a, lambda W, m: (W[e, m] + 1) % prm.p), (b, lambda W, m: (prm.p - m1["W"][e, m]) % prm.p)):
+        m = int(np.argmax(w[e] == 0)) if e == a else 3
+        W0 = m0["W"].copy()
+        W0[e, m] = make(W0, m)
+        h = B.drelu_helper(prm, W0, m1["W"], j, SEEDS.s02)
+        y0 = B.drelu_finish(prm, 0, m0["t"], h["D0"])
+        y1 = B.drelu_finish(prm, 1, m1["t"], h["D1"])
+        bad = np.nonzero((y0 != ref["y0"]) | (y1 != ref["y1"]))[0]
+        assert bad.tolist() == [e]
+        assert int(h["z"][e]) == 1 - int(ref["z"][e])

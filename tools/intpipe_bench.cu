@@ -166,6 +166,46 @@ __global__ void k_mix_xsa_half(uint32_t* out, uint32_t seed, uint32_t k) {
   if (acc == 0x12345678u) out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
+__global__ void k_dp4a(uint32_t* out, uint32_t seed, uint32_t k) {
+  BODY(asm volatile("dp4a.u32.u32 %0, %0, %1, %2;" : "+r"(v[c]) : "r"(k), "r"(seed)))
+}
+__global__ void k_mix_lop_dp4a(uint32_t* out, uint32_t seed, uint32_t k) {
+  uint32_t v[CH], w[CH];
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) { v[c] = seed + c * 0x9E3779B9u + threadIdx.x; w[c] = v[c] ^ 0x55u; }
+  for (int i = 0; i < ITERS; ++i) {
+    _Pragma("unroll") for (int c = 0; c < CH; ++c) {
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(v[c]) : "r"(k), "r"(seed));
+      asm volatile("dp4a.u32.u32 %0, %0, %1, %2;" : "+r"(w[c]) : "r"(k), "r"(seed));
+    }
+  }
+  uint32_t acc = 0;
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) acc ^= v[c] ^ w[c];
+  if (acc == 0x12345678u) out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+__global__ void k_mix_lop_imad_dp4a(uint32_t* out, uint32_t seed, uint32_t k) {
+  // 2 LOP3 : 1 IMAD : 1 DP4A -- does DP4A share the FMA pipe with IMAD?
+  uint32_t v[CH], w[CH], x[CH];
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) { v[c] = seed + c * 0x9E3779B9u + threadIdx.x; w[c] = v[c] ^ 0x55u; x[c] = w[c] + 7u; }
+  for (int i = 0; i < ITERS; ++i) {
+    _Pragma("unroll") for (int c = 0; c < CH; ++c) {
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(v[c]) : "r"(k), "r"(seed));
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x69;" : "+r"(v[c]) : "r"(k), "r"(seed));
+      asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(w[c]) : "r"(k), "r"(seed));
+      asm volatile("dp4a.u32.u32 %0, %0, %1, %2;" : "+r"(x[c]) : "r"(k), "r"(seed));
+    }
+  }
+  uint32_t acc = 0;
+  _Pragma("unroll") for (int c = 0; c < CH; ++c) acc ^= v[c] ^ w[c] ^ x[c];
+  if (acc == 0x12345678u) out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+__global__ void k_lds(uint32_t* out, uint32_t seed, uint32_t k) {
+  // random 4-B shared loads (the table kernels' access pattern): 32 lanes, random words
+  __shared__ uint32_t tab[8192];
+  for (int i = threadIdx.x; i < 8192; i += blockDim.x) tab[i] = i * 0x9E3779B9u;
+  __syncthreads();
+  BODY(v[c] = tab[(v[c] ^ k) & 8191u])
+}
+
 template <typename K>
 double rate(K kern, int ops_per_iter, int blocks, int threads) {
   uint32_t* out;
@@ -209,6 +249,10 @@ int main() {
   // the two ChaCha-like variants in the same unit as xor_rot_add: 3 algorithmic ops per step
   printf(", \"xor_rotwide_add_tops\": %.3f", rate(k_mix_xsa_wide, 3, blocks, threads));
   printf(", \"xor_rot_add_half_wide_tops\": %.3f", rate(k_mix_xsa_half, 3, blocks, threads));
+  printf(", \"dp4a_tops\": %.3f", rate(k_dp4a, 1, blocks, threads));
+  printf(", \"lop3+dp4a_tops\": %.3f", rate(k_mix_lop_dp4a, 2, blocks, threads));
+  printf(", \"2lop3+imad+dp4a_tops\": %.3f", rate(k_mix_lop_imad_dp4a, 4, blocks, threads));
+  printf(", \"lds_random_tops\": %.3f", rate(k_lds, 1, blocks, threads));
   printf("}\n");
   return 0;
 }

@@ -18,13 +18,16 @@ KNOBS = {"BC_ADD_FMA_SEND": [0, 1]}  # knobs in csrc/: also BC_ADD_FMA, BC_MATER
 
 
 def variants():
+    if os.environ.get("VARIANT_LIST"):  # explicit list: '[{"BC_X": 1}, {}, ...]' ({} = the product library's knobs)
+        yield from json.loads(os.environ["VARIANT_LIST"])
+        return
     keys = list(KNOBS)
     for vals in itertools.product(*(KNOBS[k] for k in keys)):
         yield dict(zip(keys, vals))
 
 
 def name(v):
-    return "_".join(f"{k.replace('BC_', '').lower()}{x}" for k, x in v.items())
+    return "_".join(f"{k.replace('BC_', '').lower()}{x}" for k, x in v.items()) or "default"
 
 
 if __name__ == "__main__":
