@@ -46,6 +46,10 @@ BLOCKS_PER_ELEM = {"drelu": 0.5, "relu": 1.0,   # 3/8 (tap
 BYTES_PER_ELEM = {"drelu": 32, "relu": 32, "ladder": 16,   # algorithmic HBM bytes per element
                   "drelu_rss": 48, "relu_rss": 48, "drelu_fp": 32, "relu_fp": 32}
 SM_COUNT_B200 = 148  # nominal; the roofline uses the device's own count
+# Global element-index regions of the legs that run other inputs than the headline batch, so no
+# two protocol executions of one run (any rank) share PRG draws: the headline owns [0, W 2^24),
+# the batch sweep [2^40, + W 2^27), config 5's layer streams [2^41, ...) (BC_MAX_INDEX = 2^44).
+SWEEP_BASE, STREAM_BASE = 1 << 40, 1 << 41
 
 
 def parse():
@@ -440,7 +444,9 @@ def run_cuda(a):
             xs1 = x1.repeat((m + n - 1) // n)[:m] if m > n else x1[:m]
             ys0, ys1 = torch.empty_like(xs0), torch.empty_like(xs1)
             reps = max(5, min(200, (1 << 28) // m))
-            tv, _, _ = timed(lambda: api.drelu(xs0, xs1, prm, seeds, base, ys0, ys1, stream=stream), reps, 3)
+            # its own global index range per rank (disjoint from the headline's and the other ranks')
+            sb = SWEEP_BASE + shard.elem_base(rank, 1 << 27)
+            tv, _, _ = timed(lambda: api.drelu(xs0, xs1, prm, seeds, sb, ys0, ys1, stream=stream), reps, 3)
             sweep[f"2^{lg}"] = world * m / (tv / reps * 1e-3)
             del xs0, xs1, ys0, ys1
         sweep["2^24"] = value
@@ -501,7 +507,7 @@ def run_cuda(a):
         # ---- truncation study (NEXT #3): exact e1 counting, Alg 3 vs mult-then-trc ----
         line["trunc_study"] = trunc_leg(api, seeds, x0, x1, base, dev, stream, timed, world, n)
         # ---- config 5: E2E-shaped ReLU layer streams (CUDA graph per network) ----
-        line["config5"] = relu_streams(api, prm, seeds, dev, stream, timed, world)
+        line["config5"] = relu_streams(api, prm, seeds, dev, stream, timed, world, rank)
         # ---- e2e through the public API with pinned HOST buffers ----------------
         line["e2e"] = e2e(api, prm, seeds, x0h, x1h, base, dev, world, max_over_ranks, barrier, a)
     if rank == 0 and world == 1 and not a.no_extras:  # the CPU baseline: rank 0 at N=1 only
@@ -631,18 +637,21 @@ def trunc_leg(api, seeds, x0, x1, base, dev, stream, timed, world, n):
     return res
 
 
-def relu_streams(api, prm, seeds, dev, stream, timed, world):
+def relu_streams(api, prm, seeds, dev, stream, timed, world, rank):
     """BASELINE config 5: each network's ReLU layers at the paper's batch
     (Table 7), one fused bc_relu per layer, replayed from a CUDA graph.  Inputs
     are seeded shares generated on the device (torch RNG; input generation is
     outside the timed region and holds none of the method's arithmetic)."""
     import torch
+    from paper_2309_04909_b200 import shard
     from paper_2309_04909_b200 import stream as S
     out = {}
     g = torch.Generator(device=dev)
     g.manual_seed(5)
     for name in S.NETWORKS:
-        st = S.ReluStream(S.layer_sizes(name), prm, seeds, dev)
+        sizes = S.layer_sizes(name)
+        # rank r's forward owns its own global index range (fresh randomness on every rank)
+        st = S.ReluStream(sizes, prm, seeds, dev, base=STREAM_BASE + shard.elem_base(rank, S.index_span(sizes)))
         for x0, x1 in zip(st.x0, st.x1):
             x = (torch.randn(x0.numel(), device=dev, generator=g) * 2 ** 26).round().to(torch.int64)
             r = torch.randint(-2 ** 63, 2 ** 63 - 1, (x0.numel(),), device=dev, generator=g, dtype=torch.int64)
@@ -744,12 +753,13 @@ def run_party(a):
         if a.transport == "peer":
             from paper_2309_04909_b200 import peer
             runner = peer.PeerPartyRunner("relu", prm, seeds, n, chunk=a.chunk, backend=peer.CudaIpcBackend(dev),
-                                          group=gloo_triples[role.triple])
+                                          group=gloo_triples[role.triple], triples=k)
             step = lambda: runner.run(xs)  # noqa: E731
             # egress per step: P0/P1 message + [d]_b; P2 e to both + [c]_1 (the kernels' peer stores)
             wire = {0: 9 + 8, 1: 9 + 8, 2: 8 + 8 + 8}[role.party] * n
         else:
-            runner = party.PartyRunner(prm, seeds, n, chunk=a.chunk, compute=party.CudaCompute(dev), group=group)
+            runner = party.PartyRunner(prm, seeds, n, chunk=a.chunk, compute=party.CudaCompute(dev), group=group,
+                                       triples=k)
             step = lambda: runner.relu(xs)  # noqa: E731
         for _ in range(max(a.warmup, 2)):
             step()

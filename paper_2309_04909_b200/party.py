@@ -119,7 +119,7 @@ class PartyRunner:
     """Runs DReLU / ReLU for this rank's role over a batch of n elements."""
 
     def __init__(self, prm: api.Params, seeds, n: int, chunk: int = 1 << 22, compute=None,
-                 group=None, paper_literal: bool = False, base: int | None = None):
+                 group=None, paper_literal: bool = False, base: int | None = None, triples: int = 1):
         self.rank = dist.get_rank()
         self.role = Role.of(self.rank)
         self.prm = prm
@@ -128,7 +128,11 @@ class PartyRunner:
         self.c = compute
         self.group = group
         self.paper_literal = paper_literal
-        self.base = self.role.triple * n if base is None else base
+        # run r draws from [base0 + r * triples * n, + n): fresh randomness per run (as peer.PeerPartyRunner)
+        self.base0 = self.role.triple * n if base is None else base
+        self.stride = triples * n
+        self.runs = 0
+        self.base = self.base0
         self.fmt = api.wire_format(prm)  # byte planes (p <= 257) or uint32 planes (large tape)
         self.hi_needed = self.fmt["hi"] is not None
         # seeds this party holds: P0 {01, 02}, P1 {01, 12}, P2 {02, 12}
@@ -166,8 +170,14 @@ class PartyRunner:
             w.wait()
 
     # -- DReLU (Alg 7) -----------------------------------------------------------------
-    def drelu(self, x=None):
-        """P0/P1: x is this party's share vector; returns its DReLU share.  P2: x=None, returns None."""
+    def _next_run(self, elem_base):
+        self.base = self.base0 + self.runs * self.stride if elem_base is None else elem_base
+        self.runs += 1
+
+    def drelu(self, x=None, elem_base: int | None = None):
+        """P0/P1: x is this party's share vector; returns its DReLU share.  P2: x=None, returns None.
+        Run r uses the global indices base0 + r * stride + [0, n) unless elem_base is given."""
+        self._next_run(elem_base)
         p, c = self.role.party, self.c
         out = c.empty(self.n, torch.int64) if p < 2 else None
         pending = []  # (chunk, state, works) whose round-2 messages are outstanding
@@ -207,7 +217,8 @@ class PartyRunner:
         self.c.drelu_finish(self.role.party, tb, resp, self.prm, b - a, seed02, self.base + a, out=out[a:b])  # step 11
 
     # -- ReLU (Alg 8) ------------------------------------------------------------------
-    def relu(self, x=None, with_c1: bool = True):
+    def relu(self, x=None, with_c1: bool = True, elem_base: int | None = None):
+        self._next_run(elem_base)
         p, c = self.role.party, self.c
         out = c.empty(self.n, torch.int64) if p < 2 else None
         pending = []

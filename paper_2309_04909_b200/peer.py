@@ -170,7 +170,8 @@ class PeerPartyRunner:
     the api signatures (default: the api module itself, i.e. libbicoptor)."""
 
     def __init__(self, kind, prm: api.Params, seeds, n: int, chunk: int = 1 << 22, slots: int = 2,
-                 backend=None, compute=None, group=None, paper_literal: bool = False, base: int | None = None):
+                 backend=None, compute=None, group=None, paper_literal: bool = False, base: int | None = None,
+                 triples: int = 1):
         assert kind in ("drelu", "relu")
         assert slots >= 2, "two slots per link at least (with one the d exchange of ReLU deadlocks)"
         self.kind, self.prm, self.n = kind, prm, n
@@ -182,7 +183,14 @@ class PeerPartyRunner:
         self.c = compute if compute is not None else api
         self.g = group
         self.literal = paper_literal and kind == "drelu"
-        self.base = self.role.triple * n if base is None else base
+        # PRG index range of run r: [base0 + r * stride, + n).  Every run draws fresh t, Pi, r_m,
+        # rho_m and triples: reusing them on new inputs would open
+        # x - x' to P0/P1 (d = x - a) and hand P2 several messages under one mask.  stride =
+        # triples * n keeps the triples sharing the index space disjoint across runs too.
+        self.base0 = self.role.triple * n if base is None else base
+        self.stride = triples * n
+        self.runs = 0
+        self.base = self.base0
         fmt = api.wire_format(prm)  # byte planes (p <= 257) or slot-major uint32 planes (large tape)
         self.fmt = fmt
         self.hi_needed = fmt["hi"] is not None
@@ -329,11 +337,15 @@ class PeerPartyRunner:
         from2.release(seq, be, g, self._works)
 
     # ---- public ------------------------------------------------------------------------
-    def run(self, x=None, out=None):
+    def run(self, x=None, out=None, elem_base: int | None = None):
         """P0/P1: x is this party's share vector (n,), returns its output share.
         P2: x=None, returns None.  Asynchronous on the current stream like the
-        kernels themselves: synchronise before reading the result on the host."""
+        kernels themselves: synchronise before reading the result on the host.
+        Run r uses the global element indices base0 + r * stride + [0, n) unless
+        elem_base is given (all three parties must pass the same value)."""
         p = self.role.party
+        self.base = self.base0 + self.runs * self.stride if elem_base is None else elem_base
+        self.runs += 1
         if p < 2 and out is None:
             out = self.be.alloc((self.n,), I64)
         if self.kind == "drelu":

@@ -26,6 +26,11 @@ NETWORKS = {
 }
 
 
+def index_span(sizes) -> int:
+    """Global element indices one forward over `sizes` occupies (layers padded to 8)."""
+    return sum(-(-n // 8) * 8 for n in sizes)
+
+
 def layer_sizes(name: str, batch: int | None = None):
     b, per_img = NETWORKS[name]
     b = b if batch is None else batch
@@ -39,16 +44,31 @@ class ReluStream:
         self.sizes = list(sizes)
         self.prm, self.seeds = prm, seeds
         self.dev = torch.device(device)
-        self.bases = []
-        b = base
-        for n in self.sizes:
-            self.bases.append(b)
-            b += -(-n // 8) * 8  # layer offsets stay multiples of 8 (elem_base rule)
+        self._set_bases(base)
         self.x0 = [torch.empty(n, dtype=torch.int64, device=self.dev) for n in self.sizes]
         self.x1 = [torch.empty(n, dtype=torch.int64, device=self.dev) for n in self.sizes]
         self.y0 = [torch.empty(n, dtype=torch.int64, device=self.dev) for n in self.sizes]
         self.y1 = [torch.empty(n, dtype=torch.int64, device=self.dev) for n in self.sizes]
         self.graph = None
+
+    def _set_bases(self, base: int):
+        self.base = base
+        self.bases = []
+        b = base
+        for n in self.sizes:
+            self.bases.append(b)
+            b += -(-n // 8) * 8  # layer offsets stay multiples of 8 (elem_base rule)
+
+    def advance(self, base: int | None = None):
+        """Move the forward to a fresh global index range (default: the next one) and re-capture.
+        replay() re-executes the captured protocol instance -- the same t, Pi, r_m, rho_m and
+        triples -- which is only sound on the SAME inputs (a timing loop).  Before running on
+        new inputs, call advance(): reusing the draws on new shares would open x - x' to P0/P1
+        (d = x - a, Alg 8) and give P2 two messages under one mask (Alg 7 steps 7-8)."""
+        self._set_bases(self.base + index_span(self.sizes) if base is None else base)
+        if self.graph is not None:
+            self.capture()
+        return self
 
     @property
     def total(self) -> int:

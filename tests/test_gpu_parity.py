@@ -262,6 +262,52 @@ def test_config3_full_size_sampled(api, fn):
         assert np.array_equal(y[valid], relu_plain(x, 64, 7, 24)[valid])
 
 
+@pytest.mark.parametrize("fn", ["drelu", "relu"])
+@pytest.mark.parametrize("kw", [PARAMS[0], PARAMS[7]], ids=_ids)
+def test_config3_full_size_exact(api, fn, kw):
+    """Config 3 at its full 2^24 elements, in the exact launch the bench times
+    (bc_drelu / bc_relu, no transcript, elem_base 0, D2 inputs, seeds run 0):
+    EVERY output share against the scalar C oracle (oracle/c, OpenMP over the
+    host cores; itself bit-exact with the numpy oracle, test_oracle_cref.py).
+    Alg 7, Alg 8 P:1851-1864.  Guard mode (the headline) and the
+    bench's paper-literal variant (p = 131)."""
+    from oracle import cref
+    n = 1 << 24
+    x, x0, x1 = synth.shares(n, 64, 7, 24, "D2")
+    y0, y1 = getattr(api, fn)(dev(x0), dev(x1), api.Params(**kw), SEEDS)
+    g0, g1 = host(y0), host(y1)
+    del y0, y1
+    ref = cref.fused(B.Params(**kw), x0, x1, 0, SEEDS, relu=(fn == "relu"))
+    bad = np.flatnonzero((g0 != ref["y0"]) | (g1 != ref["y1"]))
+    assert bad.size == 0, f"{bad.size} of {n} elements differ, first at {bad[:8]}"
+
+
+def test_config2_ladder_full_size_exact(api):
+    """Config 2 (Alg 7 steps 3-5 alone, ell=64, f=24, guard, 2^28 elements, one
+    call as the bench times it): every one of the 2^28 x 8 output bytes of both
+    parties against the C oracle's v' (byte = v' - 1), compared chunk by chunk;
+    plus a seeded 2^14 sample against the numpy oracle.  Alg 5, Alg 6
+    P:806-816."""
+    from oracle import cref
+    n = 1 << 28
+    kw = PARAMS[0]
+    rng = np.random.default_rng(6)
+    x = rng.integers(0, 2**64 - 1, size=n, dtype=np.uint64, endpoint=True)
+    t = dev(x)
+    oprm = B.Params(**kw)
+    idx = np.sort(rng.choice(n, 1 << 14, replace=False))
+    chunk = 1 << 24
+    for party in (0, 1):
+        out = api.ladder_modswitch(party, t, api.Params(**kw))
+        samp = out[torch.from_numpy(idx).to(DEV)].cpu().numpy()
+        assert np.array_equal(samp, B.ladder_modswitch_bytes(oprm, party, x[idx]))
+        for c in range(0, n, chunk):
+            got = out[c:c + chunk].cpu().numpy()
+            want = cref.ladder_modswitch(oprm, party, x[c:c + chunk]) - np.uint64(1)
+            assert np.array_equal(got, want.astype(np.uint8)), f"party {party} chunk {c >> 24}"
+        del out
+
+
 def test_config2_ladder_full_size_sampled(api):
     """Config 2 (trc + modswitch alone, ell=64, 2^28 elements): sampled parity."""
     n = 1 << 28
@@ -394,6 +440,17 @@ def test_relu_stream_graph_matches_eager_and_oracle(api):
     for i, n in enumerate(st.sizes):
         assert torch.equal(st.y0[i], eager[i][0]) and torch.equal(st.y1[i], eager[i][1])
         idx = np.sort(rng.choice(n, min(n, 512), replace=False))
+        x, x0, x1 = xs[i]
+        ref = B.relu(oprm, x0[idx], x1[idx], idx.astype(np.uint64) + np.uint64(st.bases[i]), SEEDS)
+        assert np.array_equal(host(st.y0[i])[idx], ref["y0"]) and np.array_equal(host(st.y1[i])[idx], ref["y1"])
+    # advance(): the next forward re-captured at the next global index range (fresh draws)
+    b0 = st.bases[0]
+    st.advance()
+    assert st.bases[0] == b0 + S.index_span(st.sizes)
+    st.replay()
+    torch.cuda.synchronize()
+    for i, n in enumerate(st.sizes):
+        idx = np.sort(rng.choice(n, min(n, 256), replace=False))
         x, x0, x1 = xs[i]
         ref = B.relu(oprm, x0[idx], x1[idx], idx.astype(np.uint64) + np.uint64(st.bases[i]), SEEDS)
         assert np.array_equal(host(st.y0[i])[idx], ref["y0"]) and np.array_equal(host(st.y1[i])[idx], ref["y1"])

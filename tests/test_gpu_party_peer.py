@@ -62,8 +62,9 @@ def _work(rank, world, port, kind, n, chunk, slots, literal, runs, outdir, kw=No
         # the fused one-GPU kernel on the same shares (bit-exact with the oracle: test_gpu_parity.py)
         t0 = torch.from_numpy(x0.view(np.int64)).cuda()
         t1 = torch.from_numpy(x1.view(np.int64)).cuda()
-        ref = getattr(api, kind)(t0, t1, prm, synth.seeds(0), role.triple * n)[role.party]
-        np.save(os.path.join(outdir, f"fused_{rank}.npy"), ref.cpu().numpy().view(np.uint64))
+        for r in range(runs):  # run r draws from global indices r n + [0, n) (one triple)
+            ref = getattr(api, kind)(t0, t1, prm, synth.seeds(0), role.triple * n + r * n)[role.party]
+            np.save(os.path.join(outdir, f"fused_{rank}_{r}.npy"), ref.cpu().numpy().view(np.uint64))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -76,9 +77,9 @@ def _run(tmp_path, kind, n, chunk, slots, literal, runs, kw=None):
         errs = "".join(f"--- rank {r}\n" + open(tmp_path / f"err_{r}.txt").read()
                        for r in range(3) if (tmp_path / f"err_{r}.txt").exists())
         raise AssertionError(errs or "worker failed")
-    for rank in (0, 1):  # every run equals the fused kernel's share
-        ref = np.load(tmp_path / f"fused_{rank}.npy")
+    for rank in (0, 1):  # every run equals the fused kernel's share at that run's indices
         for r in range(runs):
+            ref = np.load(tmp_path / f"fused_{rank}_{r}.npy")
             assert np.array_equal(np.load(tmp_path / f"y_{rank}_{r}.npy"), ref), (kind, rank, r)
 
 
@@ -92,8 +93,8 @@ def test_party_peer_three_processes_vs_oracle(tmp_path, kind, slots, literal):
     _run(tmp_path, kind, n, chunk, slots, literal, runs=2)
     o = B.Params(ell=64, lx=7, f=24, mode="guard", rounds=20)
     x, x0, x1 = synth.shares(n, 64, 7, 24, "D1", run=0)
-    ref = getattr(B, kind)(o, x0, x1, np.arange(n, dtype=np.uint64), synth.seeds(0))
     for r in range(2):
+        ref = getattr(B, kind)(o, x0, x1, np.arange(n, dtype=np.uint64) + np.uint64(r * n), synth.seeds(0))
         assert np.array_equal(np.load(tmp_path / f"y_0_{r}.npy"), ref["y0"])
         assert np.array_equal(np.load(tmp_path / f"y_1_{r}.npy"), ref["y1"])
 
