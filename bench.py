@@ -58,7 +58,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
-    ap.add_argument("--n", type=int, default=N_PER_GPU)
+    ap.add_argument("--elems", "--n", dest="n", type=int, default=N_PER_GPU,
+                    help="elements per GPU (--elems under torchrun: its parser takes --n as an abbreviation)")
     ap.add_argument("--rounds", type=int, default=ROUNDS)
     ap.add_argument("--no-extras", action="store_true", help="skip ReLU / ladder / variants / e2e / cpu legs")
     ap.add_argument("--only", choices=["drelu", "relu", "ladder", "drelu_rss", "relu_rss", "drelu_fp", "relu_fp",
@@ -70,6 +71,9 @@ def parse():
                     help="party: config 4, P0/P1/P2 on distinct GPUs (needs >= 3 ranks), ReLU over NCCL P2P")
     ap.add_argument("--party-n", type=int, default=1 << 26, help="elements per P0/P1/P2 triple (config 4)")
     ap.add_argument("--chunk", type=int, default=1 << 22, help="party mode: elements per pipelined chunk")
+    ap.add_argument("--domain", default=MODE, choices=["guard", "literal"],
+                    help="party mode: guard (w = lx+1, p = 257, 72-bit messages) or the paper-literal Z_{2^lx} "
+                         "(p = 131, 64-bit messages; reading C6)")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
                     help="party mode: NCCL P2P (party.PartyRunner) or peer memory (peer.PeerPartyRunner: the "
                          "phase kernels store each message into the receiver's HBM over NVLink, CUDA IPC)")
@@ -740,9 +744,9 @@ def run_party(a):
     gloo_triples = [dist.new_group([3 * t, 3 * t + 1, 3 * t + 2], backend="gloo") for t in range(k)] \
         if a.transport == "peer" else None
     n = a.party_n
-    prm = api.Params(ell=ELL, lx=LX, f=F, mode=MODE, rounds=a.rounds)
+    prm = api.Params(ell=ELL, lx=LX, f=F, mode=a.domain, rounds=a.rounds)
     seeds = synth.seeds(0)
-    t_ms, bytes_sent = 0.0, 0
+    t_ms, bytes_sent, msg_bits = 0.0, 0, 0
     if rank < 3 * k:
         role = party.Role.of(rank)
         xs = None
@@ -755,8 +759,12 @@ def run_party(a):
             runner = peer.PeerPartyRunner("relu", prm, seeds, n, chunk=a.chunk, backend=peer.CudaIpcBackend(dev),
                                           group=gloo_triples[role.triple], triples=k)
             step = lambda: runner.run(xs)  # noqa: E731
-            # egress per step: P0/P1 message + [d]_b; P2 e to both + [c]_1 (the kernels' peer stores)
-            wire = {0: 9 + 8, 1: 9 + 8, 2: 8 + 8 + 8}[role.party] * n
+            # egress per step: every link this rank's kernels store into (P0/P1: message + [d]_b; P2: e to
+            # both + [c]_1), from the inbox field shapes
+            eg = runner.egress_bytes_per_elem()
+            wire = sum(eg.values()) * n
+            if role.party < 2:  # the one-pass message to P2 (Alg 7 step 8), in bits per element
+                msg_bits = 8 * eg["linkA->P2" if role.party == 0 else "linkB->P2"]
         else:
             runner = party.PartyRunner(prm, seeds, n, chunk=a.chunk, compute=party.CudaCompute(dev), group=group,
                                        triples=k)
@@ -777,13 +785,16 @@ def run_party(a):
         dist.barrier(group=group)
         t_ms = e0.elapsed_time(e1) / steps
         bytes_sent = runner.bytes_sent / steps if a.transport == "nccl" else wire
+        if a.transport == "nccl" and role.party < 2:
+            fmt = api.wire_format(prm)
+            msg_bits = 8 * (8 + (1 if fmt["hi"] is not None else 0))
         if a.transport == "peer":
             runner.close()
     rdev = "cpu" if share else dev
-    t = torch.tensor([t_ms, bytes_sent], dtype=torch.float64, device=rdev)
+    t = torch.tensor([t_ms, bytes_sent, msg_bits], dtype=torch.float64, device=rdev)
     tm = t.clone()
     dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-    per_rank = [torch.zeros(2, dtype=torch.float64, device=rdev) for _ in range(world)]
+    per_rank = [torch.zeros(3, dtype=torch.float64, device=rdev) for _ in range(world)]
     dist.all_gather(per_rank, t)
     if rank == 0:
         ms = float(tm[0])
@@ -793,9 +804,10 @@ def run_party(a):
                       f"{'NCCL P2P' if a.transport == 'nccl' else 'peer-memory stores from the phase kernels'})",
             "mode": "party", "transport": a.transport, "value": k * n / (ms * 1e-3), "unit": "elements/s", "n_gpus": world, "triples": k,
             "ms_per_step": ms, "steps": steps, "chunk": a.chunk, "higher_is_better": True, "dtype": "u64",
-            "config": {"workload": f"config4: ReLU ell={ELL} lx={LX} f={F} {MODE} ChaCha{a.rounds}, 2^{int(math.log2(n))} elements per triple"},
+            "config": {"workload": f"config4: ReLU ell={ELL} lx={LX} f={F} {a.domain} ChaCha{a.rounds}, 2^{int(math.log2(n))} elements per triple"},
             "wire_bytes_per_elem": egress,
-            "paper_one_pass_bits": 64, "guard_one_pass_bits": 72,
+            "one_pass_bits_per_party": {"P0->P2": float(per_rank[0][2]), "P1->P2": float(per_rank[1][2])},
+            "paper_one_pass_bits": (LX + 1) * (LX + 1), "guard_one_pass_bits": (LX + 1) * 9,
             "p2_egress_GBs": float(per_rank[2][1]) / (ms * 1e-3) / 1e9}))
     dist.destroy_process_group()
 

@@ -126,6 +126,23 @@ int bc_modswitch(int party, const uint64_t *in, uint32_t *out, size_t n, int lp,
 int bc_ladder_modswitch(int party, const uint64_t *x, uint8_t *v, size_t n,
                         const bc_params *prm, void *stream);
 
+/* Alg 6 at any width, for the full-precision guard domain (lp = 32,
+ * p = 2^32 + 15) and beyond: shares in Z_{2^lp} -> shares in Z_p, as
+ * bc_modswitch.  Requires 1 <= lp <= 63 and 2^lp < p (p < 2^64; p need not be
+ * checked prime).  in: uint64_t[n] (low lp bits used), out: uint64_t[n]; both
+ * 16-B aligned, caller-owned, not overlapping.  Both results already lie in
+ * [0, p): P0's share is in (0, 2^lp], P1's in [p - 2^lp, p). */
+int bc_modswitch64(int party, const uint64_t *in, uint64_t *out, size_t n, int lp, uint64_t p,
+                   void *stream);
+
+/* Alg 7 steps 3-5 for one party, every tape including the large one (lx up to
+ * 31, p < 2^33; Alg 5, Alg 6): as
+ * bc_ladder_modswitch, but the output is the v'_m themselves, uint64_t[n][slots]
+ * (row-major, slot m of element i at v[i * slots + m]), each in [1, p).  x and v
+ * 16-B aligned, caller-owned, not overlapping. */
+int bc_ladder_modswitch64(int party, const uint64_t *x, uint64_t *v, size_t n,
+                          const bc_params *prm, void *stream);
+
 /* Alg 7, all three parties simulated on one GPU in one fused
  * kernel: y0 + y1 = DReLU(x0 + x1) mod 2^ell (1 for positive, 0 for negative
  * in-band x; x = 0 gives the random bit t, reading C13).  tr may be NULL. */

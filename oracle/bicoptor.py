@@ -4,9 +4,11 @@ Follows Alg 7 and Alg 8 step by step, per party,
 vectorised over the element batch with numpy (elements are independent,
 P:996).  Every random value is drawn from the pre-shared seeds with
 the ChaCha keystream of ``oracle.chacha``; the byte layout of those draws is
-the spec's own -- the paper fixes none, so the exact
-share values are "parity unpinned" beyond the RFC 8439 vector, while every
-reconstructed output is pinned against plaintext sign / ReLU by the tests.
+the spec's own -- the paper fixes none (readings
+C9-C11).  The tapes are pinned by re-reading their draws from an independent
+keystream (OpenSSL's ChaCha20 via ``cryptography``) for the compact, pair and
+large layouts, the permutation by a literal Fisher-Yates over all S! indices,
+and every reconstructed output against plaintext sign / ReLU.
 
 Notation: ell ring bits; lx key-bit width (ell_x); f window
 offset of the key bits (sec. 6.1, reading C5); w = lx+1 ("guard", default,
@@ -122,7 +124,8 @@ def tape(prm: Params, seed01: bytes, j) -> dict:
     Fisher-Yates swaps (reading C9).  Step 7: masks r_m in Z_p^*.
     Step 8: reshare values rho_m in Z_p (reading C11).  Exact
     rejection sampling with a deterministic fallback stream (reading C10).
-    Parity unpinned beyond the ChaCha vector (the layout is the spec's).
+    The layout is the spec's; its draws are pinned by re-reads from an
+    independent keystream (tests/test_oracle_drelu.py, test_oracle_fullprec.py).
     """
     j = np.atleast_1d(np.asarray(j, dtype=np.uint64))
     if prm.layout == "compact":

@@ -59,6 +59,8 @@ _SIG = {
     "bc_trc_prob": (ctypes.c_int, [ctypes.c_int, _P, _P, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, _P]),
     "bc_modswitch": (ctypes.c_int, [ctypes.c_int, _P, _P, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint32, _P]),
     "bc_ladder_modswitch": (ctypes.c_int, [ctypes.c_int, _P, _P, ctypes.c_size_t, ctypes.POINTER(bc_params), _P]),
+    "bc_modswitch64": (ctypes.c_int, [ctypes.c_int, _P, _P, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint64, _P]),
+    "bc_ladder_modswitch64": (ctypes.c_int, [ctypes.c_int, _P, _P, ctypes.c_size_t, ctypes.POINTER(bc_params), _P]),
     "bc_drelu": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64, ctypes.POINTER(bc_params),
                                 ctypes.POINTER(bc_seeds), ctypes.POINTER(bc_transcript), _P]),
     "bc_relu": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_size_t, ctypes.c_uint64, ctypes.POINTER(bc_params),
@@ -176,6 +178,23 @@ def _opt(t, name, itemsize=8):
     return None if t is None else _dev(t, name, itemsize)
 
 
+def _need(t, name: str, nbytes: int) -> None:
+    """The C ABI takes raw pointers and cannot see buffer sizes: refuse a caller buffer
+    smaller than the call will read or write (None = not passed)."""
+    if t is not None and t.numel() * t.element_size() < nbytes:
+        raise BicoptorError(f"{name} holds {t.numel() * t.element_size()} B, the call needs {nbytes} B")
+
+
+def _need_msg(lo, hi, n: int, prm: "Params", what: str) -> None:
+    """Message planes of n elements in the wire format of prm (wire_format)."""
+    fmt = wire_format(prm)
+    (los, lot), hf = fmt["lo"], fmt["hi"]
+    isz = torch.empty((), dtype=lot).element_size()
+    _need(lo, f"{what} lo", n * los[0] * isz)
+    if hf is not None:
+        _need(hi, f"{what} hi", n * torch.empty((), dtype=hf[1]).element_size())
+
+
 def _stream(stream) -> int | None:
     if stream is None:
         return torch.cuda.current_stream().cuda_stream
@@ -224,6 +243,7 @@ def trc_prob(party: int, x: torch.Tensor, ell: int, k: int, out=None, stream=Non
 def modswitch(party: int, x: torch.Tensor, lp: int, p: int, out=None, stream=None) -> torch.Tensor:
     """Alg 6 modulo switch Z_{2^lp} -> Z_p of one party's share (uint32 out, in int32 storage)."""
     out = torch.empty(x.numel(), dtype=torch.int32, device=x.device) if out is None else out
+    _need(out, "out", 4 * x.numel())
     _check(lib().bc_modswitch(party, _dev(x, "x"), _dev(out, "out", 4), x.numel(), lp, p, _stream(stream)),
            "bc_modswitch")
     return out
@@ -233,8 +253,30 @@ def modswitch(party: int, x: torch.Tensor, lp: int, p: int, out=None, stream=Non
 def ladder_modswitch(party: int, x: torch.Tensor, prm: Params, out=None, stream=None) -> torch.Tensor:
     """Alg 7 steps 3-5 on one party's share: (n, 8) uint8, byte m = v'_m - 1."""
     out = torch.empty((x.numel(), 8), dtype=torch.uint8, device=x.device) if out is None else out
+    _need(out, "out", 8 * x.numel())
     _check(lib().bc_ladder_modswitch(party, _dev(x, "x"), _dev(out, "out", 1), x.numel(), ctypes.byref(prm.c()),
                                      _stream(stream)), "bc_ladder_modswitch")
+    return out
+
+
+@_on_input_device
+def modswitch64(party: int, x: torch.Tensor, lp: int, p: int, out=None, stream=None) -> torch.Tensor:
+    """Alg 6 at any width 1 <= lp <= 63, 2^lp < p < 2^64 (uint64 out, in int64 storage)."""
+    out = torch.empty_like(x) if out is None else out
+    _need(out, "out", 8 * x.numel())
+    _check(lib().bc_modswitch64(party, _dev(x, "x"), _dev(out, "out"), x.numel(), lp, p, _stream(stream)),
+           "bc_modswitch64")
+    return out
+
+
+@_on_input_device
+def ladder_modswitch64(party: int, x: torch.Tensor, prm: Params, out=None, stream=None) -> torch.Tensor:
+    """Alg 7 steps 3-5 on one party's share, any tape: (n, slots) uint64 (int64 storage), the v'_m."""
+    S = prm.lx + 1
+    out = torch.empty((x.numel(), S), dtype=torch.int64, device=x.device) if out is None else out
+    _need(out, "out", 8 * S * x.numel())
+    _check(lib().bc_ladder_modswitch64(party, _dev(x, "x"), _dev(out, "out"), x.numel(), ctypes.byref(prm.c()),
+                                       _stream(stream)), "bc_ladder_modswitch64")
     return out
 
 
@@ -246,8 +288,14 @@ def _fused(fn, what, x0, x1, prm, seeds, elem_base, y0, y1, transcript, stream):
         raise BicoptorError("x0 and x1 differ in length")
     y0 = torch.empty_like(x0) if y0 is None else y0
     y1 = torch.empty_like(x1) if y1 is None else y1
+    _need(y0, "y0", 8 * n)
+    _need(y1, "y1", 8 * n)
     tr = None
     if transcript is not None:
+        S = prm.lx + 1
+        for k in ("w0", "w1"):  # large tape / Bicoptor-1: (n, S) u64 planes; otherwise lo (n, 8) + hi (n,) bytes
+            _need(transcript.get(k + "_lo"), k + "_lo", n * (8 * S if prm.lx >= 8 or what == "bc_drelu_b1" else 8))
+            _need(transcript.get(k + "_hi"), k + "_hi", n)
         tr = bc_transcript(*(_opt(transcript.get(k), k, None) for k in ("w0_lo", "w0_hi", "w1_lo", "w1_hi")))
     cp, cs = prm.c(), seeds_struct(seeds)
     _check(fn(_dev(x0, "x0"), _dev(x1, "x1"), _dev(y0, "y0"), _dev(y1, "y1"), n, elem_base, ctypes.byref(cp),
@@ -369,6 +417,9 @@ def drelu_send(party, x, prm: Params, seed01: bytes, elem_base=0, out=None, stre
     bc_drelu_send_p0, P0's output share computed in the same kernel (reading C12)."""
     n = x.numel()
     lo, hi, tb = msg_buffers(n, x.device, prm) if out is None else out
+    _need_msg(lo, hi, n, prm, "drelu_send")
+    _need(tb, "tbits", (n + 7) // 8)
+    _need(y, "y", 8 * n)
     if y is None:
         _check(lib().bc_drelu_send(party, _dev(x, "x"), _dev(lo, "lo", None), _opt(hi, "hi", None),
                                    _dev(tb, "tbits", 1), n, elem_base, ctypes.byref(prm.c()), seed01,
@@ -392,6 +443,10 @@ def drelu_helper(lo0, hi0, lo1, hi1, prm: Params, seed02: bytes, elem_base=0, pa
         r1 = torch.empty(n, dtype=torch.int64, device=lo0.device)
     else:
         r0, r1 = out
+    _need_msg(lo0, hi0, n, prm, "drelu_helper P0")
+    _need_msg(lo1, hi1, n, prm, "drelu_helper P1")
+    _need(r0, "resp0", 8 * n)
+    _need(r1, "resp1", 8 * n)
     _check(lib().bc_drelu_helper(_dev(lo0, "lo0", None), _opt(hi0, "hi0", None), _dev(lo1, "lo1", None),
                                  _opt(hi1, "hi1", None),
                                  _opt(r0, "resp0"), _dev(r1, "resp1"), n, elem_base, ctypes.byref(prm.c()), seed02,
@@ -404,6 +459,9 @@ def drelu_finish(party, tbits, resp, prm: Params, n: int, seed02: bytes | None =
                  stream=None):
     """Alg 7 step 11 for P0/P1 (P0 may pass resp=None and seed02)."""
     y = torch.empty(n, dtype=torch.int64, device=tbits.device) if out is None else out
+    _need(tbits, "tbits", (n + 7) // 8)
+    _need(resp, "resp", 8 * n)
+    _need(y, "y", 8 * n)
     _check(lib().bc_drelu_finish(party, _dev(tbits, "tbits", 1), _opt(resp, "resp"), _dev(y, "y"), n, elem_base,
                                  ctypes.byref(prm.c()), seed02, _stream(stream)), "bc_drelu_finish")
     return y
@@ -420,6 +478,10 @@ def relu_send(party, x, prm: Params, seed01: bytes, seed_tr: bytes, elem_base=0,
         d = torch.empty_like(x)
     else:
         lo, hi, tb, d = out
+    _need_msg(lo, hi, n, prm, "relu_send")
+    _need(tb, "tbits", (n + 7) // 8)
+    _need(d, "dshare", 8 * n)
+    _need(d_peer, "d_peer", 8 * n)
     if d_peer is None:
         _check(lib().bc_relu_send(party, _dev(x, "x"), _dev(lo, "lo", None), _opt(hi, "hi", None),
                                   _dev(tb, "tbits", 1),
@@ -443,6 +505,10 @@ def relu_helper(lo0, hi0, lo1, hi1, prm: Params, seed02: bytes, seed12: bytes, e
         c1 = torch.empty(n, dtype=torch.int64, device=lo0.device) if with_c1 else None
     else:
         e, c1 = out
+    _need_msg(lo0, hi0, n, prm, "relu_helper P0")
+    _need_msg(lo1, hi1, n, prm, "relu_helper P1")
+    for t, name in ((e, "e"), (c1, "c1"), (e_dup, "e_dup")):
+        _need(t, name, 8 * n)
     if e_dup is None:
         _check(lib().bc_relu_helper(_dev(lo0, "lo0", None), _opt(hi0, "hi0", None), _dev(lo1, "lo1", None),
                                     _opt(hi1, "hi1", None), _dev(e, "e"), _opt(c1, "c1"), n, elem_base,
@@ -461,6 +527,9 @@ def relu_finish(party, x, tbits, d_own, d_peer, e, c1, prm: Params, seed_tr: byt
     """Alg 8 steps 4-5 for P0/P1."""
     n = x.numel()
     y = torch.empty_like(x) if out is None else out
+    _need(tbits, "tbits", (n + 7) // 8)
+    for t, name in ((d_own, "d_own"), (d_peer, "d_peer"), (e, "e"), (c1, "c1"), (y, "y")):
+        _need(t, name, 8 * n)
     _check(lib().bc_relu_finish(party, _dev(x, "x"), _dev(tbits, "tbits", 1), _dev(d_own, "d_own"),
                                 _dev(d_peer, "d_peer"), _dev(e, "e"), _opt(c1, "c1"), _dev(y, "y"), n, elem_base,
                                 ctypes.byref(prm.c()), seed_tr, _stream(stream)), "bc_relu_finish")

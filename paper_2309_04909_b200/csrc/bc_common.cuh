@@ -2,7 +2,8 @@
 //
 // Thread <-> data mapping: one thread owns a group of 8
 // consecutive elements.  That is the natural unit of the PRG: the compact
-// seed01 tape is 32 B per element (4 ChaCha blocks per group) and every 8-B
+// seed01 tape is 24 B per element (3 ChaCha blocks per group: two of part A,
+// one of part B), the pair tape 32 B (4 blocks per group), and every 8-B
 // per-element stream of seed02 / seed12 is exactly one block per group, so no
 // keystream byte is generated twice and no keystream is exchanged between
 // threads.  Share vectors move as 4 x 16-B vector accesses per party per group.

@@ -62,9 +62,10 @@ struct TapeC {
 
 // x / 257 for any 32-bit x: floor(x * (2^40 + 1)/257 / 2^40) (exact).
 __device__ __forceinline__ uint32_t div257(uint32_t x) { return __umulhi(x, 0xFF00FF01u) >> 8; }
-// x / 257 for x < 2^24 with one IMAD.HI and no shift: umulhi(x, ceil(2^32 / 257)); the
-// magic overshoots 2^32/257 by 1/8, harmless while x / 8 / 2^32 < 1/257, i.e. x < 2^27
-// (tests/test_kernel_arith.py, exhaustive below 2^24).
+// x / 257 for x < 2^24 with one IMAD.HI and no shift: umulhi(x, ceil(2^32 / 257)).  Since
+// 2^32 - 1 = 257 * 16711935, the magic 16711936 overshoots 2^32/257 by 256/257, harmless while
+// x * (256/257) / 2^32 < 1/257, i.e. x < 2^24 exactly: the first failure is x = 2^24 = 257 * 65281 - 1
+// (tests/test_kernel_arith.py: exhaustive below 2^24, and that failure).
 __device__ __forceinline__ uint32_t div257s(uint32_t x) { return __umulhi(x, 0xFF0100u); }
 
 struct FbC {  // the draws a compact tape can reject, passed by value (registers, not local memory)
@@ -380,13 +381,17 @@ __device__ __forceinline__ uint32_t elem_both_t(uint64_t x0, uint64_t x1, uint32
 // ---- v2 of the table kernel's slot arithmetic (BC_TBL_V2) ----------------------------
 // The reshare enters as congruent offsets decoded straight from the digit quotients:
 //   P0: x0_m = (v'_m) r_m + o0_m, o0_m = rho_m + 257 k  (k >= 0; < 2^24)
-//   P1: x1_m = (v'_m) r_m + o1_m, o1_m = 257 K - rho_m  (> 0;     < 2^25)
+//   P1: x1_m = (v'_m) r_m + o1_m, o1_m = 257 K - rho_m  (> 0;     <= 16710397)
 // with rho_{3k} = w - 257 q1 (reduced), rho_{3k+1} = q1 - 257 q2 (== q1), rho_{3k+2}
 // = q2 mod 257 (== q2), q1 = w div 257, q2 = q1 div 257.  The bytes v'-1 and r-1 are
 // extracted with the +1 folded in: dp4a(word, unit byte vector, 1) = byte + 1 (IDP.4A,
-// FMA pipe).  W0 = x0 mod 257 (< 2^25: div257s exact); P2 tests 257 | (W0 + x1).
+// FMA pipe).  Both x0, x1 <= 65536 + 16710397 < 2^24, so div257s (exact below 2^24 only)
+// reduces them; P2 tests 257 | (W0 + x1).
+#ifndef BC_P2_DIST
+#define BC_P2_DIST 1  // P2's test by distributivity (BC_MATERIALIZE 1): xm0 257^-1 + x1 257^-1 - q0
+#endif
 #ifndef BC_TBL_V2
-#define BC_TBL_V2 0
+#define BC_TBL_V2 1
 #endif
 template <int R>
 __device__ __forceinline__ uint32_t decode_t2(uint32_t T0, uint32_t w0, uint32_t w1, uint32_t w2, uint64_t j,
@@ -404,7 +409,7 @@ __device__ __forceinline__ uint32_t decode_t2(uint32_t T0, uint32_t w0, uint32_t
     o0[3 * k] = w[k] - 257u * q1;                           // rho_{3k}, reduced
     o1[3 * k] = 257u * q1 + (257u - w[k]);                  // 257 - rho_{3k} > 0
     o0[3 * k + 1] = q1;                                     // == rho_{3k+1} (mod 257)
-    o1[3 * k + 1] = 16842752u - q1;                         // 257 * 2^16 - q1 > 0
+    o1[3 * k + 1] = 16710397u - q1;                         // 257 * 65021 - q1 > 0 (q1 <= 16710396)
     if (k < 2) {
       const uint32_t q2 = div257s(q1);                      // < 2^16
       o0[3 * k + 2] = q2;                                   // == rho_{3k+2}
@@ -448,13 +453,101 @@ __device__ __forceinline__ uint32_t elem_both_t2(uint64_t x0, uint64_t x1, uint3
       W0[m] = mod257s(xm0);
       W1[m] = mod257s(xm1);
       vmin = min(vmin, add_fma(W0[m], W1[m], one) * 0xFF00FF01u);
-    } else if (BC_MATERIALIZE == 1) {
+    } else if (BC_MATERIALIZE == 1 && !BC_P2_DIST) {
       vmin = min(vmin, add_fma(mod257s(xm0), xm1, one) * 0xFF00FF01u);
+    } else if (BC_MATERIALIZE == 1) {
+      // P0 reduces its message: W0 = xm0 - 257 q0 with q0 = xm0 div 257 (xm0 < 2^24: div257s
+      // exact).  P2 tests 257 | (W0 + x1) multiplicatively; since 257 * 257^-1 = 1 (mod 2^32),
+      // (W0 + x1) 257^-1 = xm0 257^-1 + x1 257^-1 - q0 (mod 2^32): the same value, two IMADs
+      // instead of forming W0 (IMAD) and the sum (IMAD) before the multiply.
+      const uint32_t q0 = div257s(xm0);
+      vmin = min(vmin, xm0 * 0xFF00FF01u + (xm1 * 0xFF00FF01u - q0));
     } else {
       vmin = min(vmin, add_fma(xm0, xm1, one) * 0xFF00FF01u);
     }
   }
   return vmin <= 16711935u;
+}
+
+// ---- the paper-literal domain (w = lx = 7, p = 131, 8 slots, pair tape), table form ----
+// Pair-tape draws of one element (T = its 8 keystream words):
+// t, the permutation index mod 8!, and per slot r_m = 1 + x mod 130, rho_m = x div 130
+// with x = u_m mod 17030 (u_m the 28-bit draw of slot m).  Constants of kp_literal.
+template <int R>
+__device__ __forceinline__ uint32_t decode_pl(const uint32_t* T, uint64_t j, const Key& k01, const KP& kp,
+                                              uint32_t& t, uint32_t (&r)[8], uint32_t (&rho)[8]) {
+  Draws d;
+  t = T[0] >> 31;
+  d.idx = T[0] & 0x7FFFFFFFu;
+  uint32_t mx = 0;
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const int bit = 28 * m, w = bit >> 5, sh = bit & 31;
+    const uint32_t nxt = w < 6 ? T[2 + w] : 0u;
+    d.um[m] = __funnelshift_r(T[1 + w], nxt, sh) & 0x0FFFFFFFu;
+    d.ur[m] = 0u;
+    mx = max(mx, d.um[m]);
+  }
+  if (__builtin_expect((d.idx >= kp.perm_lim) | (mx >= kp.pair_lim), 0)) {
+    Draws f = d;
+    fallback<R>(f, j, k01, 8u, kp.perm_lim, kp.pair_lim, 1u, 0x0FFFFFFFu);
+    d = f;
+  }
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const uint32_t x = d.um[m] - kp.pair_d * (__umulhi(d.um[m], kp.pair_mag) >> kp.pair_sh);  // u mod (p-1) p
+    const uint32_t q = __umulhi(x, kp.mag_q);                                                // x div (p-1)
+    r[m] = x - (kp.p - 1u) * q + 1u;
+    rho[m] = q;
+  }
+  return d.idx - 40320u * __umulhi(d.idx >> 7, 13634817u);  // idx mod 8! (as decode_t)
+}
+
+constexpr uint32_t kInv131 = 0xC9484E2Bu;     // 131^-1 mod 2^32
+constexpr uint32_t kLim131 = 32786009u;       // floor((2^32 - 1) / 131)
+constexpr uint32_t kMag131 = 32786010u;       // ceil(2^32 / 131): x div 131 = umulhi(x, kMag131) for x < 2^16
+
+// Alg 7 steps 1-9 of both computing parties and P2 in the literal domain, table form
+// (bc_tables.cuh LiteralTables; sbase = its shared-window address).  P0's message
+// x0_m = v'_m r_m + rho_m is reduced (W0 = x0 - 131 q0); P1's is the congruent
+// x1_m = v'_m r_m + 131 - rho_m; P2 tests 131 | (W0 + x1) as the compact path does.
+template <bool KEEP_W, bool FHI>
+__device__ __forceinline__ uint32_t elem_both_tl(uint64_t x0, uint64_t x1, uint32_t t, uint32_t ix,
+                                                 const uint32_t (&r)[8], const uint32_t (&rho)[8], uint32_t sbase,
+                                                 uint32_t fsh, uint32_t (&W0)[8], uint32_t (&W1)[8]) {
+  const uint64_t v0 = t ? 0ull - x0 : x0;   // steps 1-2: P0 blinds s_0
+  const uint64_t v1 = t ? x1 : 0ull - x1;   // P1 windows -s_1 (Alg 5, reading C3)
+  const uint32_t wn0 = win_at<FHI>(v0, fsh), wn1 = win_at<FHI>(v1, fsh);
+  constexpr uint32_t LAD = 4u * kPermN;
+  // steps 3-5 (table): bytes v'_i - 1; lo bytes from win bits [0, 11), hi from [4, 14)
+  const uint32_t c_lo = lds_u32(sbase + LAD + 4u * kLitP0Lo + ((wn0 << 2) & 0x1FFCu));
+  const uint32_t c_hi = lds_u32(sbase + LAD + 4u * kLitP0Hi + ((wn0 >> 2) & 0x0FFCu));
+  const uint32_t d_lo = lds_u32(sbase + LAD + 4u * kLitP1Lo + ((wn1 << 2) & 0x1FFCu));
+  const uint32_t d_hi = lds_u32(sbase + LAD + 4u * kLitP1Hi + ((wn1 >> 2) & 0x0FFCu));
+  // step 6: the permutation as one selector
+  const uint32_t sel = lds_u32(sbase + ix * 4u);
+  const uint32_t selh = lds_u16(sbase + ix * 4u + 2u);
+  const uint32_t C_lo = prmt(c_lo, c_hi, sel), C_hi = prmt(c_lo, c_hi, selh);
+  const uint32_t D_lo = prmt(d_lo, d_hi, sel), D_hi = prmt(d_lo, d_hi, selh);
+  uint32_t vmin = 0xFFFFFFFFu;
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const uint32_t unit = 1u << (8 * (m & 3));
+    const uint32_t c1 = __dp4a(m < 4 ? C_lo : C_hi, unit, 1u);  // v'_m of P0 (byte + 1)
+    const uint32_t d1 = __dp4a(m < 4 ? D_lo : D_hi, unit, 1u);  // v'_m of P1
+    // steps 7-8: mask and reshare (x0 < 2^15, x1 < 2^16)
+    const uint32_t xm0 = c1 * r[m] + rho[m];
+    const uint32_t xm1 = d1 * r[m] + (131u - rho[m]);
+    const uint32_t q0 = __umulhi(xm0, kMag131);
+    if (KEEP_W) {
+      W0[m] = xm0 - 131u * q0;
+      W1[m] = xm1 - 131u * __umulhi(xm1, kMag131);
+      vmin = min(vmin, (W0[m] + W1[m]) * kInv131);
+    } else {  // step 9: (W0 + x1) 131^-1 = x0 131^-1 + x1 131^-1 - q0 (mod 2^32)
+      vmin = min(vmin, xm0 * kInv131 + (xm1 * kInv131 - q0));
+    }
+  }
+  return vmin <= kLim131;  // some W0_m + W1_m divisible by 131
 }
 
 template <int PARTY, bool ADDF = false>

@@ -136,9 +136,99 @@ __global__ void __launch_bounds__(TPB) k_ladder(const uint64_t* __restrict__ x, 
   }
 }
 
+// Alg 6 at any width: 1 <= lp <= 63, 2^lp < p < 2^64.  Both results are
+// already reduced: P0's x < 2^lp < p (and 2^lp mod p = 2^lp), P1's p - 2^lp + x < p.
+__global__ void __launch_bounds__(TPB) k_modswitch64(const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
+                                                     uint64_t n, uint32_t lp, uint64_t p, int party) {
+  const uint64_t npairs = (n + 1) >> 1;
+  const uint64_t two_lp = 1ull << lp, lmask = two_lp - 1ull;
+  for (uint64_t i = (uint64_t)blockIdx.x * TPB + threadIdx.x; i < npairs; i += (uint64_t)gridDim.x * TPB) {
+    uint64_t v[2];
+    load_pair(in, i, n, v);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const uint64_t x = v[k] & lmask;
+      v[k] = party == 0 ? (x == 0 ? two_lp : x) : (p - two_lp) + x;
+    }
+    store_pair(out, i, n, v);
+  }
+}
+
+// Alg 7 steps 3-5 for one party, any tape (up to 32 slots, p < 2^33): v'_m as uint64_t[n][S].
+// A warp owns 32 consecutive elements; element e's row is written by lanes m < S together
+// (S consecutive words), lane m computing slot m from the broadcast share.
+struct Lad64 {
+  const uint64_t* x;
+  uint64_t* v;
+  uint64_t n, inmask, wmask, two_w, p;
+  uint32_t f, lx, S;
+};
+template <int PARTY>
+__global__ void __launch_bounds__(TPB) k_ladder64(Lad64 a) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t nwarps = (uint64_t)gridDim.x * (TPB / 32);
+  for (uint64_t wbase = ((uint64_t)blockIdx.x * (TPB / 32) + threadIdx.x / 32) * 32; wbase < a.n;
+       wbase += nwarps * 32) {
+    const uint64_t i = wbase + lane;
+    const uint64_t xi = i < a.n ? __ldg(a.x + i) : 0ull;
+    const uint32_t cnt = (uint32_t)min((uint64_t)32, a.n - wbase);
+    for (uint32_t e = 0; e < cnt; ++e) {
+      const uint64_t s = __shfl_sync(0xFFFFFFFFu, xi, (int)e);
+      if (lane >= a.S) continue;
+      // Alg 5 windows (k1 = f + m): P0 reads s, P1 reads -s (reading C3) and negates the window (C4)
+      const uint64_t op = PARTY == 0 ? (s & a.inmask) : ((0ull - s) & a.inmask);
+      uint64_t u = (op >> (a.f + lane)) & a.wmask;
+      uint64_t u1 = lane < a.lx ? (op >> (a.f + lane + 1)) & a.wmask : 0ull;
+      if (PARTY == 1) { u = (0ull - u) & a.wmask; u1 = (0ull - u1) & a.wmask; }
+      const uint64_t vm = (u + u1 - (PARTY == 0 ? 1ull : 0ull)) & a.wmask;  // P0 carries the -1 (C8)
+      // Alg 6: P0 v = 0 -> 2^w (= 2^w mod p); P1 p + v - 2^w (both already in [1, p))
+      a.v[(wbase + e) * a.S + lane] = PARTY == 0 ? (vm == 0 ? a.two_w : vm) : (a.p - a.two_w) + vm;
+    }
+  }
+}
+
 }  // namespace
 
 extern "C" {
+
+int bc_modswitch64(int party, const uint64_t* in, uint64_t* out, size_t n, int lp, uint64_t p, void* stream) {
+  if ((party != 0 && party != 1) || lp < 1 || lp > 63 || p <= (1ull << lp)) return BC_EINVAL;
+  if (n == 0) return BC_OK;  // no-op after parameter validation
+  if (!in || !out) return BC_EINVAL;
+  if (!aligned16(in) || !aligned16(out)) return BC_EALIGN;
+  if (overlap(in, n * 8, out, n * 8)) return BC_EALIAS;
+  k_modswitch64<<<grid_for((const void*)k_modswitch64, (n + 1) / 2), TPB, 0, static_cast<cudaStream_t>(stream)>>>(
+      in, out, n, (uint32_t)lp, p, party);
+  return check_launch();
+}
+
+int bc_ladder_modswitch64(int party, const uint64_t* x, uint64_t* v, size_t n, const bc_params* prm, void* stream) {
+  const int rc = check_params(prm);
+  if (rc) return rc;
+  if (n == 0) return BC_OK;  // no-op after parameter validation
+  if (party != 0 && party != 1) return BC_EINVAL;
+  if (!x || !v) return BC_EINVAL;
+  if (!aligned16(x) || !aligned16(v)) return BC_EALIGN;
+  if (overlap(x, n * 8, v, n * 8 * prm->slots)) return BC_EALIAS;
+  Lad64 a{};
+  a.x = x;
+  a.v = v;
+  a.n = n;
+  a.inmask = prm->ell == 64 ? ~0ull : ((1ull << prm->ell) - 1ull);
+  a.two_w = 1ull << prm->w;
+  a.wmask = a.two_w - 1ull;
+  a.p = prm->p;
+  a.f = (uint32_t)prm->f;
+  a.lx = (uint32_t)prm->lx;
+  a.S = prm->slots;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t warps = (n + 31) / 32;
+  if (party == 0)
+    k_ladder64<0><<<grid_for((const void*)k_ladder64<0>, warps * 32), TPB, 0, st>>>(a);
+  else
+    k_ladder64<1><<<grid_for((const void*)k_ladder64<1>, warps * 32), TPB, 0, st>>>(a);
+  return check_launch();
+}
 
 int bc_trc(int party, const uint64_t* in, uint64_t* out, size_t n, int ell, int k1, int k2, void* stream) {
   if ((party != 0 && party != 1) || ell < 2 || ell > 64 || k1 < 0 || k2 < 0 || k1 + k2 >= ell)

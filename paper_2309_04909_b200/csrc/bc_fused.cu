@@ -176,7 +176,10 @@ __global__ void __launch_bounds__(TPB, FUSED_MINB) k_fused_c(FusedArgs a, KP kp,
 #ifndef BC_FUSED_TABLES
 #define BC_FUSED_TABLES 1  // 0: the SWAR kernel k_fused_c for the compact tape
 #endif
-constexpr int TPB_T = 512;
+#ifndef BC_TPB_T
+#define BC_TPB_T 512  // threads of the one CTA per SM (65536 registers / TPB_T per thread)
+#endif
+constexpr int TPB_T = BC_TPB_T;
 constexpr size_t kTabBytes = sizeof(uint32_t) * kTabWords;
 __device__ constexpr CompactTables kTables{};
 
@@ -244,7 +247,62 @@ __global__ void __launch_bounds__(TPB_T, 1) k_fused_t(FusedArgs a, KP kp, Key k0
   }
 }
 
-// Wide tape (any p <= 257, 3..8 slots): one seed01 block per element.
+// The paper-literal domain at lx = 7 (BC_TAPE_COMPACT_LIT: w = 7, p = 131, 8 slots; pair
+// tape), table form: one CTA of TPB_T threads per SM with the 186 KB of LiteralTables in
+// shared memory.  Same thread mapping and finish as k_fused_w.
+#ifndef BC_FUSED_LIT_TABLES
+#define BC_FUSED_LIT_TABLES 1  // 0: k_fused_w<CL = true>
+#endif
+constexpr size_t kLitTabBytes = sizeof(uint32_t) * kLitTabWords;
+__device__ constexpr LiteralTables kLitTables{};
+
+template <int R, bool RELU, bool TRANSCRIPT, bool FULL, bool FHI>
+__global__ void __launch_bounds__(TPB_T, 1) k_fused_tl(FusedArgs a, KP kp_, Key k01, Key k02, Key k12, PreKeys pk) {
+  const KP kp = kp_literal(kp_);
+  extern __shared__ uint4 smem_t[];
+  {
+    const uint4* g = reinterpret_cast<const uint4*>(kLitTables.w);
+    for (int i = threadIdx.x; i < kLitTabWords / 4; i += blockDim.x) smem_t[i] = g[i];
+  }
+  __syncthreads();
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_t);
+  const uint64_t ngroups = (a.n + 7) >> 3;
+  for (uint64_t g = (uint64_t)blockIdx.x * TPB_T + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB_T) {
+    const uint64_t i0 = g << 3;
+    const uint64_t j0 = a.base + i0;
+    const uint32_t cnt = (uint32_t)min((uint64_t)8, a.n - i0);
+    uint32_t zbits = 0, tbits = 0;
+#pragma unroll 1
+    for (int e2 = 0; e2 < 8; e2 += 2) {  // one seed01 block holds elements e2, e2 + 1 (j0 is a multiple of 8)
+      uint32_t B[16];
+      stream_blk<R, !RELU>(pk.tpa, k01, L_TAPEP, (j0 + (uint64_t)e2) >> 1, B);  // pk.tpa: bc2.tpp1
+      const ulonglong2 u0 = load2(a.x0, i0 + e2, a.n), u1 = load2(a.x1, i0 + e2, a.n);
+      const uint32_t bit0 = 1u << e2;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e = e2 + h;
+        uint32_t t, r[8], rho[8];
+        const uint32_t ix = decode_pl<R>(B + 8 * h, j0 + (uint64_t)e, k01, kp, t, r, rho);
+        uint32_t W0[8], W1[8];
+        const uint32_t z = elem_both_tl<TRANSCRIPT, FHI>(h ? u0.y : u0.x, h ? u1.y : u1.x, t, ix, r, rho, sbase,
+                                                         kp.fsh, W0, W1);
+        if (TRANSCRIPT && (uint32_t)e < cnt) {  // the P0/P1 -> P2 messages, wire format
+          reinterpret_cast<uint64_t*>(a.w0lo)[i0 + e] = pack_lo(W0);
+          reinterpret_cast<uint64_t*>(a.w1lo)[i0 + e] = pack_lo(W1);
+          a.w0hi[i0 + e] = (uint8_t)pack_hi(W0);
+          a.w1hi[i0 + e] = (uint8_t)pack_hi(W1);
+        }
+        const uint32_t bit = bit0 << h;
+        zbits = z * bit + zbits;
+        tbits = t * bit + tbits;
+      }
+    }
+    finish_group<R, RELU, FULL>(a, kp, k02, k12, pk, i0, j0, cnt, zbits, tbits);
+  }
+}
+
+// Pair tape (every lx <= 7 domain but the compact one: p <= 131, 3..8 slots): one
+// seed01 block per two elements (bc2.tpp1, 32 B each).
 template <int R, bool RELU, bool CL>
 __global__ void __launch_bounds__(TPB, 2) k_fused_w(FusedArgs a, KP kp_, Key k01, Key k02, Key k12, PreKeys pk) {
   const KP kp = CL ? kp_literal(kp_) : kp_;
@@ -282,7 +340,7 @@ __global__ void __launch_bounds__(TPB, 2) k_fused_w(FusedArgs a, KP kp_, Key k01
   }
 }
 
-// Large tape (lx >= 8, up to 32 slots, p < 2^33): 9 seed01 blocks per element,
+// Large tape (lx >= 8, up to 32 slots, p < 2^33): 7 seed01 blocks per element (bc2.tpL2),
 // the 8 elements of a group in sequence, then the shared finish.
 constexpr int TPB_L = TPB_LARGE;
 #ifndef BC_LARGE_MINB
@@ -474,6 +532,14 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
       auto fn = tr ? k_fused_c<R, RELU, true, false>
                    : (prm->ell == 64 ? k_fused_c<R, RELU, false, true> : k_fused_c<R, RELU, false, false>);
       fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k01, k02, k12, pk);
+    } else if (prm->tape == BC_TAPE_COMPACT_LIT && BC_FUSED_LIT_TABLES) {
+      const bool fhi = kp.fhi != 0;
+      auto fn = tr ? (fhi ? k_fused_tl<R, RELU, true, false, true> : k_fused_tl<R, RELU, true, false, false>)
+                   : prm->ell == 64 ? (fhi ? k_fused_tl<R, RELU, false, true, true> : k_fused_tl<R, RELU, false, true, false>)
+                                    : (fhi ? k_fused_tl<R, RELU, false, false, true> : k_fused_tl<R, RELU, false, false, false>);
+      const int rc = allow_smem((const void*)fn, kLitTabBytes);
+      if (rc) return rc;
+      fn<<<grid_for((const void*)fn, ngroups, TPB_T, kLitTabBytes), TPB_T, kLitTabBytes, st>>>(a, kp, k01, k02, k12, pk);
     } else {
       auto fn = prm->tape == BC_TAPE_COMPACT_LIT ? k_fused_w<R, RELU, true> : k_fused_w<R, RELU, false>;
       fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k01, k02, k12, pk);

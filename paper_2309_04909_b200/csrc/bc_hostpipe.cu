@@ -30,6 +30,7 @@ struct Ring {
   cudaStream_t s[NS];
   cudaEvent_t ev[NS];
   cudaEvent_t start;
+  std::mutex start_mu;  // one caller at a time between recording `start` and the ring's waits on it
   std::atomic<uint64_t> next{0};  // chunk rotation continues across calls (async calls pipeline evenly)
 };
 
@@ -80,6 +81,10 @@ int host_run(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1,
   if (rr) return rr;
   cudaStream_t caller = static_cast<cudaStream_t>(stream);
   if (SYNC) {  // order after the caller's prior work on `stream`
+    // held across record and waits: a concurrent caller's record in between would make this
+    // call's chunks wait on THAT caller's stream instead of its own (cudaStreamWaitEvent takes
+    // the event's most recent record at the time of the call)
+    std::lock_guard<std::mutex> lk(ring->start_mu);
     cudaEventRecord(ring->start, caller);
     for (int i = 0; i < NS; ++i) cudaStreamWaitEvent(ring->s[i], ring->start, 0);
   }

@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(TPB, 2) k_send_c(SendArgs a, KP kp, Key k01, K
   }
 }
 
-// Wide tape.
+// Pair tape (one seed01 block per two elements).
 template <int R, int PARTY, bool RELU, bool CL>
 __global__ void __launch_bounds__(TPB, 2) k_send_w(SendArgs a, KP kp_, Key k01, Key ktr) {
   const KP kp = CL ? kp_literal(kp_) : kp_;

@@ -129,8 +129,9 @@ class PartyRunner:
         self.group = group
         self.paper_literal = paper_literal
         # run r draws from [base0 + r * triples * n, + n): fresh randomness per run (as peer.PeerPartyRunner)
-        self.base0 = self.role.triple * n if base is None else base
-        self.stride = triples * n
+        span = -(-n // 8) * 8  # index ranges start at multiples of 8 (the elem_base rule)
+        self.base0 = self.role.triple * span if base is None else base
+        self.stride = triples * span
         self.runs = 0
         self.base = self.base0
         self.fmt = api.wire_format(prm)  # byte planes (p <= 257) or uint32 planes (large tape)

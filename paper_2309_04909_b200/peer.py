@@ -44,10 +44,22 @@ class CudaIpcBackend:
     def __init__(self, device):
         self.device = torch.device(device)
         self._maps = {}  # handle -> base address of the mapping in this process
+        self._pools = []  # one private pool per inbox (alloc_inbox)
         api.lib()
 
     def alloc(self, shape, dtype):
+        """Local working memory (never exported)."""
         return torch.zeros(shape, dtype=dtype, device=self.device)
+
+    def alloc_inbox(self, shape, dtype):
+        """An inbox that one producer maps.  bc_ipc_export exports the whole allocation that
+        holds the tensor, so every inbox gets a private memory pool: its segment then holds
+        that inbox and nothing else -- not this party's own shares or blinding bits, and not
+        the inbox another party writes (P2's inbox from P1 must stay invisible to P0)."""
+        pool = torch.cuda.MemPool()
+        self._pools.append(pool)  # the pool must outlive its tensor
+        with torch.cuda.use_mem_pool(pool, device=self.device):
+            return torch.zeros(shape, dtype=dtype, device=self.device)
 
     def export(self, t):
         h, off = api.ipc_export(t)
@@ -103,7 +115,7 @@ class Link:
         """What this rank publishes about the link (all_gather'd)."""
         out = {}
         if rank == self.dst:
-            self.ring = {k: be.alloc((self.slots, self.chunk) + shp, dt) for k, (shp, dt) in self.fields.items()}
+            self.ring = {k: be.alloc_inbox((self.slots, self.chunk) + shp, dt) for k, (shp, dt) in self.fields.items()}
             self.consumed = [be.new_event() for _ in range(self.slots)]
             out["ring"] = {k: be.export(t) for k, t in self.ring.items()}
             out["consumed"] = [be.export_event(e) for e in self.consumed]
@@ -187,8 +199,9 @@ class PeerPartyRunner:
         # rho_m and triples: reusing them on new inputs would open
         # x - x' to P0/P1 (d = x - a) and hand P2 several messages under one mask.  stride =
         # triples * n keeps the triples sharing the index space disjoint across runs too.
-        self.base0 = self.role.triple * n if base is None else base
-        self.stride = triples * n
+        span = -(-n // 8) * 8  # index ranges start at multiples of 8 (the elem_base rule)
+        self.base0 = self.role.triple * span if base is None else base
+        self.stride = triples * span
         self.runs = 0
         self.base = self.base0
         fmt = api.wire_format(prm)  # byte planes (p <= 257) or slot-major uint32 planes (large tape)
@@ -337,11 +350,29 @@ class PeerPartyRunner:
         from2.release(seq, be, g, self._works)
 
     # ---- public ------------------------------------------------------------------------
+    def egress_bytes_per_elem(self) -> dict:
+        """Bytes per element this rank's kernels store into each peer's inbox per run (every
+        link it produces: the message planes to P2, [d]_b, e, [c]_1, the response), from the
+        link field shapes -- the wire cost the protocol pays (Table 1)."""
+        out = {}
+        for name, lk in self.L.items():
+            if lk.src != self.rank:
+                continue
+            b = 0
+            for shp, dt in lk.fields.values():
+                k = 1
+                for s_ in shp:
+                    k *= s_
+                b += k * torch.empty((), dtype=dt).element_size()
+            out[f"link{name}->P{Role.of(lk.dst).party}"] = b
+        return out
+
     def run(self, x=None, out=None, elem_base: int | None = None):
         """P0/P1: x is this party's share vector (n,), returns its output share.
         P2: x=None, returns None.  Asynchronous on the current stream like the
         kernels themselves: synchronise before reading the result on the host.
-        Run r uses the global element indices base0 + r * stride + [0, n) unless
+        Run r uses the global element indices base0 + r * stride + [0, n) (stride =
+        triples * n rounded up to a multiple of 8) unless
         elem_base is given (all three parties must pass the same value)."""
         p = self.role.party
         self.base = self.base0 + self.runs * self.stride if elem_base is None else elem_base

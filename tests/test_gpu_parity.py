@@ -97,6 +97,35 @@ def test_ladder_modswitch_parity(api, kw):
         assert np.array_equal(got, B.ladder_modswitch_bytes(oprm, party, xs))
 
 
+@pytest.mark.parametrize("lp,p", [(1, 3), (8, 257), (31, (1 << 31) + 11), (32, (1 << 32) + 15), (33, (1 << 33) + 17),
+                                  (48, (1 << 48) + 12345), (63, (1 << 63) + 29), (63, (1 << 64) - 59)])
+def test_modswitch64_parity(api, lp, p):
+    """Alg 6 beyond 31 bits (bc_modswitch64): the full-precision guard domain lp = 32,
+    p = 2^32 + 15, and moduli up to 2^64 - 59, against ring.modswitch (Python ints)."""
+    rng = np.random.default_rng(lp)
+    x = rng.integers(0, 2**64 - 1, size=2049, dtype=np.uint64, endpoint=True)
+    x[:3] = 0
+    x[3] = np.uint64((1 << lp) - 1)
+    xl = [int(v) & ((1 << lp) - 1) for v in x]
+    for party in (0, 1):
+        got = host(api.modswitch64(party, dev(x), lp, p))
+        want = np.array([ring.modswitch(party, v, lp, p) for v in xl], dtype=np.uint64)
+        assert np.array_equal(got, want), party
+
+
+@pytest.mark.parametrize("kw", PARAMS + [dict(ell=64, lx=31, f=0, mode="guard", rounds=20),
+                                         dict(ell=64, lx=31, f=0, mode="literal", rounds=8),
+                                         dict(ell=40, lx=12, f=3, mode="guard", rounds=8)], ids=_ids)
+def test_ladder_modswitch64_parity(api, kw):
+    """Alg 7 steps 3-5 with the v'_m as u64 (bc_ladder_modswitch64), every tape up to
+    the full-precision 32 slots, n across several warps with a ragged tail."""
+    oprm = B.Params(**kw)
+    x, x0, x1 = synth.shares(4099, kw["ell"], kw["lx"], kw["f"], "D1")
+    for party, xs in ((0, x0), (1, x1)):
+        got = api.ladder_modswitch64(party, dev(xs), api.Params(**kw)).cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, B.ladder_modswitch(oprm, party, xs)), party
+
+
 # ---- fused three-party DReLU / ReLU ------------------------------------------------
 
 @pytest.mark.parametrize("kw", PARAMS, ids=_ids)

@@ -62,8 +62,9 @@ def _work(rank, world, port, kind, n, chunk, slots, literal, runs, outdir, kw=No
         # the fused one-GPU kernel on the same shares (bit-exact with the oracle: test_gpu_parity.py)
         t0 = torch.from_numpy(x0.view(np.int64)).cuda()
         t1 = torch.from_numpy(x1.view(np.int64)).cuda()
-        for r in range(runs):  # run r draws from global indices r n + [0, n) (one triple)
-            ref = getattr(api, kind)(t0, t1, prm, synth.seeds(0), role.triple * n + r * n)[role.party]
+        span = -(-n // 8) * 8
+        for r in range(runs):  # run r draws from global indices r span + [0, n) (one triple)
+            ref = getattr(api, kind)(t0, t1, prm, synth.seeds(0), (role.triple + r) * span)[role.party]
             np.save(os.path.join(outdir, f"fused_{rank}_{r}.npy"), ref.cpu().numpy().view(np.uint64))
     dist.barrier()
     dist.destroy_process_group()
@@ -93,8 +94,9 @@ def test_party_peer_three_processes_vs_oracle(tmp_path, kind, slots, literal):
     _run(tmp_path, kind, n, chunk, slots, literal, runs=2)
     o = B.Params(ell=64, lx=7, f=24, mode="guard", rounds=20)
     x, x0, x1 = synth.shares(n, 64, 7, 24, "D1", run=0)
+    span = -(-n // 8) * 8
     for r in range(2):
-        ref = getattr(B, kind)(o, x0, x1, np.arange(n, dtype=np.uint64) + np.uint64(r * n), synth.seeds(0))
+        ref = getattr(B, kind)(o, x0, x1, np.arange(n, dtype=np.uint64) + np.uint64(r * span), synth.seeds(0))
         assert np.array_equal(np.load(tmp_path / f"y_0_{r}.npy"), ref["y0"])
         assert np.array_equal(np.load(tmp_path / f"y_1_{r}.npy"), ref["y1"])
 
@@ -114,3 +116,24 @@ def test_party_peer_full_precision(tmp_path, kind):
         pytest.skip("no CUDA device")
     kw = dict(ell=64, lx=31, f=0, mode="guard", rounds=8)
     _run(tmp_path, kind, 2003, 512, 2, kind == "drelu", 2, kw)
+
+
+def test_inbox_exports_only_itself():
+    """Every inbox sits alone in the allocation bc_ipc_export hands to its producer:
+    offset 0 and a handle of its own, distinct from the party's local buffers'."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    sys.path[:0] = [ROOT]
+    from paper_2309_04909_b200 import api, peer
+    be = peer.CudaIpcBackend("cuda:0")
+    local = be.alloc((1000,), torch.int64)
+    boxes = [be.alloc_inbox((2, 4096, 8), torch.uint8), be.alloc_inbox((2, 4096), torch.uint8),
+             be.alloc_inbox((2, 4096), torch.int64)]
+    local2 = be.alloc((1000,), torch.int64)
+    handles = set()
+    for b in boxes:
+        h, off = api.ipc_export(b)
+        assert off == 0
+        handles.add(h)
+    assert len(handles) == len(boxes)
+    assert api.ipc_export(local)[0] not in handles and api.ipc_export(local2)[0] not in handles

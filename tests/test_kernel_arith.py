@@ -19,8 +19,29 @@ def test_div257s_exact_below_2pow24():
     kernel applies it to quotients q1 = w // 257 < 2^24 and q2 < 2^16)."""
     x = np.arange(1 << 24, dtype=np.uint64)
     assert np.array_equal((x * np.uint64(0xFF0100)) >> np.uint64(32), x // np.uint64(257))
-    x = np.array([(1 << 27) - 1, (1 << 27) - 257, (1 << 26) + 12345], dtype=np.uint64)   # the stated bound
-    assert np.array_equal((x * np.uint64(0xFF0100)) >> np.uint64(32), x // np.uint64(257))
+    # and not one step further: 2^24 = 257 * 65281 - 1 is the first x whose quotient overshoots
+    x = np.uint64(1 << 24)
+    assert (x * np.uint64(0xFF0100)) >> np.uint64(32) == x // np.uint64(257) + np.uint64(1)
+
+
+def test_table_v2_offsets_stay_below_2pow24():
+    """decode_t2 / elem_both_t2 (csrc/bc_compact.cuh): the reshare offsets o0 = rho + 257 k and
+    o1 = 257 K - rho are congruent to +-rho_m mod 257, positive, and keep the messages
+    x = v' r + o below 2^24 (div257s' exact range) for every reshare word below the limit."""
+    LIM = 253 * 257 ** 3
+    rng = np.random.default_rng(7)
+    w = np.concatenate([rng.integers(0, LIM, 1 << 20, dtype=np.uint64),
+                        np.array([0, 1, 256, 257, LIM - 1, LIM - 257, 257 ** 3 - 1], dtype=np.uint64)])
+    q1 = w // np.uint64(257)
+    q2 = q1 // np.uint64(257)
+    rho = [w % np.uint64(257), q1 % np.uint64(257), q2 % np.uint64(257)]
+    o0 = [w - np.uint64(257) * q1, q1, q2]
+    o1 = [np.uint64(257) * q1 + np.uint64(257) - w, np.uint64(16710397) - q1, np.uint64(65792) - q2]
+    for i in range(3):
+        assert (o1[i].astype(np.int64) > 0).all()
+        assert np.array_equal(o0[i] % np.uint64(257), rho[i])
+        assert np.array_equal((o1[i] + rho[i]) % np.uint64(257), np.zeros_like(w))
+        assert int(o0[i].max()) + 256 * 256 < (1 << 24) and int(o1[i].max()) + 256 * 256 < (1 << 24)
 
 
 def test_div257_exact_all_u32_sample_and_edges():
@@ -181,10 +202,10 @@ def test_fpmod48_quotient_exact():
                 assert _fp_quotient(u >> s, qo) == u // q, (w, q, u)
 
 
-def test_wide_tape_magic_divisions():
-    """The pair tape's runtime divisions by host-computed magics (KP::mag_p, mag_q,
-    mag_f): x / d = umulhi(x, ceil(2^32/d)) for every 16-bit draw and every d = p, p-1
-    of a wide-tape setting (w = 2..8); x / S! = umulhi(x, ceil(2^(31+l)/S!)) >> (l-1)
+def test_small_domain_magic_divisions():
+    """The runtime divisions by host-computed magics of the small domains (KP::mag_p,
+    mag_q, mag_f): x / d = umulhi(x, ceil(2^32/d)) for every 16-bit value and every
+    d = p, p-1 of an lx <= 7 setting (w = 2..8); x / S! = umulhi(x, ceil(2^(31+l)/S!)) >> (l-1)
     for 31-bit indices (l = ceil(log2 S!)), sampled plus the multiples' edges."""
     import math
     from oracle.ring import prime_above

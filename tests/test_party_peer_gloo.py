@@ -77,8 +77,9 @@ def test_peer_runtime_gloo_single_chunk_many_slots(tmp_path):
                        nprocs=3, join=True, start_method="spawn")
     o = B.Params(**CONFIGS["guard"])
     x, x0, x1 = synth.shares(n, o.ell, o.lx, o.f, "D1", run=0)
-    for r in range(runs):  # run r draws fresh randomness: global indices r n + [0, n)
-        ref = B.relu(o, x0, x1, np.arange(n, dtype=np.uint64) + np.uint64(r * n), synth.seeds(0))
+    span = -(-n // 8) * 8
+    for r in range(runs):  # run r draws fresh randomness: global indices r span + [0, n)
+        ref = B.relu(o, x0, x1, np.arange(n, dtype=np.uint64) + np.uint64(r * span), synth.seeds(0))
         assert np.array_equal(np.load(tmp_path / f"y_0_{r}.npy"), ref["y0"])
         assert np.array_equal(np.load(tmp_path / f"y_1_{r}.npy"), ref["y1"])
 
@@ -95,11 +96,11 @@ def test_peer_runtime_gloo(tmp_path, kind, world, slots, mode, literal):
                                       str(tmp_path)), nprocs=world, join=True, start_method="spawn")
     o = B.Params(**CONFIGS[mode])
     ell, lx, f = o.ell, o.lx, o.f
-    k = world // 3
+    k, span = world // 3, -(-n // 8) * 8
     for t in range(k):
         x, x0, x1 = synth.shares(n, ell, lx, f, "D1", run=t)
         for r in range(runs):  # run r of triple t: global indices (r k + t) n + [0, n), disjoint over runs and triples
-            j = np.arange(n, dtype=np.uint64) + np.uint64((r * k + t) * n)
+            j = np.arange(n, dtype=np.uint64) + np.uint64((r * k + t) * span)
             ref = getattr(B, kind)(o, x0, x1, j, synth.seeds(0))
             assert np.array_equal(np.load(tmp_path / f"y_{3 * t}_{r}.npy"), ref["y0"]), (t, r)
             assert np.array_equal(np.load(tmp_path / f"y_{3 * t + 1}_{r}.npy"), ref["y1"]), (t, r)
