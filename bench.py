@@ -88,6 +88,16 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "src": "fallback"}
 
 
+def load_alu_ops():
+    """Executed ALU-pipe thread instructions per element per op (tools/alu_ops_json.py from the
+    committed ncu source-level SASS mix), or {}."""
+    p = os.path.join(ROOT, "profiles", "ncu_alu_ops.json")
+    try:
+        return json.load(open(p)) if os.path.exists(p) else {}
+    except Exception:
+        return {}
+
+
 def load_traffic():
     """Per-launch DRAM bytes from the committed ncu --set full capture (or None)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -398,6 +408,7 @@ def run_cuda(a):
     value = world * n / (ms * 1e-3)
     peaks = load_peaks()
     traffic = load_traffic()
+    alu_ops = load_alu_ops()
     clk_mhz = peaks["sm_max_mhz"]
     # ALU pipe (LOP3/SHF/PRMT/IADD3): 1 warp instruction per 2 clk per SMSP = 16 lanes/clk/SMSP
     sms = torch.cuda.get_device_properties(dev).multi_processor_count or SM_COUNT_B200
@@ -421,6 +432,12 @@ def run_cuda(a):
         tr = traffic.get(kind)
         out["traffic"] = tr
         out["launch_ms"] = launch_ms
+        out["hbm_frac"] = out["hbm"]["frac"]
+        ex = alu_ops.get(kind)
+        if ex and out["bound"] == "alu":  # every ALU-pipe instruction the kernel executes (ncu), not just ChaCha's
+            ach_ex = elems_per_s / max(world, 1) * ex / 1e12
+            out.update({"alu_ops_per_elem_executed": ex, "alu_achieved_executed": ach_ex,
+                        "alu_frac_executed": ach_ex / alu_peak, "alu_ops_source": alu_ops.get("_source")})
         return out
 
     line = {
@@ -434,6 +451,18 @@ def run_cuda(a):
     }
 
     if not a.no_extras:
+        # ---- the headline kernel with BOTH parties' messages reduced to wire values (P2 adds W0 + W1
+        # in [0, 257), as the transcript path and the party kernels do); the headline reduces P0's
+        # and tests it against P1's congruent message (BC_MATERIALIZE) ----
+        os.environ["BICOPTOR_MATERIALIZE"] = "2"
+        try:
+            t_m2, _, _ = timed(step, max(a.steps // 2, 5), 3)
+        finally:
+            del os.environ["BICOPTOR_MATERIALIZE"]
+        ms_m2 = t_m2 / max(a.steps // 2, 5)
+        line["materialize2"] = {"value": world * n / (ms_m2 * 1e-3), "unit": "elements/s", "ms_per_step": ms_m2,
+                                "note": "same kernel, both wire values W0, W1 in [0, 257) formed per slot and added "
+                                        "by P2 (env BICOPTOR_MATERIALIZE=2); results identical"}
         # ---- ReLU (Alg 8) on the same batch ------------------------------------
         t_ms_r, _, _ = timed(lambda: api.relu(x0, x1, prm, seeds, base, y0, y1, stream=stream),
                              max(a.steps // 2, 5), 3)

@@ -86,6 +86,14 @@ __device__ __noinline__ FbC fallback_c(FbC d, uint64_t j, Key key) {
   if (d.w2 >= RHO_WORD_LIMIT) { uint32_t v = fb.next(); while (v >= RHO_WORD_LIMIT) v = fb.next(); d.w2 = v; }
   return d;
 }
+// The same with the key passed by address: the table kernels take their keys as
+// __grid_constant__ parameters, so &key points into the parameter bank and the eight key
+// words are read inside this rare path instead of being loaded before every element's
+// branch (ptxas hoisted those LDCs: ~10 issue slots per element).
+template <int R>
+__device__ __noinline__ FbC fallback_c(FbC d, uint64_t j, const Key* key) {
+  return fallback_c<R>(d, j, *key);
+}
 
 // Compact tape (24 B): T0 = t | perm index, T1, T2 = mask bytes, reshare words
 // w0 = T3 (part A), w1, w2 = T4, T5 (part B) holding rho_0..7 as base-257 digits.
@@ -419,7 +427,7 @@ __device__ __forceinline__ uint32_t decode_t2(uint32_t T0, uint32_t w0, uint32_t
   return ix;
 }
 
-template <bool KEEP_W, bool FHI>
+template <bool KEEP_W, bool FHI, int MAT = BC_MATERIALIZE>
 __device__ __forceinline__ uint32_t elem_both_t2(uint64_t x0, uint64_t x1, uint32_t t, uint32_t ix, const uint32_t (&rb)[2],
                                                  const uint32_t (&o0)[8], const uint32_t (&o1)[8], uint32_t sbase,
                                                  uint32_t fsh, uint32_t one, uint32_t (&W0)[8], uint32_t (&W1)[8]) {
@@ -449,13 +457,13 @@ __device__ __forceinline__ uint32_t elem_both_t2(uint64_t x0, uint64_t x1, uint3
     const uint32_t d1 = __dp4a(m < 4 ? D_lo : D_hi, unit, 1u);        // v'_m (P1)
     const uint32_t xm0 = c1 * r + o0[m];                              // == W0_m (mod 257)
     const uint32_t xm1 = d1 * r + o1[m];                              // == W1_m (mod 257)
-    if (KEEP_W || BC_MATERIALIZE == 2) {
+    if (KEEP_W || MAT == 2) {
       W0[m] = mod257s(xm0);
       W1[m] = mod257s(xm1);
       vmin = min(vmin, add_fma(W0[m], W1[m], one) * 0xFF00FF01u);
-    } else if (BC_MATERIALIZE == 1 && !BC_P2_DIST) {
+    } else if (MAT == 1 && !BC_P2_DIST) {
       vmin = min(vmin, add_fma(mod257s(xm0), xm1, one) * 0xFF00FF01u);
-    } else if (BC_MATERIALIZE == 1) {
+    } else if (MAT == 1) {
       // P0 reduces its message: W0 = xm0 - 257 q0 with q0 = xm0 div 257 (xm0 < 2^24: div257s
       // exact).  P2 tests 257 | (W0 + x1) multiplicatively; since 257 * 257^-1 = 1 (mod 2^32),
       // (W0 + x1) 257^-1 = xm0 257^-1 + x1 257^-1 - q0 (mod 2^32): the same value, two IMADs
@@ -490,7 +498,7 @@ __device__ __forceinline__ uint32_t decode_pl(const uint32_t* T, uint64_t j, con
   }
   if (__builtin_expect((d.idx >= kp.perm_lim) | (mx >= kp.pair_lim), 0)) {
     Draws f = d;
-    fallback<R>(f, j, k01, 8u, kp.perm_lim, kp.pair_lim, 1u, 0x0FFFFFFFu);
+    fallback<R>(f, j, &k01, 8u, kp.perm_lim, kp.pair_lim, 1u, 0x0FFFFFFFu);
     d = f;
   }
 #pragma unroll

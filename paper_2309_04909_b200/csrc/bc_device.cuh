@@ -141,19 +141,27 @@ struct KeyPre {
   uint32_t k[8];
   uint32_t l0, l1;
   uint32_t c[8];  // x2, x6, x10, x14, x3, x7, x11, x15 after the first column round
+  uint32_t c1[4]; // x1, x5, x9, x13 after it when the counter's high word x13 is 0 (chacha_pre<R, true>)
 };
 
-template <int R>
+// HI0: every counter of the launch is below 2^32 (chosen on the host from elem_base + n), so
+// column 1 of the first round (x1, x5, x9, x13 = 0) is precomputed too: one quarter round left.
+template <int R, bool HI0 = false, int UNR = kChachaUnroll>
 __device__ __forceinline__ void chacha_pre(const KeyPre& P, uint64_t ctr, uint32_t (&o)[16]) {
   uint32_t x0 = 0x61707865u, x1 = 0x3320646eu;
   uint32_t x4 = P.k[0], x5 = P.k[1], x8 = P.k[4], x9 = P.k[5];
-  const uint32_t c0 = (uint32_t)ctr, c1 = (uint32_t)(ctr >> 32);
+  const uint32_t c0 = (uint32_t)ctr, c1 = HI0 ? 0u : (uint32_t)(ctr >> 32);
   uint32_t x12 = c0, x13 = c1;
-  BC_QR_ALU(x0, x4, x8, x12) BC_QR_ALU(x1, x5, x9, x13)
+  if (HI0) {
+    x1 = P.c1[0]; x5 = P.c1[1]; x9 = P.c1[2]; x13 = P.c1[3];
+    BC_QR_ALU(x0, x4, x8, x12)
+  } else {
+    BC_QR_ALU(x0, x4, x8, x12) BC_QR_ALU(x1, x5, x9, x13)
+  }
   uint32_t x2 = P.c[0], x6 = P.c[1], x10 = P.c[2], x14 = P.c[3];
   uint32_t x3 = P.c[4], x7 = P.c[5], x11 = P.c[6], x15 = P.c[7];
   BC_QR_ALU(x0, x5, x10, x15) BC_QR_ALU(x1, x6, x11, x12) BC_QR_ALU(x2, x7, x8, x13) BC_QR_ALU(x3, x4, x9, x14)
-#pragma unroll kChachaUnroll
+#pragma unroll UNR
   for (int r = 2; r < R; r += 2) {
     BC_QR_ALU(x0, x4, x8, x12) BC_QR_ALU(x1, x5, x9, x13) BC_QR_ALU(x2, x6, x10, x14) BC_QR_ALU(x3, x7, x11, x15)
     BC_QR_ALU(x0, x5, x10, x15) BC_QR_ALU(x1, x6, x11, x12) BC_QR_ALU(x2, x7, x8, x13) BC_QR_ALU(x3, x4, x9, x14)
@@ -257,6 +265,11 @@ __device__ __noinline__ void fallback(Draws& d, uint64_t j, Key key, uint32_t S,
       while (v >= rho_lim) v = fb.next() & dmask;
       d.ur[m] = v;
     }
+}
+template <int R>
+__device__ __noinline__ void fallback(Draws& d, uint64_t j, const Key* key, uint32_t S, uint32_t perm_lim,
+                                      uint32_t mask_lim, uint32_t rho_lim, uint32_t dmask) {
+  fallback<R>(d, j, *key, S, perm_lim, mask_lim, rho_lim, dmask);  // key by address (__grid_constant__ params)
 }
 
 // ---------------------------------------------------------------------------

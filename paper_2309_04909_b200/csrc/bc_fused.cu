@@ -4,6 +4,8 @@
 // and reshare (steps 9-10) and the finish (step 11, or Alg 8's Beaver
 // combine) per element, with no HBM round trip for the messages: per element
 // 16 B of input shares are read and 16 B of output shares written.
+#include <cstdlib>
+
 #include "bc_common.cuh"
 
 using namespace bc;
@@ -28,15 +30,18 @@ struct PreKeys {
 #ifndef BC_CHACHA_PRE
 #define BC_CHACHA_PRE 1
 #endif
+#ifndef BC_RELU_PRE
+#define BC_RELU_PRE 0  // the ReLU table kernel's blocks with the first-round precomputation too
+#endif
 // PRE: use the precomputation at this call site.  Measured (tools/variants.py):
 // DReLU 0.490 -> 0.484 ms / 2^24; ReLU 0.860 -> 0.880 (the peeled first double
 // round at its seven call sites costs more instruction cache than it saves), so
 // the ReLU kernels keep the plain block function.
-template <int R, bool PRE>
+template <int R, bool PRE, bool HI0 = false>
 __device__ __forceinline__ void stream_blk(const KeyPre& P, const Key& k, uint64_t label, uint64_t ctr,
                                            uint32_t (&o)[16]) {
   if (PRE && BC_CHACHA_PRE)
-    chacha_pre<R>(P, ctr, o);
+    chacha_pre<R, HI0>(P, ctr, o);
   else
     chacha<R>(k, ctr, label, o);
 }
@@ -45,7 +50,7 @@ __device__ __forceinline__ void stream_blk(const KeyPre& P, const Key& k, uint64
 // FULL (ell = 64): every value is already reduced mod 2^ell, the masks fold away.
 // The sign (1 - 2t) is applied as a 64-bit multiply (FMA pipe) rather than as
 // negate-and-select (ALU pipe, which the ChaCha rounds saturate).
-template <int R, bool RELU, bool FULL>
+template <int R, bool RELU, bool FULL, bool HI0 = false>
 __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, const Key& k02, const Key& k12,
                                              const PreKeys& pk, uint64_t i0, uint64_t j0, uint32_t cnt,
                                              uint32_t zbits, uint32_t tbits) {
@@ -54,7 +59,7 @@ __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, c
   if (!RELU) {
     // Alg 7 step 10: P2 reshares DReLU' ([D']_0 from seed02); step 11: P0/P1 unblind.
     uint32_t Q[16];
-    stream_blk<R, true>(pk.resp, k02, L_RESP, j0 >> 3, Q);
+    stream_blk<R, true, HI0>(pk.resp, k02, L_RESP, j0 >> 3, Q);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const uint64_t z = (zbits >> e) & 1u, t = (tbits >> e) & 1u;
@@ -68,10 +73,10 @@ __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, c
     uint64_t b0[8], b1[8], ev[8];
     {
       uint32_t Bk[16];
-      stream_blk<R, false>(pk.b02, k02, L_B02, j0 >> 3, Bk);
+      stream_blk<R, BC_RELU_PRE != 0, HI0>(pk.b02, k02, L_B02, j0 >> 3, Bk);
 #pragma unroll
       for (int e = 0; e < 8; ++e) b0[e] = u64_of(Bk, e);
-      stream_blk<R, false>(pk.b12, k12, L_B12, j0 >> 3, Bk);
+      stream_blk<R, BC_RELU_PRE != 0, HI0>(pk.b12, k12, L_B12, j0 >> 3, Bk);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         b1[e] = u64_of(Bk, e);
@@ -80,8 +85,8 @@ __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, c
     }
     {
       uint32_t Ak0[16], Ak1[16];
-      stream_blk<R, false>(pk.a02, k02, L_A02, j0 >> 3, Ak0);
-      stream_blk<R, false>(pk.a12, k12, L_A12, j0 >> 3, Ak1);
+      stream_blk<R, BC_RELU_PRE != 0, HI0>(pk.a02, k02, L_A02, j0 >> 3, Ak0);
+      stream_blk<R, BC_RELU_PRE != 0, HI0>(pk.a12, k12, L_A12, j0 >> 3, Ak1);
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
         const ulonglong2 v0 = load2(a.x0, i0 + 2 * h, a.n), v1 = load2(a.x1, i0 + 2 * h, a.n);
@@ -97,7 +102,7 @@ __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, c
     }
     {
       uint32_t Ck[16];
-      stream_blk<R, false>(pk.c02, k02, L_C02, j0 >> 3, Ck);
+      stream_blk<R, BC_RELU_PRE != 0, HI0>(pk.c02, k02, L_C02, j0 >> 3, Ck);
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
         const ulonglong2 v0 = load2(a.x0, i0 + 2 * h, a.n), v1 = load2(a.x1, i0 + 2 * h, a.n);
@@ -189,8 +194,8 @@ __device__ __forceinline__ void load_tables(uint32_t* s) {
   for (int i = threadIdx.x; i < kTabWords / 4; i += blockDim.x) d[i] = g[i];
 }
 
-template <int R, bool RELU, bool TRANSCRIPT, bool FULL, bool FHI>
-__global__ void __launch_bounds__(TPB_T, 1) k_fused_t(FusedArgs a, KP kp, Key k01, Key k02, Key k12, PreKeys pk) {
+template <int R, bool RELU, bool TRANSCRIPT, bool FULL, bool FHI, int MAT = BC_MATERIALIZE, bool HI0 = false>
+__global__ void __launch_bounds__(TPB_T, 1) k_fused_t(FusedArgs a, KP kp, const __grid_constant__ Key k01, Key k02, Key k12, PreKeys pk) {
   extern __shared__ uint4 smem_t[];
   uint32_t* tabs = reinterpret_cast<uint32_t*>(smem_t);
   load_tables(tabs);
@@ -203,14 +208,14 @@ __global__ void __launch_bounds__(TPB_T, 1) k_fused_t(FusedArgs a, KP kp, Key k0
     const uint32_t cnt = (uint32_t)min((uint64_t)8, a.n - i0);
     uint32_t zbits = 0, tbits = 0;
     uint32_t Bp[16];  // part B: words 2e, 2e+1 of element e (reshare words w1, w2)
-    stream_blk<R, !RELU>(pk.tpb, k01, L_TAPEB, j0 >> 3, Bp);
+    stream_blk<R, !RELU || BC_RELU_PRE, HI0>(pk.tpb, k01, L_TAPEB, j0 >> 3, Bp);
 #pragma unroll 1
     for (int hb = 0; hb < 2; ++hb) {
       const uint64_t ib = i0 + 4 * hb;
       const ulonglong2 u0 = load2(a.x0, ib, a.n), u1 = load2(a.x1, ib, a.n);
       const ulonglong2 v0 = load2(a.x0, ib + 2, a.n), v1 = load2(a.x1, ib + 2, a.n);
       uint32_t A[16];  // part A: words 4q..4q+3 of element 4 hb + q
-      stream_blk<R, !RELU>(pk.tpa, k01, L_TAPEA, (j0 >> 2) + (uint64_t)hb, A);
+      stream_blk<R, !RELU || BC_RELU_PRE, HI0>(pk.tpa, k01, L_TAPEA, (j0 >> 2) + (uint64_t)hb, A);
       const uint32_t bit0 = 1u << (4 * hb);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -224,7 +229,7 @@ __global__ void __launch_bounds__(TPB_T, 1) k_fused_t(FusedArgs a, KP kp, Key k0
 #if BC_TBL_V2
         uint32_t o0[8], o1[8];
         const uint32_t ix = decode_t2<R>(T0, A[4 * q + 3], Bp[2 * q], Bp[2 * q + 1], j0 + (uint64_t)e, k01, o0, o1);
-        const uint32_t z = elem_both_t2<TRANSCRIPT, FHI>(xa, xb, t, ix, rb, o0, o1, sbase, kp.fsh, kp.one, W0, W1);
+        const uint32_t z = elem_both_t2<TRANSCRIPT, FHI, MAT>(xa, xb, t, ix, rb, o0, o1, sbase, kp.fsh, kp.one, W0, W1);
 #else
         uint32_t rho[8];
         const uint32_t ix = decode_t<R>(T0, A[4 * q + 3], Bp[2 * q], Bp[2 * q + 1], j0 + (uint64_t)e, k01, rho);
@@ -243,7 +248,7 @@ __global__ void __launch_bounds__(TPB_T, 1) k_fused_t(FusedArgs a, KP kp, Key k0
 #pragma unroll
       for (int k = 0; k < 8; ++k) Bp[k] = Bp[k + 8];  // elements 4..7 next
     }
-    finish_group<R, RELU, FULL>(a, kp, k02, k12, pk, i0, j0, cnt, zbits, tbits);
+    finish_group<R, RELU, FULL, HI0>(a, kp, k02, k12, pk, i0, j0, cnt, zbits, tbits);
   }
 }
 
@@ -256,8 +261,8 @@ __global__ void __launch_bounds__(TPB_T, 1) k_fused_t(FusedArgs a, KP kp, Key k0
 constexpr size_t kLitTabBytes = sizeof(uint32_t) * kLitTabWords;
 __device__ constexpr LiteralTables kLitTables{};
 
-template <int R, bool RELU, bool TRANSCRIPT, bool FULL, bool FHI>
-__global__ void __launch_bounds__(TPB_T, 1) k_fused_tl(FusedArgs a, KP kp_, Key k01, Key k02, Key k12, PreKeys pk) {
+template <int R, bool RELU, bool TRANSCRIPT, bool FULL, bool FHI, bool HI0 = false>
+__global__ void __launch_bounds__(TPB_T, 1) k_fused_tl(FusedArgs a, KP kp_, const __grid_constant__ Key k01, Key k02, Key k12, PreKeys pk) {
   const KP kp = kp_literal(kp_);
   extern __shared__ uint4 smem_t[];
   {
@@ -275,7 +280,7 @@ __global__ void __launch_bounds__(TPB_T, 1) k_fused_tl(FusedArgs a, KP kp_, Key 
 #pragma unroll 1
     for (int e2 = 0; e2 < 8; e2 += 2) {  // one seed01 block holds elements e2, e2 + 1 (j0 is a multiple of 8)
       uint32_t B[16];
-      stream_blk<R, !RELU>(pk.tpa, k01, L_TAPEP, (j0 + (uint64_t)e2) >> 1, B);  // pk.tpa: bc2.tpp1
+      stream_blk<R, !RELU || BC_RELU_PRE, HI0>(pk.tpa, k01, L_TAPEP, (j0 + (uint64_t)e2) >> 1, B);  // bc2.tpp1
       const ulonglong2 u0 = load2(a.x0, i0 + e2, a.n), u1 = load2(a.x1, i0 + e2, a.n);
       const uint32_t bit0 = 1u << e2;
 #pragma unroll
@@ -297,7 +302,7 @@ __global__ void __launch_bounds__(TPB_T, 1) k_fused_tl(FusedArgs a, KP kp_, Key 
         tbits = t * bit + tbits;
       }
     }
-    finish_group<R, RELU, FULL>(a, kp, k02, k12, pk, i0, j0, cnt, zbits, tbits);
+    finish_group<R, RELU, FULL, HI0>(a, kp, k02, k12, pk, i0, j0, cnt, zbits, tbits);
   }
 }
 
@@ -472,6 +477,16 @@ __global__ void __launch_bounds__(TPB_L) k_fused_b1(FusedArgs a, KP kp, Key k01,
   }
 }
 
+// BICOPTOR_MATERIALIZE=2 in the environment (a measurement knob, read per call; bench.py's
+// "materialize2" leg): the compact table kernel at ell = 64 reduces BOTH computing parties'
+// messages to their wire values W in [0, 257) and P2 adds wire values, as the transcript
+// path and the party kernels do, instead of testing P0's W0 + P1's
+// congruent x1.  Same results; this times the difference.
+bool wire_values_mode() {
+  const char* e = std::getenv("BICOPTOR_MATERIALIZE");
+  return e && e[0] == '2';
+}
+
 template <bool RELU>
 int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, size_t n, uint64_t base,
           const bc_params* prm, const bc_seeds* seeds, const bc_transcript* tr, void* stream) {
@@ -525,6 +540,15 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
       auto fn = tr ? (fhi ? k_fused_t<R, RELU, true, false, true> : k_fused_t<R, RELU, true, false, false>)
                    : prm->ell == 64 ? (fhi ? k_fused_t<R, RELU, false, true, true> : k_fused_t<R, RELU, false, true, false>)
                                     : (fhi ? k_fused_t<R, RELU, false, false, true> : k_fused_t<R, RELU, false, false, false>);
+      if (!tr && prm->ell == 64 && !fhi) {
+        // every keystream counter below 2^32 (part A: j/4, part B and the response: j/8): the
+        // first round's column 1 is precomputed on the host as well (chacha_pre<R, true>)
+        const bool hi0 = base + n <= (1ull << 34);
+        if (wire_values_mode())  // measurement knob: both wire values reduced
+          fn = hi0 ? k_fused_t<R, RELU, false, true, false, 2, true> : k_fused_t<R, RELU, false, true, false, 2>;
+        else if (hi0)
+          fn = k_fused_t<R, RELU, false, true, false, BC_MATERIALIZE, true>;
+      }
       const int rc = allow_smem((const void*)fn, kTabBytes);
       if (rc) return rc;
       fn<<<grid_for((const void*)fn, ngroups, TPB_T, kTabBytes), TPB_T, kTabBytes, st>>>(a, kp, k01, k02, k12, pk);
@@ -537,6 +561,8 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
       auto fn = tr ? (fhi ? k_fused_tl<R, RELU, true, false, true> : k_fused_tl<R, RELU, true, false, false>)
                    : prm->ell == 64 ? (fhi ? k_fused_tl<R, RELU, false, true, true> : k_fused_tl<R, RELU, false, true, false>)
                                     : (fhi ? k_fused_tl<R, RELU, false, false, true> : k_fused_tl<R, RELU, false, false, false>);
+      if (!tr && prm->ell == 64 && !fhi && base + n <= (1ull << 33))  // pair-tape counters j/2 below 2^32
+        fn = k_fused_tl<R, RELU, false, true, false, true>;
       const int rc = allow_smem((const void*)fn, kLitTabBytes);
       if (rc) return rc;
       fn<<<grid_for((const void*)fn, ngroups, TPB_T, kLitTabBytes), TPB_T, kLitTabBytes, st>>>(a, kp, k01, k02, k12, pk);

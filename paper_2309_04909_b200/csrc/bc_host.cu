@@ -196,6 +196,10 @@ KeyPre make_keypre(const uint8_t* s, uint64_t label) {
   qr(x3, x7, x11, x15);
   const uint32_t c[8] = {x2, x6, x10, x14, x3, x7, x11, x15};
   std::memcpy(p.c, c, sizeof c);
+  uint32_t x1 = 0x3320646eu, x5 = p.k[1], x9 = p.k[5], x13 = 0u;  // column 1 with a zero counter high word
+  qr(x1, x5, x9, x13);
+  const uint32_t c1[4] = {x1, x5, x9, x13};
+  std::memcpy(p.c1, c1, sizeof c1);
   return p;
 }
 

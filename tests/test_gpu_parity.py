@@ -311,6 +311,20 @@ def test_config3_full_size_exact(api, fn, kw):
     assert bad.size == 0, f"{bad.size} of {n} elements differ, first at {bad[:8]}"
 
 
+@pytest.mark.parametrize("fn", ["drelu", "relu"])
+def test_materialize2_knob_same_results(api, fn, monkeypatch):
+    """BICOPTOR_MATERIALIZE=2 (bench.py's materialize2 leg: both parties' wire values
+    reduced, P2 adds W0 + W1) runs another instantiation of the headline kernel; its
+    outputs equal the oracle's (Alg 7 step 9)."""
+    kw = PARAMS[0]
+    n = 40003
+    x, x0, x1 = synth.shares(n, 64, 7, 24, "D2", run=3)
+    monkeypatch.setenv("BICOPTOR_MATERIALIZE", "2")
+    y0, y1 = getattr(api, fn)(dev(x0), dev(x1), api.Params(**kw), SEEDS, elem_base=64)
+    ref = getattr(B, fn)(B.Params(**kw), x0, x1, np.arange(n, dtype=np.uint64) + np.uint64(64), SEEDS)
+    assert np.array_equal(host(y0), ref["y0"]) and np.array_equal(host(y1), ref["y1"])
+
+
 def test_config2_ladder_full_size_exact(api):
     """Config 2 (Alg 7 steps 3-5 alone, ell=64, f=24, guard, 2^28 elements, one
     call as the bench times it): every one of the 2^28 x 8 output bytes of both

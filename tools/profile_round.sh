@@ -24,5 +24,7 @@ for r in $out/prof_*.ncu-rep; do
   op=$(basename $r .ncu-rep); op=${op#prof_}
   python tools/sass_mix.py $r $((1<<24)) --top 30 > $out/summary/${tag}_${op}_sass_mix.txt 2>&1
 done
+# per-instruction source view of the headline kernel (stall samples, executed counts) for offline reading
+ncu -i $out/prof_drelu.ncu-rep --page source --csv --print-source sass > $out/summary/${tag}_drelu_source.csv 2>&1
 rm -f $out/prof_*.ncu-rep
 ls -la $out $out/summary
