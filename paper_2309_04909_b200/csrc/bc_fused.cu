@@ -31,7 +31,7 @@ struct PreKeys {
 #define BC_CHACHA_PRE 1
 #endif
 #ifndef BC_RELU_PRE
-#define BC_RELU_PRE 0  // the ReLU table kernel's blocks with the first-round precomputation too
+#define BC_RELU_PRE 1  // the ReLU table kernel's blocks with the first-round precomputation too
 #endif
 // PRE: use the precomputation at this call site.  Measured (tools/variants.py):
 // DReLU 0.490 -> 0.484 ms / 2^24; ReLU 0.860 -> 0.880 (the peeled first double
@@ -348,18 +348,22 @@ __global__ void __launch_bounds__(TPB, 2) k_fused_w(FusedArgs a, KP kp_, Key k01
 // Large tape (lx >= 8, up to 32 slots, p < 2^33): 7 seed01 blocks per element (bc2.tpL2),
 // the 8 elements of a group in sequence, then the shared finish.
 constexpr int TPB_L = TPB_LARGE;
+#ifndef BC_LARGE_PRE
+#define BC_LARGE_PRE 1  // the large tape's 7 blocks through chacha_pre (pk.tpa = (seed01, bc2.tpL2))
+#endif
 #ifndef BC_LARGE_MINB
 #define BC_LARGE_MINB 1  // resident CTAs per SM the large-tape kernel is compiled for (register cap)
 #endif
 
-template <int R, bool RELU, bool TRANSCRIPT>
-__global__ void __launch_bounds__(TPB_L, BC_LARGE_MINB) k_fused_l(FusedArgs a, KP kp, KPL kl, Key k01, Key k02, Key k12, PreKeys pk) {
-  __shared__ uint8_t sidx[32 * TPB_L];
+template <int R, bool RELU, bool TRANSCRIPT, bool HI0 = false>
+__global__ void __launch_bounds__(TPB_L, BC_LARGE_MINB) k_fused_l(FusedArgs a, KP kp, KPL kl, Key k01, Key k02, Key k12,
+                                                                  const __grid_constant__ PreKeys pk) {
+  __shared__ LargeIdx sidx[32 * TPB_L];
   __shared__ uint32_t sstg[LARGE_STG_ROWS * TPB_L];
   __shared__ uint32_t magic[33], hlim[33];
   large_tables(magic, hlim);
   __syncthreads();
-  uint8_t* idx = sidx + threadIdx.x;
+  LargeIdx* idx = sidx + threadIdx.x;
   uint32_t* stg = sstg + threadIdx.x;
   const uint64_t ngroups = (a.n + 7) >> 3;
   for (uint64_t g = (uint64_t)blockIdx.x * TPB_L + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB_L) {
@@ -373,7 +377,8 @@ __global__ void __launch_bounds__(TPB_L, BC_LARGE_MINB) k_fused_l(FusedArgs a, K
       uint64_t* w0 = TRANSCRIPT ? reinterpret_cast<uint64_t*>(a.w0lo) + i * kl.S : nullptr;
       uint64_t* w1 = TRANSCRIPT ? reinterpret_cast<uint64_t*>(a.w1lo) + i * kl.S : nullptr;
       const uint32_t r =
-          elem_large<R, TRANSCRIPT, TPB_L>(__ldg(a.x0 + i), __ldg(a.x1 + i), j0 + e, k01, kl, idx, stg, magic, hlim, w0, w1);
+          elem_large<R, TRANSCRIPT, TPB_L, BC_LARGE_PRE != 0, HI0>(__ldg(a.x0 + i), __ldg(a.x1 + i), j0 + e, k01, kl, idx,
+                                                                    stg, magic, hlim, w0, w1, &pk.tpa);
       zbits |= (r & 1u) << e;
       tbits |= (r >> 1) << e;
     }
@@ -522,7 +527,7 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
   }
   const KP kp = make_kp(prm);
   const Key k01 = make_key(seeds->s01), k02 = make_key(seeds->s02), k12 = make_key(seeds->s12);
-  const uint64_t tape_a = prm->tape == BC_TAPE_COMPACT ? L_TAPEA : L_TAPEP;  // the stream the tape kernel reads
+  const uint64_t tape_a = prm->tape == BC_TAPE_COMPACT ? L_TAPEA : prm->tape == BC_TAPE_LARGE ? L_TAPEL : L_TAPEP;
   const PreKeys pk{make_keypre(seeds->s01, tape_a), make_keypre(seeds->s01, L_TAPEB),
                    make_keypre(seeds->s02, L_RESP),  make_keypre(seeds->s02, L_A02),
                    make_keypre(seeds->s02, L_B02),   make_keypre(seeds->s02, L_C02),
@@ -534,6 +539,8 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
     if (large) {
       const KPL kl = make_kpl(prm);
       auto fn = tr ? k_fused_l<R, RELU, true> : k_fused_l<R, RELU, false>;
+      if (!tr && base + n <= (1ull << 32) / 7)  // every tape counter 7j + b below 2^32
+        fn = k_fused_l<R, RELU, false, true>;
       fn<<<grid_for((const void*)fn, ngroups, TPB_L), TPB_L, 0, st>>>(a, kp, kl, k01, k02, k12, pk);
     } else if (prm->tape == BC_TAPE_COMPACT && BC_FUSED_TABLES) {
       const bool fhi = kp.fhi != 0;

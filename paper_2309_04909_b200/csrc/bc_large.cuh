@@ -9,8 +9,8 @@
 //               is its Montgomery form), then 8 reshares (u -> rho_m = u mod p),
 // streamed 3 blocks (two slot groups) at a time through shared memory.
 // Arithmetic mod p: one Montgomery product (R = 2^64) per party and slot,
-// W = REDC(v' rM) = v' r; Barrett reductions for the draws.  The permutation
-// is a byte table per thread in shared memory ([slot][thread]) and is applied
+// W = REDC(v' rM) = v' r; binary64 quotients for the draws.  The permutation
+// is a word table per thread in shared memory ([slot][thread]) and is applied
 // by evaluating slot m's source window v'_{Pi(m)} directly from the share.
 #pragma once
 #include <cstdint>
@@ -117,6 +117,18 @@ __device__ __forceinline__ void slot_values(uint64_t s0f, uint64_t n1f, uint32_t
 
 constexpr int TPB_LARGE = 128;  // threads per CTA of the large-tape kernels (shared tables are [32][TPB_LARGE])
 
+// The per-thread permutation table: 32-bit entries ([slot][thread] words: thread t's column sits
+// in bank t mod 32, so the Fisher-Yates swaps at random slots are conflict-free; byte entries put
+// four threads' columns in one bank word and the random-row swaps conflicted 4-way).
+#ifndef BC_LARGE_IDX32
+#define BC_LARGE_IDX32 1
+#endif
+#if BC_LARGE_IDX32
+typedef uint32_t LargeIdx;
+#else
+typedef uint8_t LargeIdx;
+#endif
+
 // Per-CTA constant tables of the Fisher-Yates draws: magic[s] = ceil(2^32 / s),
 // hlim[s] = floor(2^16 / s) s (the u16 rejection limit), s = 2..32.
 __device__ __forceinline__ void large_tables(uint32_t* magic, uint32_t* hlim) {
@@ -127,25 +139,36 @@ __device__ __forceinline__ void large_tables(uint32_t* magic, uint32_t* hlim) {
 }
 
 // Block 0 of element j's tape: t and step 6's Fisher-Yates permutation into
-// this thread's idx column.  idx: this thread's column of a [32][TPB_L] byte
-// table; stg: its column of a [32][TPB_L] word table (keystream staging, so the
+// this thread's idx column.  idx: this thread's column of a [32][TPB_L]
+// LargeIdx table; stg: its column of a [32][TPB_L] word table (keystream staging, so the
 // Fisher-Yates and slot loops stay rolled: the kernel must fit the instruction
 // cache).  magic[s] = ceil(2^32 / s), hlim[s] = floor(2^16 / s) s.  fbc counts
 // the fallback words consumed.  Returns t.
-template <int R, int TPB_L>
-__device__ __forceinline__ uint32_t large_perm(uint64_t j, const Key& k01, const KPL& kp, uint8_t* idx, uint32_t* stg,
-                                               const uint32_t* magic, const uint32_t* hlim, uint32_t& fbc) {
+// PRE: the tape blocks through chacha_pre (pre = the (seed01, bc2.tpL2) precomputation; HI0: every
+// counter 7j + b of the launch below 2^32).
+template <int R, int TPB_L, bool PRE = false, bool HI0 = false>
+__device__ __forceinline__ void large_block(const Key& k01, const KeyPre* pre, uint64_t ctr, uint32_t (&B)[16]) {
+  if (PRE)
+    chacha_pre<R, HI0>(*pre, ctr, B);
+  else
+    chacha<R>(k01, ctr, L_TAPEL, B);
+}
+
+template <int R, int TPB_L, bool PRE = false, bool HI0 = false>
+__device__ __forceinline__ uint32_t large_perm(uint64_t j, const Key& k01, const KPL& kp, LargeIdx* idx, uint32_t* stg,
+                                               const uint32_t* magic, const uint32_t* hlim, uint32_t& fbc,
+                                               const KeyPre* pre = nullptr) {
   const uint32_t S = kp.S;
   uint32_t t;
   {
     uint32_t B[16];
-    chacha<R>(k01, j * 7, L_TAPEL, B);
+    large_block<R, TPB_L, PRE, HI0>(k01, pre, j * 7, B);
     t = B[0] & 1u;
 #pragma unroll
     for (int w = 0; w < 16; ++w) stg[w * TPB_L] = B[w];
   }
 #pragma unroll 4
-  for (uint32_t m = 0; m < 32; ++m) idx[m * TPB_L] = (uint8_t)m;
+  for (uint32_t m = 0; m < 32; ++m) idx[m * TPB_L] = (LargeIdx)m;
   // step 6: Fisher-Yates, slot m = S-1 .. 1 draws h[S-m]
 #pragma unroll 1
   for (uint32_t q = 1; q < S; ++q) {
@@ -153,7 +176,7 @@ __device__ __forceinline__ uint32_t large_perm(uint64_t j, const Key& k01, const
     uint32_t d = (stg[(q >> 1) * TPB_L] >> (16 * (q & 1))) & 0xFFFFu;
     while (d >= hlim[s]) d = (uint32_t)fbl_word<R>(k01, j, fbc++) & 0xFFFFu;
     const uint32_t k = d - __umulhi(d, magic[s]) * s;
-    const uint8_t a = idx[m * TPB_L], b = idx[k * TPB_L];
+    const LargeIdx a = idx[m * TPB_L], b = idx[k * TPB_L];
     idx[m * TPB_L] = b;
     idx[k * TPB_L] = a;
   }
@@ -193,12 +216,13 @@ __device__ __forceinline__ void large_draws(uint32_t m, uint64_t j, const Key& k
 }
 
 // Blocks 1 + 3h .. 3 + 3h (slot groups 2h, 2h + 1) into staged rows 0..47.
-template <int R, int TPB_L>
-__device__ __forceinline__ void large_stage(uint32_t h, uint64_t j, const Key& k01, uint32_t* stg) {
+template <int R, int TPB_L, bool PRE = false, bool HI0 = false>
+__device__ __forceinline__ void large_stage(uint32_t h, uint64_t j, const Key& k01, uint32_t* stg,
+                                            const KeyPre* pre = nullptr) {
 #pragma unroll 1
   for (uint32_t b = 0; b < 3; ++b) {
     uint32_t B[16];
-    chacha<R>(k01, j * 7 + 1 + 3 * h + b, L_TAPEL, B);
+    large_block<R, TPB_L, PRE, HI0>(k01, pre, j * 7 + 1 + 3 * h + b, B);
 #pragma unroll
     for (int w = 0; w < 16; ++w) stg[(16 * b + w) * TPB_L] = B[w];
   }
@@ -206,13 +230,14 @@ __device__ __forceinline__ void large_stage(uint32_t h, uint64_t j, const Key& k
 
 // Alg 7 steps 1-9 for element j with shares x0, x1 (both computing parties and
 // P2's zero test): returns DReLU' (bit 0) and t (bit 1).
-template <int R, bool TRANSCRIPT, int TPB_L>
+template <int R, bool TRANSCRIPT, int TPB_L, bool PRE = false, bool HI0 = false>
 __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_t j, const Key& k01, const KPL& kp,
-                                               uint8_t* idx, uint32_t* stg, const uint32_t* magic,
-                                               const uint32_t* hlim, uint64_t* w0, uint64_t* w1) {
+                                               LargeIdx* idx, uint32_t* stg, const uint32_t* magic,
+                                               const uint32_t* hlim, uint64_t* w0, uint64_t* w1,
+                                               const KeyPre* pre = nullptr) {
   const uint32_t S = kp.S;
   uint32_t fbc = 0;  // fallback words consumed
-  const uint32_t t = large_perm<R, TPB_L>(j, k01, kp, idx, stg, magic, hlim, fbc);
+  const uint32_t t = large_perm<R, TPB_L, PRE, HI0>(j, k01, kp, idx, stg, magic, hlim, fbc, pre);
   // steps 1-2: blind both shares by (-1)^t
   const uint64_t s0 = t ? (0ull - x0) & kp.ymask : x0 & kp.ymask;
   const uint64_t s1 = t ? (0ull - x1) & kp.ymask : x1 & kp.ymask;
@@ -220,7 +245,7 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
   uint32_t z = 0;
 #pragma unroll 1
   for (uint32_t h = 0; 16 * h < S; ++h) {
-    large_stage<R, TPB_L>(h, j, k01, stg);
+    large_stage<R, TPB_L, PRE, HI0>(h, j, k01, stg, pre);
     const uint32_t mend = min(S, 16 * h + 16);
 #pragma unroll kLargeSlotUnroll
     for (uint32_t m = 16 * h; m < mend; ++m) {
@@ -255,7 +280,7 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
 // Returns t in bit 32 of the result.
 template <int R, int PARTY, int TPB_L>
 __device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, const Key& k01, const KPL& kp,
-                                                     uint8_t* idx, uint32_t* stg, const uint32_t* magic,
+                                                     LargeIdx* idx, uint32_t* stg, const uint32_t* magic,
                                                      const uint32_t* hlim, uint32_t* lo, uint64_t stride) {
   const uint32_t S = kp.S;
   uint32_t fbc = 0;
