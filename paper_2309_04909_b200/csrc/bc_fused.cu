@@ -30,6 +30,9 @@ struct PreKeys {
 #ifndef BC_CHACHA_PRE
 #define BC_CHACHA_PRE 1
 #endif
+#ifndef BC_RELU_FUSED_ADDS
+#define BC_RELU_FUSED_ADDS 1
+#endif
 #ifndef BC_RELU_PRE
 #define BC_RELU_PRE 1  // the ReLU table kernel's blocks with the first-round precomputation too
 #endif
@@ -80,7 +83,12 @@ __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, c
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         b1[e] = u64_of(Bk, e);
+#if BC_RELU_FUSED_ADDS
+        b0[e] = b0[e] + b1[e];                        // b = [b]_0 + [b]_1 (P2), kept in place of [b]_0
+        ev[e] = ((zbits >> e) & 1u) - b0[e];          // P2: e = DReLU' - b
+#else
         ev[e] = ((zbits >> e) & 1u) - b0[e] - b1[e];  // P2: e = DReLU' - ([b]_0 + [b]_1)
+#endif
       }
     }
     {
@@ -94,9 +102,20 @@ __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, c
         for (int s = 0; s < 2; ++s) {
           const int e = 2 * h + s;
           const uint64_t a0 = u64_of(Ak0, e), a1 = u64_of(Ak1, e);
+#if BC_RELU_FUSED_ADDS
+          // the same sums with fewer separate 64-bit adds (ALU pipe, which ChaCha saturates): the
+          // products' addends fold into their multiply-adds (IMAD.WIDE chains, FMA pipe).
+          // b0 holds b = [b]_0 + [b]_1 (above); e + [b]_0 = DReLU' - [b]_1.
+          const uint64_t av = a0 + a1;                                         // a (P2)
+          const uint64_t d = ((s ? v0.y : v0.x) + (s ? v1.y : v1.x)) - av;     // opened d = x - a
+          const uint64_t zb1 = ((zbits >> e) & 1u) - b1[e];                    // e + [b]_0
+          y0[e] = d * zb1 + ev[e] * a0;                                        // P0: de + d[b]_0 + e[a]_0
+          y1[e] = d * b1[e] + (ev[e] * a1 + av * b0[e]);                       // P1: d[b]_1 + e[a]_1 + ab
+#else
           const uint64_t d = ((s ? v0.y : v0.x) - a0) + ((s ? v1.y : v1.x) - a1);  // opened d = x - a
           y0[e] = d * ev[e] + d * b0[e] + ev[e] * a0;                          // P0: de + d[b]_0 + e[a]_0
           y1[e] = d * b1[e] + ev[e] * a1 + (a0 + a1) * (b0[e] + b1[e]);        // P1: d[b]_1 + e[a]_1 + ab
+#endif
         }
       }
     }

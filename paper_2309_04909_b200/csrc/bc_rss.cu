@@ -46,8 +46,13 @@ struct RssArgs {
 
 struct RssKeys {
   Key k01, k02, k12, k012, k2;
+  KeyPre pre[NS_MAX];    // every preprocessing stream's (key, label) with chacha_pre's first-round columns
+  KeyPre tpa, tpb;       // the compact tape's two seed01 streams
 };
 
+#ifndef BC_RSS_PRE
+#define BC_RSS_PRE 1  // every block through chacha_pre at one call site (stream s selects K.pre[s])
+#endif
 template <int R>
 __device__ __forceinline__ void stream_block(const RssKeys& K, int s, uint64_t blk, uint32_t (&B)[16]) {
   switch (s) {
@@ -76,8 +81,8 @@ __device__ __forceinline__ void rss_mul(const uint64_t (&a)[3], const uint64_t (
   }
 }
 
-template <int R, bool RELU>
-__global__ void __launch_bounds__(TPB_RSS) k_fused_rss(RssArgs a, KP kp, RssKeys K) {
+template <int R, bool RELU, bool HI0 = false>
+__global__ void __launch_bounds__(TPB_RSS) k_fused_rss(RssArgs a, KP kp, const __grid_constant__ RssKeys K) {
   constexpr int NS = RELU ? 12 : 9;
   __shared__ uint32_t sA[2 * PERM_A], sB[2 * PERM_B];
   extern __shared__ uint32_t ks[];  // [NS][16][TPB_RSS]
@@ -94,21 +99,30 @@ __global__ void __launch_bounds__(TPB_RSS) k_fused_rss(RssArgs a, KP kp, RssKeys
 #pragma unroll 1
     for (int s = 0; s < NS; ++s) {
       uint32_t B[16];
-      stream_block<R>(K, s, j0 >> 3, B);
+      if (BC_RSS_PRE)
+        chacha_pre<R, HI0>(K.pre[s], j0 >> 3, B);  // s is warp-uniform: K.pre[s] is a uniform constant-bank read
+      else
+        stream_block<R>(K, s, j0 >> 3, B);
 #pragma unroll
       for (int w = 0; w < 16; ++w) ks[(s * 16 + w) * TPB_RSS + tid] = B[w];
     }
     // ---- 2. Alg 7 steps 1-9 on the bridged sharing (P0: x_0 + x_1, P1: x_2) ---
     uint32_t zbits = 0, tbits = 0;
     uint32_t Bp[16];
-    chacha<R>(K.k01, j0 >> 3, L_TAPEB, Bp);
+    if (BC_RSS_PRE)
+      chacha_pre<R, HI0>(K.tpb, j0 >> 3, Bp);
+    else
+      chacha<R>(K.k01, j0 >> 3, L_TAPEB, Bp);
 #pragma unroll 1
     for (int hb = 0; hb < 2; ++hb) {
       const uint64_t ib = i0 + 4 * hb;
       const ulonglong2 p0 = load2(a.x0, ib, a.n), p1 = load2(a.x1, ib, a.n), p2 = load2(a.x2, ib, a.n);
       const ulonglong2 q0 = load2(a.x0, ib + 2, a.n), q1 = load2(a.x1, ib + 2, a.n), q2 = load2(a.x2, ib + 2, a.n);
       uint32_t A[16];
-      chacha<R>(K.k01, (j0 >> 2) + (uint64_t)hb, L_TAPEA, A);
+      if (BC_RSS_PRE)
+        chacha_pre<R, HI0>(K.tpa, (j0 >> 2) + (uint64_t)hb, A);
+      else
+        chacha<R>(K.k01, (j0 >> 2) + (uint64_t)hb, L_TAPEA, A);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int e = 4 * hb + q;
@@ -189,13 +203,23 @@ int fused_rss(const uint64_t* x0, const uint64_t* x1, const uint64_t* x2, uint64
   }
   RssArgs a{x0, x1, x2, y0, y1, y2, (uint64_t)n, base};
   const KP kp = make_kp(prm);
-  RssKeys K{make_key(seeds->s01), make_key(seeds->s02), make_key(seeds->s12), make_key(s012), make_key(s2)};
+  RssKeys K{make_key(seeds->s01), make_key(seeds->s02), make_key(seeds->s12), make_key(s012), make_key(s2), {}, {}, {}};
+  {
+    const uint8_t* ks[NS_MAX] = {s012, s012, s012, s012, seeds->s12, s2, seeds->s02, seeds->s01, seeds->s12,
+                                 seeds->s02, seeds->s01, seeds->s12};
+    const uint64_t ls[NS_MAX] = {L_RA0, L_RA1, L_RA2, L_RS01, L_RS12, L_RS2B, L_RM02, L_RM01, L_RM12,
+                                 L_RN02, L_RN01, L_RN12};
+    for (int s = 0; s < NS_MAX; ++s) K.pre[s] = make_keypre(ks[s], ls[s]);
+    K.tpa = make_keypre(seeds->s01, L_TAPEA);
+    K.tpb = make_keypre(seeds->s01, L_TAPEB);
+  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint64_t ngroups = (n + 7) / 8;
   const size_t smem = (size_t)(RELU ? 12 : 9) * 16 * TPB_RSS * sizeof(uint32_t);
   return dispatch_rounds(prm->rounds, [&](auto Rc) {
     constexpr int R = decltype(Rc)::value;
-    auto fn = k_fused_rss<R, RELU>;
+    // every counter (j/8, j/4 + 1) below 2^32: the first round's column 1 is precomputed too
+    auto fn = base + n <= (1ull << 34) ? k_fused_rss<R, RELU, true> : k_fused_rss<R, RELU, false>;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int dev = 0, sms = 0, occ = 0;
     cudaGetDevice(&dev);
