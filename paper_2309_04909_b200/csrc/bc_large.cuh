@@ -215,6 +215,54 @@ __device__ __forceinline__ void large_draws(uint32_t m, uint64_t j, const Key& k
 #endif
 }
 
+// The same with the slot's position inside its group of 8 a compile-time constant K (the
+// group-of-8 slot loop, BC_LARGE_GROUP8): the byte offsets 6K and 48 + 6K fold into the
+// staged-word index and a constant shift, G = 24 (m div 8 mod 2) is the group's first word.
+// The rare exact acceptance test and redraw live out of line (large_redraw), so the common
+// path is one 32-bit compare per draw.
+struct Redraw {
+  uint64_t u;
+  uint32_t fbc;
+};
+template <int R>
+__device__ __noinline__ Redraw large_redraw(uint64_t u, uint64_t lim_m1, Key k01, uint64_t j, uint32_t fbc) {
+  while (!accept64(u, lim_m1)) u = fbl_word<R>(k01, j, fbc++) & DRAW48;
+  return Redraw{u, fbc};
+}
+template <int TPB_L, int BYTE>
+__device__ __forceinline__ uint64_t draw48c(const uint32_t* stg, uint32_t G) {
+  constexpr uint32_t w = BYTE >> 2, sh = (BYTE & 3) * 8;  // sh is 0 or 16
+  const uint32_t a = stg[(G + w) * TPB_L], b = stg[(G + w + 1) * TPB_L];
+  if (sh == 0) return (uint64_t)a | ((uint64_t)(b & 0xFFFFu) << 32);
+  return (uint64_t)__funnelshift_r(a, b, sh) | ((uint64_t)(b >> 16) << 32);
+}
+template <int R, int TPB_L, int K>
+__device__ __forceinline__ void large_draws_k(uint32_t G, uint64_t j, const Key& k01, const KPL& kp,
+                                              const uint32_t* stg, uint32_t& fbc, uint64_t& rM, uint64_t& rho) {
+  uint64_t ur = draw48c<TPB_L, 6 * K>(stg, G);
+  if (__builtin_expect((uint32_t)(ur >> 32) >= (uint32_t)(kp.qlim >> 32), 0)) {
+    const Redraw d = large_redraw<R>(ur, kp.qlim, k01, j, fbc);
+    ur = d.u;
+    fbc = d.fbc;
+  }
+  uint64_t uq = draw48c<TPB_L, 48 + 6 * K>(stg, G);
+  if (__builtin_expect((uint32_t)(uq >> 32) >= (uint32_t)(kp.plim >> 32), 0)) {
+    const Redraw d = large_redraw<R>(uq, kp.plim, k01, j, fbc);
+    uq = d.u;
+    fbc = d.fbc;
+  }
+#if BC_LARGE_FPMOD
+  rM = 1ull + fpmod48(ur, kp.p - 1ull, kp.s_q, kp.qinv_q, kp.qoff_q);
+  rho = fpmod48(uq, kp.p, 0u, kp.qinv_p, kp.qoff_p);
+#else
+  rM = 1ull + barrett(ur, kp.p - 1ull, kp.mu_q);
+  rho = barrett(uq, kp.p, kp.mu_p);
+#endif
+}
+#ifndef BC_LARGE_GROUP8
+#define BC_LARGE_GROUP8 1
+#endif
+
 // Blocks 1 + 3h .. 3 + 3h (slot groups 2h, 2h + 1) into staged rows 0..47.
 template <int R, int TPB_L, bool PRE = false, bool HI0 = false>
 __device__ __forceinline__ void large_stage(uint32_t h, uint64_t j, const Key& k01, uint32_t* stg,
@@ -243,6 +291,45 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
   const uint64_t s1 = t ? (0ull - x1) & kp.ymask : x1 & kp.ymask;
   const uint64_t s0f = s0 >> kp.f, n1f = ((0ull - s1) & kp.ymask) >> kp.f;
   uint32_t z = 0;
+  // steps 6-9 for slot m with its draws rM, rho
+  auto slot = [&](uint32_t m, uint64_t rM, uint64_t rho) {
+      uint64_t c, d;
+      slot_values(s0f, n1f, idx[m * TPB_L], kp, c, d);                // v'_{Pi(m)} of each party
+      uint64_t W0 = mont(c, rM, kp) + rho;                           // steps 7-8, P0: v'r + rho
+      W0 = W0 >= kp.p ? W0 - kp.p : W0;
+      uint64_t W1 = mont(d, rM, kp) + (kp.p - rho);                  //            P1: v'r - rho
+      if (TRANSCRIPT) {
+        W1 = W1 >= kp.p ? W1 - kp.p : W1;
+        w0[m] = W0;
+        w1[m] = W1;
+        const uint64_t sum = W0 + W1;                                // step 9 (P2): w_m = 0 mod p?
+        z |= (sum == 0 || sum == kp.p) ? 1u : 0u;
+      } else {
+        const uint64_t sum = W0 + W1;  // P0's W0 in [0, p) + P1's congruent x1 in (0, 2p]: 0 mod p iff p or 2p
+        z |= (sum == kp.p || sum == 2 * kp.p) ? 1u : 0u;
+      }
+  };
+  if (BC_LARGE_GROUP8) {
+#pragma unroll 1
+    for (uint32_t h = 0; 16 * h < S; ++h) {
+      large_stage<R, TPB_L, PRE, HI0>(h, j, k01, stg, pre);
+      const uint32_t mend = min(S, 16 * h + 16);
+#pragma unroll 1
+      for (uint32_t g8 = 16 * h; g8 < mend; g8 += 8) {
+        const uint32_t G = 24u * ((g8 >> 3) & 1u);
+        uint64_t rM, rho;
+#define BC_LARGE_SLOT(K)                                                     \
+        if (g8 + K < mend) {                                                 \
+          large_draws_k<R, TPB_L, K>(G, j, k01, kp, stg, fbc, rM, rho);      \
+          slot(g8 + K, rM, rho);                                             \
+        }
+        BC_LARGE_SLOT(0) BC_LARGE_SLOT(1) BC_LARGE_SLOT(2) BC_LARGE_SLOT(3)
+        BC_LARGE_SLOT(4) BC_LARGE_SLOT(5) BC_LARGE_SLOT(6) BC_LARGE_SLOT(7)
+#undef BC_LARGE_SLOT
+      }
+    }
+    return z | (t << 1);
+  }
 #pragma unroll 1
   for (uint32_t h = 0; 16 * h < S; ++h) {
     large_stage<R, TPB_L, PRE, HI0>(h, j, k01, stg, pre);
@@ -289,6 +376,35 @@ __device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, con
   // P0 reads windows of s, P1 of (-s) mod 2^ell (Alg 5, readings C3, C4)
   const uint64_t sf = (PARTY == 0 ? s : (0ull - s) & kp.ymask) >> kp.f;
   uint32_t hib = 0;
+  auto slot = [&](uint32_t m, uint64_t rM, uint64_t rho) {
+      uint64_t c, d;
+      slot_values(sf, sf, idx[m * TPB_L], kp, c, d);                  // one of the two is this party's
+      uint64_t W = PARTY == 0 ? mont(c, rM, kp) + rho : mont(d, rM, kp) + (kp.p - rho);  // steps 7-8
+      W = W >= kp.p ? W - kp.p : W;
+      lo[m * stride] = (uint32_t)W;
+      hib |= (uint32_t)(W >> 32) << m;
+  };
+  if (BC_LARGE_GROUP8) {
+#pragma unroll 1
+    for (uint32_t h = 0; 16 * h < S; ++h) {
+      large_stage<R, TPB_L>(h, j, k01, stg);
+      const uint32_t mend = min(S, 16 * h + 16);
+#pragma unroll 1
+      for (uint32_t g8 = 16 * h; g8 < mend; g8 += 8) {
+        const uint32_t G = 24u * ((g8 >> 3) & 1u);
+        uint64_t rM, rho;
+#define BC_LARGE_SLOT(K)                                                     \
+        if (g8 + K < mend) {                                                 \
+          large_draws_k<R, TPB_L, K>(G, j, k01, kp, stg, fbc, rM, rho);      \
+          slot(g8 + K, rM, rho);                                             \
+        }
+        BC_LARGE_SLOT(0) BC_LARGE_SLOT(1) BC_LARGE_SLOT(2) BC_LARGE_SLOT(3)
+        BC_LARGE_SLOT(4) BC_LARGE_SLOT(5) BC_LARGE_SLOT(6) BC_LARGE_SLOT(7)
+#undef BC_LARGE_SLOT
+      }
+    }
+    return (uint64_t)hib | ((uint64_t)t << 32);
+  }
 #pragma unroll 1
   for (uint32_t h = 0; 16 * h < S; ++h) {
     large_stage<R, TPB_L>(h, j, k01, stg);
