@@ -200,6 +200,10 @@ __global__ void __launch_bounds__(TPB, FUSED_MINB) k_fused_c(FusedArgs a, KP kp,
 #ifndef BC_FUSED_TABLES
 #define BC_FUSED_TABLES 1  // 0: the SWAR kernel k_fused_c for the compact tape
 #endif
+#ifndef BC_HB_UNROLL
+#define BC_HB_UNROLL 1  // the table kernel's two half-group iterations rolled (1) or unrolled (2)
+#endif
+constexpr int kHbUnroll = BC_HB_UNROLL;
 #ifndef BC_TPB_T
 #define BC_TPB_T 512  // threads of the one CTA per SM (65536 registers / TPB_T per thread)
 #endif
@@ -228,7 +232,7 @@ __global__ void __launch_bounds__(TPB_T, 1) k_fused_t(FusedArgs a, KP kp, const 
     uint32_t zbits = 0, tbits = 0;
     uint32_t Bp[16];  // part B: words 2e, 2e+1 of element e (reshare words w1, w2)
     stream_blk<R, !RELU || BC_RELU_PRE, HI0>(pk.tpb, k01, L_TAPEB, j0 >> 3, Bp);
-#pragma unroll 1
+#pragma unroll kHbUnroll
     for (int hb = 0; hb < 2; ++hb) {
       const uint64_t ib = i0 + 4 * hb;
       const ulonglong2 u0 = load2(a.x0, ib, a.n), u1 = load2(a.x1, ib, a.n);
@@ -374,7 +378,7 @@ constexpr int TPB_L = TPB_LARGE;
 #define BC_LARGE_MINB 1  // resident CTAs per SM the large-tape kernel is compiled for (register cap)
 #endif
 
-template <int R, bool RELU, bool TRANSCRIPT, bool HI0 = false>
+template <int R, bool RELU, bool TRANSCRIPT, bool HI0 = false, bool W32 = false>
 __global__ void __launch_bounds__(TPB_L, BC_LARGE_MINB) k_fused_l(FusedArgs a, KP kp, KPL kl, Key k01, Key k02, Key k12,
                                                                   const __grid_constant__ PreKeys pk) {
   __shared__ LargeIdx sidx[32 * TPB_L];
@@ -396,7 +400,7 @@ __global__ void __launch_bounds__(TPB_L, BC_LARGE_MINB) k_fused_l(FusedArgs a, K
       uint64_t* w0 = TRANSCRIPT ? reinterpret_cast<uint64_t*>(a.w0lo) + i * kl.S : nullptr;
       uint64_t* w1 = TRANSCRIPT ? reinterpret_cast<uint64_t*>(a.w1lo) + i * kl.S : nullptr;
       const uint32_t r =
-          elem_large<R, TRANSCRIPT, TPB_L, BC_LARGE_PRE != 0, HI0>(__ldg(a.x0 + i), __ldg(a.x1 + i), j0 + e, k01, kl, idx,
+          elem_large<R, TRANSCRIPT, TPB_L, BC_LARGE_PRE != 0, HI0, W32>(__ldg(a.x0 + i), __ldg(a.x1 + i), j0 + e, k01, kl, idx,
                                                                     stg, magic, hlim, w0, w1, &pk.tpa);
       zbits |= (r & 1u) << e;
       tbits |= (r >> 1) << e;
@@ -559,7 +563,7 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
       const KPL kl = make_kpl(prm);
       auto fn = tr ? k_fused_l<R, RELU, true> : k_fused_l<R, RELU, false>;
       if (!tr && base + n <= (1ull << 32) / 7)  // every tape counter 7j + b below 2^32
-        fn = k_fused_l<R, RELU, false, true>;
+        fn = kl.w == 32 ? k_fused_l<R, RELU, false, true, true> : k_fused_l<R, RELU, false, true>;
       fn<<<grid_for((const void*)fn, ngroups, TPB_L), TPB_L, 0, st>>>(a, kp, kl, k01, k02, k12, pk);
     } else if (prm->tape == BC_TAPE_COMPACT && BC_FUSED_TABLES) {
       const bool fhi = kp.fhi != 0;

@@ -99,10 +99,25 @@ __device__ __noinline__ uint64_t fbl_word(Key k01, uint64_t j, uint32_t c) {
 // offset applied once per element), so window i is bits [i, i+w) of a 64-bit
 // value with i + w <= 64 - f: one 32-bit funnel shift (i <= 31, w <= 32).
 // Returns P0's c'_i and P1's d'_i in [0, p).
+// W32: w = 32 (the full-precision guard domain lx = 31): every window is a whole 32-bit word,
+// the masks vanish and the sums wrap mod 2^32 by themselves.
+template <bool W32 = false>
 __device__ __forceinline__ void slot_values(uint64_t s0f, uint64_t n1f, uint32_t i, const KPL& kp, uint64_t& c,
                                             uint64_t& d) {
   const uint32_t l0 = (uint32_t)s0f, h0 = (uint32_t)(s0f >> 32);
   const uint32_t l1 = (uint32_t)n1f, h1 = (uint32_t)(n1f >> 32);
+  if (W32) {
+    const bool last = i + 1 >= kp.S;                                    // slot lx has no successor
+    const uint32_t a_i = __funnelshift_r(l0, h0, i);
+    const uint32_t a_n = last ? 0u : __funnelshift_rc(l0, h0, i + 1);
+    const uint32_t b_i = __funnelshift_r(l1, h1, i);                    // P1: -(window of -s_1), below
+    const uint32_t b_n = last ? 0u : __funnelshift_rc(l1, h1, i + 1);
+    const uint32_t cv = a_i + a_n - 1u;                                 // step 4 (mod 2^32)
+    const uint32_t dv = 0u - (b_i + b_n);                               // -b_i - b_{i+1} (readings C3, C4)
+    c = cv == 0 ? kp.two_w : (uint64_t)cv;                              // step 5 (Alg 6)
+    d = (uint64_t)dv + kp.off1;
+    return;
+  }
   const uint32_t wm = kp.wm32;
   const uint32_t nm = i + 1 < kp.S ? wm : 0u;                          // slot lx has no successor
   const uint32_t a_i = __funnelshift_r(l0, h0, i) & wm;
@@ -278,7 +293,7 @@ __device__ __forceinline__ void large_stage(uint32_t h, uint64_t j, const Key& k
 
 // Alg 7 steps 1-9 for element j with shares x0, x1 (both computing parties and
 // P2's zero test): returns DReLU' (bit 0) and t (bit 1).
-template <int R, bool TRANSCRIPT, int TPB_L, bool PRE = false, bool HI0 = false>
+template <int R, bool TRANSCRIPT, int TPB_L, bool PRE = false, bool HI0 = false, bool W32 = false>
 __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_t j, const Key& k01, const KPL& kp,
                                                LargeIdx* idx, uint32_t* stg, const uint32_t* magic,
                                                const uint32_t* hlim, uint64_t* w0, uint64_t* w1,
@@ -294,7 +309,7 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
   // steps 6-9 for slot m with its draws rM, rho
   auto slot = [&](uint32_t m, uint64_t rM, uint64_t rho) {
       uint64_t c, d;
-      slot_values(s0f, n1f, idx[m * TPB_L], kp, c, d);                // v'_{Pi(m)} of each party
+      slot_values<W32>(s0f, n1f, idx[m * TPB_L], kp, c, d);           // v'_{Pi(m)} of each party
       uint64_t W0 = mont(c, rM, kp) + rho;                           // steps 7-8, P0: v'r + rho
       W0 = W0 >= kp.p ? W0 - kp.p : W0;
       uint64_t W1 = mont(d, rM, kp) + (kp.p - rho);                  //            P1: v'r - rho
@@ -339,7 +354,7 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
       uint64_t rM, rho;
       large_draws<R, TPB_L>(m, j, k01, kp, stg, fbc, rM, rho);
       uint64_t c, d;
-      slot_values(s0f, n1f, idx[m * TPB_L], kp, c, d);                // v'_{Pi(m)} of each party
+      slot_values<W32>(s0f, n1f, idx[m * TPB_L], kp, c, d);           // v'_{Pi(m)} of each party
       uint64_t W0 = mont(c, rM, kp) + rho;                           // steps 7-8, P0: v'r + rho
       W0 = W0 >= kp.p ? W0 - kp.p : W0;
       uint64_t W1 = mont(d, rM, kp) + (kp.p - rho);                  //            P1: v'r - rho
@@ -365,7 +380,7 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
 // the message W_m, m < S, as 32-bit low words lo[m * stride] (slot-major wire
 // planes) and bit m of the returned high-bit word (bit 32 of W_m; p < 2^33).
 // Returns t in bit 32 of the result.
-template <int R, int PARTY, int TPB_L>
+template <int R, int PARTY, int TPB_L, bool W32 = false>
 __device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, const Key& k01, const KPL& kp,
                                                      LargeIdx* idx, uint32_t* stg, const uint32_t* magic,
                                                      const uint32_t* hlim, uint32_t* lo, uint64_t stride) {
@@ -378,7 +393,7 @@ __device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, con
   uint32_t hib = 0;
   auto slot = [&](uint32_t m, uint64_t rM, uint64_t rho) {
       uint64_t c, d;
-      slot_values(sf, sf, idx[m * TPB_L], kp, c, d);                  // one of the two is this party's
+      slot_values<W32>(sf, sf, idx[m * TPB_L], kp, c, d);             // one of the two is this party's
       uint64_t W = PARTY == 0 ? mont(c, rM, kp) + rho : mont(d, rM, kp) + (kp.p - rho);  // steps 7-8
       W = W >= kp.p ? W - kp.p : W;
       lo[m * stride] = (uint32_t)W;
@@ -414,7 +429,7 @@ __device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, con
       uint64_t rM, rho;
       large_draws<R, TPB_L>(m, j, k01, kp, stg, fbc, rM, rho);
       uint64_t c, d;
-      slot_values(sf, sf, idx[m * TPB_L], kp, c, d);                  // one of the two is this party's
+      slot_values<W32>(sf, sf, idx[m * TPB_L], kp, c, d);             // one of the two is this party's
       uint64_t W = PARTY == 0 ? mont(c, rM, kp) + rho : mont(d, rM, kp) + (kp.p - rho);  // steps 7-8
       W = W >= kp.p ? W - kp.p : W;
       lo[m * stride] = (uint32_t)W;

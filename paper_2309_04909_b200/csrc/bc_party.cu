@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(TPB, 2) k_send_w(SendArgs a, KP kp_, Key k01, 
 // stores of slot m are 128 coalesced bytes (over NVLink in the peer
 // transport) and the blinding bits come out of one ballot per 32 elements;
 // then (ReLU) lane l computes [d]_b for its group of 8 (send_dshare).
-template <int R, int PARTY, bool RELU>
+template <int R, int PARTY, bool RELU, bool W32 = false>
 __global__ void __launch_bounds__(TPB_LARGE) k_send_l(SendArgs a, KP kp, KPL kl, Key k01, Key ktr) {
   __shared__ LargeIdx sidx[32 * TPB_LARGE];
   __shared__ uint32_t sstg[LARGE_STG_ROWS * TPB_LARGE];
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(TPB_LARGE) k_send_l(SendArgs a, KP kp, KPL kl,
       const uint64_t i = wb + 32 * e + lane;
       uint32_t tb = 0;
       if (i < a.n) {
-        const uint64_t r = elem_large_party<R, PARTY, TPB_LARGE>(__ldg(a.x + i), a.base + i, k01, kl, idx, stg,
+        const uint64_t r = elem_large_party<R, PARTY, TPB_LARGE, W32>(__ldg(a.x + i), a.base + i, k01, kl, idx, stg,
                                                                  magic, hlim, lo + i, a.n);
         if (hi) hi[i] = (uint32_t)r;
         tb = (uint32_t)(r >> 32);
@@ -448,7 +448,8 @@ int send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits,
     auto go = [&](auto fn) { fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k01, ktr); };
     if (large) {
       const KPL kl = make_kpl(prm);
-      auto fn = party == 0 ? k_send_l<R, 0, RELU> : k_send_l<R, 1, RELU>;
+      auto fn = party == 0 ? (kl.w == 32 ? k_send_l<R, 0, RELU, true> : k_send_l<R, 0, RELU>)
+                           : (kl.w == 32 ? k_send_l<R, 1, RELU, true> : k_send_l<R, 1, RELU>);
       fn<<<grid_for((const void*)fn, ngroups, TPB_LARGE), TPB_LARGE, 0, st>>>(a, kp, kl, k01, ktr);
     } else if (prm->tape == BC_TAPE_COMPACT) {
       if (party == 0) go(k_send_c<R, 0, RELU>);
