@@ -149,14 +149,29 @@ class Params:
     rounds: int = 20
 
     def c(self) -> bc_params:
-        p = bc_params()
-        _check(lib().bc_params_init(ctypes.byref(p), self.ell, self.lx, self.f, MODE[self.mode], self.rounds),
-               "bc_params_init")
+        """The derived bc_params (bc_params_init), cached per parameter set: the C side only reads it."""
+        key = (self.ell, self.lx, self.f, self.mode, self.rounds)
+        p = _PARAMS_CACHE.get(key)
+        if p is None:
+            p = bc_params()
+            _check(lib().bc_params_init(ctypes.byref(p), self.ell, self.lx, self.f, MODE[self.mode], self.rounds),
+                   "bc_params_init")
+            _PARAMS_CACHE[key] = p
         return p
 
 
+_PARAMS_CACHE: dict = {}
+_SEEDS_CACHE: dict = {}
+
+
 def seeds_struct(seeds) -> bc_seeds:
-    s = bc_seeds()
+    key = (bytes(seeds.s01), bytes(seeds.s02), bytes(seeds.s12))
+    s = _SEEDS_CACHE.get(key)
+    if s is not None:
+        return s
+    if len(_SEEDS_CACHE) > 64:
+        _SEEDS_CACHE.clear()
+    s = _SEEDS_CACHE[key] = bc_seeds()
     for name in ("s01", "s02", "s12"):
         v = getattr(seeds, name)
         assert len(v) == 32
