@@ -477,6 +477,30 @@ __device__ __forceinline__ uint32_t elem_both_t2(uint64_t x0, uint64_t x1, uint3
   return vmin <= 16711935u;
 }
 
+// Alg 7 steps 1-8 for ONE computing party, table form with the V2 slot arithmetic (the
+// party-separated send kernel): its message W_m in [0, 257), the wire value.  o: the party's
+// reshare offsets from decode_t2 (P0 o0 = rho + 257k, P1 o1 = 257K - rho); x < 2^24.
+template <int PARTY, bool FHI>
+__device__ __forceinline__ void elem_one_t2(uint64_t x, uint32_t t, uint32_t ix, const uint32_t (&rb)[2],
+                                            const uint32_t (&o)[8], uint32_t sbase, uint32_t fsh, uint32_t (&W)[8]) {
+  const uint64_t v = PARTY == 0 ? (t ? 0ull - x : x) : (t ? x : 0ull - x);  // P1 windows -s_1 (C3)
+  const uint32_t wn = win_at<FHI>(v, fsh);
+  constexpr uint32_t LAD = 4u * kPermN;
+  constexpr uint32_t TLO = 4u * (PARTY == 0 ? kLadP0Lo : kLadP1Lo), THI = 4u * (PARTY == 0 ? kLadP0Hi : kLadP1Hi);
+  const uint32_t c_lo = lds_u32(sbase + LAD + TLO + lad_lo_off(wn));
+  const uint32_t c_hi = lds_u32(sbase + LAD + THI + lad_hi_off(wn));
+  const uint32_t sel = lds_u32(sbase + ix * 4u);
+  const uint32_t selh = lds_u16(sbase + ix * 4u + 2u);
+  const uint32_t C_lo = prmt(c_lo, c_hi, sel), C_hi = prmt(c_lo, c_hi, selh);
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const uint32_t unit = 1u << (8 * (m & 3));
+    const uint32_t r = __dp4a(rb[m >> 2], unit, 1u);            // r_m = 1 + mask byte
+    const uint32_t c1 = __dp4a(m < 4 ? C_lo : C_hi, unit, 1u);  // v'_m
+    W[m] = mod257s(c1 * r + o[m]);                              // steps 7-8, reduced (x < 2^24)
+  }
+}
+
 // ---- the paper-literal domain (w = lx = 7, p = 131, 8 slots, pair tape), table form ----
 // Pair-tape draws of one element (T = its 8 keystream words):
 // t, the permutation index mod 8!, and per slot r_m = 1 + x mod 130, rho_m = x div 130

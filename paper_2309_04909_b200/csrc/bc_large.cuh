@@ -380,13 +380,14 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
 // the message W_m, m < S, as 32-bit low words lo[m * stride] (slot-major wire
 // planes) and bit m of the returned high-bit word (bit 32 of W_m; p < 2^33).
 // Returns t in bit 32 of the result.
-template <int R, int PARTY, int TPB_L, bool W32 = false>
+template <int R, int PARTY, int TPB_L, bool W32 = false, bool PRE = false, bool HI0 = false>
 __device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, const Key& k01, const KPL& kp,
                                                      LargeIdx* idx, uint32_t* stg, const uint32_t* magic,
-                                                     const uint32_t* hlim, uint32_t* lo, uint64_t stride) {
+                                                     const uint32_t* hlim, uint32_t* lo, uint64_t stride,
+                                                     const KeyPre* pre = nullptr) {
   const uint32_t S = kp.S;
   uint32_t fbc = 0;
-  const uint32_t t = large_perm<R, TPB_L>(j, k01, kp, idx, stg, magic, hlim, fbc);
+  const uint32_t t = large_perm<R, TPB_L, PRE, HI0>(j, k01, kp, idx, stg, magic, hlim, fbc, pre);
   const uint64_t s = t ? (0ull - x) & kp.ymask : x & kp.ymask;                  // steps 1-2
   // P0 reads windows of s, P1 of (-s) mod 2^ell (Alg 5, readings C3, C4)
   const uint64_t sf = (PARTY == 0 ? s : (0ull - s) & kp.ymask) >> kp.f;
@@ -402,7 +403,7 @@ __device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, con
   if (BC_LARGE_GROUP8) {
 #pragma unroll 1
     for (uint32_t h = 0; 16 * h < S; ++h) {
-      large_stage<R, TPB_L>(h, j, k01, stg);
+      large_stage<R, TPB_L, PRE, HI0>(h, j, k01, stg, pre);
       const uint32_t mend = min(S, 16 * h + 16);
 #pragma unroll 1
       for (uint32_t g8 = 16 * h; g8 < mend; g8 += 8) {
@@ -422,7 +423,7 @@ __device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, con
   }
 #pragma unroll 1
   for (uint32_t h = 0; 16 * h < S; ++h) {
-    large_stage<R, TPB_L>(h, j, k01, stg);
+    large_stage<R, TPB_L, PRE, HI0>(h, j, k01, stg, pre);
     const uint32_t mend = min(S, 16 * h + 16);
 #pragma unroll kLargeSlotUnroll
     for (uint32_t m = 16 * h; m < mend; ++m) {

@@ -97,6 +97,103 @@ __global__ void __launch_bounds__(TPB, 2) k_send_c(SendArgs a, KP kp, Key k01, K
   }
 }
 
+// Compact tape, table form (as the fused k_fused_t): one CTA of TPB_ST threads per SM with the
+// 210 KB of ladder and 8! selector tables in shared memory, the V2 slot arithmetic, and every
+// keystream block through chacha_pre (HI0: every counter of the launch below 2^32).
+#ifndef BC_SEND_TABLES
+#define BC_SEND_TABLES 1  // 0: the SWAR kernel k_send_c
+#endif
+constexpr int TPB_ST = 512;
+constexpr size_t kSendTabBytes = sizeof(uint32_t) * kTabWords;
+__device__ constexpr CompactTables kSendTables{};
+
+struct SendPre {
+  KeyPre tpa, tpb;  // seed01: compact tape parts A and B
+  KeyPre tra;       // ReLU: the party's [a]_b stream (seed02 bc2.ta02 for P0, seed12 bc2.ta12 for P1)
+  KeyPre resp;      // DReLU, P0 with y0: seed02 bc2.resp
+};
+
+template <int R, int PARTY, bool RELU, bool FHI, bool HI0>
+__global__ void __launch_bounds__(TPB_ST, 1) k_send_t(SendArgs a, KP kp, const __grid_constant__ Key k01, Key ktr,
+                                                       const __grid_constant__ SendPre sp) {
+  extern __shared__ uint4 smem_st[];
+  {
+    const uint4* g = reinterpret_cast<const uint4*>(kSendTables.w);
+    for (int i = threadIdx.x; i < kTabWords / 4; i += blockDim.x) smem_st[i] = g[i];
+  }
+  __syncthreads();
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_st);
+  const uint64_t ngroups = (a.n + 7) >> 3;
+  for (uint64_t g = (uint64_t)blockIdx.x * TPB_ST + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB_ST) {
+    const uint64_t i0 = g << 3;
+    const uint64_t j0 = a.base + i0;
+    const uint32_t cnt = (uint32_t)min((uint64_t)8, a.n - i0);
+    uint32_t tb = 0;
+    uint64_t hi = 0;
+    uint32_t Bp[16];
+    chacha_pre<R, HI0>(sp.tpb, j0 >> 3, Bp);
+#pragma unroll 1
+    for (int hb = 0; hb < 2; ++hb) {
+      const ulonglong2 u = load2(a.x, i0 + 4 * hb, a.n), v = load2(a.x, i0 + 4 * hb + 2, a.n);
+      uint32_t A[16];
+      chacha_pre<R, HI0>(sp.tpa, (j0 >> 2) + (uint64_t)hb, A);
+      uint64_t lo[4];  // the half group's low-byte planes, stored at the end of the iteration
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = 4 * hb + q;
+        const uint32_t t = A[4 * q] >> 31;
+        const uint32_t rb[2] = {A[4 * q + 1], A[4 * q + 2]};
+        uint32_t o0[8], o1[8], W[8];
+        const uint32_t ix = decode_t2<R>(A[4 * q], A[4 * q + 3], Bp[2 * q], Bp[2 * q + 1], j0 + (uint64_t)e, k01, o0, o1);
+        elem_one_t2<PARTY, FHI>(q == 0 ? u.x : q == 1 ? u.y : q == 2 ? v.x : v.y, t, ix, rb, PARTY == 0 ? o0 : o1,
+                                sbase, kp.fsh, W);
+        lo[q] = pack_lo(W);
+        hi |= (uint64_t)pack_hi(W) << (8 * e);
+        tb |= t << e;
+      }
+      uint64_t* lop = reinterpret_cast<uint64_t*>(a.lo) + i0 + 4 * hb;
+      const uint32_t c4 = cnt > 4u * hb ? min(4u, cnt - 4u * hb) : 0u;
+      if (c4 == 4) {
+        reinterpret_cast<ulonglong2*>(lop)[0] = make_ulonglong2(lo[0], lo[1]);
+        reinterpret_cast<ulonglong2*>(lop)[1] = make_ulonglong2(lo[2], lo[3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if ((uint32_t)q < c4) lop[q] = lo[q];
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) Bp[k] = Bp[k + 8];  // elements 4..7 next
+    }
+    if (a.hi) {  // the high-bit plane (bit 8 of each W_m) and the blinding bits, as store_msg
+      if (cnt == 8) *reinterpret_cast<uint64_t*>(a.hi + i0) = hi;
+      else
+        for (uint32_t e = 0; e < cnt; ++e) a.hi[i0 + e] = (uint8_t)(hi >> (8 * e));
+    }
+    if (a.tbits) a.tbits[g] = (uint8_t)(tb & ((1u << cnt) - 1u));
+    if (RELU) {  // Alg 8 step 4: [d]_b = [x]_b - [a]_b (as send_dshare, block through chacha_pre)
+      uint32_t Ak[16];
+      chacha_pre<R, HI0>(sp.tra, j0 >> 3, Ak);
+      uint64_t x[8], d[8];
+      load8(a.x + i0, x, cnt);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) d[e] = (x[e] - u64_of(Ak, e)) & kp.ymask;
+      store8(a.dshare + i0, d, cnt);
+      if (a.dpeer) store8(a.dpeer + i0, d, cnt);
+    }
+    if (!RELU && PARTY == 0 && a.y0) {  // Alg 7 steps 10-11 for P0 (as send_finish_p0)
+      uint32_t Q[16];
+      chacha_pre<R, HI0>(sp.resp, j0 >> 3, Q);
+      uint64_t y[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint64_t t = (tb >> e) & 1u;
+        y[e] = (t + (1ull - 2ull * t) * u64_of(Q, e)) & kp.ymask;
+      }
+      store8(a.y0 + i0, y, cnt);
+    }
+  }
+}
+
 // Pair tape (one seed01 block per two elements).
 template <int R, int PARTY, bool RELU, bool CL>
 __global__ void __launch_bounds__(TPB, 2) k_send_w(SendArgs a, KP kp_, Key k01, Key ktr) {
@@ -144,8 +241,9 @@ __global__ void __launch_bounds__(TPB, 2) k_send_w(SendArgs a, KP kp_, Key k01, 
 // stores of slot m are 128 coalesced bytes (over NVLink in the peer
 // transport) and the blinding bits come out of one ballot per 32 elements;
 // then (ReLU) lane l computes [d]_b for its group of 8 (send_dshare).
-template <int R, int PARTY, bool RELU, bool W32 = false>
-__global__ void __launch_bounds__(TPB_LARGE) k_send_l(SendArgs a, KP kp, KPL kl, Key k01, Key ktr) {
+template <int R, int PARTY, bool RELU, bool W32 = false, bool HI0 = false>
+__global__ void __launch_bounds__(TPB_LARGE) k_send_l(SendArgs a, KP kp, KPL kl, Key k01, Key ktr,
+                                                      const __grid_constant__ KeyPre tpl) {
   __shared__ LargeIdx sidx[32 * TPB_LARGE];
   __shared__ uint32_t sstg[LARGE_STG_ROWS * TPB_LARGE];
   __shared__ uint32_t magic[33], hlim[33];
@@ -166,8 +264,8 @@ __global__ void __launch_bounds__(TPB_LARGE) k_send_l(SendArgs a, KP kp, KPL kl,
       const uint64_t i = wb + 32 * e + lane;
       uint32_t tb = 0;
       if (i < a.n) {
-        const uint64_t r = elem_large_party<R, PARTY, TPB_LARGE, W32>(__ldg(a.x + i), a.base + i, k01, kl, idx, stg,
-                                                                 magic, hlim, lo + i, a.n);
+        const uint64_t r = elem_large_party<R, PARTY, TPB_LARGE, W32, true, HI0>(__ldg(a.x + i), a.base + i, k01, kl, idx, stg,
+                                                                 magic, hlim, lo + i, a.n, &tpl);
         if (hi) hi[i] = (uint32_t)r;
         tb = (uint32_t)(r >> 32);
       }
@@ -213,16 +311,22 @@ struct HelperArgs {
   uint64_t n, base;
 };
 
+// The seed02 / seed12 streams of the helper and finish phases with chacha_pre's first-round
+// precomputation (host: make_keypre; only the streams of the seeds the caller passed are set).
+struct StreamPre {
+  KeyPre resp, b02, b12, a02, a12, c02;
+};
+
 // P2's response for a group with zero-test bits zbits: Alg 7 step 10 ([D']_0
 // from seed02, [D']_1 = DReLU' - [D']_0), or Alg 8 steps 2-3 (e = DReLU' - b and
 // [c]_1 = ab - [c]_0 from the triple seeds).
-template <int R, bool RELU>
-__device__ __forceinline__ void helper_respond(const HelperArgs& a, const KP& kp, const Key& k02, const Key& k12,
+template <int R, bool RELU, bool HI0>
+__device__ __forceinline__ void helper_respond(const HelperArgs& a, const KP& kp, const StreamPre& sp,
                                                uint64_t i0, uint64_t j0, uint32_t cnt, uint32_t zbits) {
   uint64_t o0[8], o1[8];
   if (!RELU) {
     uint32_t Q[16];
-    chacha<R>(k02, j0 >> 3, L_RESP, Q);
+    chacha_pre<R, HI0>(sp.resp, j0 >> 3, Q);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const uint64_t q = u64_of(Q, e) & kp.ymask;
@@ -231,8 +335,8 @@ __device__ __forceinline__ void helper_respond(const HelperArgs& a, const KP& kp
     }
   } else {
     uint32_t Bk0[16], Bk1[16];
-    chacha<R>(k02, j0 >> 3, L_B02, Bk0);
-    chacha<R>(k12, j0 >> 3, L_B12, Bk1);
+    chacha_pre<R, HI0>(sp.b02, j0 >> 3, Bk0);
+    chacha_pre<R, HI0>(sp.b12, j0 >> 3, Bk1);
     uint64_t bsum[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
@@ -241,12 +345,12 @@ __device__ __forceinline__ void helper_respond(const HelperArgs& a, const KP& kp
     }
     if (a.out1) {  // [c]_1 = ([a]_0 + [a]_1)([b]_0 + [b]_1) - [c]_0
       uint32_t Ak0[16], Ak1[16];
-      chacha<R>(k02, j0 >> 3, L_A02, Ak0);
-      chacha<R>(k12, j0 >> 3, L_A12, Ak1);
+      chacha_pre<R, HI0>(sp.a02, j0 >> 3, Ak0);
+      chacha_pre<R, HI0>(sp.a12, j0 >> 3, Ak1);
 #pragma unroll
       for (int e = 0; e < 8; ++e) o1[e] = (u64_of(Ak0, e) + u64_of(Ak1, e)) * bsum[e];
       uint32_t Ck[16];
-      chacha<R>(k02, j0 >> 3, L_C02, Ck);
+      chacha_pre<R, HI0>(sp.c02, j0 >> 3, Ck);
 #pragma unroll
       for (int e = 0; e < 8; ++e) o1[e] = (o1[e] - u64_of(Ck, e)) & kp.ymask;
     }
@@ -257,8 +361,8 @@ __device__ __forceinline__ void helper_respond(const HelperArgs& a, const KP& kp
 }
 
 // P2: Alg 7 steps 9-10, or Alg 8 steps 2-3 with the triple's [c]_1.
-template <int R, bool RELU>
-__global__ void __launch_bounds__(TPB, 2) k_helper(HelperArgs a, KP kp, Key k02, Key k12) {
+template <int R, bool RELU, bool HI0 = false>
+__global__ void __launch_bounds__(TPB, 2) k_helper(HelperArgs a, KP kp, const __grid_constant__ StreamPre sp) {
   const uint64_t ngroups = (a.n + 7) >> 3;
   for (uint64_t g = (uint64_t)blockIdx.x * TPB + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB) {
     const uint64_t i0 = g << 3;
@@ -276,7 +380,7 @@ __global__ void __launch_bounds__(TPB, 2) k_helper(HelperArgs a, KP kp, Key k02,
       unpack_W(l1[e], (uint32_t)(h1 >> (8 * e)) & 0xFFu, W1);
       zbits |= zero_test(W0, W1, kp.p, kp.S) << e;
     }
-    helper_respond<R, RELU>(a, kp, k02, k12, i0, j0, cnt, zbits);
+    helper_respond<R, RELU, HI0>(a, kp, sp, i0, j0, cnt, zbits);
   }
 }
 
@@ -288,8 +392,9 @@ __global__ void __launch_bounds__(TPB, 2) k_helper(HelperArgs a, KP kp, Key k02,
 #ifndef BC_HELPER_L_MINB
 #define BC_HELPER_L_MINB 2
 #endif
-template <int R, bool RELU>
-__global__ void __launch_bounds__(TPB, BC_HELPER_L_MINB) k_helper_l(HelperArgs a, KP kp, KPL kl, Key k02, Key k12) {
+template <int R, bool RELU, bool HI0 = false>
+__global__ void __launch_bounds__(TPB, BC_HELPER_L_MINB) k_helper_l(HelperArgs a, KP kp, KPL kl,
+                                                                    const __grid_constant__ StreamPre sp) {
   const uint32_t* lo0 = reinterpret_cast<const uint32_t*>(a.lo0);
   const uint32_t* lo1 = reinterpret_cast<const uint32_t*>(a.lo1);
   const uint32_t* hi0 = reinterpret_cast<const uint32_t*>(a.hi0);
@@ -329,7 +434,7 @@ __global__ void __launch_bounds__(TPB, BC_HELPER_L_MINB) k_helper_l(HelperArgs a
     const uint64_t g = wb / 8 + lane;
     if (g < ngroups) {
       const uint64_t i0 = g << 3;
-      helper_respond<R, RELU>(a, kp, k02, k12, i0, a.base + i0, (uint32_t)min((uint64_t)8, n - i0), zbits);
+      helper_respond<R, RELU, HI0>(a, kp, sp, i0, a.base + i0, (uint32_t)min((uint64_t)8, n - i0), zbits);
     }
   }
 }
@@ -345,8 +450,8 @@ struct FinishArgs {
   uint64_t n, base;
 };
 
-template <int R, int PARTY, bool RELU>
-__global__ void __launch_bounds__(TPB, 2) k_finish(FinishArgs a, KP kp, Key ks) {
+template <int R, int PARTY, bool RELU, bool HI0 = false>
+__global__ void __launch_bounds__(TPB, 2) k_finish(FinishArgs a, KP kp, const __grid_constant__ StreamPre sp) {
   const uint64_t ngroups = (a.n + 7) >> 3;
   for (uint64_t g = (uint64_t)blockIdx.x * TPB + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB) {
     const uint64_t i0 = g << 3;
@@ -360,7 +465,7 @@ __global__ void __launch_bounds__(TPB, 2) k_finish(FinishArgs a, KP kp, Key ks) 
         load8(a.resp + i0, D, cnt);
       } else {  // P0 derives [D']_0 from seed02 (reading C12)
         uint32_t Q[16];
-        chacha<R>(ks, j0 >> 3, L_RESP, Q);
+        chacha_pre<R, HI0>(sp.resp, j0 >> 3, Q);
 #pragma unroll
         for (int e = 0; e < 8; ++e) D[e] = u64_of(Q, e);
       }
@@ -384,7 +489,7 @@ __global__ void __launch_bounds__(TPB, 2) k_finish(FinishArgs a, KP kp, Key ks) 
         for (int e = 0; e < 8; ++e) acc[e] = own[e] + dp[e];  // d = [d]_0 + [d]_1 (opened)
       }
       uint32_t Bk[16];
-      chacha<R>(ks, j0 >> 3, PARTY == 0 ? L_B02 : L_B12, Bk);
+      chacha_pre<R, HI0>(PARTY == 0 ? sp.b02 : sp.b12, j0 >> 3, Bk);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const uint64_t d = acc[e], ab = x[e] - own[e];  // [a]_b
@@ -392,7 +497,7 @@ __global__ void __launch_bounds__(TPB, 2) k_finish(FinishArgs a, KP kp, Key ks) 
       }
       if (PARTY == 0) {
         uint32_t Ck[16];
-        chacha<R>(ks, j0 >> 3, L_C02, Ck);
+        chacha_pre<R, HI0>(sp.c02, j0 >> 3, Ck);
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[e] += u64_of(Ck, e);
       } else {
@@ -448,9 +553,31 @@ int send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits,
     auto go = [&](auto fn) { fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k01, ktr); };
     if (large) {
       const KPL kl = make_kpl(prm);
-      auto fn = party == 0 ? (kl.w == 32 ? k_send_l<R, 0, RELU, true> : k_send_l<R, 0, RELU>)
-                           : (kl.w == 32 ? k_send_l<R, 1, RELU, true> : k_send_l<R, 1, RELU>);
-      fn<<<grid_for((const void*)fn, ngroups, TPB_LARGE), TPB_LARGE, 0, st>>>(a, kp, kl, k01, ktr);
+      const KeyPre tpl = make_keypre(s01, L_TAPEL);
+      const bool c32 = base + n <= (1ull << 32) / 7;  // every tape counter 7j + b below 2^32
+      auto pick = [&](auto P) {
+        constexpr int PARTY = decltype(P)::value;
+        return kl.w == 32 ? (c32 ? k_send_l<R, PARTY, RELU, true, true> : k_send_l<R, PARTY, RELU, true, false>)
+                          : (c32 ? k_send_l<R, PARTY, RELU, false, true> : k_send_l<R, PARTY, RELU, false, false>);
+      };
+      auto fn = party == 0 ? pick(std::integral_constant<int, 0>{}) : pick(std::integral_constant<int, 1>{});
+      fn<<<grid_for((const void*)fn, ngroups, TPB_LARGE), TPB_LARGE, 0, st>>>(a, kp, kl, k01, ktr, tpl);
+    } else if (prm->tape == BC_TAPE_COMPACT && BC_SEND_TABLES) {
+      SendPre sp{};
+      sp.tpa = make_keypre(s01, L_TAPEA);
+      sp.tpb = make_keypre(s01, L_TAPEB);
+      if (RELU) sp.tra = make_keypre(str, party == 0 ? L_A02 : L_A12);
+      if (!RELU && y0) sp.resp = make_keypre(str, L_RESP);
+      const bool fhi = kp.fhi != 0, hi0 = base + n <= (1ull << 34);
+      auto pick = [&](auto P) {
+        constexpr int PARTY = decltype(P)::value;
+        return fhi ? (hi0 ? k_send_t<R, PARTY, RELU, true, true> : k_send_t<R, PARTY, RELU, true, false>)
+                   : (hi0 ? k_send_t<R, PARTY, RELU, false, true> : k_send_t<R, PARTY, RELU, false, false>);
+      };
+      auto fn = party == 0 ? pick(std::integral_constant<int, 0>{}) : pick(std::integral_constant<int, 1>{});
+      const int rc = allow_smem((const void*)fn, kSendTabBytes);
+      if (rc) return rc;
+      fn<<<grid_for((const void*)fn, ngroups, TPB_ST, kSendTabBytes), TPB_ST, kSendTabBytes, st>>>(a, kp, k01, ktr, sp);
     } else if (prm->tape == BC_TAPE_COMPACT) {
       if (party == 0) go(k_send_c<R, 0, RELU>);
       else go(k_send_c<R, 1, RELU>);
@@ -490,18 +617,27 @@ int helper(const uint8_t* lo0, const uint8_t* hi0, const uint8_t* lo1, const uin
     return BC_EALIAS;
   HelperArgs a{lo0, hi0, lo1, hi1, out0, out0b, out1, (uint64_t)n, base};
   const KP kp = make_kp(prm);
-  const Key k02 = make_key(s02);
-  const Key k12 = RELU ? make_key(s12) : Key{};
+  StreamPre sp{};
+  if (RELU) {
+    sp.b02 = make_keypre(s02, L_B02);
+    sp.a02 = make_keypre(s02, L_A02);
+    sp.c02 = make_keypre(s02, L_C02);
+    sp.b12 = make_keypre(s12, L_B12);
+    sp.a12 = make_keypre(s12, L_A12);
+  } else {
+    sp.resp = make_keypre(s02, L_RESP);
+  }
+  const bool c32 = base + n <= (1ull << 35);  // every counter j / 8 below 2^32
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint64_t ngroups = (n + 7) / 8;
   return dispatch_rounds(prm->rounds, [&](auto Rc) {
     constexpr int R = decltype(Rc)::value;
     if (large) {
-      auto fn = k_helper_l<R, RELU>;
-      fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, make_kpl(prm), k02, k12);
+      auto fn = c32 ? k_helper_l<R, RELU, true> : k_helper_l<R, RELU, false>;
+      fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, make_kpl(prm), sp);
     } else {
-      auto fn = k_helper<R, RELU>;
-      fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, k02, k12);
+      auto fn = c32 ? k_helper<R, RELU, true> : k_helper<R, RELU, false>;
+      fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, sp);
     }
     return check_launch();
   });
@@ -527,14 +663,25 @@ int finish(int party, const uint64_t* x, const uint8_t* tbits, const uint64_t* r
     return BC_EALIAS;
   FinishArgs a{x, tbits, resp, d_own, d_peer, party == 1 ? c1 : nullptr, y, (uint64_t)n, base};
   const KP kp = make_kp(prm);
-  const Key ks = seed ? make_key(seed) : Key{};
+  StreamPre sp{};  // the finishing party's own seed: seed02 (P0) or seed12 (P1)
+  if (seed) {
+    if (!RELU) {
+      sp.resp = make_keypre(seed, L_RESP);
+    } else if (party == 0) {
+      sp.b02 = make_keypre(seed, L_B02);
+      sp.c02 = make_keypre(seed, L_C02);
+    } else {
+      sp.b12 = make_keypre(seed, L_B12);
+    }
+  }
+  const bool hi0 = base + n <= (1ull << 35);  // every counter j / 8 below 2^32
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint64_t ngroups = (n + 7) / 8;
   return dispatch_rounds(prm->rounds, [&](auto Rc) {
     constexpr int R = decltype(Rc)::value;
-    auto go = [&](auto fn) { fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, ks); };
-    if (party == 0) go(k_finish<R, 0, RELU>);
-    else go(k_finish<R, 1, RELU>);
+    auto go = [&](auto fn) { fn<<<grid_for((const void*)fn, ngroups), TPB, 0, st>>>(a, kp, sp); };
+    if (party == 0) hi0 ? go(k_finish<R, 0, RELU, true>) : go(k_finish<R, 0, RELU, false>);
+    else hi0 ? go(k_finish<R, 1, RELU, true>) : go(k_finish<R, 1, RELU, false>);
     return check_launch();
   });
 }

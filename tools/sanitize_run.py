@@ -8,7 +8,7 @@ from paper_2309_04909_b200 import api
 dev = "cuda:0"
 sd = synth.seeds(0)
 def t(a): return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).to(dev)
-for kw in (dict(), dict(ell=16, lx=7, f=0, mode="literal"), dict(ell=32, lx=5, f=3)):
+for kw in (dict(), dict(ell=16, lx=7, f=0, mode="literal"), dict(ell=32, lx=5, f=3), dict(mode="literal")):
     prm = api.Params(**kw, rounds=8)
     for n in (1, 13, 1003):
         x, x0, x1 = synth.shares(n, prm.ell, prm.lx, prm.f, "D1")
@@ -19,6 +19,12 @@ for kw in (dict(), dict(ell=16, lx=7, f=0, mode="literal"), dict(ell=32, lx=5, f
         api.drelu(a0, a1, prm, sd, 16)
         api.relu(a0, a1, prm, sd, 16)
         api.ladder_modswitch(0, a0, prm); api.ladder_modswitch(1, a1, prm)
+        api.ladder_modswitch64(0, a0, prm); api.ladder_modswitch64(1, a1, prm)
+        api.modswitch64(0, a0, 32, (1 << 32) + 15); api.modswitch64(1, a1, 63, (1 << 64) - 59)
+        if prm.ell == 64 and prm.mode == "guard":  # the materialize2 instantiation (bench knob)
+            os.environ["BICOPTOR_MATERIALIZE"] = "2"
+            api.drelu(a0, a1, prm, sd, 24)
+            del os.environ["BICOPTOR_MATERIALIZE"]
         api.trc(0, a0, prm.ell, 3, 1); api.trc(1, a1, prm.ell, 3, 1)
         api.trc_prob(0, a0, prm.ell, 3); api.modswitch(1, a1, 7, 131)
         lo0, hi0, tb0 = api.drelu_send(0, a0, prm, sd.s01, 8)
@@ -44,6 +50,7 @@ for n in (1, 13, 1003):
     tr = api.transcript_buffers(n, dev, big)
     api.drelu(a0, a1, big, sd, 8, transcript=tr)
     api.relu(a0, a1, big, sd, 8)
+    api.ladder_modswitch64(0, a0, big); api.ladder_modswitch64(1, a1, big)
     for pk in (big, api.Params(ell=64, lx=31, f=0, mode="literal", rounds=8), api.Params(ell=24, lx=10, f=0, rounds=8)):
         x, x0, x1 = synth.shares(n, pk.ell, pk.lx, pk.f, "D1")   # party phases on the uint32 wire planes
         b0, b1 = t(x0), t(x1)
