@@ -59,6 +59,9 @@ def _worker(rank, world, port, kind, n, chunk, slots, mode, literal, runs, outdi
                                   backend=FileBackend(outdir, rank), compute=OracleApiCompute(), group=group,
                                   paper_literal=literal, triples=world // 3)
     ys = [runner.run(xs if role.party < 2 else None) for _ in range(runs)]
+    import json
+    with open(os.path.join(outdir, f"egress_{rank}.json"), "w") as fh:
+        json.dump(runner.egress_bytes_per_elem(), fh)
     runner.close()
     if role.party < 2:
         for r, y in enumerate(ys):
@@ -82,6 +85,21 @@ def test_peer_runtime_gloo_single_chunk_many_slots(tmp_path):
         ref = B.relu(o, x0, x1, np.arange(n, dtype=np.uint64) + np.uint64(r * span), synth.seeds(0))
         assert np.array_equal(np.load(tmp_path / f"y_0_{r}.npy"), ref["y0"])
         assert np.array_equal(np.load(tmp_path / f"y_1_{r}.npy"), ref["y1"])
+
+
+@pytest.mark.parametrize("mode,msg", [("guard", 9), ("literal", 8)])
+def test_peer_egress_bytes_match_table1(tmp_path, mode, msg):
+    """The bytes each party's kernels store into its peers' inboxes per element, from the
+    inbox field shapes (PeerPartyRunner.egress_bytes_per_elem): the one-pass message to P2
+    is (lx+1) ceil(log2 p) bits = 72 (guard, p = 257) or 64 (the paper's Table 1, P:93-96,
+    literal p = 131); ReLU adds [d]_b to the other computing party and e (+ [c]_1) from P2."""
+    import json
+    mp.start_processes(_worker, args=(3, _free_port(), "relu", 64, 64, 2, mode, False, 1, str(tmp_path)),
+                       nprocs=3, join=True, start_method="spawn")
+    eg = [json.load(open(tmp_path / f"egress_{r}.json")) for r in range(3)]
+    assert eg[0] == {"linkA->P2": msg, "linkE->P1": 8}
+    assert eg[1] == {"linkB->P2": msg, "linkF->P0": 8}
+    assert eg[2] == {"linkG->P0": 8, "linkH->P1": 16}
 
 
 @pytest.mark.parametrize("kind,world,slots,mode,literal", [
