@@ -54,6 +54,18 @@ __device__ __forceinline__ uint64_t mont(uint64_t a, uint64_t b, const KPL& kp) 
   return hi >= mh ? hi - mh : hi - mh + kp.p;
 }
 
+// The same product for a multiplier b shared by several a (both parties multiply by the slot's
+// rM): m = (a b mod 2^64) p^-1 = a (b p^-1) mod 2^64, so with bp = b p^-1 mod 2^64 computed once
+// per slot the low product a b is not needed -- the same m, the same result.
+__device__ __forceinline__ uint64_t mont_shared(uint64_t a, uint64_t b, uint64_t bp, const KPL& kp) {
+  const uint64_t hi = __umul64hi(a, b);
+  const uint64_t mh = __umul64hi(a * bp, kp.p);
+  return hi >= mh ? hi - mh : hi - mh + kp.p;
+}
+#ifndef BC_LARGE_MONT_SHARED
+#define BC_LARGE_MONT_SHARED 1
+#endif
+
 // BC_LARGE_FPMOD = 1: the draws' reductions u mod q (u < 2^48, the tape's draws)
 // by a binary64 quotient.  Write q = q' 2^s with q' odd; floor(u / q) =
 // floor(v / q') with v = u >> s, and for odd q' floor(v / q') = round((v -
@@ -310,9 +322,10 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
   auto slot = [&](uint32_t m, uint64_t rM, uint64_t rho) {
       uint64_t c, d;
       slot_values<W32>(s0f, n1f, idx[m * TPB_L], kp, c, d);           // v'_{Pi(m)} of each party
-      uint64_t W0 = mont(c, rM, kp) + rho;                           // steps 7-8, P0: v'r + rho
+      const uint64_t rp = rM * kp.pinv;                              // shared by both products
+      uint64_t W0 = (BC_LARGE_MONT_SHARED ? mont_shared(c, rM, rp, kp) : mont(c, rM, kp)) + rho;  // steps 7-8, P0
       W0 = W0 >= kp.p ? W0 - kp.p : W0;
-      uint64_t W1 = mont(d, rM, kp) + (kp.p - rho);                  //            P1: v'r - rho
+      uint64_t W1 = (BC_LARGE_MONT_SHARED ? mont_shared(d, rM, rp, kp) : mont(d, rM, kp)) + (kp.p - rho);  // P1
       if (TRANSCRIPT) {
         W1 = W1 >= kp.p ? W1 - kp.p : W1;
         w0[m] = W0;
@@ -355,9 +368,10 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
       large_draws<R, TPB_L>(m, j, k01, kp, stg, fbc, rM, rho);
       uint64_t c, d;
       slot_values<W32>(s0f, n1f, idx[m * TPB_L], kp, c, d);           // v'_{Pi(m)} of each party
-      uint64_t W0 = mont(c, rM, kp) + rho;                           // steps 7-8, P0: v'r + rho
+      const uint64_t rp = rM * kp.pinv;                              // shared by both products
+      uint64_t W0 = (BC_LARGE_MONT_SHARED ? mont_shared(c, rM, rp, kp) : mont(c, rM, kp)) + rho;  // steps 7-8, P0
       W0 = W0 >= kp.p ? W0 - kp.p : W0;
-      uint64_t W1 = mont(d, rM, kp) + (kp.p - rho);                  //            P1: v'r - rho
+      uint64_t W1 = (BC_LARGE_MONT_SHARED ? mont_shared(d, rM, rp, kp) : mont(d, rM, kp)) + (kp.p - rho);  // P1
       if (TRANSCRIPT) {
         W1 = W1 >= kp.p ? W1 - kp.p : W1;
         w0[m] = W0;
