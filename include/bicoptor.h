@@ -145,7 +145,11 @@ int bc_ladder_modswitch64(int party, const uint64_t *x, uint64_t *v, size_t n,
 
 /* Alg 7, all three parties simulated on one GPU in one fused
  * kernel: y0 + y1 = DReLU(x0 + x1) mod 2^ell (1 for positive, 0 for negative
- * in-band x; x = 0 gives the random bit t, reading C13).  tr may be NULL. */
+ * in-band x; x = 0 gives the random bit t, reading C13).  tr may be NULL.
+ * Without a transcript P2 tests P0's reduced message against P1's congruent
+ * integer; the environment variable BICOPTOR_MATERIALIZE=2,
+ * read on each call, selects an instantiation that reduces both messages to
+ * wire values first (a measurement knob: the outputs are identical). */
 int bc_drelu(const uint64_t *x0, const uint64_t *x1, uint64_t *y0, uint64_t *y1, size_t n,
              uint64_t elem_base, const bc_params *prm, const bc_seeds *seeds,
              const bc_transcript *tr, void *stream);
