@@ -501,6 +501,41 @@ __device__ __forceinline__ void elem_one_t2(uint64_t x, uint32_t t, uint32_t ix,
   }
 }
 
+// BC_TAB_TMA: the tables arrive by bulk asynchronous copies (TMA, cp.async.bulk, one elected
+// thread, completion counted on an mbarrier) while every thread expands its first group's
+// keystream; the first table access waits on the barrier.  Without it the CTA copies them with
+// vector loads and a __syncthreads before any work.
+#ifndef BC_TAB_TMA
+#define BC_TAB_TMA 1
+#endif
+__device__ __forceinline__ void tab_bar_init(uint64_t* bar) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// issued by one thread: 4 bulk copies of the table image (each a multiple of 16 B, < 2^20 B in total)
+__device__ __forceinline__ void tab_bulk_load(uint32_t* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(sdst);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  uint64_t g;
+  asm("cvta.to.global.u64 %0, %1;" : "=l"(g) : "l"(gsrc));  // the source operand is a .global address
+  const uint32_t q = ((bytes / 4u) + 15u) & ~15u;  // chunk size, 16-B multiple
+  for (uint32_t off = 0; off < bytes; off += q) {
+    const uint32_t sz = min(q, bytes - off);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(d + off), "l"(g + off), "r"(sz), "r"(b) : "memory");
+  }
+}
+__device__ __forceinline__ void tab_bar_wait(uint64_t* bar) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(b) : "memory");
+}
+
+
 // ---- the paper-literal domain (w = lx = 7, p = 131, 8 slots, pair tape), table form ----
 // Pair-tape draws of one element (T = its 8 keystream words):
 // t, the permutation index mod 8!, and per slot r_m = 1 + x mod 130, rho_m = x div 130

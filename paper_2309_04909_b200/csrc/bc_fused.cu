@@ -221,8 +221,16 @@ template <int R, bool RELU, bool TRANSCRIPT, bool FULL, bool FHI, int MAT = BC_M
 __global__ void __launch_bounds__(TPB_T, 1) k_fused_t(FusedArgs a, KP kp, const __grid_constant__ Key k01, Key k02, Key k12, PreKeys pk) {
   extern __shared__ uint4 smem_t[];
   uint32_t* tabs = reinterpret_cast<uint32_t*>(smem_t);
-  load_tables(tabs);
-  __syncthreads();
+  __shared__ __align__(8) uint64_t tab_bar;
+  bool tab_ready = !BC_TAB_TMA;
+  if (BC_TAB_TMA) {
+    if (threadIdx.x == 0) tab_bar_init(&tab_bar);
+    __syncthreads();
+    if (threadIdx.x == 0) tab_bulk_load(tabs, kTables.w, (uint32_t)kTabBytes, &tab_bar);
+  } else {
+    load_tables(tabs);
+    __syncthreads();
+  }
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tabs);
   const uint64_t ngroups = (a.n + 7) >> 3;
   for (uint64_t g = (uint64_t)blockIdx.x * TPB_T + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB_T) {
@@ -240,6 +248,10 @@ __global__ void __launch_bounds__(TPB_T, 1) k_fused_t(FusedArgs a, KP kp, const 
       uint32_t A[16];  // part A: words 4q..4q+3 of element 4 hb + q
       stream_blk<R, !RELU || BC_RELU_PRE, HI0>(pk.tpa, k01, L_TAPEA, (j0 >> 2) + (uint64_t)hb, A);
       const uint32_t bit0 = 1u << (4 * hb);
+      if (BC_TAB_TMA && !tab_ready) {  // the first table access of this thread: the bulk copies have landed
+        tab_bar_wait(&tab_bar);
+        tab_ready = true;
+      }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int e = 4 * hb + q;
@@ -273,6 +285,7 @@ __global__ void __launch_bounds__(TPB_T, 1) k_fused_t(FusedArgs a, KP kp, const 
     }
     finish_group<R, RELU, FULL, HI0>(a, kp, k02, k12, pk, i0, j0, cnt, zbits, tbits);
   }
+  if (BC_TAB_TMA && !tab_ready) tab_bar_wait(&tab_bar);  // no CTA exits with its bulk copies in flight
 }
 
 // The paper-literal domain at lx = 7 (BC_TAPE_COMPACT_LIT: w = 7, p = 131, 8 slots; pair
@@ -288,11 +301,17 @@ template <int R, bool RELU, bool TRANSCRIPT, bool FULL, bool FHI, bool HI0 = fal
 __global__ void __launch_bounds__(TPB_T, 1) k_fused_tl(FusedArgs a, KP kp_, const __grid_constant__ Key k01, Key k02, Key k12, PreKeys pk) {
   const KP kp = kp_literal(kp_);
   extern __shared__ uint4 smem_t[];
-  {
+  __shared__ __align__(8) uint64_t tab_bar;
+  bool tab_ready = !BC_TAB_TMA;
+  if (BC_TAB_TMA) {  // bulk copies (TMA) of the tables, overlapped with the first keystream blocks
+    if (threadIdx.x == 0) tab_bar_init(&tab_bar);
+    __syncthreads();
+    if (threadIdx.x == 0) tab_bulk_load(reinterpret_cast<uint32_t*>(smem_t), kLitTables.w, (uint32_t)kLitTabBytes, &tab_bar);
+  } else {
     const uint4* g = reinterpret_cast<const uint4*>(kLitTables.w);
     for (int i = threadIdx.x; i < kLitTabWords / 4; i += blockDim.x) smem_t[i] = g[i];
+    __syncthreads();
   }
-  __syncthreads();
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_t);
   const uint64_t ngroups = (a.n + 7) >> 3;
   for (uint64_t g = (uint64_t)blockIdx.x * TPB_T + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB_T) {
@@ -306,6 +325,10 @@ __global__ void __launch_bounds__(TPB_T, 1) k_fused_tl(FusedArgs a, KP kp_, cons
       stream_blk<R, !RELU || BC_RELU_PRE, HI0>(pk.tpa, k01, L_TAPEP, (j0 + (uint64_t)e2) >> 1, B);  // bc2.tpp1
       const ulonglong2 u0 = load2(a.x0, i0 + e2, a.n), u1 = load2(a.x1, i0 + e2, a.n);
       const uint32_t bit0 = 1u << e2;
+      if (BC_TAB_TMA && !tab_ready) {  // this thread's first table access
+        tab_bar_wait(&tab_bar);
+        tab_ready = true;
+      }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int e = e2 + h;
@@ -327,6 +350,7 @@ __global__ void __launch_bounds__(TPB_T, 1) k_fused_tl(FusedArgs a, KP kp_, cons
     }
     finish_group<R, RELU, FULL, HI0>(a, kp, k02, k12, pk, i0, j0, cnt, zbits, tbits);
   }
+  if (BC_TAB_TMA && !tab_ready) tab_bar_wait(&tab_bar);  // no CTA exits with its bulk copies in flight
 }
 
 // Pair tape (every lx <= 7 domain but the compact one: p <= 131, 3..8 slots): one

@@ -117,11 +117,17 @@ template <int R, int PARTY, bool RELU, bool FHI, bool HI0>
 __global__ void __launch_bounds__(TPB_ST, 1) k_send_t(SendArgs a, KP kp, const __grid_constant__ Key k01, Key ktr,
                                                        const __grid_constant__ SendPre sp) {
   extern __shared__ uint4 smem_st[];
-  {
+  __shared__ __align__(8) uint64_t tab_bar;
+  bool tab_ready = !BC_TAB_TMA;
+  if (BC_TAB_TMA) {  // bulk copies (TMA) of the tables, overlapped with the first keystream blocks
+    if (threadIdx.x == 0) tab_bar_init(&tab_bar);
+    __syncthreads();
+    if (threadIdx.x == 0) tab_bulk_load(reinterpret_cast<uint32_t*>(smem_st), kSendTables.w, (uint32_t)kSendTabBytes, &tab_bar);
+  } else {
     const uint4* g = reinterpret_cast<const uint4*>(kSendTables.w);
     for (int i = threadIdx.x; i < kTabWords / 4; i += blockDim.x) smem_st[i] = g[i];
+    __syncthreads();
   }
-  __syncthreads();
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_st);
   const uint64_t ngroups = (a.n + 7) >> 3;
   for (uint64_t g = (uint64_t)blockIdx.x * TPB_ST + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB_ST) {
@@ -138,6 +144,10 @@ __global__ void __launch_bounds__(TPB_ST, 1) k_send_t(SendArgs a, KP kp, const _
       uint32_t A[16];
       chacha_pre<R, HI0>(sp.tpa, (j0 >> 2) + (uint64_t)hb, A);
       uint64_t lo[4];  // the half group's low-byte planes, stored at the end of the iteration
+      if (BC_TAB_TMA && !tab_ready) {  // this thread's first table access
+        tab_bar_wait(&tab_bar);
+        tab_ready = true;
+      }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int e = 4 * hb + q;
@@ -192,6 +202,7 @@ __global__ void __launch_bounds__(TPB_ST, 1) k_send_t(SendArgs a, KP kp, const _
       store8(a.y0 + i0, y, cnt);
     }
   }
+  if (BC_TAB_TMA && !tab_ready) tab_bar_wait(&tab_bar);  // no CTA exits with its bulk copies in flight
 }
 
 // Pair tape (one seed01 block per two elements).
