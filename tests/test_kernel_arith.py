@@ -63,12 +63,33 @@ def test_mod257s_exact_below_2_18():
     assert np.array_equal(x - np.uint64(257) * q, x % np.uint64(257))
 
 
-def test_multiplicative_divisibility_test_below_2_19():
-    """257 | s  <=>  s * 257^-1 mod 2^32 <= floor((2^32-1)/257), for s < 2^19."""
-    s = np.arange(1 << 19, dtype=np.uint64)
+def test_multiplicative_divisibility_test_below_2_25():
+    """257 | s  <=>  s * 257^-1 mod 2^32 <= floor((2^32-1)/257) for every s < 2^32 (s -> s 257^-1 is a
+    bijection of Z_{2^32} taking the multiples 257 k, k <= floor((2^32-1)/257), to k); checked
+    exhaustively below 2^25, the range of P2's sums W0 + x1 in the table kernels (< 257 + 2^24),
+    and the same for 131 (the literal table kernel, sums < 2^17)."""
+    s = np.arange(1 << 25, dtype=np.uint64)
     lhs = ((s * np.uint64(0xFF00FF01)) & np.uint64(M32)) <= np.uint64(16711935)
     assert (0xFF00FF01 * 257) & M32 == 1
     assert np.array_equal(lhs, s % np.uint64(257) == 0)
+    s = np.arange(1 << 18, dtype=np.uint64)
+    assert (0xC9484E2B * 131) & M32 == 1 and (2**32 - 1) // 131 == 32786009
+    lhs = ((s * np.uint64(0xC9484E2B)) & np.uint64(M32)) <= np.uint64(32786009)
+    assert np.array_equal(lhs, s % np.uint64(131) == 0)
+
+
+def test_p2_distributive_form():
+    """P2's test by distributivity (BC_P2_DIST, elem_both_t2 / elem_both_tl): with q0 = x0 div p,
+    (W0 + x1) p^-1 = x0 p^-1 + x1 p^-1 - q0 (mod 2^32) because p p^-1 = 1; random x0 < 2^24, x1 < 2^24."""
+    rng = np.random.default_rng(11)
+    for p, inv in ((257, 0xFF00FF01), (131, 0xC9484E2B)):
+        x0 = rng.integers(0, 1 << 24, 1 << 20, dtype=np.uint64)
+        x1 = rng.integers(0, 1 << 24, 1 << 20, dtype=np.uint64)
+        q0 = x0 // np.uint64(p)
+        w0 = x0 - np.uint64(p) * q0
+        lhs = ((w0 + x1) * np.uint64(inv)) & np.uint64(M32)
+        rhs = (x0 * np.uint64(inv) + x1 * np.uint64(inv) - q0) & np.uint64(M32)
+        assert np.array_equal(lhs, rhs)
 
 
 def test_ladder_swar_all_windows():
@@ -262,3 +283,12 @@ def test_pair_tape_runtime_magic():
                             np.arange(d * 3, dtype=np.uint64), np.arange((1 << 28) - d * 3, 1 << 28, dtype=np.uint64)])
         q = ((u * np.uint64(mag)) >> np.uint64(32)) >> np.uint64(k)
         assert np.array_equal(q, u // np.uint64(d)), p
+
+
+def test_literal_table_kernel_divisions():
+    """elem_both_tl (csrc/bc_compact.cuh): x div 131 = umulhi(x, ceil(2^32/131)) for every x < 2^16
+    (P0's message x0 = v' r + rho < 130 * 130 + 131, P1's x1 < 2^16), and the wire value x - 131 q."""
+    x = np.arange(1 << 16, dtype=np.uint64)
+    q = (x * np.uint64(32786010)) >> np.uint64(32)
+    assert -(-(2**32) // 131) == 32786010
+    assert np.array_equal(q, x // np.uint64(131))
