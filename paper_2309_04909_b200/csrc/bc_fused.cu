@@ -26,6 +26,7 @@ struct FusedArgs {
 // (KeyPre, chacha_pre); BC_CHACHA_PRE = 0 runs the plain block function.
 struct PreKeys {
   KeyPre tpa, tpb, resp, a02, b02, c02, a12, b12;
+  KeyPre tri[5];  // the triple streams in the order the streamed ReLU finish consumes them: a12, a02, b02, b12, c02
 };
 #ifndef BC_CHACHA_PRE
 #define BC_CHACHA_PRE 1
@@ -35,6 +36,9 @@ struct PreKeys {
 #endif
 #ifndef BC_RELU_PRE
 #define BC_RELU_PRE 1  // the ReLU table kernel's blocks with the first-round precomputation too
+#endif
+#ifndef BC_RELU_STREAMED
+#define BC_RELU_STREAMED 0  // 1: Alg 8's five triple blocks at ONE chacha_pre call site, each consumed before the next
 #endif
 // PRE: use the precomputation at this call site.  Measured (tools/variants.py):
 // DReLU 0.490 -> 0.484 ms / 2^24; ReLU 0.860 -> 0.880 (the peeled first double
@@ -70,6 +74,68 @@ __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, c
       const uint64_t q = u64_of(Q, e);       // [D']_0 (mod 2^ell)
       y0[e] = (t + sgn * q) & ym;            // t + (1-2t)[D']_0
       y1[e] = (sgn * (z - q)) & ym;          // (1-2t)[D']_1, [D']_1 = D' - [D']_0
+    }
+  } else if (BC_RELU_STREAMED && BC_RELU_PRE) {
+    // Alg 8 with the Beaver combine regrouped so that each triple block is consumed before the
+    // next one is generated, all five at one call site (instruction cache).  With X = [x]_0 + [x]_1,
+    // d = X - a, e = z - b and P = X - [a]_1 (= d + [a]_0), in Z_{2^64}:
+    //   y0' = de + d[b]_0 + e[a]_0 + [c]_0   = (z - [b]_1) P - [a]_0 [b]_0 + [c]_0
+    //   y1' = d[b]_1 + e[a]_1 + ab - [c]_0   = [b]_1 P + z [a]_1 + [a]_0 [b]_0 - [c]_0
+    // (ring identities: the outputs are the same integers as the form below).
+    uint64_t P[8], acc0[8], acc1[8];
+#pragma unroll 1
+    for (int s = 0; s < 5; ++s) {  // pk.tri: a12, a02, b02, b12, c02; s is uniform
+      uint32_t B[16];
+      chacha_pre<R, HI0>(pk.tri[s], j0 >> 3, B);
+      if (s == 0) {  // [a]_1 (seed12)
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const ulonglong2 v0 = load2(a.x0, i0 + 2 * h, a.n), v1 = load2(a.x1, i0 + 2 * h, a.n);
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int e = 2 * h + q;
+            const uint64_t a1 = u64_of(B, e);
+            P[e] = ((q ? v0.y : v0.x) + (q ? v1.y : v1.x)) - a1;
+            acc1[e] = a1 * (uint64_t)((zbits >> e) & 1u);  // z [a]_1
+          }
+        }
+      } else if (s == 1) {  // [a]_0 (seed02), parked in acc0 until [b]_0 arrives
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc0[e] = u64_of(B, e);
+      } else if (s == 2) {  // [b]_0 (seed02)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const uint64_t m = acc0[e] * u64_of(B, e);  // [a]_0 [b]_0
+          acc0[e] = 0ull - m;
+          acc1[e] += m;
+        }
+      } else if (s == 3) {  // [b]_1 (seed12)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const uint64_t b1 = u64_of(B, e);
+          acc0[e] += ((uint64_t)((zbits >> e) & 1u) - b1) * P[e];
+          acc1[e] += b1 * P[e];
+        }
+      } else {  // [c]_0 (seed02); [c]_1 = ab - [c]_0 is P2's
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const uint64_t c0v = u64_of(B, e);
+          acc0[e] += c0v;
+          acc1[e] -= c0v;
+        }
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const ulonglong2 v0 = load2(a.x0, i0 + 2 * h, a.n), v1 = load2(a.x1, i0 + 2 * h, a.n);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int e = 2 * h + q;
+        const uint64_t t = (tbits >> e) & 1u;
+        const uint64_t sgn = 1ull - 2ull * t;
+        y0[e] = (t * (q ? v0.y : v0.x) + sgn * acc0[e]) & ym;  // t[x]_0 + (1-2t) y0'
+        y1[e] = (t * (q ? v1.y : v1.x) + sgn * acc1[e]) & ym;
+      }
     }
   } else {
     // Alg 8: triple from seed02 / seed12, e from P2, d opened by P0/P1, combine.
@@ -148,7 +214,7 @@ __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, c
 // (8 B/element) and two part-A blocks (16 B/element, 4 elements each) -- 3
 // ChaCha blocks per 8 elements, none shared between threads.
 template <int R, bool RELU, bool TRANSCRIPT, bool FULL>
-__global__ void __launch_bounds__(TPB, FUSED_MINB) k_fused_c(FusedArgs a, KP kp, Key k01, Key k02, Key k12, PreKeys pk) {
+__global__ void __launch_bounds__(TPB, FUSED_MINB) k_fused_c(FusedArgs a, KP kp, Key k01, Key k02, Key k12, const __grid_constant__ PreKeys pk) {
   __shared__ uint32_t sA[2 * PERM_A], sB[2 * PERM_B];
   build_perm_tables(sA, sB);
   __syncthreads();
@@ -218,7 +284,7 @@ __device__ __forceinline__ void load_tables(uint32_t* s) {
 }
 
 template <int R, bool RELU, bool TRANSCRIPT, bool FULL, bool FHI, int MAT = BC_MATERIALIZE, bool HI0 = false>
-__global__ void __launch_bounds__(TPB_T, 1) k_fused_t(FusedArgs a, KP kp, const __grid_constant__ Key k01, Key k02, Key k12, PreKeys pk) {
+__global__ void __launch_bounds__(TPB_T, 1) k_fused_t(FusedArgs a, KP kp, const __grid_constant__ Key k01, Key k02, Key k12, const __grid_constant__ PreKeys pk) {
   extern __shared__ uint4 smem_t[];
   uint32_t* tabs = reinterpret_cast<uint32_t*>(smem_t);
   __shared__ __align__(8) uint64_t tab_bar;
@@ -298,7 +364,7 @@ constexpr size_t kLitTabBytes = sizeof(uint32_t) * kLitTabWords;
 __device__ constexpr LiteralTables kLitTables{};
 
 template <int R, bool RELU, bool TRANSCRIPT, bool FULL, bool FHI, bool HI0 = false>
-__global__ void __launch_bounds__(TPB_T, 1) k_fused_tl(FusedArgs a, KP kp_, const __grid_constant__ Key k01, Key k02, Key k12, PreKeys pk) {
+__global__ void __launch_bounds__(TPB_T, 1) k_fused_tl(FusedArgs a, KP kp_, const __grid_constant__ Key k01, Key k02, Key k12, const __grid_constant__ PreKeys pk) {
   const KP kp = kp_literal(kp_);
   extern __shared__ uint4 smem_t[];
   __shared__ __align__(8) uint64_t tab_bar;
@@ -356,7 +422,7 @@ __global__ void __launch_bounds__(TPB_T, 1) k_fused_tl(FusedArgs a, KP kp_, cons
 // Pair tape (every lx <= 7 domain but the compact one: p <= 131, 3..8 slots): one
 // seed01 block per two elements (bc2.tpp1, 32 B each).
 template <int R, bool RELU, bool CL>
-__global__ void __launch_bounds__(TPB, 2) k_fused_w(FusedArgs a, KP kp_, Key k01, Key k02, Key k12, PreKeys pk) {
+__global__ void __launch_bounds__(TPB, 2) k_fused_w(FusedArgs a, KP kp_, Key k01, Key k02, Key k12, const __grid_constant__ PreKeys pk) {
   const KP kp = CL ? kp_literal(kp_) : kp_;
   const uint64_t ngroups = (a.n + 7) >> 3;
   for (uint64_t g = (uint64_t)blockIdx.x * TPB + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB) {
@@ -454,7 +520,7 @@ __device__ __noinline__ uint32_t fallback_b1(uint64_t j, Key key, uint32_t lim) 
 }
 
 template <int R, bool TRANSCRIPT>
-__global__ void __launch_bounds__(TPB_L) k_fused_b1(FusedArgs a, KP kp, Key k01, Key k02, Key k12, PreKeys pk) {
+__global__ void __launch_bounds__(TPB_L) k_fused_b1(FusedArgs a, KP kp, Key k01, Key k02, Key k12, const __grid_constant__ PreKeys pk) {
   __shared__ uint64_t sv[2 * 8 * TPB_L];  // [party][slot][thread]
   const uint32_t tid = threadIdx.x, S = kp.S;
   const uint64_t ym = kp.ymask;
@@ -578,7 +644,9 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
   const PreKeys pk{make_keypre(seeds->s01, tape_a), make_keypre(seeds->s01, L_TAPEB),
                    make_keypre(seeds->s02, L_RESP),  make_keypre(seeds->s02, L_A02),
                    make_keypre(seeds->s02, L_B02),   make_keypre(seeds->s02, L_C02),
-                   make_keypre(seeds->s12, L_A12),   make_keypre(seeds->s12, L_B12)};
+                   make_keypre(seeds->s12, L_A12),   make_keypre(seeds->s12, L_B12),
+                   {make_keypre(seeds->s12, L_A12), make_keypre(seeds->s02, L_A02), make_keypre(seeds->s02, L_B02),
+                    make_keypre(seeds->s12, L_B12), make_keypre(seeds->s02, L_C02)}};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint64_t ngroups = (n + 7) / 8;
   return dispatch_rounds(prm->rounds, [&](auto Rc) {
@@ -660,7 +728,9 @@ int drelu_b1(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1,
   const PreKeys pk{make_keypre(seeds->s01, L_TAPEA), make_keypre(seeds->s01, L_TAPEB),
                    make_keypre(seeds->s02, L_RESP),  make_keypre(seeds->s02, L_A02),
                    make_keypre(seeds->s02, L_B02),   make_keypre(seeds->s02, L_C02),
-                   make_keypre(seeds->s12, L_A12),   make_keypre(seeds->s12, L_B12)};
+                   make_keypre(seeds->s12, L_A12),   make_keypre(seeds->s12, L_B12),
+                   {make_keypre(seeds->s12, L_A12), make_keypre(seeds->s02, L_A02), make_keypre(seeds->s02, L_B02),
+                    make_keypre(seeds->s12, L_B12), make_keypre(seeds->s02, L_C02)}};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   return dispatch_rounds(prm->rounds, [&](auto Rc) {
     constexpr int R = decltype(Rc)::value;

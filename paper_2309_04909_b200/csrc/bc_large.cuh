@@ -210,6 +210,52 @@ __device__ __forceinline__ uint32_t large_perm(uint64_t j, const Key& k01, const
   return t;
 }
 
+// The same for S = 32 (lx = 31, the full-precision domains): the 31 swaps unrolled, the draws
+// read from the block in registers with compile-time shifts, limits and moduli.  An element
+// whose draw q rejects (~0.35 %) stages the block and finishes from q in large_perm's loop.
+#ifndef BC_LARGE_PERM32
+#define BC_LARGE_PERM32 1
+#endif
+template <int R, int TPB_L, bool PRE = false, bool HI0 = false>
+__device__ __forceinline__ uint32_t large_perm32(uint64_t j, const Key& k01, LargeIdx* idx, uint32_t* stg,
+                                                 const uint32_t* magic, const uint32_t* hlim, uint32_t& fbc,
+                                                 const KeyPre* pre = nullptr) {
+  uint32_t B[16];
+  large_block<R, TPB_L, PRE, HI0>(k01, pre, j * 7, B);
+  const uint32_t t = B[0] & 1u;
+#pragma unroll
+  for (uint32_t m = 0; m < 32; ++m) idx[m * TPB_L] = (LargeIdx)m;
+  uint32_t q0 = 32;
+#pragma unroll
+  for (uint32_t q = 1; q < 32; ++q) {
+    const uint32_t m = 32 - q, s = m + 1;
+    const uint32_t d = (B[q >> 1] >> (16 * (q & 1))) & 0xFFFFu;
+    if (__builtin_expect(d >= (65536u / s) * s, 0)) {
+      q0 = q;
+      break;
+    }
+    const uint32_t k = d % s;
+    const LargeIdx a = idx[m * TPB_L], b = idx[k * TPB_L];
+    idx[m * TPB_L] = b;
+    idx[k * TPB_L] = a;
+  }
+  if (__builtin_expect(q0 < 32, 0)) {  // a rejected draw: the generic loop from q0 on
+#pragma unroll
+    for (int w = 0; w < 16; ++w) stg[w * TPB_L] = B[w];
+#pragma unroll 1
+    for (uint32_t q = q0; q < 32; ++q) {
+      const uint32_t m = 32 - q, s = m + 1;
+      uint32_t d = (stg[(q >> 1) * TPB_L] >> (16 * (q & 1))) & 0xFFFFu;
+      while (d >= hlim[s]) d = (uint32_t)fbl_word<R>(k01, j, fbc++) & 0xFFFFu;
+      const uint32_t k = d - __umulhi(d, magic[s]) * s;
+      const LargeIdx a = idx[m * TPB_L], b = idx[k * TPB_L];
+      idx[m * TPB_L] = b;
+      idx[k * TPB_L] = a;
+    }
+  }
+  return t;
+}
+
 // 48-bit little-endian draw at byte offset `byte` (even) of the staged words.
 template <int TPB_L>
 __device__ __forceinline__ uint64_t draw48(const uint32_t* stg, uint32_t byte) {
@@ -290,6 +336,53 @@ __device__ __forceinline__ void large_draws_k(uint32_t G, uint64_t j, const Key&
 #define BC_LARGE_GROUP8 1
 #endif
 
+// ---- p = 2^32 + 15: the full-precision guard domain (w = 32, W32) -------------------------
+// A pseudo-Mersenne prime: 2^32 = -15 (mod p), so a 64-bit x = x1 2^32 + x0 folds to x0 - 15 x1
+// with two multiply-adds and no 64 x 64 products.  The slot arithmetic below runs on 32-bit
+// operands (c, d, r below 2^32: all but ~5e-9 of the slots); the rest take the generic
+// Montgomery path.  Same results: every value is the same residue (tests/test_kernel_arith.py
+// emulates fold_p15, mod_p15, mod_q15 and the zero test on edge and random inputs).
+#ifndef BC_LARGE_P15
+#define BC_LARGE_P15 1
+#endif
+constexpr uint64_t P15 = (1ull << 32) + 15ull;
+constexpr uint32_t K15 = 0x9876543Bu;  // 2^-64 mod p: r_m = rM K15 mod p (the draw's Montgomery form, C28)
+
+// x mod p up to one subtraction of p: y = x0 - 15 x1 lies in (-15 2^32, 2^32), as y1 2^32 + y0
+// with y1 in [-15, 0]; y = y0 - 15 y1 (mod p) lies in [0, 2^32 + 225].
+__device__ __forceinline__ uint64_t fold_p15(uint64_t x) {
+  const uint64_t y = (uint64_t)(uint32_t)x - (x >> 32) * 15ull;  // two's complement of the signed y
+  const int32_t y1 = (int32_t)(y >> 32);
+  return (uint64_t)(uint32_t)y + (uint64_t)(uint32_t)(-15 * y1);
+}
+// u mod p and u mod (p - 1) for u < 2^48 (the tape's draws): u0 - c u1 lies in (-c 2^16, 2^32).
+__device__ __forceinline__ uint64_t mod_p15(uint64_t u) {
+  const int64_t v = (int64_t)(uint32_t)u - (int64_t)(15u * (uint32_t)(u >> 32));
+  return (uint64_t)(v < 0 ? v + (int64_t)P15 : v);
+}
+__device__ __forceinline__ uint64_t mod_q15(uint64_t u) {
+  const int64_t v = (int64_t)(uint32_t)u - (int64_t)(14u * (uint32_t)(u >> 32));
+  return (uint64_t)(v < 0 ? v + (int64_t)(P15 - 1ull) : v);
+}
+
+// The two 48-bit draws of slot g8 + K after rejection (the exact test out of line, as large_draws_k).
+template <int R, int TPB_L, int K>
+__device__ __forceinline__ void large_raw_k(uint32_t G, uint64_t j, const Key& k01, const KPL& kp, const uint32_t* stg,
+                                            uint32_t& fbc, uint64_t& ur, uint64_t& uq) {
+  ur = draw48c<TPB_L, 6 * K>(stg, G);
+  if (__builtin_expect((uint32_t)(ur >> 32) >= (uint32_t)(kp.qlim >> 32), 0)) {
+    const Redraw d = large_redraw<R>(ur, kp.qlim, k01, j, fbc);
+    ur = d.u;
+    fbc = d.fbc;
+  }
+  uq = draw48c<TPB_L, 48 + 6 * K>(stg, G);
+  if (__builtin_expect((uint32_t)(uq >> 32) >= (uint32_t)(kp.plim >> 32), 0)) {
+    const Redraw d = large_redraw<R>(uq, kp.plim, k01, j, fbc);
+    uq = d.u;
+    fbc = d.fbc;
+  }
+}
+
 // Blocks 1 + 3h .. 3 + 3h (slot groups 2h, 2h + 1) into staged rows 0..47.
 template <int R, int TPB_L, bool PRE = false, bool HI0 = false>
 __device__ __forceinline__ void large_stage(uint32_t h, uint64_t j, const Key& k01, uint32_t* stg,
@@ -312,7 +405,8 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
                                                const KeyPre* pre = nullptr) {
   const uint32_t S = kp.S;
   uint32_t fbc = 0;  // fallback words consumed
-  const uint32_t t = large_perm<R, TPB_L, PRE, HI0>(j, k01, kp, idx, stg, magic, hlim, fbc, pre);
+  const uint32_t t = W32 && BC_LARGE_PERM32 ? large_perm32<R, TPB_L, PRE, HI0>(j, k01, idx, stg, magic, hlim, fbc, pre)
+                                             : large_perm<R, TPB_L, PRE, HI0>(j, k01, kp, idx, stg, magic, hlim, fbc, pre);
   // steps 1-2: blind both shares by (-1)^t
   const uint64_t s0 = t ? (0ull - x0) & kp.ymask : x0 & kp.ymask;
   const uint64_t s1 = t ? (0ull - x1) & kp.ymask : x1 & kp.ymask;
@@ -337,6 +431,50 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
         z |= (sum == kp.p || sum == 2 * kp.p) ? 1u : 0u;
       }
   };
+  if (W32 && !TRANSCRIPT && BC_LARGE_P15) {
+    // p = 2^32 + 15, S = 32 (every slot group full).  Per slot: r = rM K15, P0's wire value
+    // W0 = c r + rho in [0, p), P1's message d r + (p - rho) folded (congruent, below
+    // 2^32 + 226); P2: s = W0 + W1 < 3 2^32 is 0 mod p iff s0 - 15 s1 = 0 (|s0 - 15 s1| < p).
+    auto slot15 = [&](uint32_t m, uint64_t ur, uint64_t uq) {
+      const uint64_t rM = 1ull + mod_q15(ur);                          // Montgomery form of r_m (C28)
+      const uint64_t rho = mod_p15(uq);
+      uint64_t c, d;
+      slot_values<true>(s0f, n1f, idx[m * TPB_L], kp, c, d);          // c in [1, 2^32], d in [15, 2^32 + 15)
+      const uint64_t rz = fold_p15((uint64_t)(uint32_t)rM * K15);      // = r_m when below 2^32
+      const uint32_t r = (uint32_t)rz;
+      uint64_t W0 = fold_p15((uint64_t)(uint32_t)c * r + rho);         // c r + rho < 2^64
+      W0 = W0 >= P15 ? W0 - P15 : W0;                                  // P0's wire value
+      const uint64_t W1 = fold_p15((uint64_t)(uint32_t)d * r + (P15 - rho));
+      const uint64_t s = W0 + W1;
+      uint32_t zm = (uint32_t)s == 15u * (uint32_t)(s >> 32) ? 1u : 0u;
+      if (__builtin_expect((uint32_t)(c >> 32) | (uint32_t)(d >> 32) | (uint32_t)(rM >> 32) | (uint32_t)(rz >> 32), 0)) {
+        // an operand at or above 2^32 (probability ~5e-9 per slot): the generic Montgomery products
+        const uint64_t rp = rM * kp.pinv;
+        uint64_t V0 = mont_shared(c, rM, rp, kp) + rho;
+        V0 = V0 >= kp.p ? V0 - kp.p : V0;
+        const uint64_t V1 = mont_shared(d, rM, rp, kp) + (kp.p - rho);
+        const uint64_t sum = V0 + V1;
+        zm = (sum == kp.p || sum == 2 * kp.p) ? 1u : 0u;
+      }
+      z |= zm;
+    };
+#pragma unroll 1
+    for (uint32_t h = 0; h < 2; ++h) {
+      large_stage<R, TPB_L, PRE, HI0>(h, j, k01, stg, pre);
+#pragma unroll 1
+      for (uint32_t g8 = 16 * h; g8 < 16 * h + 16; g8 += 8) {
+        const uint32_t G = 24u * ((g8 >> 3) & 1u);
+        uint64_t ur, uq;
+#define BC_LARGE_SLOT(K)                                             \
+        large_raw_k<R, TPB_L, K>(G, j, k01, kp, stg, fbc, ur, uq);  \
+        slot15(g8 + K, ur, uq);
+        BC_LARGE_SLOT(0) BC_LARGE_SLOT(1) BC_LARGE_SLOT(2) BC_LARGE_SLOT(3)
+        BC_LARGE_SLOT(4) BC_LARGE_SLOT(5) BC_LARGE_SLOT(6) BC_LARGE_SLOT(7)
+#undef BC_LARGE_SLOT
+      }
+    }
+    return z | (t << 1);
+  }
   if (BC_LARGE_GROUP8) {
 #pragma unroll 1
     for (uint32_t h = 0; 16 * h < S; ++h) {
@@ -401,11 +539,46 @@ __device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, con
                                                      const KeyPre* pre = nullptr) {
   const uint32_t S = kp.S;
   uint32_t fbc = 0;
-  const uint32_t t = large_perm<R, TPB_L, PRE, HI0>(j, k01, kp, idx, stg, magic, hlim, fbc, pre);
+  const uint32_t t = W32 && BC_LARGE_PERM32 ? large_perm32<R, TPB_L, PRE, HI0>(j, k01, idx, stg, magic, hlim, fbc, pre)
+                                             : large_perm<R, TPB_L, PRE, HI0>(j, k01, kp, idx, stg, magic, hlim, fbc, pre);
   const uint64_t s = t ? (0ull - x) & kp.ymask : x & kp.ymask;                  // steps 1-2
   // P0 reads windows of s, P1 of (-s) mod 2^ell (Alg 5, readings C3, C4)
   const uint64_t sf = (PARTY == 0 ? s : (0ull - s) & kp.ymask) >> kp.f;
   uint32_t hib = 0;
+  if (W32 && BC_LARGE_P15) {  // p = 2^32 + 15, S = 32: the pseudo-Mersenne slot arithmetic of elem_large
+    auto slot15 = [&](uint32_t m, uint64_t ur, uint64_t uq) {
+      const uint64_t rM = 1ull + mod_q15(ur);
+      const uint64_t rho = mod_p15(uq);
+      uint64_t c, d;
+      slot_values<true>(sf, sf, idx[m * TPB_L], kp, c, d);            // one of the two is this party's
+      const uint64_t v = PARTY == 0 ? c : d;
+      const uint64_t rz = fold_p15((uint64_t)(uint32_t)rM * K15);      // r_m when below 2^32
+      uint64_t W = fold_p15((uint64_t)(uint32_t)v * (uint32_t)rz + (PARTY == 0 ? rho : P15 - rho));
+      W = W >= P15 ? W - P15 : W;                                      // steps 7-8, wire value in [0, p)
+      if (__builtin_expect((uint32_t)(v >> 32) | (uint32_t)(rM >> 32) | (uint32_t)(rz >> 32), 0)) {
+        W = mont(v, rM, kp) + (PARTY == 0 ? rho : kp.p - rho);        // generic path (~3e-9 of the slots)
+        W = W >= kp.p ? W - kp.p : W;
+      }
+      lo[m * stride] = (uint32_t)W;
+      hib |= (uint32_t)(W >> 32) << m;
+    };
+#pragma unroll 1
+    for (uint32_t h = 0; h < 2; ++h) {
+      large_stage<R, TPB_L, PRE, HI0>(h, j, k01, stg, pre);
+#pragma unroll 1
+      for (uint32_t g8 = 16 * h; g8 < 16 * h + 16; g8 += 8) {
+        const uint32_t G = 24u * ((g8 >> 3) & 1u);
+        uint64_t ur, uq;
+#define BC_LARGE_SLOT(K)                                             \
+        large_raw_k<R, TPB_L, K>(G, j, k01, kp, stg, fbc, ur, uq);  \
+        slot15(g8 + K, ur, uq);
+        BC_LARGE_SLOT(0) BC_LARGE_SLOT(1) BC_LARGE_SLOT(2) BC_LARGE_SLOT(3)
+        BC_LARGE_SLOT(4) BC_LARGE_SLOT(5) BC_LARGE_SLOT(6) BC_LARGE_SLOT(7)
+#undef BC_LARGE_SLOT
+      }
+    }
+    return (uint64_t)hib | ((uint64_t)t << 32);
+  }
   auto slot = [&](uint32_t m, uint64_t rM, uint64_t rho) {
       uint64_t c, d;
       slot_values<W32>(sf, sf, idx[m * TPB_L], kp, c, d);             // one of the two is this party's

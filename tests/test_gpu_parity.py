@@ -635,6 +635,24 @@ def test_full_precision_full_size_sampled(api, fn):
     assert np.array_equal(y[valid], want[valid])
 
 
+@pytest.mark.parametrize("fn", ["drelu", "relu"])
+def test_full_precision_full_size_exact(api, fn):
+    """lx = 31, f = 0, guard (p = 2^32 + 15): all 2^24 outputs of the launch the bench
+    times (no transcript, elem_base 0: the W32 kernel with the pseudo-Mersenne slot
+    arithmetic) against the scalar C oracle, element by element (Alg 7 P:875-895,
+    Alg 8)."""
+    from oracle import cref
+    n = 1 << 24
+    kw = LARGE_PARAMS[0]
+    x, x0, x1 = synth.shares(n, 64, 7, 24, "D2")
+    y0, y1 = getattr(api, fn)(dev(x0), dev(x1), api.Params(**kw), SEEDS)
+    g0, g1 = host(y0), host(y1)
+    del y0, y1
+    ref = cref.fused(B.Params(**kw), x0, x1, 0, SEEDS, relu=(fn == "relu"))
+    bad = np.flatnonzero((g0 != ref["y0"]) | (g1 != ref["y1"]))
+    assert bad.size == 0, f"{bad.size} of {n} elements differ, first at {bad[:8]}"
+
+
 def test_large_abi_errors(api):
     import ctypes
     L = api.lib()

@@ -292,3 +292,71 @@ def test_literal_table_kernel_divisions():
     q = (x * np.uint64(32786010)) >> np.uint64(32)
     assert -(-(2**32) // 131) == 32786010
     assert np.array_equal(q, x // np.uint64(131))
+
+
+# ---- large tape at p = 2^32 + 15 (csrc/bc_large.cuh, BC_LARGE_P15) -----------------------
+
+P15 = (1 << 32) + 15
+
+
+def _fold_p15(x):
+    """fold_p15 with the kernel's 32/64-bit wrap-around: y = x0 - 15 x1 (mod 2^64),
+    y1 = signed high word, result y0 + (-15 y1 mod 2^32)."""
+    y = ((x & M32) - (x >> 32) * 15) & M64
+    y1 = (y >> 32) - (1 << 32) if (y >> 63) else (y >> 32)
+    return (y & M32) + ((-15 * y1) & M32)
+
+
+def _mod_c(u, c, q):
+    v = (u & M32) - ((c * (u >> 32)) & M32)      # int64 of a u32 minus a u32 product < 2^20
+    return v + q if v < 0 else v
+
+
+def test_p15_fold_and_draw_reductions():
+    """fold_p15(x) = x mod p up to one subtraction (result <= 2^32 + 225) for every 64-bit x
+    (edges and 2e5 random); mod_p15 / mod_q15 = u mod p / u mod (p-1) for 48-bit draws;
+    K15 = 2^-64 mod p (the mask's Montgomery form, reading C28)."""
+    rng = np.random.default_rng(15)
+    xs = [0, 1, M32, 1 << 32, P15, P15 - 1, M64, M64 - 1, (M32 * M32), (M32 * M32) + P15, (1 << 63), (15 << 32), (15 << 32) - 1]
+    xs += [int(v) for v in rng.integers(0, 1 << 63, size=100000, dtype=np.uint64)]
+    xs += [int(v) | (1 << 63) for v in rng.integers(0, 1 << 63, size=100000, dtype=np.uint64)]
+    xs += [k * P15 + e for k in (1, 2, 3, (1 << 31), M32 - 1) for e in (0, 1, 14, 15, 16)]
+    for x in xs:
+        x &= M64
+        z = _fold_p15(x)
+        assert z % P15 == x % P15 and 0 <= z <= (1 << 32) + 225, x
+    us = [0, 1, (1 << 48) - 1, P15, P15 - 1, (1 << 32) - 1, 1 << 32] + \
+        [int(v) for v in rng.integers(0, 1 << 48, size=200000, dtype=np.uint64)]
+    for u in us:
+        assert _mod_c(u, 15, P15) == u % P15
+        assert _mod_c(u, 14, P15 - 1) == u % (P15 - 1)
+    assert pow(2, -64, P15) == 0x9876543B
+
+
+def test_p15_slot_zero_test():
+    """The W32 slot of elem_large: W0 = c r + rho reduced, W1 = d r + (p - rho) folded; P2's
+    test s0 == 15 s1 on s = W0 + W1 is exactly (c + d) r = 0 (mod p), i.e. c + d = 0 (r a
+    unit); and the 64-bit products plus addends never wrap for operands below 2^32."""
+    rng = np.random.default_rng(16)
+    cases = []
+    for _ in range(50000):
+        c = int(rng.integers(1, 1 << 32))
+        r = int(rng.integers(1, 1 << 32))
+        rho = int(rng.integers(0, P15))
+        d = (P15 - c) % P15 if rng.random() < 0.3 else int(rng.integers(15, 1 << 32))
+        cases.append((c, d, r, rho))
+    cases += [(M32, M32, M32, P15 - 1), (1, M32, M32, 0), (M32, 16, M32, P15 - 1), (1, M32, 1, 0),
+              (16, M32, M32, 5)]  # c + d = p: a zero slot at the operand edges
+    for c, d, r, rho in cases:
+        if d >= (1 << 32):
+            continue
+        x0 = c * r + rho
+        x1 = d * r + (P15 - rho)
+        assert x0 <= M64 and x1 <= M64
+        w0 = _fold_p15(x0)
+        w0 = w0 - P15 if w0 >= P15 else w0
+        w1 = _fold_p15(x1)
+        s = w0 + w1
+        assert s < 3 << 32
+        got = (s & M32) == 15 * (s >> 32)
+        assert got == (((c + d) * r) % P15 == 0), (c, d, r, rho)
