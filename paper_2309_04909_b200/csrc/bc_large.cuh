@@ -213,8 +213,10 @@ __device__ __forceinline__ uint32_t large_perm(uint64_t j, const Key& k01, const
 // The same for S = 32 (lx = 31, the full-precision domains): the 31 swaps unrolled, the draws
 // read from the block in registers with compile-time shifts, limits and moduli.  An element
 // whose draw q rejects (~0.35 %) stages the block and finishes from q in large_perm's loop.
+// BC_LARGE_PERM32: bit 0 the fused kernel, bit 1 the party send kernel.  Measured (DReLU, 2^24):
+// fused 7.89 -> 8.04 ms (slower: registers and instruction cache), send 7.44 -> 7.20 ms.
 #ifndef BC_LARGE_PERM32
-#define BC_LARGE_PERM32 1
+#define BC_LARGE_PERM32 2
 #endif
 template <int R, int TPB_L, bool PRE = false, bool HI0 = false>
 __device__ __forceinline__ uint32_t large_perm32(uint64_t j, const Key& k01, LargeIdx* idx, uint32_t* stg,
@@ -365,20 +367,30 @@ __device__ __forceinline__ uint64_t mod_q15(uint64_t u) {
   return (uint64_t)(v < 0 ? v + (int64_t)(P15 - 1ull) : v);
 }
 
-// The two 48-bit draws of slot g8 + K after rejection (the exact test out of line, as large_draws_k).
+// The two 48-bit draws of slot g8 + K after rejection: one branch for both (a draw can reject
+// only if its high 16 bits reach the limit's), the exact tests and redraws out of line, in draw
+// order (r_m's, then rho_m's: the fallback stream's order).
+struct Redraw2 {
+  uint64_t ur, uq;
+  uint32_t fbc;
+};
+template <int R>
+__device__ __noinline__ Redraw2 large_redraw2(uint64_t ur, uint64_t uq, uint64_t qlim, uint64_t plim, Key k01,
+                                              uint64_t j, uint32_t fbc) {
+  while (!accept64(ur, qlim)) ur = fbl_word<R>(k01, j, fbc++) & DRAW48;
+  while (!accept64(uq, plim)) uq = fbl_word<R>(k01, j, fbc++) & DRAW48;
+  return Redraw2{ur, uq, fbc};
+}
 template <int R, int TPB_L, int K>
 __device__ __forceinline__ void large_raw_k(uint32_t G, uint64_t j, const Key& k01, const KPL& kp, const uint32_t* stg,
                                             uint32_t& fbc, uint64_t& ur, uint64_t& uq) {
   ur = draw48c<TPB_L, 6 * K>(stg, G);
-  if (__builtin_expect((uint32_t)(ur >> 32) >= (uint32_t)(kp.qlim >> 32), 0)) {
-    const Redraw d = large_redraw<R>(ur, kp.qlim, k01, j, fbc);
-    ur = d.u;
-    fbc = d.fbc;
-  }
   uq = draw48c<TPB_L, 48 + 6 * K>(stg, G);
-  if (__builtin_expect((uint32_t)(uq >> 32) >= (uint32_t)(kp.plim >> 32), 0)) {
-    const Redraw d = large_redraw<R>(uq, kp.plim, k01, j, fbc);
-    uq = d.u;
+  if (__builtin_expect(((uint32_t)(ur >> 32) >= (uint32_t)(kp.qlim >> 32)) |
+                       ((uint32_t)(uq >> 32) >= (uint32_t)(kp.plim >> 32)), 0)) {
+    const Redraw2 d = large_redraw2<R>(ur, uq, kp.qlim, kp.plim, k01, j, fbc);
+    ur = d.ur;
+    uq = d.uq;
     fbc = d.fbc;
   }
 }
@@ -405,8 +417,8 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
                                                const KeyPre* pre = nullptr) {
   const uint32_t S = kp.S;
   uint32_t fbc = 0;  // fallback words consumed
-  const uint32_t t = W32 && BC_LARGE_PERM32 ? large_perm32<R, TPB_L, PRE, HI0>(j, k01, idx, stg, magic, hlim, fbc, pre)
-                                             : large_perm<R, TPB_L, PRE, HI0>(j, k01, kp, idx, stg, magic, hlim, fbc, pre);
+  const uint32_t t = W32 && (BC_LARGE_PERM32 & 1) ? large_perm32<R, TPB_L, PRE, HI0>(j, k01, idx, stg, magic, hlim, fbc, pre)
+                                                   : large_perm<R, TPB_L, PRE, HI0>(j, k01, kp, idx, stg, magic, hlim, fbc, pre);
   // steps 1-2: blind both shares by (-1)^t
   const uint64_t s0 = t ? (0ull - x0) & kp.ymask : x0 & kp.ymask;
   const uint64_t s1 = t ? (0ull - x1) & kp.ymask : x1 & kp.ymask;
@@ -539,8 +551,8 @@ __device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, con
                                                      const KeyPre* pre = nullptr) {
   const uint32_t S = kp.S;
   uint32_t fbc = 0;
-  const uint32_t t = W32 && BC_LARGE_PERM32 ? large_perm32<R, TPB_L, PRE, HI0>(j, k01, idx, stg, magic, hlim, fbc, pre)
-                                             : large_perm<R, TPB_L, PRE, HI0>(j, k01, kp, idx, stg, magic, hlim, fbc, pre);
+  const uint32_t t = W32 && (BC_LARGE_PERM32 & 2) ? large_perm32<R, TPB_L, PRE, HI0>(j, k01, idx, stg, magic, hlim, fbc, pre)
+                                                   : large_perm<R, TPB_L, PRE, HI0>(j, k01, kp, idx, stg, magic, hlim, fbc, pre);
   const uint64_t s = t ? (0ull - x) & kp.ymask : x & kp.ymask;                  // steps 1-2
   // P0 reads windows of s, P1 of (-s) mod 2^ell (Alg 5, readings C3, C4)
   const uint64_t sf = (PARTY == 0 ? s : (0ull - s) & kp.ymask) >> kp.f;
