@@ -9,7 +9,9 @@
 //               is its Montgomery form), then 8 reshares (u -> rho_m = u mod p),
 // streamed 3 blocks (two slot groups) at a time through shared memory.
 // Arithmetic mod p: one Montgomery product (R = 2^64) per party and slot,
-// W = REDC(v' rM) = v' r; binary64 quotients for the draws.  The permutation
+// W = REDC(v' rM) = v' r; binary64 quotients for the draws.  At p = 2^32 + 15
+// (the full-precision guard domain, W32) the slot runs on 32-bit operands with
+// pseudo-Mersenne folds instead (fold_p15; BC_LARGE_P15).  The permutation
 // is a word table per thread in shared memory ([slot][thread]) and is applied
 // by evaluating slot m's source window v'_{Pi(m)} directly from the share.
 #pragma once
