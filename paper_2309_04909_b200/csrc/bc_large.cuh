@@ -16,6 +16,7 @@
 // by evaluating slot m's source window v'_{Pi(m)} directly from the share.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #include "bc_device.cuh"
 
@@ -144,7 +145,10 @@ __device__ __forceinline__ void slot_values(uint64_t s0f, uint64_t n1f, uint32_t
   d = (uint64_t)dv + kp.off1;                                          //                 P1: p + d - 2^w
 }
 
-constexpr int TPB_LARGE = 128;  // threads per CTA of the large-tape kernels (shared tables are [32][TPB_LARGE])
+#ifndef BC_TPB_LARGE
+#define BC_TPB_LARGE 128
+#endif
+constexpr int TPB_LARGE = BC_TPB_LARGE;  // threads per CTA of the large-tape kernels (shared tables are [32][TPB_LARGE])
 
 // The per-thread permutation table: 32-bit entries ([slot][thread] words: thread t's column sits
 // in bank t mod 32, so the Fisher-Yates swaps at random slots are conflict-free; byte entries put
@@ -369,6 +373,19 @@ __device__ __forceinline__ uint64_t mod_q15(uint64_t u) {
   return (uint64_t)(v < 0 ? v + (int64_t)(P15 - 1ull) : v);
 }
 
+// Both draws of a W32 slot on 32 bits: with m = c u1 (< 2^20), u0 - m wraps iff u0 < m and the
+// residue is then (u0 - m mod 2^32) + c; rM = 1 + (ur mod (p-1)).  Returns false (take the 64-bit
+// path: mod_q15 / mod_p15) when rM or rho reaches 2^32 (a sum below wraps: ~2^-28 per draw).
+__device__ __forceinline__ bool draws_p15(uint64_t ur, uint64_t uq, uint32_t& rM, uint32_t& rho) {
+  const uint32_t mr = 14u * (uint32_t)(ur >> 32), u0 = (uint32_t)ur;
+  const uint32_t ar = u0 < mr ? 15u : 1u;  // (p - 1) - 2^32 + 1, or 1
+  rM = (u0 - mr) + ar;
+  const uint32_t mq = 15u * (uint32_t)(uq >> 32), v0 = (uint32_t)uq;
+  const uint32_t aq = v0 < mq ? 15u : 0u;  // p - 2^32, or 0
+  rho = (v0 - mq) + aq;
+  return (rM >= ar) & (rho >= aq);         // no 32-bit wrap in the sums
+}
+
 // The two 48-bit draws of slot g8 + K after rejection: one branch for both (a draw can reject
 // only if its high 16 bits reach the limit's), the exact tests and redraws out of line, in draw
 // order (r_m's, then rho_m's: the fallback stream's order).
@@ -449,20 +466,37 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
     // p = 2^32 + 15, S = 32 (every slot group full).  Per slot: r = rM K15, P0's wire value
     // W0 = c r + rho in [0, p), P1's message d r + (p - rho) folded (congruent, below
     // 2^32 + 226); P2: s = W0 + W1 < 3 2^32 is 0 mod p iff s0 - 15 s1 = 0 (|s0 - 15 s1| < p).
-    auto slot15 = [&](uint32_t m, uint64_t ur, uint64_t uq) {
-      const uint64_t rM = 1ull + mod_q15(ur);                          // Montgomery form of r_m (C28)
-      const uint64_t rho = mod_p15(uq);
-      uint64_t c, d;
-      slot_values<true>(s0f, n1f, idx[m * TPB_L], kp, c, d);          // c in [1, 2^32], d in [15, 2^32 + 15)
-      const uint64_t rz = fold_p15((uint64_t)(uint32_t)rM * K15);      // = r_m when below 2^32
+    const uint32_t l0 = (uint32_t)s0f, h0 = (uint32_t)(s0f >> 32), l1 = (uint32_t)n1f, h1 = (uint32_t)(n1f >> 32);
+    // Slot g8 + K of the staged groups: one branch per slot covers the draws' rejection (the
+    // exact test and the fallback stream, in draw order) and every operand at or above 2^32.
+    auto slot15 = [&](auto Kc, uint32_t G, uint32_t m) {
+      constexpr int K = decltype(Kc)::value;
+      uint64_t ur = draw48c<TPB_L, 6 * K>(stg, G), uq = draw48c<TPB_L, 48 + 6 * K>(stg, G);
+      const bool rej = ((uint32_t)(ur >> 32) >= (uint32_t)(kp.qlim >> 32)) | ((uint32_t)(uq >> 32) >= (uint32_t)(kp.plim >> 32));
+      uint32_t rM32, rho32;                                            // Montgomery form of r_m (C28), rho_m
+      const bool ok = draws_p15(ur, uq, rM32, rho32);
+      // steps 3-5 for slot i = Pi(m) (slot_values<true> on 32 bits): c = 2^32 and d >= 2^32 are flagged
+      const uint32_t i = idx[m * TPB_L];
+      const bool last = i == 31u;                                      // slot lx has no successor
+      const uint32_t cv = __funnelshift_r(l0, h0, i) + (last ? 0u : __funnelshift_rc(l0, h0, i + 1)) - 1u;
+      const uint32_t d32 = 15u - (__funnelshift_r(l1, h1, i) + (last ? 0u : __funnelshift_rc(l1, h1, i + 1)));
+      const uint64_t rz = fold_p15((uint64_t)rM32 * K15);              // = r_m when below 2^32
       const uint32_t r = (uint32_t)rz;
-      uint64_t W0 = fold_p15((uint64_t)(uint32_t)c * r + rho);         // c r + rho < 2^64
+      uint64_t W0 = fold_p15((uint64_t)cv * r + rho32);                // c r + rho < 2^64
       W0 = W0 >= P15 ? W0 - P15 : W0;                                  // P0's wire value
-      const uint64_t W1 = fold_p15((uint64_t)(uint32_t)d * r + (P15 - rho));
-      const uint64_t s = W0 + W1;
-      uint32_t zm = (uint32_t)s == 15u * (uint32_t)(s >> 32) ? 1u : 0u;
-      if (__builtin_expect((uint32_t)(c >> 32) | (uint32_t)(d >> 32) | (uint32_t)(rM >> 32) | (uint32_t)(rz >> 32), 0)) {
-        // an operand at or above 2^32 (probability ~5e-9 per slot): the generic Montgomery products
+      const uint64_t W1 = fold_p15((uint64_t)d32 * r + (P15 - rho32));
+      const uint64_t sm = W0 + W1;
+      uint32_t zm = (uint32_t)sm == 15u * (uint32_t)(sm >> 32) ? 1u : 0u;
+      if (__builtin_expect(rej | !ok | (cv == 0u) | (d32 < 15u) | ((uint32_t)(rz >> 32) != 0u), 0)) {
+        if (rej) {
+          const Redraw2 dr = large_redraw2<R>(ur, uq, kp.qlim, kp.plim, k01, j, fbc);
+          ur = dr.ur;
+          uq = dr.uq;
+          fbc = dr.fbc;
+        }
+        uint64_t c, d;
+        slot_values<true>(s0f, n1f, i, kp, c, d);
+        const uint64_t rM = 1ull + mod_q15(ur), rho = mod_p15(uq);
         const uint64_t rp = rM * kp.pinv;
         uint64_t V0 = mont_shared(c, rM, rp, kp) + rho;
         V0 = V0 >= kp.p ? V0 - kp.p : V0;
@@ -478,13 +512,11 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
 #pragma unroll 1
       for (uint32_t g8 = 16 * h; g8 < 16 * h + 16; g8 += 8) {
         const uint32_t G = 24u * ((g8 >> 3) & 1u);
-        uint64_t ur, uq;
-#define BC_LARGE_SLOT(K)                                             \
-        large_raw_k<R, TPB_L, K>(G, j, k01, kp, stg, fbc, ur, uq);  \
-        slot15(g8 + K, ur, uq);
-        BC_LARGE_SLOT(0) BC_LARGE_SLOT(1) BC_LARGE_SLOT(2) BC_LARGE_SLOT(3)
-        BC_LARGE_SLOT(4) BC_LARGE_SLOT(5) BC_LARGE_SLOT(6) BC_LARGE_SLOT(7)
-#undef BC_LARGE_SLOT
+        using std::integral_constant;
+        slot15(integral_constant<int, 0>{}, G, g8 + 0); slot15(integral_constant<int, 1>{}, G, g8 + 1);
+        slot15(integral_constant<int, 2>{}, G, g8 + 2); slot15(integral_constant<int, 3>{}, G, g8 + 3);
+        slot15(integral_constant<int, 4>{}, G, g8 + 4); slot15(integral_constant<int, 5>{}, G, g8 + 5);
+        slot15(integral_constant<int, 6>{}, G, g8 + 6); slot15(integral_constant<int, 7>{}, G, g8 + 7);
       }
     }
     return z | (t << 1);
@@ -560,17 +592,31 @@ __device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, con
   const uint64_t sf = (PARTY == 0 ? s : (0ull - s) & kp.ymask) >> kp.f;
   uint32_t hib = 0;
   if (W32 && BC_LARGE_P15) {  // p = 2^32 + 15, S = 32: the pseudo-Mersenne slot arithmetic of elem_large
-    auto slot15 = [&](uint32_t m, uint64_t ur, uint64_t uq) {
-      const uint64_t rM = 1ull + mod_q15(ur);
-      const uint64_t rho = mod_p15(uq);
-      uint64_t c, d;
-      slot_values<true>(sf, sf, idx[m * TPB_L], kp, c, d);            // one of the two is this party's
-      const uint64_t v = PARTY == 0 ? c : d;
-      const uint64_t rz = fold_p15((uint64_t)(uint32_t)rM * K15);      // r_m when below 2^32
-      uint64_t W = fold_p15((uint64_t)(uint32_t)v * (uint32_t)rz + (PARTY == 0 ? rho : P15 - rho));
+    const uint32_t l0 = (uint32_t)sf, h0 = (uint32_t)(sf >> 32);
+    auto slot15 = [&](auto Kc, uint32_t G, uint32_t m) {
+      constexpr int K = decltype(Kc)::value;
+      uint64_t ur = draw48c<TPB_L, 6 * K>(stg, G), uq = draw48c<TPB_L, 48 + 6 * K>(stg, G);
+      const bool rej = ((uint32_t)(ur >> 32) >= (uint32_t)(kp.qlim >> 32)) | ((uint32_t)(uq >> 32) >= (uint32_t)(kp.plim >> 32));
+      uint32_t rM32, rho32;
+      const bool ok = draws_p15(ur, uq, rM32, rho32);
+      const uint32_t i = idx[m * TPB_L];
+      const uint32_t ws = __funnelshift_r(l0, h0, i) + (i == 31u ? 0u : __funnelshift_rc(l0, h0, i + 1));
+      const uint32_t v32 = PARTY == 0 ? ws - 1u : 15u - ws;            // c (flag c = 2^32) / d (flag d >= 2^32)
+      const bool vbad = PARTY == 0 ? v32 == 0u : v32 < 15u;
+      const uint64_t rz = fold_p15((uint64_t)rM32 * K15);              // r_m when below 2^32
+      uint64_t W = fold_p15((uint64_t)v32 * (uint32_t)rz + (PARTY == 0 ? (uint64_t)rho32 : P15 - rho32));
       W = W >= P15 ? W - P15 : W;                                      // steps 7-8, wire value in [0, p)
-      if (__builtin_expect((uint32_t)(v >> 32) | (uint32_t)(rM >> 32) | (uint32_t)(rz >> 32), 0)) {
-        W = mont(v, rM, kp) + (PARTY == 0 ? rho : kp.p - rho);        // generic path (~3e-9 of the slots)
+      if (__builtin_expect(rej | !ok | vbad | ((uint32_t)(rz >> 32) != 0u), 0)) {
+        if (rej) {
+          const Redraw2 dr = large_redraw2<R>(ur, uq, kp.qlim, kp.plim, k01, j, fbc);
+          ur = dr.ur;
+          uq = dr.uq;
+          fbc = dr.fbc;
+        }
+        uint64_t c, d;
+        slot_values<true>(sf, sf, i, kp, c, d);
+        const uint64_t rM = 1ull + mod_q15(ur), rho = mod_p15(uq);
+        W = mont(PARTY == 0 ? c : d, rM, kp) + (PARTY == 0 ? rho : kp.p - rho);  // generic path
         W = W >= kp.p ? W - kp.p : W;
       }
       lo[m * stride] = (uint32_t)W;
@@ -582,13 +628,11 @@ __device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, con
 #pragma unroll 1
       for (uint32_t g8 = 16 * h; g8 < 16 * h + 16; g8 += 8) {
         const uint32_t G = 24u * ((g8 >> 3) & 1u);
-        uint64_t ur, uq;
-#define BC_LARGE_SLOT(K)                                             \
-        large_raw_k<R, TPB_L, K>(G, j, k01, kp, stg, fbc, ur, uq);  \
-        slot15(g8 + K, ur, uq);
-        BC_LARGE_SLOT(0) BC_LARGE_SLOT(1) BC_LARGE_SLOT(2) BC_LARGE_SLOT(3)
-        BC_LARGE_SLOT(4) BC_LARGE_SLOT(5) BC_LARGE_SLOT(6) BC_LARGE_SLOT(7)
-#undef BC_LARGE_SLOT
+        using std::integral_constant;
+        slot15(integral_constant<int, 0>{}, G, g8 + 0); slot15(integral_constant<int, 1>{}, G, g8 + 1);
+        slot15(integral_constant<int, 2>{}, G, g8 + 2); slot15(integral_constant<int, 3>{}, G, g8 + 3);
+        slot15(integral_constant<int, 4>{}, G, g8 + 4); slot15(integral_constant<int, 5>{}, G, g8 + 5);
+        slot15(integral_constant<int, 6>{}, G, g8 + 6); slot15(integral_constant<int, 7>{}, G, g8 + 7);
       }
     }
     return (uint64_t)hib | ((uint64_t)t << 32);

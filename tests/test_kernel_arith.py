@@ -330,6 +330,22 @@ def test_p15_fold_and_draw_reductions():
     for u in us:
         assert _mod_c(u, 15, P15) == u % P15
         assert _mod_c(u, 14, P15 - 1) == u % (P15 - 1)
+    # draws_p15: the same reductions on 32 bits, with the wrap flag exactly "result >= 2^32"
+    edge = [(k << 32) + e for k in (0, 1, 2, 0xFFFF) for e in
+            (0, 1, 13, 14, 15, 16, 14 * k, 15 * k, 14 * k - 1, 15 * k - 1, M32, M32 - 14)]
+    for u in us[:50000] + [v & ((1 << 48) - 1) for v in edge if v >= 0]:
+        for v in (u, (u * 7919) & ((1 << 48) - 1)):
+            mr, u0 = (14 * (u >> 32)) & M32, u & M32
+            ar = 15 if u0 < mr else 1
+            rM = ((u0 - mr) + ar) & M32
+            mq, v0 = (15 * (v >> 32)) & M32, v & M32
+            aq = 15 if v0 < mq else 0
+            rho = ((v0 - mq) + aq) & M32
+            want_r, want_q = 1 + u % (P15 - 1), v % P15
+            ok = rM >= ar and rho >= aq
+            assert ok == (want_r < (1 << 32) and want_q < (1 << 32)), (u, v)
+            if ok:
+                assert rM == want_r and rho == want_q
     assert pow(2, -64, P15) == 0x9876543B
 
 
