@@ -490,12 +490,12 @@ __global__ void __launch_bounds__(TPB_L, BC_LARGE_MINB) k_fused_l(FusedArgs a, K
       uint64_t* w0 = TRANSCRIPT ? reinterpret_cast<uint64_t*>(a.w0lo) + i * kl.S : nullptr;
       uint64_t* w1 = TRANSCRIPT ? reinterpret_cast<uint64_t*>(a.w1lo) + i * kl.S : nullptr;
       const uint32_t r =
-          elem_large<R, TRANSCRIPT, TPB_L, BC_LARGE_PRE != 0, HI0, W32>(__ldg(a.x0 + i), __ldg(a.x1 + i), j0 + e, k01, kl, idx,
+          elem_large<R, TRANSCRIPT, TPB_L, BC_LARGE_PRE != 0, HI0, W32, RELU>(__ldg(a.x0 + i), __ldg(a.x1 + i), j0 + e, k01, kl, idx,
                                                                     stg, magic, hlim, w0, w1, &pk.tpa);
       zbits |= (r & 1u) << e;
       tbits |= (r >> 1) << e;
     }
-    finish_group<R, RELU, false>(a, kp, k02, k12, pk, i0, j0, cnt, zbits, tbits);
+    finish_group<R, RELU, false, HI0>(a, kp, k02, k12, pk, i0, j0, cnt, zbits, tbits);
   }
 }
 

@@ -219,10 +219,11 @@ __device__ __forceinline__ uint32_t large_perm(uint64_t j, const Key& k01, const
 // The same for S = 32 (lx = 31, the full-precision domains): the 31 swaps unrolled, the draws
 // read from the block in registers with compile-time shifts, limits and moduli.  An element
 // whose draw q rejects (~0.35 %) stages the block and finishes from q in large_perm's loop.
-// BC_LARGE_PERM32: bit 0 the fused kernel, bit 1 the party send kernel.  Measured (DReLU, 2^24):
-// fused 7.89 -> 8.04 ms (slower: registers and instruction cache), send 7.44 -> 7.20 ms.
+// BC_LARGE_PERM32: bit 0 the fused DReLU kernel, bit 1 the party send kernel, bit 2 the fused ReLU
+// kernel.  Measured (2^24, with the p = 2^32 + 15 slot arithmetic): fused DReLU 7.35 -> 7.07 ms,
+// fused ReLU 7.93 -> 8.07 (slower: its Beaver finish holds more registers), send 6.95 -> 6.61.
 #ifndef BC_LARGE_PERM32
-#define BC_LARGE_PERM32 2
+#define BC_LARGE_PERM32 3
 #endif
 template <int R, int TPB_L, bool PRE = false, bool HI0 = false>
 __device__ __forceinline__ uint32_t large_perm32(uint64_t j, const Key& k01, LargeIdx* idx, uint32_t* stg,
@@ -429,14 +430,14 @@ __device__ __forceinline__ void large_stage(uint32_t h, uint64_t j, const Key& k
 
 // Alg 7 steps 1-9 for element j with shares x0, x1 (both computing parties and
 // P2's zero test): returns DReLU' (bit 0) and t (bit 1).
-template <int R, bool TRANSCRIPT, int TPB_L, bool PRE = false, bool HI0 = false, bool W32 = false>
+template <int R, bool TRANSCRIPT, int TPB_L, bool PRE = false, bool HI0 = false, bool W32 = false, bool RELU = false>
 __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_t j, const Key& k01, const KPL& kp,
                                                LargeIdx* idx, uint32_t* stg, const uint32_t* magic,
                                                const uint32_t* hlim, uint64_t* w0, uint64_t* w1,
                                                const KeyPre* pre = nullptr) {
   const uint32_t S = kp.S;
   uint32_t fbc = 0;  // fallback words consumed
-  const uint32_t t = W32 && (BC_LARGE_PERM32 & 1) ? large_perm32<R, TPB_L, PRE, HI0>(j, k01, idx, stg, magic, hlim, fbc, pre)
+  const uint32_t t = W32 && (BC_LARGE_PERM32 & (RELU ? 4 : 1)) ? large_perm32<R, TPB_L, PRE, HI0>(j, k01, idx, stg, magic, hlim, fbc, pre)
                                                    : large_perm<R, TPB_L, PRE, HI0>(j, k01, kp, idx, stg, magic, hlim, fbc, pre);
   // steps 1-2: blind both shares by (-1)^t
   const uint64_t s0 = t ? (0ull - x0) & kp.ymask : x0 & kp.ymask;
