@@ -654,8 +654,13 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
     if (large) {
       const KPL kl = make_kpl(prm);
       auto fn = tr ? k_fused_l<R, RELU, true> : k_fused_l<R, RELU, false>;
-      if (!tr && base + n <= (1ull << 32) / 7)  // every tape counter 7j + b below 2^32
-        fn = kl.w == 32 ? k_fused_l<R, RELU, false, true, true> : k_fused_l<R, RELU, false, true>;
+      if (!tr) {
+        const bool hi0 = base + n <= (1ull << 32) / 7;  // every tape counter 7j + b below 2^32
+        if (kl.w == 32)  // p = 2^32 + 15: the pseudo-Mersenne slot arithmetic
+          fn = hi0 ? k_fused_l<R, RELU, false, true, true> : k_fused_l<R, RELU, false, false, true>;
+        else if (hi0)
+          fn = k_fused_l<R, RELU, false, true>;
+      }
       fn<<<grid_for((const void*)fn, ngroups, TPB_L), TPB_L, 0, st>>>(a, kp, kl, k01, k02, k12, pk);
     } else if (prm->tape == BC_TAPE_COMPACT && BC_FUSED_TABLES) {
       const bool fhi = kp.fhi != 0;

@@ -78,6 +78,10 @@ def test_random_parameters(api, case):
                 lo, hi = B.encode_msg(ref["W" + k])
                 assert np.array_equal(tr[f"w{k}_lo"].cpu().numpy(), lo)
                 assert np.array_equal(tr[f"w{k}_hi"].cpu().numpy(), hi)
+        # the same call without a transcript: the instantiation the bench times (other slot
+        # arithmetic where it differs, e.g. the p = 2^32 + 15 kernel), here at a random base
+        z0, z1 = getattr(api, fn)(dev(x0), dev(x1), prm, SEEDS, elem_base=base)
+        assert np.array_equal(host(z0), ref["y0"]) and np.array_equal(host(z1), ref["y1"]), (fn, o, n, base, "no tr")
     # the party phases on the same inputs (the message wire format of the tape)
     lo0, hi0, tb0 = api.drelu_send(0, dev(x0), prm, SEEDS.s01, base)
     lo1, hi1, tb1 = api.drelu_send(1, dev(x1), prm, SEEDS.s01, base)
