@@ -41,9 +41,10 @@ struct PreKeys {
 #define BC_RELU_STREAMED 0  // 1: Alg 8's five triple blocks at ONE chacha_pre call site, each consumed before the next
 #endif
 // PRE: use the precomputation at this call site.  Measured (tools/variants.py):
-// DReLU 0.490 -> 0.484 ms / 2^24; ReLU 0.860 -> 0.880 (the peeled first double
-// round at its seven call sites costs more instruction cache than it saves), so
-// the ReLU kernels keep the plain block function.
+// DReLU 0.490 -> 0.484 ms / 2^24; in round 1's SWAR ReLU kernel 0.860 -> 0.880 (the
+// peeled first double round at its seven call sites cost more instruction cache than
+// it saved), so k_fused_c's ReLU keeps the plain block function; the table kernels
+// (k_fused_t / k_fused_tl) take it for every block (BC_RELU_PRE, ReLU 0.804 -> 0.788).
 template <int R, bool PRE, bool HI0 = false>
 __device__ __forceinline__ void stream_blk(const KeyPre& P, const Key& k, uint64_t label, uint64_t ctr,
                                            uint32_t (&o)[16]) {

@@ -169,3 +169,38 @@ def test_elementwise_and_rss_outputs_stay_in_bounds(n):
     torch.cuda.synchronize()
     for i, b in enumerate(bands):
         assert b.intact(), i
+
+
+@pytest.mark.parametrize("n,chunk", [(1, 8), (9, 8), (1003, 64), (5000, 1024)])
+def test_host_entries_stay_in_bounds(n, chunk):
+    """bc_drelu_host / bc_relu_host (synchronous and async): pinned host inputs and outputs
+    inside canary bands, chunked H2D / kernel / D2H with a ragged last chunk; the bands of the
+    host outputs and of the device workspace stay intact and the results equal the fused call."""
+    api = _need_gpu()
+    prm = api.Params(ell=64, lx=7, f=24, mode="guard", rounds=8)
+    sd = synth.seeds(6)
+    x, x0, x1 = synth.shares(n, 64, 7, 24, "D2", run=n + 3)
+
+    def hband(vals=None):
+        raw = torch.full((PAD + 8 * n + PAD,), CANARY, dtype=torch.uint8).pin_memory()
+        t = raw[PAD:PAD + 8 * n].view(torch.int64)
+        if vals is not None:
+            t.copy_(torch.from_numpy(np.ascontiguousarray(vals).view(np.int64)))
+        return raw, t
+
+    def intact(raw):
+        r = raw.numpy()
+        return bool((r[:PAD] == CANARY).all() and (r[PAD + 8 * n:] == CANARY).all())
+
+    wsb = api.lib().bc_host_workspace_bytes(chunk)
+    ws = Banded((wsb // 8,), torch.int64)
+    for fn, host_fn in ((api.drelu, api.drelu_host), (api.relu, api.relu_host)):
+        f0, f1 = fn(_u64(x0), _u64(x1), prm, sd, 8)
+        for sync in (True, False):
+            (rx0, hx0), (rx1, hx1) = hband(x0), hband(x1)
+            (ry0, hy0), (ry1, hy1) = hband(), hband()
+            host_fn(hx0, hx1, hy0, hy1, prm, sd, ws.t, chunk, 8, sync=sync)
+            torch.cuda.synchronize()
+            assert all(intact(r) for r in (rx0, rx1, ry0, ry1)) and ws.intact(), (fn.__name__, sync)
+            assert torch.equal(hy0, f0.cpu()) and torch.equal(hy1, f1.cpu()), (fn.__name__, sync)
+            assert np.array_equal(hx0.numpy().view(np.uint64), x0)
