@@ -387,9 +387,9 @@ __device__ __forceinline__ bool draws_p15(uint64_t ur, uint64_t uq, uint32_t& rM
   return (rM >= ar) & (rho >= aq);         // no 32-bit wrap in the sums
 }
 
-// The two 48-bit draws of slot g8 + K after rejection: one branch for both (a draw can reject
-// only if its high 16 bits reach the limit's), the exact tests and redraws out of line, in draw
-// order (r_m's, then rho_m's: the fallback stream's order).
+// The exact acceptance tests and redraws of a slot's two 48-bit draws, out of line, in draw order
+// (r_m's, then rho_m's: the fallback stream's order); the W32 slot calls it when a draw's high
+// 16 bits reach the limit's (the only way it can reject).
 struct Redraw2 {
   uint64_t ur, uq;
   uint32_t fbc;
@@ -401,20 +401,6 @@ __device__ __noinline__ Redraw2 large_redraw2(uint64_t ur, uint64_t uq, uint64_t
   while (!accept64(uq, plim)) uq = fbl_word<R>(k01, j, fbc++) & DRAW48;
   return Redraw2{ur, uq, fbc};
 }
-template <int R, int TPB_L, int K>
-__device__ __forceinline__ void large_raw_k(uint32_t G, uint64_t j, const Key& k01, const KPL& kp, const uint32_t* stg,
-                                            uint32_t& fbc, uint64_t& ur, uint64_t& uq) {
-  ur = draw48c<TPB_L, 6 * K>(stg, G);
-  uq = draw48c<TPB_L, 48 + 6 * K>(stg, G);
-  if (__builtin_expect(((uint32_t)(ur >> 32) >= (uint32_t)(kp.qlim >> 32)) |
-                       ((uint32_t)(uq >> 32) >= (uint32_t)(kp.plim >> 32)), 0)) {
-    const Redraw2 d = large_redraw2<R>(ur, uq, kp.qlim, kp.plim, k01, j, fbc);
-    ur = d.ur;
-    uq = d.uq;
-    fbc = d.fbc;
-  }
-}
-
 // Blocks 1 + 3h .. 3 + 3h (slot groups 2h, 2h + 1) into staged rows 0..47.
 template <int R, int TPB_L, bool PRE = false, bool HI0 = false>
 __device__ __forceinline__ void large_stage(uint32_t h, uint64_t j, const Key& k01, uint32_t* stg,

@@ -653,6 +653,37 @@ def test_full_precision_full_size_exact(api, fn):
     assert bad.size == 0, f"{bad.size} of {n} elements differ, first at {bad[:8]}"
 
 
+@pytest.mark.parametrize("base", [0, 1 << 40])
+def test_p15_wide_operand_slots(api, base):
+    """The p = 2^32 + 15 kernels' generic path, forced: shares chosen from each element's t
+    (the oracle's tape) so that the blinded s_0 = 1 and -s_1 = 1 + k (k < 15).  Window 0 then
+    gives P0 c = 2^32 (Alg 6's image of 0) and P1 d = 2^32 + 14 - k >= 2^32 in the slot Pi
+    sends it to -- operands the 32-bit fast path flags.  Fused DReLU / ReLU (both elem_base
+    ranges: with and without the first-round precomputation) and the party phases equal the
+    oracle (Alg 7 steps 3-9)."""
+    kw = LARGE_PARAMS[0]
+    oprm, prm = B.Params(**kw), api.Params(**kw)
+    n = 203
+    j = np.arange(n, dtype=np.uint64) + np.uint64(base)
+    t = B.tape(oprm, SEEDS.s01, j)["t"].astype(np.uint64)
+    k = np.arange(n, dtype=np.uint64) % np.uint64(15)
+    with np.errstate(over="ignore"):
+        s0 = np.ones(n, dtype=np.uint64)
+        s1 = np.uint64(0) - (np.uint64(1) + k)                   # -s_1 = 1 + k
+        x0 = np.where(t == 1, np.uint64(0) - s0, s0)             # s_b = (-1)^t x_b
+        x1 = np.where(t == 1, np.uint64(0) - s1, s1)
+    for fn in ("drelu", "relu"):
+        ref = getattr(B, fn)(oprm, x0, x1, j, SEEDS)
+        y0, y1 = getattr(api, fn)(dev(x0), dev(x1), prm, SEEDS, elem_base=int(base))
+        assert np.array_equal(host(y0), ref["y0"]) and np.array_equal(host(y1), ref["y1"]), fn
+    lo0, hi0, tb0 = api.drelu_send(0, dev(x0), prm, SEEDS.s01, int(base))
+    lo1, hi1, tb1 = api.drelu_send(1, dev(x1), prm, SEEDS.s01, int(base))
+    r0, r1 = api.drelu_helper(lo0, hi0, lo1, hi1, prm, SEEDS.s02, int(base), paper_literal=True)
+    ref = B.drelu(oprm, x0, x1, j, SEEDS)
+    assert np.array_equal(host(api.drelu_finish(0, tb0, r0, prm, n, None, int(base))), ref["y0"])
+    assert np.array_equal(host(api.drelu_finish(1, tb1, r1, prm, n, None, int(base))), ref["y1"])
+
+
 def test_large_abi_errors(api):
     import ctypes
     L = api.lib()
