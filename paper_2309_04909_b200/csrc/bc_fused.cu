@@ -58,7 +58,7 @@ __device__ __forceinline__ void stream_blk(const KeyPre& P, const Key& k, uint64
 // FULL (ell = 64): every value is already reduced mod 2^ell, the masks fold away.
 // The sign (1 - 2t) is applied as a 64-bit multiply (FMA pipe) rather than as
 // negate-and-select (ALU pipe, which the ChaCha rounds saturate).
-template <int R, bool RELU, bool FULL, bool HI0 = false>
+template <int R, bool RELU, bool FULL, bool HI0 = false, bool STREAMED = (BC_RELU_STREAMED != 0)>
 __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, const Key& k02, const Key& k12,
                                              const PreKeys& pk, uint64_t i0, uint64_t j0, uint32_t cnt,
                                              uint32_t zbits, uint32_t tbits) {
@@ -76,7 +76,7 @@ __device__ __forceinline__ void finish_group(const FusedArgs& a, const KP& kp, c
       y0[e] = (t + sgn * q) & ym;            // t + (1-2t)[D']_0
       y1[e] = (sgn * (z - q)) & ym;          // (1-2t)[D']_1, [D']_1 = D' - [D']_0
     }
-  } else if (BC_RELU_STREAMED && BC_RELU_PRE) {
+  } else if (STREAMED && BC_RELU_PRE) {
     // Alg 8 with the Beaver combine regrouped so that each triple block is consumed before the
     // next one is generated, all five at one call site (instruction cache).  With X = [x]_0 + [x]_1,
     // d = X - a, e = z - b and P = X - [a]_1 (= d + [a]_0), in Z_{2^64}:
@@ -465,12 +465,18 @@ constexpr int TPB_L = TPB_LARGE;
 #ifndef BC_LARGE_PRE
 #define BC_LARGE_PRE 1  // the large tape's 7 blocks through chacha_pre (pk.tpa = (seed01, bc2.tpL2))
 #endif
+#ifndef BC_LARGE_RELU_MINB
+#define BC_LARGE_RELU_MINB 5  // resident CTAs the large-tape ReLU kernel is compiled for (register cap 102; measured 7.91 -> 7.70 ms, 4 CTAs: 8.00)
+#endif
+#ifndef BC_LARGE_RELU_STREAMED
+#define BC_LARGE_RELU_STREAMED 0  // 1: the large-tape ReLU kernel's finish with the streamed Beaver blocks (137 registers, was 124)
+#endif
 #ifndef BC_LARGE_MINB
 #define BC_LARGE_MINB 1  // resident CTAs per SM the large-tape kernel is compiled for (register cap)
 #endif
 
 template <int R, bool RELU, bool TRANSCRIPT, bool HI0 = false, bool W32 = false>
-__global__ void __launch_bounds__(TPB_L, BC_LARGE_MINB) k_fused_l(FusedArgs a, KP kp, KPL kl, Key k01, Key k02, Key k12,
+__global__ void __launch_bounds__(TPB_L, RELU ? BC_LARGE_RELU_MINB : BC_LARGE_MINB) k_fused_l(FusedArgs a, KP kp, KPL kl, Key k01, Key k02, Key k12,
                                                                   const __grid_constant__ PreKeys pk) {
   __shared__ LargeIdx sidx[32 * TPB_L];
   __shared__ uint32_t sstg[LARGE_STG_ROWS * TPB_L];
@@ -496,7 +502,7 @@ __global__ void __launch_bounds__(TPB_L, BC_LARGE_MINB) k_fused_l(FusedArgs a, K
       zbits |= (r & 1u) << e;
       tbits |= (r >> 1) << e;
     }
-    finish_group<R, RELU, false, HI0>(a, kp, k02, k12, pk, i0, j0, cnt, zbits, tbits);
+    finish_group<R, RELU, false, HI0, BC_LARGE_RELU_STREAMED != 0>(a, kp, k02, k12, pk, i0, j0, cnt, zbits, tbits);
   }
 }
 
