@@ -475,7 +475,7 @@ constexpr int TPB_L = TPB_LARGE;
 #define BC_LARGE_MINB 1  // resident CTAs per SM the large-tape kernel is compiled for (register cap)
 #endif
 
-template <int R, bool RELU, bool TRANSCRIPT, bool HI0 = false, bool W32 = false>
+template <int R, bool RELU, bool TRANSCRIPT, bool HI0 = false, bool W32 = false, bool L31 = false>
 __global__ void __launch_bounds__(TPB_L, RELU ? BC_LARGE_RELU_MINB : BC_LARGE_MINB) k_fused_l(FusedArgs a, KP kp, KPL kl, Key k01, Key k02, Key k12,
                                                                   const __grid_constant__ PreKeys pk) {
   __shared__ LargeIdx sidx[32 * TPB_L];
@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(TPB_L, RELU ? BC_LARGE_RELU_MINB : BC_LARGE_MI
       uint64_t* w0 = TRANSCRIPT ? reinterpret_cast<uint64_t*>(a.w0lo) + i * kl.S : nullptr;
       uint64_t* w1 = TRANSCRIPT ? reinterpret_cast<uint64_t*>(a.w1lo) + i * kl.S : nullptr;
       const uint32_t r =
-          elem_large<R, TRANSCRIPT, TPB_L, BC_LARGE_PRE != 0, HI0, W32, RELU>(__ldg(a.x0 + i), __ldg(a.x1 + i), j0 + e, k01, kl, idx,
+          elem_large<R, TRANSCRIPT, TPB_L, BC_LARGE_PRE != 0, HI0, W32, RELU, L31>(__ldg(a.x0 + i), __ldg(a.x1 + i), j0 + e, k01, kl, idx,
                                                                     stg, magic, hlim, w0, w1, &pk.tpa);
       zbits |= (r & 1u) << e;
       tbits |= (r >> 1) << e;
@@ -665,6 +665,8 @@ int fused(const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1, si
         const bool hi0 = base + n <= (1ull << 32) / 7;  // every tape counter 7j + b below 2^32
         if (kl.w == 32)  // p = 2^32 + 15: the pseudo-Mersenne slot arithmetic
           fn = hi0 ? k_fused_l<R, RELU, false, true, true> : k_fused_l<R, RELU, false, false, true>;
+        else if (kl.w == 31 && kl.S == 32 && kl.p == P31)  // the paper-literal full precision, p = 2^31 + 11
+          fn = hi0 ? k_fused_l<R, RELU, false, true, false, true> : k_fused_l<R, RELU, false, false, false, true>;
         else if (hi0)
           fn = k_fused_l<R, RELU, false, true>;
       }

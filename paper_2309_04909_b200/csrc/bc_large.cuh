@@ -387,6 +387,33 @@ __device__ __forceinline__ bool draws_p15(uint64_t ur, uint64_t uq, uint32_t& rM
   return (rM >= ar) & (rho >= aq);         // no 32-bit wrap in the sums
 }
 
+// ---- p = 2^31 + 11: the paper-literal full-precision domain (w = 31, "31 * 31 ~ 1,000 bits") ----
+// 2^32 = -22 (mod p) and 2^32 = -20 (mod p - 1); every operand (c, d, r, rho < p) is a 32-bit word,
+// so there is no wide-operand path.  x < 2^63: y = x0 - 22 x1 in (-2^35, 2^32), y = y1 2^32 + y0 with
+// y1 in [-8, 0], and y0 - 22 y1 in [0, 2^32 + 176] (< 3p): fold31 stops there, red31 finishes.
+#ifndef BC_LARGE_P31
+#define BC_LARGE_P31 1
+#endif
+constexpr uint64_t P31 = (1ull << 31) + 11ull;
+constexpr uint32_t K31 = 0x5E69C906u;  // 2^-64 mod p
+__device__ __forceinline__ uint64_t fold31(uint64_t x) {
+  const uint64_t y = (uint64_t)(uint32_t)x - (x >> 32) * 22ull;
+  const int32_t y1 = (int32_t)(y >> 32);
+  return (uint64_t)(uint32_t)y + (uint64_t)(uint32_t)(-22 * y1);
+}
+__device__ __forceinline__ uint32_t red31(uint64_t x) {
+  const uint64_t z = fold31(x);
+  return (uint32_t)(z >= P31 ? (z >= 2 * P31 ? z - 2 * P31 : z - P31) : z);
+}
+// u mod M for u < 2^48 and M = 2^31 + c' (c = 2^32 mod M taken negative: 22 for p, 20 for p - 1):
+// v = u0 - c u1 on 32 bits; a wrap adds M - 2^32 + ... = c back after subtracting M once.
+template <uint32_t M, uint32_t C>
+__device__ __forceinline__ uint32_t mod31(uint64_t u) {
+  const uint32_t m = C * (uint32_t)(u >> 32), u0 = (uint32_t)u;
+  const uint32_t v = u0 - m;
+  return v - (v >= M ? M : 0u) + (u0 < m ? C : 0u);
+}
+
 // The exact acceptance tests and redraws of a slot's two 48-bit draws, out of line, in draw order
 // (r_m's, then rho_m's: the fallback stream's order); the W32 slot calls it when a draw's high
 // 16 bits reach the limit's (the only way it can reject).
@@ -416,14 +443,15 @@ __device__ __forceinline__ void large_stage(uint32_t h, uint64_t j, const Key& k
 
 // Alg 7 steps 1-9 for element j with shares x0, x1 (both computing parties and
 // P2's zero test): returns DReLU' (bit 0) and t (bit 1).
-template <int R, bool TRANSCRIPT, int TPB_L, bool PRE = false, bool HI0 = false, bool W32 = false, bool RELU = false>
+template <int R, bool TRANSCRIPT, int TPB_L, bool PRE = false, bool HI0 = false, bool W32 = false, bool RELU = false,
+          bool L31 = false>
 __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_t j, const Key& k01, const KPL& kp,
                                                LargeIdx* idx, uint32_t* stg, const uint32_t* magic,
                                                const uint32_t* hlim, uint64_t* w0, uint64_t* w1,
                                                const KeyPre* pre = nullptr) {
   const uint32_t S = kp.S;
   uint32_t fbc = 0;  // fallback words consumed
-  const uint32_t t = W32 && (BC_LARGE_PERM32 & (RELU ? 4 : 1)) ? large_perm32<R, TPB_L, PRE, HI0>(j, k01, idx, stg, magic, hlim, fbc, pre)
+  const uint32_t t = (W32 || L31) && (BC_LARGE_PERM32 & (RELU ? 4 : 1)) ? large_perm32<R, TPB_L, PRE, HI0>(j, k01, idx, stg, magic, hlim, fbc, pre)
                                                    : large_perm<R, TPB_L, PRE, HI0>(j, k01, kp, idx, stg, magic, hlim, fbc, pre);
   // steps 1-2: blind both shares by (-1)^t
   const uint64_t s0 = t ? (0ull - x0) & kp.ymask : x0 & kp.ymask;
@@ -449,6 +477,46 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
         z |= (sum == kp.p || sum == 2 * kp.p) ? 1u : 0u;
       }
   };
+  if (L31 && !TRANSCRIPT && BC_LARGE_P31) {
+    // p = 2^31 + 11, S = 32: r = rM K31, P0's wire value W0 = c r + rho in [0, p), P1's message
+    // d r + (p - rho) folded (below 2^32 + 177); P2: s = W0 + W1 < 2^33 is 0 mod p iff
+    // s0 - 22 s1 (in [-22, 2^32)) is 0 or p.
+    auto slot31 = [&](auto Kc, uint32_t G, uint32_t m) {
+      constexpr int K = decltype(Kc)::value;
+      uint64_t ur = draw48c<TPB_L, 6 * K>(stg, G), uq = draw48c<TPB_L, 48 + 6 * K>(stg, G);
+      if (__builtin_expect(((uint32_t)(ur >> 32) >= (uint32_t)(kp.qlim >> 32)) |
+                           ((uint32_t)(uq >> 32) >= (uint32_t)(kp.plim >> 32)), 0)) {
+        const Redraw2 dr = large_redraw2<R>(ur, uq, kp.qlim, kp.plim, k01, j, fbc);
+        ur = dr.ur;
+        uq = dr.uq;
+        fbc = dr.fbc;
+      }
+      const uint32_t rM = 1u + mod31<(uint32_t)(P31 - 1), 20u>(ur);    // Montgomery form of r_m (C28)
+      const uint32_t rho = mod31<(uint32_t)P31, 22u>(uq);
+      uint64_t c, d;
+      slot_values<false>(s0f, n1f, idx[m * TPB_L], kp, c, d);         // c in [1, 2^31], d in [11, p)
+      const uint32_t r = red31((uint64_t)rM * K31);
+      const uint32_t W0 = red31((uint64_t)(uint32_t)c * r + rho);      // P0's wire value
+      const uint64_t W1 = fold31((uint64_t)(uint32_t)d * r + (P31 - rho));
+      const uint64_t sm = W0 + W1;
+      const int64_t tz = (int64_t)(uint32_t)sm - 22ll * (int64_t)(sm >> 32);
+      z |= (tz == 0 || tz == (int64_t)P31) ? 1u : 0u;
+    };
+#pragma unroll 1
+    for (uint32_t h = 0; h < 2; ++h) {
+      large_stage<R, TPB_L, PRE, HI0>(h, j, k01, stg, pre);
+#pragma unroll 1
+      for (uint32_t g8 = 16 * h; g8 < 16 * h + 16; g8 += 8) {
+        const uint32_t G = 24u * ((g8 >> 3) & 1u);
+        using std::integral_constant;
+        slot31(integral_constant<int, 0>{}, G, g8 + 0); slot31(integral_constant<int, 1>{}, G, g8 + 1);
+        slot31(integral_constant<int, 2>{}, G, g8 + 2); slot31(integral_constant<int, 3>{}, G, g8 + 3);
+        slot31(integral_constant<int, 4>{}, G, g8 + 4); slot31(integral_constant<int, 5>{}, G, g8 + 5);
+        slot31(integral_constant<int, 6>{}, G, g8 + 6); slot31(integral_constant<int, 7>{}, G, g8 + 7);
+      }
+    }
+    return z | (t << 1);
+  }
   if (W32 && !TRANSCRIPT && BC_LARGE_P15) {
     // p = 2^32 + 15, S = 32 (every slot group full).  Per slot: r = rM K15, P0's wire value
     // W0 = c r + rho in [0, p), P1's message d r + (p - rho) folded (congruent, below
@@ -565,19 +633,53 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
 // the message W_m, m < S, as 32-bit low words lo[m * stride] (slot-major wire
 // planes) and bit m of the returned high-bit word (bit 32 of W_m; p < 2^33).
 // Returns t in bit 32 of the result.
-template <int R, int PARTY, int TPB_L, bool W32 = false, bool PRE = false, bool HI0 = false>
+template <int R, int PARTY, int TPB_L, bool W32 = false, bool PRE = false, bool HI0 = false, bool L31 = false>
 __device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, const Key& k01, const KPL& kp,
                                                      LargeIdx* idx, uint32_t* stg, const uint32_t* magic,
                                                      const uint32_t* hlim, uint32_t* lo, uint64_t stride,
                                                      const KeyPre* pre = nullptr) {
   const uint32_t S = kp.S;
   uint32_t fbc = 0;
-  const uint32_t t = W32 && (BC_LARGE_PERM32 & 2) ? large_perm32<R, TPB_L, PRE, HI0>(j, k01, idx, stg, magic, hlim, fbc, pre)
+  const uint32_t t = (W32 || L31) && (BC_LARGE_PERM32 & 2) ? large_perm32<R, TPB_L, PRE, HI0>(j, k01, idx, stg, magic, hlim, fbc, pre)
                                                    : large_perm<R, TPB_L, PRE, HI0>(j, k01, kp, idx, stg, magic, hlim, fbc, pre);
   const uint64_t s = t ? (0ull - x) & kp.ymask : x & kp.ymask;                  // steps 1-2
   // P0 reads windows of s, P1 of (-s) mod 2^ell (Alg 5, readings C3, C4)
   const uint64_t sf = (PARTY == 0 ? s : (0ull - s) & kp.ymask) >> kp.f;
   uint32_t hib = 0;
+  if (L31 && BC_LARGE_P31) {  // p = 2^31 + 11, S = 32: the slot arithmetic of elem_large's L31 path
+    auto slot31 = [&](auto Kc, uint32_t G, uint32_t m) {
+      constexpr int K = decltype(Kc)::value;
+      uint64_t ur = draw48c<TPB_L, 6 * K>(stg, G), uq = draw48c<TPB_L, 48 + 6 * K>(stg, G);
+      if (__builtin_expect(((uint32_t)(ur >> 32) >= (uint32_t)(kp.qlim >> 32)) |
+                           ((uint32_t)(uq >> 32) >= (uint32_t)(kp.plim >> 32)), 0)) {
+        const Redraw2 dr = large_redraw2<R>(ur, uq, kp.qlim, kp.plim, k01, j, fbc);
+        ur = dr.ur;
+        uq = dr.uq;
+        fbc = dr.fbc;
+      }
+      const uint32_t rM = 1u + mod31<(uint32_t)(P31 - 1), 20u>(ur);
+      const uint32_t rho = mod31<(uint32_t)P31, 22u>(uq);
+      uint64_t c, d;
+      slot_values<false>(sf, sf, idx[m * TPB_L], kp, c, d);           // one of the two is this party's
+      const uint32_t r = red31((uint64_t)rM * K31);
+      const uint32_t W = red31((uint64_t)(uint32_t)(PARTY == 0 ? c : d) * r + (PARTY == 0 ? (uint64_t)rho : P31 - rho));
+      lo[m * stride] = W;                                               // p < 2^32: no bit-32 plane
+    };
+#pragma unroll 1
+    for (uint32_t h = 0; h < 2; ++h) {
+      large_stage<R, TPB_L, PRE, HI0>(h, j, k01, stg, pre);
+#pragma unroll 1
+      for (uint32_t g8 = 16 * h; g8 < 16 * h + 16; g8 += 8) {
+        const uint32_t G = 24u * ((g8 >> 3) & 1u);
+        using std::integral_constant;
+        slot31(integral_constant<int, 0>{}, G, g8 + 0); slot31(integral_constant<int, 1>{}, G, g8 + 1);
+        slot31(integral_constant<int, 2>{}, G, g8 + 2); slot31(integral_constant<int, 3>{}, G, g8 + 3);
+        slot31(integral_constant<int, 4>{}, G, g8 + 4); slot31(integral_constant<int, 5>{}, G, g8 + 5);
+        slot31(integral_constant<int, 6>{}, G, g8 + 6); slot31(integral_constant<int, 7>{}, G, g8 + 7);
+      }
+    }
+    return (uint64_t)hib | ((uint64_t)t << 32);
+  }
   if (W32 && BC_LARGE_P15) {  // p = 2^32 + 15, S = 32: the pseudo-Mersenne slot arithmetic of elem_large
     const uint32_t l0 = (uint32_t)sf, h0 = (uint32_t)(sf >> 32);
     auto slot15 = [&](auto Kc, uint32_t G, uint32_t m) {

@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(TPB, 2) k_send_w(SendArgs a, KP kp_, Key k01, 
 // stores of slot m are 128 coalesced bytes (over NVLink in the peer
 // transport) and the blinding bits come out of one ballot per 32 elements;
 // then (ReLU) lane l computes [d]_b for its group of 8 (send_dshare).
-template <int R, int PARTY, bool RELU, bool W32 = false, bool HI0 = false>
+template <int R, int PARTY, bool RELU, bool W32 = false, bool HI0 = false, bool L31 = false>
 __global__ void __launch_bounds__(TPB_LARGE) k_send_l(SendArgs a, KP kp, KPL kl, Key k01, Key ktr,
                                                       const __grid_constant__ KeyPre tpl) {
   __shared__ LargeIdx sidx[32 * TPB_LARGE];
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(TPB_LARGE) k_send_l(SendArgs a, KP kp, KPL kl,
       const uint64_t i = wb + 32 * e + lane;
       uint32_t tb = 0;
       if (i < a.n) {
-        const uint64_t r = elem_large_party<R, PARTY, TPB_LARGE, W32, true, HI0>(__ldg(a.x + i), a.base + i, k01, kl, idx, stg,
+        const uint64_t r = elem_large_party<R, PARTY, TPB_LARGE, W32, true, HI0, L31>(__ldg(a.x + i), a.base + i, k01, kl, idx, stg,
                                                                  magic, hlim, lo + i, a.n, &tpl);
         if (hi) hi[i] = (uint32_t)r;
         tb = (uint32_t)(r >> 32);
@@ -568,6 +568,8 @@ int send(int party, const uint64_t* x, uint8_t* lo, uint8_t* hi, uint8_t* tbits,
       const bool c32 = base + n <= (1ull << 32) / 7;  // every tape counter 7j + b below 2^32
       auto pick = [&](auto P) {
         constexpr int PARTY = decltype(P)::value;
+        if (kl.w == 31 && kl.S == 32 && kl.p == P31)  // the paper-literal full precision, p = 2^31 + 11
+          return c32 ? k_send_l<R, PARTY, RELU, false, true, true> : k_send_l<R, PARTY, RELU, false, false, true>;
         return kl.w == 32 ? (c32 ? k_send_l<R, PARTY, RELU, true, true> : k_send_l<R, PARTY, RELU, true, false>)
                           : (c32 ? k_send_l<R, PARTY, RELU, false, true> : k_send_l<R, PARTY, RELU, false, false>);
       };

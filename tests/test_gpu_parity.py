@@ -653,6 +653,35 @@ def test_full_precision_full_size_exact(api, fn):
     assert bad.size == 0, f"{bad.size} of {n} elements differ, first at {bad[:8]}"
 
 
+@pytest.mark.parametrize("fn", ["drelu", "relu"])
+def test_literal_full_precision_exact(api, fn):
+    """The paper-literal full precision (lx = 31, w = 31, p = 2^31 + 11: the kernels with the
+    p = 2^31 + 11 slot arithmetic): 2^22 outputs without a transcript at elem_base 0 against
+    the scalar C oracle element by element, and a ragged batch at a high base against the
+    numpy oracle, both fused and through the party phases (Alg 7, Alg 8)."""
+    from oracle import cref
+    kw = LARGE_PARAMS[1]
+    oprm, prm = B.Params(**kw), api.Params(**kw)
+    n = 1 << 22
+    x, x0, x1 = synth.shares(n, 64, 7, 24, "D2")
+    y0, y1 = getattr(api, fn)(dev(x0), dev(x1), prm, SEEDS)
+    ref = cref.fused(oprm, x0, x1, 0, SEEDS, relu=(fn == "relu"))
+    bad = np.flatnonzero((host(y0) != ref["y0"]) | (host(y1) != ref["y1"]))
+    assert bad.size == 0, f"{bad.size} of {n} elements differ, first at {bad[:8]}"
+    m, base = 1003, (1 << 40) + 8
+    x, x0, x1 = synth.shares(m, 64, 31, 0, "D1", run=7)
+    j = np.arange(m, dtype=np.uint64) + np.uint64(base)
+    ref = getattr(B, fn)(oprm, x0, x1, j, SEEDS)
+    y0, y1 = getattr(api, fn)(dev(x0), dev(x1), prm, SEEDS, elem_base=base)
+    assert np.array_equal(host(y0), ref["y0"]) and np.array_equal(host(y1), ref["y1"])
+    if fn == "drelu":
+        lo0, hi0, tb0 = api.drelu_send(0, dev(x0), prm, SEEDS.s01, base)
+        lo1, hi1, tb1 = api.drelu_send(1, dev(x1), prm, SEEDS.s01, base)
+        r0, r1 = api.drelu_helper(lo0, hi0, lo1, hi1, prm, SEEDS.s02, base, paper_literal=True)
+        assert np.array_equal(host(api.drelu_finish(0, tb0, r0, prm, m, None, base)), ref["y0"])
+        assert np.array_equal(host(api.drelu_finish(1, tb1, r1, prm, m, None, base)), ref["y1"])
+
+
 @pytest.mark.parametrize("base", [0, 1 << 40])
 def test_p15_wide_operand_slots(api, base):
     """The p = 2^32 + 15 kernels' generic path, forced: shares chosen from each element's t

@@ -376,3 +376,67 @@ def test_p15_slot_zero_test():
         assert s < 3 << 32
         got = (s & M32) == 15 * (s >> 32)
         assert got == (((c + d) * r) % P15 == 0), (c, d, r, rho)
+
+
+# ---- large tape at p = 2^31 + 11 (csrc/bc_large.cuh, BC_LARGE_P31) -----------------------
+
+P31 = (1 << 31) + 11
+
+
+def _fold31(x):
+    y = ((x & M32) - (x >> 32) * 22) & M64
+    y1 = (y >> 32) - (1 << 32) if (y >> 63) else (y >> 32)
+    return (y & M32) + ((-22 * y1) & M32)
+
+
+def _red31(x):
+    z = _fold31(x)
+    return z - 2 * P31 if z >= 2 * P31 else (z - P31 if z >= P31 else z)
+
+
+def _mod31(u, M, C):
+    m, u0 = (C * (u >> 32)) & M32, u & M32
+    v = (u0 - m) & M32
+    return (v - (M if v >= M else 0) + (C if u0 < m else 0)) & M32
+
+
+def test_p31_fold_reduce_and_draws():
+    """The paper-literal full-precision domain p = 2^31 + 11: fold31 is x mod p within
+    [0, 2^32 + 176] and red31 the exact residue for every x < 2^63 (edges and 2e5 random);
+    mod31 = u mod p and u mod (p - 1) for 48-bit draws; K31 = 2^-64 mod p (reading C28)."""
+    rng = np.random.default_rng(31)
+    xs = [0, 1, M32, 1 << 32, P31, P31 - 1, 2 * P31, 2 * P31 - 1, (1 << 63) - 1, P31 * P31 + P31 - 1,
+          (1 << 31) * (P31 - 1) + P31 - 1] + [k * P31 + e for k in (1, 2, 3, 1 << 30, (1 << 31) + 9) for e in (0, 1, 21, 22)]
+    xs += [int(v) for v in rng.integers(0, 1 << 63, size=200000, dtype=np.uint64)]
+    for x in xs:
+        z = _fold31(x)
+        assert z % P31 == x % P31 and 0 <= z <= (1 << 32) + 176, x
+        assert _red31(x) == x % P31, x
+    us = [0, 1, (1 << 48) - 1, P31, P31 - 1, M32, 1 << 32] + [(k << 32) + e for k in (1, 2, 0xFFFF)
+                                                              for e in (0, 19, 20, 21, 22, 23, 20 * k - 1, 22 * k - 1)]
+    us += [int(v) for v in rng.integers(0, 1 << 48, size=200000, dtype=np.uint64)]
+    for u in us:
+        assert _mod31(u, P31, 22) == u % P31, u
+        assert _mod31(u, P31 - 1, 20) == u % (P31 - 1), u
+    assert pow(2, -64, P31) == 0x5E69C906
+
+
+def test_p31_slot_zero_test():
+    """The L31 slot: W0 = red31(c r + rho), W1 = fold31(d r + (p - rho)); P2's test
+    t = s0 - 22 s1 in {0, p} on s = W0 + W1 is exactly (c + d) r = 0 (mod p); no operand
+    product plus addend reaches 2^63."""
+    rng = np.random.default_rng(32)
+    cases = [(1 << 31, P31 - (1 << 31), P31 - 1, P31 - 1), (1, P31 - 1, P31 - 1, 0), (1 << 31, 11, 1, 5)]
+    for _ in range(50000):
+        c = int(rng.integers(1, (1 << 31) + 1))
+        r = int(rng.integers(1, P31))
+        rho = int(rng.integers(0, P31))
+        d = (P31 - c) % P31 if rng.random() < 0.3 else int(rng.integers(11, P31))
+        cases.append((c, d, r, rho))
+    for c, d, r, rho in cases:
+        x0, x1 = c * r + rho, d * r + (P31 - rho)
+        assert x0 < 1 << 63 and x1 < 1 << 63
+        s = _red31(x0) + _fold31(x1)
+        assert s < 1 << 33
+        t = (s & M32) - 22 * (s >> 32)
+        assert (t in (0, P31)) == (((c + d) * r) % P31 == 0), (c, d, r, rho)

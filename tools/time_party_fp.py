@@ -16,7 +16,7 @@ n = 1 << 24
 dev = torch.device("cuda:0")
 LX = int(os.environ.get("TIME_LX", "31"))  # 7: the compact tape (f = 24)
 F = 24 if LX == 7 else 0
-prm = api.Params(ell=64, lx=LX, f=F, mode="guard", rounds=20)
+prm = api.Params(ell=64, lx=LX, f=F, mode=os.environ.get("TIME_MODE", "guard"), rounds=20)  # TIME_MODE=literal: p = 2^31 + 11
 sd = synth.seeds(0)
 x, x0, x1 = synth.shares(n, 64, LX, F, "D2")
 t0 = torch.from_numpy(x0.view(np.int64)).to(dev)
