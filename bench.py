@@ -528,7 +528,14 @@ def run_cuda(a):
             fp[name] = {"value": v_fp, "unit": "elements/s", "ms_per_step": ms_fp,
                         "roofline": roofline(name, v_fp, ms_fp)}
         fp["party_chain_1gpu"] = party_chain(api, pfp, seeds, x0, x1, base, dev, stream, timed, world, n)
-        fp["note"] = "lx=31, f=0, guard (w=32, p=2^32+15, 32 slots): the paper's full 5+26 precision, same batch"
+        # the paper-literal domain at full precision (w = 31, p = 2^31 + 11: "31 * 31 ~ 1,000 bits")
+        plit = api.Params(ell=ELL, lx=31, f=0, mode="literal", rounds=a.rounds)
+        for name, fn in (("drelu", api.drelu), ("relu", api.relu)):
+            t_fp, _, _ = timed(lambda: fn(x0, x1, plit, seeds, base, y0, y1, stream=stream), 10, 3)
+            fp.setdefault("literal", {})[name] = {"value": world * n / (t_fp / 10 * 1e-3), "unit": "elements/s",
+                                                  "ms_per_step": t_fp / 10}
+        fp["note"] = ("lx=31, f=0, guard (w=32, p=2^32+15, 32 slots): the paper's full 5+26 precision, same batch; "
+                      "literal: w=31, p=2^31+11 (the paper's own domain; C6's false positives apply)")
         line["full_precision"] = fp
         # ---- Bicoptor-1 as the paper describes it (NEXT #4), same batch and seeds ----
         t_b1, _, _ = timed(lambda: api.drelu_b1(x0, x1, prm, seeds, base, y0, y1, stream=stream), 20, 3)
