@@ -478,12 +478,12 @@ constexpr int TPB_L = TPB_LARGE;
 template <int R, bool RELU, bool TRANSCRIPT, bool HI0 = false, bool W32 = false, bool L31 = false>
 __global__ void __launch_bounds__(TPB_L, RELU ? BC_LARGE_RELU_MINB : BC_LARGE_MINB) k_fused_l(FusedArgs a, KP kp, KPL kl, Key k01, Key k02, Key k12,
                                                                   const __grid_constant__ PreKeys pk) {
-  __shared__ LargeIdx sidx[32 * TPB_L];
+  __shared__ uint32_t sidx[kIdxWords * TPB_L];
   __shared__ uint32_t sstg[LARGE_STG_ROWS * TPB_L];
   __shared__ uint32_t magic[33], hlim[33];
   large_tables(magic, hlim);
   __syncthreads();
-  LargeIdx* idx = sidx + threadIdx.x;
+  LargeIdx* idx = reinterpret_cast<LargeIdx*>(sidx + threadIdx.x);
   uint32_t* stg = sstg + threadIdx.x;
   const uint64_t ngroups = (a.n + 7) >> 3;
   for (uint64_t g = (uint64_t)blockIdx.x * TPB_L + threadIdx.x; g < ngroups; g += (uint64_t)gridDim.x * TPB_L) {

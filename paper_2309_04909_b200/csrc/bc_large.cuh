@@ -150,16 +150,25 @@ __device__ __forceinline__ void slot_values(uint64_t s0f, uint64_t n1f, uint32_t
 #endif
 constexpr int TPB_LARGE = BC_TPB_LARGE;  // threads per CTA of the large-tape kernels (shared tables are [32][TPB_LARGE])
 
-// The per-thread permutation table: 32-bit entries ([slot][thread] words: thread t's column sits
-// in bank t mod 32, so the Fisher-Yates swaps at random slots are conflict-free; byte entries put
-// four threads' columns in one bank word and the random-row swaps conflicted 4-way).
+// The per-thread permutation table.  BC_LARGE_IDX32 = 1: 32-bit entries, [slot][thread] words
+// (thread t's column sits in bank t mod 32, so the Fisher-Yates swaps at random slots are
+// conflict-free; round 1's byte entries in the same [slot][thread] order put four threads' columns
+// in one bank word and the random-row swaps conflicted 4-way).  0: byte entries with each thread
+// owning whole words ([slot / 4][thread] words, byte slot mod 4): as conflict-free, 4 KB per CTA
+// instead of 16 KB.  Entry m of this thread is idx[idx_off(m)] (idx = this thread's row-0 word).
 #ifndef BC_LARGE_IDX32
 #define BC_LARGE_IDX32 1
 #endif
 #if BC_LARGE_IDX32
 typedef uint32_t LargeIdx;
+constexpr int kIdxWords = 32;  // table words per thread
+template <int TPB_L>
+__device__ __forceinline__ uint32_t idx_off(uint32_t m) { return m * (uint32_t)TPB_L; }
 #else
 typedef uint8_t LargeIdx;
+constexpr int kIdxWords = 8;
+template <int TPB_L>
+__device__ __forceinline__ uint32_t idx_off(uint32_t m) { return (m >> 2) * (4u * TPB_L) + (m & 3u); }
 #endif
 
 // Per-CTA constant tables of the Fisher-Yates draws: magic[s] = ceil(2^32 / s),
@@ -201,7 +210,7 @@ __device__ __forceinline__ uint32_t large_perm(uint64_t j, const Key& k01, const
     for (int w = 0; w < 16; ++w) stg[w * TPB_L] = B[w];
   }
 #pragma unroll 4
-  for (uint32_t m = 0; m < 32; ++m) idx[m * TPB_L] = (LargeIdx)m;
+  for (uint32_t m = 0; m < 32; ++m) idx[idx_off<TPB_L>(m)] = (LargeIdx)m;
   // step 6: Fisher-Yates, slot m = S-1 .. 1 draws h[S-m]
 #pragma unroll 1
   for (uint32_t q = 1; q < S; ++q) {
@@ -209,9 +218,9 @@ __device__ __forceinline__ uint32_t large_perm(uint64_t j, const Key& k01, const
     uint32_t d = (stg[(q >> 1) * TPB_L] >> (16 * (q & 1))) & 0xFFFFu;
     while (d >= hlim[s]) d = (uint32_t)fbl_word<R>(k01, j, fbc++) & 0xFFFFu;
     const uint32_t k = d - __umulhi(d, magic[s]) * s;
-    const LargeIdx a = idx[m * TPB_L], b = idx[k * TPB_L];
-    idx[m * TPB_L] = b;
-    idx[k * TPB_L] = a;
+    const LargeIdx a = idx[idx_off<TPB_L>(m)], b = idx[idx_off<TPB_L>(k)];
+    idx[idx_off<TPB_L>(m)] = b;
+    idx[idx_off<TPB_L>(k)] = a;
   }
   return t;
 }
@@ -233,7 +242,7 @@ __device__ __forceinline__ uint32_t large_perm32(uint64_t j, const Key& k01, Lar
   large_block<R, TPB_L, PRE, HI0>(k01, pre, j * 7, B);
   const uint32_t t = B[0] & 1u;
 #pragma unroll
-  for (uint32_t m = 0; m < 32; ++m) idx[m * TPB_L] = (LargeIdx)m;
+  for (uint32_t m = 0; m < 32; ++m) idx[idx_off<TPB_L>(m)] = (LargeIdx)m;
   uint32_t q0 = 32;
 #pragma unroll
   for (uint32_t q = 1; q < 32; ++q) {
@@ -244,9 +253,9 @@ __device__ __forceinline__ uint32_t large_perm32(uint64_t j, const Key& k01, Lar
       break;
     }
     const uint32_t k = d % s;
-    const LargeIdx a = idx[m * TPB_L], b = idx[k * TPB_L];
-    idx[m * TPB_L] = b;
-    idx[k * TPB_L] = a;
+    const LargeIdx a = idx[idx_off<TPB_L>(m)], b = idx[idx_off<TPB_L>(k)];
+    idx[idx_off<TPB_L>(m)] = b;
+    idx[idx_off<TPB_L>(k)] = a;
   }
   if (__builtin_expect(q0 < 32, 0)) {  // a rejected draw: the generic loop from q0 on
 #pragma unroll
@@ -257,9 +266,9 @@ __device__ __forceinline__ uint32_t large_perm32(uint64_t j, const Key& k01, Lar
       uint32_t d = (stg[(q >> 1) * TPB_L] >> (16 * (q & 1))) & 0xFFFFu;
       while (d >= hlim[s]) d = (uint32_t)fbl_word<R>(k01, j, fbc++) & 0xFFFFu;
       const uint32_t k = d - __umulhi(d, magic[s]) * s;
-      const LargeIdx a = idx[m * TPB_L], b = idx[k * TPB_L];
-      idx[m * TPB_L] = b;
-      idx[k * TPB_L] = a;
+      const LargeIdx a = idx[idx_off<TPB_L>(m)], b = idx[idx_off<TPB_L>(k)];
+      idx[idx_off<TPB_L>(m)] = b;
+      idx[idx_off<TPB_L>(k)] = a;
     }
   }
   return t;
@@ -461,7 +470,7 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
   // steps 6-9 for slot m with its draws rM, rho
   auto slot = [&](uint32_t m, uint64_t rM, uint64_t rho) {
       uint64_t c, d;
-      slot_values<W32>(s0f, n1f, idx[m * TPB_L], kp, c, d);           // v'_{Pi(m)} of each party
+      slot_values<W32>(s0f, n1f, idx[idx_off<TPB_L>(m)], kp, c, d);           // v'_{Pi(m)} of each party
       const uint64_t rp = rM * kp.pinv;                              // shared by both products
       uint64_t W0 = (BC_LARGE_MONT_SHARED ? mont_shared(c, rM, rp, kp) : mont(c, rM, kp)) + rho;  // steps 7-8, P0
       W0 = W0 >= kp.p ? W0 - kp.p : W0;
@@ -494,7 +503,7 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
       const uint32_t rM = 1u + mod31<(uint32_t)(P31 - 1), 20u>(ur);    // Montgomery form of r_m (C28)
       const uint32_t rho = mod31<(uint32_t)P31, 22u>(uq);
       uint64_t c, d;
-      slot_values<false>(s0f, n1f, idx[m * TPB_L], kp, c, d);         // c in [1, 2^31], d in [11, p)
+      slot_values<false>(s0f, n1f, idx[idx_off<TPB_L>(m)], kp, c, d);         // c in [1, 2^31], d in [11, p)
       const uint32_t r = red31((uint64_t)rM * K31);
       const uint32_t W0 = red31((uint64_t)(uint32_t)c * r + rho);      // P0's wire value
       const uint64_t W1 = fold31((uint64_t)(uint32_t)d * r + (P31 - rho));
@@ -531,7 +540,7 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
       uint32_t rM32, rho32;                                            // Montgomery form of r_m (C28), rho_m
       const bool ok = draws_p15(ur, uq, rM32, rho32);
       // steps 3-5 for slot i = Pi(m) (slot_values<true> on 32 bits): c = 2^32 and d >= 2^32 are flagged
-      const uint32_t i = idx[m * TPB_L];
+      const uint32_t i = idx[idx_off<TPB_L>(m)];
       const bool last = i == 31u;                                      // slot lx has no successor
       const uint32_t cv = __funnelshift_r(l0, h0, i) + (last ? 0u : __funnelshift_rc(l0, h0, i + 1)) - 1u;
       const uint32_t d32 = 15u - (__funnelshift_r(l1, h1, i) + (last ? 0u : __funnelshift_rc(l1, h1, i + 1)));
@@ -606,7 +615,7 @@ __device__ __forceinline__ uint32_t elem_large(uint64_t x0, uint64_t x1, uint64_
       uint64_t rM, rho;
       large_draws<R, TPB_L>(m, j, k01, kp, stg, fbc, rM, rho);
       uint64_t c, d;
-      slot_values<W32>(s0f, n1f, idx[m * TPB_L], kp, c, d);           // v'_{Pi(m)} of each party
+      slot_values<W32>(s0f, n1f, idx[idx_off<TPB_L>(m)], kp, c, d);           // v'_{Pi(m)} of each party
       const uint64_t rp = rM * kp.pinv;                              // shared by both products
       uint64_t W0 = (BC_LARGE_MONT_SHARED ? mont_shared(c, rM, rp, kp) : mont(c, rM, kp)) + rho;  // steps 7-8, P0
       W0 = W0 >= kp.p ? W0 - kp.p : W0;
@@ -660,7 +669,7 @@ __device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, con
       const uint32_t rM = 1u + mod31<(uint32_t)(P31 - 1), 20u>(ur);
       const uint32_t rho = mod31<(uint32_t)P31, 22u>(uq);
       uint64_t c, d;
-      slot_values<false>(sf, sf, idx[m * TPB_L], kp, c, d);           // one of the two is this party's
+      slot_values<false>(sf, sf, idx[idx_off<TPB_L>(m)], kp, c, d);           // one of the two is this party's
       const uint32_t r = red31((uint64_t)rM * K31);
       const uint32_t W = red31((uint64_t)(uint32_t)(PARTY == 0 ? c : d) * r + (PARTY == 0 ? (uint64_t)rho : P31 - rho));
       lo[m * stride] = W;                                               // p < 2^32: no bit-32 plane
@@ -688,7 +697,7 @@ __device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, con
       const bool rej = ((uint32_t)(ur >> 32) >= (uint32_t)(kp.qlim >> 32)) | ((uint32_t)(uq >> 32) >= (uint32_t)(kp.plim >> 32));
       uint32_t rM32, rho32;
       const bool ok = draws_p15(ur, uq, rM32, rho32);
-      const uint32_t i = idx[m * TPB_L];
+      const uint32_t i = idx[idx_off<TPB_L>(m)];
       const uint32_t ws = __funnelshift_r(l0, h0, i) + (i == 31u ? 0u : __funnelshift_rc(l0, h0, i + 1));
       const uint32_t v32 = PARTY == 0 ? ws - 1u : 15u - ws;            // c (flag c = 2^32) / d (flag d >= 2^32)
       const bool vbad = PARTY == 0 ? v32 == 0u : v32 < 15u;
@@ -728,7 +737,7 @@ __device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, con
   }
   auto slot = [&](uint32_t m, uint64_t rM, uint64_t rho) {
       uint64_t c, d;
-      slot_values<W32>(sf, sf, idx[m * TPB_L], kp, c, d);             // one of the two is this party's
+      slot_values<W32>(sf, sf, idx[idx_off<TPB_L>(m)], kp, c, d);             // one of the two is this party's
       uint64_t W = PARTY == 0 ? mont(c, rM, kp) + rho : mont(d, rM, kp) + (kp.p - rho);  // steps 7-8
       W = W >= kp.p ? W - kp.p : W;
       lo[m * stride] = (uint32_t)W;
@@ -764,7 +773,7 @@ __device__ __forceinline__ uint64_t elem_large_party(uint64_t x, uint64_t j, con
       uint64_t rM, rho;
       large_draws<R, TPB_L>(m, j, k01, kp, stg, fbc, rM, rho);
       uint64_t c, d;
-      slot_values<W32>(sf, sf, idx[m * TPB_L], kp, c, d);             // one of the two is this party's
+      slot_values<W32>(sf, sf, idx[idx_off<TPB_L>(m)], kp, c, d);             // one of the two is this party's
       uint64_t W = PARTY == 0 ? mont(c, rM, kp) + rho : mont(d, rM, kp) + (kp.p - rho);  // steps 7-8
       W = W >= kp.p ? W - kp.p : W;
       lo[m * stride] = (uint32_t)W;

@@ -255,12 +255,12 @@ __global__ void __launch_bounds__(TPB, 2) k_send_w(SendArgs a, KP kp_, Key k01, 
 template <int R, int PARTY, bool RELU, bool W32 = false, bool HI0 = false, bool L31 = false>
 __global__ void __launch_bounds__(TPB_LARGE) k_send_l(SendArgs a, KP kp, KPL kl, Key k01, Key ktr,
                                                       const __grid_constant__ KeyPre tpl) {
-  __shared__ LargeIdx sidx[32 * TPB_LARGE];
+  __shared__ uint32_t sidx[kIdxWords * TPB_LARGE];
   __shared__ uint32_t sstg[LARGE_STG_ROWS * TPB_LARGE];
   __shared__ uint32_t magic[33], hlim[33];
   large_tables(magic, hlim);
   __syncthreads();
-  LargeIdx* idx = sidx + threadIdx.x;
+  LargeIdx* idx = reinterpret_cast<LargeIdx*>(sidx + threadIdx.x);
   uint32_t* stg = sstg + threadIdx.x;
   uint32_t* lo = reinterpret_cast<uint32_t*>(a.lo);
   uint32_t* hi = reinterpret_cast<uint32_t*>(a.hi);
