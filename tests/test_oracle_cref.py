@@ -27,6 +27,7 @@ CASES = [
     (dict(ell=16, lx=7, f=0, mode="guard", rounds=8), 100_000, 0),           # config 1 domain
     (dict(ell=64, lx=31, f=0, mode="guard", rounds=20), 4_000, 1 << 40),     # large tape, p = 2^32 + 15, 32 slots
     (dict(ell=24, lx=10, f=0, mode="literal", rounds=8), 20_000, 0),         # large tape, p = 1031
+    (dict(ell=64, lx=31, f=0, mode="literal", rounds=12), 3_000, 0),        # large tape, p = 2^31 + 11 (paper-literal)
 ]
 
 
