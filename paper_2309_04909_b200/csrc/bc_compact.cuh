@@ -324,6 +324,12 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t saddr) {
 #ifndef BC_SELH_LDS
 #define BC_SELH_LDS 0  // selector high half: 1 = a second LDS.U16, 0 = a shift; measured DReLU 0.4139 -> 0.4126 ms (0), ReLU equal
 #endif
+#ifndef BC_SELH_LDS_SEND
+#define BC_SELH_LDS_SEND 0  // the same choice in the party send kernels (elem_one_t2; measured equal)
+#endif
+#ifndef BC_SELH_LDS_LIT
+#define BC_SELH_LDS_LIT 0  // and in the paper-literal table kernel (elem_both_tl; 0.5261 -> 0.5246 ms)
+#endif
 #ifndef BC_EXTRACT_DP4A
 #define BC_EXTRACT_DP4A 0
 #endif
@@ -504,7 +510,11 @@ __device__ __forceinline__ void elem_one_t2(uint64_t x, uint32_t t, uint32_t ix,
   const uint32_t c_lo = lds_u32(sbase + LAD + TLO + lad_lo_off(wn));
   const uint32_t c_hi = lds_u32(sbase + LAD + THI + lad_hi_off(wn));
   const uint32_t sel = lds_u32(sbase + ix * 4u);
+#if BC_SELH_LDS_SEND
   const uint32_t selh = lds_u16(sbase + ix * 4u + 2u);
+#else
+  const uint32_t selh = sel >> 16;
+#endif
   const uint32_t C_lo = prmt(c_lo, c_hi, sel), C_hi = prmt(c_lo, c_hi, selh);
 #pragma unroll
   for (int m = 0; m < 8; ++m) {
@@ -607,7 +617,11 @@ __device__ __forceinline__ uint32_t elem_both_tl(uint64_t x0, uint64_t x1, uint3
   const uint32_t d_hi = lds_u32(sbase + LAD + 4u * kLitP1Hi + ((wn1 >> 2) & 0x0FFCu));
   // step 6: the permutation as one selector
   const uint32_t sel = lds_u32(sbase + ix * 4u);
+#if BC_SELH_LDS_LIT
   const uint32_t selh = lds_u16(sbase + ix * 4u + 2u);
+#else
+  const uint32_t selh = sel >> 16;
+#endif
   const uint32_t C_lo = prmt(c_lo, c_hi, sel), C_hi = prmt(c_lo, c_hi, selh);
   const uint32_t D_lo = prmt(d_lo, d_hi, sel), D_hi = prmt(d_lo, d_hi, selh);
   uint32_t vmin = 0xFFFFFFFFu;
